@@ -1,0 +1,268 @@
+/*
+ * seed.h — C ABI of libseed.so, the B200 (sm_100a) hot path of SEED
+ * (Espeholt et al., arXiv 1910.06591): the centralized data-parallel learner
+ * step over [T+1][B] unroll batches, V-trace, and centralized batched inference
+ * with an on-device per-actor recurrent-state table.
+ *
+ * Citations: P:NNN = line of /root/reference/PAPER.md, S:NNN = line of
+ * /root/reference/SPEC.md, C# = reading
+ *
+ * ---- conventions (apply to every call) -----------------------------------
+ * Memory:    every tensor pointer is caller-owned DEVICE memory unless a
+ *            parameter says "host".  The library never allocates inside a hot
+ *            call; scratch comes from a caller workspace sized by the matching
+ *            *_workspace_size() query.  The library keeps no pointer after a
+ *            call returns (except inside a seed_comm, which owns an NCCL comm).
+ * Streams:   `stream` is a cudaStream_t passed as void*; NULL = legacy default
+ *            stream.  All calls are asynchronous on that stream.
+ * Errors:    return codes only (seed_status); nothing is thrown across the ABI.
+ *            Host-checkable argument errors return synchronously and launch
+ *            nothing.  Data-dependent numeric problems are reported through
+ *            device-side flags/metrics and never force a host sync.
+ * Layout:    batch-major, trajectory-contiguous, row-major: [B][T] and
+ *            [B][T+1][...]; bootstrap values separate [B].  16-byte aligned
+ *            pointers are required (torch allocations satisfy this).
+ * Threads:   no global mutable state; calls on different streams with disjoint
+ *            buffers are independent.
+ */
+#ifndef SEED_H_
+#define SEED_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SEED_OK = 0,
+  SEED_E_ARG = 1,          /* null / misaligned pointer, bad hyper-parameter   */
+  SEED_E_SHAPE = 2,        /* T, B, A, n out of the supported range            */
+  SEED_E_NONFINITE = 3,    /* reserved: numeric problems are device flags      */
+  SEED_E_CUDA = 4,         /* a CUDA runtime call failed (launch, attribute)   */
+  SEED_E_NCCL = 5,         /* NCCL missing or an NCCL call failed              */
+  SEED_E_UNSUPPORTED = 6,  /* net kind / size not built into this library      */
+  SEED_E_WORKSPACE = 7     /* ws_bytes smaller than the *_workspace_size query */
+} seed_status;
+
+const char* seed_status_string(int status);
+/* Library ABI version (this header): 1. */
+int seed_abi_version(void);
+
+/* ===========================================================================
+ * seed_vtrace — V-trace targets (H6).
+ * Definition: S:140 (the IMPALA recursion cited at P:143-145; PAPER.md prints
+ * no formula, reading C1):
+ *   ratio_t = exp(target_logp_t - behaviour_logp_t)
+ *   rho_t   = min(rho_bar, ratio_t);  c_t = lambda * min(c_bar, ratio_t)   (C2)
+ *   delta_t = rho_t (r_t + gamma_t V_{t+1} - V_t),   V_T := bootstrap     (C4)
+ *   vs_t    = V_t + delta_t + gamma_t c_t (vs_{t+1} - V_{t+1}), vs_T - V_T := 0
+ *   pg_t    = rho_t (r_t + gamma_t vs_{t+1} - V_t),  vs_T := bootstrap    (C3)
+ * Arguments: all [B][T] float32 row-major (trajectory b contiguous), bootstrap
+ *   [B].  discounts gamma_t = gamma * (1 - done_{t->t+1}) (C5).
+ *   rho_bar, c_bar may be +INFINITY (no clipping); require c_bar > 0,
+ *   rho_bar >= c_bar, 0 <= lambda <= 1 (C6) else SEED_E_ARG.
+ *   T >= 1, B >= 1 else SEED_E_SHAPE.  T % 4 == 0 takes the float4 path.
+ * Outputs: vs, pg_advantages [B][T] (may not alias inputs).
+ *   nonfinite_flag: nullable device int32; set to 1 (never cleared) when any
+ *   target-behaviour log-prob difference, reward, discount, value or
+ *   bootstrap is NaN/Inf (C7).  Outputs are still written.
+ * ======================================================================== */
+seed_status seed_vtrace(int T, int B,
+                        const float* behaviour_logp, const float* target_logp,
+                        const float* rewards, const float* discounts,
+                        const float* values, const float* bootstrap_value,
+                        float rho_bar, float c_bar, float lambda,
+                        float* vs, float* pg_advantages,
+                        int* nonfinite_flag, void* stream);
+
+/* ===========================================================================
+ * Networks (C14).  Flat fp32 parameter layout = the tensors below, row-major,
+ * concatenated in this order (query with seed_net_param_tensor):
+ *  SEED_NET_MLP (configs[0]): mlp0.w[64][D] mlp0.b[64] mlp1.w[64][64] mlp1.b[64]
+ *      heads.w[A+1][64] heads.b[A+1];  D = obs_h*obs_w*obs_c, obs fp32.
+ *  SEED_NET_ATARI_SHALLOW (configs[1], 84x84x4 uint8):
+ *      conv1.w[16][8][8][C] conv1.b[16]  (8x8 stride 4 valid, ReLU)
+ *      conv2.w[32][4][4][16] conv2.b[32] (4x4 stride 2 valid, ReLU)
+ *      fc.w[256][9*9*32] fc.b[256]        (input flattened (y, x, c); ReLU)
+ *      lstm.wx[4U][256+A+1] lstm.wh[4U][U] lstm.b[4U]   (gates [i,f,g,o], C15)
+ *      heads.w[A+1][U] heads.b[A+1]       (rows 0..A-1 logits, row A value)
+ *  SEED_NET_IMPALA_DEEP / SEED_NET_GFOOTBALL (configs[2]/[3]): per section s
+ *      s{s}.conv.w[ch][3][3][cin] .b, then res{0,1}.conv{0,1}.w[ch][3][3][ch] .b;
+ *      then fc / lstm / heads as above.  (Declared; this build returns
+ *      SEED_E_UNSUPPORTED for their learner/infer calls.)
+ *  Observations enter as obs/255 (uint8 nets).  LSTM core input
+ *  x_t = [fc_t, onehot(prev_action_t), clip(reward_t,-1,1)], one-hot and reward
+ *  zeroed when done_t, and (h,c) reset to 0 before step t when done_t
+ *  (C15).
+ * ======================================================================== */
+enum { SEED_NET_MLP = 0, SEED_NET_ATARI_SHALLOW = 1, SEED_NET_IMPALA_DEEP = 2,
+       SEED_NET_GFOOTBALL = 3 };
+
+typedef struct {
+  int kind;                       /* SEED_NET_*                                  */
+  int obs_h, obs_w, obs_c;        /* MLP: 1, 1, D                                */
+  int num_actions;                /* A >= 2                               */
+  int lstm_units;                 /* 0 for the MLP; 256 for the conv nets        */
+} seed_net_spec;
+
+seed_status seed_net_param_count(const seed_net_spec* spec, int64_t* n_out /* host */);
+/* Describe parameter tensor `index` (0-based).  name_out: host char[64];
+ * shape_out: host int64[4] (unused dims 0); offset_out: element offset in the
+ * flat vector.  Returns SEED_E_ARG when index >= tensor count. */
+seed_status seed_net_param_tensor(const seed_net_spec* spec, int index, char* name_out,
+                                  int* ndim_out, int64_t* shape_out, int64_t* offset_out);
+/* Bytes of the library-private low-precision operand image (bf16 weights in
+ * the GEMM-ready layout) that seed_train_state.params_lowp points to. */
+seed_status seed_net_lowp_bytes(const seed_net_spec* spec, size_t* bytes_out);
+/* Rebuild params_lowp from fp32 params (call once after initialising params;
+ * seed_learner_step keeps it in sync afterwards). */
+seed_status seed_net_refresh_lowp(const seed_net_spec* spec, const float* params,
+                                  void* params_lowp, void* stream);
+
+/* ===========================================================================
+ * seed_learner_step — one synchronous learner update (H0-H11; P:125
+ * "computes gradients ... and applies the gradients ... synchronously").
+ * Forward over the whole [B][T+1] batch, V-trace targets (stop-gradient), loss
+ *   L = loss_scale * sum_{b,t<T} [ -pg_t log pi(a_t|x_t)
+ *                                  + 1/2 vf_coef (vs_t - V_t)^2 - ent_coef H_t ]
+ * (C8-C10), backward, optional NCCL allreduce (sum) of the flat
+ * grads across the comm's ranks (C20: loss_scale = 1/(N B T) makes the
+ * sum a global mean), global-norm clip, Adam (C11-C12), bf16
+ * shadow refresh, step += 1.  A non-finite gradient norm skips the update
+ * and leaves params, moments and step unchanged.
+ * Trained steps t = 0..T-1 use reward[t+1], discount gamma*(1-done[t+1]),
+ * behaviour_logp[t], action[t]; bootstrap = V(x_T) (C5).
+ * ======================================================================== */
+typedef struct {
+  float discount;        /* gamma (.99)                         */
+  float lambda;          /* V-trace lambda                     */
+  float rho_bar, c_bar;  /* C6: 1, 1                                   */
+  float vf_coef;         /* .5                                  */
+  float ent_coef;
+  float loss_scale;      /* 1/(N*B*T) for a global mean                */
+  float lr, beta1, beta2, eps;   /* Adam (C12)                         */
+  float max_grad_norm;   /* C11: 40                                    */
+} seed_hparams;
+
+typedef struct {
+  const void* obs;             /* uint8 [B][T+1][H][W][C]; MLP: fp32 [B][T+1][D] */
+  const int32_t* action;       /* [B][T+1]  a_t taken at obs t                  */
+  const int32_t* prev_action;  /* [B][T+1]  action before obs t (<0 = none)     */
+  const float* reward;         /* [B][T+1]  reward received with obs t          */
+  const uint8_t* done;         /* [B][T+1]  1: obs t starts a new episode (C5)  */
+  const float* behaviour_logp; /* [B][T+1]  log mu(a_t|x_t) recorded at inference */
+  const float* h0;             /* [B][U]    LSTM state before slot 0 (C19)      */
+  const float* c0;             /* [B][U]                                        */
+} seed_batch;
+
+typedef struct {
+  float* params;       /* [P] fp32 master (flat layout above)          */
+  float* grads;        /* [P] fp32: receives the (allreduced, unclipped) grads */
+  float* adam_m;       /* [P]                                          */
+  float* adam_v;       /* [P]                                          */
+  void* params_lowp;   /* seed_net_lowp_bytes() bytes                  */
+  int64_t* step;       /* device int64: ParamSnapshot.version */
+} seed_train_state;
+
+typedef struct seed_comm seed_comm;  /* wraps an ncclComm_t */
+
+seed_status seed_learner_workspace_size(const seed_net_spec* spec, int T, int B,
+                                        size_t* bytes_out);
+/* metrics: device float[8] = {loss, pg, baseline, entropy, grad_norm,
+ * applied (1/0), version (after the step), nonfinite (1/0)}; loss terms are
+ * this rank's (scaled) sums, grad_norm is of the allreduced gradient.
+ * comm == NULL: single GPU.  Shapes: 1 <= T <= 256, 1 <= B <= 1024 (MLP: B*(T+1)
+ * <= 65536), 2 <= A <= 32; SEED_E_SHAPE otherwise. */
+seed_status seed_learner_step(const seed_net_spec* spec, int T, int B,
+                              const seed_batch* batch, const seed_train_state* state,
+                              const seed_hparams* hp, seed_comm* comm,
+                              void* workspace, size_t ws_bytes, float* metrics,
+                              void* stream);
+/* Views into a workspace after seed_learner_step (for tests / metrics):
+ * logits [B][T+1][A], values [B][T+1], vs [B][T], pg_adv [B][T] (fp32). */
+seed_status seed_learner_outputs(const seed_net_spec* spec, int T, int B, void* workspace,
+                                 float** logits, float** values, float** vs,
+                                 float** pg_adv);
+
+/* ===========================================================================
+ * Data-parallel communicator.  The caller broadcasts the
+ * 128-byte unique id (host buffer) from rank 0 via torch.distributed.
+ * NCCL is loaded at run time (libnccl.so.2); SEED_E_NCCL if unavailable.
+ * ======================================================================== */
+seed_status seed_comm_get_unique_id(void* id128 /* host, 128 bytes */);
+seed_status seed_comm_init(const void* id128, int rank, int world, seed_comm** out);
+seed_status seed_comm_destroy(seed_comm* comm);
+/* In-place sum allreduce of n fp32 device values (metrics, probes). */
+seed_status seed_comm_allreduce_f32(seed_comm* comm, float* data, int64_t n, void* stream);
+
+/* ===========================================================================
+ * Centralized inference (H12-H13; "load the recurrent states ... the
+ * latest recurrent states are stored").
+ * For each request i (actor a = actor_ids[i], unique within a call):
+ *   (h, c, prev) <- table[a]; if done[i]: h = c = 0, prev = none, reward = 0
+ *   forward one step with params_lowp; action = min{ j : u_i < CDF_j } over
+ *   softmax(logits) (C18; A-1 if none); behaviour_logp = log pi(action);
+ *   table[a] <- (h', c', action).  Rows of actors not in the call are untouched.
+ * uniforms: nullable [n]; NULL = counter-based Philox4x32-10 keyed
+ *   (seed, counter, actor_id) (C18).
+ * store: nullable unroll store; each step is recorded (C17, C19) and completed
+ *   unrolls (T+1 slots, slot T copied into slot 0 of the next) are pushed to
+ *   the ready ring.
+ * ======================================================================== */
+typedef struct {
+  float* h;              /* [num_actors][U] */
+  float* c;              /* [num_actors][U] */
+  int32_t* last_action;  /* [num_actors]; < 0 = none */
+  int num_actors;
+} seed_state_table;
+
+typedef struct {
+  int T;                   /* unroll length; buffers hold T+1 slots           */
+  int num_actors;
+  uint8_t* obs;            /* [num_actors][2][T+1][obs_bytes]                 */
+  int32_t* action;         /* [num_actors][2][T+1]                            */
+  int32_t* prev_action;    /* [num_actors][2][T+1]                            */
+  float* reward;           /* [num_actors][2][T+1]                            */
+  uint8_t* done;           /* [num_actors][2][T+1]                            */
+  float* behaviour_logp;   /* [num_actors][2][T+1]                            */
+  float* h0;               /* [num_actors][2][U]                              */
+  float* c0;               /* [num_actors][2][U]                              */
+  int32_t* fill;           /* [num_actors]  slots filled in the current buffer */
+  int32_t* cur;            /* [num_actors]  current buffer 0/1                */
+  int32_t* ready_ring;     /* [ring_capacity] entries actor*2 + buffer        */
+  int32_t* ready_count;    /* device int32[2]: {pushed total, consumed total} */
+  int ring_capacity;
+} seed_unroll_store;
+
+seed_status seed_infer_workspace_size(const seed_net_spec* spec, int max_n, size_t* bytes_out);
+seed_status seed_infer(const seed_net_spec* spec, const void* params_lowp, const float* params,
+                       const seed_state_table* table, int n, const int32_t* actor_ids,
+                       const uint8_t* obs, const float* reward, const uint8_t* done,
+                       const float* uniforms, uint64_t seed, uint64_t counter,
+                       int32_t* action_out, float* behaviour_logp_out, float* logits_out,
+                       const seed_unroll_store* store, void* workspace, size_t ws_bytes,
+                       void* stream);
+/* Gather B completed unrolls (entries ready_ring[consumed .. consumed+B)) into
+ * the seed_batch layout buffers given in `out` (device pointers, cast away
+ * const), and advance the consumed counter.  The caller must only ask for
+ * unrolls already pushed (host-visible count). */
+seed_status seed_assemble_batch(const seed_unroll_store* store, int obs_bytes, int lstm_units,
+                                int B, const seed_batch* out, void* stream);
+
+/* ===========================================================================
+ * Test / benchmark hooks (not part of the method):
+ * seed_debug_gemm: D[M][N] (fp32, row-major) = A . B^T with A [M][K], B [N][K]
+ * bf16 row-major (a_t / b_t != 0: A given as [K][M] / B as [K][N]), on the
+ * tcgen05 engine the learner uses.  Requires K % 8 == 0, M % 8 == 0 and
+ * N % 8 == 0.  Returns the kernel's BN tile in *bn_out (host, nullable).
+ * ======================================================================== */
+seed_status seed_debug_gemm(int M, int N, int K, const void* A, int a_t, const void* B,
+                            int b_t, float* D, int bn, int splits, void* workspace,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEED_H_ */

@@ -1,0 +1,348 @@
+"""Python binding of the libseed C ABI (include/seed.h) over torch tensors.
+
+Marshalling only: validates dtype / device / contiguity, passes raw pointers
+and the current CUDA stream to the library.  No computation happens here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+NET_MLP, NET_ATARI_SHALLOW, NET_IMPALA_DEEP, NET_GFOOTBALL = 0, 1, 2, 3
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _need(t, dtype, name, device=True):
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if device and not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor")
+
+
+# --------------------------------------------------------------------------- V-trace
+def vtrace(behaviour_logp, target_logp, rewards, discounts, values, bootstrap, rho_bar=1.0,
+           c_bar=1.0, lam=1.0, vs=None, pg_advantages=None, nonfinite_flag=None, stream=None):
+    """seed_vtrace: [B][T] float32 CUDA tensors -> (vs, pg_advantages)."""
+    B, T = values.shape
+    for n, t in (("behaviour_logp", behaviour_logp), ("target_logp", target_logp),
+                 ("rewards", rewards), ("discounts", discounts), ("values", values)):
+        _need(t, torch.float32, n)
+        if tuple(t.shape) != (B, T):
+            raise ValueError(f"{n}: shape {tuple(t.shape)} != {(B, T)}")
+    _need(bootstrap, torch.float32, "bootstrap")
+    if vs is None:
+        vs = torch.empty_like(values)
+    if pg_advantages is None:
+        pg_advantages = torch.empty_like(values)
+    st = L.load().seed_vtrace(T, B, _ptr(behaviour_logp), _ptr(target_logp), _ptr(rewards),
+                              _ptr(discounts), _ptr(values), _ptr(bootstrap), float(rho_bar),
+                              float(c_bar), float(lam), _ptr(vs), _ptr(pg_advantages),
+                              _ptr(nonfinite_flag), _stream(stream))
+    L.check(st, "seed_vtrace")
+    return vs, pg_advantages
+
+
+def debug_gemm(A, B, a_t=False, b_t=False, bn=64, splits=1, out=None, stream=None):
+    """Test hook: D = A @ B^T on the tcgen05 engine (bf16 in, fp32 out)."""
+    _need(A, torch.bfloat16, "A")
+    _need(B, torch.bfloat16, "B")
+    M, K = (A.shape[1], A.shape[0]) if a_t else A.shape
+    N = B.shape[1] if b_t else B.shape[0]
+    D = out if out is not None else torch.empty(M, N, device=A.device, dtype=torch.float32)
+    ws = torch.empty(max(splits, 1) * M * N, device=A.device, dtype=torch.float32) \
+        if splits > 1 else None
+    st = L.load().seed_debug_gemm(M, N, K, _ptr(A), int(a_t), _ptr(B), int(b_t), _ptr(D), bn,
+                                  splits, _ptr(ws), _stream(stream))
+    L.check(st, "seed_debug_gemm")
+    return D
+
+
+# --------------------------------------------------------------------------- networks
+@dataclass
+class NetSpec:
+    kind: int
+    obs_h: int
+    obs_w: int
+    obs_c: int
+    num_actions: int
+    lstm_units: int = 256
+
+    def c(self):
+        return L.NetSpec(self.kind, self.obs_h, self.obs_w, self.obs_c, self.num_actions,
+                         self.lstm_units)
+
+    @property
+    def obs_shape(self):
+        return (self.obs_h * self.obs_w * self.obs_c,) if self.kind == NET_MLP else \
+            (self.obs_h, self.obs_w, self.obs_c)
+
+    @property
+    def obs_dtype(self):
+        return torch.float32 if self.kind == NET_MLP else torch.uint8
+
+
+def spec_for_config(cfg):
+    """BASELINE.json configs -> NetSpec (c1..c5)."""
+    return {
+        "c1": NetSpec(NET_MLP, 1, 1, 16, 4, 0),
+        "c2": NetSpec(NET_ATARI_SHALLOW, 84, 84, 4, 18, 256),
+        "c3": NetSpec(NET_IMPALA_DEEP, 72, 96, 3, 15, 256),
+        "c4": NetSpec(NET_GFOOTBALL, 72, 96, 16, 19, 256),
+        "c5": NetSpec(NET_ATARI_SHALLOW, 84, 84, 4, 18, 256),
+    }[cfg]
+
+
+def net_param_count(spec):
+    n = C.c_int64()
+    L.check(L.load().seed_net_param_count(C.byref(spec.c()), C.byref(n)), "param_count")
+    return n.value
+
+
+def net_param_layout(spec):
+    """[(name, shape)] in flat order, as the library defines it."""
+    out = []
+    lib = L.load()
+    i = 0
+    while True:
+        name = C.create_string_buffer(64)
+        nd = C.c_int()
+        shape = (C.c_int64 * 4)()
+        off = C.c_int64()
+        st = lib.seed_net_param_tensor(C.byref(spec.c()), i, name, C.byref(nd), shape,
+                                       C.byref(off))
+        if st != 0:
+            break
+        out.append((name.value.decode(), tuple(shape[k] for k in range(nd.value))))
+        i += 1
+    return out
+
+
+@dataclass
+class HParams:
+    discount: float = 0.99
+    lam: float = 1.0
+    rho_bar: float = 1.0
+    c_bar: float = 1.0
+    vf_coef: float = 0.5
+    ent_coef: float = 0.01
+    loss_scale: float = 1.0
+    lr: float = 3e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-5
+    max_grad_norm: float = 40.0
+
+    def c(self):
+        return L.HParams(self.discount, self.lam, self.rho_bar, self.c_bar, self.vf_coef,
+                         self.ent_coef, self.loss_scale, self.lr, self.beta1, self.beta2,
+                         self.eps, self.max_grad_norm)
+
+    def as_oracle(self):
+        return dict(discount=self.discount, rho_bar=self.rho_bar, c_bar=self.c_bar,
+                    vf_coef=self.vf_coef, ent_coef=self.ent_coef, loss_scale=self.loss_scale,
+                    lr=self.lr, beta1=self.beta1, beta2=self.beta2, eps=self.eps,
+                    max_grad_norm=self.max_grad_norm, **{"lambda": self.lam})
+
+
+class Comm:
+    """NCCL communicator owned by libseed; the unique id travels over the
+    caller's torch.distributed process group (gloo or nccl)."""
+
+    def __init__(self, rank, world, group=None):
+        import torch.distributed as dist
+        lib = L.load()
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            L.check(lib.seed_comm_get_unique_id(buf), "seed_comm_get_unique_id")
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        C.memmove(buf, obj[0], 128)
+        h = C.c_void_p()
+        L.check(lib.seed_comm_init(buf, rank, world, C.byref(h)), "seed_comm_init")
+        self.handle = h
+        self.rank, self.world = rank, world
+
+    def allreduce_(self, t, stream=None):
+        _need(t, torch.float32, "allreduce buffer")
+        L.check(L.load().seed_comm_allreduce_f32(self.handle, _ptr(t), t.numel(),
+                                                 _stream(stream)), "allreduce")
+        return t
+
+    def close(self):
+        if self.handle:
+            L.load().seed_comm_destroy(self.handle)
+            self.handle = None
+
+
+class Learner:
+    """Device-resident train state (fp32 master params, Adam moments, bf16
+    operand image, version counter) + workspace for seed_learner_step."""
+
+    def __init__(self, spec, T, B, params, hp=None, comm=None, device="cuda"):
+        lib = L.load()
+        self.spec, self.T, self.B = spec, T, B
+        self.hp = hp or HParams()
+        self.comm = comm
+        n = net_param_count(spec)
+        params = torch.as_tensor(params, dtype=torch.float32).reshape(-1)
+        if params.numel() != n:
+            raise ValueError(f"params has {params.numel()} values, net needs {n}")
+        self.params = params.to(device).contiguous()
+        self.grads = torch.zeros_like(self.params)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        nb = C.c_size_t()
+        L.check(lib.seed_net_lowp_bytes(C.byref(spec.c()), C.byref(nb)), "lowp_bytes")
+        self.lowp = torch.zeros(max(nb.value, 16), dtype=torch.uint8, device=device)
+        self.step_counter = torch.zeros(1, dtype=torch.int64, device=device)
+        L.check(lib.seed_learner_workspace_size(C.byref(spec.c()), T, B, C.byref(nb)),
+                "learner_workspace_size")
+        self.ws = torch.empty(max(nb.value, 16), dtype=torch.uint8, device=device)
+        self.metrics = torch.zeros(8, dtype=torch.float32, device=device)
+        self._spec_c = spec.c()
+        self.refresh_lowp()
+
+    def refresh_lowp(self, stream=None):
+        L.check(L.load().seed_net_refresh_lowp(C.byref(self._spec_c), _ptr(self.params),
+                                               _ptr(self.lowp), _stream(stream)), "refresh_lowp")
+
+    def _batch(self, batch):
+        B, T1 = self.B, self.T + 1
+        _need(batch["obs"], self.spec.obs_dtype, "obs")
+        if tuple(batch["obs"].shape[:2]) != (B, T1):
+            raise ValueError("obs must be [B][T+1][...]")
+        for k, dt in (("action", torch.int32), ("prev_action", torch.int32),
+                      ("reward", torch.float32), ("done", torch.uint8),
+                      ("behaviour_logp", torch.float32)):
+            _need(batch[k], dt, k)
+            if tuple(batch[k].shape) != (B, T1):
+                raise ValueError(f"{k} must be [B][T+1]")
+        h0 = batch.get("h0")
+        c0 = batch.get("c0")
+        if self.spec.lstm_units > 0:
+            _need(h0, torch.float32, "h0")
+            _need(c0, torch.float32, "c0")
+        return L.Batch(*(_ptr(batch.get(k)) for k in ("obs", "action", "prev_action", "reward",
+                                                      "done", "behaviour_logp", "h0", "c0")))
+
+    def step(self, batch, stream=None):
+        """One seed_learner_step (asynchronous); returns the device metrics[8]."""
+        cb = self._batch(batch)
+        ts = L.TrainState(_ptr(self.params), _ptr(self.grads), _ptr(self.m), _ptr(self.v),
+                          _ptr(self.lowp), _ptr(self.step_counter))
+        hp = self.hp.c()
+        st = L.load().seed_learner_step(C.byref(self._spec_c), self.T, self.B, C.byref(cb),
+                                        C.byref(ts), C.byref(hp),
+                                        self.comm.handle if self.comm else None,
+                                        _ptr(self.ws), self.ws.numel(), _ptr(self.metrics),
+                                        _stream(stream))
+        L.check(st, "seed_learner_step")
+        return self.metrics
+
+    def outputs(self):
+        """Views (logits, values, vs, pg_adv) into the workspace after a step."""
+        ptrs = [C.c_void_p() for _ in range(4)]
+        L.check(L.load().seed_learner_outputs(C.byref(self._spec_c), self.T, self.B,
+                                              _ptr(self.ws), *[C.byref(p) for p in ptrs]),
+                "learner_outputs")
+        B, T1, A = self.B, self.T + 1, self.spec.num_actions
+        base = self.ws.data_ptr()
+        flat = self.ws.view(torch.float32) if self.ws.numel() % 4 == 0 else None
+
+        def view(p, shape):
+            off = (p.value - base) // 4
+            n = 1
+            for s in shape:
+                n *= s
+            return flat[off:off + n].view(*shape)
+        return (view(ptrs[0], (B, T1, A)), view(ptrs[1], (B, T1)), view(ptrs[2], (B, T1 - 1)),
+                view(ptrs[3], (B, T1 - 1)))
+
+
+class InferenceServer:
+    """Centralized batched inference (seed_infer) with the per-actor recurrent
+    state table and the device unroll store."""
+
+    def __init__(self, spec, num_actors, max_n, learner=None, T=None, ring_capacity=None,
+                 device="cuda"):
+        lib = L.load()
+        self.spec, self.num_actors, self.max_n = spec, num_actors, max_n
+        U = max(spec.lstm_units, 1)
+        self.h = torch.zeros(num_actors, U, dtype=torch.float32, device=device)
+        self.c = torch.zeros(num_actors, U, dtype=torch.float32, device=device)
+        self.last_action = torch.full((num_actors,), -1, dtype=torch.int32, device=device)
+        self.table = L.StateTable(_ptr(self.h), _ptr(self.c), _ptr(self.last_action), num_actors)
+        nb = C.c_size_t()
+        L.check(lib.seed_infer_workspace_size(C.byref(spec.c()), max_n, C.byref(nb)),
+                "infer_workspace_size")
+        self.ws = torch.empty(max(nb.value, 16), dtype=torch.uint8, device=device)
+        self.learner = learner
+        self._spec_c = spec.c()
+        self.store = None
+        if T is not None:
+            self._make_store(T, ring_capacity or 4 * num_actors, device)
+
+    def _make_store(self, T, cap, device):
+        NA, T1, U = self.num_actors, T + 1, max(self.spec.lstm_units, 1)
+        obs_bytes = 1
+        for s in self.spec.obs_shape:
+            obs_bytes *= s
+        self.obs_bytes = obs_bytes
+        z = lambda *shape, dt: torch.zeros(*shape, dtype=dt, device=device)
+        self.st = dict(obs=z(NA, 2, T1, obs_bytes, dt=torch.uint8),
+                       action=z(NA, 2, T1, dt=torch.int32), prev_action=z(NA, 2, T1, dt=torch.int32),
+                       reward=z(NA, 2, T1, dt=torch.float32), done=z(NA, 2, T1, dt=torch.uint8),
+                       behaviour_logp=z(NA, 2, T1, dt=torch.float32),
+                       h0=z(NA, 2, U, dt=torch.float32), c0=z(NA, 2, U, dt=torch.float32),
+                       fill=z(NA, dt=torch.int32), cur=z(NA, dt=torch.int32),
+                       ready_ring=z(cap, dt=torch.int32), ready_count=z(2, dt=torch.int32))
+        s = self.st
+        self.T = T
+        self.store = L.UnrollStore(T, NA, *(_ptr(s[k]) for k in (
+            "obs", "action", "prev_action", "reward", "done", "behaviour_logp", "h0", "c0",
+            "fill", "cur", "ready_ring", "ready_count")), cap)
+
+    def infer(self, actor_ids, obs, reward, done, uniforms=None, seed=0, counter=0,
+              action_out=None, blp_out=None, logits_out=None, stream=None):
+        n = actor_ids.numel()
+        if n > self.max_n:
+            raise ValueError("n > max_n")
+        _need(actor_ids, torch.int32, "actor_ids")
+        _need(obs, torch.uint8, "obs")
+        _need(reward, torch.float32, "reward")
+        _need(done, torch.uint8, "done")
+        if uniforms is not None:
+            _need(uniforms, torch.float32, "uniforms")
+        dev = actor_ids.device
+        a = action_out if action_out is not None else torch.empty(n, dtype=torch.int32, device=dev)
+        blp = blp_out if blp_out is not None else torch.empty(n, dtype=torch.float32, device=dev)
+        lr = self.learner
+        st = L.load().seed_infer(C.byref(self._spec_c), _ptr(lr.lowp), _ptr(lr.params),
+                                 C.byref(self.table), n, _ptr(actor_ids), _ptr(obs), _ptr(reward),
+                                 _ptr(done), _ptr(uniforms), seed, counter, _ptr(a), _ptr(blp),
+                                 _ptr(logits_out), C.byref(self.store) if self.store else None,
+                                 _ptr(self.ws), self.ws.numel(), _stream(stream))
+        L.check(st, "seed_infer")
+        return a, blp
+
+    def assemble(self, B, out, stream=None):
+        cb = L.Batch(*(_ptr(out.get(k)) for k in ("obs", "action", "prev_action", "reward",
+                                                  "done", "behaviour_logp", "h0", "c0")))
+        L.check(L.load().seed_assemble_batch(C.byref(self.store), self.obs_bytes,
+                                             max(self.spec.lstm_units, 1), B, C.byref(cb),
+                                             _stream(stream)), "seed_assemble_batch")
+        return out
