@@ -180,11 +180,33 @@ seed_status seed_learner_step(const seed_net_spec* spec, int T, int B,
                               const seed_hparams* hp, seed_comm* comm,
                               void* workspace, size_t ws_bytes, float* metrics,
                               void* stream);
+/* Bench / profiling hook: identical to seed_learner_step, and additionally
+ * records events[0] (cudaEvent_t as void*) before the first kernel and
+ * events[i] after the i-th phase of the step (a phase = one kernel, or a
+ * split-K GEMM + its fixed-order reduction).  names_out (host, nullable,
+ * max_events entries) receives static phase names (names_out[i] ends at
+ * events[i]); *n_events_out (host) the number of events recorded and
+ * *n_launches_out (host, nullable) the number of kernels the step launched. */
+seed_status seed_learner_step_traced(const seed_net_spec* spec, int T, int B,
+                                     const seed_batch* batch, const seed_train_state* state,
+                                     const seed_hparams* hp, seed_comm* comm,
+                                     void* workspace, size_t ws_bytes, float* metrics,
+                                     void* stream, void** events, int max_events,
+                                     const char** names_out, int* n_events_out,
+                                     int* n_launches_out);
 /* Views into a workspace after seed_learner_step (for tests / metrics):
  * logits [B][T+1][A], values [B][T+1], vs [B][T], pg_adv [B][T] (fp32). */
 seed_status seed_learner_outputs(const seed_net_spec* spec, int T, int B, void* workspace,
                                  float** logits, float** values, float** vs,
                                  float** pg_adv);
+
+/* Test hook: device pointer + byte size of a named internal buffer of the
+ * learner workspace (after a step): "act1", "act2", "X", "xproj", "H",
+ * "Hprev", "gates", "C", "dlogits", "dvalues", "dH", "dG", "dfc", "dY2",
+ * "dY1", "h1", "h2", "dh1", "dh2".  SEED_E_ARG if the name is unknown for
+ * this net. */
+seed_status seed_learner_debug_buffer(const seed_net_spec* spec, int T, int B, void* workspace,
+                                      const char* name, void** ptr_out, size_t* bytes_out);
 
 /* ===========================================================================
  * Data-parallel communicator.  The caller broadcasts the

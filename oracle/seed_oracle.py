@@ -33,6 +33,25 @@ from dataclasses import dataclass, field
 import numpy as np
 
 # --------------------------------------------------------------------------
+# bf16 emulation (reading C26): the tensor-core path rounds GEMM operands and
+# stored activations / gradients to bf16 (round-to-nearest-even).  A ReLU mask
+# is a floating-point decision of an integer (a mask bit), so parity compares
+# the kernels with this oracle taking the same decisions at the same rounding
+# points ("emu" mode); "exact" mode is the plain fp64 definition.
+# --------------------------------------------------------------------------
+def bf16_round(x):
+    """Round to the nearest bf16 (ties to even), via the float32 bit pattern."""
+    f = np.ascontiguousarray(np.asarray(x, np.float64).astype(np.float32))
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64).reshape(np.shape(x))
+
+
+def _q(x, emu):
+    return bf16_round(x) if emu else x
+
+
+# --------------------------------------------------------------------------
 # network specs (C14) — the architecture definitions, independent of the GPU
 # side's own definitions in include/seed.h.
 # --------------------------------------------------------------------------
@@ -349,8 +368,9 @@ def maxpool_same_backward(x_shape, arg, offs, dy, k=3, s=2):
 
 
 # ---- torsos ---------------------------------------------------------------
-def torso_forward(spec, P, obs):
-    """obs [N][H][W][C] uint8 (or [N][D] float for the MLP).  Returns (features, cache)."""
+def torso_forward(spec, P, obs, emu=False):
+    """obs [N][H][W][C] uint8 (or [N][D] float for the MLP).  Returns (features, cache).
+    emu: bf16 weights and stored activations (C26); the MLP is fp32 on the GPU."""
     if spec.kind == NET_MLP:
         x = np.asarray(obs, np.float64).reshape(obs.shape[0], -1)
         cache = {"x0": x}
@@ -360,9 +380,10 @@ def torso_forward(spec, P, obs):
         return x, cache
     x = np.asarray(obs, np.float64) / 255.0
     cache = {"x0": x}
+    q = lambda t: _q(t, emu)
     if spec.kind == NET_ATARI_SHALLOW:
-        a1 = relu(conv2d(x, P["conv1.w"], P["conv1.b"], 4, 0))
-        a2 = relu(conv2d(a1, P["conv2.w"], P["conv2.b"], 2, 0))
+        a1 = q(relu(conv2d(x, q(P["conv1.w"]), P["conv1.b"], 4, 0)))
+        a2 = q(relu(conv2d(a1, q(P["conv2.w"]), P["conv2.b"], 2, 0)))
         cache.update(a1=a1, a2=a2)
         flat = a2.reshape(a2.shape[0], -1)
     else:
@@ -382,13 +403,14 @@ def torso_forward(spec, P, obs):
                 h = h + t1
         cache["torso_pre"] = h
         flat = relu(h).reshape(h.shape[0], -1)
-    fc = relu(flat @ P["fc.w"].T + P["fc.b"])
+    fc = q(relu(flat @ q(P["fc.w"]).T + P["fc.b"]))
     cache.update(flat=flat, fc=fc)
     return fc, cache
 
 
-def torso_backward(spec, P, cache, dfeat, grads):
-    """Backprop from d(features) into grads (dict); no gradient into obs."""
+def torso_backward(spec, P, cache, dfeat, grads, emu=False):
+    """Backprop from d(features) into grads (dict); no gradient into obs.
+    emu: bf16 weights in the data-gradient products and bf16-stored gradients."""
     if spec.kind == NET_MLP:
         d = dfeat
         for i in reversed(range(len(spec.mlp_hidden))):
@@ -397,15 +419,16 @@ def torso_backward(spec, P, cache, dfeat, grads):
             grads[f"mlp{i}.b"] = d.sum(axis=0)
             d = d @ P[f"mlp{i}.w"]
         return
-    dfc = dfeat * (cache["fc"] > 0)
+    q = lambda t: _q(t, emu)
+    dfc = q(dfeat * (cache["fc"] > 0))
     grads["fc.w"] = dfc.T @ cache["flat"]
     grads["fc.b"] = dfc.sum(axis=0)
-    dflat = dfc @ P["fc.w"]
+    dflat = dfc @ q(P["fc.w"])
     if spec.kind == NET_ATARI_SHALLOW:
         a1, a2 = cache["a1"], cache["a2"]
-        da2 = dflat.reshape(a2.shape) * (a2 > 0)
-        da1, grads["conv2.w"], grads["conv2.b"] = conv2d_backward(a1, P["conv2.w"], da2, 2, 0)
-        da1 = da1 * (a1 > 0)
+        da2 = q(dflat.reshape(a2.shape) * (a2 > 0))
+        da1, grads["conv2.w"], grads["conv2.b"] = conv2d_backward(a1, q(P["conv2.w"]), da2, 2, 0)
+        da1 = q(da1 * (a1 > 0))
         _, grads["conv1.w"], grads["conv1.b"] = conv2d_backward(cache["x0"], P["conv1.w"], da1,
                                                                 4, 0, need_dx=False)
         return
@@ -427,7 +450,7 @@ def torso_backward(spec, P, cache, dfeat, grads):
 
 
 # ---- LSTM core (H3, H8; P:591 inputs, S:47/S:57 reset, C15) ----------------
-def core_inputs(spec, fc, prev_action, reward, done):
+def core_inputs(spec, fc, prev_action, reward, done, emu=False):
     """x_t = [fc_t, onehot(prev_a_t), clip(r_t, -1, 1)], one-hot and reward
     zeroed when done_t (C15); prev_action < 0 means 'none' (zero one-hot)."""
     A = spec.num_actions
@@ -438,10 +461,10 @@ def core_inputs(spec, fc, prev_action, reward, done):
     ok = (pa >= 0) & (pa < A) & ~d
     oh[np.nonzero(ok)[0], pa[ok]] = 1.0
     r = np.clip(np.asarray(reward, np.float64).reshape(n), -1.0, 1.0) * (~d)
-    return np.concatenate([fc, oh, r[:, None]], axis=1)
+    return np.concatenate([fc, oh, _q(r, emu)[:, None]], axis=1)
 
 
-def lstm_forward(P, X, done, h0, c0):
+def lstm_forward(P, X, done, h0, c0, emu=False):
     """X [B][T1][K] core inputs, done [B][T1], h0/c0 [B][U].  Gate order [i,f,g,o].
     for t: if done_t: (h,c) <- 0; z = Wx x_t + Wh h + b; c = f c + i g; h = o tanh c."""
     B, T1, _ = X.shape
@@ -456,7 +479,7 @@ def lstm_forward(P, X, done, h0, c0):
         h = np.where(d[:, t, None], 0.0, h)
         c = np.where(d[:, t, None], 0.0, c)
         cache["hprev"][:, t], cache["cprev"][:, t] = h, c
-        z = X[:, t] @ P["lstm.wx"].T + h @ P["lstm.wh"].T + P["lstm.b"]
+        z = X[:, t] @ _q(P["lstm.wx"], emu).T + _q(h, emu) @ _q(P["lstm.wh"], emu).T + P["lstm.b"]
         i, f, g, o = (sigmoid(z[:, :U]), sigmoid(z[:, U:2 * U]), np.tanh(z[:, 2 * U:3 * U]),
                       sigmoid(z[:, 3 * U:]))
         c = f * c + i * g
@@ -467,8 +490,9 @@ def lstm_forward(P, X, done, h0, c0):
     return H, cache
 
 
-def lstm_backward(P, X, done, cache, dH, grads):
-    """BPTT through lstm_forward; returns dX.  No gradient into h0/c0."""
+def lstm_backward(P, X, done, cache, dH, grads, emu=False):
+    """BPTT through lstm_forward; returns dX.  No gradient into h0/c0.
+    emu: dz rounded to bf16 for every product it enters (C26)."""
     B, T1, K = X.shape
     U = P["lstm.wh"].shape[1]
     d = np.asarray(done).astype(bool)
@@ -488,11 +512,12 @@ def lstm_backward(P, X, done, cache, dH, grads):
         dc = dc_next + dh * o * (1.0 - tc ** 2)
         dz = np.concatenate([dc * g * i * (1 - i), dc * cp * f * (1 - f),
                              dc * i * (1 - g ** 2), dh * tc * o * (1 - o)], axis=1)
-        dWx += dz.T @ X[:, t]
-        dWh += dz.T @ cache["hprev"][:, t]
-        db += dz.sum(axis=0)
-        dX[:, t] = dz @ P["lstm.wx"]
-        dh_prev = dz @ P["lstm.wh"]
+        dzq = _q(dz, emu)
+        dWx += dzq.T @ X[:, t]
+        dWh += dzq.T @ _q(cache["hprev"][:, t], emu)
+        db += dzq.sum(axis=0)
+        dX[:, t] = dzq @ _q(P["lstm.wx"], emu)
+        dh_prev = dzq @ _q(P["lstm.wh"], emu)
         dc_prev = dc * f
         # the state entering step t was zeroed when done_t: no gradient flows past it
         dh_next = np.where(d[:, t, None], 0.0, dh_prev)
@@ -502,17 +527,17 @@ def lstm_backward(P, X, done, cache, dH, grads):
 
 
 # ---- whole network over a [B][T+1] batch ----------------------------------
-def network_forward(spec, P, batch):
+def network_forward(spec, P, batch, emu=False):
     """Returns logits [B][T1][A], values [B][T1] and a cache for backward."""
     obs = batch["obs"]
     B, T1 = obs.shape[:2]
     frames = np.asarray(obs).reshape((B * T1,) + tuple(obs.shape[2:]))
-    feat, tcache = torso_forward(spec, P, frames)
-    cache = dict(torso=tcache, B=B, T1=T1)
+    feat, tcache = torso_forward(spec, P, frames, emu)
+    cache = dict(torso=tcache, B=B, T1=T1, emu=emu)
     if spec.lstm_units > 0:
-        X = core_inputs(spec, feat, batch["prev_action"], batch["reward"], batch["done"])
+        X = core_inputs(spec, feat, batch["prev_action"], batch["reward"], batch["done"], emu)
         X = X.reshape(B, T1, -1)
-        H, lcache = lstm_forward(P, X, batch["done"], batch["h0"], batch["c0"])
+        H, lcache = lstm_forward(P, X, batch["done"], batch["h0"], batch["c0"], emu)
         cache.update(X=X, lstm=lcache)
         Hf = H.reshape(B * T1, -1)
     else:
@@ -529,13 +554,14 @@ def network_backward(spec, P, batch, cache, dlogits, dvalues):
     dout = np.concatenate([dlogits.reshape(B * T1, A), dvalues.reshape(B * T1, 1)], axis=1)
     grads = {"heads.w": dout.T @ cache["H"], "heads.b": dout.sum(axis=0)}
     dH = dout @ P["heads.w"]
+    emu = cache.get("emu", False)
     if spec.lstm_units > 0:
         dX = lstm_backward(P, cache["X"], batch["done"], cache["lstm"],
-                           dH.reshape(B, T1, -1), grads)
+                           dH.reshape(B, T1, -1), grads, emu)
         dfeat = dX.reshape(B * T1, -1)[:, :256]
     else:
         dfeat = dH
-    torso_backward(spec, P, cache["torso"], dfeat, grads)
+    torso_backward(spec, P, cache["torso"], dfeat, grads, emu)
     return grads
 
 
@@ -561,11 +587,12 @@ def clip_adam(params, grads, m, v, step, hp):
     return p2, m2, v2, t, norm, 1
 
 
-def learner_step(spec, params, m, v, step, batch, hp):
+def learner_step(spec, params, m, v, step, batch, hp, emu=False):
     """One full learner step (H1-H11) on one [B][T+1] batch; DP semantics (C20):
-    a single process on the concatenated batch with loss_scale = 1/(N B T)."""
+    a single process on the concatenated batch with loss_scale = 1/(N B T).
+    emu: bf16 rounding at the tensor-core path's rounding points (C26)."""
     P = unflatten(spec, params)
-    logits, values, cache = network_forward(spec, P, batch)
+    logits, values, cache = network_forward(spec, P, batch, emu)
     L = policy_loss(logits, values, batch["action"], batch["behaviour_logp"],
                     batch["reward"], batch["done"], hp)
     grads = network_backward(spec, P, batch, cache, L["dlogits"], L["dvalues"])
@@ -591,19 +618,19 @@ def sample_inverse_cdf(logits, u):
 
 
 def infer(spec, params, table_h, table_c, table_last_action, actor_ids, obs, reward, done,
-          uniforms):
+          uniforms, emu=False):
     """One batched inference call.  Returns (action, behaviour_logp, logits, new table
     arrays).  Actors not in actor_ids are untouched."""
     P = unflatten(spec, params)
     ids = np.asarray(actor_ids).astype(np.int64)
     d = np.asarray(done).astype(bool)
     th, tc, tla = table_h.copy(), table_c.copy(), table_last_action.copy()
-    feat, _ = torso_forward(spec, P, np.asarray(obs))
+    feat, _ = torso_forward(spec, P, np.asarray(obs), emu)
     if spec.lstm_units > 0:
-        X = core_inputs(spec, feat, tla[ids], reward, d)
+        X = core_inputs(spec, feat, tla[ids], reward, d, emu)
         h0 = np.where(d[:, None], 0.0, th[ids].astype(np.float64))
         c0 = np.where(d[:, None], 0.0, tc[ids].astype(np.float64))
-        H, lc = lstm_forward(P, X[:, None, :], np.zeros((len(ids), 1), bool), h0, c0)
+        H, lc = lstm_forward(P, X[:, None, :], np.zeros((len(ids), 1), bool), h0, c0, emu)
         h1, c1 = H[:, 0], lc["c"][:, 0]
         th[ids], tc[ids] = h1, c1
         feat = h1

@@ -59,8 +59,14 @@ _SIGS = {
     "seed_learner_step": (c_int, [P(NetSpec), c_int, c_int, P(Batch), P(TrainState),
                                   P(HParams), c_void_p, c_void_p, c_size_t, c_void_p,
                                   c_void_p]),
+    "seed_learner_step_traced": (c_int, [P(NetSpec), c_int, c_int, P(Batch), P(TrainState),
+                                         P(HParams), c_void_p, c_void_p, c_size_t, c_void_p,
+                                         c_void_p, P(c_void_p), c_int, P(C.c_char_p), P(c_int),
+                                         P(c_int)]),
     "seed_learner_outputs": (c_int, [P(NetSpec), c_int, c_int, c_void_p, P(c_void_p),
                                      P(c_void_p), P(c_void_p), P(c_void_p)]),
+    "seed_learner_debug_buffer": (c_int, [P(NetSpec), c_int, c_int, c_void_p, C.c_char_p,
+                                          P(c_void_p), P(c_size_t)]),
     "seed_comm_get_unique_id": (c_int, [c_void_p]),
     "seed_comm_init": (c_int, [c_void_p, c_int, c_int, P(c_void_p)]),
     "seed_comm_destroy": (c_int, [c_void_p]),

@@ -152,10 +152,15 @@ class HParams:
                          self.eps, self.max_grad_norm)
 
     def as_oracle(self):
-        return dict(discount=self.discount, rho_bar=self.rho_bar, c_bar=self.c_bar,
-                    vf_coef=self.vf_coef, ent_coef=self.ent_coef, loss_scale=self.loss_scale,
-                    lr=self.lr, beta1=self.beta1, beta2=self.beta2, eps=self.eps,
-                    max_grad_norm=self.max_grad_norm, **{"lambda": self.lam})
+        """The same hyper-parameters as the fp32 values the ABI receives (the
+        oracle gets the same input bytes as the kernels)."""
+        import struct
+        f = lambda x: struct.unpack("f", struct.pack("f", x))[0]
+        return dict(discount=f(self.discount), rho_bar=f(self.rho_bar), c_bar=f(self.c_bar),
+                    vf_coef=f(self.vf_coef), ent_coef=f(self.ent_coef),
+                    loss_scale=f(self.loss_scale), lr=f(self.lr), beta1=f(self.beta1),
+                    beta2=f(self.beta2), eps=f(self.eps), max_grad_norm=f(self.max_grad_norm),
+                    **{"lambda": f(self.lam)})
 
 
 class Comm:
@@ -252,6 +257,15 @@ class Learner:
                                         _stream(stream))
         L.check(st, "seed_learner_step")
         return self.metrics
+
+    def debug_buffer(self, name, dtype, shape):
+        """Test hook: a torch view of an internal workspace buffer (seed_learner_debug_buffer)."""
+        ptr, nb = C.c_void_p(), C.c_size_t()
+        L.check(L.load().seed_learner_debug_buffer(C.byref(self._spec_c), self.T, self.B,
+                                                   _ptr(self.ws), name.encode(), C.byref(ptr),
+                                                   C.byref(nb)), f"debug_buffer {name}")
+        off = ptr.value - self.ws.data_ptr()
+        return self.ws[off:off + nb.value].view(dtype).view(*shape)
 
     def outputs(self):
         """Views (logits, values, vs, pg_adv) into the workspace after a step."""

@@ -40,7 +40,7 @@ def build(force=False, verbose=False, jobs=None):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
-        if verbose:
+        if verbose > 1:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     failed = False

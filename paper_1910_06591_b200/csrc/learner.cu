@@ -1,0 +1,629 @@
+// learner.cu — seed_learner_step: one synchronous SEED learner update on one
+// GPU's [B][T+1] shard, with the DP gradient
+// allreduce (H10) when a communicator is given.
+//
+// Atari-shallow path (configs[1]; C14), every dense contraction on the
+// tcgen05 engine (gemm_tc.cuh), activations bf16 NHWC, rows f = b*(T+1)+t:
+//   conv1  implicit GEMM  [F*400 x 256] . [256 x 16]    (uint8 obs, /255 in the epilogue)
+//   conv2  implicit GEMM  [F*81  x 256] . [256 x 32]
+//   fc     GEMM           [F x 2592] . [2592 x 256]       (split-K)
+//   Xproj  GEMM           [F x 288]  . [288 x 1024]       (+ bias; x = [fc, onehot, r, 1])
+//   LSTM   persistent cluster kernel, T+1 serial steps (lstm.cu)
+//   heads  fp32 warp-per-row; K2 fused log-softmax + V-trace + loss + output grads
+//   heads backward; LSTM BPTT (cluster kernel)
+//   dW_x|b|dW_h  one GEMM  [1024 x F] . [F x (288+256)]    (ones column -> bias grad)
+//   dfc    GEMM  [F x 1024] . [1024 x 256]   (ReLU mask)
+//   dW_fc|b  GEMM [256 x F] . [F x 2600]    (ones column -> bias grad)
+//   dY2    GEMM  [F x 256] . [256 x 2592]   (ReLU mask)
+//   dW2    GEMM  [256 x F*81] . [F*81 x 32] (split-K)
+//   dY1    implicit transposed-conv GEMM [F*400 x 512] . [512 x 16] (ReLU mask)
+//   dW1    GEMM  [256 x F*400] . [F*400 x 16] (split-K, /255)
+//   conv biases: deterministic column sums
+//   [allreduce] -> global-norm clip + Adam -> bf16 operand image refresh
+#include <string.h>
+#include "gemm_tc.cuh"
+#include "learner_kernels.cuh"
+#include "lstm.cuh"
+#include "net.cuh"
+
+namespace seed {
+
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ bf16 to_bf(float v) { return __float2bfloat16_rn(v); }
+__device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
+
+struct Geo {
+  int H, W, C, oh1, ow1, oh2, ow2, fc_in, Kx, Kxp;
+};
+
+// conv1: A(m = (f, oy, ox), k = (ky, kx, c)) = obs[f][4oy+ky][4ox+kx][c] (uint8)
+struct Conv1Fwd {
+  static constexpr bool A_MN = false, B_MN = false;
+  int M, N, K, kb_per_split;
+  Geo g;
+  const uint8_t* obs;
+  const bf16* w;
+  const float* bias;
+  bf16* out;
+  __device__ uint4 load_a(int m, int k) const {
+    const int hw = g.oh1 * g.ow1;
+    const int f = m / hw, p = m % hw, oy = p / g.ow1, ox = p % g.ow1;
+    const int ky = k / (8 * g.C), kx = (k % (8 * g.C)) / g.C;
+    const uint8_t* src = obs + (((size_t)f * g.H + oy * 4 + ky) * g.W + ox * 4 + kx) * g.C;
+    return u8x8_to_bf16(__ldg(reinterpret_cast<const uint2*>(src)));
+  }
+  __device__ uint4 load_b(int n, int k) const { return ld16(w + (size_t)n * K + k); }
+  __device__ void store(int m, int n, float v) const {
+    out[(size_t)m * 16 + n] = to_bf(fmaxf(v * (1.f / 255.f) + bias[n], 0.f));
+  }
+};
+
+// conv2: A(m = (f, oy, ox), k = (ky, kx, c)) = act1[f][2oy+ky][2ox+kx][c]
+struct Conv2Fwd {
+  static constexpr bool A_MN = false, B_MN = false;
+  int M, N, K, kb_per_split;
+  Geo g;
+  const bf16* act1;
+  const bf16* w;
+  const float* bias;
+  bf16* out;
+  __device__ uint4 load_a(int m, int k) const {
+    const int hw = g.oh2 * g.ow2;
+    const int f = m / hw, p = m % hw, oy = p / g.ow2, ox = p % g.ow2;
+    const int ky = k >> 6, kx = (k >> 4) & 3, c0 = k & 15;
+    return ld16(act1 + (((size_t)f * g.oh1 + oy * 2 + ky) * g.ow1 + ox * 2 + kx) * 16 + c0);
+  }
+  __device__ uint4 load_b(int n, int k) const { return ld16(w + (size_t)n * 256 + k); }
+  __device__ void store(int m, int n, float v) const {
+    out[(size_t)m * 32 + n] = to_bf(fmaxf(v + bias[n], 0.f));
+  }
+};
+
+// fc: X[f][0:256] = relu(act2[f] . Wfc^T + b)
+struct FcFwd {
+  static constexpr bool A_MN = false, B_MN = false;
+  int M, N, K, kb_per_split;
+  int Kxp;
+  const bf16* act2;
+  const bf16* w;
+  const float* bias;
+  bf16* X;
+  __device__ uint4 load_a(int m, int k) const { return ld16(act2 + (size_t)m * K + k); }
+  __device__ uint4 load_b(int n, int k) const { return ld16(w + (size_t)n * K + k); }
+  __device__ void store(int m, int n, float v) const {
+    X[(size_t)m * Kxp + n] = to_bf(fmaxf(v + bias[n], 0.f));
+  }
+};
+
+// LSTM input projection: xproj[f][n] = X[f] . Wx[n] + b[n]
+struct XprojFwd {
+  static constexpr bool A_MN = false, B_MN = false;
+  int M, N, K, kb_per_split;
+  const bf16* X;
+  const bf16* w;
+  const float* bias;
+  float* out;
+  __device__ uint4 load_a(int m, int k) const { return ld16(X + (size_t)m * K + k); }
+  __device__ uint4 load_b(int n, int k) const { return ld16(w + (size_t)n * K + k); }
+  __device__ void store(int m, int n, float v) const { out[(size_t)m * N + n] = v + bias[n]; }
+};
+
+// [dWx | db | dWh] = dG^T . [X | Hprev]   (M = 4U gate rows, K = F rows)
+struct LstmWgrad {
+  static constexpr bool A_MN = true, B_MN = true;
+  int M, N, K, kb_per_split;
+  int Kx, Kxp, U;
+  const bf16* dG;
+  const bf16* X;
+  const bf16* Hprev;
+  float* g_wx;
+  float* g_b;
+  float* g_wh;
+  __device__ uint4 load_a(int row, int m8) const { return ld16(dG + (size_t)row * M + m8); }
+  __device__ uint4 load_b(int row, int n8) const {
+    return n8 < Kxp ? ld16(X + (size_t)row * Kxp + n8) : ld16(Hprev + (size_t)row * U + n8 - Kxp);
+  }
+  __device__ void store(int m, int n, float v) const {
+    if (n < Kx) g_wx[(size_t)m * Kx + n] = v;
+    else if (n == Kx) g_b[m] = v;
+    else if (n >= Kxp) g_wh[(size_t)m * U + (n - Kxp)] = v;
+  }
+};
+
+// dfc = (dG . Wx)[:, 0:256] masked by fc > 0
+struct DxFc {
+  static constexpr bool A_MN = false, B_MN = true;
+  int M, N, K, kb_per_split;
+  int Kxp;
+  const bf16* dG;
+  const bf16* wx;
+  const bf16* X;
+  bf16* dfc;
+  __device__ uint4 load_a(int m, int k) const { return ld16(dG + (size_t)m * K + k); }
+  __device__ uint4 load_b(int k, int n8) const { return ld16(wx + (size_t)k * Kxp + n8); }
+  __device__ void store(int m, int n, float v) const {
+    dfc[(size_t)m * 256 + n] = to_bf(bf2f(X[(size_t)m * Kxp + n]) > 0.f ? v : 0.f);
+  }
+};
+
+// [dWfc | dbfc] = dfc^T . [act2 | 1]
+struct FcWgrad {
+  static constexpr bool A_MN = true, B_MN = true;
+  int M, N, K, kb_per_split;
+  int fc_in;
+  const bf16* dfc;
+  const bf16* act2;
+  float* g_w;
+  float* g_b;
+  __device__ uint4 load_a(int row, int m8) const { return ld16(dfc + (size_t)row * 256 + m8); }
+  __device__ uint4 load_b(int row, int n8) const {
+    if (n8 < fc_in) return ld16(act2 + (size_t)row * fc_in + n8);
+    return make_uint4(0x3F80u, 0u, 0u, 0u);  // bf16 1.0 in column fc_in, zeros after
+  }
+  __device__ void store(int m, int n, float v) const {
+    if (n < fc_in) g_w[(size_t)m * fc_in + n] = v;
+    else if (n == fc_in) g_b[m] = v;
+  }
+};
+
+// dY2 = (dfc . Wfc) masked by act2 > 0
+struct FcDgrad {
+  static constexpr bool A_MN = false, B_MN = true;
+  int M, N, K, kb_per_split;
+  const bf16* dfc;
+  const bf16* w;
+  const bf16* act2;
+  bf16* dY2;
+  __device__ uint4 load_a(int m, int k) const { return ld16(dfc + (size_t)m * 256 + k); }
+  __device__ uint4 load_b(int k, int n8) const { return ld16(w + (size_t)k * N + n8); }
+  __device__ void store(int m, int n, float v) const {
+    const size_t i = (size_t)m * N + n;
+    dY2[i] = to_bf(bf2f(act2[i]) > 0.f ? v : 0.f);
+  }
+};
+
+// dW2^T[kin][co] = sum_rows im2col(act1)[row][kin] dY2[row][co]
+struct Conv2Wgrad {
+  static constexpr bool A_MN = true, B_MN = true;
+  int M, N, K, kb_per_split;
+  Geo g;
+  const bf16* act1;
+  const bf16* dY2;
+  float* g_w;
+  __device__ uint4 load_a(int row, int m8) const {
+    const int hw = g.oh2 * g.ow2;
+    const int f = row / hw, p = row % hw, oy = p / g.ow2, ox = p % g.ow2;
+    const int ky = m8 >> 6, kx = (m8 >> 4) & 3, c0 = m8 & 15;
+    return ld16(act1 + (((size_t)f * g.oh1 + oy * 2 + ky) * g.ow1 + ox * 2 + kx) * 16 + c0);
+  }
+  __device__ uint4 load_b(int row, int n8) const { return ld16(dY2 + (size_t)row * 32 + n8); }
+  __device__ void store(int m, int n, float v) const { g_w[(size_t)n * 256 + m] = v; }
+};
+
+// dY1 = transposed conv of dY2 (implicit GEMM, k = (ky, kx, co)), masked by act1 > 0
+struct Conv2Dgrad {
+  static constexpr bool A_MN = false, B_MN = false;
+  int M, N, K, kb_per_split;
+  Geo g;
+  const bf16* dY2;
+  const bf16* wdg;  // [16 ci][4 ky][4 kx][32 co]
+  const bf16* act1;
+  bf16* dY1;
+  __device__ uint4 load_a(int m, int k) const {
+    const int hw = g.oh1 * g.ow1;
+    const int f = m / hw, p = m % hw, y = p / g.ow1, x = p % g.ow1;
+    const int ky = k >> 7, kx = (k >> 5) & 3, co0 = k & 31;
+    const int yy = y - ky, xx = x - kx;
+    if (yy < 0 || xx < 0 || (yy & 1) || (xx & 1)) return make_uint4(0, 0, 0, 0);
+    const int oy = yy >> 1, ox = xx >> 1;
+    if (oy >= g.oh2 || ox >= g.ow2) return make_uint4(0, 0, 0, 0);
+    return ld16(dY2 + (((size_t)f * g.oh2 + oy) * g.ow2 + ox) * 32 + co0);
+  }
+  __device__ uint4 load_b(int n, int k) const { return ld16(wdg + (size_t)n * K + k); }
+  __device__ void store(int m, int n, float v) const {
+    const size_t i = (size_t)m * 16 + n;
+    dY1[i] = to_bf(bf2f(act1[i]) > 0.f ? v : 0.f);
+  }
+};
+
+// dW1^T[kin][co] = (1/255) sum_rows im2col(obs)[row][kin] dY1[row][co]
+struct Conv1Wgrad {
+  static constexpr bool A_MN = true, B_MN = true;
+  int M, N, K, kb_per_split;
+  Geo g;
+  const uint8_t* obs;
+  const bf16* dY1;
+  float* g_w;
+  __device__ uint4 load_a(int row, int m8) const {
+    const int hw = g.oh1 * g.ow1;
+    const int f = row / hw, p = row % hw, oy = p / g.ow1, ox = p % g.ow1;
+    const int ky = m8 / (8 * g.C), kx = (m8 % (8 * g.C)) / g.C;
+    const uint8_t* src = obs + (((size_t)f * g.H + oy * 4 + ky) * g.W + ox * 4 + kx) * g.C;
+    return u8x8_to_bf16(__ldg(reinterpret_cast<const uint2*>(src)));
+  }
+  __device__ uint4 load_b(int row, int n8) const { return ld16(dY1 + (size_t)row * 16 + n8); }
+  __device__ void store(int m, int n, float v) const {
+    g_w[(size_t)n * M + m] = v * (1.f / 255.f);
+  }
+};
+
+struct Trace {
+  void** events = nullptr;
+  const char** names = nullptr;
+  int max = 0, n = 0, launches = 0;
+};
+
+struct StepCtx {
+  const NetPlan* p;
+  LearnerWs w;
+  uint8_t* ws;
+  Geo g;
+  Trace* tr = nullptr;
+  cudaStream_t st;
+  template <class T>
+  T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+  // end of a phase of `k` kernel launches
+  void mark(const char* name, int k = 1) const {
+    if (!tr) return;
+    tr->launches += k;
+    if (tr->events && tr->n < tr->max) {
+      cudaEventRecord((cudaEvent_t)tr->events[tr->n], st);
+      if (tr->names) tr->names[tr->n] = name;
+      tr->n++;
+    }
+  }
+};
+
+template <int BN, class Prob>
+static seed_status gemm(const StepCtx& c, Prob pr, cudaStream_t st, const char* name) {
+  const int s = pick_splits(pr.M, pr.N, BN, pr.K);
+  const seed_status r = launch_gemm<BN>(pr, s, st, c.at<float>(c.w.splitk));
+  c.mark(name, s > 1 ? 2 : 1);
+  return r;
+}
+
+static seed_status shallow_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
+                                   const float* params, cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int F = w.F;
+  {
+    Conv1Fwd pr{};
+    pr.M = F * p.oh1 * p.ow1; pr.N = 16; pr.K = 64 * p.C;
+    pr.g = c.g; pr.obs = (const uint8_t*)bt->obs; pr.w = lowp + p.im_conv1;
+    pr.bias = params + p.t[p.i_conv1b].off; pr.out = c.at<bf16>(w.act1);
+    SEED_TRY(gemm<16>(c, pr, st, "conv1_fwd"));
+  }
+  {
+    Conv2Fwd pr{};
+    pr.M = F * p.oh2 * p.ow2; pr.N = 32; pr.K = 256;
+    pr.g = c.g; pr.act1 = c.at<bf16>(w.act1); pr.w = lowp + p.im_conv2;
+    pr.bias = params + p.t[p.i_conv2b].off; pr.out = c.at<bf16>(w.act2);
+    SEED_TRY(gemm<32>(c, pr, st, "conv2_fwd"));
+  }
+  {
+    FcFwd pr{};
+    pr.M = F; pr.N = 256; pr.K = p.fc_in; pr.Kxp = p.Kxp;
+    pr.act2 = c.at<bf16>(w.act2); pr.w = lowp + p.im_fc;
+    pr.bias = params + p.t[p.i_fcb].off; pr.X = c.at<bf16>(w.X);
+    SEED_TRY(gemm<128>(c, pr, st, "fc_fwd"));
+  }
+  {
+    const int E = p.Kxp - 256;
+    const int64_t n = (int64_t)F * E;
+    core_extras_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(
+        F, p.A, p.Kxp, bt->prev_action, bt->reward, bt->done, c.at<bf16>(w.X));
+    c.mark("core_extras");
+  }
+  {
+    XprojFwd pr{};
+    pr.M = F; pr.N = 4 * p.U; pr.K = p.Kxp;
+    pr.X = c.at<bf16>(w.X); pr.w = lowp + p.im_wx;
+    pr.bias = params + p.t[p.i_lb].off; pr.out = c.at<float>(w.xproj);
+    SEED_TRY(gemm<128>(c, pr, st, "xproj_fwd"));
+  }
+  LstmFwdArgs la{};
+  la.B = w.B; la.T1 = w.T1;
+  la.xproj = c.at<float>(w.xproj);
+  la.wh = lowp + p.im_wh;
+  la.h0 = bt->h0; la.c0 = bt->c0; la.state_rows = nullptr;
+  la.done = bt->done;
+  la.H = c.at<float>(w.H); la.Hb = nullptr; la.Hprev = c.at<bf16>(w.Hprev);
+  la.gates = c.at<float>(w.gates); la.C = c.at<float>(w.Cst);
+  la.hT = la.cT = nullptr;
+  SEED_TRY(lstm_forward(la, st));
+  c.mark("lstm_fwd");
+  dense_fwd_f32<<<ceil_div(F * 32, 256), 256, 0, st>>>(
+      F, p.U, p.A + 1, c.at<float>(w.H), params + p.t[p.i_hw].off, params + p.t[p.i_hb].off,
+      c.at<float>(w.logits), p.A, c.at<float>(w.values), 0);
+  c.mark("heads_fwd");
+  return last_launch();
+}
+
+static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
+                                    const float* params, float* grads, cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int F = w.F, U = p.U, A = p.A;
+  // heads
+  dense_dgrad_f32<<<ceil_div(F * U, 256), 256, 0, st>>>(
+      F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), params + p.t[p.i_hw].off,
+      nullptr, c.at<float>(w.dH));
+  dense_wgrad_f32<<<ceil_div((A + 1) * (U + 1), 256), 256, 0, st>>>(
+      F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), c.at<float>(w.H),
+      grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off);
+  SEED_TRY(last_launch());
+  c.mark("heads_bwd", 2);
+  // LSTM BPTT
+  LstmBwdArgs lb{};
+  lb.B = w.B; lb.T1 = w.T1; lb.wh = lowp + p.im_wh;
+  lb.gates = c.at<float>(w.gates); lb.C = c.at<float>(w.Cst); lb.c0 = bt->c0;
+  lb.done = bt->done; lb.dH = c.at<float>(w.dH); lb.dG = c.at<bf16>(w.dG);
+  SEED_TRY(lstm_backward(lb, st));
+  c.mark("lstm_bwd");
+  {
+    LstmWgrad pr{};
+    pr.M = 4 * U; pr.N = p.Kxp + U; pr.K = F;
+    pr.Kx = p.Kx; pr.Kxp = p.Kxp; pr.U = U;
+    pr.dG = c.at<bf16>(w.dG); pr.X = c.at<bf16>(w.X); pr.Hprev = c.at<bf16>(w.Hprev);
+    pr.g_wx = grads + p.t[p.i_wx].off; pr.g_b = grads + p.t[p.i_lb].off;
+    pr.g_wh = grads + p.t[p.i_wh].off;
+    SEED_TRY(gemm<128>(c, pr, st, "lstm_wgrad"));
+  }
+  {
+    DxFc pr{};
+    pr.M = F; pr.N = 256; pr.K = 4 * U; pr.Kxp = p.Kxp;
+    pr.dG = c.at<bf16>(w.dG); pr.wx = lowp + p.im_wx; pr.X = c.at<bf16>(w.X);
+    pr.dfc = c.at<bf16>(w.dfc);
+    SEED_TRY(gemm<128>(c, pr, st, "dx_fc"));
+  }
+  {
+    FcWgrad pr{};
+    pr.M = 256; pr.N = p.fc_in + 8; pr.K = F; pr.fc_in = p.fc_in;
+    pr.dfc = c.at<bf16>(w.dfc); pr.act2 = c.at<bf16>(w.act2);
+    pr.g_w = grads + p.t[p.i_fcw].off; pr.g_b = grads + p.t[p.i_fcb].off;
+    SEED_TRY(gemm<128>(c, pr, st, "fc_wgrad"));
+  }
+  {
+    FcDgrad pr{};
+    pr.M = F; pr.N = p.fc_in; pr.K = 256;
+    pr.dfc = c.at<bf16>(w.dfc); pr.w = lowp + p.im_fc; pr.act2 = c.at<bf16>(w.act2);
+    pr.dY2 = c.at<bf16>(w.dY2);
+    SEED_TRY(gemm<128>(c, pr, st, "fc_dgrad"));
+  }
+  {
+    Conv2Wgrad pr{};
+    pr.M = 256; pr.N = 32; pr.K = F * p.oh2 * p.ow2; pr.g = c.g;
+    pr.act1 = c.at<bf16>(w.act1); pr.dY2 = c.at<bf16>(w.dY2);
+    pr.g_w = grads + p.t[p.i_conv2w].off;
+    SEED_TRY(gemm<32>(c, pr, st, "conv2_wgrad"));
+  }
+  SEED_TRY(colsum_bf16(c.at<bf16>(w.dY2), (int64_t)F * p.oh2 * p.ow2, 32,
+                       c.at<float>(w.colsum_part), grads + p.t[p.i_conv2b].off, st));
+  c.mark("conv2_bias", 2);
+  {
+    Conv2Dgrad pr{};
+    pr.M = F * p.oh1 * p.ow1; pr.N = 16; pr.K = 512; pr.g = c.g;  // k = (ky, kx, co)
+    pr.dY2 = c.at<bf16>(w.dY2); pr.wdg = lowp + p.im_conv2dg; pr.act1 = c.at<bf16>(w.act1);
+    pr.dY1 = c.at<bf16>(w.dY1);
+    SEED_TRY(gemm<16>(c, pr, st, "conv2_dgrad"));
+  }
+  {
+    Conv1Wgrad pr{};
+    pr.M = 64 * p.C; pr.N = 16; pr.K = F * p.oh1 * p.ow1; pr.g = c.g;
+    pr.obs = (const uint8_t*)bt->obs; pr.dY1 = c.at<bf16>(w.dY1);
+    pr.g_w = grads + p.t[p.i_conv1w].off;
+    SEED_TRY(gemm<16>(c, pr, st, "conv1_wgrad"));
+  }
+  SEED_TRY(colsum_bf16(c.at<bf16>(w.dY1), (int64_t)F * p.oh1 * p.ow1, 16,
+                       c.at<float>(w.colsum_part), grads + p.t[p.i_conv1b].off, st));
+  c.mark("conv1_bias", 2);
+  return SEED_OK;
+}
+
+static seed_status mlp_forward(const StepCtx& c, const seed_batch* bt, const float* params,
+                               cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int F = w.F;
+  const int blocks = ceil_div(F * 32, 256);
+  dense_fwd_f32<<<blocks, 256, 0, st>>>(F, p.D, 64, (const float*)bt->obs, params + p.t[p.i_m0w].off,
+                                        params + p.t[p.i_m0b].off, c.at<float>(w.h1), 64, nullptr, 1);
+  dense_fwd_f32<<<blocks, 256, 0, st>>>(F, 64, 64, c.at<float>(w.h1), params + p.t[p.i_m1w].off,
+                                        params + p.t[p.i_m1b].off, c.at<float>(w.h2), 64, nullptr, 1);
+  dense_fwd_f32<<<blocks, 256, 0, st>>>(F, 64, p.A + 1, c.at<float>(w.h2), params + p.t[p.i_hw].off,
+                                        params + p.t[p.i_hb].off, c.at<float>(w.logits), p.A,
+                                        c.at<float>(w.values), 0);
+  c.mark("mlp_fwd", 3);
+  return last_launch();
+}
+
+static seed_status mlp_backward(const StepCtx& c, const seed_batch* bt, const float* params,
+                                float* grads, cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int F = w.F, A = p.A;
+  dense_dgrad_f32<<<ceil_div(F * 64, 256), 256, 0, st>>>(
+      F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), params + p.t[p.i_hw].off,
+      c.at<float>(w.h2), c.at<float>(w.dh2));
+  dense_wgrad_f32<<<ceil_div((A + 1) * 65, 256), 256, 0, st>>>(
+      F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), c.at<float>(w.h2),
+      grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off);
+  dense_dgrad_f32<<<ceil_div(F * 64, 256), 256, 0, st>>>(
+      F, 64, 64, c.at<float>(w.dh2), 64, nullptr, params + p.t[p.i_m1w].off, c.at<float>(w.h1),
+      c.at<float>(w.dh1));
+  dense_wgrad_f32<<<ceil_div(64 * 65, 256), 256, 0, st>>>(
+      F, 64, 64, c.at<float>(w.dh2), 64, nullptr, c.at<float>(w.h1), grads + p.t[p.i_m1w].off,
+      grads + p.t[p.i_m1b].off);
+  dense_wgrad_f32<<<ceil_div(64 * (p.D + 1), 256), 256, 0, st>>>(
+      F, p.D, 64, c.at<float>(w.dh1), 64, nullptr, (const float*)bt->obs,
+      grads + p.t[p.i_m0w].off, grads + p.t[p.i_m0b].off);
+  c.mark("mlp_bwd", 5);
+  return last_launch();
+}
+
+seed_status comm_allreduce(seed_comm* comm, float* data, int64_t n, cudaStream_t st);
+
+static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
+                                     const seed_batch* batch, const seed_train_state* state,
+                                     const seed_hparams* hp, seed_comm* comm, void* ws,
+                                     size_t ws_bytes, float* metrics, void* stream, Trace* tr) {
+  NetPlan p;
+  SEED_TRY(make_net_plan(spec, &p));
+  if (!learner_supported(p)) return SEED_E_UNSUPPORTED;
+  if (T < 1 || T > 256 || B < 1 || B > 1024) return SEED_E_SHAPE;
+  if (!batch || !state || !hp || !ws || !metrics) return SEED_E_ARG;
+  if (!batch->obs || !batch->action || !batch->reward || !batch->done || !batch->behaviour_logp ||
+      !state->params || !state->grads || !state->adam_m || !state->adam_v || !state->step)
+    return SEED_E_ARG;
+  if (p.kind != SEED_NET_MLP &&
+      (!batch->prev_action || !batch->h0 || !batch->c0 || !state->params_lowp ||
+       !aligned16(batch->obs) || !aligned16(ws) || !aligned16(state->params_lowp)))
+    return SEED_E_ARG;
+  if (!(hp->c_bar > 0.f) || !(hp->rho_bar >= hp->c_bar) || !(hp->lambda >= 0.f && hp->lambda <= 1.f) ||
+      !(hp->max_grad_norm > 0.f))
+    return SEED_E_ARG;
+  StepCtx c;
+  c.p = &p;
+  SEED_TRY(make_learner_ws(p, T, B, &c.w));
+  if (ws_bytes < c.w.total) return SEED_E_WORKSPACE;
+  c.ws = (uint8_t*)ws;
+  c.g = Geo{p.H, p.W, p.C, p.oh1, p.ow1, p.oh2, p.ow2, p.fc_in, p.Kx, p.Kxp};
+  cudaStream_t st = (cudaStream_t)stream;
+  c.st = st;
+  c.tr = tr;
+  if (tr && tr->events && tr->max > 0) {
+    cudaEventRecord((cudaEvent_t)tr->events[0], st);
+    if (tr->names) tr->names[0] = "begin";
+    tr->n = 1;
+  }
+  const float* params = state->params;
+  const bf16* lowp = (const bf16*)state->params_lowp;
+  float* grads = state->grads;
+
+  if (p.kind == SEED_NET_MLP) SEED_TRY(mlp_forward(c, batch, params, st));
+  else SEED_TRY(shallow_forward(c, batch, lowp, params, st));
+
+  LossArgs la{};
+  la.B = B; la.T = T; la.A = p.A;
+  la.logits = c.at<float>(c.w.logits); la.values = c.at<float>(c.w.values);
+  la.action = batch->action; la.blp = batch->behaviour_logp; la.reward = batch->reward;
+  la.done = batch->done;
+  la.discount = hp->discount; la.rho_bar = hp->rho_bar; la.c_bar = hp->c_bar;
+  la.lam = hp->lambda; la.vf_coef = hp->vf_coef; la.ent_coef = hp->ent_coef;
+  la.scale = hp->loss_scale;
+  la.dlogits = c.at<float>(c.w.dlogits); la.dvalues = c.at<float>(c.w.dvalues);
+  la.vs = c.at<float>(c.w.vs); la.pg = c.at<float>(c.w.pg); la.part = c.at<float>(c.w.loss_part);
+  SEED_TRY(launch_policy_loss(la, st));
+  c.mark("policy_loss");
+
+  if (p.kind == SEED_NET_MLP) SEED_TRY(mlp_backward(c, batch, params, grads, st));
+  else SEED_TRY(shallow_backward(c, batch, lowp, params, grads, st));
+
+  if (comm) {
+    SEED_TRY(comm_allreduce(comm, grads, p.P, st));
+    c.mark("allreduce");
+  }
+
+  grad_norm_kernel<<<NORM_BLOCKS, 256, 0, st>>>(grads, p.P, c.at<double>(c.w.norm_part),
+                                                state->step, c.at<int64_t>(c.w.step_in));
+  c.mark("grad_norm");
+  AdamArgs aa{};
+  aa.P = p.P; aa.params = state->params; aa.grads = grads; aa.m = state->adam_m;
+  aa.v = state->adam_v; aa.step = state->step; aa.step_in = c.at<int64_t>(c.w.step_in);
+  aa.norm_part = c.at<double>(c.w.norm_part); aa.nblocks_norm = NORM_BLOCKS;
+  aa.lr = hp->lr; aa.beta1 = hp->beta1; aa.beta2 = hp->beta2; aa.eps = hp->eps;
+  aa.max_norm = hp->max_grad_norm; aa.loss_part = c.at<float>(c.w.loss_part); aa.B = B;
+  aa.metrics = metrics;
+  SEED_TRY(launch_clip_adam(aa, st));
+  c.mark("clip_adam");
+  if (p.nimg) {
+    SEED_TRY(refresh_lowp(p, state->params, state->params_lowp, st));
+    c.mark("lowp_refresh", p.nimg);
+  }
+  return last_launch();
+}
+
+}  // namespace seed
+
+extern "C" seed_status seed_learner_step(const seed_net_spec* spec, int T, int B,
+                                         const seed_batch* batch, const seed_train_state* state,
+                                         const seed_hparams* hp, seed_comm* comm, void* ws,
+                                         size_t ws_bytes, float* metrics, void* stream) {
+  return seed::learner_step_impl(spec, T, B, batch, state, hp, comm, ws, ws_bytes, metrics,
+                                 stream, nullptr);
+}
+
+extern "C" seed_status seed_learner_step_traced(const seed_net_spec* spec, int T, int B,
+                                                const seed_batch* batch,
+                                                const seed_train_state* state,
+                                                const seed_hparams* hp, seed_comm* comm,
+                                                void* ws, size_t ws_bytes, float* metrics,
+                                                void* stream, void** events, int max_events,
+                                                const char** names_out, int* n_events_out,
+                                                int* n_launches_out) {
+  seed::Trace tr;
+  tr.events = events;
+  tr.names = names_out;
+  tr.max = events ? max_events : 0;
+  const seed_status r = seed::learner_step_impl(spec, T, B, batch, state, hp, comm, ws, ws_bytes,
+                                                metrics, stream, &tr);
+  if (n_events_out) *n_events_out = tr.n;
+  if (n_launches_out) *n_launches_out = tr.launches;
+  return r;
+}
+
+namespace seed {
+
+}  // namespace seed
+
+using namespace seed;
+
+extern "C" seed_status seed_learner_outputs(const seed_net_spec* spec, int T, int B, void* ws,
+                                            float** logits, float** values, float** vs,
+                                            float** pg) {
+  NetPlan p;
+  SEED_TRY(make_net_plan(spec, &p));
+  if (!learner_supported(p)) return SEED_E_UNSUPPORTED;
+  if (!ws) return SEED_E_ARG;
+  LearnerWs w;
+  SEED_TRY(make_learner_ws(p, T, B, &w));
+  uint8_t* b = (uint8_t*)ws;
+  if (logits) *logits = (float*)(b + w.logits);
+  if (values) *values = (float*)(b + w.values);
+  if (vs) *vs = (float*)(b + w.vs);
+  if (pg) *pg = (float*)(b + w.pg);
+  return SEED_OK;
+}
+
+extern "C" seed_status seed_learner_debug_buffer(const seed_net_spec* spec, int T, int B, void* ws,
+                                                 const char* name, void** ptr, size_t* bytes) {
+  NetPlan p;
+  SEED_TRY(make_net_plan(spec, &p));
+  if (!learner_supported(p)) return SEED_E_UNSUPPORTED;
+  if (!ws || !name || !ptr) return SEED_E_ARG;
+  LearnerWs w;
+  SEED_TRY(make_learner_ws(p, T, B, &w));
+  const size_t F = w.F, U = p.U;
+  struct Ent { const char* n; size_t off, bytes; };
+  const bool mlp = p.kind == SEED_NET_MLP;
+  const Ent ents[] = {
+      {"dlogits", w.dlogits, F * p.A * 4}, {"dvalues", w.dvalues, F * 4},
+      {"act1", mlp ? 0 : w.act1, F * p.oh1 * p.ow1 * 16 * 2}, {"act2", mlp ? 0 : w.act2, F * p.fc_in * 2},
+      {"X", mlp ? 0 : w.X, F * p.Kxp * 2}, {"xproj", mlp ? 0 : w.xproj, F * 4 * U * 4},
+      {"H", mlp ? 0 : w.H, F * U * 4}, {"Hprev", mlp ? 0 : w.Hprev, F * U * 2},
+      {"gates", mlp ? 0 : w.gates, F * 4 * U * 4}, {"C", mlp ? 0 : w.Cst, F * U * 4},
+      {"dH", mlp ? 0 : w.dH, F * U * 4}, {"dG", mlp ? 0 : w.dG, F * 4 * U * 2},
+      {"dfc", mlp ? 0 : w.dfc, F * 256 * 2}, {"dY2", mlp ? 0 : w.dY2, F * p.fc_in * 2},
+      {"dY1", mlp ? 0 : w.dY1, F * p.oh1 * p.ow1 * 16 * 2},
+      {"h1", mlp ? w.h1 : 0, F * 64 * 4}, {"h2", mlp ? w.h2 : 0, F * 64 * 4},
+      {"dh1", mlp ? w.dh1 : 0, F * 64 * 4}, {"dh2", mlp ? w.dh2 : 0, F * 64 * 4}};
+  for (const Ent& e : ents)
+    if (strcmp(e.n, name) == 0 && e.off) {
+      *ptr = (uint8_t*)ws + e.off;
+      if (bytes) *bytes = e.bytes;
+      return SEED_OK;
+    }
+  return SEED_E_ARG;
+}

@@ -1,0 +1,73 @@
+// learner_kernels.cuh — the non-GEMM kernels of the learner step: fp32 dense
+// layers (the configs[0] MLP and the policy/value heads), the fused policy
+// loss (K2: log-softmax + V-trace scan + loss + output gradients), column sums
+// for conv bias gradients, LSTM core-input extras, global-norm clip + Adam (K9).
+#pragma once
+#include "common.cuh"
+#include "vtrace_scan.cuh"
+
+namespace seed {
+
+// Y[r][o] = act(b[o] + sum_i X[r][i] W[o][i]); one warp per row.  Optional split
+// output: columns o < A go to Y (ld A), column A to Yv (heads: logits / value).
+__global__ void dense_fwd_f32(int R, int I, int O, const float* __restrict__ X,
+                              const float* __restrict__ W, const float* __restrict__ b,
+                              float* __restrict__ Y, int ldy, float* __restrict__ Yv, int relu);
+
+// dX[r][i] = (sum_o dY(r,o) W[o][i]) * (mask ? mask[r][i] > 0 : 1), dY(r,o) = o < ldy ?
+// dy[r*ldy+o] : dv[r] (dv used for the last column when non-null).
+__global__ void dense_dgrad_f32(int R, int I, int O, const float* __restrict__ dy, int ldy,
+                                const float* __restrict__ dv, const float* __restrict__ W,
+                                const float* __restrict__ mask, float* __restrict__ dX);
+
+// gW[o][i] = sum_r dY(r,o) X[r][i];  gb[o] = sum_r dY(r,o)  (thread per (o,i), fixed order)
+__global__ void dense_wgrad_f32(int R, int I, int O, const float* __restrict__ dy, int ldy,
+                                const float* __restrict__ dv, const float* __restrict__ X,
+                                float* __restrict__ gW, float* __restrict__ gb);
+
+struct LossArgs {
+  int B, T, A;
+  const float* logits;   // [B][T+1][A]
+  const float* values;   // [B][T+1]
+  const int32_t* action;
+  const float* blp;
+  const float* reward;
+  const uint8_t* done;   // [B][T+1]
+  float discount, rho_bar, c_bar, lam, vf_coef, ent_coef, scale;
+  float* dlogits;        // [B][T+1][A]
+  float* dvalues;        // [B][T+1]
+  float* vs;             // [B][T]
+  float* pg;             // [B][T]
+  float* part;           // [B][4]: scaled pg, baseline, entropy terms, nonfinite
+};
+seed_status launch_policy_loss(const LossArgs& a, cudaStream_t st);
+
+// X[f][256 + j] for j in [0, Kxp-256): onehot(prev_action), clip(reward), 1, 0 pad (C15)
+__global__ void core_extras_kernel(int F, int A, int Kxp, const int32_t* __restrict__ prev_action,
+                                   const float* __restrict__ reward,
+                                   const uint8_t* __restrict__ done, __nv_bfloat16* X);
+
+// out[c] = sum_r X[r][c] (bf16 input), deterministic two-phase.
+seed_status colsum_bf16(const __nv_bfloat16* X, int64_t R, int C, float* part, float* out,
+                        cudaStream_t st);
+
+struct AdamArgs {
+  int64_t P;
+  float* params;
+  const float* grads;
+  float* m;
+  float* v;
+  int64_t* step;
+  const int64_t* step_in;
+  const double* norm_part;
+  int nblocks_norm;
+  float lr, beta1, beta2, eps, max_norm;
+  const float* loss_part;  // [B][4]
+  int B;
+  float* metrics;          // [8]
+};
+seed_status launch_clip_adam(const AdamArgs& a, cudaStream_t st);
+__global__ void grad_norm_kernel(const float* __restrict__ g, int64_t P, double* __restrict__ part,
+                                 const int64_t* step, int64_t* step_in);
+
+}  // namespace seed

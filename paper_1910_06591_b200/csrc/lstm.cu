@@ -1,0 +1,351 @@
+// lstm.cu — K7/K8: persistent cluster LSTM core over T+1 serial steps.
+//
+// Definition (P:591 core inputs; S:47/S:57 reset; reading C15): for t = 0..T,
+//   if done_t: (h, c) <- 0;  z = Xproj_t + W_h h;  i,f,o = sigmoid, g = tanh
+//   c = f c + i g;  h = o tanh(c)
+// The input projection Xproj = W_x x_t + b for all (T+1)B rows is one tcgen05
+// GEMM beforehand; only the recurrent product is serial.  A cluster of 8 CTAs
+// serves 32 batch rows: CTA r owns hidden units [32r, 32r+32), keeps its
+// 128x256 slice of W_h (i,f,g,o rows of those units) resident in shared
+// memory for all steps, computes its 32x128 gate block with mma.sync
+// (latency-bound recurrence: the per-step product is 32x128x256), updates the
+// cell for its units, and broadcasts its slice of h_t to the 8 CTAs through
+// distributed shared memory; one cluster barrier per step.
+// BPTT mirrors it: each CTA forms dz for its 128 gate columns, multiplies by
+// its W_h slice (dz W_h, 32x256 partial), scatters the partial columns to the
+// owning CTAs over DSMEM, and each owner sums the 8 partials in fixed order
+// (deterministic, no atomics).
+#include "lstm.cuh"
+#include "gemm_tc.cuh"
+
+namespace seed {
+
+constexpr int HP = LSTM_U + 8;  // padded bf16 row for W slice / h buffers (conflict-free ldmatrix)
+constexpr int DP = 128 + 8;     // padded bf16 row for dz
+constexpr int GP = 128 + 4;     // padded fp32 row for the gate pre-activations
+constexpr int RP = 36;          // padded fp32 row for the dh reduction slots
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_f32x2(uint32_t addr, float a, float b) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+
+// CTA r's W_h slice: local row lc = gate*32 + j  <-  global row gate*U + 32r + j
+__device__ __forceinline__ void load_wh_slice(__nv_bfloat16* Ws, const __nv_bfloat16* wh, int r) {
+  for (int c = threadIdx.x; c < 128 * 32; c += blockDim.x) {
+    const int lc = c >> 5, kc = c & 31;
+    const int gr = (lc >> 5) * LSTM_U + 32 * r + (lc & 31);
+    *reinterpret_cast<uint4*>(Ws + lc * HP + kc * 8) = ld16(wh + (size_t)gr * LSTM_U + kc * 8);
+  }
+}
+
+constexpr int FWD_SMEM = 128 * HP * 2 + 2 * 32 * HP * 2 + 32 * GP * 4 + 32 * 32 * 4;
+constexpr int BWD_SMEM = 128 * HP * 2 + 32 * DP * 2 + 2 * 8 * 32 * RP * 4 + 32 * 32 * 4;
+
+__global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
+    lstm_fwd_kernel(const LstmFwdArgs a) {
+  constexpr int U = LSTM_U;
+  extern __shared__ __align__(16) uint8_t sm[];
+  __nv_bfloat16* Ws = reinterpret_cast<__nv_bfloat16*>(sm);
+  __nv_bfloat16* hb = Ws + 128 * HP;
+  float* gpre = reinterpret_cast<float*>(hb + 2 * 32 * HP);
+  float* cst = gpre + 32 * GP;
+  const int r = (int)cluster_rank();
+  const int b0 = (blockIdx.x / LSTM_CLUSTER) * LSTM_BB;
+  const int BB = min(LSTM_BB, a.B - b0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T1 = a.T1;
+
+  load_wh_slice(Ws, a.wh, r);
+  for (int idx = tid; idx < 32 * U; idx += 256) {
+    const int b = idx / U, k = idx % U;
+    float v = 0.f;
+    if (b < BB) {
+      const int bb = b0 + b;
+      const int srow = a.state_rows ? a.state_rows[bb] : bb;
+      if (!a.done[(size_t)bb * T1]) v = a.h0[(size_t)srow * U + k];
+    }
+    hb[b * HP + k] = __float2bfloat16_rn(v);
+  }
+  for (int idx = tid; idx < 32 * 32; idx += 256) {
+    const int b = idx >> 5, j = idx & 31;
+    float c = 0.f, h = 0.f;
+    if (b < BB) {
+      const int bb = b0 + b;
+      const int srow = a.state_rows ? a.state_rows[bb] : bb;
+      if (!a.done[(size_t)bb * T1]) {
+        c = a.c0[(size_t)srow * U + 32 * r + j];
+        h = a.h0[(size_t)srow * U + 32 * r + j];
+      }
+      if (a.Hprev) a.Hprev[((size_t)bb * T1) * U + 32 * r + j] = __float2bfloat16_rn(h);
+    }
+    cst[b * 32 + j] = c;
+  }
+  __syncthreads();
+  cluster_sync_all();
+
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int t = 0; t < T1; ++t) {
+    const __nv_bfloat16* hcur = hb + (t & 1) * 32 * HP;
+    float acc[2][2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.f;
+#pragma unroll 4
+    for (int ks = 0; ks < 16; ++ks) {
+      uint32_t af[2][4], bfr[4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+        ldsm_x4(smem_u32(hcur + (mt * 16 + (lane & 15)) * HP + ks * 16 + (lane >> 4) * 8), af[mt]);
+      const int mi = lane >> 3;
+      ldsm_x4(smem_u32(Ws + (warp * 16 + (mi >> 1) * 8 + (lane & 7)) * HP + ks * 16 + (mi & 1) * 8),
+              bfr);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        mma16816(acc[mt][0], af[mt], bfr[0], bfr[1]);
+        mma16816(acc[mt][1], af[mt], bfr[2], bfr[3]);
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int row = mt * 16 + gid, col = warp * 16 + nt * 8 + tig * 2;
+        gpre[row * GP + col] = acc[mt][nt][0];
+        gpre[row * GP + col + 1] = acc[mt][nt][1];
+        gpre[(row + 8) * GP + col] = acc[mt][nt][2];
+        gpre[(row + 8) * GP + col + 1] = acc[mt][nt][3];
+      }
+    __syncthreads();
+    const int nbuf = (t + 1) & 1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = tid + 256 * q;
+      const int b = idx >> 4, j = (idx & 15) * 2;
+      if (b < BB) {
+        const int bb = b0 + b;
+        const size_t row = (size_t)bb * T1 + t;
+        const int col = 32 * r + j;
+        const float* xp = a.xproj + row * (4 * U) + col;
+        const float2 xi = *reinterpret_cast<const float2*>(xp);
+        const float2 xf = *reinterpret_cast<const float2*>(xp + U);
+        const float2 xg = *reinterpret_cast<const float2*>(xp + 2 * U);
+        const float2 xo = *reinterpret_cast<const float2*>(xp + 3 * U);
+        const float* gp = gpre + b * GP + j;
+        float hv[2], cv[2], gi[2], gf[2], gg[2], go[2];
+        const float xiv[2] = {xi.x, xi.y}, xfv[2] = {xf.x, xf.y}, xgv[2] = {xg.x, xg.y},
+                    xov[2] = {xo.x, xo.y};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          gi[e] = sigm(gp[e] + xiv[e]);
+          gf[e] = sigm(gp[32 + e] + xfv[e]);
+          gg[e] = tanhf(gp[64 + e] + xgv[e]);
+          go[e] = sigm(gp[96 + e] + xov[e]);
+          cv[e] = gf[e] * cst[b * 32 + j + e] + gi[e] * gg[e];
+          hv[e] = go[e] * tanhf(cv[e]);
+        }
+        *reinterpret_cast<float2*>(a.H + row * U + col) = make_float2(hv[0], hv[1]);
+        if (a.Hb)
+          *reinterpret_cast<uint32_t*>(a.Hb + row * U + col) = pack_bf16(hv[0], hv[1]);
+        if (a.C) *reinterpret_cast<float2*>(a.C + row * U + col) = make_float2(cv[0], cv[1]);
+        if (a.gates) {
+          float* gq = a.gates + row * (4 * U) + col;
+          *reinterpret_cast<float2*>(gq) = make_float2(gi[0], gi[1]);
+          *reinterpret_cast<float2*>(gq + U) = make_float2(gf[0], gf[1]);
+          *reinterpret_cast<float2*>(gq + 2 * U) = make_float2(gg[0], gg[1]);
+          *reinterpret_cast<float2*>(gq + 3 * U) = make_float2(go[0], go[1]);
+        }
+        if (t + 1 < T1) {
+          const bool dn = a.done[(size_t)bb * T1 + t + 1] != 0;
+          const float h0n = dn ? 0.f : hv[0], h1n = dn ? 0.f : hv[1];
+          cst[b * 32 + j] = dn ? 0.f : cv[0];
+          cst[b * 32 + j + 1] = dn ? 0.f : cv[1];
+          const uint32_t pv = pack_bf16(h0n, h1n);
+          if (a.Hprev) *reinterpret_cast<uint32_t*>(a.Hprev + (row + 1) * U + col) = pv;
+          const uint32_t local = smem_u32(hb + nbuf * 32 * HP + b * HP + col);
+#pragma unroll
+          for (int s = 0; s < LSTM_CLUSTER; ++s) st_cluster_u32(mapa_u32(local, s), pv);
+        } else if (a.hT) {
+          const int srow = a.state_rows ? a.state_rows[bb] : bb;
+          *reinterpret_cast<float2*>(a.hT + (size_t)srow * U + col) = make_float2(hv[0], hv[1]);
+          *reinterpret_cast<float2*>(a.cT + (size_t)srow * U + col) = make_float2(cv[0], cv[1]);
+        }
+      }
+    }
+    cluster_sync_all();
+  }
+}
+
+__global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
+    lstm_bwd_kernel(const LstmBwdArgs a) {
+  constexpr int U = LSTM_U;
+  extern __shared__ __align__(16) uint8_t sm[];
+  __nv_bfloat16* Ws = reinterpret_cast<__nv_bfloat16*>(sm);
+  __nv_bfloat16* dzs = Ws + 128 * HP;
+  float* red = reinterpret_cast<float*>(dzs + 32 * DP);   // [2][8][32][RP]
+  float* dcs = red + 2 * 8 * 32 * RP;                      // [32][32]
+  const int r = (int)cluster_rank();
+  const int b0 = (blockIdx.x / LSTM_CLUSTER) * LSTM_BB;
+  const int BB = min(LSTM_BB, a.B - b0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T1 = a.T1;
+
+  load_wh_slice(Ws, a.wh, r);
+  for (int i = tid; i < 32 * DP; i += 256) dzs[i] = __float2bfloat16_rn(0.f);
+  for (int i = tid; i < 32 * 32; i += 256) dcs[i] = 0.f;
+  __syncthreads();
+  cluster_sync_all();
+
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int t = T1 - 1; t >= 0; --t) {
+    const float* rin = red + ((t + 1) & 1) * 8 * 32 * RP;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + 256 * q;
+      const int b = idx >> 5, j = idx & 31;
+      if (b < BB) {
+        const int bb = b0 + b;
+        const size_t row = (size_t)bb * T1 + t;
+        const int col = 32 * r + j;
+        float dh = a.dH[row * U + col];
+        if (t + 1 < T1 && !a.done[(size_t)bb * T1 + t + 1]) {
+          float s = 0.f;
+#pragma unroll
+          for (int src = 0; src < LSTM_CLUSTER; ++src) s += rin[(src * 32 + b) * RP + j];
+          dh += s;
+        }
+        const float* gq = a.gates + row * (4 * U) + col;
+        const float gi = gq[0], gf = gq[U], gg = gq[2 * U], go = gq[3 * U];
+        const float c = a.C[row * U + col];
+        const bool dn = a.done[(size_t)bb * T1 + t] != 0;
+        const float cp = dn ? 0.f : (t > 0 ? a.C[(row - 1) * U + col] : a.c0[(size_t)bb * U + col]);
+        const float tc = tanhf(c);
+        const float dc = dcs[b * 32 + j] + dh * go * (1.f - tc * tc);
+        const float dzi = dc * gg * gi * (1.f - gi);
+        const float dzf = dc * cp * gf * (1.f - gf);
+        const float dzg = dc * gi * (1.f - gg * gg);
+        const float dzo = dh * tc * go * (1.f - go);
+        dcs[b * 32 + j] = dn ? 0.f : dc * gf;
+        __nv_bfloat16* dg = a.dG + row * (4 * U) + col;
+        const __nv_bfloat16 bi = __float2bfloat16_rn(dzi), bf = __float2bfloat16_rn(dzf),
+                            bg = __float2bfloat16_rn(dzg), bo = __float2bfloat16_rn(dzo);
+        dg[0] = bi;
+        dg[U] = bf;
+        dg[2 * U] = bg;
+        dg[3 * U] = bo;
+        dzs[b * DP + j] = bi;
+        dzs[b * DP + 32 + j] = bf;
+        dzs[b * DP + 64 + j] = bg;
+        dzs[b * DP + 96 + j] = bo;
+      }
+    }
+    __syncthreads();
+    if (t > 0) {
+      float acc[2][4][4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t af[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+          ldsm_x4(smem_u32(dzs + (mt * 16 + (lane & 15)) * DP + ks * 16 + (lane >> 4) * 8),
+                  af[mt]);
+        const int mi = lane >> 3;
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+          uint32_t bfr[4];
+          ldsm_x4_t(smem_u32(Ws + (ks * 16 + (mi & 1) * 8 + (lane & 7)) * HP + 32 * warp +
+                             np * 16 + (mi >> 1) * 8),
+                    bfr);
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            mma16816(acc[mt][2 * np], af[mt], bfr[0], bfr[1]);
+            mma16816(acc[mt][2 * np + 1], af[mt], bfr[2], bfr[3]);
+          }
+        }
+      }
+      // columns [32*warp, 32*warp+32) belong to CTA `warp`: slot r of its buffer t&1
+      const uint32_t base = smem_u32(red + ((t & 1) * 8 + r) * 32 * RP);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int row = mt * 16 + gid, j = nt * 8 + tig * 2;
+          st_cluster_f32x2(mapa_u32(base + (row * RP + j) * 4, warp), acc[mt][nt][0],
+                           acc[mt][nt][1]);
+          st_cluster_f32x2(mapa_u32(base + ((row + 8) * RP + j) * 4, warp), acc[mt][nt][2],
+                           acc[mt][nt][3]);
+        }
+    }
+    cluster_sync_all();
+  }
+}
+
+seed_status lstm_forward(const LstmFwdArgs& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       FWD_SMEM));
+    attr = true;
+  }
+  const int clusters = ceil_div(a.B, LSTM_BB);
+  lstm_fwd_kernel<<<clusters * LSTM_CLUSTER, 256, FWD_SMEM, st>>>(a);
+  return last_launch();
+}
+
+seed_status lstm_backward(const LstmBwdArgs& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       BWD_SMEM));
+    attr = true;
+  }
+  const int clusters = ceil_div(a.B, LSTM_BB);
+  lstm_bwd_kernel<<<clusters * LSTM_CLUSTER, 256, BWD_SMEM, st>>>(a);
+  return last_launch();
+}
+
+}  // namespace seed

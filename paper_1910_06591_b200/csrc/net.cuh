@@ -1,0 +1,66 @@
+// net.cuh — host-side plans: parameter layout (include/seed.h), the bf16
+// operand image ("lowp"), and the learner / inference workspace layouts.
+#pragma once
+#include <string.h>
+#include "common.cuh"
+
+namespace seed {
+
+struct PTensor {
+  char name[32];
+  int ndim;
+  int64_t shape[4];
+  int64_t off, n;
+};
+
+// One bf16 operand image inside params_lowp.
+enum { IMG_COPY_PAD = 0, IMG_CONV_DGRAD = 1 };
+struct LowpImg {
+  int kind;
+  int64_t src;          // fp32 element offset of the source tensor
+  int64_t dst;          // bf16 element offset in params_lowp
+  int rows, cols, ld;   // COPY_PAD: dst[r][c] (ld) = src[r][c] (cols) for c < cols, else 0
+  int d0, d1, d2, d3;   // CONV_DGRAD: src [d0=CO][d1=KH][d2=KW][d3=CI] -> dst [CI][KH][KW][CO]
+};
+
+struct NetPlan {
+  int kind, H, W, C, A, U, D;
+  int nt;
+  PTensor t[64];
+  int64_t P;
+  // shallow-net geometry
+  int oh1, ow1, oh2, ow2, fc_in, Kx, Kxp;
+  // tensor indices
+  int i_conv1w, i_conv1b, i_conv2w, i_conv2b, i_fcw, i_fcb, i_wx, i_wh, i_lb, i_hw, i_hb;
+  int i_m0w, i_m0b, i_m1w, i_m1b;
+  // lowp images
+  int nimg;
+  LowpImg img[8];
+  int64_t lowp_elems;
+  int64_t im_conv1, im_conv2, im_conv2dg, im_fc, im_wx, im_wh;  // bf16 offsets
+};
+
+seed_status make_net_plan(const seed_net_spec* s, NetPlan* p);
+bool learner_supported(const NetPlan& p);
+
+// Learner workspace: byte offsets (256-aligned) of every buffer.
+struct LearnerWs {
+  int T, B, T1, F;
+  size_t total;
+  // common
+  size_t logits, values, vs, pg, dlogits, dvalues, loss_part, flag, norm_part, step_in, splitk,
+      colsum_part, dH;
+  size_t splitk_bytes;
+  // shallow
+  size_t act1, act2, X, xproj, H, Hprev, gates, Cst, dG, dfc, dY2, dY1;
+  // mlp
+  size_t h1, h2, dh1, dh2;
+};
+constexpr int NORM_BLOCKS = 296;
+constexpr int COLSUM_BLOCKS = 148;
+
+seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w);
+int pick_splits(int M, int N, int BN, int K);
+seed_status refresh_lowp(const NetPlan& p, const float* params, void* lowp, cudaStream_t st);
+
+}  // namespace seed

@@ -469,3 +469,24 @@ def test_unroll_accounting_S442():
     assert [s["step"] for s in st.steps[(0, 0)]["slots"]] == [1, 2, 3, 4, 5]
     assert [s["step"] for s in st.steps[(0, 1)]["slots"]] == [5]
     assert st.steps[(0, 1)]["h0"][0] == 4        # state before step 5 (C19)
+
+
+# ------------------------------------------------------------------ bf16 emulation (C26)
+def test_bf16_round_matches_torch_bfloat16():
+    g = seedgen.rng(12)
+    x = np.concatenate([g.standard_normal(10000) * 10.0 ** g.integers(-30, 30, 10000),
+                        [0.0, -0.0, 1.0, 1.00390625, 1.01171875, 65504.0, 3.0e38]])
+    ref = torch.tensor(x.astype(np.float32)).to(torch.bfloat16).double().numpy()
+    np.testing.assert_array_equal(O.bf16_round(x), ref)
+
+
+def test_emulated_oracle_stays_close_to_exact():
+    """The bf16-emulated forward differs from the exact fp64 definition only by
+    bf16 rounding (a few 1e-3 relative on the outputs)."""
+    spec = O.spec_c2()
+    batch = seedgen.learner_batch((84, 84, 4), 18, 2, 3, seed=3, done_p=0.2)
+    P = O.unflatten(spec, seedgen.glorot_params(O.param_layout(spec), seed=4, bias_std=0.1))
+    le, ve, _ = O.network_forward(spec, P, batch, emu=True)
+    lx, vx, _ = O.network_forward(spec, P, batch, emu=False)
+    assert np.linalg.norm(le - lx) / np.linalg.norm(lx) < 2e-2
+    assert np.linalg.norm(ve - vx) / np.linalg.norm(vx) < 2e-2
