@@ -278,7 +278,8 @@ seed_status seed_assemble_batch(const seed_unroll_store* store, int obs_bytes, i
  * seed_debug_gemm: D[M][N] (fp32, row-major) = A . B^T with A [M][K], B [N][K]
  * bf16 row-major (a_t / b_t != 0: A given as [K][M] / B as [K][N]), on the
  * tcgen05 engine the learner uses.  Requires K % 8 == 0, M % 8 == 0 and
- * N % 8 == 0.  Returns the kernel's BN tile in *bn_out (host, nullable).
+ * N % 8 == 0.  splits < 0 selects the register-staged producer with |splits|
+ * K splits (default: the cp.async producer).
  * ======================================================================== */
 seed_status seed_debug_gemm(int M, int N, int K, const void* A, int a_t, const void* B,
                             int b_t, float* D, int bn, int splits, void* workspace,

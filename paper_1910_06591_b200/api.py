@@ -63,8 +63,8 @@ def debug_gemm(A, B, a_t=False, b_t=False, bn=64, splits=1, out=None, stream=Non
     M, K = (A.shape[1], A.shape[0]) if a_t else A.shape
     N = B.shape[1] if b_t else B.shape[0]
     D = out if out is not None else torch.empty(M, N, device=A.device, dtype=torch.float32)
-    ws = torch.empty(max(splits, 1) * M * N, device=A.device, dtype=torch.float32) \
-        if splits > 1 else None
+    ws = torch.empty(max(abs(splits), 1) * M * N, device=A.device, dtype=torch.float32) \
+        if abs(splits) > 1 else None
     st = L.load().seed_debug_gemm(M, N, K, _ptr(A), int(a_t), _ptr(B), int(b_t), _ptr(D), bn,
                                   splits, _ptr(ws), _stream(stream))
     L.check(st, "seed_debug_gemm")

@@ -34,6 +34,29 @@ static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Division by a runtime-constant divisor via multiply-high + shift (dividend
+// < 2^31): the implicit-GEMM producers decompose row indices per 16-byte chunk.
+struct FastDiv {
+  uint32_t d = 1, mul = 0, shr = 0;
+  FastDiv() = default;
+  __host__ explicit FastDiv(uint32_t div) : d(div) {
+    if (div > 1) {
+      uint32_t l = 0;
+      while ((1u << l) < div) ++l;                 // ceil(log2(div))
+      const uint32_t p = 31 + l;
+      mul = (uint32_t)(((1ull << p) + div - 1) / div);
+      shr = p - 32;
+    }
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return d == 1 ? n : (__umulhi(n, mul) >> shr);
+  }
+  __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
+    q = div(n);
+    r = n - q * d;
+  }
+};
+
 // ---------------------------------------------------------------- smem / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -122,16 +145,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// UMMA shared-memory matrix descriptor, SWIZZLE_NONE ("interleaved" core
-// matrices of 8 rows x 16 bytes).  lbo = byte stride between core matrices
-// adjacent in K, sbo = byte stride between core matrices adjacent in M/N.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory matrix descriptor (sm_100, version 1): start address,
+// leading / stride byte offsets (>>4), base offset 0, layout type in bits
+// 61-63 (0 = SWIZZLE_NONE, 2 = SWIZZLE_128B).  No-swizzle: lbo = K-direction
+// core-matrix stride, sbo = M/N-direction stride.  128B-swizzle K-major: sbo =
+// 8-row atom stride (lbo unused); MN-major: lbo = MN-atom stride, sbo = 8-k-row
+// stride.  Swizzled atoms must be 1024-byte aligned.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout = 0) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100)
-  return d;                // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7) << 61;
+  return d;
 }
 
 // Instruction descriptor for kind::f16 with bf16 A/B and fp32 D.

@@ -5,9 +5,11 @@
 
 namespace seed {
 
-template <bool AT, bool BT>
+template <bool AT, bool BT, bool ASYNC_MODE>
 struct DebugGemm {
   static constexpr bool A_MN = AT, B_MN = BT;
+  static constexpr bool ASYNC = ASYNC_MODE;
+  const void* dummy = k_ones_chunk;
   int M, N, K, kb_per_split;
   const __nv_bfloat16* A;
   const __nv_bfloat16* B;
@@ -18,13 +20,27 @@ struct DebugGemm {
   __device__ uint4 load_b(int i, int j) const {
     return BT ? ld16(B + (size_t)i * N + j) : ld16(B + (size_t)i * K + j);
   }
+  __device__ const void* ptr_a(int i, int j) const {
+    return AT ? A + (size_t)i * M + j : A + (size_t)i * K + j;
+  }
+  __device__ const void* ptr_b(int i, int j) const {
+    return BT ? B + (size_t)i * N + j : B + (size_t)i * K + j;
+  }
   __device__ void store(int m, int n, float v) const { D[(size_t)m * N + n] = v; }
 };
 
 template <int BN, bool AT, bool BT>
 static seed_status run_dbg(int M, int N, int K, const void* A, const void* B, float* D,
                            int splits, void* ws, cudaStream_t st) {
-  DebugGemm<AT, BT> p;
+  if (splits < 0) {  // register-staged producer
+    DebugGemm<AT, BT, false> p;
+    p.M = M; p.N = N; p.K = K;
+    p.A = (const __nv_bfloat16*)A;
+    p.B = (const __nv_bfloat16*)B;
+    p.D = D;
+    return launch_gemm<BN>(p, -splits, st, (float*)ws);
+  }
+  DebugGemm<AT, BT, true> p;
   p.M = M; p.N = N; p.K = K;
   p.A = (const __nv_bfloat16*)A;
   p.B = (const __nv_bfloat16*)B;

@@ -4,17 +4,20 @@
 //
 //   D[m][n] = sum_k A(m,k) * B(n,k)          bf16 x bf16 -> fp32 (TMEM)
 //
-// One CTA = 128 threads computes a 128 x BN tile (tcgen05.mma.cta_group::1,
-// M=128, N=BN, K=16 per instruction) over a K range (split-K over grid.z).
-// All four warps act as the operand producer: each 16-byte chunk of the
-// 128x64 A tile and BNx64 B tile is fetched through the Problem's loader
-// (implicit-GEMM gathers, uint8 -> bf16 conversion, transposed sources) and
-// stored into the UMMA no-swizzle core-matrix layout in shared memory; a
-// single elected thread issues the MMAs and commits them to a per-stage
-// mbarrier that releases the stage; the fp32 accumulator lives in TMEM and
-// the epilogue (bias, ReLU, masks, bf16 packing, split-K partials) reads it
-// back with tcgen05.ld.  Loads for k-block i+1 are in flight while the MMAs
-// of k-block i run.
+// Persistent, warp-specialized (one CTA per SM, 288 threads):
+//   warps 0-3  producers: fill a ring of S shared-memory stages with the
+//              128x64 A tile and BNx64 B tile of each k-block through the
+//              Problem's loaders (implicit-GEMM gathers, transposed sources):
+//              cp.async (LDGSTS) chunks that arrive on the stage's full
+//              mbarrier when they land, or register-staged chunks (uint8 ->
+//              bf16 conversion) followed by a proxy fence and an arrive;
+//   warp 4     MMA issuer: one thread issues tcgen05.mma (cta_group::1,
+//              M=128, N=BN, K=16, bf16 -> fp32) into one of two TMEM
+//              accumulators and commits each stage back to the producers;
+//   warps 5-8  epilogue: tcgen05.ld of the finished accumulator (bias, ReLU,
+//              masks, bf16 packing or split-K partials), overlapped with the
+//              MMAs of the next tile in the other accumulator.
+// Work items (m tile, n tile, K split) are strided over the CTAs.
 //
 // Problem concept (all __device__):
 //   static constexpr bool A_MN, B_MN;   // false: K-major source, true: MN-major
@@ -29,162 +32,321 @@
 // sources need K % 8 == 0, MN-major sources need M (or N) % 8 == 0.
 #pragma once
 #include <algorithm>
+#include <stdio.h>
+#include <stdlib.h>
+#include <type_traits>
 #include "common.cuh"
 
 namespace seed {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 128;
 
-template <int BN>
-struct GemmCfg {
-  static constexpr int STAGES = (BN >= 128) ? 3 : 4;
-  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr int B_BYTES = BN * GEMM_BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 128;
-  static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-  static constexpr int B_CHUNKS = BN * GEMM_BK / 8 / GEMM_THREADS;  // per thread (>= 1 for BN>=16)
+// Shared-memory image of one R x 64 (bf16) operand tile in a canonical UMMA
+// layout.  Chunks (16 B) are assigned so that consecutive lanes read
+// consecutive 16-byte pieces of one source row (coalesced) and the 8 lanes of
+// a shared-memory store phase hit distinct bank groups.
+//  * K-major (source row = MN index, contiguous along K): 128-byte swizzle —
+//    row r at r*128, chunk kc stored at ((kc ^ (r & 7)) * 16); SBO = 1024
+//    (8-row atom stride); per-MMA K advance = 32 bytes.
+//  * MN-major, R % 64 == 0 (source row = k, contiguous along MN): 128-byte
+//    swizzle — atom = 64 MN x 8 k (1024 B), k-row j of an atom at j*128,
+//    chunk mc%8 at ((mc%8 ^ k%8) * 16); LBO = 1024 (MN-atom stride),
+//    SBO = (R/64)*1024 (8-k-row stride); per-MMA K advance = 2*SBO.
+//  * MN-major, R < 64: no swizzle, core matrices (8 k x 16 B), SBO = 144
+//    (padded MN-core stride), LBO = 144 R/8 (K-core stride).
+template <int R, bool MN>
+struct TileMap {
+  static constexpr bool SWZ = !MN || (R % 64 == 0);
+  static constexpr uint32_t LAYOUT = SWZ ? 2u : 0u;   // SWIZZLE_128B / SWIZZLE_NONE
+  static constexpr int LBO = !MN ? 16 : (SWZ ? 1024 : (R / 8) * 144);
+  static constexpr int SBO = !MN ? 1024 : (SWZ ? (R / 64) * 1024 : 144);
+  static constexpr int KSTEP = !MN ? 32 : (SWZ ? 2 * SBO : 2 * LBO);
+  static constexpr int BYTES = !MN ? R * 128 : (SWZ ? 8 * SBO : 8 * LBO);
+  static constexpr int CHUNKS = R * GEMM_BK / 8;
+  __device__ __forceinline__ static void chunk(int c, int r0, int k0, int& i, int& j, int& off,
+                                               bool& in_r, bool& in_k, int Rlim, int Klim) {
+    if (!MN) {
+      const int kc = c & 7, r = c >> 3;
+      i = r0 + r; j = k0 + kc * 8;
+      off = r * 128 + ((kc ^ (r & 7)) << 4);
+      in_r = i < Rlim; in_k = j < Klim;
+    } else if (SWZ) {
+      const int mc = c % (R / 8), k = c / (R / 8);
+      i = k0 + k; j = r0 + mc * 8;
+      off = (k >> 3) * SBO + (mc >> 3) * LBO + (k & 7) * 128 + (((mc & 7) ^ (k & 7)) << 4);
+      in_r = j < Rlim; in_k = i < Klim;
+    } else {
+      const int mc = c % (R / 8), k = c / (R / 8);
+      i = k0 + k; j = r0 + mc * 8;
+      off = (k >> 3) * LBO + mc * SBO + (k & 7) * 16;
+      in_r = j < Rlim; in_k = i < Klim;
+    }
+  }
+  __device__ __forceinline__ static uint64_t desc(uint32_t base, int kk) {
+    return umma_desc(base + kk * KSTEP, LBO, SBO, LAYOUT);
+  }
 };
 
+constexpr int GEMM_PRODUCER_WARPS = 8;
+constexpr int GEMM_PRODUCERS = 32 * GEMM_PRODUCER_WARPS;   // warps 0-7
+constexpr int GEMM_MMA_WARP = GEMM_PRODUCER_WARPS;           // warp 8
+constexpr int GEMM_THREADS = GEMM_PRODUCERS + 32 + 128;     // + MMA warp + 4 epilogue warps
+
+template <int BN, bool A_MN, bool B_MN>
+struct GemmCfg {
+  using TA = TileMap<GEMM_BM, A_MN>;
+  using TB = TileMap<BN, B_MN>;
+  static constexpr int A_BYTES = (TA::BYTES + 1023) / 1024 * 1024;   // swizzle atoms 1024-aligned
+  static constexpr int B_BYTES = (TB::BYTES + 1023) / 1024 * 1024;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_FIT = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 256;
+  static constexpr uint32_t ACC_COLS = BN;   // two accumulators of BN columns
+  static constexpr uint32_t TMEM_COLS =
+      2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr int A_CHUNKS = (TA::CHUNKS + GEMM_PRODUCERS - 1) / GEMM_PRODUCERS;
+  static constexpr int B_CHUNKS = (TB::CHUNKS + GEMM_PRODUCERS - 1) / GEMM_PRODUCERS;
+  static_assert(STAGES >= 2, "stage ring");
+};
+
+template <class Prob, class = void>
+struct IsAsync : std::false_type {};
+template <class Prob>
+struct IsAsync<Prob, decltype((void)Prob::ASYNC)> : std::integral_constant<bool, Prob::ASYNC> {};
+
+template <class Prob, class = void>
+struct HasStore16 : std::false_type {};
+template <class Prob>
+struct HasStore16<Prob, decltype((void)Prob::VEC_STORE)> : std::integral_constant<bool, Prob::VEC_STORE> {};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_zero16(uint32_t dst) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0) : "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Epilogue of one 128 x BN accumulator: epilogue warp `q` (0..3) owns TMEM
+// lanes / tile rows [32q, 32q+32).
 template <int BN, class Prob>
-__global__ void __launch_bounds__(GEMM_THREADS) gemm_tc_kernel(const Prob p, float* __restrict__ part) {
-  using Cfg = GemmCfg<BN>;
-  constexpr int BM = GEMM_BM, BK = GEMM_BK, S = Cfg::STAGES;
-  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+__device__ __forceinline__ void gemm_epilogue(const Prob& p, float* __restrict__ part, int splits,
+                                              int z, int m0, int n0, bool have, uint32_t tmem,
+                                              int q, int lane) {
+  const int m = m0 + q * 32 + lane;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 16) {
+    float v[16];
+    if (have) {
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    }
+    const int n = n0 + c;
+    if (m < p.M && n < p.N) {
+      if (splits > 1) {
+        float* dst = part + ((size_t)z * p.M + m) * p.N + n;
+        if (n + 16 <= p.N) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (n + i < p.N) dst[i] = v[i];
+        }
+      } else {
+        bool done_vec = false;
+        if constexpr (HasStore16<Prob>::value) {
+          if (n + 16 <= p.N) {
+            p.store16(m, n, v);
+            done_vec = true;
+          }
+        }
+        if (!done_vec) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (n + i < p.N) p.store(m, n + i, v[i]);
+        }
+      }
+    }
+  }
+}
+
+template <int BN, class Prob>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, float* __restrict__ part,
+                                                                  int splits) {
+  using Cfg = GemmCfg<BN, Prob::A_MN, Prob::B_MN>;
+  using TA = typename Cfg::TA;
+  using TB = typename Cfg::TB;
+  constexpr int BK = GEMM_BK, S = Cfg::STAGES;
+  constexpr bool ASYNC = IsAsync<Prob>::value;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
-  uint64_t* done = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int mt = (p.M + GEMM_BM - 1) / GEMM_BM, nt = (p.N + BN - 1) / BN;
+  const int nitems = mt * nt * splits;
   const int nkb_total = (p.K + BK - 1) / BK;
-  const int kb_begin = blockIdx.z * p.kb_per_split;
-  const int kb_end = min(nkb_total, kb_begin + p.kb_per_split);
-  const int nkb = max(0, kb_end - kb_begin);
 
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&empty[s], 1);
-    mbar_init(done, 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], GEMM_PRODUCERS);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == GEMM_MMA_WARP) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, Prob::A_MN, Prob::B_MN);
 
-  uint4 ra[8];
-  uint4 rb[Cfg::B_CHUNKS];
-  const uint4 zero4 = make_uint4(0, 0, 0, 0);
-
-  auto load_stage = [&](int kb) {
-    const int k0 = kb * BK;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = j * GEMM_THREADS + tid;
-      if (!Prob::A_MN) {
-        const int m = m0 + (c & 127), k = k0 + (c >> 7) * 8;
-        ra[j] = (m < p.M && k < p.K) ? p.load_a(m, k) : zero4;
-      } else {
-        const int kl = c & 7, mc = (c >> 3) & 15, kh = c >> 7;
-        const int k = k0 + kh * 8 + kl, m = m0 + mc * 8;
-        ra[j] = (m < p.M && k < p.K) ? p.load_a(k, m) : zero4;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < Cfg::B_CHUNKS; ++j) {
-      const int c = j * GEMM_THREADS + tid;
-      if (!Prob::B_MN) {
-        const int n = n0 + (c % BN), k = k0 + (c / BN) * 8;
-        rb[j] = (n < p.N && k < p.K) ? p.load_b(n, k) : zero4;
-      } else {
-        const int kl = c & 7, rest = c >> 3;
-        const int nc = rest % (BN / 8), kh = rest / (BN / 8);
-        const int k = k0 + kh * 8 + kl, n = n0 + nc * 8;
-        rb[j] = (n < p.N && k < p.K) ? p.load_b(k, n) : zero4;
-      }
-    }
-  };
-  auto store_stage = [&](int s) {
-    uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
-    uint8_t* sb = sa + Cfg::A_BYTES;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = j * GEMM_THREADS + tid;
-      int off;
-      if (!Prob::A_MN) off = (c >> 7) * (BM * 16) + (c & 127) * 16;
-      else off = (c >> 7) * (BM * 16) + ((c >> 3) & 15) * 128 + (c & 7) * 16;
-      *reinterpret_cast<uint4*>(sa + off) = ra[j];
-    }
-#pragma unroll
-    for (int j = 0; j < Cfg::B_CHUNKS; ++j) {
-      const int c = j * GEMM_THREADS + tid;
-      int off;
-      if (!Prob::B_MN) off = (c / BN) * (BN * 16) + (c % BN) * 16;
-      else {
-        const int rest = c >> 3;
-        off = (rest / (BN / 8)) * (BN * 16) + (rest % (BN / 8)) * 128 + (c & 7) * 16;
-      }
-      *reinterpret_cast<uint4*>(sb + off) = rb[j];
-    }
+  auto decode = [&](int w, int& m0, int& n0, int& kb0, int& nkb, int& z) {
+    z = w % splits;
+    const int t = w / splits;
+    m0 = (t % mt) * GEMM_BM;
+    n0 = (t / mt) * BN;
+    kb0 = z * p.kb_per_split;
+    nkb = max(0, min(nkb_total, kb0 + p.kb_per_split) - kb0);
   };
 
-  if (nkb > 0) load_stage(kb_begin);
-  for (int i = 0; i < nkb; ++i) {
-    const int s = i % S;
-    if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-    store_stage(s);
-    fence_proxy_async_smem();
-    if (i + 1 < nkb) load_stage(kb_begin + i + 1);
-    __syncthreads();
-    if (tid == 0) {
+  if (warp < GEMM_PRODUCER_WARPS) {
+    // ------------------------------------------------------------ producers
+    const uint32_t smem0 = smem_u32(smem);
+    int g = 0;
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+      int m0, n0, kb0, nkb, z;
+      decode(w, m0, n0, kb0, nkb, z);
+      for (int i = 0; i < nkb; ++i, ++g) {
+        const int s = g % S;
+        if (g >= S) mbar_wait(&empty[s], ((g / S) - 1) & 1);
+        const int k0 = (kb0 + i) * BK;
+        const uint32_t sa = smem0 + s * Cfg::STAGE_BYTES, sb = sa + Cfg::A_BYTES;
+        if constexpr (ASYNC) {
+          // zero chunks (padding, transposed-conv zero taps) are plain shared
+          // stores: a zero-fill cp.async would still send a request to memory
+          bool zeroed = false;
+#pragma unroll
+          for (int j = 0; j < Cfg::A_CHUNKS; ++j) {
+            int a, b, off;
+            bool ir, ik;
+            TA::chunk(j * GEMM_PRODUCERS + tid, m0, k0, a, b, off, ir, ik, p.M, p.K);
+            const void* src = (ir && ik) ? p.ptr_a(a, b) : nullptr;
+            if (src) cp_async16(sa + off, src, true);
+            else { st_shared_zero16(sa + off); zeroed = true; }
+          }
+#pragma unroll
+          for (int j = 0; j < Cfg::B_CHUNKS; ++j) {
+            const int cb = j * GEMM_PRODUCERS + tid;
+            if (TB::CHUNKS % GEMM_PRODUCERS != 0 && cb >= TB::CHUNKS) continue;
+            int a, b, off;
+            bool ir, ik;
+            TB::chunk(cb, n0, k0, a, b, off, ir, ik, p.N, p.K);
+            const void* src = (ir && ik) ? p.ptr_b(a, b) : nullptr;
+            if (src) cp_async16(sb + off, src, true);
+            else { st_shared_zero16(sb + off); zeroed = true; }
+          }
+          if (zeroed) fence_proxy_async_smem();
+          cp_async_arrive(&full[s]);
+        } else {
+          uint4 ra[Cfg::A_CHUNKS], rb[Cfg::B_CHUNKS];
+          int oa[Cfg::A_CHUNKS], ob[Cfg::B_CHUNKS];
+          const uint4 zero4 = make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int j = 0; j < Cfg::A_CHUNKS; ++j) {
+            int a, b;
+            bool ir, ik;
+            TA::chunk(j * GEMM_PRODUCERS + tid, m0, k0, a, b, oa[j], ir, ik, p.M, p.K);
+            ra[j] = (ir && ik) ? p.load_a(a, b) : zero4;
+          }
+#pragma unroll
+          for (int j = 0; j < Cfg::B_CHUNKS; ++j) {
+            const int cb = j * GEMM_PRODUCERS + tid;
+            int a, b;
+            bool ir, ik;
+            TB::chunk(cb < TB::CHUNKS ? cb : 0, n0, k0, a, b, ob[j], ir, ik, p.N, p.K);
+            rb[j] = (cb < TB::CHUNKS && ir && ik) ? p.load_b(a, b) : zero4;
+            if (cb >= TB::CHUNKS) ob[j] = -1;
+          }
+          uint8_t* gsa = smem + s * Cfg::STAGE_BYTES;
+#pragma unroll
+          for (int j = 0; j < Cfg::A_CHUNKS; ++j) *reinterpret_cast<uint4*>(gsa + oa[j]) = ra[j];
+#pragma unroll
+          for (int j = 0; j < Cfg::B_CHUNKS; ++j)
+            if (ob[j] >= 0) *reinterpret_cast<uint4*>(gsa + Cfg::A_BYTES + ob[j]) = rb[j];
+          fence_proxy_async_smem();
+          mbar_arrive(&full[s]);
+        }
+      }
+    }
+  } else if (warp == GEMM_MMA_WARP) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(GEMM_BM, BN, Prob::A_MN, Prob::B_MN);
+      const uint32_t smem0 = smem_u32(smem);
+      int g = 0, it = 0;
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+        int m0, n0, kb0, nkb, z;
+        decode(w, m0, n0, kb0, nkb, z);
+        const int acc = it & 1;
+        if (it >= 2) mbar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * Cfg::ACC_COLS;
+        for (int i = 0; i < nkb; ++i, ++g) {
+          const int s = g % S;
+          mbar_wait(&full[s], (g / S) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem0 + s * Cfg::STAGE_BYTES;
+          const uint32_t b_base = a_base + Cfg::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = TA::desc(a_base, kk);
+            const uint64_t bd = TB::desc(b_base, kk);
+            tc_mma_bf16(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);
+        }
+        if (nkb > 0) tc_commit(&tfull[acc]);
+        else mbar_arrive(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;   // TMEM lane quarter of this warp (warps 9..12 -> 1,2,3,0)
+    int it = 0;
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+      int m0, n0, kb0, nkb, z;
+      decode(w, m0, n0, kb0, nkb, z);
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const uint32_t a_base = smem_u32(smem + s * Cfg::STAGE_BYTES);
-      const uint32_t b_base = a_base + Cfg::A_BYTES;
-#pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk) {
-        const uint64_t ad = umma_desc(a_base + kk * 2 * (BM * 16), BM * 16, 128);
-        const uint64_t bd = umma_desc(b_base + kk * 2 * (BN * 16), BN * 16, 128);
-        tc_mma_bf16(tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-      }
-      tc_commit(&empty[s]);
-    }
-  }
-  if (nkb > 0) {
-    if (tid == 0) tc_commit(done);
-    mbar_wait(done, 0);
-    tc_fence_after();
-  }
-  const int m = m0 + warp * 32 + lane;
-#pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    float v[16];
-    if (nkb > 0) {
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = 0.f;
-    }
-    if (m < p.M && n0 + c < p.N) {
-      if (gridDim.z > 1) {
-        float* dst = part + ((size_t)blockIdx.z * p.M + m) * p.N + n0 + c;
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (n0 + c + q < p.N) dst[q] = v[q];
-      } else {
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (n0 + c + q < p.N) p.store(m, n0 + c + q, v[q]);
-      }
+      gemm_epilogue<BN>(p, part, splits, z, m0, n0, nkb > 0, tmem + acc * Cfg::ACC_COLS, q, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, Cfg::TMEM_COLS);
+  if (warp == GEMM_MMA_WARP) tmem_dealloc(tmem, Cfg::TMEM_COLS);
 }
 
 template <class Prob>
@@ -198,27 +360,31 @@ __global__ void splitk_finish(const Prob p, const float* __restrict__ part, int 
   }
 }
 
-// Host launcher.  splits > 1 runs split-K over grid.z into `part`
-// ([splits][M][N] fp32, caller workspace) followed by splitk_finish.
+// Host launcher.  splits > 1 runs split-K into `part` ([splits][M][N] fp32,
+// caller workspace) followed by the fixed-order splitk_finish reduction.
 template <int BN, class Prob>
 seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullptr) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, Prob::A_MN, Prob::B_MN>;
   if (p.M <= 0 || p.N <= 0) return SEED_OK;
   const int nkb = (p.K + GEMM_BK - 1) / GEMM_BK;
   if (splits < 1) splits = 1;
   if (splits > nkb) splits = nkb > 0 ? nkb : 1;
   p.kb_per_split = (nkb + splits - 1) / splits;
   splits = nkb > 0 ? (nkb + p.kb_per_split - 1) / p.kb_per_split : 1;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static int sms = 0;
+  if (!sms) {
     if (cudaFuncSetAttribute(gemm_tc_kernel<BN, Prob>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::SMEM) != cudaSuccess)
       return SEED_E_CUDA;
-    attr_done = true;
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms = n;
   }
   if (splits > 1 && !part) return SEED_E_WORKSPACE;
-  dim3 grid(ceil_div(p.M, GEMM_BM), ceil_div(p.N, BN), splits);
-  gemm_tc_kernel<BN, Prob><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(p, part);
+  const int items = ceil_div(p.M, GEMM_BM) * ceil_div(p.N, BN) * splits;
+  const int grid = std::min(items, sms);
+  gemm_tc_kernel<BN, Prob><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(p, part, splits);
   if (splits > 1) {
     const size_t MN = (size_t)p.M * p.N;
     const int blocks = (int)std::min<size_t>((MN + 255) / 256, 148 * 8);
@@ -237,6 +403,11 @@ inline int gemm_effective_splits(int K, int splits) {
 }
 
 // ---------------------------------------------------------------- common loaders
+// A 16-byte bf16 chunk [1, 0, 0, 0, 0, 0, 0, 0]: the all-ones column that turns a
+// weight-gradient GEMM's extra output column into the bias gradient; also a
+// valid dummy source address for zero-filled cp.async chunks.
+__device__ __align__(16) const uint32_t k_ones_chunk[4] = {0x3F80u, 0u, 0u, 0u};
+
 __device__ __forceinline__ uint4 ld16(const void* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }

@@ -35,32 +35,86 @@ __device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
 
 struct Geo {
   int H, W, C, oh1, ow1, oh2, ow2, fc_in, Kx, Kxp;
+  FastDiv hw1, w1, hw2, w2;   // oh1*ow1, ow1, oh2*ow2, ow2
 };
+// row of conv1 output (f, oy, ox) / conv2 output
+__device__ __forceinline__ void split_row(const FastDiv& hw, const FastDiv& w, int m, uint32_t& f,
+                                          uint32_t& oy, uint32_t& ox) {
+  uint32_t p;
+  hw.divmod((uint32_t)m, f, p);
+  w.divmod(p, oy, ox);
+}
 
-// conv1: A(m = (f, oy, ox), k = (ky, kx, c)) = obs[f][4oy+ky][4ox+kx][c] (uint8)
+// 16 fp32 -> 16 bf16 (two 16-byte stores)
+__device__ __forceinline__ void st_bf16x16(bf16* dst, const float (&v)[16]) {
+  uint4 a, b;
+  a.x = pack_bf16(v[0], v[1]); a.y = pack_bf16(v[2], v[3]);
+  a.z = pack_bf16(v[4], v[5]); a.w = pack_bf16(v[6], v[7]);
+  b.x = pack_bf16(v[8], v[9]); b.y = pack_bf16(v[10], v[11]);
+  b.z = pack_bf16(v[12], v[13]); b.w = pack_bf16(v[14], v[15]);
+  reinterpret_cast<uint4*>(dst)[0] = a;
+  reinterpret_cast<uint4*>(dst)[1] = b;
+}
+// mask v[q] by (src[q] > 0) for 16 bf16 values of a ReLU output
+__device__ __forceinline__ void relu_mask16(const bf16* src, float (&v)[16]) {
+  const uint4 a = reinterpret_cast<const uint4*>(src)[0];
+  const uint4 b = reinterpret_cast<const uint4*>(src)[1];
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (!(bf16_lo(w[q]) > 0.f)) v[2 * q] = 0.f;
+    if (!(bf16_hi(w[q]) > 0.f)) v[2 * q + 1] = 0.f;
+  }
+}
+
+
+// obs (uint8) -> bf16 (exact integers 0..255; the 1/255 scale is applied in the
+// conv1 epilogue / weight gradient), 16 values per thread.
+__global__ void obs_to_bf16_kernel(const uint8_t* __restrict__ obs, bf16* __restrict__ out,
+                                   int64_t n16) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(obs) + i);
+    uint4* o = reinterpret_cast<uint4*>(out) + 2 * i;
+    o[0] = u8x8_to_bf16(make_uint2(v.x, v.y));
+    o[1] = u8x8_to_bf16(make_uint2(v.z, v.w));
+  }
+}
+
+// conv1: A(m = (f, oy, ox), k = (ky, kx, c)) = obs[f][4oy+ky][4ox+kx][c]
+// (8 consecutive k = 2 pixels x 4 channels = 16 contiguous bytes of obs_bf16)
 struct Conv1Fwd {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = false;
   int M, N, K, kb_per_split;
   Geo g;
-  const uint8_t* obs;
+  const bf16* obs;
   const bf16* w;
   const float* bias;
   bf16* out;
-  __device__ uint4 load_a(int m, int k) const {
-    const int hw = g.oh1 * g.ow1;
-    const int f = m / hw, p = m % hw, oy = p / g.ow1, ox = p % g.ow1;
-    const int ky = k / (8 * g.C), kx = (k % (8 * g.C)) / g.C;
-    const uint8_t* src = obs + (((size_t)f * g.H + oy * 4 + ky) * g.W + ox * 4 + kx) * g.C;
-    return u8x8_to_bf16(__ldg(reinterpret_cast<const uint2*>(src)));
+  __device__ const void* ptr_a(int m, int k) const {
+    uint32_t f, oy, ox;
+    split_row(g.hw1, g.w1, m, f, oy, ox);
+    const int ky = k >> 5, kx = (k & 31) >> 2;   // k = (ky*8 + kx)*4 + c, C == 4
+    return obs + (((size_t)f * g.H + oy * 4 + ky) * g.W + ox * 4 + kx) * 4;
   }
-  __device__ uint4 load_b(int n, int k) const { return ld16(w + (size_t)n * K + k); }
+  __device__ const void* ptr_b(int n, int k) const { return w + (size_t)n * K + k; }
   __device__ void store(int m, int n, float v) const {
     out[(size_t)m * 16 + n] = to_bf(fmaxf(v * (1.f / 255.f) + bias[n], 0.f));
+  }
+  static constexpr bool VEC_STORE = true;
+  __device__ void store16(int m, int n0, float (&v)[16]) const {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = fmaxf(v[q] * (1.f / 255.f) + bias[n0 + q], 0.f);
+    st_bf16x16(out + (size_t)m * 16 + n0, v);
   }
 };
 
 // conv2: A(m = (f, oy, ox), k = (ky, kx, c)) = act1[f][2oy+ky][2ox+kx][c]
 struct Conv2Fwd {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = false;
   int M, N, K, kb_per_split;
   Geo g;
@@ -68,20 +122,28 @@ struct Conv2Fwd {
   const bf16* w;
   const float* bias;
   bf16* out;
-  __device__ uint4 load_a(int m, int k) const {
-    const int hw = g.oh2 * g.ow2;
-    const int f = m / hw, p = m % hw, oy = p / g.ow2, ox = p % g.ow2;
+  __device__ const void* ptr_a(int m, int k) const {
+    uint32_t f, oy, ox;
+    split_row(g.hw2, g.w2, m, f, oy, ox);
     const int ky = k >> 6, kx = (k >> 4) & 3, c0 = k & 15;
-    return ld16(act1 + (((size_t)f * g.oh1 + oy * 2 + ky) * g.ow1 + ox * 2 + kx) * 16 + c0);
+    return act1 + (((size_t)f * g.oh1 + oy * 2 + ky) * g.ow1 + ox * 2 + kx) * 16 + c0;
   }
-  __device__ uint4 load_b(int n, int k) const { return ld16(w + (size_t)n * 256 + k); }
+  __device__ const void* ptr_b(int n, int k) const { return w + (size_t)n * 256 + k; }
   __device__ void store(int m, int n, float v) const {
     out[(size_t)m * 32 + n] = to_bf(fmaxf(v + bias[n], 0.f));
+  }
+  static constexpr bool VEC_STORE = true;
+  __device__ void store16(int m, int n0, float (&v)[16]) const {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = fmaxf(v[q] + bias[n0 + q], 0.f);
+    st_bf16x16(out + (size_t)m * 32 + n0, v);
   }
 };
 
 // fc: X[f][0:256] = relu(act2[f] . Wfc^T + b)
 struct FcFwd {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = false;
   int M, N, K, kb_per_split;
   int Kxp;
@@ -89,28 +151,46 @@ struct FcFwd {
   const bf16* w;
   const float* bias;
   bf16* X;
-  __device__ uint4 load_a(int m, int k) const { return ld16(act2 + (size_t)m * K + k); }
-  __device__ uint4 load_b(int n, int k) const { return ld16(w + (size_t)n * K + k); }
+  __device__ const void* ptr_a(int m, int k) const { return act2 + (size_t)m * K + k; }
+  __device__ const void* ptr_b(int n, int k) const { return w + (size_t)n * K + k; }
   __device__ void store(int m, int n, float v) const {
     X[(size_t)m * Kxp + n] = to_bf(fmaxf(v + bias[n], 0.f));
+  }
+  static constexpr bool VEC_STORE = true;
+  __device__ void store16(int m, int n0, float (&v)[16]) const {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = fmaxf(v[q] + bias[n0 + q], 0.f);
+    st_bf16x16(X + (size_t)m * Kxp + n0, v);
   }
 };
 
 // LSTM input projection: xproj[f][n] = X[f] . Wx[n] + b[n]
 struct XprojFwd {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = false;
   int M, N, K, kb_per_split;
   const bf16* X;
   const bf16* w;
   const float* bias;
   float* out;
-  __device__ uint4 load_a(int m, int k) const { return ld16(X + (size_t)m * K + k); }
-  __device__ uint4 load_b(int n, int k) const { return ld16(w + (size_t)n * K + k); }
+  __device__ const void* ptr_a(int m, int k) const { return X + (size_t)m * K + k; }
+  __device__ const void* ptr_b(int n, int k) const { return w + (size_t)n * K + k; }
   __device__ void store(int m, int n, float v) const { out[(size_t)m * N + n] = v + bias[n]; }
+  static constexpr bool VEC_STORE = true;
+  __device__ void store16(int m, int n0, float (&v)[16]) const {
+    float4* o = reinterpret_cast<float4*>(out + (size_t)m * N + n0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[q] = make_float4(v[4 * q] + bias[n0 + 4 * q], v[4 * q + 1] + bias[n0 + 4 * q + 1],
+                         v[4 * q + 2] + bias[n0 + 4 * q + 2], v[4 * q + 3] + bias[n0 + 4 * q + 3]);
+  }
 };
 
 // [dWx | db | dWh] = dG^T . [X | Hprev]   (M = 4U gate rows, K = F rows)
 struct LstmWgrad {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = true, B_MN = true;
   int M, N, K, kb_per_split;
   int Kx, Kxp, U;
@@ -120,9 +200,10 @@ struct LstmWgrad {
   float* g_wx;
   float* g_b;
   float* g_wh;
-  __device__ uint4 load_a(int row, int m8) const { return ld16(dG + (size_t)row * M + m8); }
-  __device__ uint4 load_b(int row, int n8) const {
-    return n8 < Kxp ? ld16(X + (size_t)row * Kxp + n8) : ld16(Hprev + (size_t)row * U + n8 - Kxp);
+  __device__ const void* ptr_a(int row, int m8) const { return dG + (size_t)row * M + m8; }
+  __device__ const void* ptr_b(int row, int n8) const {
+    return n8 < Kxp ? (const void*)(X + (size_t)row * Kxp + n8)
+                    : (const void*)(Hprev + (size_t)row * U + n8 - Kxp);
   }
   __device__ void store(int m, int n, float v) const {
     if (n < Kx) g_wx[(size_t)m * Kx + n] = v;
@@ -133,6 +214,8 @@ struct LstmWgrad {
 
 // dfc = (dG . Wx)[:, 0:256] masked by fc > 0
 struct DxFc {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = true;
   int M, N, K, kb_per_split;
   int Kxp;
@@ -140,15 +223,22 @@ struct DxFc {
   const bf16* wx;
   const bf16* X;
   bf16* dfc;
-  __device__ uint4 load_a(int m, int k) const { return ld16(dG + (size_t)m * K + k); }
-  __device__ uint4 load_b(int k, int n8) const { return ld16(wx + (size_t)k * Kxp + n8); }
+  __device__ const void* ptr_a(int m, int k) const { return dG + (size_t)m * K + k; }
+  __device__ const void* ptr_b(int k, int n8) const { return wx + (size_t)k * Kxp + n8; }
   __device__ void store(int m, int n, float v) const {
     dfc[(size_t)m * 256 + n] = to_bf(bf2f(X[(size_t)m * Kxp + n]) > 0.f ? v : 0.f);
+  }
+  static constexpr bool VEC_STORE = true;
+  __device__ void store16(int m, int n0, float (&v)[16]) const {
+    relu_mask16(X + (size_t)m * Kxp + n0, v);
+    st_bf16x16(dfc + (size_t)m * 256 + n0, v);
   }
 };
 
 // [dWfc | dbfc] = dfc^T . [act2 | 1]
 struct FcWgrad {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = true, B_MN = true;
   int M, N, K, kb_per_split;
   int fc_in;
@@ -156,10 +246,10 @@ struct FcWgrad {
   const bf16* act2;
   float* g_w;
   float* g_b;
-  __device__ uint4 load_a(int row, int m8) const { return ld16(dfc + (size_t)row * 256 + m8); }
-  __device__ uint4 load_b(int row, int n8) const {
-    if (n8 < fc_in) return ld16(act2 + (size_t)row * fc_in + n8);
-    return make_uint4(0x3F80u, 0u, 0u, 0u);  // bf16 1.0 in column fc_in, zeros after
+  __device__ const void* ptr_a(int row, int m8) const { return dfc + (size_t)row * 256 + m8; }
+  __device__ const void* ptr_b(int row, int n8) const {
+    if (n8 < fc_in) return act2 + (size_t)row * fc_in + n8;
+    return k_ones_chunk;  // bf16 1.0 in column fc_in, zeros after
   }
   __device__ void store(int m, int n, float v) const {
     if (n < fc_in) g_w[(size_t)m * fc_in + n] = v;
@@ -169,40 +259,52 @@ struct FcWgrad {
 
 // dY2 = (dfc . Wfc) masked by act2 > 0
 struct FcDgrad {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = true;
   int M, N, K, kb_per_split;
   const bf16* dfc;
   const bf16* w;
   const bf16* act2;
   bf16* dY2;
-  __device__ uint4 load_a(int m, int k) const { return ld16(dfc + (size_t)m * 256 + k); }
-  __device__ uint4 load_b(int k, int n8) const { return ld16(w + (size_t)k * N + n8); }
+  __device__ const void* ptr_a(int m, int k) const { return dfc + (size_t)m * 256 + k; }
+  __device__ const void* ptr_b(int k, int n8) const { return w + (size_t)k * N + n8; }
   __device__ void store(int m, int n, float v) const {
     const size_t i = (size_t)m * N + n;
     dY2[i] = to_bf(bf2f(act2[i]) > 0.f ? v : 0.f);
+  }
+  static constexpr bool VEC_STORE = true;
+  __device__ void store16(int m, int n0, float (&v)[16]) const {
+    const size_t i = (size_t)m * N + n0;
+    relu_mask16(act2 + i, v);
+    st_bf16x16(dY2 + i, v);
   }
 };
 
 // dW2^T[kin][co] = sum_rows im2col(act1)[row][kin] dY2[row][co]
 struct Conv2Wgrad {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = true, B_MN = true;
   int M, N, K, kb_per_split;
   Geo g;
   const bf16* act1;
   const bf16* dY2;
   float* g_w;
-  __device__ uint4 load_a(int row, int m8) const {
-    const int hw = g.oh2 * g.ow2;
-    const int f = row / hw, p = row % hw, oy = p / g.ow2, ox = p % g.ow2;
+  __device__ const void* ptr_a(int row, int m8) const {
+    uint32_t f, oy, ox;
+    split_row(g.hw2, g.w2, row, f, oy, ox);
     const int ky = m8 >> 6, kx = (m8 >> 4) & 3, c0 = m8 & 15;
-    return ld16(act1 + (((size_t)f * g.oh1 + oy * 2 + ky) * g.ow1 + ox * 2 + kx) * 16 + c0);
+    return act1 + (((size_t)f * g.oh1 + oy * 2 + ky) * g.ow1 + ox * 2 + kx) * 16 + c0;
   }
-  __device__ uint4 load_b(int row, int n8) const { return ld16(dY2 + (size_t)row * 32 + n8); }
+  __device__ const void* ptr_b(int row, int n8) const { return dY2 + (size_t)row * 32 + n8; }
   __device__ void store(int m, int n, float v) const { g_w[(size_t)n * 256 + m] = v; }
 };
 
 // dY1 = transposed conv of dY2 (implicit GEMM, k = (ky, kx, co)), masked by act1 > 0
 struct Conv2Dgrad {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = false;
   int M, N, K, kb_per_split;
   Geo g;
@@ -210,39 +312,47 @@ struct Conv2Dgrad {
   const bf16* wdg;  // [16 ci][4 ky][4 kx][32 co]
   const bf16* act1;
   bf16* dY1;
-  __device__ uint4 load_a(int m, int k) const {
-    const int hw = g.oh1 * g.ow1;
-    const int f = m / hw, p = m % hw, y = p / g.ow1, x = p % g.ow1;
+  __device__ const void* ptr_a(int m, int k) const {
+    uint32_t f, uy, ux;
+    split_row(g.hw1, g.w1, m, f, uy, ux);
+    const int y = (int)uy, x = (int)ux;
     const int ky = k >> 7, kx = (k >> 5) & 3, co0 = k & 31;
     const int yy = y - ky, xx = x - kx;
-    if (yy < 0 || xx < 0 || (yy & 1) || (xx & 1)) return make_uint4(0, 0, 0, 0);
+    if (yy < 0 || xx < 0 || (yy & 1) || (xx & 1)) return nullptr;
     const int oy = yy >> 1, ox = xx >> 1;
-    if (oy >= g.oh2 || ox >= g.ow2) return make_uint4(0, 0, 0, 0);
-    return ld16(dY2 + (((size_t)f * g.oh2 + oy) * g.ow2 + ox) * 32 + co0);
+    if (oy >= g.oh2 || ox >= g.ow2) return nullptr;
+    return dY2 + (((size_t)f * g.oh2 + oy) * g.ow2 + ox) * 32 + co0;
   }
-  __device__ uint4 load_b(int n, int k) const { return ld16(wdg + (size_t)n * K + k); }
+  __device__ const void* ptr_b(int n, int k) const { return wdg + (size_t)n * K + k; }
   __device__ void store(int m, int n, float v) const {
     const size_t i = (size_t)m * 16 + n;
     dY1[i] = to_bf(bf2f(act1[i]) > 0.f ? v : 0.f);
+  }
+  static constexpr bool VEC_STORE = true;
+  __device__ void store16(int m, int n0, float (&v)[16]) const {
+    const size_t i = (size_t)m * 16 + n0;
+    relu_mask16(act1 + i, v);
+    st_bf16x16(dY1 + i, v);
   }
 };
 
 // dW1^T[kin][co] = (1/255) sum_rows im2col(obs)[row][kin] dY1[row][co]
 struct Conv1Wgrad {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = true, B_MN = true;
   int M, N, K, kb_per_split;
   Geo g;
-  const uint8_t* obs;
+  const bf16* obs;
   const bf16* dY1;
   float* g_w;
-  __device__ uint4 load_a(int row, int m8) const {
-    const int hw = g.oh1 * g.ow1;
-    const int f = row / hw, p = row % hw, oy = p / g.ow1, ox = p % g.ow1;
-    const int ky = m8 / (8 * g.C), kx = (m8 % (8 * g.C)) / g.C;
-    const uint8_t* src = obs + (((size_t)f * g.H + oy * 4 + ky) * g.W + ox * 4 + kx) * g.C;
-    return u8x8_to_bf16(__ldg(reinterpret_cast<const uint2*>(src)));
+  __device__ const void* ptr_a(int row, int m8) const {
+    uint32_t f, oy, ox;
+    split_row(g.hw1, g.w1, row, f, oy, ox);
+    const int ky = m8 >> 5, kx = (m8 & 31) >> 2;   // C == 4
+    return obs + (((size_t)f * g.H + oy * 4 + ky) * g.W + ox * 4 + kx) * 4;
   }
-  __device__ uint4 load_b(int row, int n8) const { return ld16(dY1 + (size_t)row * 16 + n8); }
+  __device__ const void* ptr_b(int row, int n8) const { return dY1 + (size_t)row * 16 + n8; }
   __device__ void store(int m, int n, float v) const {
     g_w[(size_t)n * M + m] = v * (1.f / 255.f);
   }
@@ -252,7 +362,15 @@ struct Trace {
   void** events = nullptr;
   const char** names = nullptr;
   int max = 0, n = 0, launches = 0;
+  bool capturing = false;
 };
+
+// Inside stream capture an event record must be an explicit graph node
+// (cudaEventRecordExternal) to be recorded on every replay.
+static inline void trace_record(const Trace* tr, void* ev, cudaStream_t st) {
+  if (tr->capturing) cudaEventRecordWithFlags((cudaEvent_t)ev, st, cudaEventRecordExternal);
+  else cudaEventRecord((cudaEvent_t)ev, st);
+}
 
 struct StepCtx {
   const NetPlan* p;
@@ -268,7 +386,7 @@ struct StepCtx {
     if (!tr) return;
     tr->launches += k;
     if (tr->events && tr->n < tr->max) {
-      cudaEventRecord((cudaEvent_t)tr->events[tr->n], st);
+      trace_record(tr, tr->events[tr->n], st);
       if (tr->names) tr->names[tr->n] = name;
       tr->n++;
     }
@@ -289,9 +407,15 @@ static seed_status shallow_forward(const StepCtx& c, const seed_batch* bt, const
   const LearnerWs& w = c.w;
   const int F = w.F;
   {
+    const int64_t n16 = (int64_t)F * p.H * p.W * p.C / 16;
+    obs_to_bf16_kernel<<<(int)std::min<int64_t>((n16 + 255) / 256, 148 * 16), 256, 0, st>>>(
+        (const uint8_t*)bt->obs, c.at<bf16>(w.obs_bf16), n16);
+    c.mark("obs_bf16");
+  }
+  {
     Conv1Fwd pr{};
     pr.M = F * p.oh1 * p.ow1; pr.N = 16; pr.K = 64 * p.C;
-    pr.g = c.g; pr.obs = (const uint8_t*)bt->obs; pr.w = lowp + p.im_conv1;
+    pr.g = c.g; pr.obs = c.at<bf16>(w.obs_bf16); pr.w = lowp + p.im_conv1;
     pr.bias = params + p.t[p.i_conv1b].off; pr.out = c.at<bf16>(w.act1);
     SEED_TRY(gemm<16>(c, pr, st, "conv1_fwd"));
   }
@@ -350,7 +474,7 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
   dense_dgrad_f32<<<ceil_div(F * U, 256), 256, 0, st>>>(
       F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), params + p.t[p.i_hw].off,
       nullptr, c.at<float>(w.dH));
-  dense_wgrad_f32<<<ceil_div((A + 1) * (U + 1), 256), 256, 0, st>>>(
+  dense_wgrad_f32<<<dim3(A + 1, ceil_div(U + 1, 32)), 256, 0, st>>>(
       F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), c.at<float>(w.H),
       grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off);
   SEED_TRY(last_launch());
@@ -412,7 +536,7 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
   {
     Conv1Wgrad pr{};
     pr.M = 64 * p.C; pr.N = 16; pr.K = F * p.oh1 * p.ow1; pr.g = c.g;
-    pr.obs = (const uint8_t*)bt->obs; pr.dY1 = c.at<bf16>(w.dY1);
+    pr.obs = c.at<bf16>(w.obs_bf16); pr.dY1 = c.at<bf16>(w.dY1);
     pr.g_w = grads + p.t[p.i_conv1w].off;
     SEED_TRY(gemm<16>(c, pr, st, "conv1_wgrad"));
   }
@@ -447,16 +571,16 @@ static seed_status mlp_backward(const StepCtx& c, const seed_batch* bt, const fl
   dense_dgrad_f32<<<ceil_div(F * 64, 256), 256, 0, st>>>(
       F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), params + p.t[p.i_hw].off,
       c.at<float>(w.h2), c.at<float>(w.dh2));
-  dense_wgrad_f32<<<ceil_div((A + 1) * 65, 256), 256, 0, st>>>(
+  dense_wgrad_f32<<<dim3(A + 1, ceil_div(65, 32)), 256, 0, st>>>(
       F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), c.at<float>(w.h2),
       grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off);
   dense_dgrad_f32<<<ceil_div(F * 64, 256), 256, 0, st>>>(
       F, 64, 64, c.at<float>(w.dh2), 64, nullptr, params + p.t[p.i_m1w].off, c.at<float>(w.h1),
       c.at<float>(w.dh1));
-  dense_wgrad_f32<<<ceil_div(64 * 65, 256), 256, 0, st>>>(
+  dense_wgrad_f32<<<dim3(64, ceil_div(65, 32)), 256, 0, st>>>(
       F, 64, 64, c.at<float>(w.dh2), 64, nullptr, c.at<float>(w.h1), grads + p.t[p.i_m1w].off,
       grads + p.t[p.i_m1b].off);
-  dense_wgrad_f32<<<ceil_div(64 * (p.D + 1), 256), 256, 0, st>>>(
+  dense_wgrad_f32<<<dim3(64, ceil_div(p.D + 1, 32)), 256, 0, st>>>(
       F, p.D, 64, c.at<float>(w.dh1), 64, nullptr, (const float*)bt->obs,
       grads + p.t[p.i_m0w].off, grads + p.t[p.i_m0b].off);
   c.mark("mlp_bwd", 5);
@@ -489,12 +613,17 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   SEED_TRY(make_learner_ws(p, T, B, &c.w));
   if (ws_bytes < c.w.total) return SEED_E_WORKSPACE;
   c.ws = (uint8_t*)ws;
-  c.g = Geo{p.H, p.W, p.C, p.oh1, p.ow1, p.oh2, p.ow2, p.fc_in, p.Kx, p.Kxp};
+  c.g = Geo{p.H, p.W, p.C, p.oh1, p.ow1, p.oh2, p.ow2, p.fc_in, p.Kx, p.Kxp,
+             FastDiv((uint32_t)(p.oh1 * p.ow1)), FastDiv((uint32_t)p.ow1),
+             FastDiv((uint32_t)(p.oh2 * p.ow2)), FastDiv((uint32_t)p.ow2)};
   cudaStream_t st = (cudaStream_t)stream;
   c.st = st;
   c.tr = tr;
   if (tr && tr->events && tr->max > 0) {
-    cudaEventRecord((cudaEvent_t)tr->events[0], st);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    tr->capturing = cs == cudaStreamCaptureStatusActive;
+    trace_record(tr, tr->events[0], st);
     if (tr->names) tr->names[0] = "begin";
     tr->n = 1;
   }

@@ -46,19 +46,39 @@ __global__ void dense_dgrad_f32(int R, int I, int O, const float* __restrict__ d
   dX[idx] = s;
 }
 
-__global__ void dense_wgrad_f32(int R, int I, int O, const float* __restrict__ dy, int ldy,
-                                const float* __restrict__ dv, const float* __restrict__ X,
-                                float* __restrict__ gW, float* __restrict__ gb) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= O * (I + 1)) return;
-  const int o = idx / (I + 1), i = idx % (I + 1);
-  float s = 0.f;
-  if (i < I) {
-    for (int r = 0; r < R; ++r) s += dy_at(dy, ldy, dv, r, o) * X[(size_t)r * I + i];
-    gW[(size_t)o * I + i] = s;
-  } else {
-    for (int r = 0; r < R; ++r) s += dy_at(dy, ldy, dv, r, o);
-    gb[o] = s;
+// grid (O, ceil((I+1)/32)), block 256 = 32 columns x 8 row groups; each thread
+// keeps 4 independent accumulators, the 8 row groups are summed in fixed order.
+__global__ void __launch_bounds__(256) dense_wgrad_f32(int R, int I, int O, const float* __restrict__ dy,
+                                                       int ldy, const float* __restrict__ dv,
+                                                       const float* __restrict__ X,
+                                                       float* __restrict__ gW, float* __restrict__ gb) {
+  const int o = blockIdx.x;
+  const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int i = blockIdx.y * 32 + lane;
+  const bool isb = i == I, valid = i <= I;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (valid) {
+    int r = rg;
+    for (; r + 24 < R; r += 32) {
+      const float d0 = dy_at(dy, ldy, dv, r, o), d1 = dy_at(dy, ldy, dv, r + 8, o);
+      const float d2 = dy_at(dy, ldy, dv, r + 16, o), d3 = dy_at(dy, ldy, dv, r + 24, o);
+      const float x0 = isb ? 1.f : X[(size_t)r * I + i];
+      const float x1 = isb ? 1.f : X[(size_t)(r + 8) * I + i];
+      const float x2 = isb ? 1.f : X[(size_t)(r + 16) * I + i];
+      const float x3 = isb ? 1.f : X[(size_t)(r + 24) * I + i];
+      a0 += d0 * x0; a1 += d1 * x1; a2 += d2 * x2; a3 += d3 * x3;
+    }
+    for (; r < R; r += 8) a0 += dy_at(dy, ldy, dv, r, o) * (isb ? 1.f : X[(size_t)r * I + i]);
+  }
+  __shared__ float sh[8][33];
+  sh[rg][lane] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (rg == 0 && valid) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][lane];
+    if (isb) gb[o] = t;
+    else gW[(size_t)o * I + i] = t;
   }
 }
 

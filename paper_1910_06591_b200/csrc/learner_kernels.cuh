@@ -20,7 +20,8 @@ __global__ void dense_dgrad_f32(int R, int I, int O, const float* __restrict__ d
                                 const float* __restrict__ dv, const float* __restrict__ W,
                                 const float* __restrict__ mask, float* __restrict__ dX);
 
-// gW[o][i] = sum_r dY(r,o) X[r][i];  gb[o] = sum_r dY(r,o)  (thread per (o,i), fixed order)
+// gW[o][i] = sum_r dY(r,o) X[r][i];  gb[o] = sum_r dY(r,o)  (grid (O, ceil((I+1)/32)), 256
+// threads; fixed-order reduction)
 __global__ void dense_wgrad_f32(int R, int I, int O, const float* __restrict__ dy, int ldy,
                                 const float* __restrict__ dv, const float* __restrict__ X,
                                 float* __restrict__ gW, float* __restrict__ gb);

@@ -74,8 +74,31 @@ __device__ __forceinline__ void load_wh_slice(__nv_bfloat16* Ws, const __nv_bflo
   }
 }
 
-constexpr int FWD_SMEM = 128 * HP * 2 + 2 * 32 * HP * 2 + 32 * GP * 4 + 32 * 32 * 4;
-constexpr int BWD_SMEM = 128 * HP * 2 + 32 * DP * 2 + 2 * 8 * 32 * RP * 4 + 32 * 32 * 4;
+// ---- DSMEM transaction handshake (no cluster barrier inside the step loop):
+// a producer writes its slice into every CTA's buffer with st.async, which
+// credits the receiving CTA's mbarrier with the bytes; the receiver arms the
+// barrier once per phase with the total bytes it expects and waits on it.
+__device__ __forceinline__ void st_async_u32(uint32_t raddr, uint32_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr),
+               "r"(v), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_f32x2(uint32_t raddr, float a, float b, uint32_t rbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+      "f"(a), "f"(b), "r"(rbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arm_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+constexpr int MAX_T1 = 257;
+constexpr int FWD_SMEM = 128 * HP * 2 + 2 * 32 * HP * 2 + 32 * GP * 4 + 32 * 32 * 4 + 32 * MAX_T1 + 64;
+constexpr int BWD_SMEM = 128 * HP * 2 + 32 * DP * 2 + 2 * 8 * 32 * RP * 4 + 32 * 32 * 4 + 32 * MAX_T1 + 64;
+constexpr uint32_t H_TX_BYTES = 32 * LSTM_U * 2;          // h slices from 8 CTAs, bf16
+constexpr uint32_t R_TX_BYTES = 8 * 32 * 32 * 4;          // 8 partial dh slices, fp32
 
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_fwd_kernel(const LstmFwdArgs a) {
@@ -85,13 +108,24 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   __nv_bfloat16* hb = Ws + 128 * HP;
   float* gpre = reinterpret_cast<float*>(hb + 2 * 32 * HP);
   float* cst = gpre + 32 * GP;
+  uint8_t* dn_s = reinterpret_cast<uint8_t*>(cst + 32 * 32);   // [32][T1]
+  uint64_t* hbar = reinterpret_cast<uint64_t*>(dn_s + ((32 * MAX_T1 + 15) & ~15));
   const int r = (int)cluster_rank();
   const int b0 = (blockIdx.x / LSTM_CLUSTER) * LSTM_BB;
   const int BB = min(LSTM_BB, a.B - b0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T1 = a.T1;
 
+  if (tid == 0) {
+    mbar_init(&hbar[0], 1);
+    mbar_init(&hbar[1], 1);
+    fence_mbar_init();
+  }
   load_wh_slice(Ws, a.wh, r);
+  for (int i = tid; i < 32 * T1; i += 256) {
+    const int b = i / T1, t = i % T1;
+    dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
+  }
   for (int idx = tid; idx < 32 * U; idx += 256) {
     const int b = idx / U, k = idx % U;
     float v = 0.f;
@@ -117,11 +151,34 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     cst[b * 32 + j] = c;
   }
   __syncthreads();
-  cluster_sync_all();
+  cluster_sync_all();   // barriers initialised everywhere before any st.async
 
+  // per-thread cell work: two (row, unit pair) items
+  int it_b[2], it_j[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int idx = tid + 256 * q;
+    it_b[q] = idx >> 4;
+    it_j[q] = (idx & 15) * 2;
+  }
+  float2 xq[2][4];
+  auto load_x = [&](int t) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (it_b[q] < BB) {
+        const float* xp = a.xproj + ((size_t)(b0 + it_b[q]) * T1 + t) * (4 * U) + 32 * r + it_j[q];
+#pragma unroll
+        for (int gq = 0; gq < 4; ++gq) xq[q][gq] = __ldg(reinterpret_cast<const float2*>(xp + gq * U));
+      }
+    }
+  };
+  load_x(0);
   const int gid = lane >> 2, tig = lane & 3;
   for (int t = 0; t < T1; ++t) {
-    const __nv_bfloat16* hcur = hb + (t & 1) * 32 * HP;
+    const int cur = t & 1, nbuf = cur ^ 1;
+    if (tid == 0 && t + 1 < T1) mbar_arm_tx(&hbar[nbuf], H_TX_BYTES);
+    if (t > 0) mbar_wait(&hbar[cur], ((t - 1) >> 1) & 1);
+    const __nv_bfloat16* hcur = hb + cur * 32 * HP;
     float acc[2][2][4];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -149,30 +206,28 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int row = mt * 16 + gid, col = warp * 16 + nt * 8 + tig * 2;
-        gpre[row * GP + col] = acc[mt][nt][0];
-        gpre[row * GP + col + 1] = acc[mt][nt][1];
-        gpre[(row + 8) * GP + col] = acc[mt][nt][2];
-        gpre[(row + 8) * GP + col + 1] = acc[mt][nt][3];
+        *reinterpret_cast<float2*>(gpre + row * GP + col) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
+        *reinterpret_cast<float2*>(gpre + (row + 8) * GP + col) =
+            make_float2(acc[mt][nt][2], acc[mt][nt][3]);
       }
     __syncthreads();
-    const int nbuf = (t + 1) & 1;
+    float2 xc[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int gq = 0; gq < 4; ++gq) xc[q][gq] = xq[q][gq];
+    if (t + 1 < T1) load_x(t + 1);   // prefetch: in flight during this step's cell + exchange
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const int idx = tid + 256 * q;
-      const int b = idx >> 4, j = (idx & 15) * 2;
+      const int b = it_b[q], j = it_j[q];
       if (b < BB) {
         const int bb = b0 + b;
         const size_t row = (size_t)bb * T1 + t;
         const int col = 32 * r + j;
-        const float* xp = a.xproj + row * (4 * U) + col;
-        const float2 xi = *reinterpret_cast<const float2*>(xp);
-        const float2 xf = *reinterpret_cast<const float2*>(xp + U);
-        const float2 xg = *reinterpret_cast<const float2*>(xp + 2 * U);
-        const float2 xo = *reinterpret_cast<const float2*>(xp + 3 * U);
         const float* gp = gpre + b * GP + j;
         float hv[2], cv[2], gi[2], gf[2], gg[2], go[2];
-        const float xiv[2] = {xi.x, xi.y}, xfv[2] = {xf.x, xf.y}, xgv[2] = {xg.x, xg.y},
-                    xov[2] = {xo.x, xo.y};
+        const float xiv[2] = {xc[q][0].x, xc[q][0].y}, xfv[2] = {xc[q][1].x, xc[q][1].y},
+                    xgv[2] = {xc[q][2].x, xc[q][2].y}, xov[2] = {xc[q][3].x, xc[q][3].y};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           gi[e] = sigm(gp[e] + xiv[e]);
@@ -182,36 +237,46 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
           cv[e] = gf[e] * cst[b * 32 + j + e] + gi[e] * gg[e];
           hv[e] = go[e] * tanhf(cv[e]);
         }
-        *reinterpret_cast<float2*>(a.H + row * U + col) = make_float2(hv[0], hv[1]);
-        if (a.Hb)
-          *reinterpret_cast<uint32_t*>(a.Hb + row * U + col) = pack_bf16(hv[0], hv[1]);
-        if (a.C) *reinterpret_cast<float2*>(a.C + row * U + col) = make_float2(cv[0], cv[1]);
-        if (a.gates) {
-          float* gq = a.gates + row * (4 * U) + col;
-          *reinterpret_cast<float2*>(gq) = make_float2(gi[0], gi[1]);
-          *reinterpret_cast<float2*>(gq + U) = make_float2(gf[0], gf[1]);
-          *reinterpret_cast<float2*>(gq + 2 * U) = make_float2(gg[0], gg[1]);
-          *reinterpret_cast<float2*>(gq + 3 * U) = make_float2(go[0], go[1]);
-        }
         if (t + 1 < T1) {
-          const bool dn = a.done[(size_t)bb * T1 + t + 1] != 0;
+          const bool dn = dn_s[b * T1 + t + 1] != 0;
           const float h0n = dn ? 0.f : hv[0], h1n = dn ? 0.f : hv[1];
           cst[b * 32 + j] = dn ? 0.f : cv[0];
           cst[b * 32 + j + 1] = dn ? 0.f : cv[1];
           const uint32_t pv = pack_bf16(h0n, h1n);
-          if (a.Hprev) *reinterpret_cast<uint32_t*>(a.Hprev + (row + 1) * U + col) = pv;
           const uint32_t local = smem_u32(hb + nbuf * 32 * HP + b * HP + col);
+          const uint32_t lbar = smem_u32(&hbar[nbuf]);
 #pragma unroll
-          for (int s = 0; s < LSTM_CLUSTER; ++s) st_cluster_u32(mapa_u32(local, s), pv);
+          for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2)
+            st_async_u32(mapa_u32(local, s2), pv, mapa_u32(lbar, s2));
+          if (a.Hprev) *reinterpret_cast<uint32_t*>(a.Hprev + (row + 1) * U + col) = pv;
         } else if (a.hT) {
           const int srow = a.state_rows ? a.state_rows[bb] : bb;
           *reinterpret_cast<float2*>(a.hT + (size_t)srow * U + col) = make_float2(hv[0], hv[1]);
           *reinterpret_cast<float2*>(a.cT + (size_t)srow * U + col) = make_float2(cv[0], cv[1]);
         }
+        *reinterpret_cast<float2*>(a.H + row * U + col) = make_float2(hv[0], hv[1]);
+        if (a.Hb)
+          *reinterpret_cast<uint32_t*>(a.Hb + row * U + col) = pack_bf16(hv[0], hv[1]);
+        if (a.C) *reinterpret_cast<float2*>(a.C + row * U + col) = make_float2(cv[0], cv[1]);
+        if (a.gates) {
+          float* gq2 = a.gates + row * (4 * U) + col;
+          *reinterpret_cast<float2*>(gq2) = make_float2(gi[0], gi[1]);
+          *reinterpret_cast<float2*>(gq2 + U) = make_float2(gf[0], gf[1]);
+          *reinterpret_cast<float2*>(gq2 + 2 * U) = make_float2(gg[0], gg[1]);
+          *reinterpret_cast<float2*>(gq2 + 3 * U) = make_float2(go[0], go[1]);
+        }
+      } else if (t + 1 < T1) {
+        // rows beyond B still credit the receivers' transaction count (zeros)
+        const uint32_t local = smem_u32(hb + nbuf * 32 * HP + b * HP + 32 * r + j);
+        const uint32_t lbar = smem_u32(&hbar[nbuf]);
+#pragma unroll
+        for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2)
+          st_async_u32(mapa_u32(local, s2), 0u, mapa_u32(lbar, s2));
       }
     }
-    cluster_sync_all();
+    __syncthreads();   // gpre / cst reuse
   }
+  cluster_sync_all();
 }
 
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
@@ -222,21 +287,64 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   __nv_bfloat16* dzs = Ws + 128 * HP;
   float* red = reinterpret_cast<float*>(dzs + 32 * DP);   // [2][8][32][RP]
   float* dcs = red + 2 * 8 * 32 * RP;                      // [32][32]
+  uint8_t* dn_s = reinterpret_cast<uint8_t*>(dcs + 32 * 32);
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(dn_s + ((32 * MAX_T1 + 15) & ~15));
   const int r = (int)cluster_rank();
   const int b0 = (blockIdx.x / LSTM_CLUSTER) * LSTM_BB;
   const int BB = min(LSTM_BB, a.B - b0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T1 = a.T1;
 
+  if (tid == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    fence_mbar_init();
+  }
   load_wh_slice(Ws, a.wh, r);
+  for (int i = tid; i < 32 * T1; i += 256) {
+    const int b = i / T1, t = i % T1;
+    dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
+  }
   for (int i = tid; i < 32 * DP; i += 256) dzs[i] = __float2bfloat16_rn(0.f);
   for (int i = tid; i < 32 * 32; i += 256) dcs[i] = 0.f;
   __syncthreads();
   cluster_sync_all();
 
+  // per-thread cell work: four (row, unit) items; prefetched per step
+  float pdh[4], pg[4][4], pc[4], pcp[4];
+  auto load_in = [&](int t) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + 256 * q, b = idx >> 5, j = idx & 31;
+      if (b < BB) {
+        const int bb = b0 + b;
+        const size_t row = (size_t)bb * T1 + t;
+        const int col = 32 * r + j;
+        pdh[q] = __ldg(a.dH + row * U + col);
+        const float* gq = a.gates + row * (4 * U) + col;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pg[q][k] = __ldg(gq + k * U);
+        pc[q] = __ldg(a.C + row * U + col);
+        pcp[q] = t > 0 ? __ldg(a.C + (row - 1) * U + col) : __ldg(a.c0 + (size_t)bb * U + col);
+      }
+    }
+  };
+  load_in(T1 - 1);
   const int gid = lane >> 2, tig = lane & 3;
-  for (int t = T1 - 1; t >= 0; --t) {
-    const float* rin = red + ((t + 1) & 1) * 8 * 32 * RP;
+  for (int u = 0; u < T1; ++u) {
+    const int t = T1 - 1 - u;
+    // partials produced at step u land in buffer u&1; consumed at step u+1
+    if (tid == 0 && t > 0) mbar_arm_tx(&rbar[u & 1], R_TX_BYTES);
+    if (u > 0) mbar_wait(&rbar[(u - 1) & 1], ((u - 1) >> 1) & 1);
+    const float* rin = red + ((u - 1) & 1) * 8 * 32 * RP;
+    float cdh[4], cg[4][4], cc[4], ccp[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cdh[q] = pdh[q]; cc[q] = pc[q]; ccp[q] = pcp[q];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cg[q][k] = pg[q][k];
+    }
+    if (t > 0) load_in(t - 1);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int idx = tid + 256 * q;
@@ -245,19 +353,17 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
         const int bb = b0 + b;
         const size_t row = (size_t)bb * T1 + t;
         const int col = 32 * r + j;
-        float dh = a.dH[row * U + col];
-        if (t + 1 < T1 && !a.done[(size_t)bb * T1 + t + 1]) {
+        float dh = cdh[q];
+        if (u > 0 && !dn_s[b * T1 + t + 1]) {
           float s = 0.f;
 #pragma unroll
           for (int src = 0; src < LSTM_CLUSTER; ++src) s += rin[(src * 32 + b) * RP + j];
           dh += s;
         }
-        const float* gq = a.gates + row * (4 * U) + col;
-        const float gi = gq[0], gf = gq[U], gg = gq[2 * U], go = gq[3 * U];
-        const float c = a.C[row * U + col];
-        const bool dn = a.done[(size_t)bb * T1 + t] != 0;
-        const float cp = dn ? 0.f : (t > 0 ? a.C[(row - 1) * U + col] : a.c0[(size_t)bb * U + col]);
-        const float tc = tanhf(c);
+        const float gi = cg[q][0], gf = cg[q][1], gg = cg[q][2], go = cg[q][3];
+        const bool dn = dn_s[b * T1 + t] != 0;
+        const float cp = dn ? 0.f : ccp[q];
+        const float tc = tanhf(cc[q]);
         const float dc = dcs[b * 32 + j] + dh * go * (1.f - tc * tc);
         const float dzi = dc * gg * gi * (1.f - gi);
         const float dzf = dc * cp * gf * (1.f - gf);
@@ -307,21 +413,23 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
           }
         }
       }
-      // columns [32*warp, 32*warp+32) belong to CTA `warp`: slot r of its buffer t&1
-      const uint32_t base = smem_u32(red + ((t & 1) * 8 + r) * 32 * RP);
+      // columns [32*warp, 32*warp+32) belong to CTA `warp`: its slot r of buffer u&1
+      const uint32_t base = smem_u32(red + ((u & 1) * 8 + r) * 32 * RP);
+      const uint32_t rb = mapa_u32(smem_u32(&rbar[u & 1]), warp);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
           const int row = mt * 16 + gid, j = nt * 8 + tig * 2;
-          st_cluster_f32x2(mapa_u32(base + (row * RP + j) * 4, warp), acc[mt][nt][0],
-                           acc[mt][nt][1]);
-          st_cluster_f32x2(mapa_u32(base + ((row + 8) * RP + j) * 4, warp), acc[mt][nt][2],
-                           acc[mt][nt][3]);
+          st_async_f32x2(mapa_u32(base + (row * RP + j) * 4, warp), acc[mt][nt][0],
+                         acc[mt][nt][1], rb);
+          st_async_f32x2(mapa_u32(base + ((row + 8) * RP + j) * 4, warp), acc[mt][nt][2],
+                         acc[mt][nt][3], rb);
         }
     }
-    cluster_sync_all();
+    __syncthreads();   // dzs / dcs reuse
   }
+  cluster_sync_all();
 }
 
 seed_status lstm_forward(const LstmFwdArgs& a, cudaStream_t st) {

@@ -109,7 +109,7 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
 
 bool learner_supported(const NetPlan& p) {
   if (p.kind == SEED_NET_MLP) return true;
-  if (p.kind == SEED_NET_ATARI_SHALLOW) return p.C == 4 && p.fc_in % 8 == 0;
+  if (p.kind == SEED_NET_ATARI_SHALLOW) return p.C == 4 && p.fc_in % 8 == 0 && (p.W * p.C) % 16 == 0;
   return false;
 }
 
@@ -157,6 +157,7 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   }
   const size_t U = p.U;
   w->dH = bump(cur, F * U * 4);
+  w->obs_bf16 = bump(cur, F * p.H * p.W * p.C * 2);
   w->act1 = bump(cur, F * p.oh1 * p.ow1 * 16 * 2);
   w->act2 = bump(cur, F * p.fc_in * 2);
   w->X = bump(cur, F * p.Kxp * 2);

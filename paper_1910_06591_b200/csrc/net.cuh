@@ -52,7 +52,7 @@ struct LearnerWs {
       colsum_part, dH;
   size_t splitk_bytes;
   // shallow
-  size_t act1, act2, X, xproj, H, Hprev, gates, Cst, dG, dfc, dY2, dY1;
+  size_t obs_bf16, act1, act2, X, xproj, H, Hprev, gates, Cst, dG, dfc, dY2, dY1;
   // mlp
   size_t h1, h2, dh1, dh2;
 };

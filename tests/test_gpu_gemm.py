@@ -10,7 +10,9 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("bn", [16, 32, 64, 128, 256])
 @pytest.mark.parametrize("at,bt", [(False, False), (False, True), (True, False), (True, True)])
 @pytest.mark.parametrize("M,N,K,splits", [(128, 64, 64, 1), (200, 40, 136, 1),
-                                          (384, 256, 1024, 1), (256, 32, 4096, 5)])
+                                          (384, 256, 1024, 1), (256, 32, 4096, 5),
+                                          (200, 40, 136, -1), (256, 32, 4096, -3),
+                                          (1152, 48, 520, 1)])
 def test_gemm_engine(bn, at, bt, M, N, K, splits):
     import paper_1910_06591_b200 as S
     g = torch.Generator().manual_seed(M * 7 + N * 3 + K)
