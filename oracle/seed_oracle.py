@@ -671,3 +671,36 @@ class UnrollStore:
                                    c0=np.array(c_before))
             self.cur[actor] = 1 - self.cur[actor]
             self.fill[actor] = 1
+
+
+# --------------------------------------------------------------------------
+# Counter-based sampling stream (C18): Philox4x32-10 (Salmon et al., SC'11,
+# the Random123 generator), keyed (seed) with counter (counter, actor id).
+# --------------------------------------------------------------------------
+_PHILOX_M = (0xD2511F53, 0xCD9E8D57)
+_PHILOX_W = (0x9E3779B9, 0xBB67AE85)
+
+
+def philox4x32_10(ctr, key):
+    """ctr: 4 uint32 (arrays broadcast), key: 2 uint32.  10 rounds, key bumped
+    between rounds: out = {hi1^c1^k0, lo1, hi0^c3^k1, lo0}."""
+    c = [np.asarray(x, np.uint64) & 0xFFFFFFFF for x in ctr]
+    k = [np.asarray(x, np.uint64) & 0xFFFFFFFF for x in key]
+    for r in range(10):
+        if r:
+            k = [(k[0] + _PHILOX_W[0]) & 0xFFFFFFFF, (k[1] + _PHILOX_W[1]) & 0xFFFFFFFF]
+        p0 = c[0] * _PHILOX_M[0]
+        p1 = c[2] * _PHILOX_M[1]
+        hi0, lo0 = p0 >> 32, p0 & 0xFFFFFFFF
+        hi1, lo1 = p1 >> 32, p1 & 0xFFFFFFFF
+        c = [hi1 ^ c[1] ^ k[0], lo1, hi0 ^ c[3] ^ k[1], lo0]
+    return [x.astype(np.uint32) for x in c]
+
+
+def philox_uniforms(seed, counter, actor_ids):
+    """u = (x0 >> 8) * 2^-24 with x = Philox4x32-10(ctr = (counter lo, counter hi,
+    actor id, 0), key = (seed lo, seed hi)) — one uniform per actor."""
+    ids = np.asarray(actor_ids, np.uint64)
+    x = philox4x32_10([counter & 0xFFFFFFFF, counter >> 32, ids, 0],
+                      [seed & 0xFFFFFFFF, seed >> 32])
+    return (x[0] >> 8).astype(np.float64) * (1.0 / 16777216.0)

@@ -1,0 +1,399 @@
+// infer.cu — centralized batched inference (H12, H13): seed_infer and
+// seed_assemble_batch.
+//
+// P:125 "Inference threads receive a batch of observations, rewards and episode
+// termination flags. They load the recurrent states and send the data to the
+// inference TPU core. The sampled actions and new recurrent states are
+// received ... the latest recurrent states are stored.  When a trajectory is
+// fully unrolled it is added to a FIFO queue"; S:434-442 (serve_inference).
+//
+// One call over n requests (unique actor ids):
+//   pre      gather last_action / (h, c) of each actor (pre-reset copy kept for
+//            the unroll store, C19), core-input extras onehot(prev a), clip(r),
+//            zeroed on done (C15)
+//   torso    obs -> bf16, conv1, conv2, fc on the tcgen05 engine (shallow_net.cuh)
+//   core     LSTM input projection GEMM + the cluster LSTM kernel with T+1 = 1,
+//            reading (h, c) from the table rows (reset on done) and writing the
+//            new state back to the same rows
+//   heads    logits / value (fp32)
+//   sample   warp per request: softmax, CDF, a = min{j : u < CDF_j} (C18),
+//            behaviour log-prob; u from the caller or Philox4x32-10
+//            keyed (seed, counter, actor id)
+//   record   (optional) obs/action/reward/done/log-prob into each actor's
+//            current unroll buffer; a completed unroll (T+1 slots) is pushed to
+//            the ready ring at a position given by a block-wide prefix sum in
+//            request order (deterministic) and slot T is copied into slot 0
+//            of the actor's other buffer (C17)
+#include "learner_kernels.cuh"
+#include "lstm.cuh"
+#include "net.cuh"
+#include "shallow_net.cuh"
+
+namespace seed {
+
+struct InferWs {
+  int n;
+  size_t total, obs_bf16, act1, act2, X, xproj, H, logits, values, hpre, cpre, prev, splitk;
+};
+
+static size_t ibump(size_t& cur, size_t bytes) {
+  const size_t at = cur;
+  cur = align_up(cur + bytes, 256);
+  return at;
+}
+
+static seed_status make_infer_ws(const NetPlan& p, int n, InferWs* w) {
+  memset(w, 0, sizeof(*w));
+  w->n = n;
+  size_t cur = 0;
+  const size_t N = n;
+  w->obs_bf16 = ibump(cur, N * p.H * p.W * p.C * 2);
+  w->act1 = ibump(cur, N * p.oh1 * p.ow1 * 16 * 2);
+  w->act2 = ibump(cur, N * p.fc_in * 2);
+  w->X = ibump(cur, N * p.Kxp * 2);
+  w->xproj = ibump(cur, N * 4 * p.U * 4);
+  w->H = ibump(cur, N * p.U * 4);
+  w->logits = ibump(cur, N * p.A * 4);
+  w->values = ibump(cur, N * 4);
+  w->hpre = ibump(cur, N * p.U * 4);
+  w->cpre = ibump(cur, N * p.U * 4);
+  w->prev = ibump(cur, N * 4);
+  size_t sk = 0;
+  auto need = [&](int M, int Nn, int BN, int K) {
+    const int s = pick_splits(M, Nn, BN, K);
+    if (s > 1) sk = std::max(sk, (size_t)s * M * Nn * 4);
+  };
+  need(n, 256, 128, p.fc_in);
+  need(n, 4 * p.U, 128, p.Kxp);
+  w->splitk = ibump(cur, sk + 16);
+  w->total = cur;
+  return SEED_OK;
+}
+
+// ------------------------------------------------------------------ pre
+__global__ void infer_pre_kernel(int n, int A, int U, int Kxp, const int32_t* __restrict__ ids,
+                                 const float* __restrict__ reward, const uint8_t* __restrict__ done,
+                                 const float* __restrict__ th, const float* __restrict__ tc,
+                                 const int32_t* __restrict__ tla, float* __restrict__ hpre,
+                                 float* __restrict__ cpre, int32_t* __restrict__ prev,
+                                 __nv_bfloat16* __restrict__ X) {
+  const int E = Kxp - 256;
+  const int per = U + E;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * per) return;
+  const int i = (int)(idx / per), j = (int)(idx % per);
+  const int a = ids[i];
+  if (j < U) {
+    hpre[(size_t)i * U + j] = th[(size_t)a * U + j];
+    cpre[(size_t)i * U + j] = tc[(size_t)a * U + j];
+    return;
+  }
+  const int e = j - U;
+  const bool dn = done[i] != 0;
+  const int pa = tla[a];
+  if (e == 0) prev[i] = pa;
+  float v = 0.f;
+  if (e < A) v = (!dn && pa == e) ? 1.f : 0.f;
+  else if (e == A) v = dn ? 0.f : fminf(fmaxf(reward[i], -1.f), 1.f);
+  else if (e == A + 1) v = 1.f;
+  X[(size_t)i * Kxp + 256 + e] = __float2bfloat16_rn(v);
+}
+
+// ------------------------------------------------------------------ Philox4x32-10
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// ------------------------------------------------------------------ sample
+// warp per request; lane j holds action j (A <= 32)
+__global__ void infer_sample_kernel(int n, int A, const float* __restrict__ logits,
+                                    const float* __restrict__ uniforms, uint64_t seed,
+                                    uint64_t counter, const int32_t* __restrict__ ids,
+                                    int32_t* __restrict__ action_out, float* __restrict__ blp_out,
+                                    int32_t* __restrict__ tla) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const float z = lane < A ? logits[(size_t)i * A + lane] : -INFINITY;
+  const float mx = warp_max(z);
+  const float e = lane < A ? expf(z - mx) : 0.f;
+  const float se = warp_sum(e);
+  // inclusive prefix sum of probabilities (CDF), fp32, in action order
+  float cdf = e / se;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float t = __shfl_up_sync(0xffffffffu, cdf, o);
+    if (lane >= o) cdf += t;
+  }
+  float u;
+  if (uniforms) {
+    u = uniforms[i];
+  } else {
+    const uint4 r = philox4x32_10(
+        make_uint4((uint32_t)counter, (uint32_t)(counter >> 32), (uint32_t)ids[i], 0u),
+        make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+    u = (float)(r.x >> 8) * (1.f / 16777216.f);
+  }
+  const unsigned hit = __ballot_sync(0xffffffffu, lane < A && u < cdf);
+  const int a = hit ? (__ffs(hit) - 1) : A - 1;
+  const float za = __shfl_sync(0xffffffffu, z, a);
+  if (lane == 0) {
+    action_out[i] = a;
+    blp_out[i] = za - mx - logf(se);
+    tla[ids[i]] = a;
+  }
+}
+
+// ------------------------------------------------------------------ unroll store
+__global__ void infer_store_obs_kernel(int n, int64_t obs16, const uint8_t* __restrict__ obs,
+                                       const int32_t* __restrict__ ids, seed_unroll_store st) {
+  const int T1 = st.T + 1;
+  const int64_t total = (int64_t)n * obs16;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / obs16);
+    const int64_t q = idx % obs16;
+    const int a = ids[i];
+    const int buf = st.cur[a], slot = st.fill[a];
+    const uint4 v = reinterpret_cast<const uint4*>(obs)[idx];
+    uint4* base = reinterpret_cast<uint4*>(st.obs);
+    base[(((int64_t)a * 2 + buf) * T1 + slot) * obs16 + q] = v;
+    if (slot == st.T) base[(((int64_t)a * 2 + (1 - buf)) * T1 + 0) * obs16 + q] = v;
+  }
+}
+
+// single block, blockDim >= n (n <= 1024): request order defines ring order
+__global__ void infer_store_record_kernel(int n, int U, const int32_t* __restrict__ ids,
+                                          const int32_t* __restrict__ action,
+                                          const int32_t* __restrict__ prev,
+                                          const float* __restrict__ reward,
+                                          const uint8_t* __restrict__ done,
+                                          const float* __restrict__ blp,
+                                          const float* __restrict__ hpre,
+                                          const float* __restrict__ cpre, seed_unroll_store st) {
+  const int i = threadIdx.x;
+  const int T1 = st.T + 1;
+  int a = 0, buf = 0, slot = 0;
+  bool completed = false;
+  if (i < n) {
+    a = ids[i];
+    buf = st.cur[a];
+    slot = st.fill[a];
+    completed = slot == st.T;
+  }
+  // block-wide exclusive prefix count of completions (request order)
+  __shared__ int warp_tot[32];
+  __shared__ int base_pos;
+  const int lane = i & 31, wid = i >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, completed);
+  const int within = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 0) warp_tot[wid] = __popc(bal);
+  if (i == 0) base_pos = st.ready_count[0];
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < wid; ++w) before += warp_tot[w];
+  if (i < n) {
+    const int64_t s0 = ((int64_t)a * 2 + buf) * T1 + slot;
+    st.action[s0] = action[i];
+    st.prev_action[s0] = prev[i];
+    st.reward[s0] = reward[i];
+    st.done[s0] = done[i];
+    st.behaviour_logp[s0] = blp[i];
+    if (slot == 0) {
+      for (int u = 0; u < U; ++u) {
+        st.h0[((int64_t)a * 2 + buf) * U + u] = hpre[(size_t)i * U + u];
+        st.c0[((int64_t)a * 2 + buf) * U + u] = cpre[(size_t)i * U + u];
+      }
+    }
+    if (completed) {
+      st.ready_ring[(base_pos + before + within) % st.ring_capacity] = a * 2 + buf;
+      const int nb = 1 - buf;
+      const int64_t d0 = ((int64_t)a * 2 + nb) * T1;
+      st.action[d0] = action[i];
+      st.prev_action[d0] = prev[i];
+      st.reward[d0] = reward[i];
+      st.done[d0] = done[i];
+      st.behaviour_logp[d0] = blp[i];
+      for (int u = 0; u < U; ++u) {   // state before slot T's step = before slot 0 (C19)
+        st.h0[((int64_t)a * 2 + nb) * U + u] = hpre[(size_t)i * U + u];
+        st.c0[((int64_t)a * 2 + nb) * U + u] = cpre[(size_t)i * U + u];
+      }
+      st.cur[a] = nb;
+      st.fill[a] = 1;
+    } else {
+      st.fill[a] = slot + 1;
+    }
+  }
+  __syncthreads();
+  if (i == 0) {
+    int tot = 0;
+    for (int w = 0; w < (n + 31) / 32; ++w) tot += warp_tot[w];
+    st.ready_count[0] = base_pos + tot;
+  }
+}
+
+// ------------------------------------------------------------------ assemble
+__global__ void assemble_kernel(seed_unroll_store st, int64_t obs16, int U, int B, seed_batch out) {
+  const int b = blockIdx.y;
+  const int T1 = st.T + 1;
+  const int consumed = st.ready_count[1];
+  const int e = st.ready_ring[(consumed + b) % st.ring_capacity];
+  const int a = e >> 1, buf = e & 1;
+  const int64_t src = ((int64_t)a * 2 + buf) * T1;
+  const uint4* so = reinterpret_cast<const uint4*>(st.obs) + src * obs16;
+  uint4* dob = reinterpret_cast<uint4*>(const_cast<void*>(out.obs)) + (int64_t)b * T1 * obs16;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < T1 * obs16;
+       q += (int64_t)gridDim.x * blockDim.x)
+    dob[q] = so[q];
+  if (blockIdx.x == 0) {
+    for (int t = threadIdx.x; t < T1; t += blockDim.x) {
+      const int64_t d = (int64_t)b * T1 + t;
+      const_cast<int32_t*>(out.action)[d] = st.action[src + t];
+      const_cast<int32_t*>(out.prev_action)[d] = st.prev_action[src + t];
+      const_cast<float*>(out.reward)[d] = st.reward[src + t];
+      const_cast<uint8_t*>(out.done)[d] = st.done[src + t];
+      const_cast<float*>(out.behaviour_logp)[d] = st.behaviour_logp[src + t];
+    }
+    for (int u = threadIdx.x; u < U; u += blockDim.x) {
+      const_cast<float*>(out.h0)[(int64_t)b * U + u] = st.h0[((int64_t)a * 2 + buf) * U + u];
+      const_cast<float*>(out.c0)[(int64_t)b * U + u] = st.c0[((int64_t)a * 2 + buf) * U + u];
+    }
+  }
+}
+
+__global__ void assemble_advance_kernel(int* ready_count, int B) { ready_count[1] += B; }
+
+}  // namespace seed
+
+using namespace seed;
+
+extern "C" seed_status seed_infer_workspace_size(const seed_net_spec* spec, int max_n,
+                                                 size_t* bytes) {
+  if (!bytes) return SEED_E_ARG;
+  NetPlan p;
+  SEED_TRY(make_net_plan(spec, &p));
+  if (p.kind != SEED_NET_ATARI_SHALLOW || !learner_supported(p)) return SEED_E_UNSUPPORTED;
+  if (max_n < 1 || max_n > 1024) return SEED_E_SHAPE;
+  InferWs w;
+  SEED_TRY(make_infer_ws(p, max_n, &w));
+  *bytes = w.total;
+  return SEED_OK;
+}
+
+extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_lowp,
+                                  const float* params, const seed_state_table* table, int n,
+                                  const int32_t* actor_ids, const uint8_t* obs,
+                                  const float* reward, const uint8_t* done,
+                                  const float* uniforms, uint64_t seed, uint64_t counter,
+                                  int32_t* action_out, float* blp_out, float* logits_out,
+                                  const seed_unroll_store* store, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  NetPlan p;
+  SEED_TRY(make_net_plan(spec, &p));
+  if (p.kind != SEED_NET_ATARI_SHALLOW || !learner_supported(p)) return SEED_E_UNSUPPORTED;
+  if (n < 1 || n > 1024) return SEED_E_SHAPE;
+  if (!params_lowp || !params || !table || !actor_ids || !obs || !reward || !done ||
+      !action_out || !blp_out || !ws || !table->h || !table->c || !table->last_action)
+    return SEED_E_ARG;
+  if (!aligned16(obs) || !aligned16(ws) || !aligned16(params_lowp)) return SEED_E_ARG;
+  InferWs w;
+  SEED_TRY(make_infer_ws(p, n, &w));
+  if (ws_bytes < w.total) return SEED_E_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* base = (uint8_t*)ws;
+  auto at = [&](size_t off) { return base + off; };
+  const bf16* lowp = (const bf16*)params_lowp;
+  const int U = p.U, A = p.A;
+  Geo g{p.H, p.W, p.C, p.oh1, p.ow1, p.oh2, p.ow2, p.fc_in, p.Kx, p.Kxp,
+        FastDiv((uint32_t)(p.oh1 * p.ow1)), FastDiv((uint32_t)p.ow1),
+        FastDiv((uint32_t)(p.oh2 * p.ow2)), FastDiv((uint32_t)p.ow2)};
+  float* splitk = (float*)at(w.splitk);
+  {
+    const int64_t tot = (int64_t)n * (U + p.Kxp - 256);
+    infer_pre_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(
+        n, A, U, p.Kxp, actor_ids, reward, done, table->h, table->c, table->last_action,
+        (float*)at(w.hpre), (float*)at(w.cpre), (int32_t*)at(w.prev), (bf16*)at(w.X));
+  }
+  {
+    const int64_t n16 = (int64_t)n * p.H * p.W * p.C / 16;
+    obs_to_bf16_kernel<<<(int)std::min<int64_t>((n16 + 255) / 256, 148 * 16), 256, 0, st>>>(
+        obs, (bf16*)at(w.obs_bf16), n16);
+  }
+  {
+    Conv1Fwd pr{};
+    pr.M = n * p.oh1 * p.ow1; pr.N = 16; pr.K = 64 * p.C; pr.g = g;
+    pr.obs = (const bf16*)at(w.obs_bf16); pr.w = lowp + p.im_conv1;
+    pr.bias = params + p.t[p.i_conv1b].off; pr.out = (bf16*)at(w.act1);
+    SEED_TRY(launch_gemm<16>(pr, pick_splits(pr.M, pr.N, 16, pr.K), st, splitk));
+  }
+  {
+    Conv2Fwd pr{};
+    pr.M = n * p.oh2 * p.ow2; pr.N = 32; pr.K = 256; pr.g = g;
+    pr.act1 = (const bf16*)at(w.act1); pr.w = lowp + p.im_conv2;
+    pr.bias = params + p.t[p.i_conv2b].off; pr.out = (bf16*)at(w.act2);
+    SEED_TRY(launch_gemm<32>(pr, pick_splits(pr.M, pr.N, 32, pr.K), st, splitk));
+  }
+  {
+    FcFwd pr{};
+    pr.M = n; pr.N = 256; pr.K = p.fc_in; pr.Kxp = p.Kxp;
+    pr.act2 = (const bf16*)at(w.act2); pr.w = lowp + p.im_fc;
+    pr.bias = params + p.t[p.i_fcb].off; pr.X = (bf16*)at(w.X);
+    SEED_TRY(launch_gemm<128>(pr, pick_splits(pr.M, pr.N, 128, pr.K), st, splitk));
+  }
+  {
+    XprojFwd pr{};
+    pr.M = n; pr.N = 4 * U; pr.K = p.Kxp;
+    pr.X = (const bf16*)at(w.X); pr.w = lowp + p.im_wx;
+    pr.bias = params + p.t[p.i_lb].off; pr.out = (float*)at(w.xproj);
+    SEED_TRY(launch_gemm<128>(pr, pick_splits(pr.M, pr.N, 128, pr.K), st, splitk));
+  }
+  {
+    LstmFwdArgs la{};
+    la.B = n; la.T1 = 1;
+    la.xproj = (const float*)at(w.xproj);
+    la.wh = lowp + p.im_wh;
+    la.h0 = table->h; la.c0 = table->c; la.state_rows = actor_ids;
+    la.done = done;
+    la.H = (float*)at(w.H);
+    la.hT = table->h; la.cT = table->c;
+    SEED_TRY(lstm_forward(la, st));
+  }
+  float* logits = logits_out ? logits_out : (float*)at(w.logits);
+  dense_fwd_f32<<<ceil_div(n * 32, 256), 256, 0, st>>>(
+      n, U, A + 1, (const float*)at(w.H), params + p.t[p.i_hw].off, params + p.t[p.i_hb].off,
+      logits, A, (float*)at(w.values), 0);
+  infer_sample_kernel<<<ceil_div(n * 32, 256), 256, 0, st>>>(
+      n, A, logits, uniforms, seed, counter, actor_ids, action_out, blp_out, table->last_action);
+  if (store) {
+    const int64_t obs16 = (int64_t)p.H * p.W * p.C / 16;
+    infer_store_obs_kernel<<<(int)std::min<int64_t>((n * obs16 + 255) / 256, 148 * 8), 256, 0,
+                             st>>>(n, obs16, obs, actor_ids, *store);
+    infer_store_record_kernel<<<1, ((n + 31) / 32) * 32, 0, st>>>(
+        n, U, actor_ids, action_out, (const int32_t*)at(w.prev), reward, done, blp_out,
+        (const float*)at(w.hpre), (const float*)at(w.cpre), *store);
+  }
+  return last_launch();
+}
+
+extern "C" seed_status seed_assemble_batch(const seed_unroll_store* store, int obs_bytes,
+                                           int lstm_units, int B, const seed_batch* out,
+                                           void* stream) {
+  if (!store || !out || B < 1 || obs_bytes <= 0 || obs_bytes % 16 || lstm_units < 1)
+    return SEED_E_ARG;
+  if (!out->obs || !out->action || !out->prev_action || !out->reward || !out->done ||
+      !out->behaviour_logp || !out->h0 || !out->c0)
+    return SEED_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t obs16 = obs_bytes / 16;
+  dim3 grid((unsigned)std::min<int64_t>((store->T + 1) * obs16 / 256 + 1, 64), B);
+  assemble_kernel<<<grid, 256, 0, st>>>(*store, obs16, lstm_units, B, *out);
+  assemble_advance_kernel<<<1, 1, 0, st>>>(store->ready_count, B);
+  return last_launch();
+}

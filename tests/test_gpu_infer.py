@@ -1,0 +1,171 @@
+"""GPU parity of seed_infer / seed_assemble_batch (H12, H13) against the oracle
+(bf16-emulated network, C26), the state-table semantics, the unroll
+store accounting (C17, C19) and the behaviour-fidelity self-consistency."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import seedgen
+
+pytestmark = pytest.mark.gpu
+NA, T, A = 48, 4, 18
+
+
+def _setup(seed=0, store=True, max_n=16):
+    import paper_1910_06591_b200 as S
+    spec = S.spec_for_config("c5")
+    ospec = O.spec_c2()
+    params = seedgen.glorot_params(O.param_layout(ospec), seed=seed + 3, bias_std=0.1)
+    learner = S.Learner(spec, T, 2, params)
+    srv = S.InferenceServer(spec, NA, max_n, learner=learner, T=T if store else None)
+    g = seedgen.rng(seed + 100)
+    h = (0.5 * g.standard_normal((NA, 256))).astype(np.float32)
+    c = (0.5 * g.standard_normal((NA, 256))).astype(np.float32)
+    la = g.integers(-1, A, NA).astype(np.int32)
+    srv.h.copy_(torch.from_numpy(h))
+    srv.c.copy_(torch.from_numpy(c))
+    srv.last_action.copy_(torch.from_numpy(la))
+    return S, srv, ospec, params
+
+
+def _call(srv, req, uniforms=True, seed=0, counter=0):
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in req.items()}
+    logits = torch.empty(len(req["actor_ids"]), A, device="cuda")
+    a, blp = srv.infer(d["actor_ids"], d["obs"], d["reward"], d["done"],
+                       d["uniforms"] if uniforms else None, seed=seed, counter=counter,
+                       logits_out=logits)
+    torch.cuda.synchronize()
+    return a.cpu().numpy(), blp.cpu().numpy(), logits.cpu().numpy()
+
+
+def _relL2(x, y):
+    return np.linalg.norm(np.asarray(x, np.float64) - y) / max(np.linalg.norm(y), 1e-30)
+
+
+def _near_boundary(logits, u, tol=2e-3):
+    p = np.exp(O.log_softmax(np.asarray(logits, np.float64)))
+    cdf = np.cumsum(p, axis=-1)
+    return np.any(np.abs(cdf - u[:, None]) < tol, axis=-1)
+
+
+@pytest.mark.parametrize("n", [1, 7, 16])
+def test_infer_parity_and_table(n):
+    S, srv, ospec, params = _setup(store=False)
+    th, tc, tla = (srv.h.cpu().numpy(), srv.c.cpu().numpy(), srv.last_action.cpu().numpy())
+    req = seedgen.infer_requests((84, 84, 4), A, NA, n, seed=5)
+    req["done"][: min(2, n)] = 1
+    a, blp, logits = _call(srv, req)
+    ra, rblp, rlg, rth, rtc, rtla = O.infer(ospec, params, th, tc, tla, req["actor_ids"],
+                                            req["obs"], req["reward"], req["done"],
+                                            req["uniforms"], emu=True)
+    assert _relL2(logits, rlg) < 2e-2
+    nb = _near_boundary(rlg, req["uniforms"].astype(np.float64))
+    assert np.all((a == ra) | nb), (a, ra)
+    ok = a == ra
+    np.testing.assert_allclose(blp[ok], rblp[ok], atol=2e-2 * max(1.0, np.abs(rblp).max()))
+    ids = req["actor_ids"]
+    assert _relL2(srv.h.cpu().numpy()[ids], rth[ids]) < 2e-2
+    assert _relL2(srv.c.cpu().numpy()[ids], rtc[ids]) < 2e-2
+    others = np.setdiff1d(np.arange(NA), ids)
+    np.testing.assert_array_equal(srv.h.cpu().numpy()[others], th[others])   # untouched, bitwise
+    np.testing.assert_array_equal(srv.c.cpu().numpy()[others], tc[others])
+    np.testing.assert_array_equal(srv.last_action.cpu().numpy()[ids], a)
+    np.testing.assert_array_equal(srv.last_action.cpu().numpy()[others], tla[others])
+
+
+def test_infer_philox_stream():
+    S, srv, ospec, params = _setup(store=False)
+    th, tc, tla = (srv.h.cpu().numpy(), srv.c.cpu().numpy(), srv.last_action.cpu().numpy())
+    req = seedgen.infer_requests((84, 84, 4), A, NA, 16, seed=9)
+    a, blp, logits = _call(srv, req, uniforms=False, seed=1234567, counter=42)
+    u = O.philox_uniforms(1234567, 42, req["actor_ids"])
+    ra, *_ = O.infer(ospec, params, th, tc, tla, req["actor_ids"], req["obs"], req["reward"],
+                     req["done"], u, emu=True)
+    p = np.exp(O.log_softmax(logits.astype(np.float64)))
+    cdf = np.cumsum(p, axis=-1)
+    expect = (u[:, None] < cdf).argmax(-1)      # GPU logits, oracle uniforms
+    nb = _near_boundary(logits, u)
+    assert np.all((a == expect) | nb)
+    assert np.all((a == ra) | _near_boundary(logits, u, 2e-2))
+
+
+def _batch_bufs(B, flat_obs=True):
+    shape = (B, T + 1, 84 * 84 * 4) if flat_obs else (B, T + 1, 84, 84, 4)
+    return dict(obs=torch.empty(*shape, dtype=torch.uint8, device="cuda"),
+                action=torch.empty(B, T + 1, dtype=torch.int32, device="cuda"),
+                prev_action=torch.empty(B, T + 1, dtype=torch.int32, device="cuda"),
+                reward=torch.empty(B, T + 1, device="cuda"),
+                done=torch.empty(B, T + 1, dtype=torch.uint8, device="cuda"),
+                behaviour_logp=torch.empty(B, T + 1, device="cuda"),
+                h0=torch.empty(B, 256, device="cuda"), c0=torch.empty(B, 256, device="cuda"))
+
+
+def test_unroll_store_and_assemble():
+    """Two unroll rounds over all actors: completed unrolls, overlap slot, h0
+    (C17, C19), deterministic ready-ring order, seed_assemble_batch (an unroll is
+    consumed before its buffer is reused T steps later)."""
+    S, srv, ospec, params = _setup(store=True, max_n=NA)
+    ref = O.UnrollStore(T=T, num_actors=NA)
+    completed = []          # (key, snapshot of slots, h0, c0) in completion order
+    consumed = 0
+    call = 0
+    for rnd in range(2):
+        ncalls = T + 1 if rnd == 0 else T
+        for _ in range(ncalls):
+            req = seedgen.infer_requests((84, 84, 4), A, NA, NA, seed=3, call_index=call)
+            call += 1
+            hpre = srv.h.cpu().numpy()[req["actor_ids"]]
+            cpre = srv.c.cpu().numpy()[req["actor_ids"]]
+            prev = srv.last_action.cpu().numpy()[req["actor_ids"]]
+            a, blp, _ = _call(srv, req)
+            for i, act in enumerate(req["actor_ids"]):
+                rec = dict(obs=req["obs"][i], action=a[i], prev=prev[i], reward=req["reward"][i],
+                           done=req["done"][i], blp=blp[i])
+                before = len(ref.ready)
+                ref.record(int(act), rec, hpre[i], cpre[i])
+                if len(ref.ready) > before:
+                    key = ref.ready[-1]
+                    st = ref.steps[key]
+                    completed.append((key, list(st["slots"]), st["h0"].copy(), st["c0"].copy()))
+        cnt = srv.st["ready_count"].cpu().numpy()
+        assert cnt[0] == len(completed) == NA * (rnd + 1)
+        ring = srv.st["ready_ring"].cpu().numpy()[consumed: cnt[0]]
+        assert [(e >> 1, e & 1) for e in ring] == [k for k, *_ in completed[consumed:]]
+        B = NA
+        out = _batch_bufs(B)
+        srv.assemble(B, out)
+        torch.cuda.synchronize()
+        assert srv.st["ready_count"].cpu().numpy()[1] == consumed + B
+        for b in range(B):
+            key, slots, h0, c0 = completed[consumed + b]
+            assert len(slots) == T + 1
+            np.testing.assert_array_equal(out["obs"][b].cpu().numpy(),
+                                          np.stack([s["obs"].reshape(-1) for s in slots]))
+            for f, k in (("action", "action"), ("prev_action", "prev"), ("done", "done"),
+                         ("reward", "reward"), ("behaviour_logp", "blp")):
+                np.testing.assert_array_equal(out[f][b].cpu().numpy(), [s[k] for s in slots])
+            np.testing.assert_array_equal(out["h0"][b].cpu().numpy(), h0)
+            np.testing.assert_array_equal(out["c0"][b].cpu().numpy(), c0)
+        consumed += B
+
+
+def test_behaviour_fidelity_self_consistency():
+    """S:466 / SURVEY §4.4: with frozen params, the learner forward on an assembled
+    unroll reproduces the behaviour log-probs recorded at inference (ratio == 1)."""
+    S, srv, ospec, params = _setup(store=True, max_n=NA)
+    for call in range(T + 1):
+        req = seedgen.infer_requests((84, 84, 4), A, NA, NA, seed=11, call_index=call)
+        _call(srv, req)
+    B = NA
+    out = _batch_bufs(B, flat_obs=False)
+    srv.assemble(B, out)
+    L = S.Learner(S.spec_for_config("c2"), T, B, params, S.HParams(lr=0.0))
+    L.step(out)
+    torch.cuda.synchronize()
+    logits = L.outputs()[0].cpu().numpy().astype(np.float64)
+    logp = O.log_softmax(logits)
+    act = out["action"].cpu().numpy()
+    tlp = np.take_along_axis(logp, act[:, :, None], 2)[:, :, 0]
+    blp = out["behaviour_logp"].cpu().numpy()
+    assert np.max(np.abs(tlp - blp)) < 1e-4, np.max(np.abs(tlp - blp))

@@ -490,3 +490,12 @@ def test_emulated_oracle_stays_close_to_exact():
     lx, vx, _ = O.network_forward(spec, P, batch, emu=False)
     assert np.linalg.norm(le - lx) / np.linalg.norm(lx) < 2e-2
     assert np.linalg.norm(ve - vx) / np.linalg.norm(vx) < 2e-2
+
+
+def test_philox4x32_10_known_answers():
+    g = _gold("philox4x32_10_kat.json")
+    for v in g["vectors"]:
+        out = O.philox4x32_10([int(x, 16) for x in v["ctr"]], [int(x, 16) for x in v["key"]])
+        assert [int(x) for x in out] == [int(x, 16) for x in v["out"]]
+    u = O.philox_uniforms(7, 3, np.arange(1000))
+    assert np.all((u >= 0) & (u < 1)) and abs(u.mean() - 0.5) < 0.05
