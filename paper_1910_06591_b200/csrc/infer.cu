@@ -366,9 +366,8 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
     SEED_TRY(lstm_forward(la, st));
   }
   float* logits = logits_out ? logits_out : (float*)at(w.logits);
-  dense_fwd_f32<<<ceil_div(n * 32, 256), 256, 0, st>>>(
-      n, U, A + 1, (const float*)at(w.H), params + p.t[p.i_hw].off, params + p.t[p.i_hb].off,
-      logits, A, (float*)at(w.values), 0);
+  SEED_TRY(launch_dense_fwd(n, U, A + 1, (const float*)at(w.H), params + p.t[p.i_hw].off,
+                            params + p.t[p.i_hb].off, logits, A, (float*)at(w.values), 0, st));
   infer_sample_kernel<<<ceil_div(n * 32, 256), 256, 0, st>>>(
       n, A, logits, uniforms, seed, counter, actor_ids, action_out, blp_out, table->last_action);
   if (store) {

@@ -16,7 +16,7 @@
 //   dW_fc|b  GEMM [256 x F] . [F x 2600]    (ones column -> bias grad)
 //   dY2    GEMM  [F x 256] . [256 x 2592]   (ReLU mask)
 //   dW2    GEMM  [256 x F*81] . [F*81 x 32] (split-K)
-//   dY1    implicit transposed-conv GEMM [F*400 x 512] . [512 x 16] (ReLU mask)
+//   dY1    sub-pixel transposed-conv GEMM [4*F*100 x 128] . [128 x 4*16] (ReLU mask)
 //   dW1    GEMM  [256 x F*400] . [F*400 x 16] (split-K, /255)
 //   conv biases: deterministic column sums
 //   [allreduce] -> global-norm clip + Adam -> bf16 operand image refresh
@@ -129,9 +129,9 @@ static seed_status shallow_forward(const StepCtx& c, const seed_batch* bt, const
   la.hT = la.cT = nullptr;
   SEED_TRY(lstm_forward(la, st));
   c.mark("lstm_fwd");
-  dense_fwd_f32<<<ceil_div(F * 32, 256), 256, 0, st>>>(
-      F, p.U, p.A + 1, c.at<float>(w.H), params + p.t[p.i_hw].off, params + p.t[p.i_hb].off,
-      c.at<float>(w.logits), p.A, c.at<float>(w.values), 0);
+  SEED_TRY(launch_dense_fwd(F, p.U, p.A + 1, c.at<float>(w.H), params + p.t[p.i_hw].off,
+                            params + p.t[p.i_hb].off, c.at<float>(w.logits), p.A,
+                            c.at<float>(w.values), 0, st));
   c.mark("heads_fwd");
   return last_launch();
 }
@@ -142,9 +142,8 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
   const LearnerWs& w = c.w;
   const int F = w.F, U = p.U, A = p.A;
   // heads
-  dense_dgrad_f32<<<ceil_div(F * U, 256), 256, 0, st>>>(
-      F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), params + p.t[p.i_hw].off,
-      nullptr, c.at<float>(w.dH));
+  SEED_TRY(launch_dense_dgrad(F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues),
+                              params + p.t[p.i_hw].off, nullptr, c.at<float>(w.dH), st));
   dense_wgrad_f32<<<dim3(A + 1, ceil_div(U + 1, 32)), 256, 0, st>>>(
       F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), c.at<float>(w.H),
       grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off);
@@ -196,13 +195,17 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
   }
   SEED_TRY(colsum_bf16(c.at<bf16>(w.dY2), (int64_t)F * p.oh2 * p.ow2, 32,
                        c.at<float>(w.colsum_part), grads + p.t[p.i_conv2b].off, st));
-  c.mark("conv2_bias", 2);
+  c.mark("conv2_bias");
   {
     Conv2Dgrad pr{};
-    pr.M = F * p.oh1 * p.ow1; pr.N = 16; pr.K = 512; pr.g = c.g;  // k = (ky, kx, co)
+    const int QH = (p.oh1 + 1) / 2, QW = (p.ow1 + 1) / 2;
+    pr.F = F; pr.QH = QH; pr.QW = QW;
+    pr.fcls = FastDiv((uint32_t)(F * QH * QW)); pr.fq = FastDiv((uint32_t)(QH * QW));
+    pr.fqw = FastDiv((uint32_t)QW);
+    pr.M = 4 * F * QH * QW; pr.N = 64; pr.K = 128; pr.g = c.g;   // k = (kyi, kxi, co)
     pr.dY2 = c.at<bf16>(w.dY2); pr.wdg = lowp + p.im_conv2dg; pr.act1 = c.at<bf16>(w.act1);
     pr.dY1 = c.at<bf16>(w.dY1);
-    SEED_TRY(gemm<16>(c, pr, st, "conv2_dgrad"));
+    SEED_TRY(gemm<64>(c, pr, st, "conv2_dgrad"));
   }
   {
     Conv1Wgrad pr{};
@@ -213,7 +216,7 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
   }
   SEED_TRY(colsum_bf16(c.at<bf16>(w.dY1), (int64_t)F * p.oh1 * p.ow1, 16,
                        c.at<float>(w.colsum_part), grads + p.t[p.i_conv1b].off, st));
-  c.mark("conv1_bias", 2);
+  c.mark("conv1_bias");
   return SEED_OK;
 }
 
@@ -222,14 +225,13 @@ static seed_status mlp_forward(const StepCtx& c, const seed_batch* bt, const flo
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
   const int F = w.F;
-  const int blocks = ceil_div(F * 32, 256);
-  dense_fwd_f32<<<blocks, 256, 0, st>>>(F, p.D, 64, (const float*)bt->obs, params + p.t[p.i_m0w].off,
-                                        params + p.t[p.i_m0b].off, c.at<float>(w.h1), 64, nullptr, 1);
-  dense_fwd_f32<<<blocks, 256, 0, st>>>(F, 64, 64, c.at<float>(w.h1), params + p.t[p.i_m1w].off,
-                                        params + p.t[p.i_m1b].off, c.at<float>(w.h2), 64, nullptr, 1);
-  dense_fwd_f32<<<blocks, 256, 0, st>>>(F, 64, p.A + 1, c.at<float>(w.h2), params + p.t[p.i_hw].off,
-                                        params + p.t[p.i_hb].off, c.at<float>(w.logits), p.A,
-                                        c.at<float>(w.values), 0);
+  SEED_TRY(launch_dense_fwd(F, p.D, 64, (const float*)bt->obs, params + p.t[p.i_m0w].off,
+                            params + p.t[p.i_m0b].off, c.at<float>(w.h1), 64, nullptr, 1, st));
+  SEED_TRY(launch_dense_fwd(F, 64, 64, c.at<float>(w.h1), params + p.t[p.i_m1w].off,
+                            params + p.t[p.i_m1b].off, c.at<float>(w.h2), 64, nullptr, 1, st));
+  SEED_TRY(launch_dense_fwd(F, 64, p.A + 1, c.at<float>(w.h2), params + p.t[p.i_hw].off,
+                            params + p.t[p.i_hb].off, c.at<float>(w.logits), p.A,
+                            c.at<float>(w.values), 0, st));
   c.mark("mlp_fwd", 3);
   return last_launch();
 }
@@ -239,15 +241,13 @@ static seed_status mlp_backward(const StepCtx& c, const seed_batch* bt, const fl
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
   const int F = w.F, A = p.A;
-  dense_dgrad_f32<<<ceil_div(F * 64, 256), 256, 0, st>>>(
-      F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), params + p.t[p.i_hw].off,
-      c.at<float>(w.h2), c.at<float>(w.dh2));
+  SEED_TRY(launch_dense_dgrad(F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues),
+                              params + p.t[p.i_hw].off, c.at<float>(w.h2), c.at<float>(w.dh2), st));
   dense_wgrad_f32<<<dim3(A + 1, ceil_div(65, 32)), 256, 0, st>>>(
       F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), c.at<float>(w.h2),
       grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off);
-  dense_dgrad_f32<<<ceil_div(F * 64, 256), 256, 0, st>>>(
-      F, 64, 64, c.at<float>(w.dh2), 64, nullptr, params + p.t[p.i_m1w].off, c.at<float>(w.h1),
-      c.at<float>(w.dh1));
+  SEED_TRY(launch_dense_dgrad(F, 64, 64, c.at<float>(w.dh2), 64, nullptr,
+                              params + p.t[p.i_m1w].off, c.at<float>(w.h1), c.at<float>(w.dh1), st));
   dense_wgrad_f32<<<dim3(64, ceil_div(65, 32)), 256, 0, st>>>(
       F, 64, 64, c.at<float>(w.dh2), 64, nullptr, c.at<float>(w.h1), grads + p.t[p.i_m1w].off,
       grads + p.t[p.i_m1b].off);
@@ -301,6 +301,8 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   const float* params = state->params;
   const bf16* lowp = (const bf16*)state->params_lowp;
   float* grads = state->grads;
+  // column-sum completion ticket (re-armed by the kernel after each use)
+  SEED_CUDA_TRY(cudaMemsetAsync(c.at<float>(c.w.colsum_part) + COLSUM_BLOCKS * 64, 0, 16, st));
 
   if (p.kind == SEED_NET_MLP) SEED_TRY(mlp_forward(c, batch, params, st));
   else SEED_TRY(shallow_forward(c, batch, lowp, params, st));
@@ -336,12 +338,11 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   aa.lr = hp->lr; aa.beta1 = hp->beta1; aa.beta2 = hp->beta2; aa.eps = hp->eps;
   aa.max_norm = hp->max_grad_norm; aa.loss_part = c.at<float>(c.w.loss_part); aa.B = B;
   aa.metrics = metrics;
+  aa.lowp = (bf16*)state->params_lowp;
+  aa.nimg = p.nimg;
+  for (int k = 0; k < p.nimg; ++k) aa.img[k] = p.img[k];
   SEED_TRY(launch_clip_adam(aa, st));
   c.mark("clip_adam");
-  if (p.nimg) {
-    SEED_TRY(refresh_lowp(p, state->params, state->params_lowp, st));
-    c.mark("lowp_refresh", p.nimg);
-  }
   return last_launch();
 }
 

@@ -1,32 +1,51 @@
 // learner_kernels.cu — see learner_kernels.cuh.
+#include <algorithm>
 #include "learner_kernels.cuh"
 #include "net.cuh"
 
 namespace seed {
 
-__global__ void dense_fwd_f32(int R, int I, int O, const float* __restrict__ X,
-                              const float* __restrict__ W, const float* __restrict__ b,
-                              float* __restrict__ Y, int ldy, float* __restrict__ Yv, int relu) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= R) return;
-  const float* x = X + (size_t)warp * I;
-  float xv[8];
-  const int nq = (I + 31) / 32;  // I <= 256
+// Warp per row, lane = output (O <= 64: two outputs per lane), row staged in
+// shared memory, weights staged transposed [I][O] (conflict-free), 4 partial
+// accumulators per output.  I <= 256.
+__global__ void __launch_bounds__(256) dense_fwd_f32(int R, int I, int O, const float* __restrict__ X,
+                                                     const float* __restrict__ W,
+                                                     const float* __restrict__ b,
+                                                     float* __restrict__ Y, int ldy,
+                                                     float* __restrict__ Yv, int relu) {
+  extern __shared__ float shf[];
+  float* Wt = shf;                  // [I][O]
+  float* xs = shf + I * O;          // [8][I]
+  for (int q = threadIdx.x; q < I * O; q += blockDim.x) {
+    const int o = q / I, i = q % I;
+    Wt[i * O + o] = W[q];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* xw = xs + warp * I;
+  for (int r = blockIdx.x * 8 + warp; r < R; r += gridDim.x * 8) {
+    for (int i = lane; i < I; i += 32) xw[i] = X[(size_t)r * I + i];
+    __syncwarp();
 #pragma unroll
-  for (int q = 0; q < 8; ++q) xv[q] = (q < nq && lane + 32 * q < I) ? x[lane + 32 * q] : 0.f;
-  for (int o = 0; o < O; ++o) {
-    const float* w = W + (size_t)o * I;
-    float s = 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q < nq && lane + 32 * q < I) s += xv[q] * w[lane + 32 * q];
-    s = warp_sum(s);
-    if (lane == 0) {
-      float y = s + b[o];
-      if (relu) y = fmaxf(y, 0.f);
-      if (Yv && o == O - 1) Yv[warp] = y;
-      else Y[(size_t)warp * ldy + o] = y;
+    for (int h = 0; h < 2; ++h) {
+      const int o = lane + 32 * h;
+      if (o < O) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        int i = 0;
+        for (; i + 3 < I; i += 4) {
+          a0 += xw[i] * Wt[i * O + o];
+          a1 += xw[i + 1] * Wt[(i + 1) * O + o];
+          a2 += xw[i + 2] * Wt[(i + 2) * O + o];
+          a3 += xw[i + 3] * Wt[(i + 3) * O + o];
+        }
+        for (; i < I; ++i) a0 += xw[i] * Wt[i * O + o];
+        float y = ((a0 + a1) + (a2 + a3)) + b[o];
+        if (relu) y = fmaxf(y, 0.f);
+        if (Yv && o == O - 1) Yv[r] = y;
+        else Y[(size_t)r * ldy + o] = y;
+      }
     }
+    __syncwarp();
   }
 }
 
@@ -34,16 +53,37 @@ __device__ __forceinline__ float dy_at(const float* dy, int ldy, const float* dv
   return (dv && o == ldy) ? dv[r] : dy[(size_t)r * ldy + o];
 }
 
-__global__ void dense_dgrad_f32(int R, int I, int O, const float* __restrict__ dy, int ldy,
-                                const float* __restrict__ dv, const float* __restrict__ W,
-                                const float* __restrict__ mask, float* __restrict__ dX) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)R * I) return;
-  const int r = (int)(idx / I), i = (int)(idx % I);
-  float s = 0.f;
-  for (int o = 0; o < O; ++o) s += dy_at(dy, ldy, dv, r, o) * W[(size_t)o * I + i];
-  if (mask && !(mask[idx] > 0.f)) s = 0.f;
-  dX[idx] = s;
+// block = 8 rows x all I columns; W [O][I] and the 8 dY rows staged in shared memory
+__global__ void __launch_bounds__(256) dense_dgrad_f32(int R, int I, int O, const float* __restrict__ dy,
+                                                       int ldy, const float* __restrict__ dv,
+                                                       const float* __restrict__ W,
+                                                       const float* __restrict__ mask,
+                                                       float* __restrict__ dX) {
+  extern __shared__ float shf[];
+  float* Ws = shf;              // [O][I]
+  float* ds = shf + O * I;      // [8][O]
+  for (int q = threadIdx.x; q < O * I; q += blockDim.x) Ws[q] = W[q];
+  const int r0 = blockIdx.x * 8;
+  for (int q = threadIdx.x; q < 8 * O; q += blockDim.x) {
+    const int rr = r0 + q / O, o = q % O;
+    ds[q] = rr < R ? dy_at(dy, ldy, dv, rr, o) : 0.f;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 8 * I; q += blockDim.x) {
+    const int rl = q / I, i = q % I, r = r0 + rl;
+    if (r >= R) continue;
+    float s0 = 0.f, s1 = 0.f;
+    int o = 0;
+    for (; o + 1 < O; o += 2) {
+      s0 += ds[rl * O + o] * Ws[o * I + i];
+      s1 += ds[rl * O + o + 1] * Ws[(o + 1) * I + i];
+    }
+    if (o < O) s0 += ds[rl * O + o] * Ws[o * I + i];
+    float sres = s0 + s1;
+    const size_t idx = (size_t)r * I + i;
+    if (mask && !(mask[idx] > 0.f)) sres = 0.f;
+    dX[idx] = sres;
+  }
 }
 
 // grid (O, ceil((I+1)/32)), block 256 = 32 columns x 8 row groups; each thread
@@ -82,115 +122,132 @@ __global__ void __launch_bounds__(256) dense_wgrad_f32(int R, int I, int O, cons
   }
 }
 
+seed_status launch_dense_fwd(int R, int I, int O, const float* X, const float* W, const float* b,
+                             float* Y, int ldy, float* Yv, int relu, cudaStream_t st) {
+  if (I > 256 || O > 64) return SEED_E_SHAPE;
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(dense_fwd_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (256 * 64 + 8 * 256) * 4));
+    attr = true;
+  }
+  const size_t smem = (size_t)(I * O + 8 * I) * 4;
+  const int blocks = std::min(ceil_div(R, 8), 148 * 4);
+  dense_fwd_f32<<<blocks, 256, smem, st>>>(R, I, O, X, W, b, Y, ldy, Yv, relu);
+  return last_launch();
+}
+
+seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, const float* dv,
+                               const float* W, const float* mask, float* dX, cudaStream_t st) {
+  if (I > 256 || O > 64) return SEED_E_SHAPE;
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(dense_dgrad_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (256 * 64 + 8 * 64) * 4));
+    attr = true;
+  }
+  const size_t smem = (size_t)(O * I + 8 * O) * 4;
+  dense_dgrad_f32<<<ceil_div(R, 8), 256, smem, st>>>(R, I, O, dy, ldy, dv, W, mask, dX);
+  return last_launch();
+}
+
 // ------------------------------------------------------------------ K2 policy loss
-// Group of G lanes per trajectory; lane owns 4 consecutive trained steps of a
-// chunk (the vtrace_chunk scheme), computes log-softmax / target log-prob /
-// entropy of its steps, feeds the V-trace scan, then writes the output
-// gradients (H7 closed forms) and its share of the loss sums.
-template <int G>
+// One block per trajectory b (T <= 256):
+//  1. warps compute the per-step policy statistics (lane = action): log-sum-exp,
+//     target log-prob, entropy H_t (H5);
+//  2. warp 0 runs the V-trace scan (vtrace_chunk, 4 steps per lane, H6) and the
+//     loss sums;
+//  3. all threads write the closed-form output gradients (H7).
 __global__ void __launch_bounds__(256) policy_loss_kernel(const LossArgs a) {
-  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int lane = threadIdx.x % G;
-  const bool active = gid < a.B;
-  const int b = active ? gid : a.B - 1;
+  __shared__ float s_lse[256], s_tlp[256], s_H[256], s_vs[256], s_pg[256];
+  const int b = blockIdx.x;
   const int T = a.T, T1 = a.T + 1, A = a.A;
   const size_t row0 = (size_t)b * T1;
-  VtraceLaneState st;
-  st.init(a.values[row0 + T]);
-  bool bad = !isfinite(st.carry_vs);
-  float sum_pg = 0.f, sum_b = 0.f, sum_h = 0.f;
-  const int CH = 4 * G;
-  const int nch = (T + CH - 1) / CH;
-  for (int ch = nch - 1; ch >= 0; --ch) {
-    const int t0 = ch * CH + 4 * lane;
-    float d[4], r[4], g[4], v[4], tl[4], H[4], lse4[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int t = t0 + j;
-      d[j] = r[j] = g[j] = v[j] = tl[j] = H[j] = lse4[j] = 0.f;
-      if (t < T) {
-        const float* z = a.logits + (row0 + t) * A;
-        float mx = -INFINITY;
-        for (int k = 0; k < A; ++k) mx = fmaxf(mx, z[k]);
-        float se = 0.f;
-        for (int k = 0; k < A; ++k) se += expf(z[k] - mx);
-        const float lse = mx + logf(se);
-        float h = 0.f;
-        for (int k = 0; k < A; ++k) {
-          const float lp = z[k] - lse;
-          h -= expf(lp) * lp;
-        }
-        const int act = a.action[row0 + t];
-        tl[j] = z[act] - lse;
-        lse4[j] = lse;
-        H[j] = h;
-        d[j] = tl[j] - a.blp[row0 + t];
-        r[j] = a.reward[row0 + t + 1];
-        g[j] = a.discount * (a.done[row0 + t + 1] ? 0.f : 1.f);
-        v[j] = a.values[row0 + t];
-      }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = warp; t < T; t += 8) {
+    const float z = lane < A ? a.logits[(row0 + t) * A + lane] : -INFINITY;
+    const float mx = warp_max(z);
+    const float e = lane < A ? expf(z - mx) : 0.f;
+    const float se = warp_sum(e);
+    const float lse = mx + logf(se);
+    const float lp = z - lse;
+    const float H = -warp_sum(lane < A ? expf(lp) * lp : 0.f);
+    const int act = a.action[row0 + t];
+    const float tl = __shfl_sync(0xffffffffu, lp, act & 31);
+    if (lane == 0) {
+      s_lse[t] = lse;
+      s_tlp[t] = tl;
+      s_H[t] = H;
     }
-    float vs[4], pg[4];
-    bad |= vtrace_chunk<G>(st, lane, t0, T, d, r, g, v, a.rho_bar, a.c_bar, a.lam, vs, pg);
-    if (active) {
+  }
+  __syncthreads();
+  if (warp == 0) {
+    VtraceLaneState st;
+    st.init(a.values[row0 + T]);
+    bool bad = !isfinite(st.carry_vs);
+    float sum_pg = 0.f, sum_b = 0.f, sum_h = 0.f;
+    const int nch = (T + 127) / 128;
+    for (int ch = nch - 1; ch >= 0; --ch) {
+      const int t0 = ch * 128 + 4 * lane;
+      float d[4], r[4], g[4], v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = t0 + j;
+        d[j] = r[j] = g[j] = v[j] = 0.f;
+        if (t < T) {
+          d[j] = s_tlp[t] - a.blp[row0 + t];
+          r[j] = a.reward[row0 + t + 1];
+          g[j] = a.discount * (a.done[row0 + t + 1] ? 0.f : 1.f);
+          v[j] = a.values[row0 + t];
+        }
+      }
+      float vs[4], pg[4];
+      bad |= vtrace_chunk<32>(st, lane, t0, T, d, r, g, v, a.rho_bar, a.c_bar, a.lam, vs, pg);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int t = t0 + j;
         if (t >= T) continue;
+        s_vs[t] = vs[j];
+        s_pg[t] = pg[j];
         a.vs[(size_t)b * T + t] = vs[j];
         a.pg[(size_t)b * T + t] = pg[j];
-        sum_pg += -pg[j] * tl[j];
-        sum_b += (vs[j] - v[j]) * (vs[j] - v[j]);
-        sum_h += H[j];
         a.dvalues[row0 + t] = a.scale * a.vf_coef * (v[j] - vs[j]);
-        const float* z = a.logits + (row0 + t) * A;
-        float* dz = a.dlogits + (row0 + t) * A;
-        const int act = a.action[row0 + t];
-        for (int k = 0; k < A; ++k) {
-          const float lp = z[k] - lse4[j];  // log pi(k | x_t)
-          const float p = expf(lp);
-          const float onehot = (k == act) ? 1.f : 0.f;
-          dz[k] = a.scale * (-pg[j] * (onehot - p) + a.ent_coef * p * (lp + H[j]));
-        }
+        sum_pg += -pg[j] * s_tlp[t];
+        sum_b += (vs[j] - v[j]) * (vs[j] - v[j]);
+        sum_h += s_H[t];
       }
     }
+    sum_pg = warp_sum(sum_pg);
+    sum_b = warp_sum(sum_b);
+    sum_h = warp_sum(sum_h);
+    const unsigned anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      float* pp = a.part + (size_t)b * 4;
+      pp[0] = a.scale * sum_pg;
+      pp[1] = a.scale * 0.5f * a.vf_coef * sum_b;
+      pp[2] = -a.scale * a.ent_coef * sum_h;
+      pp[3] = anybad ? 1.f : 0.f;
+      a.dvalues[row0 + T] = 0.f;   // bootstrap is a constant (C4)
+    }
   }
-  // row T: no loss term, zero gradients (bootstrap is a constant, C4)
-  if (active) {
-    for (int k = lane; k < A; k += G) a.dlogits[(row0 + T) * A + k] = 0.f;
-    if (lane == 0) a.dvalues[row0 + T] = 0.f;
+  __syncthreads();
+  for (int q = threadIdx.x; q < T1 * A; q += blockDim.x) {
+    const int t = q / A, k = q % A;
+    const size_t idx = (row0 + t) * A + k;
+    if (t == T) {
+      a.dlogits[idx] = 0.f;
+      continue;
+    }
+    const float lp = a.logits[idx] - s_lse[t];
+    const float p = expf(lp);
+    const float onehot = (k == a.action[row0 + t]) ? 1.f : 0.f;
+    a.dlogits[idx] = a.scale * (-s_pg[t] * (onehot - p) + a.ent_coef * p * (lp + s_H[t]));
   }
-#pragma unroll
-  for (int off = G / 2; off > 0; off >>= 1) {
-    sum_pg += __shfl_xor_sync(0xffffffffu, sum_pg, off, G);
-    sum_b += __shfl_xor_sync(0xffffffffu, sum_b, off, G);
-    sum_h += __shfl_xor_sync(0xffffffffu, sum_h, off, G);
-  }
-  const unsigned anybad = __any_sync(0xffffffffu, bad);  // warp-wide is fine: flag only
-  if (active && lane == 0) {
-    float* pp = a.part + (size_t)b * 4;
-    pp[0] = a.scale * sum_pg;
-    pp[1] = a.scale * 0.5f * a.vf_coef * sum_b;
-    pp[2] = -a.scale * a.ent_coef * sum_h;
-    pp[3] = anybad ? 1.f : 0.f;
-  }
-}
-
-template <int G>
-static void launch_loss_g(const LossArgs& a, cudaStream_t st) {
-  const long long threads = (long long)a.B * G;
-  policy_loss_kernel<G><<<(int)((threads + 255) / 256), 256, 0, st>>>(a);
 }
 
 seed_status launch_policy_loss(const LossArgs& a, cudaStream_t st) {
-  switch (vtrace_group_size(a.T)) {
-    case 1: launch_loss_g<1>(a, st); break;
-    case 2: launch_loss_g<2>(a, st); break;
-    case 4: launch_loss_g<4>(a, st); break;
-    case 8: launch_loss_g<8>(a, st); break;
-    case 16: launch_loss_g<16>(a, st); break;
-    default: launch_loss_g<32>(a, st); break;
-  }
+  if (a.T > 256 || a.A > 32) return SEED_E_SHAPE;
+  policy_loss_kernel<<<a.B, 256, 0, st>>>(a);
   return last_launch();
 }
 
@@ -211,40 +268,59 @@ __global__ void core_extras_kernel(int F, int A, int Kxp, const int32_t* __restr
 }
 
 // ------------------------------------------------------------------ column sums
-__global__ void colsum_part_kernel(const __nv_bfloat16* __restrict__ X, int64_t R, int C,
-                                   float* __restrict__ part) {
-  // blockDim 256: thread (rl, c) with rl in [0, 256/C)
-  const int RL = 256 / C;
-  const int c = threadIdx.x % C, rl = threadIdx.x / C;
+// out[c] = sum_r X[r][c] (bf16 X, C in {16, 32}): each block sums a contiguous row
+// range with 16-byte loads (8 columns per thread), writes its partial, and the
+// last block to finish (integer ticket) adds the partials in block order —
+// deterministic, one launch.
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ X, int64_t R,
+                                                     int C, float* __restrict__ part,
+                                                     unsigned* ticket, float* __restrict__ out) {
+  const int G = C / 8;                         // 16-byte groups per row
+  const int RL = 256 / G;                      // rows in flight per block
+  const int grp = threadIdx.x % G, rl = threadIdx.x / G;
   const int64_t per = (R + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = blockIdx.x * per, r1 = min(R, r0 + per);
-  float s = 0.f;
-  if (rl < RL)
-    for (int64_t r = r0 + rl; r < r1; r += RL) s += __bfloat162float(X[r * C + c]);
-  __shared__ float sh[256];
-  sh[threadIdx.x] = s;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int64_t r = r0 + rl; r < r1; r += RL) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(X + r * C) + grp);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      acc[2 * q] += bf16_lo(w[q]);
+      acc[2 * q + 1] += bf16_hi(w[q]);
+    }
+  }
+  __shared__ float sh[256][9];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) sh[threadIdx.x][q] = acc[q];
   __syncthreads();
   if (threadIdx.x < C) {
+    const int c = threadIdx.x, g0 = c / 8, e = c % 8;
     float t = 0.f;
-    for (int k = 0; k < RL; ++k) t += sh[k * C + threadIdx.x];
-    part[blockIdx.x * C + threadIdx.x] = t;
+    for (int k = 0; k < RL; ++k) t += sh[k * G + g0][e];
+    part[blockIdx.x * C + c] = t;
   }
-}
-
-__global__ void colsum_final_kernel(const float* __restrict__ part, int nb, int C,
-                                    float* __restrict__ out) {
-  const int c = threadIdx.x;
-  if (c >= C) return;
-  float s = 0.f;
-  for (int k = 0; k < nb; ++k) s += part[k * C + c];
-  out[c] = s;
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < C) {
+    __threadfence();
+    float t = 0.f;
+    for (int k = 0; k < (int)gridDim.x; ++k) t += part[k * C + threadIdx.x];
+    out[threadIdx.x] = t;
+    if (threadIdx.x == 0) *ticket = 0;   // re-arm for the next use
+  }
 }
 
 seed_status colsum_bf16(const __nv_bfloat16* X, int64_t R, int C, float* part, float* out,
                         cudaStream_t st) {
-  if (C > 64 || 256 % C) return SEED_E_SHAPE;
-  colsum_part_kernel<<<COLSUM_BLOCKS, 256, 0, st>>>(X, R, C, part);
-  colsum_final_kernel<<<1, 64, 0, st>>>(part, COLSUM_BLOCKS, C, out);
+  if (C % 8 || C > 64) return SEED_E_SHAPE;
+  unsigned* ticket = reinterpret_cast<unsigned*>(part + COLSUM_BLOCKS * 64);
+  colsum_kernel<<<COLSUM_BLOCKS, 256, 0, st>>>(X, R, C, part, ticket, out);
   return last_launch();
 }
 
@@ -270,7 +346,30 @@ __global__ void grad_norm_kernel(const float* __restrict__ g, int64_t P, double*
   }
 }
 
-__global__ void adam_kernel(const AdamArgs a) {
+// bf16 operand images of the updated parameters (net.cuh LowpImg), written by
+// the Adam kernel so no separate refresh pass is needed.
+__device__ __forceinline__ void lowp_write(const AdamArgs& a, int64_t i, float v) {
+  for (int k = 0; k < a.nimg; ++k) {
+    const LowpImg& m = a.img[k];
+    const int64_t n = (int64_t)m.rows * m.cols;
+    const int64_t e = i - m.src;
+    if (e < 0 || e >= n) continue;
+    int64_t dst;
+    if (m.kind == IMG_COPY_PAD) {
+      dst = (e / m.cols) * m.ld + (e % m.cols);
+    } else {  // src [CO][KH][KW][CI] -> dst [CI][KH][KW][CO]
+      const int ci = (int)(e % m.d3);
+      int64_t q = e / m.d3;
+      const int kx = (int)(q % m.d2); q /= m.d2;
+      const int ky = (int)(q % m.d1);
+      const int co = (int)(q / m.d1);
+      dst = (((int64_t)ci * m.d1 + ky) * m.d2 + kx) * m.d0 + co;
+    }
+    a.lowp[m.dst + dst] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
   __shared__ double tot;
   if (threadIdx.x == 0) {
     double s = 0.0;
@@ -292,7 +391,9 @@ __global__ void adam_kernel(const AdamArgs a) {
       const float v = a.beta2 * a.v[i] + (1.f - a.beta2) * g * g;
       a.m[i] = m;
       a.v[i] = v;
-      a.params[i] -= a.lr * (m / bc1) / (sqrtf(v / bc2) + a.eps);
+      const float p = a.params[i] - a.lr * (m / bc1) / (sqrtf(v / bc2) + a.eps);
+      a.params[i] = p;
+      if (a.nimg) lowp_write(a, i, p);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -318,7 +419,7 @@ __global__ void adam_kernel(const AdamArgs a) {
 }
 
 seed_status launch_clip_adam(const AdamArgs& a, cudaStream_t st) {
-  adam_kernel<<<148 * 4, 256, 0, st>>>(a);
+  adam_kernel<<<148 * 8, 256, 0, st>>>(a);
   return last_launch();
 }
 

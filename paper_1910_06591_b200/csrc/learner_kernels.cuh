@@ -5,20 +5,28 @@
 #pragma once
 #include "common.cuh"
 #include "vtrace_scan.cuh"
+#include "net.cuh"
 
 namespace seed {
 
-// Y[r][o] = act(b[o] + sum_i X[r][i] W[o][i]); one warp per row.  Optional split
-// output: columns o < A go to Y (ld A), column A to Yv (heads: logits / value).
+// Y[r][o] = act(b[o] + sum_i X[r][i] W[o][i]); warp per row, lane per output
+// (I <= 256, O <= 64; dynamic smem (I*O + 8*I)*4).  Optional split output:
+// columns o < A go to Y (ld A), column A to Yv (heads: logits / value).
 __global__ void dense_fwd_f32(int R, int I, int O, const float* __restrict__ X,
                               const float* __restrict__ W, const float* __restrict__ b,
                               float* __restrict__ Y, int ldy, float* __restrict__ Yv, int relu);
 
 // dX[r][i] = (sum_o dY(r,o) W[o][i]) * (mask ? mask[r][i] > 0 : 1), dY(r,o) = o < ldy ?
-// dy[r*ldy+o] : dv[r] (dv used for the last column when non-null).
+// dy[r*ldy+o] : dv[r] (dv used for the last column when non-null).  Block = 8
+// rows (grid ceil(R/8)), dynamic smem (O*I + 8*O)*4.
 __global__ void dense_dgrad_f32(int R, int I, int O, const float* __restrict__ dy, int ldy,
                                 const float* __restrict__ dv, const float* __restrict__ W,
                                 const float* __restrict__ mask, float* __restrict__ dX);
+
+seed_status launch_dense_fwd(int R, int I, int O, const float* X, const float* W, const float* b,
+                             float* Y, int ldy, float* Yv, int relu, cudaStream_t st);
+seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, const float* dv,
+                               const float* W, const float* mask, float* dX, cudaStream_t st);
 
 // gW[o][i] = sum_r dY(r,o) X[r][i];  gb[o] = sum_r dY(r,o)  (grid (O, ceil((I+1)/32)), 256
 // threads; fixed-order reduction)
@@ -66,6 +74,9 @@ struct AdamArgs {
   const float* loss_part;  // [B][4]
   int B;
   float* metrics;          // [8]
+  __nv_bfloat16* lowp;     // bf16 operand images refreshed in the same pass
+  int nimg;
+  LowpImg img[8];
 };
 seed_status launch_clip_adam(const AdamArgs& a, cudaStream_t st);
 __global__ void grad_norm_kernel(const float* __restrict__ g, int64_t P, double* __restrict__ part,

@@ -63,7 +63,14 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+// ex2-based activations (the cell is fp32; these are within a few ulp of the
+// libm versions, far below the bf16 rounding of the recurrent operands)
+__device__ __forceinline__ float sigm(float x) { return __frcp_rn(1.f + __expf(-x)); }
+__device__ __forceinline__ float tanh_fast(float x) {
+  const float e = __expf(-2.f * fabsf(x));
+  const float t = (1.f - e) * __frcp_rn(1.f + e);
+  return copysignf(t, x);
+}
 
 // CTA r's W_h slice: local row lc = gate*32 + j  <-  global row gate*U + 32r + j
 __device__ __forceinline__ void load_wh_slice(__nv_bfloat16* Ws, const __nv_bfloat16* wh, int r) {
@@ -95,24 +102,34 @@ __device__ __forceinline__ void mbar_arm_tx(uint64_t* bar, uint32_t bytes) {
 }
 
 constexpr int MAX_T1 = 257;
-constexpr int FWD_SMEM = 128 * HP * 2 + 2 * 32 * HP * 2 + 32 * GP * 4 + 32 * 32 * 4 + 32 * MAX_T1 + 64;
-constexpr int BWD_SMEM = 128 * HP * 2 + 32 * DP * 2 + 2 * 8 * 32 * RP * 4 + 32 * 32 * 4 + 32 * MAX_T1 + 64;
-constexpr uint32_t H_TX_BYTES = 32 * LSTM_U * 2;          // h slices from 8 CTAs, bf16
-constexpr uint32_t R_TX_BYTES = 8 * 32 * 32 * 4;          // 8 partial dh slices, fp32
+// BB = batch rows per cluster (template); the MMA tiles cover MR = max(BB, 16) rows
+template <int BB>
+struct LstmCfg {
+  static constexpr int MR = BB < 16 ? 16 : BB;
+  static constexpr int MT = MR / 16;
+  static constexpr int FWD_SMEM =
+      128 * HP * 2 + 2 * MR * HP * 2 + MR * GP * 4 + MR * 32 * 4 + 32 * MAX_T1 + 64;
+  static constexpr int BWD_SMEM =
+      128 * HP * 2 + MR * DP * 2 + 2 * 8 * MR * RP * 4 + MR * 32 * 4 + 32 * MAX_T1 + 64;
+  static constexpr uint32_t H_TX_BYTES = BB * LSTM_U * 2;     // h rows from 8 CTAs, bf16
+  static constexpr uint32_t R_TX_BYTES = 8 * MR * 32 * 4;     // 8 partial dh slices, fp32
+};
 
+template <int BBT>
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_fwd_kernel(const LstmFwdArgs a) {
-  constexpr int U = LSTM_U;
+  using Cfg = LstmCfg<BBT>;
+  constexpr int U = LSTM_U, MR = Cfg::MR, MT = Cfg::MT;
   extern __shared__ __align__(16) uint8_t sm[];
   __nv_bfloat16* Ws = reinterpret_cast<__nv_bfloat16*>(sm);
   __nv_bfloat16* hb = Ws + 128 * HP;
-  float* gpre = reinterpret_cast<float*>(hb + 2 * 32 * HP);
-  float* cst = gpre + 32 * GP;
-  uint8_t* dn_s = reinterpret_cast<uint8_t*>(cst + 32 * 32);   // [32][T1]
+  float* gpre = reinterpret_cast<float*>(hb + 2 * MR * HP);
+  float* cst = gpre + MR * GP;
+  uint8_t* dn_s = reinterpret_cast<uint8_t*>(cst + MR * 32);   // [BBT][T1]
   uint64_t* hbar = reinterpret_cast<uint64_t*>(dn_s + ((32 * MAX_T1 + 15) & ~15));
   const int r = (int)cluster_rank();
-  const int b0 = (blockIdx.x / LSTM_CLUSTER) * LSTM_BB;
-  const int BB = min(LSTM_BB, a.B - b0);
+  const int b0 = (blockIdx.x / LSTM_CLUSTER) * BBT;
+  const int BB = min(BBT, a.B - b0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T1 = a.T1;
 
@@ -122,11 +139,11 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     fence_mbar_init();
   }
   load_wh_slice(Ws, a.wh, r);
-  for (int i = tid; i < 32 * T1; i += 256) {
+  for (int i = tid; i < BBT * T1; i += 256) {
     const int b = i / T1, t = i % T1;
     dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
   }
-  for (int idx = tid; idx < 32 * U; idx += 256) {
+  for (int idx = tid; idx < MR * U; idx += 256) {
     const int b = idx / U, k = idx % U;
     float v = 0.f;
     if (b < BB) {
@@ -136,7 +153,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     }
     hb[b * HP + k] = __float2bfloat16_rn(v);
   }
-  for (int idx = tid; idx < 32 * 32; idx += 256) {
+  for (int idx = tid; idx < MR * 32; idx += 256) {
     const int b = idx >> 5, j = idx & 31;
     float c = 0.f, h = 0.f;
     if (b < BB) {
@@ -153,18 +170,27 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   __syncthreads();
   cluster_sync_all();   // barriers initialised everywhere before any st.async
 
-  // per-thread cell work: two (row, unit pair) items
-  int it_b[2], it_j[2];
+  // per-thread cell work: NQ (row, unit pair) items; BBT*16 items per CTA
+  constexpr int NQ = (BBT * 16 + 255) / 256;
+  int it_b[NQ], it_j[NQ];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < NQ; ++q) {
     const int idx = tid + 256 * q;
-    it_b[q] = idx >> 4;
+    it_b[q] = idx < BBT * 16 ? idx >> 4 : BBT;   // BBT = no item
     it_j[q] = (idx & 15) * 2;
   }
-  float2 xq[2][4];
+  // remote (DSMEM) base addresses of the h buffers and barriers of the 8 CTAs
+  uint32_t rh[LSTM_CLUSTER], rbar[2][LSTM_CLUSTER];
+#pragma unroll
+  for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2) {
+    rh[s2] = mapa_u32(smem_u32(hb), s2);
+    rbar[0][s2] = mapa_u32(smem_u32(&hbar[0]), s2);
+    rbar[1][s2] = mapa_u32(smem_u32(&hbar[1]), s2);
+  }
+  float2 xq[NQ][4];
   auto load_x = [&](int t) {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       if (it_b[q] < BB) {
         const float* xp = a.xproj + ((size_t)(b0 + it_b[q]) * T1 + t) * (4 * U) + 32 * r + it_j[q];
 #pragma unroll
@@ -176,33 +202,33 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   const int gid = lane >> 2, tig = lane & 3;
   for (int t = 0; t < T1; ++t) {
     const int cur = t & 1, nbuf = cur ^ 1;
-    if (tid == 0 && t + 1 < T1) mbar_arm_tx(&hbar[nbuf], H_TX_BYTES);
+    if (tid == 0 && t + 1 < T1) mbar_arm_tx(&hbar[nbuf], Cfg::H_TX_BYTES);
     if (t > 0) mbar_wait(&hbar[cur], ((t - 1) >> 1) & 1);
-    const __nv_bfloat16* hcur = hb + cur * 32 * HP;
-    float acc[2][2][4];
+    const __nv_bfloat16* hcur = hb + cur * MR * HP;
+    float acc[MT][2][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.f;
 #pragma unroll 4
     for (int ks = 0; ks < 16; ++ks) {
-      uint32_t af[2][4], bfr[4];
+      uint32_t af[MT][4], bfr[4];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
         ldsm_x4(smem_u32(hcur + (mt * 16 + (lane & 15)) * HP + ks * 16 + (lane >> 4) * 8), af[mt]);
       const int mi = lane >> 3;
       ldsm_x4(smem_u32(Ws + (warp * 16 + (mi >> 1) * 8 + (lane & 7)) * HP + ks * 16 + (mi & 1) * 8),
               bfr);
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
+      for (int mt = 0; mt < MT; ++mt) {
         mma16816(acc[mt][0], af[mt], bfr[0], bfr[1]);
         mma16816(acc[mt][1], af[mt], bfr[2], bfr[3]);
       }
     }
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int row = mt * 16 + gid, col = warp * 16 + nt * 8 + tig * 2;
@@ -211,15 +237,16 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
             make_float2(acc[mt][nt][2], acc[mt][nt][3]);
       }
     __syncthreads();
-    float2 xc[2][4];
+    float2 xc[NQ][4];
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int q = 0; q < NQ; ++q)
 #pragma unroll
       for (int gq = 0; gq < 4; ++gq) xc[q][gq] = xq[q][gq];
     if (t + 1 < T1) load_x(t + 1);   // prefetch: in flight during this step's cell + exchange
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int b = it_b[q], j = it_j[q];
+      if (b >= BBT) continue;
       if (b < BB) {
         const int bb = b0 + b;
         const size_t row = (size_t)bb * T1 + t;
@@ -232,10 +259,10 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
         for (int e = 0; e < 2; ++e) {
           gi[e] = sigm(gp[e] + xiv[e]);
           gf[e] = sigm(gp[32 + e] + xfv[e]);
-          gg[e] = tanhf(gp[64 + e] + xgv[e]);
+          gg[e] = tanh_fast(gp[64 + e] + xgv[e]);
           go[e] = sigm(gp[96 + e] + xov[e]);
           cv[e] = gf[e] * cst[b * 32 + j + e] + gi[e] * gg[e];
-          hv[e] = go[e] * tanhf(cv[e]);
+          hv[e] = go[e] * tanh_fast(cv[e]);
         }
         if (t + 1 < T1) {
           const bool dn = dn_s[b * T1 + t + 1] != 0;
@@ -243,11 +270,9 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
           cst[b * 32 + j] = dn ? 0.f : cv[0];
           cst[b * 32 + j + 1] = dn ? 0.f : cv[1];
           const uint32_t pv = pack_bf16(h0n, h1n);
-          const uint32_t local = smem_u32(hb + nbuf * 32 * HP + b * HP + col);
-          const uint32_t lbar = smem_u32(&hbar[nbuf]);
+          const uint32_t off = (uint32_t)((nbuf * MR * HP + b * HP + col) * 2);
 #pragma unroll
-          for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2)
-            st_async_u32(mapa_u32(local, s2), pv, mapa_u32(lbar, s2));
+          for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2) st_async_u32(rh[s2] + off, pv, rbar[nbuf][s2]);
           if (a.Hprev) *reinterpret_cast<uint32_t*>(a.Hprev + (row + 1) * U + col) = pv;
         } else if (a.hT) {
           const int srow = a.state_rows ? a.state_rows[bb] : bb;
@@ -267,11 +292,9 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
         }
       } else if (t + 1 < T1) {
         // rows beyond B still credit the receivers' transaction count (zeros)
-        const uint32_t local = smem_u32(hb + nbuf * 32 * HP + b * HP + 32 * r + j);
-        const uint32_t lbar = smem_u32(&hbar[nbuf]);
+        const uint32_t off = (uint32_t)((nbuf * MR * HP + b * HP + 32 * r + j) * 2);
 #pragma unroll
-        for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2)
-          st_async_u32(mapa_u32(local, s2), 0u, mapa_u32(lbar, s2));
+        for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2) st_async_u32(rh[s2] + off, 0u, rbar[nbuf][s2]);
       }
     }
     __syncthreads();   // gpre / cst reuse
@@ -279,19 +302,21 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   cluster_sync_all();
 }
 
+template <int BBT>
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_bwd_kernel(const LstmBwdArgs a) {
-  constexpr int U = LSTM_U;
+  using Cfg = LstmCfg<BBT>;
+  constexpr int U = LSTM_U, MR = Cfg::MR, MT = Cfg::MT;
   extern __shared__ __align__(16) uint8_t sm[];
   __nv_bfloat16* Ws = reinterpret_cast<__nv_bfloat16*>(sm);
   __nv_bfloat16* dzs = Ws + 128 * HP;
-  float* red = reinterpret_cast<float*>(dzs + 32 * DP);   // [2][8][32][RP]
-  float* dcs = red + 2 * 8 * 32 * RP;                      // [32][32]
-  uint8_t* dn_s = reinterpret_cast<uint8_t*>(dcs + 32 * 32);
+  float* red = reinterpret_cast<float*>(dzs + MR * DP);   // [2][8][MR][RP]
+  float* dcs = red + 2 * 8 * MR * RP;                      // [MR][32]
+  uint8_t* dn_s = reinterpret_cast<uint8_t*>(dcs + MR * 32);
   uint64_t* rbar = reinterpret_cast<uint64_t*>(dn_s + ((32 * MAX_T1 + 15) & ~15));
   const int r = (int)cluster_rank();
-  const int b0 = (blockIdx.x / LSTM_CLUSTER) * LSTM_BB;
-  const int BB = min(LSTM_BB, a.B - b0);
+  const int b0 = (blockIdx.x / LSTM_CLUSTER) * BBT;
+  const int BB = min(BBT, a.B - b0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T1 = a.T1;
 
@@ -301,22 +326,31 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     fence_mbar_init();
   }
   load_wh_slice(Ws, a.wh, r);
-  for (int i = tid; i < 32 * T1; i += 256) {
+  for (int i = tid; i < BBT * T1; i += 256) {
     const int b = i / T1, t = i % T1;
     dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
   }
-  for (int i = tid; i < 32 * DP; i += 256) dzs[i] = __float2bfloat16_rn(0.f);
-  for (int i = tid; i < 32 * 32; i += 256) dcs[i] = 0.f;
+  for (int i = tid; i < MR * DP; i += 256) dzs[i] = __float2bfloat16_rn(0.f);
+  for (int i = tid; i < MR * 32; i += 256) dcs[i] = 0.f;
   __syncthreads();
   cluster_sync_all();
 
-  // per-thread cell work: four (row, unit) items; prefetched per step
-  float pdh[4], pg[4][4], pc[4], pcp[4];
+  // per-thread cell work: NQ (row, unit) items; prefetched per step
+  constexpr int NQ = (BBT * 32 + 255) / 256;
+  float pdh[NQ], pg[NQ][4], pc[NQ], pcp[NQ];
+  // remote (DSMEM) addresses: reduction buffers and barriers of the 8 CTAs
+  uint32_t rred[LSTM_CLUSTER], rrb[2][LSTM_CLUSTER];
+#pragma unroll
+  for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2) {
+    rred[s2] = mapa_u32(smem_u32(red), s2);
+    rrb[0][s2] = mapa_u32(smem_u32(&rbar[0]), s2);
+    rrb[1][s2] = mapa_u32(smem_u32(&rbar[1]), s2);
+  }
   auto load_in = [&](int t) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int idx = tid + 256 * q, b = idx >> 5, j = idx & 31;
-      if (b < BB) {
+      if (idx < BBT * 32 && b < BB) {
         const int bb = b0 + b;
         const size_t row = (size_t)bb * T1 + t;
         const int col = 32 * r + j;
@@ -334,22 +368,22 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   for (int u = 0; u < T1; ++u) {
     const int t = T1 - 1 - u;
     // partials produced at step u land in buffer u&1; consumed at step u+1
-    if (tid == 0 && t > 0) mbar_arm_tx(&rbar[u & 1], R_TX_BYTES);
+    if (tid == 0 && t > 0) mbar_arm_tx(&rbar[u & 1], Cfg::R_TX_BYTES);
     if (u > 0) mbar_wait(&rbar[(u - 1) & 1], ((u - 1) >> 1) & 1);
-    const float* rin = red + ((u - 1) & 1) * 8 * 32 * RP;
-    float cdh[4], cg[4][4], cc[4], ccp[4];
+    const float* rin = red + ((u - 1) & 1) * 8 * MR * RP;
+    float cdh[NQ], cg[NQ][4], cc[NQ], ccp[NQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       cdh[q] = pdh[q]; cc[q] = pc[q]; ccp[q] = pcp[q];
 #pragma unroll
       for (int k = 0; k < 4; ++k) cg[q][k] = pg[q][k];
     }
     if (t > 0) load_in(t - 1);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int idx = tid + 256 * q;
       const int b = idx >> 5, j = idx & 31;
-      if (b < BB) {
+      if (idx < BBT * 32 && b < BB) {
         const int bb = b0 + b;
         const size_t row = (size_t)bb * T1 + t;
         const int col = 32 * r + j;
@@ -357,13 +391,13 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
         if (u > 0 && !dn_s[b * T1 + t + 1]) {
           float s = 0.f;
 #pragma unroll
-          for (int src = 0; src < LSTM_CLUSTER; ++src) s += rin[(src * 32 + b) * RP + j];
+          for (int src = 0; src < LSTM_CLUSTER; ++src) s += rin[(src * MR + b) * RP + j];
           dh += s;
         }
         const float gi = cg[q][0], gf = cg[q][1], gg = cg[q][2], go = cg[q][3];
         const bool dn = dn_s[b * T1 + t] != 0;
         const float cp = dn ? 0.f : ccp[q];
-        const float tc = tanhf(cc[q]);
+        const float tc = tanh_fast(cc[q]);
         const float dc = dcs[b * 32 + j] + dh * go * (1.f - tc * tc);
         const float dzi = dc * gg * gi * (1.f - gi);
         const float dzf = dc * cp * gf * (1.f - gf);
@@ -385,18 +419,18 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     }
     __syncthreads();
     if (t > 0) {
-      float acc[2][4][4];
+      float acc[MT][4][4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        uint32_t af[2][4];
+        uint32_t af[MT][4];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
           ldsm_x4(smem_u32(dzs + (mt * 16 + (lane & 15)) * DP + ks * 16 + (lane >> 4) * 8),
                   af[mt]);
         const int mi = lane >> 3;
@@ -407,24 +441,22 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
                              np * 16 + (mi >> 1) * 8),
                     bfr);
 #pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
+          for (int mt = 0; mt < MT; ++mt) {
             mma16816(acc[mt][2 * np], af[mt], bfr[0], bfr[1]);
             mma16816(acc[mt][2 * np + 1], af[mt], bfr[2], bfr[3]);
           }
         }
       }
       // columns [32*warp, 32*warp+32) belong to CTA `warp`: its slot r of buffer u&1
-      const uint32_t base = smem_u32(red + ((u & 1) * 8 + r) * 32 * RP);
-      const uint32_t rb = mapa_u32(smem_u32(&rbar[u & 1]), warp);
+      const uint32_t base = rred[warp] + (uint32_t)(((u & 1) * 8 + r) * MR * RP * 4);
+      const uint32_t rb = rrb[u & 1][warp];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
           const int row = mt * 16 + gid, j = nt * 8 + tig * 2;
-          st_async_f32x2(mapa_u32(base + (row * RP + j) * 4, warp), acc[mt][nt][0],
-                         acc[mt][nt][1], rb);
-          st_async_f32x2(mapa_u32(base + ((row + 8) * RP + j) * 4, warp), acc[mt][nt][2],
-                         acc[mt][nt][3], rb);
+          st_async_f32x2(base + (row * RP + j) * 4, acc[mt][nt][0], acc[mt][nt][1], rb);
+          st_async_f32x2(base + ((row + 8) * RP + j) * 4, acc[mt][nt][2], acc[mt][nt][3], rb);
         }
     }
     __syncthreads();   // dzs / dcs reuse
@@ -432,28 +464,55 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   cluster_sync_all();
 }
 
-seed_status lstm_forward(const LstmFwdArgs& a, cudaStream_t st) {
+template <int BBT>
+static seed_status launch_fwd(const LstmFwdArgs& a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       FWD_SMEM));
+    SEED_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel<BBT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       LstmCfg<BBT>::FWD_SMEM));
     attr = true;
   }
-  const int clusters = ceil_div(a.B, LSTM_BB);
-  lstm_fwd_kernel<<<clusters * LSTM_CLUSTER, 256, FWD_SMEM, st>>>(a);
+  lstm_fwd_kernel<BBT><<<ceil_div(a.B, BBT) * LSTM_CLUSTER, 256, LstmCfg<BBT>::FWD_SMEM, st>>>(a);
+  return last_launch();
+}
+template <int BBT>
+static seed_status launch_bwd(const LstmBwdArgs& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(lstm_bwd_kernel<BBT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       LstmCfg<BBT>::BWD_SMEM));
+    attr = true;
+  }
+  lstm_bwd_kernel<BBT><<<ceil_div(a.B, BBT) * LSTM_CLUSTER, 256, LstmCfg<BBT>::BWD_SMEM, st>>>(a);
   return last_launch();
 }
 
-seed_status lstm_backward(const LstmBwdArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       BWD_SMEM));
-    attr = true;
+// rows per cluster: spread small batches over more clusters (more SMs per step),
+// fill 32-row clusters for large ones (148 SMs / 8 = 18 clusters resident)
+static int lstm_rows_per_cluster(int B) {
+  if (B <= 4 * 8) return 8;
+  if (B <= 9 * 16) return 16;
+  return 32;
+}
+
+seed_status lstm_forward(const LstmFwdArgs& a, cudaStream_t st) {
+  if (a.T1 > MAX_T1) return SEED_E_SHAPE;
+  switch (lstm_rows_per_cluster(a.B)) {
+    case 8: return launch_fwd<8>(a, st);
+    case 16: return launch_fwd<16>(a, st);
+    default: return launch_fwd<32>(a, st);
   }
-  const int clusters = ceil_div(a.B, LSTM_BB);
-  lstm_bwd_kernel<<<clusters * LSTM_CLUSTER, 256, BWD_SMEM, st>>>(a);
-  return last_launch();
+}
+
+seed_status lstm_backward(const LstmBwdArgs& a, cudaStream_t st) {
+  if (a.T1 > MAX_T1) return SEED_E_SHAPE;
+  switch (lstm_rows_per_cluster(a.B)) {
+    case 8: return launch_bwd<8>(a, st);
+    case 16: return launch_bwd<16>(a, st);
+    default: return launch_bwd<32>(a, st);
+  }
 }
 
 }  // namespace seed

@@ -146,7 +146,7 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   w->flag = bump(cur, 16);
   w->norm_part = bump(cur, NORM_BLOCKS * 8);
   w->step_in = bump(cur, 8);
-  w->colsum_part = bump(cur, COLSUM_BLOCKS * 64 * 4);
+  w->colsum_part = bump(cur, COLSUM_BLOCKS * 64 * 4 + 64);   // + ticket (zeroed at creation)
   if (p.kind == SEED_NET_MLP) {
     w->h1 = bump(cur, F * 64 * 4);
     w->h2 = bump(cur, F * 64 * 4);

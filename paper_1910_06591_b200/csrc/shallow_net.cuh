@@ -280,36 +280,67 @@ struct Conv2Wgrad {
   __device__ void store(int m, int n, float v) const { g_w[(size_t)n * 256 + m] = v; }
 };
 
-// dY1 = transposed conv of dY2 (implicit GEMM, k = (ky, kx, co)), masked by act1 > 0
+// dY1 = transposed conv of dY2, masked by act1 > 0, as a sub-pixel GEMM: the
+// stride-2 4x4 kernel splits into 4 output parity classes (py, px); class pixels
+// y = 2qy + py, x = 2qx + px receive only taps ky = py + 2kyi, kx = px + 2kxi
+// (kyi, kxi in {0,1}) from dY2[qy - kyi][qx - kxi], so K = 2*2*32 = 128 with no
+// zero taps.  Rows m = ((class * F + f) * QH + qy) * QW + qx; all four classes run
+// in one launch with N = 64 = 4 classes x 16 channels (B rows 16c..16c+15 hold
+// class c's taps) and each row keeps only its own class's 16 columns.
 struct Conv2Dgrad {
   static constexpr bool ASYNC = true;
   const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = false;
   int M, N, K, kb_per_split;
   Geo g;
+  int F, QH, QW;         // QH = ceil(oh1/2), QW = ceil(ow1/2)
+  FastDiv fcls, fq, fqw; // F*QH*QW, QH*QW, QW
   const bf16* dY2;
   const bf16* wdg;  // [16 ci][4 ky][4 kx][32 co]
   const bf16* act1;
   bf16* dY1;
+  __device__ void decode(int m, int& cls, int& f, int& y, int& x) const {
+    uint32_t c, rem, ff, q, qy, qx;
+    fcls.divmod((uint32_t)m, c, rem);
+    fq.divmod(rem, ff, q);
+    fqw.divmod(q, qy, qx);
+    cls = (int)c; f = (int)ff;
+    y = 2 * (int)qy + (cls >> 1);
+    x = 2 * (int)qx + (cls & 1);
+  }
   __device__ const void* ptr_a(int m, int k) const {
-    uint32_t f, uy, ux;
-    split_row(g.hw1, g.w1, m, f, uy, ux);
-    const int y = (int)uy, x = (int)ux;
-    const int ky = k >> 7, kx = (k >> 5) & 3, co0 = k & 31;
-    const int yy = y - ky, xx = x - kx;
-    if (yy < 0 || xx < 0 || (yy & 1) || (xx & 1)) return nullptr;
-    const int oy = yy >> 1, ox = xx >> 1;
-    if (oy >= g.oh2 || ox >= g.ow2) return nullptr;
+    int cls, f, y, x;
+    decode(m, cls, f, y, x);
+    if (y >= g.oh1 || x >= g.ow1) return nullptr;
+    const int kyi = k >> 6, kxi = (k >> 5) & 1, co0 = k & 31;
+    const int oy = (y >> 1) - kyi, ox = (x >> 1) - kxi;
+    if (oy < 0 || ox < 0 || oy >= g.oh2 || ox >= g.ow2) return nullptr;
     return dY2 + (((size_t)f * g.oh2 + oy) * g.ow2 + ox) * 32 + co0;
   }
-  __device__ const void* ptr_b(int n, int k) const { return wdg + (size_t)n * K + k; }
+  __device__ const void* ptr_b(int n, int k) const {
+    const int cls = n >> 4, ci = n & 15;
+    const int ky = (cls >> 1) + 2 * (k >> 6), kx = (cls & 1) + 2 * ((k >> 5) & 1);
+    return wdg + (size_t)ci * 512 + (ky * 4 + kx) * 32 + (k & 31);
+  }
+  __device__ size_t pix(int m, bool& ok) const {
+    int cls, f, y, x;
+    decode(m, cls, f, y, x);
+    ok = y < g.oh1 && x < g.ow1;
+    return ((size_t)f * g.oh1 + y) * g.ow1 + x;
+  }
   __device__ void store(int m, int n, float v) const {
-    const size_t i = (size_t)m * 16 + n;
+    int cls, f, y, x;
+    decode(m, cls, f, y, x);
+    if ((n >> 4) != cls || y >= g.oh1 || x >= g.ow1) return;
+    const size_t i = (((size_t)f * g.oh1 + y) * g.ow1 + x) * 16 + (n & 15);
     dY1[i] = to_bf(bf2f(act1[i]) > 0.f ? v : 0.f);
   }
   static constexpr bool VEC_STORE = true;
   __device__ void store16(int m, int n0, float (&v)[16]) const {
-    const size_t i = (size_t)m * 16 + n0;
+    int cls, f, y, x;
+    decode(m, cls, f, y, x);
+    if ((n0 >> 4) != cls || y >= g.oh1 || x >= g.ow1) return;
+    const size_t i = (((size_t)f * g.oh1 + y) * g.ow1 + x) * 16;
     relu_mask16(act1 + i, v);
     st_bf16x16(dY1 + i, v);
   }
