@@ -93,6 +93,31 @@ def phase_work(T, B, A):
     return w
 
 
+# ---------------------------------------------------------------- committed ncu evidence
+PHASE_KERNEL = {"conv1_fwd": "Conv1Fwd", "conv2_fwd": "Conv2Fwd", "fc_fwd": "FcFwd",
+                "xproj_fwd": "XprojFwd", "lstm_fwd": "lstm_fwd_kernel", "lstm_bwd": "lstm_bwd_kernel",
+                "lstm_wgrad": "LstmWgrad", "dx_fc": "DxFc", "fc_wgrad": "FcWgrad",
+                "fc_dgrad": "FcDgrad", "conv2_wgrad": "Conv2Wgrad", "conv2_dgrad": "Conv2Dgrad",
+                "conv1_wgrad": "Conv1Wgrad", "policy_loss": "policy_loss_kernel",
+                "clip_adam": "adam_kernel"}
+
+
+def ncu_traffic(phase):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's main
+    kernel from the committed `ncu --set full` capture (profiles/r01/ncu_full.json)."""
+    key = PHASE_KERNEL.get(phase)
+    path = os.path.join(ROOT, "profiles", "r01", "ncu_full.json")
+    if not key or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    for name, ents in d.items():
+        if key in name and "splitk" not in name:
+            v = [e["dram_bytes"] for e in ents if e.get("dram_bytes") is not None]
+            return round(sum(v) / len(v)) if v else None
+    return None
+
+
 # ---------------------------------------------------------------- clocks (NVML)
 class ClockSampler:
     def __init__(self, index):
@@ -390,7 +415,7 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": round(nbytes / t_s / 1e9, 2), "peak": pk["hbm_gbs"],
                 "unit": "GB/s"}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
-    roof["traffic"] = None
+    roof["traffic"] = ncu_traffic(dom)
     roof["kernel"] = dom
     roof["us_per_launch"] = round(per_phase[dom] * 1e3, 2)
     roof["peak_source"] = pk["source"]

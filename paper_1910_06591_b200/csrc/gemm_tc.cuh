@@ -349,14 +349,37 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
   if (warp == GEMM_MMA_WARP) tmem_dealloc(tmem, Cfg::TMEM_COLS);
 }
 
+// Fixed-order split-K reduction: a block owns 32 consecutive outputs; thread
+// (g, o) sums the splits z = g, g+8, ... of output o, then the 8 group sums are
+// added in group order — deterministic, and enough loads in flight per thread.
 template <class Prob>
-__global__ void splitk_finish(const Prob p, const float* __restrict__ part, int splits) {
+__global__ void __launch_bounds__(256) splitk_finish(const Prob p, const float* __restrict__ part,
+                                                     int splits) {
   const size_t MN = (size_t)p.M * p.N;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < MN;
-       i += (size_t)gridDim.x * blockDim.x) {
+  const int o = threadIdx.x & 31, g = threadIdx.x >> 5;
+  __shared__ float sh[8][33];
+  for (size_t base = (size_t)blockIdx.x * 32; base < MN; base += (size_t)gridDim.x * 32) {
+    const size_t i = base + o;
     float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[z * MN + i];
-    p.store((int)(i / p.N), (int)(i % p.N), s);
+    if (i < MN) {
+      float a0 = 0.f, a1 = 0.f;
+      int z = g;
+      for (; z + 8 < splits; z += 16) {
+        a0 += part[(size_t)z * MN + i];
+        a1 += part[(size_t)(z + 8) * MN + i];
+      }
+      if (z < splits) a0 += part[(size_t)z * MN + i];
+      s = a0 + a1;
+    }
+    sh[g][o] = s;
+    __syncthreads();
+    if (g == 0 && i < MN) {
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += sh[k][o];
+      p.store((int)(i / p.N), (int)(i % p.N), t);
+    }
+    __syncthreads();
   }
 }
 
@@ -387,7 +410,7 @@ seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullp
   gemm_tc_kernel<BN, Prob><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(p, part, splits);
   if (splits > 1) {
     const size_t MN = (size_t)p.M * p.N;
-    const int blocks = (int)std::min<size_t>((MN + 255) / 256, 148 * 8);
+    const int blocks = (int)std::min<size_t>((MN + 31) / 32, 148 * 8);
     splitk_finish<Prob><<<blocks, 256, 0, st>>>(p, part, splits);
   }
   return last_launch();
