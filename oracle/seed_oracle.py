@@ -389,18 +389,18 @@ def torso_forward(spec, P, obs, emu=False):
     else:
         h = x
         for s in range(len(spec.sections)):
-            conv = conv2d(h, P[f"s{s}.conv.w"], P[f"s{s}.conv.b"], 1, 1)
+            conv = q(conv2d(h, q(P[f"s{s}.conv.w"]), P[f"s{s}.conv.b"], 1, 1))
             pooled, arg, offs = maxpool_same(conv)
             cache[f"s{s}.in"], cache[f"s{s}.conv"] = h, conv
             cache[f"s{s}.arg"], cache[f"s{s}.offs"] = arg, offs
             h = pooled
             for r in range(2):
                 u0 = relu(h)
-                t0 = conv2d(u0, P[f"s{s}.res{r}.conv0.w"], P[f"s{s}.res{r}.conv0.b"], 1, 1)
-                u1 = relu(t0)
-                t1 = conv2d(u1, P[f"s{s}.res{r}.conv1.w"], P[f"s{s}.res{r}.conv1.b"], 1, 1)
+                t0 = conv2d(u0, q(P[f"s{s}.res{r}.conv0.w"]), P[f"s{s}.res{r}.conv0.b"], 1, 1)
+                u1 = q(relu(t0))
+                t1 = conv2d(u1, q(P[f"s{s}.res{r}.conv1.w"]), P[f"s{s}.res{r}.conv1.b"], 1, 1)
                 cache[f"s{s}.res{r}"] = (h, u0, t0, u1)
-                h = h + t1
+                h = q(h + t1)
         cache["torso_pre"] = h
         flat = relu(h).reshape(h.shape[0], -1)
     fc = q(relu(flat @ q(P["fc.w"]).T + P["fc.b"]))
@@ -433,20 +433,22 @@ def torso_backward(spec, P, cache, dfeat, grads, emu=False):
                                                                 4, 0, need_dx=False)
         return
     h_pre = cache["torso_pre"]
-    dh = dflat.reshape(h_pre.shape) * (h_pre > 0)
+    dh = q(dflat.reshape(h_pre.shape) * (h_pre > 0))
     for s in reversed(range(len(spec.sections))):
         for r in reversed(range(2)):
             h_in, u0, t0, u1 = cache[f"s{s}.res{r}"]
             du1, grads[f"s{s}.res{r}.conv1.w"], grads[f"s{s}.res{r}.conv1.b"] = \
-                conv2d_backward(u1, P[f"s{s}.res{r}.conv1.w"], dh, 1, 1)
-            dt0 = du1 * (t0 > 0)
+                conv2d_backward(u1, q(P[f"s{s}.res{r}.conv1.w"]), dh, 1, 1)
+            dt0 = q(du1 * (t0 > 0))
             du0, grads[f"s{s}.res{r}.conv0.w"], grads[f"s{s}.res{r}.conv0.b"] = \
-                conv2d_backward(u0, P[f"s{s}.res{r}.conv0.w"], dt0, 1, 1)
-            dh = dh + du0 * (h_in > 0)
+                conv2d_backward(u0, q(P[f"s{s}.res{r}.conv0.w"]), dt0, 1, 1)
+            dh = q(dh + du0 * (h_in > 0))
         conv = cache[f"s{s}.conv"]
-        dconv = maxpool_same_backward(conv.shape, cache[f"s{s}.arg"], cache[f"s{s}.offs"], dh)
+        dconv = q(maxpool_same_backward(conv.shape, cache[f"s{s}.arg"], cache[f"s{s}.offs"], dh))
         dh, grads[f"s{s}.conv.w"], grads[f"s{s}.conv.b"] = conv2d_backward(
-            cache[f"s{s}.in"], P[f"s{s}.conv.w"], dconv, 1, 1, need_dx=(s > 0))
+            cache[f"s{s}.in"], q(P[f"s{s}.conv.w"]), dconv, 1, 1, need_dx=(s > 0))
+        if dh is not None:
+            dh = q(dh)
 
 
 # ---- LSTM core (H3, H8; P:591 inputs, S:47/S:57 reset, C15) ----------------

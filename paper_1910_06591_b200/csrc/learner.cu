@@ -21,10 +21,12 @@
 //   conv biases: deterministic column sums
 //   [allreduce] -> global-norm clip + Adam -> bf16 operand image refresh
 #include <string.h>
+#include <utility>
 #include "gemm_tc.cuh"
 #include "learner_kernels.cuh"
 #include "lstm.cuh"
 #include "net.cuh"
+#include "deep_net.cuh"
 #include "shallow_net.cuh"
 
 namespace seed {
@@ -72,6 +74,7 @@ static seed_status gemm(const StepCtx& c, Prob pr, cudaStream_t st, const char* 
   return r;
 }
 
+// Atari-shallow torso: obs -> act2 (H1)
 static seed_status shallow_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                    const float* params, cudaStream_t st) {
   const NetPlan& p = *c.p;
@@ -97,6 +100,15 @@ static seed_status shallow_forward(const StepCtx& c, const seed_batch* bt, const
     pr.bias = params + p.t[p.i_conv2b].off; pr.out = c.at<bf16>(w.act2);
     SEED_TRY(gemm<32>(c, pr, st, "conv2_fwd"));
   }
+  return last_launch();
+}
+
+// FC + LSTM core + heads over the flattened torso output w.act2 (H2-H4)
+static seed_status core_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
+                                const float* params, cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int F = w.F;
   {
     FcFwd pr{};
     pr.M = F; pr.N = 256; pr.K = p.fc_in; pr.Kxp = p.Kxp;
@@ -136,7 +148,8 @@ static seed_status shallow_forward(const StepCtx& c, const seed_batch* bt, const
   return last_launch();
 }
 
-static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
+// heads + LSTM backward + FC backward, ending with w.dY2 = d(act2) (H8, H9 part)
+static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                     const float* params, float* grads, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
@@ -186,6 +199,15 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
     pr.dY2 = c.at<bf16>(w.dY2);
     SEED_TRY(gemm<128>(c, pr, st, "fc_dgrad"));
   }
+  return SEED_OK;
+}
+
+// Atari-shallow torso backward from w.dY2 (H9)
+static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
+                                    const float* params, float* grads, cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int F = w.F;
   {
     Conv2Wgrad pr{};
     pr.M = 256; pr.N = 32; pr.K = F * p.oh2 * p.ow2; pr.g = c.g;
@@ -217,6 +239,137 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
   SEED_TRY(colsum_bf16(c.at<bf16>(w.dY1), (int64_t)F * p.oh1 * p.ow1, 16,
                        c.at<float>(w.colsum_part), grads + p.t[p.i_conv1b].off, st));
   c.mark("conv1_bias");
+  return SEED_OK;
+}
+
+
+// ------------------------------------------------------------------ IMPALA-deep torso
+static Conv3Geo c3geo(int H, int W, int cin, int cout) {
+  return Conv3Geo{H, W, cin, cout, FastDiv((uint32_t)(H * W)), FastDiv((uint32_t)W)};
+}
+static int ilog2(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return l;
+}
+template <int MODE>
+static seed_status conv3_fwd(const StepCtx& c, int BN, int M, Conv3Geo g, const bf16* in,
+                             const bf16* w, const float* bias, const bf16* res, bf16* out,
+                             bf16* outr, float scale, cudaStream_t st, const char* name) {
+  Conv3Fwd<MODE> pr{};
+  pr.M = M; pr.N = g.cout; pr.K = 9 * g.cin; pr.g = g; pr.cshift = ilog2(g.cin);
+  pr.in_scale = scale; pr.in = in; pr.w = w; pr.bias = bias; pr.res = res; pr.out = out;
+  pr.outr = outr;
+  return BN == 16 ? gemm<16>(c, pr, st, name) : gemm<32>(c, pr, st, name);
+}
+template <int MODE>
+static seed_status conv3_dgrad(const StepCtx& c, int M, Conv3Geo g, const bf16* dY,
+                               const bf16* wdg, const bf16* mask, const bf16* dres, bf16* dX,
+                               cudaStream_t st, const char* name) {
+  // g.cin = dY channels (this layer's cout), g.cout = dX channels (this layer's cin)
+  Conv3Dgrad<MODE> pr{};
+  pr.M = M; pr.N = g.cout; pr.K = 9 * g.cin; pr.g = g; pr.cshift = ilog2(g.cin);
+  pr.dY = dY; pr.wdg = wdg; pr.mask = mask; pr.dres = dres; pr.dX = dX;
+  return g.cout == 16 ? gemm<16>(c, pr, st, name) : gemm<32>(c, pr, st, name);
+}
+static seed_status conv3_wgrad(const StepCtx& c, int rows, Conv3Geo g, int creal, float scale,
+                               const bf16* X, const bf16* dY, float* gw, cudaStream_t st,
+                               const char* name) {
+  Conv3Wgrad pr{};
+  pr.M = 9 * g.cin; pr.N = g.cout; pr.K = rows; pr.g = g; pr.cshift = ilog2(g.cin);
+  pr.creal = creal; pr.scale = scale; pr.X = X; pr.dY = dY; pr.g_w = gw;
+  return g.cout == 16 ? gemm<16>(c, pr, st, name) : gemm<32>(c, pr, st, name);
+}
+
+static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
+                                const float* params, cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int F = w.F;
+  {
+    const DeepSec& d = p.sec[0];
+    const int64_t npix = (int64_t)F * d.H * d.W;
+    obs_to_bf16_pad_kernel<<<(int)std::min<int64_t>((npix * d.cinp + 255) / 256, 148 * 16), 256, 0,
+                             st>>>(npix, p.C, d.cinp, (const uint8_t*)bt->obs,
+                                   c.at<bf16>(w.obs_bf16));
+    c.mark("obs_bf16");
+  }
+  for (int s = 0; s < p.nsec; ++s) {
+    const DeepSec& d = p.sec[s];
+    const LearnerWs::Sec& b = w.sec[s];
+    const bf16* in = s == 0 ? c.at<bf16>(w.obs_bf16) : c.at<bf16>(w.sec[s - 1].h[2]);
+    SEED_TRY(conv3_fwd<C3_PLAIN>(c, d.ch, F * d.H * d.W, c3geo(d.H, d.W, d.cinp, d.ch), in,
+                                 lowp + d.im_w, params + p.t[d.t_b].off, nullptr,
+                                 c.at<bf16>(b.conv), nullptr, s == 0 ? 1.f / 255.f : 1.f, st,
+                                 "deep_conv_fwd"));
+    const int64_t np = (int64_t)F * d.H2 * d.W2 * d.ch;
+    maxpool_fwd_kernel<<<(int)std::min<int64_t>((np + 255) / 256, 148 * 16), 256, 0, st>>>(
+        np, d.H, d.W, d.H2, d.W2, d.ch, d.pt, d.pl, c.at<bf16>(b.conv), c.at<bf16>(b.h[0]),
+        c.at<bf16>(b.hr[0]), c.at<uint8_t>(b.arg));
+    c.mark("deep_pool_fwd");
+    const Conv3Geo gr = c3geo(d.H2, d.W2, d.ch, d.ch);
+    const int Mr = F * d.H2 * d.W2;
+    for (int r = 0; r < 2; ++r) {
+      SEED_TRY(conv3_fwd<C3_RELU>(c, d.ch, Mr, gr, c.at<bf16>(b.hr[r]), lowp + d.im_rw[r][0],
+                                  params + p.t[d.t_rb[r][0]].off, nullptr, c.at<bf16>(b.u1[r]),
+                                  nullptr, 1.f, st, "deep_res_fwd0"));
+      SEED_TRY(conv3_fwd<C3_RES>(c, d.ch, Mr, gr, c.at<bf16>(b.u1[r]), lowp + d.im_rw[r][1],
+                                 params + p.t[d.t_rb[r][1]].off, c.at<bf16>(b.h[r]),
+                                 c.at<bf16>(b.h[r + 1]), c.at<bf16>(b.hr[r + 1]), 1.f, st,
+                                 "deep_res_fwd1"));
+    }
+  }
+  return last_launch();
+}
+
+static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
+                                 const float* params, float* grads, cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int F = w.F;
+  float* cpart = c.at<float>(w.colsum_part);
+  for (int s = p.nsec - 1; s >= 0; --s) {
+    const DeepSec& d = p.sec[s];
+    const LearnerWs::Sec& b = w.sec[s];
+    const Conv3Geo gr = c3geo(d.H2, d.W2, d.ch, d.ch);
+    const int Mr = F * d.H2 * d.W2;
+    size_t cur = b.dhA, oth = b.dhB;   // dh of h[2] arrives in dhA
+    for (int r = 1; r >= 0; --r) {
+      // t1 = conv1(u1): dt1 = dh
+      SEED_TRY(conv3_wgrad(c, Mr, gr, d.ch, 1.f, c.at<bf16>(b.u1[r]), c.at<bf16>(cur),
+                           grads + p.t[d.t_rw[r][1]].off, st, "deep_res_wgrad1"));
+      SEED_TRY(colsum_bf16(c.at<bf16>(cur), Mr, d.ch, cpart, grads + p.t[d.t_rb[r][1]].off, st));
+      c.mark("deep_bias");
+      SEED_TRY(conv3_dgrad<D3_MASK>(c, Mr, gr, c.at<bf16>(cur), lowp + d.im_rdg[r][1],
+                                    c.at<bf16>(b.u1[r]), nullptr, c.at<bf16>(b.dt0), st,
+                                    "deep_res_dgrad1"));
+      // t0 = conv0(u0 = relu(h[r])): dh[r] = dh + dconv0 * (h[r] > 0)
+      SEED_TRY(conv3_wgrad(c, Mr, gr, d.ch, 1.f, c.at<bf16>(b.hr[r]), c.at<bf16>(b.dt0),
+                           grads + p.t[d.t_rw[r][0]].off, st, "deep_res_wgrad0"));
+      SEED_TRY(colsum_bf16(c.at<bf16>(b.dt0), Mr, d.ch, cpart, grads + p.t[d.t_rb[r][0]].off, st));
+      c.mark("deep_bias");
+      SEED_TRY(conv3_dgrad<D3_RES>(c, Mr, gr, c.at<bf16>(b.dt0), lowp + d.im_rdg[r][0],
+                                   c.at<bf16>(b.hr[r]), c.at<bf16>(cur), c.at<bf16>(oth), st,
+                                   "deep_res_dgrad0"));
+      std::swap(cur, oth);
+    }
+    // max-pool backward into dconv, then the section conv
+    const int64_t nc = (int64_t)F * d.H * d.W * d.ch;
+    maxpool_bwd_kernel<<<(int)std::min<int64_t>((nc + 255) / 256, 148 * 16), 256, 0, st>>>(
+        nc, d.H, d.W, d.H2, d.W2, d.ch, d.pt, d.pl, c.at<bf16>(cur), c.at<uint8_t>(b.arg),
+        c.at<bf16>(b.dconv));
+    c.mark("deep_pool_bwd");
+    const bf16* in = s == 0 ? c.at<bf16>(w.obs_bf16) : c.at<bf16>(w.sec[s - 1].h[2]);
+    const int Mc = F * d.H * d.W;
+    SEED_TRY(conv3_wgrad(c, Mc, c3geo(d.H, d.W, d.cinp, d.ch), d.cin, s == 0 ? 1.f / 255.f : 1.f,
+                         in, c.at<bf16>(b.dconv), grads + p.t[d.t_w].off, st, "deep_conv_wgrad"));
+    SEED_TRY(colsum_bf16(c.at<bf16>(b.dconv), Mc, d.ch, cpart, grads + p.t[d.t_b].off, st));
+    c.mark("deep_bias");
+    if (s > 0)
+      SEED_TRY(conv3_dgrad<D3_PLAIN>(c, Mc, c3geo(d.H, d.W, d.ch, d.cin), c.at<bf16>(b.dconv),
+                                     lowp + d.im_dg, nullptr, nullptr,
+                                     c.at<bf16>(w.sec[s - 1].dhA), st, "deep_conv_dgrad"));
+  }
   return SEED_OK;
 }
 
@@ -304,8 +457,13 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   // column-sum completion ticket (re-armed by the kernel after each use)
   SEED_CUDA_TRY(cudaMemsetAsync(c.at<float>(c.w.colsum_part) + COLSUM_BLOCKS * 64, 0, 16, st));
 
-  if (p.kind == SEED_NET_MLP) SEED_TRY(mlp_forward(c, batch, params, st));
-  else SEED_TRY(shallow_forward(c, batch, lowp, params, st));
+  if (p.kind == SEED_NET_MLP) {
+    SEED_TRY(mlp_forward(c, batch, params, st));
+  } else {
+    if (p.nsec > 0) SEED_TRY(deep_forward(c, batch, lowp, params, st));
+    else SEED_TRY(shallow_forward(c, batch, lowp, params, st));
+    SEED_TRY(core_forward(c, batch, lowp, params, st));
+  }
 
   LossArgs la{};
   la.B = B; la.T = T; la.A = p.A;
@@ -320,8 +478,13 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   SEED_TRY(launch_policy_loss(la, st));
   c.mark("policy_loss");
 
-  if (p.kind == SEED_NET_MLP) SEED_TRY(mlp_backward(c, batch, params, grads, st));
-  else SEED_TRY(shallow_backward(c, batch, lowp, params, grads, st));
+  if (p.kind == SEED_NET_MLP) {
+    SEED_TRY(mlp_backward(c, batch, params, grads, st));
+  } else {
+    SEED_TRY(core_backward(c, batch, lowp, params, grads, st));
+    if (p.nsec > 0) SEED_TRY(deep_backward(c, batch, lowp, params, grads, st));
+    else SEED_TRY(shallow_backward(c, batch, lowp, params, grads, st));
+  }
 
   if (comm) {
     SEED_TRY(comm_allreduce(comm, grads, p.P, st));
@@ -339,10 +502,15 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   aa.max_norm = hp->max_grad_norm; aa.loss_part = c.at<float>(c.w.loss_part); aa.B = B;
   aa.metrics = metrics;
   aa.lowp = (bf16*)state->params_lowp;
-  aa.nimg = p.nimg;
-  for (int k = 0; k < p.nimg; ++k) aa.img[k] = p.img[k];
+  const bool fused_lowp = p.nimg <= 8;    // Adam writes the operand image itself
+  aa.nimg = fused_lowp ? p.nimg : 0;
+  for (int k = 0; k < aa.nimg; ++k) aa.img[k] = p.img[k];
   SEED_TRY(launch_clip_adam(aa, st));
   c.mark("clip_adam");
+  if (!fused_lowp) {
+    SEED_TRY(refresh_lowp(p, state->params, state->params_lowp, st));
+    c.mark("lowp_refresh");
+  }
   return last_launch();
 }
 
@@ -418,6 +586,7 @@ extern "C" seed_status seed_learner_debug_buffer(const seed_net_spec* spec, int 
       {"dH", mlp ? 0 : w.dH, F * U * 4}, {"dG", mlp ? 0 : w.dG, F * 4 * U * 2},
       {"dfc", mlp ? 0 : w.dfc, F * 256 * 2}, {"dY2", mlp ? 0 : w.dY2, F * p.fc_in * 2},
       {"dY1", mlp ? 0 : w.dY1, F * p.oh1 * p.ow1 * 16 * 2},
+      {"obs_bf16", w.obs_bf16, 16},
       {"h1", mlp ? w.h1 : 0, F * 64 * 4}, {"h2", mlp ? w.h2 : 0, F * 64 * 4},
       {"dh1", mlp ? w.dh1 : 0, F * 64 * 4}, {"dh2", mlp ? w.dh2 : 0, F * 64 * 4}};
   for (const Ent& e : ents)
@@ -426,5 +595,25 @@ extern "C" seed_status seed_learner_debug_buffer(const seed_net_spec* spec, int 
       if (bytes) *bytes = e.bytes;
       return SEED_OK;
     }
+  // deep torso: "s<k>.<buf>" with buf in conv, arg, h0..h2, hr0..hr2, u10, u11, dconv, dhA, dhB, dt0
+  if (p.nsec > 0 && name[0] == 's' && name[1] >= '0' && name[1] < '0' + p.nsec && name[2] == '.') {
+    const int k = name[1] - '0';
+    const DeepSec& d = p.sec[k];
+    const LearnerWs::Sec& b = w.sec[k];
+    const size_t sc = F * d.H * d.W * d.ch * 2, sp = F * d.H2 * d.W2 * d.ch * 2;
+    const char* bn = name + 3;
+    struct E2 { const char* n; size_t off, bytes; };
+    const E2 e2[] = {{"conv", b.conv, sc}, {"arg", b.arg, sp / 2}, {"h0", b.h[0], sp},
+                     {"h1", b.h[1], sp}, {"h2", b.h[2], sp}, {"hr0", b.hr[0], sp},
+                     {"hr1", b.hr[1], sp}, {"hr2", b.hr[2], sp}, {"u10", b.u1[0], sp},
+                     {"u11", b.u1[1], sp}, {"dconv", b.dconv, sc}, {"dhA", b.dhA, sp},
+                     {"dhB", b.dhB, sp}, {"dt0", b.dt0, sp}};
+    for (const E2& e : e2)
+      if (strcmp(e.n, bn) == 0) {
+        *ptr = (uint8_t*)ws + e.off;
+        if (bytes) *bytes = e.bytes;
+        return SEED_OK;
+      }
+  }
   return SEED_E_ARG;
 }

@@ -1,6 +1,7 @@
 // net.cu — network definitions (C14): parameter layout, bf16 operand image,
 // workspace planning, and the parameter-query entry points of the C ABI.
 #include <stdio.h>
+#include <algorithm>
 #include "gemm_tc.cuh"
 #include "net.cuh"
 
@@ -58,16 +59,25 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
     const int chs[4] = {16, 32, 32, 32};
     int cin = p->C, h = p->H, w = p->W;
     char nm[32];
+    p->nsec = ns;
     for (int sct = 0; sct < ns; ++sct) {
       const int ch = chs[sct];
-      snprintf(nm, 32, "s%d.conv.w", sct); add_t(p, nm, 4, ch, 3, 3, cin);
-      snprintf(nm, 32, "s%d.conv.b", sct); add_t(p, nm, 1, ch);
+      DeepSec& d = p->sec[sct];
+      d.H = h; d.W = w; d.cin = cin; d.ch = ch;
+      d.cinp = cin <= 8 ? 8 : (cin <= 16 ? 16 : (cin <= 32 ? 32 : 64));
+      d.H2 = same_out(h); d.W2 = same_out(w);
+      const int ph = std::max((d.H2 - 1) * 2 + 3 - h, 0), pw = std::max((d.W2 - 1) * 2 + 3 - w, 0);
+      d.pt = ph / 2; d.pl = pw / 2;
+      snprintf(nm, 32, "s%d.conv.w", sct); d.t_w = p->nt; add_t(p, nm, 4, ch, 3, 3, cin);
+      snprintf(nm, 32, "s%d.conv.b", sct); d.t_b = p->nt; add_t(p, nm, 1, ch);
       for (int r = 0; r < 2; ++r)
         for (int j = 0; j < 2; ++j) {
-          snprintf(nm, 32, "s%d.res%d.conv%d.w", sct, r, j); add_t(p, nm, 4, ch, 3, 3, ch);
-          snprintf(nm, 32, "s%d.res%d.conv%d.b", sct, r, j); add_t(p, nm, 1, ch);
+          snprintf(nm, 32, "s%d.res%d.conv%d.w", sct, r, j); d.t_rw[r][j] = p->nt;
+          add_t(p, nm, 4, ch, 3, 3, ch);
+          snprintf(nm, 32, "s%d.res%d.conv%d.b", sct, r, j); d.t_rb[r][j] = p->nt;
+          add_t(p, nm, 1, ch);
         }
-      cin = ch; h = same_out(h); w = same_out(w);
+      cin = ch; h = d.H2; w = d.W2;
     }
     fh = h; fw = w; fc = cin;
   } else {
@@ -83,33 +93,56 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
   p->i_lb = p->nt; add_t(p, "lstm.b", 1, 4 * p->U);
   p->i_hw = p->nt; add_t(p, "heads.w", 2, A + 1, p->U);
   p->i_hb = p->nt; add_t(p, "heads.b", 1, A + 1);
+  // bf16 operand images (GEMM-ready, K padded to multiples of 8 / 32)
+  int64_t off = 0;
+  auto img = [&](int kind, int ti, int rows, int cols, int ld) {
+    LowpImg& m = p->img[p->nimg++];
+    m.kind = kind; m.src = p->t[ti].off; m.dst = off; m.rows = rows; m.cols = cols; m.ld = ld;
+    const int64_t start = off;
+    off += (int64_t)rows * ld;
+    off = (int64_t)align_up((size_t)off, 64);
+    return start;
+  };
+  auto dgrad_img = [&](int ti, int co, int k, int ci) {   // [ci][k][k][co]
+    const int64_t at = img(IMG_CONV_DGRAD, ti, ci, k * k * co, k * k * co);
+    LowpImg& m = p->img[p->nimg - 1];
+    m.d0 = co; m.d1 = k; m.d2 = k; m.d3 = ci;
+    return at;
+  };
   if (s->kind == SEED_NET_ATARI_SHALLOW) {
-    // bf16 operand images (GEMM-ready, K padded to multiples of 8 / 32)
-    int64_t off = 0;
-    auto img = [&](int kind, int ti, int rows, int cols, int ld) {
-      LowpImg& m = p->img[p->nimg++];
-      m.kind = kind; m.src = p->t[ti].off; m.dst = off; m.rows = rows; m.cols = cols; m.ld = ld;
-      const int64_t start = off;
-      off += (int64_t)rows * ld;
-      off = (int64_t)align_up((size_t)off, 64);
-      return start;
-    };
     p->im_conv1 = img(IMG_COPY_PAD, p->i_conv1w, 16, 64 * p->C, 64 * p->C);
     p->im_conv2 = img(IMG_COPY_PAD, p->i_conv2w, 32, 256, 256);
-    p->im_conv2dg = img(IMG_CONV_DGRAD, p->i_conv2w, 16, 512, 512);  // [ci][ky][kx][co]
-    LowpImg& dg = p->img[p->nimg - 1];
-    dg.d0 = 32; dg.d1 = 4; dg.d2 = 4; dg.d3 = 16;
-    p->im_fc = img(IMG_COPY_PAD, p->i_fcw, 256, p->fc_in, p->fc_in);
-    p->im_wx = img(IMG_COPY_PAD, p->i_wx, 4 * p->U, p->Kx, p->Kxp);
-    p->im_wh = img(IMG_COPY_PAD, p->i_wh, 4 * p->U, p->U, p->U);
-    p->lowp_elems = off;
+    p->im_conv2dg = dgrad_img(p->i_conv2w, 32, 4, 16);   // [ci][ky][kx][co]
+  } else {
+    for (int sct = 0; sct < p->nsec; ++sct) {
+      DeepSec& d = p->sec[sct];
+      if (d.cin == d.cinp) {
+        d.im_w = img(IMG_COPY_PAD, d.t_w, d.ch, 9 * d.cin, 9 * d.cin);
+      } else {
+        d.im_w = img(IMG_CHAN_PAD, d.t_w, d.ch, 9 * d.cin, 9 * d.cinp);
+        LowpImg& m = p->img[p->nimg - 1];
+        m.d1 = 9; m.d2 = d.cinp; m.d3 = d.cin;
+      }
+      d.im_dg = sct > 0 ? dgrad_img(d.t_w, d.ch, 3, d.cin) : -1;
+      for (int r = 0; r < 2; ++r)
+        for (int j = 0; j < 2; ++j) {
+          d.im_rw[r][j] = img(IMG_COPY_PAD, d.t_rw[r][j], d.ch, 9 * d.ch, 9 * d.ch);
+          d.im_rdg[r][j] = dgrad_img(d.t_rw[r][j], d.ch, 3, d.ch);
+        }
+    }
   }
+  p->im_fc = img(IMG_COPY_PAD, p->i_fcw, 256, p->fc_in, p->fc_in);
+  p->im_wx = img(IMG_COPY_PAD, p->i_wx, 4 * p->U, p->Kx, p->Kxp);
+  p->im_wh = img(IMG_COPY_PAD, p->i_wh, 4 * p->U, p->U, p->U);
+  p->lowp_elems = off;
   return SEED_OK;
 }
 
 bool learner_supported(const NetPlan& p) {
   if (p.kind == SEED_NET_MLP) return true;
   if (p.kind == SEED_NET_ATARI_SHALLOW) return p.C == 4 && p.fc_in % 8 == 0 && (p.W * p.C) % 16 == 0;
+  if (p.kind == SEED_NET_IMPALA_DEEP || p.kind == SEED_NET_GFOOTBALL)
+    return p.C <= 32 && p.fc_in % 8 == 0;
   return false;
 }
 
@@ -157,9 +190,37 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   }
   const size_t U = p.U;
   w->dH = bump(cur, F * U * 4);
-  w->obs_bf16 = bump(cur, F * p.H * p.W * p.C * 2);
-  w->act1 = bump(cur, F * p.oh1 * p.ow1 * 16 * 2);
-  w->act2 = bump(cur, F * p.fc_in * 2);
+  if (p.nsec > 0) {
+    const DeepSec& d0 = p.sec[0];
+    w->obs_bf16 = bump(cur, F * d0.H * d0.W * d0.cinp * 2);
+    for (int sct = 0; sct < p.nsec; ++sct) {
+      const DeepSec& d = p.sec[sct];
+      LearnerWs::Sec& b = w->sec[sct];
+      const size_t sc = F * d.H * d.W * d.ch, sp = F * d.H2 * d.W2 * d.ch;
+      b.conv = bump(cur, sc * 2);
+      b.arg = bump(cur, sp);
+      for (int k = 0; k < 3; ++k) {
+        b.h[k] = bump(cur, sp * 2);
+        b.hr[k] = bump(cur, sp * 2);
+      }
+      b.u1[0] = bump(cur, sp * 2);
+      b.u1[1] = bump(cur, sp * 2);
+      b.dconv = bump(cur, sc * 2);
+      b.dhA = bump(cur, sp * 2);
+      b.dhB = bump(cur, sp * 2);
+      b.dt0 = bump(cur, sp * 2);
+    }
+    // the FC layer reads relu(h) of the last section and writes its data gradient
+    // into that section's dh buffer
+    w->act2 = w->sec[p.nsec - 1].hr[2];
+    w->dY2 = w->sec[p.nsec - 1].dhA;
+  } else {
+    w->obs_bf16 = bump(cur, F * p.H * p.W * p.C * 2);
+    w->act1 = bump(cur, F * p.oh1 * p.ow1 * 16 * 2);
+    w->act2 = bump(cur, F * p.fc_in * 2);
+    w->dY1 = bump(cur, F * p.oh1 * p.ow1 * 16 * 2);
+    w->dY2 = bump(cur, F * p.fc_in * 2);
+  }
   w->X = bump(cur, F * p.Kxp * 2);
   w->xproj = bump(cur, F * 4 * U * 4);
   w->H = bump(cur, F * U * 4);
@@ -168,8 +229,6 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   w->Cst = bump(cur, F * U * 4);
   w->dG = bump(cur, F * 4 * U * 2);
   w->dfc = bump(cur, F * 256 * 2);
-  w->dY2 = bump(cur, F * p.fc_in * 2);
-  w->dY1 = bump(cur, F * p.oh1 * p.ow1 * 16 * 2);
   // split-K partial buffer: max over the split GEMMs of the step
   const int Fi = (int)F;
   size_t sk = 0;
@@ -183,8 +242,15 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   need(Fi, 256, 128, 4 * (int)U);                      // dX (fc part)
   need(256, p.fc_in + 8, 128, Fi);                     // fc weight grads (+ bias column)
   need(Fi, p.fc_in, 128, 256);                         // fc dgrad
-  need(64 * p.C, 16, 16, Fi * p.oh1 * p.ow1);          // conv1 wgrad
-  need(256, 32, 32, Fi * p.oh2 * p.ow2);              // conv2 wgrad
+  if (p.nsec == 0) {
+    need(64 * p.C, 16, 16, Fi * p.oh1 * p.ow1);        // conv1 wgrad
+    need(256, 32, 32, Fi * p.oh2 * p.ow2);            // conv2 wgrad
+  }
+  for (int sct = 0; sct < p.nsec; ++sct) {            // 3x3 weight grads
+    const DeepSec& d = p.sec[sct];
+    need(9 * d.cinp, d.ch, d.ch, Fi * d.H * d.W);
+    need(9 * d.ch, d.ch, d.ch, Fi * d.H2 * d.W2);
+  }
   w->splitk_bytes = sk;
   w->splitk = bump(cur, sk + 16);
   w->total = cur;
@@ -192,34 +258,43 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
 }
 
 // ------------------------------------------------------------------ lowp image refresh
-__global__ void refresh_lowp_kernel(const float* __restrict__ params, __nv_bfloat16* lowp,
-                                    LowpImg img) {
-  const int64_t n = (int64_t)img.rows * img.ld;
+struct ImgTable {
+  int n;
+  LowpImg img[64];
+};
+
+__global__ void refresh_lowp_multi(const float* __restrict__ params, __nv_bfloat16* lowp,
+                                   const ImgTable tab) {
+  const LowpImg& m = tab.img[blockIdx.y];
+  const int64_t n = (int64_t)m.rows * m.ld;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float v;
-    if (img.kind == IMG_COPY_PAD) {
-      const int r = (int)(i / img.ld), c = (int)(i % img.ld);
-      v = c < img.cols ? params[img.src + (int64_t)r * img.cols + c] : 0.f;
+    if (m.kind == IMG_COPY_PAD) {
+      const int r = (int)(i / m.ld), c = (int)(i % m.ld);
+      v = c < m.cols ? params[m.src + (int64_t)r * m.cols + c] : 0.f;
+    } else if (m.kind == IMG_CHAN_PAD) {
+      const int r = (int)(i / m.ld), q = (int)(i % m.ld);
+      const int t = q / m.d2, c = q % m.d2;
+      v = c < m.d3 ? params[m.src + ((int64_t)r * m.d1 + t) * m.d3 + c] : 0.f;
     } else {
-      // dst [CI][KH][KW][CO] <- src [CO][KH][KW][CI]
-      const int co = (int)(i % img.d0);
-      int64_t q = i / img.d0;
-      const int kx = (int)(q % img.d2); q /= img.d2;
-      const int ky = (int)(q % img.d1);
-      const int ci = (int)(q / img.d1);
-      v = params[img.src + (((int64_t)co * img.d1 + ky) * img.d2 + kx) * img.d3 + ci];
+      const int co = (int)(i % m.d0);
+      int64_t q = i / m.d0;
+      const int kx = (int)(q % m.d2); q /= m.d2;
+      const int ky = (int)(q % m.d1);
+      const int ci = (int)(q / m.d1);
+      v = params[m.src + (((int64_t)co * m.d1 + ky) * m.d2 + kx) * m.d3 + ci];
     }
-    lowp[img.dst + i] = __float2bfloat16_rn(v);
+    lowp[m.dst + i] = __float2bfloat16_rn(v);
   }
 }
 
 seed_status refresh_lowp(const NetPlan& p, const float* params, void* lowp, cudaStream_t st) {
-  for (int k = 0; k < p.nimg; ++k) {
-    const int64_t n = (int64_t)p.img[k].rows * p.img[k].ld;
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
-    refresh_lowp_kernel<<<blocks, 256, 0, st>>>(params, (__nv_bfloat16*)lowp, p.img[k]);
-  }
+  if (p.nimg == 0) return SEED_OK;
+  ImgTable tab;
+  tab.n = p.nimg;
+  for (int k = 0; k < p.nimg; ++k) tab.img[k] = p.img[k];
+  refresh_lowp_multi<<<dim3(64, p.nimg), 256, 0, st>>>(params, (__nv_bfloat16*)lowp, tab);
   return last_launch();
 }
 

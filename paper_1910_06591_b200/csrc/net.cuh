@@ -14,13 +14,22 @@ struct PTensor {
 };
 
 // One bf16 operand image inside params_lowp.
-enum { IMG_COPY_PAD = 0, IMG_CONV_DGRAD = 1 };
+enum { IMG_COPY_PAD = 0, IMG_CONV_DGRAD = 1, IMG_CHAN_PAD = 2 };
 struct LowpImg {
   int kind;
   int64_t src;          // fp32 element offset of the source tensor
   int64_t dst;          // bf16 element offset in params_lowp
   int rows, cols, ld;   // COPY_PAD: dst[r][c] (ld) = src[r][c] (cols) for c < cols, else 0
   int d0, d1, d2, d3;   // CONV_DGRAD: src [d0=CO][d1=KH][d2=KW][d3=CI] -> dst [CI][KH][KW][CO]
+                        // CHAN_PAD: src [rows][taps=d1][d3=C] -> dst [rows][taps][d2=Cp] (0-padded)
+};
+
+// IMPALA-deep section (C14): conv3x3 (cin -> ch) at H x W, maxpool -> H2 x W2,
+// residual blocks at H2 x W2.
+struct DeepSec {
+  int H, W, cin, cinp, ch, H2, W2, pt, pl;
+  int t_w, t_b, t_rw[2][2], t_rb[2][2];              // tensor indices
+  int64_t im_w, im_dg, im_rw[2][2], im_rdg[2][2];    // bf16 image offsets
 };
 
 struct NetPlan {
@@ -33,9 +42,12 @@ struct NetPlan {
   // tensor indices
   int i_conv1w, i_conv1b, i_conv2w, i_conv2b, i_fcw, i_fcb, i_wx, i_wh, i_lb, i_hw, i_hb;
   int i_m0w, i_m0b, i_m1w, i_m1b;
+  // IMPALA-deep sections
+  int nsec;
+  DeepSec sec[4];
   // lowp images
   int nimg;
-  LowpImg img[8];
+  LowpImg img[64];
   int64_t lowp_elems;
   int64_t im_conv1, im_conv2, im_conv2dg, im_fc, im_wx, im_wh;  // bf16 offsets
 };
@@ -55,6 +67,10 @@ struct LearnerWs {
   size_t obs_bf16, act1, act2, X, xproj, H, Hprev, gates, Cst, dG, dfc, dY2, dY1;
   // mlp
   size_t h1, h2, dh1, dh2;
+  // deep torso, per section
+  struct Sec {
+    size_t conv, arg, h[3], hr[3], u1[2], dconv, dhA, dhB, dt0;
+  } sec[4];
 };
 constexpr int NORM_BLOCKS = 296;
 constexpr int COLSUM_BLOCKS = 148;

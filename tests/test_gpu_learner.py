@@ -196,3 +196,117 @@ def test_learner_nonfinite_skips_update():
     assert g["metrics"][5] == 0.0 and g["metrics"][7] == 1.0
     assert g["step"] == 0
     np.testing.assert_array_equal(g["params"], params.astype(np.float64))
+
+
+def _deep_dims(ospec):
+    H, W, out = ospec.obs_h, ospec.obs_w, []
+    for ch in ospec.sections:
+        out.append((H, W, -(-H // 2), -(-W // 2), ch))
+        H, W = out[-1][2], out[-1][3]
+    return out
+
+
+@pytest.mark.parametrize("cfg,B,T", [("c3", 2, 3), ("c4", 2, 2), ("c3", 3, 1)])
+def test_learner_deep_parity(cfg, B, T):
+    """configs[2] (DMLab IMPALA-deep, 72x96x3) / configs[3] (GRF SMM 72x96x16), full
+    image size: 3x3 'same' convs, max-pool, residual blocks (C14).
+
+    Forward: logits/values and every section's activations vs the emulated oracle
+    (C22).  Backward: 15-20 stacked bf16 convs move activations by ~3e-3 and flip
+    ~0.05% of the ReLU masks, which alone is a few % rel-L2 on torso gradients, so
+    the torso backward is checked stage-wise: the oracle's backward of each section
+    runs on the GPU's own activations and incoming gradient (teacher forcing) and
+    every weight/bias gradient (5e-3 elementwise-scaled: fp32 reductions over up to
+    F*H*W rows, and the incoming dh of a lower section is the oracle's re-rounded dgrad),
+    dh and dconv must agree.
+    FC / LSTM / heads gradients, V-trace, loss and Adam are checked end to end."""
+    S = _S()
+    spec, ospec = _spec_pair(cfg)
+    params = seedgen.glorot_params(O.param_layout(ospec), seed=21, bias_std=0.1)
+    batch = seedgen.learner_batch((ospec.obs_h, ospec.obs_w, ospec.obs_c), ospec.num_actions, B,
+                                  T, seed=22, done_p=0.2, smm=(cfg == "c4"))
+    hp = S.HParams(lam=0.95, loss_scale=1.0 / (B * T), lr=1e-3)
+    g = _run_gpu(S, spec, params, batch, hp, B, T)
+    L = g["L"]
+    ref = O.learner_step(ospec, params, np.zeros(params.size), np.zeros(params.size), 0, batch,
+                         hp.as_oracle(), emu=True)
+    bf16_check(g["logits"], ref["logits"], "logits")
+    bf16_check(g["values"], ref["values"], "values")
+    gt, rt = _per_tensor(ospec, g["grads"]), _per_tensor(ospec, ref["grads"])
+    _check_k2_and_adam(ospec, params, batch, hp, g)
+    # heads gradients on the GPU's own output gradients and LSTM outputs (fp32 path)
+    Hh = L.debug_buffer("H", torch.float32, (B * (T + 1), 256)).cpu().numpy().astype(np.float64)
+    dl = L.debug_buffer("dlogits", torch.float32, (B * (T + 1), ospec.num_actions)).cpu().numpy()
+    dv = L.debug_buffer("dvalues", torch.float32, (B * (T + 1), 1)).cpu().numpy()
+    dout = np.concatenate([dl, dv], axis=1).astype(np.float64)
+    scaled_check(gt["heads.w"], dout.T @ Hh, 1e-4, "heads.w (teacher-forced)")
+    scaled_check(gt["heads.b"], dout.sum(0), 1e-4, "heads.b (teacher-forced)")
+    # LSTM weight gradients on the GPU's own dG, core input X and h_{t-1}
+    F0 = B * (T + 1)
+    Kx = 256 + ospec.num_actions + 1
+    dG = L.debug_buffer("dG", torch.bfloat16, (F0, 1024)).float().cpu().numpy().astype(np.float64)
+    Xg = L.debug_buffer("X", torch.bfloat16, (F0, -1)).float().cpu().numpy().astype(np.float64)
+    Hp = L.debug_buffer("Hprev", torch.bfloat16, (F0, 256)).float().cpu().numpy().astype(np.float64)
+    scaled_check(gt["lstm.wx"], dG.T @ Xg[:, :Kx], 1e-3, "lstm.wx (teacher-forced)")
+    scaled_check(gt["lstm.b"], dG.sum(0), 1e-3, "lstm.b (teacher-forced)")
+    scaled_check(gt["lstm.wh"], dG.T @ Hp, 1e-3, "lstm.wh (teacher-forced)")
+
+    # ---- forward activations per section
+    F_ = B * (T + 1)
+    P = O.unflatten(ospec, params)
+    frames = batch["obs"].reshape((F_,) + batch["obs"].shape[2:])
+    _, cache = O.torso_forward(ospec, P, frames, emu=True)
+    bf = torch.bfloat16
+    dims = _deep_dims(ospec)
+
+    def buf(s, n, shape):
+        return L.debug_buffer(f"s{s}.{n}", bf, shape).float().cpu().numpy().astype(np.float64)
+
+    for s, (H, W, H2, W2, ch) in enumerate(dims):
+        bf16_check(buf(s, "conv", (F_, H, W, ch)), cache[f"s{s}.conv"], f"s{s}.conv")
+        for r in range(2):
+            bf16_check(buf(s, f"u1{r}", (F_, H2, W2, ch)), cache[f"s{s}.res{r}"][3], f"s{s}.u1[{r}]")
+    # ---- teacher-forced backward, section by section
+    q = O.bf16_round
+    Pq = {k: q(v) for k, v in P.items()}
+    last = len(dims) - 1
+    dfc = L.debug_buffer("dfc", bf, (F_, 256)).float().cpu().numpy().astype(np.float64)
+    H, W, H2, W2, ch = dims[last]
+    hr2 = buf(last, "hr2", (F_, H2, W2, ch))
+    act2 = hr2.reshape(F_, -1)
+    scaled_check(gt["fc.w"], dfc.T @ act2, 1e-3, "fc.w (teacher-forced)")
+    scaled_check(gt["fc.b"], dfc.sum(0), 1e-3, "fc.b (teacher-forced)")
+    dh = q((dfc @ Pq["fc.w"]).reshape(F_, H2, W2, ch) * (hr2 > 0))
+    for s in range(last, -1, -1):
+        H, W, H2, W2, ch = dims[s]
+        for r in (1, 0):
+            u1 = buf(s, f"u1{r}", (F_, H2, W2, ch))
+            hr = buf(s, f"hr{r}", (F_, H2, W2, ch))
+            du1, dw1, db1 = O.conv2d_backward(u1, Pq[f"s{s}.res{r}.conv1.w"], dh, 1, 1)
+            scaled_check(gt[f"s{s}.res{r}.conv1.w"], dw1, 5e-3, f"s{s}.res{r}.conv1.w")
+            scaled_check(gt[f"s{s}.res{r}.conv1.b"], db1, 5e-3, f"s{s}.res{r}.conv1.b")
+            dt0 = q(du1 * (u1 > 0))
+            du0, dw0, db0 = O.conv2d_backward(hr, Pq[f"s{s}.res{r}.conv0.w"], dt0, 1, 1)
+            scaled_check(gt[f"s{s}.res{r}.conv0.w"], dw0, 5e-3, f"s{s}.res{r}.conv0.w")
+            scaled_check(gt[f"s{s}.res{r}.conv0.b"], db0, 5e-3, f"s{s}.res{r}.conv0.b")
+            dh = q(dh + du0 * (hr > 0))
+        bf16_check(buf(s, "dhA", (F_, H2, W2, ch)), dh, f"s{s}.dh(h0)", tol=1e-2)
+        arg = L.debug_buffer(f"s{s}.arg", torch.uint8, (F_, H2, W2, ch)).cpu().numpy()
+        cin = ospec.obs_c if s == 0 else dims[s - 1][4]
+        dconv = np.zeros((F_, H, W, ch))
+        offs = ((max((H2 - 1) * 2 + 3 - H, 0)) // 2, (max((W2 - 1) * 2 + 3 - W, 0)) // 2)
+        dconv = q(O.maxpool_same_backward((F_, H, W, ch), arg.astype(np.int64), offs,
+                                          buf(s, "dhA", (F_, H2, W2, ch))))
+        gd = buf(s, "dconv", (F_, H, W, ch))
+        bf16_check(gd, dconv, f"s{s}.dconv", tol=1e-2)
+        xin = (frames.astype(np.float64) / 255.0 if s == 0 else
+               buf(s - 1, "h2", (F_, H, W, cin)))
+        dxin, dw, db = O.conv2d_backward(xin, Pq[f"s{s}.conv.w"], gd, 1, 1, need_dx=(s > 0))
+        scaled_check(gt[f"s{s}.conv.w"], dw, 5e-3, f"s{s}.conv.w")
+        scaled_check(gt[f"s{s}.conv.b"], db, 5e-3, f"s{s}.conv.b")
+        if s > 0:
+            dh = q(dxin)
+    # end-to-end deviation of the gradients from the emulated oracle (reported; sanity bound)
+    dev = {n: np.linalg.norm(gt[n] - rt[n]) / np.linalg.norm(rt[n]) for n in gt}
+    print(cfg, "grad relL2 vs emulated (end to end):", {k: f"{v:.1e}" for k, v in dev.items()})
+    assert max(dev.values()) < 0.3
