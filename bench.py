@@ -146,7 +146,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.05)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.N:
@@ -256,6 +256,109 @@ def vtrace_leg(S, torch, T=100, B=1 << 17, iters=20):
     us = e0.elapsed_time(e1) * 1e3 / iters
     nbytes = 28 * B * T + 4 * B
     return {"T": T, "B": B, "bytes": nbytes, "us": round(us, 2), "GBs": round(nbytes / us / 1e3, 1)}
+
+
+# ---------------------------------------------------------------- inference leg (c5)
+def inference_leg(S, torch, iters=20):
+    """configs[4]: 4096 actors, per-actor LSTM state table, Atari net; one
+    seed_infer call per step over n actor ids (device-resident requests, CUDA
+    graph per n) and host-fed (pinned H2D of the n observations inside the timed
+    region).  steps/s = n / call time."""
+    import seedgen
+    NA = 4096
+    spec = S.spec_for_config("c5")
+    params = seedgen.glorot_params(S.net_param_layout(spec), seed=0)
+    learner = S.Learner(spec, 1, 1, params)
+    srv = S.InferenceServer(spec, NA, 1024, learner=learner)
+    out = {"actors": NA, "sweep": []}
+    for n in (64, 128, 256, 512, 1024):
+        req = seedgen.infer_requests((84, 84, 4), 18, NA, n, seed=0)
+        d = {k: torch.from_numpy(v).cuda() for k, v in req.items()}
+        a = torch.empty(n, dtype=torch.int32, device="cuda")
+        blp = torch.empty(n, device="cuda")
+        call = lambda st=None: srv.infer(d["actor_ids"], d["obs"], d["reward"], d["done"],
+                                         d["uniforms"], action_out=a, blp_out=blp, stream=st)
+        for _ in range(3):
+            call()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            call(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            call(s)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / iters
+        row = {"n": n, "us_per_call": round(us, 2), "steps_per_s": round(n / us * 1e6, 1)}
+        if n == 1024:   # host-fed: pinned H2D of the requests + D2H of the actions
+            hobs = torch.from_numpy(req["obs"]).pin_memory()
+            hact = torch.empty(n, dtype=torch.int32).pin_memory()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tot = 0.0
+            for _ in range(iters):
+                t0.record()
+                d["obs"].copy_(hobs, non_blocking=True)
+                g.replay()
+                hact.copy_(a, non_blocking=True)
+                t1.record()
+                torch.cuda.synchronize()
+                tot += t0.elapsed_time(t1)
+            hus = tot * 1e3 / iters
+            row.update(host_fed_us=round(hus, 2), host_fed_steps_per_s=round(n / hus * 1e6, 1),
+                       h2d_bytes=int(hobs.numel()))
+        out["sweep"].append(row)
+    return out
+
+
+def other_configs_leg(S, torch, steps=3):
+    """Learner-step timing of the other BASELINE.json configs (CUDA graph, L2
+    flushed between steps): c1 MLP fp32 (T=20, B=8), c3 DMLab IMPALA-deep
+    (T=100, B=32), c4 GRF SMM (T=32, B=128, repeat 1)."""
+    import seedgen
+    res = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for cfg, T, B, rep, kw in (("c1", 20, 8, 1, dict(float_obs=True, lstm_units=0)),
+                               ("c3", 100, 32, 4, {}), ("c4", 32, 128, 1, dict(smm=True))):
+        spec = S.spec_for_config(cfg)
+        params = seedgen.glorot_params(S.net_param_layout(spec), seed=0,
+                                       lstm_units=max(spec.lstm_units, 1))
+        L = S.Learner(spec, T, B, params, S.HParams(loss_scale=1.0 / (B * T)))
+        host = seedgen.learner_batch(spec.obs_shape, spec.num_actions, B, T, seed=1, **kw)
+        dev = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
+        L.step(dev)
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            L.step(dev, stream=s)
+        torch.cuda.synchronize()
+        g.replay()
+        ms = 0.0
+        for _ in range(steps):
+            flush.add_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        ms /= steps
+        res[cfg] = {"T": T, "B": B, "ms_per_step": round(ms, 3),
+                    "learner_frames_per_s": round(B * T * rep / (ms / 1e3), 1),
+                    "env_steps_per_s": round(B * T / (ms / 1e3), 1)}
+        del L, dev, g
+        torch.cuda.empty_cache()
+    return res
 
 
 # ---------------------------------------------------------------- ours
@@ -428,6 +531,10 @@ def run_ours(args):
                         "GBs": round(b / (us * 1e-6) / 1e9, 1) if b else None})
     vt = vtrace_leg(S, torch)
     vt["frac"] = round(vt["GBs"] / pk["hbm_gbs"], 4)
+    extra = {}
+    if world == 1 and not args.no_extra:
+        extra["inference"] = inference_leg(S, torch)
+        extra["other_configs"] = other_configs_leg(S, torch)
     line = {
         "metric": "learner frames/sec", "value": round(value, 1), "unit": "frames/s",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
@@ -447,6 +554,7 @@ def run_ours(args):
         "e2e": {"value": round(e2e_value, 1), "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "Learner.step (eager) + pinned copies"},
         "clocks": clk.summary(),
+        **extra,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(T)
@@ -458,10 +566,11 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the inference / other-config legs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
