@@ -90,6 +90,7 @@ def phase_work(T, B, A):
     w["clip_adam"] = (0, Pn * 28)
     w["lowp_refresh"] = (0, Pn * 6)
     w["allreduce"] = (0, Pn * 4 * 2)
+    w["allreduce_tail"] = (0, 12336 * 4 * 2)
     return w
 
 

@@ -385,8 +385,11 @@ __global__ void __launch_bounds__(256) splitk_finish(const Prob p, const float* 
 
 // Host launcher.  splits > 1 runs split-K into `part` ([splits][M][N] fp32,
 // caller workspace) followed by the fixed-order splitk_finish reduction.
+// max_ctas > 0 caps the persistent grid (leaves SMs free for concurrent
+// collectives on another stream).
 template <int BN, class Prob>
-seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullptr) {
+seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullptr,
+                        int max_ctas = 0) {
   using Cfg = GemmCfg<BN, Prob::A_MN, Prob::B_MN>;
   if (p.M <= 0 || p.N <= 0) return SEED_OK;
   const int nkb = (p.K + GEMM_BK - 1) / GEMM_BK;
@@ -406,7 +409,7 @@ seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullp
   }
   if (splits > 1 && !part) return SEED_E_WORKSPACE;
   const int items = ceil_div(p.M, GEMM_BM) * ceil_div(p.N, BN) * splits;
-  const int grid = std::min(items, sms);
+  const int grid = std::min(items, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   gemm_tc_kernel<BN, Prob><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(p, part, splits);
   if (splits > 1) {
     const size_t MN = (size_t)p.M * p.N;

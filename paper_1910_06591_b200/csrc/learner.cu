@@ -52,6 +52,7 @@ struct StepCtx {
   Geo g;
   Trace* tr = nullptr;
   cudaStream_t st;
+  int max_ctas = 0;   // > 0 while collectives run concurrently (SMs left for NCCL)
   template <class T>
   T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
   // end of a phase of `k` kernel launches
@@ -69,7 +70,7 @@ struct StepCtx {
 template <int BN, class Prob>
 static seed_status gemm(const StepCtx& c, Prob pr, cudaStream_t st, const char* name) {
   const int s = pick_splits(pr.M, pr.N, BN, pr.K);
-  const seed_status r = launch_gemm<BN>(pr, s, st, c.at<float>(c.w.splitk));
+  const seed_status r = launch_gemm<BN>(pr, s, st, c.at<float>(c.w.splitk), c.max_ctas);
   c.mark(name, s > 1 ? 2 : 1);
   return r;
 }
@@ -412,6 +413,8 @@ static seed_status mlp_backward(const StepCtx& c, const seed_batch* bt, const fl
 }
 
 seed_status comm_allreduce(seed_comm* comm, float* data, int64_t n, cudaStream_t st);
+seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaEvent_t* ev);
+int comm_world(const seed_comm* c);
 
 static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
                                      const seed_batch* batch, const seed_train_state* state,
@@ -478,17 +481,40 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   SEED_TRY(launch_policy_loss(la, st));
   c.mark("policy_loss");
 
+  const bool dp = comm && comm_world(comm) > 1;
   if (p.kind == SEED_NET_MLP) {
     SEED_TRY(mlp_backward(c, batch, params, grads, st));
+    if (dp) {
+      SEED_TRY(comm_allreduce(comm, grads, p.P, st));
+      c.mark("allreduce");
+    }
   } else {
     SEED_TRY(core_backward(c, batch, lowp, params, grads, st));
+    // H10 overlapped with the torso backward: the FC / LSTM / heads gradients
+    // (a contiguous tail of the flat layout, ~99% of the parameters) are final
+    // here; both buckets are reduced on the comm's side stream in the same
+    // order on every rank, and the step joins before the clip.
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev[3];
+    const int64_t tail = p.t[p.i_fcw].off;
+    if (dp) {
+      SEED_TRY(comm_side(comm, &side, ev));
+      SEED_CUDA_TRY(cudaEventRecord(ev[0], st));
+      SEED_CUDA_TRY(cudaStreamWaitEvent(side, ev[0], 0));
+      SEED_TRY(comm_allreduce(comm, grads + tail, p.P - tail, side));
+      // (capping the GEMM grids to leave SMs to NCCL measured slower at N=2)
+    }
     if (p.nsec > 0) SEED_TRY(deep_backward(c, batch, lowp, params, grads, st));
     else SEED_TRY(shallow_backward(c, batch, lowp, params, grads, st));
-  }
-
-  if (comm) {
-    SEED_TRY(comm_allreduce(comm, grads, p.P, st));
-    c.mark("allreduce");
+    if (dp) {
+      SEED_CUDA_TRY(cudaEventRecord(ev[1], st));
+      SEED_CUDA_TRY(cudaStreamWaitEvent(side, ev[1], 0));
+      SEED_TRY(comm_allreduce(comm, grads, tail, side));
+      SEED_CUDA_TRY(cudaEventRecord(ev[2], side));
+      SEED_CUDA_TRY(cudaStreamWaitEvent(st, ev[2], 0));
+      c.mark("allreduce_tail");
+      c.max_ctas = 0;
+    }
   }
 
   grad_norm_kernel<<<NORM_BLOCKS, 256, 0, st>>>(grads, p.P, c.at<double>(c.w.norm_part),
