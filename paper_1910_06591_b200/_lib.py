@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libseed.so")
+LIB_PATH = os.environ.get("SEED_LIB", os.path.join(HERE, "libseed.so"))
 
 c_int, c_float, c_void_p, c_size_t = C.c_int, C.c_float, C.c_void_p, C.c_size_t
 c_int64, c_uint64 = C.c_int64, C.c_uint64

@@ -9,7 +9,10 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libseed.so")
+# SEED_LIB / SEED_NVCC_EXTRA select a diagnostic variant (e.g. -DSEED_LSTM_PROF)
+# built beside the product library; the product build uses neither.
+LIB = os.environ.get("SEED_LIB", os.path.join(HERE, "libseed.so"))
+EXTRA = os.environ.get("SEED_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -32,14 +35,14 @@ def needs_build():
 def build(force=False, verbose=False, jobs=None):
     if not force and not needs_build():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + ("_" + os.path.basename(LIB)[:-3] if EXTRA else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
-        cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + ARCH + FLAGS + EXTRA + ["-c", src, "-o", obj]
         if verbose > 1:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -53,7 +53,8 @@ __device__ __forceinline__ float dy_at(const float* dy, int ldy, const float* dv
   return (dv && o == ldy) ? dv[r] : dy[(size_t)r * ldy + o];
 }
 
-// block = 8 rows x all I columns; W [O][I] and the 8 dY rows staged in shared memory
+// block = DG_ROWS rows x all I columns; W [O][I] and the dY rows staged in shared memory
+constexpr int DG_ROWS = 8;
 __global__ void __launch_bounds__(256) dense_dgrad_f32(int R, int I, int O, const float* __restrict__ dy,
                                                        int ldy, const float* __restrict__ dv,
                                                        const float* __restrict__ W,
@@ -61,15 +62,15 @@ __global__ void __launch_bounds__(256) dense_dgrad_f32(int R, int I, int O, cons
                                                        float* __restrict__ dX) {
   extern __shared__ float shf[];
   float* Ws = shf;              // [O][I]
-  float* ds = shf + O * I;      // [8][O]
+  float* ds = shf + O * I;      // [DG_ROWS][O]
   for (int q = threadIdx.x; q < O * I; q += blockDim.x) Ws[q] = W[q];
-  const int r0 = blockIdx.x * 8;
-  for (int q = threadIdx.x; q < 8 * O; q += blockDim.x) {
+  const int r0 = blockIdx.x * DG_ROWS;
+  for (int q = threadIdx.x; q < DG_ROWS * O; q += blockDim.x) {
     const int rr = r0 + q / O, o = q % O;
     ds[q] = rr < R ? dy_at(dy, ldy, dv, rr, o) : 0.f;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < 8 * I; q += blockDim.x) {
+  for (int q = threadIdx.x; q < DG_ROWS * I; q += blockDim.x) {
     const int rl = q / I, i = q % I, r = r0 + rl;
     if (r >= R) continue;
     float s0 = 0.f, s1 = 0.f;
@@ -143,11 +144,11 @@ seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, co
   static bool attr = false;
   if (!attr) {
     SEED_CUDA_TRY(cudaFuncSetAttribute(dense_dgrad_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (256 * 64 + 8 * 64) * 4));
+                                       (256 * 64 + DG_ROWS * 64) * 4));
     attr = true;
   }
-  const size_t smem = (size_t)(O * I + 8 * O) * 4;
-  dense_dgrad_f32<<<ceil_div(R, 8), 256, smem, st>>>(R, I, O, dy, ldy, dv, W, mask, dX);
+  const size_t smem = (size_t)(O * I + DG_ROWS * O) * 4;
+  dense_dgrad_f32<<<ceil_div(R, DG_ROWS), 256, smem, st>>>(R, I, O, dy, ldy, dv, W, mask, dX);
   return last_launch();
 }
 
@@ -307,12 +308,21 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x < C) {
+  if (last) {
     __threadfence();
+    // thread (g, c): partials k = g, g+RG, ... of column c; then RG group sums in order
+    const int RG = 256 / C, g2 = threadIdx.x / C, c2 = threadIdx.x % C;
     float t = 0.f;
-    for (int k = 0; k < (int)gridDim.x; ++k) t += part[k * C + threadIdx.x];
-    out[threadIdx.x] = t;
-    if (threadIdx.x == 0) *ticket = 0;   // re-arm for the next use
+    for (int k = g2; k < (int)gridDim.x; k += RG) t += part[k * C + c2];
+    __shared__ float red[256];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x < C) {
+      float u = 0.f;
+      for (int k = 0; k < RG; ++k) u += red[k * C + threadIdx.x];
+      out[threadIdx.x] = u;
+      if (threadIdx.x == 0) *ticket = 0;   // re-arm for the next use
+    }
   }
 }
 
@@ -369,6 +379,16 @@ __device__ __forceinline__ void lowp_write(const AdamArgs& a, int64_t i, float v
   }
 }
 
+// 4 consecutive parameters per thread (float4 when aligned); the bf16 image of
+// the group is found once per group.
+__device__ __forceinline__ int find_img(const AdamArgs& a, int64_t i) {
+  for (int k = 0; k < a.nimg; ++k) {
+    const int64_t e = i - a.img[k].src;
+    if (e >= 0 && e < (int64_t)a.img[k].rows * a.img[k].cols) return k;
+  }
+  return -1;
+}
+
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
   __shared__ double tot;
   if (threadIdx.x == 0) {
@@ -384,16 +404,65 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
     const float scale = norm > (double)a.max_norm ? (float)((double)a.max_norm / norm) : 1.f;
     const float bc1 = (float)(1.0 - pow((double)a.beta1, (double)t));
     const float bc2 = (float)(1.0 - pow((double)a.beta2, (double)t));
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.P;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      const float g = a.grads[i] * scale;
-      const float m = a.beta1 * a.m[i] + (1.f - a.beta1) * g;
-      const float v = a.beta2 * a.v[i] + (1.f - a.beta2) * g * g;
-      a.m[i] = m;
-      a.v[i] = v;
-      const float p = a.params[i] - a.lr * (m / bc1) / (sqrtf(v / bc2) + a.eps);
-      a.params[i] = p;
-      if (a.nimg) lowp_write(a, i, p);
+    const int64_t ngroups = (a.P + 3) / 4;
+    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ngroups;
+         gi += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i0 = gi * 4;
+      float g[4], m[4], v[4], p[4];
+      const bool full = i0 + 3 < a.P;
+      if (full) {
+        const float4 G = reinterpret_cast<const float4*>(a.grads)[gi];
+        const float4 M = reinterpret_cast<const float4*>(a.m)[gi];
+        const float4 V = reinterpret_cast<const float4*>(a.v)[gi];
+        const float4 Pp = reinterpret_cast<const float4*>(a.params)[gi];
+        g[0] = G.x; g[1] = G.y; g[2] = G.z; g[3] = G.w;
+        m[0] = M.x; m[1] = M.y; m[2] = M.z; m[3] = M.w;
+        v[0] = V.x; v[1] = V.y; v[2] = V.z; v[3] = V.w;
+        p[0] = Pp.x; p[1] = Pp.y; p[2] = Pp.z; p[3] = Pp.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool ok = i0 + q < a.P;
+          g[q] = ok ? a.grads[i0 + q] : 0.f;
+          m[q] = ok ? a.m[i0 + q] : 0.f;
+          v[q] = ok ? a.v[i0 + q] : 0.f;
+          p[q] = ok ? a.params[i0 + q] : 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float gg = g[q] * scale;
+        m[q] = a.beta1 * m[q] + (1.f - a.beta1) * gg;
+        v[q] = a.beta2 * v[q] + (1.f - a.beta2) * gg * gg;
+        p[q] = p[q] - a.lr * (m[q] / bc1) / (sqrtf(v[q] / bc2) + a.eps);
+      }
+      if (full) {
+        reinterpret_cast<float4*>(a.m)[gi] = make_float4(m[0], m[1], m[2], m[3]);
+        reinterpret_cast<float4*>(a.v)[gi] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(a.params)[gi] = make_float4(p[0], p[1], p[2], p[3]);
+      } else {
+        for (int q = 0; q < 4 && i0 + q < a.P; ++q) {
+          a.m[i0 + q] = m[q];
+          a.v[i0 + q] = v[q];
+          a.params[i0 + q] = p[q];
+        }
+      }
+      if (a.nimg) {
+        const int k0 = find_img(a, i0);
+        const int k3 = find_img(a, min(i0 + 3, a.P - 1));
+        if (k0 >= 0 && k0 == k3 && a.img[k0].kind == IMG_COPY_PAD) {
+          const LowpImg& im = a.img[k0];
+          const int64_t e = i0 - im.src;
+          const int64_t r = e / im.cols, c = e % im.cols;
+          if (c + 3 < im.cols) {   // the group stays in one image row
+            __nv_bfloat16* d = a.lowp + im.dst + r * im.ld + c;
+            d[0] = __float2bfloat16_rn(p[0]); d[1] = __float2bfloat16_rn(p[1]);
+            d[2] = __float2bfloat16_rn(p[2]); d[3] = __float2bfloat16_rn(p[3]);
+            continue;
+          }
+        }
+        for (int q = 0; q < 4 && i0 + q < a.P; ++q) lowp_write(a, i0 + q, p[q]);
+      }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -419,7 +488,8 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
 }
 
 seed_status launch_clip_adam(const AdamArgs& a, cudaStream_t st) {
-  adam_kernel<<<148 * 8, 256, 0, st>>>(a);
+  const int64_t groups = (a.P + 3) / 4;
+  adam_kernel<<<(int)std::min<int64_t>((groups + 255) / 256, 148 * 8), 256, 0, st>>>(a);
   return last_launch();
 }
 

@@ -50,6 +50,11 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t (&r)[2]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r[0]), "=r"(r[1])
+               : "r"(addr));
+}
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -63,21 +68,36 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-// ex2-based activations (the cell is fp32; these are within a few ulp of the
-// libm versions, far below the bf16 rounding of the recurrent operands)
-__device__ __forceinline__ float sigm(float x) { return __frcp_rn(1.f + __expf(-x)); }
+// ex2 / rcp.approx activations (MUFU.EX2 + MUFU.RCP, no IEEE-division slow
+// path on the serial critical path); the cell is fp32 and these are within a
+// few ulp of the libm versions (relative 2^-15 for |x| << 1 in tanh), far below
+// the bf16 rounding of the recurrent operands.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sigm(float x) { return rcp_approx(1.f + __expf(-x)); }
 __device__ __forceinline__ float tanh_fast(float x) {
   const float e = __expf(-2.f * fabsf(x));
-  const float t = (1.f - e) * __frcp_rn(1.f + e);
+  const float t = (1.f - e) * rcp_approx(1.f + e);
   return copysignf(t, x);
 }
 
 // CTA r's W_h slice: local row lc = gate*32 + j  <-  global row gate*U + 32r + j
+// (blockDim 256: 16 chunks per thread, all loads issued before the first store)
 __device__ __forceinline__ void load_wh_slice(__nv_bfloat16* Ws, const __nv_bfloat16* wh, int r) {
-  for (int c = threadIdx.x; c < 128 * 32; c += blockDim.x) {
-    const int lc = c >> 5, kc = c & 31;
+  uint4 v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int c = threadIdx.x + 256 * q, lc = c >> 5, kc = c & 31;
     const int gr = (lc >> 5) * LSTM_U + 32 * r + (lc & 31);
-    *reinterpret_cast<uint4*>(Ws + lc * HP + kc * 8) = ld16(wh + (size_t)gr * LSTM_U + kc * 8);
+    v[q] = ld16(wh + (size_t)gr * LSTM_U + kc * 8);
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int c = threadIdx.x + 256 * q, lc = c >> 5, kc = c & 31;
+    *reinterpret_cast<uint4*>(Ws + lc * HP + kc * 8) = v[q];
   }
 }
 
@@ -102,11 +122,26 @@ __device__ __forceinline__ void mbar_arm_tx(uint64_t* bar, uint32_t bytes) {
 }
 
 constexpr int MAX_T1 = 257;
-// BB = batch rows per cluster (template); the MMA tiles cover MR = max(BB, 16) rows
+
+#ifdef SEED_LSTM_PROF
+// diagnostic build only: per-step clock64 stamps of CTA 0, thread 0
+// [kernel 0 fwd / 1 bwd][step][stamp 0..3]
+__device__ long long g_lstm_prof[2][MAX_T1 + 1][4];
+#define LSTM_STAMP(K, T, I) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_lstm_prof[K][T][I] = clock64();
+extern "C" int seed_debug_lstm_prof(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_lstm_prof, sizeof(g_lstm_prof)) == cudaSuccess ? 0 : 5;
+}
+#else
+#define LSTM_STAMP(K, T, I)
+#endif
+// BB = batch rows per cluster (template, multiple of 8).  The recurrent
+// products put the 16-row MMA side on the gate / hidden columns and the batch
+// rows on the 8-wide N side (NT = BB/8 n-tiles), so no MMA row is padding.
 template <int BB>
 struct LstmCfg {
-  static constexpr int MR = BB < 16 ? 16 : BB;
-  static constexpr int MT = MR / 16;
+  static constexpr int MR = BB;
+  static constexpr int NT = MR / 8;
   static constexpr int FWD_SMEM =
       128 * HP * 2 + 2 * MR * HP * 2 + MR * GP * 4 + MR * 32 * 4 + 32 * MAX_T1 + 64;
   static constexpr int BWD_SMEM =
@@ -118,8 +153,9 @@ struct LstmCfg {
 template <int BBT>
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_fwd_kernel(const LstmFwdArgs a) {
+  LSTM_STAMP(0, MAX_T1, 0)
   using Cfg = LstmCfg<BBT>;
-  constexpr int U = LSTM_U, MR = Cfg::MR, MT = Cfg::MT;
+  constexpr int U = LSTM_U, MR = Cfg::MR, NT = Cfg::NT;
   extern __shared__ __align__(16) uint8_t sm[];
   __nv_bfloat16* Ws = reinterpret_cast<__nv_bfloat16*>(sm);
   __nv_bfloat16* hb = Ws + 128 * HP;
@@ -138,20 +174,23 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     mbar_init(&hbar[1], 1);
     fence_mbar_init();
   }
-  load_wh_slice(Ws, a.wh, r);
   for (int i = tid; i < BBT * T1; i += 256) {
     const int b = i / T1, t = i % T1;
     dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
   }
-  for (int idx = tid; idx < MR * U; idx += 256) {
-    const int b = idx / U, k = idx % U;
-    float v = 0.f;
-    if (b < BB) {
+  load_wh_slice(Ws, a.wh, r);
+  __syncthreads();   // dn_s visible: the initial state reads use its step-0 flags
+  // bf16 h_{-1} for all MR rows (zero past B and on a step-0 reset), float4 reads
+#pragma unroll
+  for (int q = 0; q < MR * U / 4 / 256; ++q) {
+    const int idx = tid + 256 * q, b = idx / (U / 4), k = (idx % (U / 4)) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (b < BB && !dn_s[b * T1]) {
       const int bb = b0 + b;
       const int srow = a.state_rows ? a.state_rows[bb] : bb;
-      if (!a.done[(size_t)bb * T1]) v = a.h0[(size_t)srow * U + k];
+      v = *reinterpret_cast<const float4*>(a.h0 + (size_t)srow * U + k);
     }
-    hb[b * HP + k] = __float2bfloat16_rn(v);
+    *reinterpret_cast<uint2*>(hb + b * HP + k) = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
   }
   for (int idx = tid; idx < MR * 32; idx += 256) {
     const int b = idx >> 5, j = idx & 31;
@@ -159,7 +198,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     if (b < BB) {
       const int bb = b0 + b;
       const int srow = a.state_rows ? a.state_rows[bb] : bb;
-      if (!a.done[(size_t)bb * T1]) {
+      if (!dn_s[b * T1]) {
         c = a.c0[(size_t)srow * U + 32 * r + j];
         h = a.h0[(size_t)srow * U + 32 * r + j];
       }
@@ -169,6 +208,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   }
   __syncthreads();
   cluster_sync_all();   // barriers initialised everywhere before any st.async
+  LSTM_STAMP(0, MAX_T1, 1)
 
   // per-thread cell work: NQ (row, unit pair) items; BBT*16 items per CTA
   constexpr int NQ = (BBT * 16 + 255) / 256;
@@ -202,41 +242,51 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   const int gid = lane >> 2, tig = lane & 3;
   for (int t = 0; t < T1; ++t) {
     const int cur = t & 1, nbuf = cur ^ 1;
+    LSTM_STAMP(0, t, 0)
     if (tid == 0 && t + 1 < T1) mbar_arm_tx(&hbar[nbuf], Cfg::H_TX_BYTES);
     if (t > 0) mbar_wait(&hbar[cur], ((t - 1) >> 1) & 1);
+    LSTM_STAMP(0, t, 1)
     const __nv_bfloat16* hcur = hb + cur * MR * HP;
-    float acc[MT][2][4];
+    // z^T[gate col][b] = W_h slice (A, 16 gate rows per warp) x h^T (B, NT
+    // n-tiles of 8 batch rows); four independent K chains (ks mod 4) shorten
+    // the dependent HMMA sequence, summed in fixed order afterwards.
+    float acc[4][NT][4];
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < NT; ++j)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.f;
-#pragma unroll 4
+    const int mi = lane >> 3;
+#pragma unroll
     for (int ks = 0; ks < 16; ++ks) {
-      uint32_t af[MT][4], bfr[4];
+      uint32_t af[4];
+      ldsm_x4(smem_u32(Ws + (warp * 16 + (lane & 15)) * HP + ks * 16 + (lane >> 4) * 8), af);
+      if constexpr (NT == 1) {
+        uint32_t b2[2];
+        ldsm_x2(smem_u32(hcur + (lane & 7) * HP + ks * 16 + (mi & 1) * 8), b2);
+        mma16816(acc[ks & 3][0], af, b2[0], b2[1]);
+      } else {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-        ldsm_x4(smem_u32(hcur + (mt * 16 + (lane & 15)) * HP + ks * 16 + (lane >> 4) * 8), af[mt]);
-      const int mi = lane >> 3;
-      ldsm_x4(smem_u32(Ws + (warp * 16 + (mi >> 1) * 8 + (lane & 7)) * HP + ks * 16 + (mi & 1) * 8),
-              bfr);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        mma16816(acc[mt][0], af[mt], bfr[0], bfr[1]);
-        mma16816(acc[mt][1], af[mt], bfr[2], bfr[3]);
+        for (int np = 0; np < NT / 2; ++np) {
+          uint32_t bfr[4];
+          ldsm_x4(smem_u32(hcur + (np * 16 + (mi >> 1) * 8 + (lane & 7)) * HP + ks * 16 + (mi & 1) * 8),
+                  bfr);
+          mma16816(acc[ks & 3][2 * np], af, bfr[0], bfr[1]);
+          mma16816(acc[ks & 3][2 * np + 1], af, bfr[2], bfr[3]);
+        }
       }
     }
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int row = mt * 16 + gid, col = warp * 16 + nt * 8 + tig * 2;
-        *reinterpret_cast<float2*>(gpre + row * GP + col) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
-        *reinterpret_cast<float2*>(gpre + (row + 8) * GP + col) =
-            make_float2(acc[mt][nt][2], acc[mt][nt][3]);
+      for (int q = 0; q < 4; ++q) {
+        const float v = (acc[0][nt][q] + acc[1][nt][q]) + (acc[2][nt][q] + acc[3][nt][q]);
+        const int col = warp * 16 + gid + (q >> 1) * 8, row = nt * 8 + tig * 2 + (q & 1);
+        gpre[row * GP + col] = v;
       }
     __syncthreads();
+    LSTM_STAMP(0, t, 2)
     float2 xc[NQ][4];
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
@@ -298,15 +348,18 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
       }
     }
     __syncthreads();   // gpre / cst reuse
+    LSTM_STAMP(0, t, 3)
   }
+  LSTM_STAMP(0, MAX_T1, 2)
   cluster_sync_all();
 }
 
 template <int BBT>
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_bwd_kernel(const LstmBwdArgs a) {
+  LSTM_STAMP(1, MAX_T1, 0)
   using Cfg = LstmCfg<BBT>;
-  constexpr int U = LSTM_U, MR = Cfg::MR, MT = Cfg::MT;
+  constexpr int U = LSTM_U, MR = Cfg::MR, NT = Cfg::NT;
   extern __shared__ __align__(16) uint8_t sm[];
   __nv_bfloat16* Ws = reinterpret_cast<__nv_bfloat16*>(sm);
   __nv_bfloat16* dzs = Ws + 128 * HP;
@@ -334,6 +387,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   for (int i = tid; i < MR * 32; i += 256) dcs[i] = 0.f;
   __syncthreads();
   cluster_sync_all();
+  LSTM_STAMP(1, MAX_T1, 1)
 
   // per-thread cell work: NQ (row, unit) items; prefetched per step
   constexpr int NQ = (BBT * 32 + 255) / 256;
@@ -368,8 +422,10 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   for (int u = 0; u < T1; ++u) {
     const int t = T1 - 1 - u;
     // partials produced at step u land in buffer u&1; consumed at step u+1
+    LSTM_STAMP(1, u, 0)
     if (tid == 0 && t > 0) mbar_arm_tx(&rbar[u & 1], Cfg::R_TX_BYTES);
     if (u > 0) mbar_wait(&rbar[(u - 1) & 1], ((u - 1) >> 1) & 1);
+    LSTM_STAMP(1, u, 1)
     const float* rin = red + ((u - 1) & 1) * 8 * MR * RP;
     float cdh[NQ], cg[NQ][4], cc[NQ], ccp[NQ];
 #pragma unroll
@@ -418,49 +474,66 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
       }
     }
     __syncthreads();
+    LSTM_STAMP(1, u, 2)
     if (t > 0) {
-      float acc[MT][4][4];
+      // partial dh^T[j][b] over this CTA's 128 gate columns: A = W_h slice^T
+      // (2 m-tiles of 16 hidden units owned by CTA `warp`), B = dz^T (NT
+      // n-tiles of 8 batch rows); two K chains (ks parity), fixed-order sum.
+      float acc[2][2][NT][4];
 #pragma unroll
-      for (int i = 0; i < MT; ++i)
+      for (int c2 = 0; c2 < 2; ++c2)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.f;
+          for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[c2][i][j][q] = 0.f;
+      const int mi = lane >> 3;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        uint32_t af[MT][4];
+        uint32_t af[2][4];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-          ldsm_x4(smem_u32(dzs + (mt * 16 + (lane & 15)) * DP + ks * 16 + (lane >> 4) * 8),
-                  af[mt]);
-        const int mi = lane >> 3;
+        for (int mt = 0; mt < 2; ++mt)
+          ldsm_x4_t(smem_u32(Ws + (ks * 16 + (mi >> 1) * 8 + (lane & 7)) * HP + 32 * warp + mt * 16 +
+                             (mi & 1) * 8),
+                    af[mt]);
+        if constexpr (NT == 1) {
+          uint32_t b2[2];
+          ldsm_x2(smem_u32(dzs + (lane & 7) * DP + ks * 16 + (mi & 1) * 8), b2);
 #pragma unroll
-        for (int np = 0; np < 2; ++np) {
-          uint32_t bfr[4];
-          ldsm_x4_t(smem_u32(Ws + (ks * 16 + (mi & 1) * 8 + (lane & 7)) * HP + 32 * warp +
-                             np * 16 + (mi >> 1) * 8),
+          for (int mt = 0; mt < 2; ++mt) mma16816(acc[ks & 1][mt][0], af[mt], b2[0], b2[1]);
+        } else {
+#pragma unroll
+          for (int np = 0; np < NT / 2; ++np) {
+            uint32_t bfr[4];
+            ldsm_x4(smem_u32(dzs + (np * 16 + (mi >> 1) * 8 + (lane & 7)) * DP + ks * 16 + (mi & 1) * 8),
                     bfr);
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            mma16816(acc[mt][2 * np], af[mt], bfr[0], bfr[1]);
-            mma16816(acc[mt][2 * np + 1], af[mt], bfr[2], bfr[3]);
+            for (int mt = 0; mt < 2; ++mt) {
+              mma16816(acc[ks & 1][mt][2 * np], af[mt], bfr[0], bfr[1]);
+              mma16816(acc[ks & 1][mt][2 * np + 1], af[mt], bfr[2], bfr[3]);
+            }
           }
         }
       }
-      // columns [32*warp, 32*warp+32) belong to CTA `warp`: its slot r of buffer u&1
+      // hidden units [32*warp, 32*warp+32) belong to CTA `warp`: its slot r of buffer u&1
       const uint32_t base = rred[warp] + (uint32_t)(((u & 1) * 8 + r) * MR * RP * 4);
       const uint32_t rb = rrb[u & 1][warp];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const int row = mt * 16 + gid, j = nt * 8 + tig * 2;
-          st_async_f32x2(base + (row * RP + j) * 4, acc[mt][nt][0], acc[mt][nt][1], rb);
-          st_async_f32x2(base + ((row + 8) * RP + j) * 4, acc[mt][nt][2], acc[mt][nt][3], rb);
-        }
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = mt * 16 + gid + (q >> 1) * 8, row = nt * 8 + tig * 2 + (q & 1);
+            st_async_u32(base + (row * RP + j) * 4,
+                         __float_as_uint(acc[0][mt][nt][q] + acc[1][mt][nt][q]), rb);
+          }
     }
     __syncthreads();   // dzs / dcs reuse
+    LSTM_STAMP(1, u, 3)
   }
+  LSTM_STAMP(1, MAX_T1, 2)
   cluster_sync_all();
 }
 
