@@ -173,6 +173,35 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, bool a_mn, 
          | ((uint32_t)(M >> 4) << 24);  // M / 16
 }
 
+// Pre-swizzled row storage: 16-byte chunk j of row `row` (rb bytes per row,
+// rb in {32, 64, 128}) sits at chunk position swz_chunk(row, rb, j) — the
+// 32B / 64B / 128B swizzle of the byte address (bits [4:..] ^= bits [7:..]) for
+// a 1024-aligned buffer, so a linear copy that keeps the address phase lands
+// the rows in the canonical UMMA layout.
+__host__ __device__ __forceinline__ int swz_chunk(int64_t row, int rb, int j) {
+  return rb == 128 ? (j ^ (int)(row & 7)) : rb == 64 ? (j ^ (int)((row >> 1) & 3))
+                                                     : (j ^ (int)((row >> 2) & 1));
+}
+__host__ __device__ constexpr uint32_t swz_layout_code(int rb) {   // UMMA descriptor layout type
+  return rb == 128 ? 2u : rb == 64 ? 4u : 6u;
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// TMA bulk copy global -> shared (16-byte aligned, size multiple of 16),
+// completion counted on `bar` in bytes
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------- bf16 helpers
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);

@@ -28,6 +28,7 @@
 #include "lstm.cuh"
 #include "net.cuh"
 #include "shallow_net.cuh"
+#include "conv_s2d.cuh"
 
 namespace seed {
 
@@ -47,8 +48,9 @@ static seed_status make_infer_ws(const NetPlan& p, int n, InferWs* w) {
   w->n = n;
   size_t cur = 0;
   const size_t N = n;
-  w->obs_bf16 = ibump(cur, N * p.H * p.W * p.C * 2);
-  w->act1 = ibump(cur, N * p.oh1 * p.ow1 * 16 * 2);
+  const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
+  w->obs_bf16 = ibump(cur, s2d_S0_bytes(sg, N));   // S0 (conv_s2d.cuh)
+  w->act1 = ibump(cur, s2d_S1_bytes(sg, N));       // S1
   w->act2 = ibump(cur, N * p.fc_in * 2);
   w->X = ibump(cur, N * p.Kxp * 2);
   w->xproj = ibump(cur, N * 4 * p.U * 4);
@@ -311,9 +313,6 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
   auto at = [&](size_t off) { return base + off; };
   const bf16* lowp = (const bf16*)params_lowp;
   const int U = p.U, A = p.A;
-  Geo g{p.H, p.W, p.C, p.oh1, p.ow1, p.oh2, p.ow2, p.fc_in, p.Kx, p.Kxp,
-        FastDiv((uint32_t)(p.oh1 * p.ow1)), FastDiv((uint32_t)p.ow1),
-        FastDiv((uint32_t)(p.oh2 * p.ow2)), FastDiv((uint32_t)p.ow2)};
   float* splitk = (float*)at(w.splitk);
   {
     const int64_t tot = (int64_t)n * (U + p.Kxp - 256);
@@ -321,25 +320,10 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
         n, A, U, p.Kxp, actor_ids, reward, done, table->h, table->c, table->last_action,
         (float*)at(w.hpre), (float*)at(w.cpre), (int32_t*)at(w.prev), (bf16*)at(w.X));
   }
-  {
-    const int64_t n16 = (int64_t)n * p.H * p.W * p.C / 16;
-    obs_to_bf16_kernel<<<(int)std::min<int64_t>((n16 + 255) / 256, 148 * 16), 256, 0, st>>>(
-        obs, (bf16*)at(w.obs_bf16), n16);
-  }
-  {
-    Conv1Fwd pr{};
-    pr.M = n * p.oh1 * p.ow1; pr.N = 16; pr.K = 64 * p.C; pr.g = g;
-    pr.obs = (const bf16*)at(w.obs_bf16); pr.w = lowp + p.im_conv1;
-    pr.bias = params + p.t[p.i_conv1b].off; pr.out = (bf16*)at(w.act1);
-    SEED_TRY(launch_gemm<16>(pr, pick_splits(pr.M, pr.N, 16, pr.K), st, splitk));
-  }
-  {
-    Conv2Fwd pr{};
-    pr.M = n * p.oh2 * p.ow2; pr.N = 32; pr.K = 256; pr.g = g;
-    pr.act1 = (const bf16*)at(w.act1); pr.w = lowp + p.im_conv2;
-    pr.bias = params + p.t[p.i_conv2b].off; pr.out = (bf16*)at(w.act2);
-    SEED_TRY(launch_gemm<32>(pr, pick_splits(pr.M, pr.N, 32, pr.K), st, splitk));
-  }
+  SEED_TRY(shallow_s2d_forward(shallow_s2d_geometry(p.H, p.W, p.C), n, obs, lowp + p.im_conv1,
+                               params + p.t[p.i_conv1b].off, lowp + p.im_conv2,
+                               params + p.t[p.i_conv2b].off, (uint8_t*)at(w.obs_bf16),
+                               (uint8_t*)at(w.act1), (bf16*)at(w.act2), nullptr, st));
   {
     FcFwd pr{};
     pr.M = n; pr.N = 256; pr.K = p.fc_in; pr.Kxp = p.Kxp;

@@ -2,10 +2,10 @@
 // GPU's [B][T+1] shard, with the DP gradient
 // allreduce (H10) when a communicator is given.
 //
-// Atari-shallow path (configs[1]; C14), every dense contraction on the
-// tcgen05 engine (gemm_tc.cuh), activations bf16 NHWC, rows f = b*(T+1)+t:
-//   conv1  implicit GEMM  [F*400 x 256] . [256 x 16]    (uint8 obs, /255 in the epilogue)
-//   conv2  implicit GEMM  [F*81  x 256] . [256 x 32]
+// Atari-shallow path (configs[1]; C14), every dense contraction on tcgen05,
+// rows f = b*(T+1)+t:
+//   obs -> S0 (space-to-depth, bf16, pre-swizzled), conv1 / conv2 as 2x2
+//   shifted-window GEMMs over TMA-loaded slabs (conv_s2d.cuh)
 //   fc     GEMM           [F x 2592] . [2592 x 256]       (split-K)
 //   Xproj  GEMM           [F x 288]  . [288 x 1024]       (+ bias; x = [fc, onehot, r, 1])
 //   LSTM   persistent cluster kernel, T+1 serial steps (lstm.cu)
@@ -14,11 +14,9 @@
 //   dW_x|b|dW_h  one GEMM  [1024 x F] . [F x (288+256)]    (ones column -> bias grad)
 //   dfc    GEMM  [F x 1024] . [1024 x 256]   (ReLU mask)
 //   dW_fc|b  GEMM [256 x F] . [F x 2600]    (ones column -> bias grad)
-//   dY2    GEMM  [F x 256] . [256 x 2592]   (ReLU mask)
-//   dW2    GEMM  [256 x F*81] . [F*81 x 32] (split-K)
-//   dY1    sub-pixel transposed-conv GEMM [4*F*100 x 128] . [128 x 4*16] (ReLU mask)
-//   dW1    GEMM  [256 x F*400] . [F*400 x 16] (split-K, /255)
-//   conv biases: deterministic column sums
+//   dY2    GEMM  [F x 256] . [256 x 2592]   (ReLU mask; written in conv2 s2d row space)
+//   dW2|db2, dY1 (masked), dW1|db1: window GEMMs (conv_s2d.cuh; all-ones operand
+//   for the bias sums, fixed-order split-K finish)
 //   [allreduce] -> global-norm clip + Adam -> bf16 operand image refresh
 #include <string.h>
 #include <utility>
@@ -28,6 +26,7 @@
 #include "net.cuh"
 #include "deep_net.cuh"
 #include "shallow_net.cuh"
+#include "conv_s2d.cuh"
 
 namespace seed {
 
@@ -75,33 +74,24 @@ static seed_status gemm(const StepCtx& c, Prob pr, cudaStream_t st, const char* 
   return r;
 }
 
-// Atari-shallow torso: obs -> act2 (H1)
+// Atari-shallow torso: obs -> act2 (H1), space-to-depth window convolutions
+// (conv_s2d.cuh); conv2's epilogue also zeroes the padding rows of dY2
 static seed_status shallow_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                    const float* params, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
   const int F = w.F;
-  {
-    const int64_t n16 = (int64_t)F * p.H * p.W * p.C / 16;
-    obs_to_bf16_kernel<<<(int)std::min<int64_t>((n16 + 255) / 256, 148 * 16), 256, 0, st>>>(
-        (const uint8_t*)bt->obs, c.at<bf16>(w.obs_bf16), n16);
-    c.mark("obs_bf16");
-  }
-  {
-    Conv1Fwd pr{};
-    pr.M = F * p.oh1 * p.ow1; pr.N = 16; pr.K = 64 * p.C;
-    pr.g = c.g; pr.obs = c.at<bf16>(w.obs_bf16); pr.w = lowp + p.im_conv1;
-    pr.bias = params + p.t[p.i_conv1b].off; pr.out = c.at<bf16>(w.act1);
-    SEED_TRY(gemm<16>(c, pr, st, "conv1_fwd"));
-  }
-  {
-    Conv2Fwd pr{};
-    pr.M = F * p.oh2 * p.ow2; pr.N = 32; pr.K = 256;
-    pr.g = c.g; pr.act1 = c.at<bf16>(w.act1); pr.w = lowp + p.im_conv2;
-    pr.bias = params + p.t[p.i_conv2b].off; pr.out = c.at<bf16>(w.act2);
-    SEED_TRY(gemm<32>(c, pr, st, "conv2_fwd"));
-  }
-  return last_launch();
+  const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
+  SEED_TRY(s2d_obs((const uint8_t*)bt->obs, F, p.H, p.W, c.at<uint8_t>(w.obs_bf16), st));
+  c.mark("obs_s2d");
+  SEED_TRY(shallow_s2d_conv1(sg, F, c.at<uint8_t>(w.obs_bf16), lowp + p.im_conv1,
+                             params + p.t[p.i_conv1b].off, c.at<uint8_t>(w.act1), st));
+  c.mark("conv1_fwd");
+  SEED_TRY(shallow_s2d_conv2(sg, F, c.at<uint8_t>(w.act1), lowp + p.im_conv2,
+                             params + p.t[p.i_conv2b].off, c.at<bf16>(w.act2),
+                             c.at<uint8_t>(w.dY2), st));
+  c.mark("conv2_fwd");
+  return SEED_OK;
 }
 
 // FC + LSTM core + heads over the flattened torso output w.act2 (H2-H4)
@@ -198,51 +188,34 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
     pr.M = F; pr.N = p.fc_in; pr.K = 256;
     pr.dfc = c.at<bf16>(w.dfc); pr.w = lowp + p.im_fc; pr.act2 = c.at<bf16>(w.act2);
     pr.dY2 = c.at<bf16>(w.dY2);
+    if (p.nsec == 0) {   // Atari-shallow: conv2 output space rows (conv_s2d.cuh)
+      const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
+      pr.dY2s = c.at<uint8_t>(w.dY2); pr.Wo = sg.g2.Wo; pr.W2s = sg.g2.Ws; pr.P2 = sg.g2.P;
+    }
     SEED_TRY(gemm<128>(c, pr, st, "fc_dgrad"));
   }
   return SEED_OK;
 }
 
-// Atari-shallow torso backward from w.dY2 (H9)
+// Atari-shallow torso backward from w.dY2 (H9): dW2|db2, dY1 (masked), dW1|db1
 static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                     const float* params, float* grads, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
   const int F = w.F;
-  {
-    Conv2Wgrad pr{};
-    pr.M = 256; pr.N = 32; pr.K = F * p.oh2 * p.ow2; pr.g = c.g;
-    pr.act1 = c.at<bf16>(w.act1); pr.dY2 = c.at<bf16>(w.dY2);
-    pr.g_w = grads + p.t[p.i_conv2w].off;
-    SEED_TRY(gemm<32>(c, pr, st, "conv2_wgrad"));
-  }
-  SEED_TRY(colsum_bf16(c.at<bf16>(w.dY2), (int64_t)F * p.oh2 * p.ow2, 32,
-                       c.at<float>(w.colsum_part), grads + p.t[p.i_conv2b].off, st));
-  c.mark("conv2_bias");
-  {
-    Conv2Dgrad pr{};
-    const int QH = (p.oh1 + 1) / 2, QW = (p.ow1 + 1) / 2;
-    pr.F = F; pr.QH = QH; pr.QW = QW;
-    pr.fcls = FastDiv((uint32_t)(F * QH * QW)); pr.fq = FastDiv((uint32_t)(QH * QW));
-    pr.fqw = FastDiv((uint32_t)QW);
-    pr.M = 4 * F * QH * QW; pr.N = 64; pr.K = 128; pr.g = c.g;   // k = (kyi, kxi, co)
-    pr.dY2 = c.at<bf16>(w.dY2); pr.wdg = lowp + p.im_conv2dg; pr.act1 = c.at<bf16>(w.act1);
-    pr.dY1 = c.at<bf16>(w.dY1);
-    SEED_TRY(gemm<64>(c, pr, st, "conv2_dgrad"));
-  }
-  {
-    Conv1Wgrad pr{};
-    pr.M = 64 * p.C; pr.N = 16; pr.K = F * p.oh1 * p.ow1; pr.g = c.g;
-    pr.obs = c.at<bf16>(w.obs_bf16); pr.dY1 = c.at<bf16>(w.dY1);
-    pr.g_w = grads + p.t[p.i_conv1w].off;
-    SEED_TRY(gemm<16>(c, pr, st, "conv1_wgrad"));
-  }
-  SEED_TRY(colsum_bf16(c.at<bf16>(w.dY1), (int64_t)F * p.oh1 * p.ow1, 16,
-                       c.at<float>(w.colsum_part), grads + p.t[p.i_conv1b].off, st));
-  c.mark("conv1_bias");
+  const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
+  float* part = c.at<float>(w.splitk);
+  SEED_TRY(shallow_s2d_conv2_wgrad(sg, F, c.at<uint8_t>(w.act1), c.at<uint8_t>(w.dY2), part,
+                                   grads + p.t[p.i_conv2w].off, grads + p.t[p.i_conv2b].off, st));
+  c.mark("conv2_wgrad", 2);
+  SEED_TRY(shallow_s2d_conv2_dgrad(sg, F, c.at<uint8_t>(w.dY2), lowp + p.im_conv2dg,
+                                   c.at<uint8_t>(w.act1), c.at<uint8_t>(w.dY1), st));
+  c.mark("conv2_dgrad");
+  SEED_TRY(shallow_s2d_conv1_wgrad(sg, F, c.at<uint8_t>(w.obs_bf16), c.at<uint8_t>(w.dY1), part,
+                                   grads + p.t[p.i_conv1w].off, grads + p.t[p.i_conv1b].off, st));
+  c.mark("conv1_wgrad", 2);
   return SEED_OK;
 }
-
 
 // ------------------------------------------------------------------ IMPALA-deep torso
 static Conv3Geo c3geo(int H, int W, int cin, int cout) {

@@ -337,12 +337,21 @@ seed_status colsum_bf16(const __nv_bfloat16* X, int64_t R, int C, float* part, f
 // ------------------------------------------------------------------ K9 clip + Adam
 __global__ void grad_norm_kernel(const float* __restrict__ g, int64_t P, double* __restrict__ part,
                                  const int64_t* step, int64_t* step_in) {
-  double s = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+  // float4 loads, squares summed in double (two independent accumulators)
+  double s = 0.0, s2 = 0.0;
+  const int64_t P4 = P / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P4;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = g[i];
+    const float4 x = g4[i];
+    s += (double)x.x * x.x + (double)x.y * x.y;
+    s2 += (double)x.z * x.z + (double)x.w * x.w;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < P - 4 * P4) {
+    const double x = g[4 * P4 + threadIdx.x];
     s += x * x;
   }
+  s += s2;
   __shared__ double sh[256];
   sh[threadIdx.x] = s;
   __syncthreads();
@@ -365,7 +374,9 @@ __device__ __forceinline__ void lowp_write(const AdamArgs& a, int64_t i, float v
     const int64_t e = i - m.src;
     if (e < 0 || e >= n) continue;
     int64_t dst;
-    if (m.kind == IMG_COPY_PAD) {
+    if (m.kind == IMG_S2D) {
+      dst = s2d_img_pos(m, e);
+    } else if (m.kind == IMG_COPY_PAD) {
       dst = (e / m.cols) * m.ld + (e % m.cols);
     } else {  // src [CO][KH][KW][CI] -> dst [CI][KH][KW][CO]
       const int ci = (int)(e % m.d3);
@@ -390,20 +401,31 @@ __device__ __forceinline__ int find_img(const AdamArgs& a, int64_t i) {
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
-  __shared__ double tot;
-  if (threadIdx.x == 0) {
+  // every block reduces the grad_norm partials the same way (fixed-order tree)
+  __shared__ double red[256];
+  {
     double s = 0.0;
-    for (int k = 0; k < a.nblocks_norm; ++k) s += a.norm_part[k];
-    tot = s;
+    for (int k = threadIdx.x; k < a.nblocks_norm; k += 256) s += a.norm_part[k];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+  }
+  // scalar terms once per block (double pow / divide kept off the per-thread path)
+  __shared__ float s_coef[3];
+  const double norm = sqrt(red[0]);
+  const bool finite = isfinite(norm);
+  if (threadIdx.x == 0 && finite) {
+    const int64_t t = *a.step_in + 1;
+    s_coef[0] = norm > (double)a.max_norm ? (float)((double)a.max_norm / norm) : 1.f;
+    s_coef[1] = (float)(1.0 - pow((double)a.beta1, (double)t));
+    s_coef[2] = (float)(1.0 - pow((double)a.beta2, (double)t));
   }
   __syncthreads();
-  const double norm = sqrt(tot);
-  const bool finite = isfinite(norm);
-  const int64_t t = *a.step_in + 1;
   if (finite) {
-    const float scale = norm > (double)a.max_norm ? (float)((double)a.max_norm / norm) : 1.f;
-    const float bc1 = (float)(1.0 - pow((double)a.beta1, (double)t));
-    const float bc2 = (float)(1.0 - pow((double)a.beta2, (double)t));
+    const float scale = s_coef[0], bc1 = s_coef[1], bc2 = s_coef[2];
     const int64_t ngroups = (a.P + 3) / 4;
     for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ngroups;
          gi += (int64_t)gridDim.x * blockDim.x) {

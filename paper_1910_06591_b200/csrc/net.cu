@@ -4,6 +4,7 @@
 #include <algorithm>
 #include "gemm_tc.cuh"
 #include "net.cuh"
+#include "conv_s2d.cuh"
 
 namespace seed {
 
@@ -110,9 +111,17 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
     return at;
   };
   if (s->kind == SEED_NET_ATARI_SHALLOW) {
-    p->im_conv1 = img(IMG_COPY_PAD, p->i_conv1w, 16, 64 * p->C, 64 * p->C);
-    p->im_conv2 = img(IMG_COPY_PAD, p->i_conv2w, 32, 256, 256);
-    p->im_conv2dg = dgrad_img(p->i_conv2w, 32, 4, 16);   // [ci][ky][kx][co]
+    // space-to-depth window images (conv_s2d.cuh); 1024-byte aligned starts
+    auto s2d_img = [&](int ti, int st, int C, int CO, int mode) {
+      off = (int64_t)align_up((size_t)off, 512);
+      const int64_t at = img(IMG_S2D, ti, 4 * CO, 64, 64);
+      LowpImg& m = p->img[p->nimg - 1];
+      m.d0 = st; m.d1 = C; m.d2 = CO; m.d3 = mode;
+      return at;
+    };
+    p->im_conv1 = s2d_img(p->i_conv1w, 4, p->C, 16, 0);
+    p->im_conv2 = s2d_img(p->i_conv2w, 2, 16, 32, 0);
+    p->im_conv2dg = s2d_img(p->i_conv2w, 2, 16, 32, 1);
   } else {
     for (int sct = 0; sct < p->nsec; ++sct) {
       DeepSec& d = p->sec[sct];
@@ -140,7 +149,7 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
 
 bool learner_supported(const NetPlan& p) {
   if (p.kind == SEED_NET_MLP) return true;
-  if (p.kind == SEED_NET_ATARI_SHALLOW) return p.C == 4 && p.fc_in % 8 == 0 && (p.W * p.C) % 16 == 0;
+  if (p.kind == SEED_NET_ATARI_SHALLOW) return shallow_s2d_supported(p.H, p.W, p.C);
   if (p.kind == SEED_NET_IMPALA_DEEP || p.kind == SEED_NET_GFOOTBALL)
     return p.C <= 32 && p.fc_in % 8 == 0;
   return false;
@@ -215,11 +224,12 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
     w->act2 = w->sec[p.nsec - 1].hr[2];
     w->dY2 = w->sec[p.nsec - 1].dhA;
   } else {
-    w->obs_bf16 = bump(cur, F * p.H * p.W * p.C * 2);
-    w->act1 = bump(cur, F * p.oh1 * p.ow1 * 16 * 2);
+    const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
+    w->obs_bf16 = bump(cur, s2d_S0_bytes(sg, F));   // S0
+    w->act1 = bump(cur, s2d_S1_bytes(sg, F));       // S1
     w->act2 = bump(cur, F * p.fc_in * 2);
-    w->dY1 = bump(cur, F * p.oh1 * p.ow1 * 16 * 2);
-    w->dY2 = bump(cur, F * p.fc_in * 2);
+    w->dY1 = bump(cur, s2d_dY1_bytes(sg, F));
+    w->dY2 = bump(cur, s2d_dY2_bytes(sg, F));
   }
   w->X = bump(cur, F * p.Kxp * 2);
   w->xproj = bump(cur, F * 4 * U * 4);
@@ -242,9 +252,10 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   need(Fi, 256, 128, 4 * (int)U);                      // dX (fc part)
   need(256, p.fc_in + 8, 128, Fi);                     // fc weight grads (+ bias column)
   need(Fi, p.fc_in, 128, 256);                         // fc dgrad
-  if (p.nsec == 0) {
-    need(64 * p.C, 16, 16, Fi * p.oh1 * p.ow1);        // conv1 wgrad
-    need(256, 32, 32, Fi * p.oh2 * p.ow2);            // conv2 wgrad
+  if (p.nsec == 0) {                                  // s2d weight-gradient partials
+    const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
+    sk = std::max(sk, win_wgrad_part_bytes(sg.rows1(F), 16));
+    sk = std::max(sk, win_wgrad_part_bytes(sg.rows2(F), 32));
   }
   for (int sct = 0; sct < p.nsec; ++sct) {            // 3x3 weight grads
     const DeepSec& d = p.sec[sct];
@@ -270,6 +281,10 @@ __global__ void refresh_lowp_multi(const float* __restrict__ params, __nv_bfloat
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float v;
+    if (m.kind == IMG_S2D) {   // bijective (s*s*C == 64): iterate the source elements
+      lowp[m.dst + s2d_img_pos(m, i)] = __float2bfloat16_rn(params[m.src + i]);
+      continue;
+    }
     if (m.kind == IMG_COPY_PAD) {
       const int r = (int)(i / m.ld), c = (int)(i % m.ld);
       v = c < m.cols ? params[m.src + (int64_t)r * m.cols + c] : 0.f;

@@ -14,7 +14,7 @@ struct PTensor {
 };
 
 // One bf16 operand image inside params_lowp.
-enum { IMG_COPY_PAD = 0, IMG_CONV_DGRAD = 1, IMG_CHAN_PAD = 2 };
+enum { IMG_COPY_PAD = 0, IMG_CONV_DGRAD = 1, IMG_CHAN_PAD = 2, IMG_S2D = 3 };
 struct LowpImg {
   int kind;
   int64_t src;          // fp32 element offset of the source tensor
@@ -22,7 +22,27 @@ struct LowpImg {
   int rows, cols, ld;   // COPY_PAD: dst[r][c] (ld) = src[r][c] (cols) for c < cols, else 0
   int d0, d1, d2, d3;   // CONV_DGRAD: src [d0=CO][d1=KH][d2=KW][d3=CI] -> dst [CI][KH][KW][CO]
                         // CHAN_PAD: src [rows][taps=d1][d3=C] -> dst [rows][taps][d2=Cp] (0-padded)
+                        // S2D: src W[CO=d2][2s][2s][C=d1] (s = d0) -> the pre-swizzled
+                        //   space-to-depth window image (conv_s2d.cuh): d3 = 0 forward
+                        //   [4][CO][64] (128-byte rows), d3 = 1 data gradient [4][64][CO]
 };
+
+// IMG_S2D: bf16 element position (inside the image) of source element e.
+// Window w = (ky / s) * 2 + kx / s, s2d channel ch = ((ky % s) * s + kx % s) * C + c.
+__host__ __device__ inline int64_t s2d_img_pos(const LowpImg& m, int64_t e) {
+  const int s = m.d0, C = m.d1, CO = m.d2, K = 2 * s;
+  const int c = (int)(e % C);
+  int64_t q = e / C;
+  const int kx = (int)(q % K); q /= K;
+  const int ky = (int)(q % K);
+  const int co = (int)(q / K);
+  const int w = (ky / s) * 2 + kx / s, ch = ((ky % s) * s + kx % s) * C + c;
+  int64_t row;
+  int rb, k;
+  if (m.d3 == 0) { row = (int64_t)w * CO + co; rb = 128; k = ch; }
+  else { row = (int64_t)w * 64 + ch; rb = 2 * CO; k = co; }
+  return row * (rb / 2) + swz_chunk(row, rb, k / 8) * 8 + (k % 8);
+}
 
 // IMPALA-deep section (C14): conv3x3 (cin -> ch) at H x W, maxpool -> H2 x W2,
 // residual blocks at H2 x W2.
@@ -50,6 +70,7 @@ struct NetPlan {
   LowpImg img[64];
   int64_t lowp_elems;
   int64_t im_conv1, im_conv2, im_conv2dg, im_fc, im_wx, im_wh;  // bf16 offsets
+                        // (shallow: im_conv1 / im_conv2 / im_conv2dg are IMG_S2D images)
 };
 
 seed_status make_net_plan(const seed_net_spec* s, NetPlan* p);
@@ -65,6 +86,7 @@ struct LearnerWs {
   size_t splitk_bytes;
   // shallow
   size_t obs_bf16, act1, act2, X, xproj, H, Hprev, gates, Cst, dG, dfc, dY2, dY1;
+  // shallow (conv_s2d.cuh): obs_bf16 = S0, act1 = S1, dY2 / dY1 pre-swizzled s2d rows
   // mlp
   size_t h1, h2, dh1, dh2;
   // deep torso, per section
