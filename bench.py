@@ -65,7 +65,7 @@ def phase_work(T, B, A):
     Kxp, U = 288, 256
     X = F * Kxp * 2
     w = {}
-    w["obs_bf16"] = (0, obs * 3)
+    w["obs_s2d"] = (0, obs * 3)          # uint8 obs -> space-to-depth bf16 S0
     w["conv1_fwd"] = (2 * P1 * 16 * 256, obs * 2 + a1 + 16 * 256 * 2)
     w["conv2_fwd"] = (2 * P2 * 32 * 256, a1 + a2 + 32 * 256 * 2)
     w["fc_fwd"] = (2 * F * 256 * 2592, a2 + 256 * 2592 * 2 + F * 256 * 2)
@@ -80,11 +80,9 @@ def phase_work(T, B, A):
     w["dx_fc"] = (2 * F * 256 * 1024, F * 1024 * 2 + 1024 * Kxp * 2 + F * 256 * 2 * 2)
     w["fc_wgrad"] = (2 * 256 * 2593 * F, F * 256 * 2 + a2 + 256 * 2593 * 4)
     w["fc_dgrad"] = (2 * F * 2592 * 256, F * 256 * 2 + 256 * 2592 * 2 + 2 * a2)
-    w["conv2_wgrad"] = (2 * 256 * 32 * P2, a1 + a2 + 256 * 32 * 4)
-    w["conv2_bias"] = (0, a2)
+    w["conv2_wgrad"] = (2 * 256 * 32 * P2, a1 + a2 + 257 * 32 * 4)   # + bias row
     w["conv2_dgrad"] = (2 * P2 * 32 * 256, a2 + 2 * a1 + 16 * 512 * 2)
-    w["conv1_wgrad"] = (2 * 256 * 16 * P1, obs * 2 + a1 + 256 * 16 * 4)
-    w["conv1_bias"] = (0, a1)
+    w["conv1_wgrad"] = (2 * 256 * 16 * P1, obs * 2 + a1 + 257 * 16 * 4)
     Pn = 1225795
     w["grad_norm"] = (0, Pn * 4)
     w["clip_adam"] = (0, Pn * 28)
@@ -95,11 +93,13 @@ def phase_work(T, B, A):
 
 
 # ---------------------------------------------------------------- committed ncu evidence
-PHASE_KERNEL = {"conv1_fwd": "Conv1Fwd", "conv2_fwd": "Conv2Fwd", "fc_fwd": "FcFwd",
+PHASE_KERNEL = {"obs_s2d": "s2d_obs_kernel", "conv1_fwd": "Conv1S2dEpi", "conv2_fwd": "Conv2S2dEpi",
+                "fc_fwd": "FcFwd",
                 "xproj_fwd": "XprojFwd", "lstm_fwd": "lstm_fwd_kernel", "lstm_bwd": "lstm_bwd_kernel",
                 "lstm_wgrad": "LstmWgrad", "dx_fc": "DxFc", "fc_wgrad": "FcWgrad",
-                "fc_dgrad": "FcDgrad", "conv2_wgrad": "Conv2Wgrad", "conv2_dgrad": "Conv2Dgrad",
-                "conv1_wgrad": "Conv1Wgrad", "policy_loss": "policy_loss_kernel",
+                "fc_dgrad": "FcDgrad", "conv2_wgrad": "win_wgrad_kernel<32>",
+                "conv2_dgrad": "Conv2DgradS2dEpi", "conv1_wgrad": "win_wgrad_kernel<16>",
+                "policy_loss": "policy_loss_kernel",
                 "clip_adam": "adam_kernel"}
 
 

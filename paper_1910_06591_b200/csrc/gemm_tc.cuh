@@ -134,12 +134,39 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+constexpr int GEMM_COUNTERS = 4096;   // per-tile split-K arrival counters (workspace)
+
+__device__ __forceinline__ void epi_bar_sync() {   // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+template <class Prob>
+__device__ __forceinline__ void gemm_store16(const Prob& p, int m, int n, float (&v)[16]) {
+  bool done_vec = false;
+  if constexpr (HasStore16<Prob>::value) {
+    if (n + 16 <= p.N) {
+      p.store16(m, n, v);
+      done_vec = true;
+    }
+  }
+  if (!done_vec) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (n + i < p.N) p.store(m, n + i, v[i]);
+  }
+}
+
 // Epilogue of one 128 x BN accumulator: epilogue warp `q` (0..3) owns TMEM
-// lanes / tile rows [32q, 32q+32).
+// lanes / tile rows [32q, 32q+32).  Split-K (splits > 1): the partial goes to
+// part[z]; with `cnt`, the last CTA to finish a tile (integer arrival counter,
+// re-armed by that CTA) sums the partials of all splits in z order — the same
+// fixed order whichever CTA arrives last — and runs the store epilogue, so no
+// separate reduction launch is needed.
 template <int BN, class Prob>
 __device__ __forceinline__ void gemm_epilogue(const Prob& p, float* __restrict__ part, int splits,
                                               int z, int m0, int n0, bool have, uint32_t tmem,
-                                              int q, int lane) {
+                                              int q, int lane, unsigned* cnt, int tile,
+                                              int* s_last) {
   const int m = m0 + q * 32 + lane;
 #pragma unroll 1
   for (int c = 0; c < BN; c += 16) {
@@ -164,26 +191,51 @@ __device__ __forceinline__ void gemm_epilogue(const Prob& p, float* __restrict__
             if (n + i < p.N) dst[i] = v[i];
         }
       } else {
-        bool done_vec = false;
-        if constexpr (HasStore16<Prob>::value) {
-          if (n + 16 <= p.N) {
-            p.store16(m, n, v);
-            done_vec = true;
-          }
-        }
-        if (!done_vec) {
+        gemm_store16(p, m, n, v);
+      }
+    }
+  }
+  if (splits > 1 && cnt) {
+    __threadfence();
+    epi_bar_sync();
+    if (q == 0 && lane == 0) *s_last = atomicAdd(&cnt[tile], 1u) == (unsigned)(splits - 1);
+    epi_bar_sync();
+    if (*s_last) {
+      __threadfence();
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        const int n = n0 + c;
+        if (m < p.M && n < p.N) {
+          float v[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (n + i < p.N) p.store(m, n + i, v[i]);
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          const bool vec = n + 16 <= p.N && (p.N & 3) == 0;
+#pragma unroll 1
+          for (int zz = 0; zz < splits; ++zz) {
+            const float* src = part + ((size_t)zz * p.M + m) * p.N + n;
+            if (vec) {
+#pragma unroll
+              for (int i = 0; i < 16; i += 4) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(src + i));
+                v[i] += t.x; v[i + 1] += t.y; v[i + 2] += t.z; v[i + 3] += t.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (n + i < p.N) v[i] += __ldcg(src + i);
+            }
+          }
+          gemm_store16(p, m, n, v);
         }
       }
+      if (q == 0 && lane == 0) cnt[tile] = 0u;
     }
   }
 }
 
 template <int BN, class Prob>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, float* __restrict__ part,
-                                                                  int splits) {
+                                                                  int splits, unsigned* cnt) {
   using Cfg = GemmCfg<BN, Prob::A_MN, Prob::B_MN>;
   using TA = typename Cfg::TA;
   using TB = typename Cfg::TB;
@@ -195,6 +247,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int mt = (p.M + GEMM_BM - 1) / GEMM_BM, nt = (p.N + BN - 1) / BN;
@@ -338,7 +391,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      gemm_epilogue<BN>(p, part, splits, z, m0, n0, nkb > 0, tmem + acc * Cfg::ACC_COLS, q, lane);
+      gemm_epilogue<BN>(p, part, splits, z, m0, n0, nkb > 0, tmem + acc * Cfg::ACC_COLS, q, lane, cnt,
+                        w / splits, s_last);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -349,47 +403,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
   if (warp == GEMM_MMA_WARP) tmem_dealloc(tmem, Cfg::TMEM_COLS);
 }
 
-// Fixed-order split-K reduction: a block owns 32 consecutive outputs; thread
-// (g, o) sums the splits z = g, g+8, ... of output o, then the 8 group sums are
-// added in group order — deterministic, and enough loads in flight per thread.
+// Fixed-order split-K reduction: each thread owns 4 consecutive outputs and
+// adds the splits z = 0, 1, ... in order (float4 loads, all in flight) —
+// deterministic.  Requires N % 4 == 0 (else the scalar path per output).
 template <class Prob>
 __global__ void __launch_bounds__(256) splitk_finish(const Prob p, const float* __restrict__ part,
                                                      int splits) {
   const size_t MN = (size_t)p.M * p.N;
-  const int o = threadIdx.x & 31, g = threadIdx.x >> 5;
-  __shared__ float sh[8][33];
-  for (size_t base = (size_t)blockIdx.x * 32; base < MN; base += (size_t)gridDim.x * 32) {
-    const size_t i = base + o;
-    float s = 0.f;
-    if (i < MN) {
-      float a0 = 0.f, a1 = 0.f;
-      int z = g;
-      for (; z + 8 < splits; z += 16) {
-        a0 += part[(size_t)z * MN + i];
-        a1 += part[(size_t)(z + 8) * MN + i];
+  const size_t n4 = (MN + 3) / 4;
+  const bool vec = (p.N & 3) == 0;
+  for (size_t i4 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i4 < n4;
+       i4 += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = i4 * 4;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (vec) {
+#pragma unroll 4
+      for (int z = 0; z < splits; ++z) {
+        const float4 t = __ldcs(reinterpret_cast<const float4*>(part + (size_t)z * MN + i));
+        v[0] += t.x; v[1] += t.y; v[2] += t.z; v[3] += t.w;
       }
-      if (z < splits) a0 += part[(size_t)z * MN + i];
-      s = a0 + a1;
-    }
-    sh[g][o] = s;
-    __syncthreads();
-    if (g == 0 && i < MN) {
-      float t = 0.f;
+      const int m = (int)(i / p.N), n = (int)(i % p.N);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) t += sh[k][o];
-      p.store((int)(i / p.N), (int)(i % p.N), t);
+      for (int q = 0; q < 4; ++q) p.store(m, n + q, v[q]);
+    } else {
+      for (int q = 0; q < 4 && i + q < MN; ++q) {
+        for (int z = 0; z < splits; ++z) v[q] += part[(size_t)z * MN + i + q];
+        p.store((int)((i + q) / p.N), (int)((i + q) % p.N), v[q]);
+      }
     }
-    __syncthreads();
   }
 }
 
 // Host launcher.  splits > 1 runs split-K into `part` ([splits][M][N] fp32,
-// caller workspace) followed by the fixed-order splitk_finish reduction.
-// max_ctas > 0 caps the persistent grid (leaves SMs free for concurrent
-// collectives on another stream).
+// caller workspace); with `cnt` (GEMM_COUNTERS zeroed unsigned, left zeroed)
+// the last CTA of each tile reduces in-kernel, otherwise the fixed-order
+// splitk_finish kernel follows.  max_ctas > 0 caps the persistent grid.
 template <int BN, class Prob>
 seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullptr,
-                        int max_ctas = 0) {
+                        int max_ctas = 0, unsigned* cnt = nullptr) {
   using Cfg = GemmCfg<BN, Prob::A_MN, Prob::B_MN>;
   if (p.M <= 0 || p.N <= 0) return SEED_OK;
   const int nkb = (p.K + GEMM_BK - 1) / GEMM_BK;
@@ -408,12 +459,14 @@ seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullp
     sms = n;
   }
   if (splits > 1 && !part) return SEED_E_WORKSPACE;
-  const int items = ceil_div(p.M, GEMM_BM) * ceil_div(p.N, BN) * splits;
+  const int tiles = ceil_div(p.M, GEMM_BM) * ceil_div(p.N, BN);
+  if (tiles > GEMM_COUNTERS) cnt = nullptr;
+  const int items = tiles * splits;
   const int grid = std::min(items, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
-  gemm_tc_kernel<BN, Prob><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(p, part, splits);
-  if (splits > 1) {
+  gemm_tc_kernel<BN, Prob><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(p, part, splits, splits > 1 ? cnt : nullptr);
+  if (splits > 1 && !cnt) {
     const size_t MN = (size_t)p.M * p.N;
-    const int blocks = (int)std::min<size_t>((MN + 31) / 32, 148 * 8);
+    const int blocks = (int)std::min<size_t>((MN / 4 + 255) / 256 + 1, 148 * 8);
     splitk_finish<Prob><<<blocks, 256, 0, st>>>(p, part, splits);
   }
   return last_launch();

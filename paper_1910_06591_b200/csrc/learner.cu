@@ -54,6 +54,10 @@ struct StepCtx {
   int max_ctas = 0;   // > 0 while collectives run concurrently (SMs left for NCCL)
   template <class T>
   T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+  // zeroed region after the column-sum partials: [0..15] tickets, then the
+  // split-K tile counters (memset once per step, re-armed by their users)
+  unsigned* tickets() const { return reinterpret_cast<unsigned*>(at<float>(w.colsum_part) + COLSUM_BLOCKS * 64); }
+  unsigned* gemm_counters() const { return tickets() + 16; }
   // end of a phase of `k` kernel launches
   void mark(const char* name, int k = 1) const {
     if (!tr) return;
@@ -69,6 +73,8 @@ struct StepCtx {
 template <int BN, class Prob>
 static seed_status gemm(const StepCtx& c, Prob pr, cudaStream_t st, const char* name) {
   const int s = pick_splits(pr.M, pr.N, BN, pr.K);
+  // (the in-kernel last-CTA split reduction, launch_gemm's `cnt`, measured
+  // slower here: few tiles -> the fixups serialise on a few SMs)
   const seed_status r = launch_gemm<BN>(pr, s, st, c.at<float>(c.w.splitk), c.max_ctas);
   c.mark(name, s > 1 ? 2 : 1);
   return r;
@@ -431,7 +437,7 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   const bf16* lowp = (const bf16*)state->params_lowp;
   float* grads = state->grads;
   // column-sum completion ticket (re-armed by the kernel after each use)
-  SEED_CUDA_TRY(cudaMemsetAsync(c.at<float>(c.w.colsum_part) + COLSUM_BLOCKS * 64, 0, 16, st));
+  SEED_CUDA_TRY(cudaMemsetAsync(c.tickets(), 0, 64 + GEMM_COUNTERS * 4, st));
 
   if (p.kind == SEED_NET_MLP) {
     SEED_TRY(mlp_forward(c, batch, params, st));
@@ -490,13 +496,19 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
     }
   }
 
-  grad_norm_kernel<<<NORM_BLOCKS, 256, 0, st>>>(grads, p.P, c.at<double>(c.w.norm_part),
-                                                state->step, c.at<int64_t>(c.w.step_in));
+  double* npart = c.at<double>(c.w.norm_part);
+  NormArgs na{};
+  na.g = grads; na.P = p.P; na.part = npart;
+  na.coef = reinterpret_cast<float*>(npart + NORM_BLOCKS); na.norm = npart + NORM_BLOCKS + 2;
+  na.ticket = c.tickets() + 1;
+  na.step = state->step; na.step_in = c.at<int64_t>(c.w.step_in);
+  na.beta1 = hp->beta1; na.beta2 = hp->beta2; na.max_norm = hp->max_grad_norm;
+  grad_norm_kernel<<<NORM_BLOCKS, 256, 0, st>>>(na);
   c.mark("grad_norm");
   AdamArgs aa{};
   aa.P = p.P; aa.params = state->params; aa.grads = grads; aa.m = state->adam_m;
   aa.v = state->adam_v; aa.step = state->step; aa.step_in = c.at<int64_t>(c.w.step_in);
-  aa.norm_part = c.at<double>(c.w.norm_part); aa.nblocks_norm = NORM_BLOCKS;
+  aa.coef = na.coef; aa.norm = na.norm;
   aa.lr = hp->lr; aa.beta1 = hp->beta1; aa.beta2 = hp->beta2; aa.eps = hp->eps;
   aa.max_norm = hp->max_grad_norm; aa.loss_part = c.at<float>(c.w.loss_part); aa.B = B;
   aa.metrics = metrics;

@@ -335,33 +335,67 @@ seed_status colsum_bf16(const __nv_bfloat16* X, int64_t R, int C, float* part, f
 }
 
 // ------------------------------------------------------------------ K9 clip + Adam
-__global__ void grad_norm_kernel(const float* __restrict__ g, int64_t P, double* __restrict__ part,
-                                 const int64_t* step, int64_t* step_in) {
-  // float4 loads, squares summed in double (two independent accumulators)
-  double s = 0.0, s2 = 0.0;
-  const int64_t P4 = P / 4;
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 x = g4[i];
-    s += (double)x.x * x.x + (double)x.y * x.y;
-    s2 += (double)x.z * x.z + (double)x.w * x.w;
+__device__ __forceinline__ double block_sum_double(double v, double* sh8) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh8[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh8[k];   // fixed order
+  return t;   // valid in thread 0
+}
+
+__global__ void __launch_bounds__(256) grad_norm_kernel(const NormArgs a) {
+  // 4 float4 per thread, all loads issued first; squares and sums in double
+  const int64_t P4 = a.P / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(a.g);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double s = 0.0;
+  for (int64_t base = t0; base < P4; base += 4 * stride) {
+    float4 x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = base + q * stride;
+      x[q] = i < P4 ? g4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      s += ((double)x[q].x * x[q].x + (double)x[q].y * x[q].y) +
+           ((double)x[q].z * x[q].z + (double)x[q].w * x[q].w);   // fp64: no fp32 overflow
   }
-  if (blockIdx.x == 0 && threadIdx.x < P - 4 * P4) {
-    const double x = g[4 * P4 + threadIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x < a.P - 4 * P4) {
+    const double x = a.g[4 * P4 + threadIdx.x];
     s += x * x;
   }
-  s += s2;
-  __shared__ double sh[256];
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
-  }
+  __shared__ double sh8[8];
+  __shared__ bool last;
+  const double bs = block_sum_double(s, sh8);
   if (threadIdx.x == 0) {
-    part[blockIdx.x] = sh[0];
-    if (blockIdx.x == 0) *step_in = *step;
+    a.part[blockIdx.x] = bs;
+    __threadfence();
+    last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += 256) t += __ldcg(a.part + k);
+  __syncthreads();   // sh8 reuse
+  const double tot = block_sum_double(t, sh8);
+  if (threadIdx.x == 0) {
+    const double norm = sqrt(tot);
+    const bool finite = isfinite(norm);
+    const int64_t st = *a.step;
+    const int64_t tt = st + 1;
+    *a.step_in = st;
+    *a.norm = norm;
+    a.coef[0] = finite && norm > (double)a.max_norm ? (float)((double)a.max_norm / norm) : 1.f;
+    a.coef[1] = (float)(1.0 - pow((double)a.beta1, (double)tt));
+    a.coef[2] = (float)(1.0 - pow((double)a.beta2, (double)tt));
+    a.coef[3] = finite ? 1.f : 0.f;
+    *a.ticket = 0;
   }
 }
 
@@ -377,7 +411,9 @@ __device__ __forceinline__ void lowp_write(const AdamArgs& a, int64_t i, float v
     if (m.kind == IMG_S2D) {
       dst = s2d_img_pos(m, e);
     } else if (m.kind == IMG_COPY_PAD) {
-      dst = (e / m.cols) * m.ld + (e % m.cols);
+      uint32_t r, c;
+      img_rc(m, (uint32_t)e, r, c);
+      dst = (int64_t)r * m.ld + c;
     } else {  // src [CO][KH][KW][CI] -> dst [CI][KH][KW][CO]
       const int ci = (int)(e % m.d3);
       int64_t q = e / m.d3;
@@ -392,40 +428,25 @@ __device__ __forceinline__ void lowp_write(const AdamArgs& a, int64_t i, float v
 
 // 4 consecutive parameters per thread (float4 when aligned); the bf16 image of
 // the group is found once per group.
-__device__ __forceinline__ int find_img(const AdamArgs& a, int64_t i) {
-  for (int k = 0; k < a.nimg; ++k) {
-    const int64_t e = i - a.img[k].src;
-    if (e >= 0 && e < (int64_t)a.img[k].rows * a.img[k].cols) return k;
-  }
+__device__ __forceinline__ int find_img(const uint32_t (*bounds)[2], int nimg, uint32_t i) {
+  for (int k = 0; k < nimg; ++k)
+    if (i >= bounds[k][0] && i < bounds[k][1]) return k;
   return -1;
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
-  // every block reduces the grad_norm partials the same way (fixed-order tree)
-  __shared__ double red[256];
-  {
-    double s = 0.0;
-    for (int k = threadIdx.x; k < a.nblocks_norm; k += 256) s += a.norm_part[k];
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-      __syncthreads();
-    }
-  }
-  // scalar terms once per block (double pow / divide kept off the per-thread path)
-  __shared__ float s_coef[3];
-  const double norm = sqrt(red[0]);
-  const bool finite = isfinite(norm);
-  if (threadIdx.x == 0 && finite) {
-    const int64_t t = *a.step_in + 1;
-    s_coef[0] = norm > (double)a.max_norm ? (float)((double)a.max_norm / norm) : 1.f;
-    s_coef[1] = (float)(1.0 - pow((double)a.beta1, (double)t));
-    s_coef[2] = (float)(1.0 - pow((double)a.beta2, (double)t));
+  __shared__ uint32_t bounds[8][2];   // source parameter range of each bf16 image
+  if (threadIdx.x < a.nimg) {
+    bounds[threadIdx.x][0] = (uint32_t)a.img[threadIdx.x].src;
+    bounds[threadIdx.x][1] =
+        (uint32_t)(a.img[threadIdx.x].src + (int64_t)a.img[threadIdx.x].rows * a.img[threadIdx.x].cols);
   }
   __syncthreads();
+  const bool finite = a.coef[3] != 0.f;
   if (finite) {
-    const float scale = s_coef[0], bc1 = s_coef[1], bc2 = s_coef[2];
+    // bias corrections as reciprocals; one (fast, 2-ulp) division per parameter —
+    // the IEEE-division slow path (zero / denormal operands) is kept off the loop
+    const float scale = a.coef[0], ibc1 = 1.f / a.coef[1], ibc2 = 1.f / a.coef[2];
     const int64_t ngroups = (a.P + 3) / 4;
     for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ngroups;
          gi += (int64_t)gridDim.x * blockDim.x) {
@@ -456,7 +477,7 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
         const float gg = g[q] * scale;
         m[q] = a.beta1 * m[q] + (1.f - a.beta1) * gg;
         v[q] = a.beta2 * v[q] + (1.f - a.beta2) * gg * gg;
-        p[q] = p[q] - a.lr * (m[q] / bc1) / (sqrtf(v[q] / bc2) + a.eps);
+        p[q] = p[q] - __fdividef(a.lr * (m[q] * ibc1), sqrtf(v[q] * ibc2) + a.eps);
       }
       if (full) {
         reinterpret_cast<float4*>(a.m)[gi] = make_float4(m[0], m[1], m[2], m[3]);
@@ -470,14 +491,14 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
         }
       }
       if (a.nimg) {
-        const int k0 = find_img(a, i0);
-        const int k3 = find_img(a, min(i0 + 3, a.P - 1));
+        const int k0 = find_img(bounds, a.nimg, (uint32_t)i0);
+        const int k3 = find_img(bounds, a.nimg, (uint32_t)min(i0 + 3, a.P - 1));
         if (k0 >= 0 && k0 == k3 && a.img[k0].kind == IMG_COPY_PAD) {
           const LowpImg& im = a.img[k0];
-          const int64_t e = i0 - im.src;
-          const int64_t r = e / im.cols, c = e % im.cols;
-          if (c + 3 < im.cols) {   // the group stays in one image row
-            __nv_bfloat16* d = a.lowp + im.dst + r * im.ld + c;
+          uint32_t r, c;
+          img_rc(im, (uint32_t)(i0 - im.src), r, c);
+          if ((int)c + 3 < im.cols) {   // the group stays in one image row
+            __nv_bfloat16* d = a.lowp + im.dst + (int64_t)r * im.ld + c;
             d[0] = __float2bfloat16_rn(p[0]); d[1] = __float2bfloat16_rn(p[1]);
             d[2] = __float2bfloat16_rn(p[2]); d[3] = __float2bfloat16_rn(p[3]);
             continue;
@@ -497,6 +518,7 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
       if (a.loss_part[b * 4 + 3] != 0.f) nonfin = 1.f;
     }
     const int64_t ver = *a.step_in + (finite ? 1 : 0);
+    const double norm = *a.norm;
     a.metrics[0] = (float)(l0 + l1 + l2);
     a.metrics[1] = (float)l0;
     a.metrics[2] = (float)l1;
@@ -511,7 +533,7 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
 
 seed_status launch_clip_adam(const AdamArgs& a, cudaStream_t st) {
   const int64_t groups = (a.P + 3) / 4;
-  adam_kernel<<<(int)std::min<int64_t>((groups + 255) / 256, 148 * 8), 256, 0, st>>>(a);
+  adam_kernel<<<(int)std::min<int64_t>((groups + 255) / 256, 148 * 4), 256, 0, st>>>(a);
   return last_launch();
 }
 

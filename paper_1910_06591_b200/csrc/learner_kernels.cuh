@@ -68,8 +68,8 @@ struct AdamArgs {
   float* v;
   int64_t* step;
   const int64_t* step_in;
-  const double* norm_part;
-  int nblocks_norm;
+  const float* coef;       // grad_norm_kernel output
+  const double* norm;
   float lr, beta1, beta2, eps, max_norm;
   const float* loss_part;  // [B][4]
   int B;
@@ -79,7 +79,20 @@ struct AdamArgs {
   LowpImg img[8];
 };
 seed_status launch_clip_adam(const AdamArgs& a, cudaStream_t st);
-__global__ void grad_norm_kernel(const float* __restrict__ g, int64_t P, double* __restrict__ part,
-                                 const int64_t* step, int64_t* step_in);
+// Global-norm partials; the last block (integer ticket, re-armed by itself)
+// reduces them in block order and writes the clip + Adam coefficients
+// coef = {clip scale, 1 - beta1^t, 1 - beta2^t, finite} and the norm (double).
+struct NormArgs {
+  const float* g;
+  int64_t P;
+  double* part;            // [NORM_BLOCKS]
+  float* coef;             // [4]
+  double* norm;
+  unsigned* ticket;
+  const int64_t* step;
+  int64_t* step_in;
+  float beta1, beta2, max_norm;
+};
+__global__ void grad_norm_kernel(const NormArgs a);
 
 }  // namespace seed

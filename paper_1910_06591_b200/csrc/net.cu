@@ -99,6 +99,8 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
   auto img = [&](int kind, int ti, int rows, int cols, int ld) {
     LowpImg& m = p->img[p->nimg++];
     m.kind = kind; m.src = p->t[ti].off; m.dst = off; m.rows = rows; m.cols = cols; m.ld = ld;
+    const FastDiv fd((uint32_t)cols);
+    m.cmul = fd.mul; m.cshr = fd.shr;
     const int64_t start = off;
     off += (int64_t)rows * ld;
     off = (int64_t)align_up((size_t)off, 64);
@@ -186,9 +188,10 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   w->dvalues = bump(cur, F * 4);
   w->loss_part = bump(cur, (size_t)B * 4 * 4);
   w->flag = bump(cur, 16);
-  w->norm_part = bump(cur, NORM_BLOCKS * 8);
+  w->norm_part = bump(cur, NORM_BLOCKS * 8 + 64);   // + clip/Adam coefficients, norm
   w->step_in = bump(cur, 8);
-  w->colsum_part = bump(cur, COLSUM_BLOCKS * 64 * 4 + 64);   // + ticket (zeroed at creation)
+  // + tickets and split-K tile counters (zeroed at the start of every step)
+  w->colsum_part = bump(cur, COLSUM_BLOCKS * 64 * 4 + 64 + GEMM_COUNTERS * 4);
   if (p.kind == SEED_NET_MLP) {
     w->h1 = bump(cur, F * 64 * 4);
     w->h2 = bump(cur, F * 64 * 4);

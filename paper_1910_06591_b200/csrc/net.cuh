@@ -20,6 +20,7 @@ struct LowpImg {
   int64_t src;          // fp32 element offset of the source tensor
   int64_t dst;          // bf16 element offset in params_lowp
   int rows, cols, ld;   // COPY_PAD: dst[r][c] (ld) = src[r][c] (cols) for c < cols, else 0
+  uint32_t cmul, cshr;  // cols as a multiply-high divisor (FastDiv of cols, < 2^31 dividends)
   int d0, d1, d2, d3;   // CONV_DGRAD: src [d0=CO][d1=KH][d2=KW][d3=CI] -> dst [CI][KH][KW][CO]
                         // CHAN_PAD: src [rows][taps=d1][d3=C] -> dst [rows][taps][d2=Cp] (0-padded)
                         // S2D: src W[CO=d2][2s][2s][C=d1] (s = d0) -> the pre-swizzled
@@ -29,19 +30,28 @@ struct LowpImg {
 
 // IMG_S2D: bf16 element position (inside the image) of source element e.
 // Window w = (ky / s) * 2 + kx / s, s2d channel ch = ((ky % s) * s + kx % s) * C + c.
-__host__ __device__ inline int64_t s2d_img_pos(const LowpImg& m, int64_t e) {
+__host__ __device__ inline int64_t s2d_img_pos(const LowpImg& m, int64_t e64) {
   const int s = m.d0, C = m.d1, CO = m.d2, K = 2 * s;
-  const int c = (int)(e % C);
-  int64_t q = e / C;
-  const int kx = (int)(q % K); q /= K;
-  const int ky = (int)(q % K);
-  const int co = (int)(q / K);
+  const int e = (int)e64;
+  const int c = e % C;
+  int q = e / C;
+  const int kx = q % K; q /= K;
+  const int ky = q % K;
+  const int co = q / K;
   const int w = (ky / s) * 2 + kx / s, ch = ((ky % s) * s + kx % s) * C + c;
-  int64_t row;
-  int rb, k;
-  if (m.d3 == 0) { row = (int64_t)w * CO + co; rb = 128; k = ch; }
-  else { row = (int64_t)w * 64 + ch; rb = 2 * CO; k = co; }
-  return row * (rb / 2) + swz_chunk(row, rb, k / 8) * 8 + (k % 8);
+  int row, rb, k;
+  if (m.d3 == 0) { row = w * CO + co; rb = 128; k = ch; }
+  else { row = w * 64 + ch; rb = 2 * CO; k = co; }
+  return (int64_t)row * (rb / 2) + swz_chunk(row, rb, k / 8) * 8 + (k % 8);
+}
+// row / column of element e of a COPY_PAD image (e < 2^31)
+__host__ __device__ inline void img_rc(const LowpImg& m, uint32_t e, uint32_t& r, uint32_t& c) {
+#ifdef __CUDA_ARCH__
+  r = m.cmul ? (__umulhi(e, m.cmul) >> m.cshr) : e;
+#else
+  r = e / (uint32_t)m.cols;
+#endif
+  c = e - r * (uint32_t)m.cols;
 }
 
 // IMPALA-deep section (C14): conv3x3 (cin -> ch) at H x W, maxpool -> H2 x W2,
