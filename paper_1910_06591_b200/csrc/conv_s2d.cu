@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   if (warp == 1) tmem_alloc(&tbase, TCOLS);
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = tbase;
   if (warp == 0) {
     if (lane == 0) {
@@ -165,8 +166,7 @@ seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st)
   }
   const int64_t tiles = (a.M + 127) / 128;
   const int grid = (int)std::min<int64_t>(tiles, 148);
-  win_conv_kernel<Epi, RB><<<grid, WC_THREADS, smem, st>>>(a, e, stages, slab);
-  return last_launch();
+  return launch_k(win_conv_kernel<Epi, RB>, dim3(grid), dim3(WC_THREADS), smem, st, a, e, stages, slab);
 }
 
 // ------------------------------------------------------------------ epilogues
@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   if (warp == 1) tmem_alloc(&tbase, TCOLS);
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = tbase;
   if (warp == 0) {
     for (int it = 0; it < nks; ++it) {
@@ -364,6 +365,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
 // fixed-order sum of the per-CTA partials; block = 32 outputs x 8 split groups
 __global__ void __launch_bounds__(256) win_wgrad_finish(const float* __restrict__ part, int G, int N,
                                                         const WinWgradFinish f) {
+  pdl_wait();
   const int tot = 2 * 128 * N + N;
   const int o = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
   __shared__ float sh[8][33];
@@ -420,11 +422,11 @@ seed_status launch_win_wgrad(const WinWgradArgs& a0, const WinWgradFinish& fin, 
                                        WC_SMEM_BUDGET + 2048));
     attr = true;
   }
-  win_wgrad_kernel<N><<<G, WC_THREADS, smem, st>>>(a, stages, a_bytes, b_bytes);
-  SEED_TRY(last_launch());
+  SEED_TRY(launch_k(win_wgrad_kernel<N>, dim3(G), dim3(WC_THREADS), smem, st, a, stages, a_bytes,
+                    b_bytes));
   const int tot = 2 * 128 * N + N;
-  win_wgrad_finish<<<ceil_div(tot, 32), 256, 0, st>>>(a.part, G, N, fin);
-  return last_launch();
+  return launch_k(win_wgrad_finish, dim3(ceil_div(tot, 32)), dim3(256), 0, st, (const float*)a.part, G,
+                  N, fin);
 }
 
 // ------------------------------------------------------------------ obs -> S0
@@ -432,6 +434,7 @@ seed_status launch_win_wgrad(const WinWgradArgs& a0, const WinWgradFinish& fin, 
 // pixels 4X + 2(j%2) .. +1, 4 channels = 8 input bytes): a warp writes 4 whole rows
 __global__ void s2d_obs_kernel(int64_t nrows, FastDiv P, FastDiv Wd, int H, int W,
                                const uint8_t* __restrict__ obs, uint8_t* __restrict__ S0) {
+  pdl_wait();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t g = t >> 3;
   if (g >= nrows) return;
@@ -456,8 +459,8 @@ seed_status s2d_obs(const uint8_t* obs, int64_t F, int H, int W, uint8_t* S0, cu
   const int Hs = H / 4, Ws = W / 4;
   const int64_t n = F * Hs * Ws;
   if (n == 0) return SEED_OK;
-  s2d_obs_kernel<<<(int)((n * 8 + 255) / 256), 256, 0, st>>>(n, FastDiv(Hs * Ws), FastDiv(Ws), H, W, obs, S0);
-  return last_launch();
+  return launch_k(s2d_obs_kernel, dim3((unsigned)((n * 8 + 255) / 256)), dim3(256), 0, st, n,
+                  FastDiv(Hs * Ws), FastDiv(Ws), H, W, obs, S0);
 }
 
 // ------------------------------------------------------------------ torso

@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = *tmem_slot;
 
   auto decode = [&](int w, int& m0, int& n0, int& kb0, int& nkb, int& z) {
@@ -409,6 +410,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
 template <class Prob>
 __global__ void __launch_bounds__(256) splitk_finish(const Prob p, const float* __restrict__ part,
                                                      int splits) {
+  pdl_wait();
   const size_t MN = (size_t)p.M * p.N;
   const size_t n4 = (MN + 3) / 4;
   const bool vec = (p.N & 3) == 0;
@@ -463,13 +465,14 @@ seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullp
   if (tiles > GEMM_COUNTERS) cnt = nullptr;
   const int items = tiles * splits;
   const int grid = std::min(items, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
-  gemm_tc_kernel<BN, Prob><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(p, part, splits, splits > 1 ? cnt : nullptr);
+  SEED_TRY(launch_k(gemm_tc_kernel<BN, Prob>, dim3(grid), dim3(GEMM_THREADS), (size_t)Cfg::SMEM, st, p,
+                    part, splits, splits > 1 ? cnt : (unsigned*)nullptr));
   if (splits > 1 && !cnt) {
     const size_t MN = (size_t)p.M * p.N;
     const int blocks = (int)std::min<size_t>((MN / 4 + 255) / 256 + 1, 148 * 8);
-    splitk_finish<Prob><<<blocks, 256, 0, st>>>(p, part, splits);
+    SEED_TRY(launch_k(splitk_finish<Prob>, dim3(blocks), dim3(256), 0, st, p, (const float*)part, splits));
   }
-  return last_launch();
+  return SEED_OK;
 }
 
 // effective number of splits launch_gemm will use

@@ -116,8 +116,8 @@ static seed_status core_forward(const StepCtx& c, const seed_batch* bt, const bf
   {
     const int E = p.Kxp - 256;
     const int64_t n = (int64_t)F * E;
-    core_extras_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(
-        F, p.A, p.Kxp, bt->prev_action, bt->reward, bt->done, c.at<bf16>(w.X));
+    SEED_TRY(launch_k(core_extras_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, F, p.A,
+                      p.Kxp, bt->prev_action, bt->reward, bt->done, c.at<bf16>(w.X)));
     c.mark("core_extras");
   }
   {
@@ -154,10 +154,9 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
   // heads
   SEED_TRY(launch_dense_dgrad(F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues),
                               params + p.t[p.i_hw].off, nullptr, c.at<float>(w.dH), st));
-  dense_wgrad_f32<<<dim3(A + 1, ceil_div(U + 1, 32)), 256, 0, st>>>(
-      F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), c.at<float>(w.H),
-      grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off);
-  SEED_TRY(last_launch());
+  SEED_TRY(launch_k(dense_wgrad_f32, dim3(A + 1, ceil_div(U + 1, 32)), dim3(256), 0, st, F, U, A + 1,
+                    (const float*)c.at<float>(w.dlogits), A, (const float*)c.at<float>(w.dvalues),
+                    (const float*)c.at<float>(w.H), grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off));
   c.mark("heads_bwd", 2);
   // LSTM BPTT
   LstmBwdArgs lb{};
@@ -503,7 +502,7 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   na.ticket = c.tickets() + 1;
   na.step = state->step; na.step_in = c.at<int64_t>(c.w.step_in);
   na.beta1 = hp->beta1; na.beta2 = hp->beta2; na.max_norm = hp->max_grad_norm;
-  grad_norm_kernel<<<NORM_BLOCKS, 256, 0, st>>>(na);
+  SEED_TRY(launch_k(grad_norm_kernel, dim3(NORM_BLOCKS), dim3(256), 0, st, na));
   c.mark("grad_norm");
   AdamArgs aa{};
   aa.P = p.P; aa.params = state->params; aa.grads = grads; aa.m = state->adam_m;

@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(256) dense_fwd_f32(int R, int I, int O, const 
                                                      const float* __restrict__ b,
                                                      float* __restrict__ Y, int ldy,
                                                      float* __restrict__ Yv, int relu) {
+  pdl_wait();
   extern __shared__ float shf[];
   float* Wt = shf;                  // [I][O]
   float* xs = shf + I * O;          // [8][I]
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(256) dense_dgrad_f32(int R, int I, int O, cons
                                                        const float* __restrict__ W,
                                                        const float* __restrict__ mask,
                                                        float* __restrict__ dX) {
+  pdl_wait();
   extern __shared__ float shf[];
   float* Ws = shf;              // [O][I]
   float* ds = shf + O * I;      // [DG_ROWS][O]
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(256) dense_wgrad_f32(int R, int I, int O, cons
                                                        int ldy, const float* __restrict__ dv,
                                                        const float* __restrict__ X,
                                                        float* __restrict__ gW, float* __restrict__ gb) {
+  pdl_wait();
   const int o = blockIdx.x;
   const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int i = blockIdx.y * 32 + lane;
@@ -134,8 +137,7 @@ seed_status launch_dense_fwd(int R, int I, int O, const float* X, const float* W
   }
   const size_t smem = (size_t)(I * O + 8 * I) * 4;
   const int blocks = std::min(ceil_div(R, 8), 148 * 4);
-  dense_fwd_f32<<<blocks, 256, smem, st>>>(R, I, O, X, W, b, Y, ldy, Yv, relu);
-  return last_launch();
+  return launch_k(dense_fwd_f32, dim3(blocks), dim3(256), smem, st, R, I, O, X, W, b, Y, ldy, Yv, relu);
 }
 
 seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, const float* dv,
@@ -148,8 +150,8 @@ seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, co
     attr = true;
   }
   const size_t smem = (size_t)(O * I + DG_ROWS * O) * 4;
-  dense_dgrad_f32<<<ceil_div(R, DG_ROWS), 256, smem, st>>>(R, I, O, dy, ldy, dv, W, mask, dX);
-  return last_launch();
+  return launch_k(dense_dgrad_f32, dim3(ceil_div(R, DG_ROWS)), dim3(256), smem, st, R, I, O, dy, ldy, dv,
+                  W, mask, dX);
 }
 
 // ------------------------------------------------------------------ K2 policy loss
@@ -160,6 +162,7 @@ seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, co
 //     loss sums;
 //  3. all threads write the closed-form output gradients (H7).
 __global__ void __launch_bounds__(256) policy_loss_kernel(const LossArgs a) {
+  pdl_wait();
   __shared__ float s_lse[256], s_tlp[256], s_H[256], s_vs[256], s_pg[256];
   const int b = blockIdx.x;
   const int T = a.T, T1 = a.T + 1, A = a.A;
@@ -248,14 +251,14 @@ __global__ void __launch_bounds__(256) policy_loss_kernel(const LossArgs a) {
 
 seed_status launch_policy_loss(const LossArgs& a, cudaStream_t st) {
   if (a.T > 256 || a.A > 32) return SEED_E_SHAPE;
-  policy_loss_kernel<<<a.B, 256, 0, st>>>(a);
-  return last_launch();
+  return launch_k(policy_loss_kernel, dim3(a.B), dim3(256), 0, st, a);
 }
 
 // ------------------------------------------------------------------ LSTM input extras
 __global__ void core_extras_kernel(int F, int A, int Kxp, const int32_t* __restrict__ prev_action,
                                    const float* __restrict__ reward,
                                    const uint8_t* __restrict__ done, __nv_bfloat16* X) {
+  pdl_wait();
   const int E = Kxp - 256;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)F * E) return;
@@ -276,6 +279,7 @@ __global__ void core_extras_kernel(int F, int A, int Kxp, const int32_t* __restr
 __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ X, int64_t R,
                                                      int C, float* __restrict__ part,
                                                      unsigned* ticket, float* __restrict__ out) {
+  pdl_wait();
   const int G = C / 8;                         // 16-byte groups per row
   const int RL = 256 / G;                      // rows in flight per block
   const int grp = threadIdx.x % G, rl = threadIdx.x / G;
@@ -347,6 +351,7 @@ __device__ __forceinline__ double block_sum_double(double v, double* sh8) {
 }
 
 __global__ void __launch_bounds__(256) grad_norm_kernel(const NormArgs a) {
+  pdl_wait();
   // 4 float4 per thread, all loads issued first; squares and sums in double
   const int64_t P4 = a.P / 4;
   const float4* g4 = reinterpret_cast<const float4*>(a.g);
@@ -435,6 +440,7 @@ __device__ __forceinline__ int find_img(const uint32_t (*bounds)[2], int nimg, u
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
+  pdl_wait();
   __shared__ uint32_t bounds[8][2];   // source parameter range of each bf16 image
   if (threadIdx.x < a.nimg) {
     bounds[threadIdx.x][0] = (uint32_t)a.img[threadIdx.x].src;
@@ -533,8 +539,8 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
 
 seed_status launch_clip_adam(const AdamArgs& a, cudaStream_t st) {
   const int64_t groups = (a.P + 3) / 4;
-  adam_kernel<<<(int)std::min<int64_t>((groups + 255) / 256, 148 * 4), 256, 0, st>>>(a);
-  return last_launch();
+  return launch_k(adam_kernel, dim3((unsigned)std::min<int64_t>((groups + 255) / 256, 148 * 4)), dim3(256),
+                  0, st, a);
 }
 
 }  // namespace seed

@@ -153,6 +153,7 @@ struct LstmCfg {
 template <int BBT>
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_fwd_kernel(const LstmFwdArgs a) {
+  pdl_wait();
   LSTM_STAMP(0, MAX_T1, 0)
   using Cfg = LstmCfg<BBT>;
   constexpr int U = LSTM_U, MR = Cfg::MR, NT = Cfg::NT;
@@ -357,6 +358,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
 template <int BBT>
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_bwd_kernel(const LstmBwdArgs a) {
+  pdl_wait();
   LSTM_STAMP(1, MAX_T1, 0)
   using Cfg = LstmCfg<BBT>;
   constexpr int U = LSTM_U, MR = Cfg::MR, NT = Cfg::NT;
@@ -546,8 +548,8 @@ static seed_status launch_fwd(const LstmFwdArgs& a, cudaStream_t st) {
                                        LstmCfg<BBT>::FWD_SMEM));
     attr = true;
   }
-  lstm_fwd_kernel<BBT><<<ceil_div(a.B, BBT) * LSTM_CLUSTER, 256, LstmCfg<BBT>::FWD_SMEM, st>>>(a);
-  return last_launch();
+  return launch_k(lstm_fwd_kernel<BBT>, dim3(ceil_div(a.B, BBT) * LSTM_CLUSTER), dim3(256),
+                  (size_t)LstmCfg<BBT>::FWD_SMEM, st, a);
 }
 template <int BBT>
 static seed_status launch_bwd(const LstmBwdArgs& a, cudaStream_t st) {
@@ -558,8 +560,8 @@ static seed_status launch_bwd(const LstmBwdArgs& a, cudaStream_t st) {
                                        LstmCfg<BBT>::BWD_SMEM));
     attr = true;
   }
-  lstm_bwd_kernel<BBT><<<ceil_div(a.B, BBT) * LSTM_CLUSTER, 256, LstmCfg<BBT>::BWD_SMEM, st>>>(a);
-  return last_launch();
+  return launch_k(lstm_bwd_kernel<BBT>, dim3(ceil_div(a.B, BBT) * LSTM_CLUSTER), dim3(256),
+                  (size_t)LstmCfg<BBT>::BWD_SMEM, st, a);
 }
 
 // rows per cluster: spread small batches over more clusters (more SMs per step),
