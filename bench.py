@@ -72,9 +72,10 @@ def phase_work(T, B, A):
     w["core_extras"] = (0, F * 32 * 2 + F * 9)
     w["xproj_fwd"] = (2 * F * 1024 * 275, X + 1024 * Kxp * 2 + F * 1024 * 4)
     w["lstm_fwd"] = (2 * F * 1024 * 256, F * 1024 * 4 + 1024 * 256 * 2 + F * (256 * 4 * 2 + 1024 * 4 + 256 * 2))
-    w["heads_fwd"] = (2 * F * (A + 1) * 256, F * 256 * 4 + F * (A + 1) * 4)
-    w["policy_loss"] = (0, F * (2 * A * 4 + 4 * 4 + 9) + B * T * 8)
-    w["heads_bwd"] = (4 * F * (A + 1) * 256, 2 * F * 256 * 4 + F * (A + 1) * 4)
+    # heads forward + policy loss + heads backward (one kernel + the weight-grad sum):
+    # H read, logits/values/dlogits written, dH written, per-trajectory partials
+    w["heads_loss"] = (6 * F * (A + 1) * 256,
+                       2 * F * 256 * 4 + 2 * F * (A + 1) * 4 + F * 9 + B * T * 8 + 2 * B * (A + 1) * 257 * 4)
     w["lstm_bwd"] = (2 * F * 1024 * 256, F * (1024 * 4 + 256 * 4 * 2 + 256 * 4 + 1024 * 2))
     w["lstm_wgrad"] = (2 * 1024 * (275 + 1 + 256) * F, F * 1024 * 2 + X + F * 256 * 2 + 1024 * 532 * 4)
     w["dx_fc"] = (2 * F * 256 * 1024, F * 1024 * 2 + 1024 * Kxp * 2 + F * 256 * 2 * 2)
@@ -99,7 +100,7 @@ PHASE_KERNEL = {"obs_s2d": "s2d_obs_kernel", "conv1_fwd": "Conv1S2dEpi", "conv2_
                 "lstm_wgrad": "LstmWgrad", "dx_fc": "DxFc", "fc_wgrad": "FcWgrad",
                 "fc_dgrad": "FcDgrad", "conv2_wgrad": "win_wgrad_kernel<32>",
                 "conv2_dgrad": "Conv2DgradS2dEpi", "conv1_wgrad": "win_wgrad_kernel<16>",
-                "policy_loss": "policy_loss_kernel",
+                "heads_loss": "heads_loss_kernel",
                 "clip_adam": "adam_kernel"}
 
 

@@ -9,6 +9,7 @@ namespace seed {
 constexpr int WC_THREADS = 192;   // warp 0: TMA producer, warp 1: MMA, warps 2-5: epilogue
 constexpr int WC_MAX_STAGES = 8;
 constexpr int WC_SMEM_BUDGET = 200 * 1024;
+constexpr int WG_KS = 256;        // rows per weight-gradient k-stage
 
 __device__ __forceinline__ uint4 pack8(const float* o) {
   uint4 u;
@@ -267,8 +268,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t r_end = std::min<int64_t>(a.M, r_begin + a.rows_per_cta);
-  const int nks = r_end > r_begin ? (int)((r_end - r_begin + 127) / 128) : 0;
-  const int arows = 128 + a.wsp + 1;
+  const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
+  const int arows = WG_KS + a.wsp + 1;
   for (int i = threadIdx.x; i < 64; i += blockDim.x)
     reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   fence_proxy_async_smem();
@@ -286,14 +287,14 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
     for (int it = 0; it < nks; ++it) {
       const int s = it % stages;
       mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-      const int64_t k0 = r_begin + (int64_t)it * 128;
+      const int64_t k0 = r_begin + (int64_t)it * WG_KS;
       uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
       // B first (its bytes are credited through the A call's expect_tx)
-      const int64_t blo = k0, bhi = std::min<int64_t>(k0 + 128, r_end);
+      const int64_t blo = k0, bhi = std::min<int64_t>(k0 + WG_KS, r_end);
       const int boff = slab_phase(k0, RBY);
       uint8_t* bd = sa + a_bytes + boff;
-      if (bhi - blo < 128) {
-        zero_rows(bd, RBY, (int)(bhi - blo), 128, lane);
+      if (bhi - blo < WG_KS) {
+        zero_rows(bd, RBY, (int)(bhi - blo), WG_KS, lane);
         fence_proxy_async_smem();
       }
       __syncwarp();
@@ -309,12 +310,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
         const int s = it % stages;
         mbar_wait(&full[s], (it / stages) & 1);
         tc_fence_after();
-        const int64_t k0 = r_begin + (int64_t)it * 128;
+        const int64_t k0 = r_begin + (int64_t)it * WG_KS;
         uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
         const uint32_t abase = smem_u32(sa) + slab_phase(k0, 128);
         const uint32_t bbase = smem_u32(sa + a_bytes) + slab_phase(k0, RBY);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
+        for (int ks = 0; ks < WG_KS / 16; ++ks) {
           const uint64_t bdsc = umma_desc(bbase + ks * 16 * RBY, 8 * RBY, 8 * RBY, LB);
           const uint32_t accf = (it | ks) != 0;
 #pragma unroll
@@ -395,11 +396,11 @@ __global__ void __launch_bounds__(256) win_wgrad_finish(const float* __restrict_
 }
 
 static int wgrad_grid(int64_t M, int64_t* rows_per_cta) {
-  const int64_t kst = (M + 127) / 128;
+  const int64_t kst = (M + WG_KS - 1) / WG_KS;
   const int64_t G0 = std::min<int64_t>(148, std::max<int64_t>(kst, 1));
   const int64_t per = (kst + G0 - 1) / G0;
-  *rows_per_cta = per * 128;
-  return (int)std::max<int64_t>(1, (M + per * 128 - 1) / (per * 128));
+  *rows_per_cta = per * WG_KS;
+  return (int)std::max<int64_t>(1, (M + per * WG_KS - 1) / (per * WG_KS));
 }
 
 size_t win_wgrad_part_bytes(int64_t M, int N) {
@@ -411,8 +412,8 @@ template <int N>
 seed_status launch_win_wgrad(const WinWgradArgs& a0, const WinWgradFinish& fin, cudaStream_t st) {
   WinWgradArgs a = a0;
   const int G = wgrad_grid(a.M, &a.rows_per_cta);
-  const int a_bytes = (int)align_up((size_t)(128 + a.wsp + 1) * 128 + 1024, 1024);
-  const int b_bytes = (int)align_up((size_t)128 * 2 * N + 1024, 1024);
+  const int a_bytes = (int)align_up((size_t)(WG_KS + a.wsp + 1) * 128 + 1024, 1024);
+  const int b_bytes = (int)align_up((size_t)WG_KS * 2 * N + 1024, 1024);
   const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes));
   if (stages < 2) return SEED_E_SHAPE;
   const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);

@@ -87,7 +87,7 @@ struct WinWgradArgs {
   const uint8_t* dy;     // B: pre-swizzled rows of rby = 2*N bytes
   int64_t M;             // rows summed over
   int wsp;               // window pair a starts at row offset a*wsp (b: +1 row)
-  int64_t rows_per_cta;  // multiple of 128
+  int64_t rows_per_cta;  // multiple of the k-stage (conv_s2d.cu WG_KS)
   float* part;           // [grid][3][128][N]
 };
 struct WinWgradFinish {

@@ -138,11 +138,7 @@ static seed_status core_forward(const StepCtx& c, const seed_batch* bt, const bf
   la.hT = la.cT = nullptr;
   SEED_TRY(lstm_forward(la, st));
   c.mark("lstm_fwd");
-  SEED_TRY(launch_dense_fwd(F, p.U, p.A + 1, c.at<float>(w.H), params + p.t[p.i_hw].off,
-                            params + p.t[p.i_hb].off, c.at<float>(w.logits), p.A,
-                            c.at<float>(w.values), 0, st));
-  c.mark("heads_fwd");
-  return last_launch();
+  return SEED_OK;   // the heads run inside the fused loss kernel
 }
 
 // heads + LSTM backward + FC backward, ending with w.dY2 = d(act2) (H8, H9 part)
@@ -150,14 +146,8 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
                                     const float* params, float* grads, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
-  const int F = w.F, U = p.U, A = p.A;
-  // heads
-  SEED_TRY(launch_dense_dgrad(F, U, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues),
-                              params + p.t[p.i_hw].off, nullptr, c.at<float>(w.dH), st));
-  SEED_TRY(launch_k(dense_wgrad_f32, dim3(A + 1, ceil_div(U + 1, 32)), dim3(256), 0, st, F, U, A + 1,
-                    (const float*)c.at<float>(w.dlogits), A, (const float*)c.at<float>(w.dvalues),
-                    (const float*)c.at<float>(w.H), grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off));
-  c.mark("heads_bwd", 2);
+  const int F = w.F, U = p.U;
+  // (heads backward: dH and the heads gradients come from the fused loss kernel)
   // LSTM BPTT
   LstmBwdArgs lb{};
   lb.B = w.B; lb.T1 = w.T1; lb.wh = lowp + p.im_wh;
@@ -361,10 +351,7 @@ static seed_status mlp_forward(const StepCtx& c, const seed_batch* bt, const flo
                             params + p.t[p.i_m0b].off, c.at<float>(w.h1), 64, nullptr, 1, st));
   SEED_TRY(launch_dense_fwd(F, 64, 64, c.at<float>(w.h1), params + p.t[p.i_m1w].off,
                             params + p.t[p.i_m1b].off, c.at<float>(w.h2), 64, nullptr, 1, st));
-  SEED_TRY(launch_dense_fwd(F, 64, p.A + 1, c.at<float>(w.h2), params + p.t[p.i_hw].off,
-                            params + p.t[p.i_hb].off, c.at<float>(w.logits), p.A,
-                            c.at<float>(w.values), 0, st));
-  c.mark("mlp_fwd", 3);
+  c.mark("mlp_fwd", 2);   // the heads run inside the fused loss kernel
   return last_launch();
 }
 
@@ -372,12 +359,8 @@ static seed_status mlp_backward(const StepCtx& c, const seed_batch* bt, const fl
                                 float* grads, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
-  const int F = w.F, A = p.A;
-  SEED_TRY(launch_dense_dgrad(F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues),
-                              params + p.t[p.i_hw].off, c.at<float>(w.h2), c.at<float>(w.dh2), st));
-  dense_wgrad_f32<<<dim3(A + 1, ceil_div(65, 32)), 256, 0, st>>>(
-      F, 64, A + 1, c.at<float>(w.dlogits), A, c.at<float>(w.dvalues), c.at<float>(w.h2),
-      grads + p.t[p.i_hw].off, grads + p.t[p.i_hb].off);
+  const int F = w.F;
+  // dh2 (masked) and the heads gradients come from the fused loss kernel
   SEED_TRY(launch_dense_dgrad(F, 64, 64, c.at<float>(w.dh2), 64, nullptr,
                               params + p.t[p.i_m1w].off, c.at<float>(w.h1), c.at<float>(w.dh1), st));
   dense_wgrad_f32<<<dim3(64, ceil_div(65, 32)), 256, 0, st>>>(
@@ -386,7 +369,7 @@ static seed_status mlp_backward(const StepCtx& c, const seed_batch* bt, const fl
   dense_wgrad_f32<<<dim3(64, ceil_div(p.D + 1, 32)), 256, 0, st>>>(
       F, p.D, 64, c.at<float>(w.dh1), 64, nullptr, (const float*)bt->obs,
       grads + p.t[p.i_m0w].off, grads + p.t[p.i_m0b].off);
-  c.mark("mlp_bwd", 5);
+  c.mark("mlp_bwd", 3);
   return last_launch();
 }
 
@@ -456,8 +439,17 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   la.scale = hp->loss_scale;
   la.dlogits = c.at<float>(c.w.dlogits); la.dvalues = c.at<float>(c.w.dvalues);
   la.vs = c.at<float>(c.w.vs); la.pg = c.at<float>(c.w.pg); la.part = c.at<float>(c.w.loss_part);
-  SEED_TRY(launch_policy_loss(la, st));
-  c.mark("policy_loss");
+  // heads forward + loss + heads backward (one kernel, then the weight-gradient sum)
+  const bool mlp = p.kind == SEED_NET_MLP;
+  la.H = mlp ? c.at<float>(c.w.h2) : c.at<float>(c.w.H);
+  la.I = mlp ? 64 : p.U;
+  la.hw = params + p.t[p.i_hw].off; la.hb = params + p.t[p.i_hb].off;
+  la.hmask = mlp ? c.at<float>(c.w.h2) : nullptr;
+  la.dH = mlp ? c.at<float>(c.w.dh2) : c.at<float>(c.w.dH);
+  la.wpart = c.at<float>(c.w.hpart);
+  la.g_w = grads + p.t[p.i_hw].off; la.g_b = grads + p.t[p.i_hb].off;
+  SEED_TRY(launch_heads_loss(la, st));
+  c.mark("heads_loss", 2);
 
   const bool dp = comm && comm_world(comm) > 1;
   if (p.kind == SEED_NET_MLP) {

@@ -249,6 +249,297 @@ __global__ void __launch_bounds__(256) policy_loss_kernel(const LossArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ fused heads + loss
+// One block per trajectory b.  Phase 1: logits | value = H W^T + b (H4; warp per
+// row, lane = output, H rows staged 32 at a time).  Phase 2: the policy loss of
+// policy_loss_kernel on those values (H5-H7).  Phase 3: dH = [dlogits|dvalue] W
+// (thread = hidden unit, W row in registers) and the per-trajectory weight /
+// bias gradient partials (summed over b in order by heads_wgrad_finish).
+constexpr int HL_RC = 32;
+constexpr int HL_THREADS = 512;
+constexpr int HL_CL = 4;   // CTAs (thread-block cluster) per trajectory
+#ifdef SEED_LSTM_PROF
+__device__ long long g_heads_prof[8];
+#define HL_STAMP(I) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_heads_prof[I] = clock64();
+extern "C" int seed_debug_heads_prof(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_heads_prof, sizeof(g_heads_prof)) == cudaSuccess ? 0 : 5;
+}
+#else
+#define HL_STAMP(I)
+#endif
+
+__global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS)
+    heads_loss_kernel(const LossArgs a) {
+  pdl_wait();
+  HL_STAMP(0)
+  extern __shared__ float hsm[];
+  const int I = a.I, A = a.A, A1 = A + 1, A1p = A1 | 1;
+  const int T = a.T, T1 = T + 1, b = blockIdx.x / HL_CL;
+  const int cr = (int)cluster_rank();
+  const int Rr = (T1 + HL_CL - 1) / HL_CL, rb0 = min(T1, cr * Rr), rb1 = min(T1, rb0 + Rr);
+  const size_t row0 = (size_t)b * T1;
+  float* Wt = hsm;                  // [I][A1p]
+  float* sL = Wt + I * A1p;         // [T1][A1p]: logits | value, then their gradients
+  float* Hc = hsm + (((size_t)I * A1p + (size_t)T1 * A1p + 3) & ~(size_t)3);   // [HL_RC][I], 16-B aligned
+  __shared__ float s_lse[256], s_tlp[256], s_H[256], s_pg[256], s_dv[257];
+  __shared__ int s_act[256];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = HL_THREADS / 32;
+  // per-trajectory scalars used by phase 2, loaded up front (off the critical path)
+  for (int t = tid; t < T; t += HL_THREADS) s_act[t] = a.action[row0 + t];
+  float pre_blp[8], pre_r[8], pre_g[8];   // warp 0, V-trace chunk inputs (T <= 256)
+  if (warp == 0) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = c * 128 + 4 * lane + j;
+        const bool ok = t < T;
+        pre_blp[c * 4 + j] = ok ? a.blp[row0 + t] : 0.f;
+        pre_r[c * 4 + j] = ok ? a.reward[row0 + t + 1] : 0.f;
+        pre_g[c * 4 + j] = ok ? a.discount * (a.done[row0 + t + 1] ? 0.f : 1.f) : 0.f;
+      }
+  }
+  // W^T staged with float4 loads (I % 4 == 0: a float4 never crosses a row)
+  for (int q4 = tid; q4 < A1 * I / 4; q4 += HL_THREADS) {
+    const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.hw) + q4);
+    const int q = q4 * 4, o = q / I, i = q - o * I;
+    Wt[i * A1p + o] = w4.x;
+    Wt[(i + 1) * A1p + o] = w4.y;
+    Wt[(i + 2) * A1p + o] = w4.z;
+    Wt[(i + 3) * A1p + o] = w4.w;
+  }
+  cluster_sync_all();   // every CTA of the cluster runs before any DSMEM store
+  // ---- phase 1: heads forward of this CTA's rows, one (row, output) dot product
+  // per thread; results stored into all HL_CL CTAs' sL (DSMEM all-gather)
+  for (int r0 = rb0; r0 < rb1; r0 += HL_RC) {
+    const int nr = min(HL_RC, rb1 - r0);
+    __syncthreads();
+    const float4* src = reinterpret_cast<const float4*>(a.H + (row0 + r0) * I);
+    for (int q = tid; q < nr * I / 4; q += HL_THREADS) reinterpret_cast<float4*>(Hc)[q] = src[q];
+    __syncthreads();
+    for (int q = tid; q < nr * A1; q += HL_THREADS) {
+      const int rr = q / A1, o = q - rr * A1;
+      const float* hr = Hc + rr * I;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 4
+      for (int i = 0; i < I; i += 4) {
+        const float4 h4 = *reinterpret_cast<const float4*>(hr + i);
+        a0 += h4.x * Wt[i * A1p + o];
+        a1 += h4.y * Wt[(i + 1) * A1p + o];
+        a2 += h4.z * Wt[(i + 2) * A1p + o];
+        a3 += h4.w * Wt[(i + 3) * A1p + o];
+      }
+      const float y = ((a0 + a1) + (a2 + a3)) + a.hb[o];
+      const int t = r0 + rr;
+      const uint32_t la = smem_u32(sL + t * A1p + o);
+#pragma unroll
+      for (int d = 0; d < HL_CL; ++d) st_cluster_f32(mapa_u32(la, d), y);
+      if (o < A) a.logits[(row0 + t) * A + o] = y;
+      else a.values[row0 + t] = y;
+    }
+  }
+  cluster_sync_all();   // all rows' logits | values present in every CTA
+  HL_STAMP(1)
+  // ---- phase 2: policy statistics, V-trace, losses (as policy_loss_kernel)
+  for (int t = warp; t < T; t += NW) {
+    const float z = lane < A ? sL[t * A1p + lane] : -INFINITY;
+    const float mx = warp_max(z);
+    const float e = lane < A ? expf(z - mx) : 0.f;
+    const float se = warp_sum(e);
+    const float lse = mx + logf(se);
+    const float lp = z - lse;
+    const float Hn = -warp_sum(lane < A ? expf(lp) * lp : 0.f);
+    const int act = s_act[t];
+    const float tl = __shfl_sync(0xffffffffu, lp, act & 31);
+    if (lane == 0) {
+      s_lse[t] = lse;
+      s_tlp[t] = tl;
+      s_H[t] = Hn;
+    }
+  }
+  __syncthreads();
+  HL_STAMP(2)
+  if (warp == 0) {
+    VtraceLaneState st;
+    st.init(sL[T * A1p + A]);
+    bool bad = !isfinite(st.carry_vs);
+    float sum_pg = 0.f, sum_b = 0.f, sum_h = 0.f;
+    const int nch = (T + 127) / 128;
+#pragma unroll
+    for (int ch = 1; ch >= 0; --ch) {   // static chunk index: the prefetched inputs stay in registers
+      if (ch >= nch) continue;
+      const int t0 = ch * 128 + 4 * lane;
+      float d[4], r[4], g[4], v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = t0 + j;
+        d[j] = r[j] = g[j] = v[j] = 0.f;
+        if (t < T) {
+          d[j] = s_tlp[t] - pre_blp[ch * 4 + j];
+          r[j] = pre_r[ch * 4 + j];
+          g[j] = pre_g[ch * 4 + j];
+          v[j] = sL[t * A1p + A];
+        }
+      }
+      float vs[4], pg[4];
+      bad |= vtrace_chunk<32>(st, lane, t0, T, d, r, g, v, a.rho_bar, a.c_bar, a.lam, vs, pg);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = t0 + j;
+        if (t >= T) continue;
+        s_pg[t] = pg[j];
+        const float dv = a.scale * a.vf_coef * (v[j] - vs[j]);
+        s_dv[t] = dv;
+        if (cr == 0) {   // phase 2 runs redundantly in every CTA; rank 0 writes
+          a.vs[(size_t)b * T + t] = vs[j];
+          a.pg[(size_t)b * T + t] = pg[j];
+          a.dvalues[row0 + t] = dv;
+        }
+        sum_pg += -pg[j] * s_tlp[t];
+        sum_b += (vs[j] - v[j]) * (vs[j] - v[j]);
+        sum_h += s_H[t];
+      }
+    }
+    sum_pg = warp_sum(sum_pg);
+    sum_b = warp_sum(sum_b);
+    sum_h = warp_sum(sum_h);
+    const unsigned anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0 && cr == 0) {
+      float* pp = a.part + (size_t)b * 4;
+      pp[0] = a.scale * sum_pg;
+      pp[1] = a.scale * 0.5f * a.vf_coef * sum_b;
+      pp[2] = -a.scale * a.ent_coef * sum_h;
+      pp[3] = anybad ? 1.f : 0.f;
+      a.dvalues[row0 + T] = 0.f;   // bootstrap is a constant (C4)
+    }
+    if (lane == 0) s_dv[T] = 0.f;
+  }
+  __syncthreads();
+  HL_STAMP(3)
+  for (int q = tid; q < T1 * A1; q += HL_THREADS) {
+    const int t = q / A1, k = q - t * A1;
+    float d;
+    if (k == A) {
+      d = s_dv[t];
+    } else if (t == T) {
+      d = 0.f;
+      if (cr == 0) a.dlogits[(row0 + t) * A + k] = 0.f;
+    } else {
+      const float lp = sL[t * A1p + k] - s_lse[t];
+      const float p = expf(lp);
+      const float onehot = (k == s_act[t]) ? 1.f : 0.f;
+      d = a.scale * (-s_pg[t] * (onehot - p) + a.ent_coef * p * (lp + s_H[t]));
+      if (cr == 0) a.dlogits[(row0 + t) * A + k] = d;
+    }
+    sL[t * A1p + k] = d;
+  }
+  // ---- phase 3: dH and the per-trajectory weight / bias gradients; thread =
+  // (hidden unit i, row parity rg); the two row-parity partials are added in order
+  HL_STAMP(4)
+  constexpr int AMAX = 33;
+  const int ci = tid & 255, rg = tid >> 8;
+  const bool col = ci < I;
+  float wreg[AMAX], acc[AMAX];
+#pragma unroll
+  for (int o = 0; o < AMAX; ++o) {
+    wreg[o] = (col && o < A1) ? Wt[ci * A1p + o] : 0.f;
+    acc[o] = 0.f;
+  }
+  for (int r0 = rb0; r0 < rb1; r0 += HL_RC) {
+    const int nr = min(HL_RC, rb1 - r0);
+    __syncthreads();
+    const float4* src = reinterpret_cast<const float4*>(a.H + (row0 + r0) * I);
+    for (int q = tid; q < nr * I / 4; q += HL_THREADS) reinterpret_cast<float4*>(Hc)[q] = src[q];
+    __syncthreads();
+    if (col) {
+      for (int rr = rg; rr < nr; rr += 2) {
+        const int t = r0 + rr;
+        const float h = Hc[rr * I + ci];
+        const float* dl = sL + t * A1p;
+        float dh = 0.f;
+#pragma unroll
+        for (int o = 0; o < AMAX; ++o) {
+          if (o < A1) {
+            const float d = dl[o];
+            dh += d * wreg[o];
+            acc[o] += d * h;
+          }
+        }
+        const size_t idx = (row0 + t) * I + ci;
+        if (a.hmask && !(a.hmask[idx] > 0.f)) dh = 0.f;
+        a.dH[idx] = dh;
+      }
+    }
+  }
+  __syncthreads();   // Hc free: row-parity-1 partials go through it
+  HL_STAMP(5)
+  float* red = Hc;   // [A1][I]
+  if (col && rg == 1) {
+#pragma unroll
+    for (int o = 0; o < AMAX; ++o)
+      if (o < A1) red[o * I + ci] = acc[o];
+  }
+  __syncthreads();
+  float* wp = a.wpart + (size_t)blockIdx.x * A1 * (I + 1);   // partial (b, cr)
+  if (col && rg == 0) {
+#pragma unroll
+    for (int o = 0; o < AMAX; ++o)
+      if (o < A1) wp[(size_t)o * (I + 1) + ci] = acc[o] + red[o * I + ci];
+  }
+  if (tid < A1) {
+    float sb = 0.f;
+    for (int t = rb0; t < rb1; ++t) sb += sL[t * A1p + tid];
+    wp[(size_t)tid * (I + 1) + I] = sb;
+  }
+  HL_STAMP(6)
+}
+
+// heads weight / bias gradient: fixed-order sum of the per-(trajectory, cluster
+// rank) partials.  Block = 32 outputs x 8 groups; group g adds partials
+// g, g+8, ... in order, then the 8 group sums are added in order.
+__global__ void __launch_bounds__(256) heads_wgrad_finish(int NP, int A1, int I, const float* __restrict__ wpart,
+                                                          float* __restrict__ g_w, float* __restrict__ g_b) {
+  pdl_wait();
+  const int n = A1 * (I + 1);
+  const int q = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
+  __shared__ float sh[8][33];
+  float s = 0.f;
+  if (q < n) {
+#pragma unroll 4
+    for (int b = g; b < NP; b += 8) s += __ldcg(wpart + (size_t)b * n + q);
+  }
+  sh[g][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (g == 0 && q < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x];
+    const int o = q / (I + 1), i = q - o * (I + 1);
+    if (i < I) g_w[(size_t)o * I + i] = t;
+    else g_b[o] = t;
+  }
+}
+
+seed_status launch_heads_loss(const LossArgs& a, cudaStream_t st) {
+  if (a.T > 256 || a.A > 32 || a.I > 256 || (a.I & 3)) return SEED_E_SHAPE;
+  const int A1p = (a.A + 1) | 1;
+  // Hc holds HL_RC rows of H, later the [A+1][I] row-parity partials (A+1 <= HL_RC+1)
+  const size_t smem = ((((size_t)a.I * A1p + (size_t)(a.T + 1) * A1p + 3) & ~(size_t)3) +
+                       (size_t)(HL_RC + 1) * a.I) * 4;
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(heads_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (256 * 33 + 257 * 33 + 4 + (HL_RC + 1) * 256) * 4));
+    attr = true;
+  }
+  SEED_TRY(launch_k(heads_loss_kernel, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
+  const int n = (a.A + 1) * (a.I + 1);
+  return launch_k(heads_wgrad_finish, dim3(ceil_div(n, 32)), dim3(256), 0, st, a.B * HL_CL, a.A + 1,
+                  a.I, (const float*)a.wpart, a.g_w, a.g_b);
+}
+
 seed_status launch_policy_loss(const LossArgs& a, cudaStream_t st) {
   if (a.T > 256 || a.A > 32) return SEED_E_SHAPE;
   return launch_k(policy_loss_kernel, dim3(a.B), dim3(256), 0, st, a);

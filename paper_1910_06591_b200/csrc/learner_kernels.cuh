@@ -36,8 +36,8 @@ __global__ void dense_wgrad_f32(int R, int I, int O, const float* __restrict__ d
 
 struct LossArgs {
   int B, T, A;
-  const float* logits;   // [B][T+1][A]
-  const float* values;   // [B][T+1]
+  float* logits;         // [B][T+1][A] (input of policy_loss_kernel, output of the fused kernel)
+  float* values;         // [B][T+1]
   const int32_t* action;
   const float* blp;
   const float* reward;
@@ -48,8 +48,21 @@ struct LossArgs {
   float* vs;             // [B][T]
   float* pg;             // [B][T]
   float* part;           // [B][4]: scaled pg, baseline, entropy terms, nonfinite
+  // fused heads (launch_heads_loss): the heads forward (H4) runs inside the loss
+  // kernel, which also forms the heads backward (H8): logits / values above
+  // become outputs, and
+  const float* H;        // [B*(T+1)][I] fp32 core output
+  int I;                 // I <= 256, I % 4 == 0
+  const float* hw;       // [A+1][I] heads weights (row A = value head)
+  const float* hb;       // [A+1]
+  const float* hmask;    // nullable: dH zeroed where hmask <= 0 (ReLU input)
+  float* dH;             // [B*(T+1)][I]
+  float* wpart;          // [B][A+1][I+1] per-trajectory heads weight | bias gradients
+  float* g_w;            // [A+1][I] heads weight gradient (fixed-order sum over b)
+  float* g_b;            // [A+1]
 };
 seed_status launch_policy_loss(const LossArgs& a, cudaStream_t st);
+seed_status launch_heads_loss(const LossArgs& a, cudaStream_t st);
 
 // X[f][256 + j] for j in [0, Kxp-256): onehot(prev_action), clip(reward), 1, 0 pad (C15)
 __global__ void core_extras_kernel(int F, int A, int Kxp, const int32_t* __restrict__ prev_action,

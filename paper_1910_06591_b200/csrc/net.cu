@@ -187,6 +187,7 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   w->dlogits = bump(cur, F * A * 4);
   w->dvalues = bump(cur, F * 4);
   w->loss_part = bump(cur, (size_t)B * 4 * 4);
+  w->hpart = bump(cur, (size_t)B * 4 * (A + 1) * (std::max(p.U, 64) + 1) * 4);   // heads grad partials (b, cluster rank)
   w->flag = bump(cur, 16);
   w->norm_part = bump(cur, NORM_BLOCKS * 8 + 64);   // + clip/Adam coefficients, norm
   w->step_in = bump(cur, 8);

@@ -38,6 +38,10 @@ lib = C.CDLL(PROF)
 buf = np.zeros((2, 258, 4), dtype=np.int64)
 assert lib.seed_debug_lstm_prof(buf.ctypes.data_as(C.c_void_p)) == 0
 T1 = T + 1
+hp = np.zeros(8, dtype=np.int64)
+if lib.seed_debug_heads_prof(hp.ctypes.data_as(C.c_void_p)) == 0:
+    print("heads_loss phases (cycles): fwd", hp[1] - hp[0], "stats", hp[2] - hp[1], "vtrace", hp[3] - hp[2],
+          "dlogits", hp[4] - hp[3], "bwd", hp[5] - hp[4], "partials", hp[6] - hp[5], "total", hp[6] - hp[0])
 for k, name in ((0, "fwd"), (1, "bwd")):
     st = buf[k, :T1]
     wait = st[1:, 1] - st[1:, 0]
