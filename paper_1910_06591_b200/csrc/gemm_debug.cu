@@ -27,6 +27,9 @@ struct DebugGemm {
     return BT ? B + (size_t)i * N + j : B + (size_t)i * K + j;
   }
   __device__ void store(int m, int n, float v) const { D[(size_t)m * N + n] = v; }
+  static constexpr bool ROW_OUT = true;
+  __device__ float* out_row(int m) const { return D + (size_t)m * N; }
+  __device__ float post(int, int, float v) const { return v; }
 };
 
 template <int BN, bool AT, bool BT>
@@ -76,3 +79,9 @@ extern "C" seed_status seed_debug_gemm(int M, int N, int K, const void* A, int a
     default: return SEED_E_ARG;
   }
 }
+
+#ifdef SEED_LSTM_PROF
+extern "C" int seed_debug_gemm_prof(long long* out) {
+  return cudaMemcpyFromSymbol(out, seed::g_gemm_prof, sizeof(seed::g_gemm_prof)) == cudaSuccess ? 0 : 5;
+}
+#endif

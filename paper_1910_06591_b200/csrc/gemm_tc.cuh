@@ -102,7 +102,9 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_FIT = (200 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 256;
+  // + barriers (256 B) + the epilogue's per-warp 32 x 33 fp32 transpose buffers
+  static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 256 + EPI_BYTES;
   static constexpr uint32_t ACC_COLS = BN;   // two accumulators of BN columns
   static constexpr uint32_t TMEM_COLS =
       2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
@@ -120,6 +122,12 @@ template <class Prob, class = void>
 struct HasStore16 : std::false_type {};
 template <class Prob>
 struct HasStore16<Prob, decltype((void)Prob::VEC_STORE)> : std::integral_constant<bool, Prob::VEC_STORE> {};
+
+// Problems whose output row m is a contiguous fp32 row (out_row(m)[n] = post(m, n, acc))
+template <class Prob, class = void>
+struct HasRowOut : std::false_type {};
+template <class Prob>
+struct HasRowOut<Prob, decltype((void)Prob::ROW_OUT)> : std::integral_constant<bool, Prob::ROW_OUT> {};
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
@@ -166,33 +174,72 @@ template <int BN, class Prob>
 __device__ __forceinline__ void gemm_epilogue(const Prob& p, float* __restrict__ part, int splits,
                                               int z, int m0, int n0, bool have, uint32_t tmem,
                                               int q, int lane, unsigned* cnt, int tile,
-                                              int* s_last) {
+                                              int* s_last, float* stg) {
   const int m = m0 + q * 32 + lane;
+  constexpr bool ROWOUT = HasRowOut<Prob>::value;
+  if (splits > 1 || ROWOUT) {
+    // Coalesced path: the warp's 32 rows x 32 columns go through a padded shared
+    // buffer, then each store instruction covers 4 rows x 128 contiguous bytes
+    // (one lane per row would scatter 32 rows per instruction).
+    float* out = nullptr;
+    size_t ld = 0;
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    float v[16];
-    if (have) {
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c, v);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.f;
-    }
-    const int n = n0 + c;
-    if (m < p.M && n < p.N) {
-      if (splits > 1) {
-        float* dst = part + ((size_t)z * p.M + m) * p.N + n;
-        if (n + 16 <= p.N) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      if (have) {
+        if (c + 32 <= BN) {
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, v);
         } else {
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c, v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (n + i < p.N) dst[i] = v[i];
+          for (int i = 16; i < 32; ++i) v[i] = 0.f;
         }
       } else {
-        gemm_store16(p, m, n, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
       }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+      __syncwarp();
+      const int cc = 4 * (lane & 7);
+#pragma unroll
+      for (int r0 = 0; r0 < 32; r0 += 4) {
+        const int r = r0 + (lane >> 3);
+        const int mm = m0 + q * 32 + r, nn = n0 + c + cc;
+        if (mm < p.M && nn < p.N && c + cc < BN) {
+          float4 o = make_float4(stg[r * 33 + cc], stg[r * 33 + cc + 1], stg[r * 33 + cc + 2],
+                                 stg[r * 33 + cc + 3]);
+          if constexpr (ROWOUT) {
+            if (splits == 1) {
+              out = p.out_row(mm);
+              o.x = p.post(mm, nn, o.x); o.y = p.post(mm, nn + 1, o.y);
+              o.z = p.post(mm, nn + 2, o.z); o.w = p.post(mm, nn + 3, o.w);
+            }
+          }
+          if (splits > 1) { out = part + ((size_t)z * p.M + mm) * p.N; ld = 0; }
+          (void)ld;
+          if (nn + 4 <= p.N && (p.N & 3) == 0) {
+            *reinterpret_cast<float4*>(out + nn) = o;
+          } else {
+            const float t4[4] = {o.x, o.y, o.z, o.w};
+            for (int i = 0; i < 4 && nn + i < p.N; ++i) out[nn + i] = t4[i];
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      float v[16];
+      if (have) {
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+      const int n = n0 + c;
+      if (m < p.M && n < p.N) gemm_store16(p, m, n, v);
     }
   }
   if (splits > 1 && cnt) {
@@ -233,9 +280,19 @@ __device__ __forceinline__ void gemm_epilogue(const Prob& p, float* __restrict__
   }
 }
 
+#ifdef SEED_LSTM_PROF
+// diagnostic build only: clock64 stamps of CTA 0 (setup, producer, MMA, epilogue)
+__device__ long long g_gemm_prof[8];
+#define GEMM_STAMP(I, COND) \
+  if (blockIdx.x == 0 && (COND)) g_gemm_prof[I] = clock64();
+#else
+#define GEMM_STAMP(I, COND)
+#endif
+
 template <int BN, class Prob>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, float* __restrict__ part,
                                                                   int splits, unsigned* cnt) {
+  GEMM_STAMP(0, threadIdx.x == 0)
   using Cfg = GemmCfg<BN, Prob::A_MN, Prob::B_MN>;
   using TA = typename Cfg::TA;
   using TB = typename Cfg::TB;
@@ -248,6 +305,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  float* epi_stage = reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES + 256);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int mt = (p.M + GEMM_BM - 1) / GEMM_BM, nt = (p.N + BN - 1) / BN;
@@ -270,6 +328,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
   __syncthreads();
   tc_fence_after();
   pdl_wait();
+  GEMM_STAMP(1, threadIdx.x == 0)
   const uint32_t tmem = *tmem_slot;
 
   auto decode = [&](int w, int& m0, int& n0, int& kb0, int& nkb, int& z) {
@@ -319,6 +378,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
           }
           if (zeroed) fence_proxy_async_smem();
           cp_async_arrive(&full[s]);
+          GEMM_STAMP(2, tid == 0 && g == 0)
         } else {
           uint4 ra[Cfg::A_CHUNKS], rb[Cfg::B_CHUNKS];
           int oa[Cfg::A_CHUNKS], ob[Cfg::B_CHUNKS];
@@ -366,6 +426,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
         for (int i = 0; i < nkb; ++i, ++g) {
           const int s = g % S;
           mbar_wait(&full[s], (g / S) & 1);
+          GEMM_STAMP(3, g == 0)
           tc_fence_after();
           const uint32_t a_base = smem0 + s * Cfg::STAGE_BYTES;
           const uint32_t b_base = a_base + Cfg::A_BYTES;
@@ -379,6 +440,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
         }
         if (nkb > 0) tc_commit(&tfull[acc]);
         else mbar_arrive(&tfull[acc]);
+        GEMM_STAMP(4, it == 0)
       }
     }
     __syncwarp();
@@ -391,17 +453,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
       decode(w, m0, n0, kb0, nkb, z);
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
+      GEMM_STAMP(5, it == 0 && q == 0 && lane == 0)
       tc_fence_after();
       gemm_epilogue<BN>(p, part, splits, z, m0, n0, nkb > 0, tmem + acc * Cfg::ACC_COLS, q, lane, cnt,
-                        w / splits, s_last);
+                        w / splits, s_last, epi_stage + q * 32 * 33);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      GEMM_STAMP(6, it == 0 && q == 0 && lane == 0)
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == GEMM_MMA_WARP) tmem_dealloc(tmem, Cfg::TMEM_COLS);
+  GEMM_STAMP(7, threadIdx.x == 0)
 }
 
 // Fixed-order split-K reduction: each thread owns 4 consecutive outputs and

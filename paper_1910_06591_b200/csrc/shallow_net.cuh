@@ -85,6 +85,9 @@ struct XprojFwd {
   __device__ const void* ptr_a(int m, int k) const { return X + (size_t)m * K + k; }
   __device__ const void* ptr_b(int n, int k) const { return w + (size_t)n * K + k; }
   __device__ void store(int m, int n, float v) const { out[(size_t)m * N + n] = v + bias[n]; }
+  static constexpr bool ROW_OUT = true;   // coalesced staged epilogue (gemm_tc.cuh)
+  __device__ float* out_row(int m) const { return out + (size_t)m * N; }
+  __device__ float post(int, int n, float v) const { return v + bias[n]; }
   static constexpr bool VEC_STORE = true;
   __device__ void store16(int m, int n0, float (&v)[16]) const {
     float4* o = reinterpret_cast<float4*>(out + (size_t)m * N + n0);
