@@ -64,21 +64,20 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return copysignf(t, x);
 }
 
-// CTA r's W_h slice: local row lc = gate*32 + j  <-  global row gate*U + 32r + j
-// (blockDim 256: 16 chunks per thread, all loads issued before the first store)
+// CTA r's W_h slice: local row lc = gate*32 + j  <-  global row gate*U + 32r + j.
+// cp.async (16 B, L2 only), 16 chunks per thread (blockDim 256), left in flight:
+// the caller overlaps its other setup loads and calls cp_async_wait_all().
 __device__ __forceinline__ void load_wh_slice(__nv_bfloat16* Ws, const __nv_bfloat16* wh, int r) {
-  uint4 v[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int c = threadIdx.x + 256 * q, lc = c >> 5, kc = c & 31;
     const int gr = (lc >> 5) * LSTM_U + 32 * r + (lc & 31);
-    v[q] = ld16(wh + (size_t)gr * LSTM_U + kc * 8);
+    cp_async16(smem_u32(Ws + lc * HP + kc * 8), wh + (size_t)gr * LSTM_U + kc * 8, true);
   }
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int c = threadIdx.x + 256 * q, lc = c >> 5, kc = c & 31;
-    *reinterpret_cast<uint4*>(Ws + lc * HP + kc * 8) = v[q];
-  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---- DSMEM transaction handshake (no cluster barrier inside the step loop):
@@ -155,21 +154,22 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     mbar_init(&hbar[1], 1);
     fence_mbar_init();
   }
+  load_wh_slice(Ws, a.wh, r);   // in flight during the state loads below
   for (int i = tid; i < BBT * T1; i += 256) {
     const int b = i / T1, t = i % T1;
     dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
   }
-  load_wh_slice(Ws, a.wh, r);
-  __syncthreads();   // dn_s visible: the initial state reads use its step-0 flags
   // bf16 h_{-1} for all MR rows (zero past B and on a step-0 reset), float4 reads
+  // issued unconditionally (all in flight), the reset applied afterwards
 #pragma unroll
   for (int q = 0; q < MR * U / 4 / 256; ++q) {
     const int idx = tid + 256 * q, b = idx / (U / 4), k = (idx % (U / 4)) * 4;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (b < BB && !dn_s[b * T1]) {
+    if (b < BB) {
       const int bb = b0 + b;
       const int srow = a.state_rows ? a.state_rows[bb] : bb;
-      v = *reinterpret_cast<const float4*>(a.h0 + (size_t)srow * U + k);
+      const float4 h4 = *reinterpret_cast<const float4*>(a.h0 + (size_t)srow * U + k);
+      if (!a.done[(size_t)bb * T1]) v = h4;
     }
     *reinterpret_cast<uint2*>(hb + b * HP + k) = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
   }
@@ -179,14 +179,13 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     if (b < BB) {
       const int bb = b0 + b;
       const int srow = a.state_rows ? a.state_rows[bb] : bb;
-      if (!dn_s[b * T1]) {
-        c = a.c0[(size_t)srow * U + 32 * r + j];
-        h = a.h0[(size_t)srow * U + 32 * r + j];
-      }
+      const float c0 = a.c0[(size_t)srow * U + 32 * r + j], h0 = a.h0[(size_t)srow * U + 32 * r + j];
+      if (!a.done[(size_t)bb * T1]) { c = c0; h = h0; }
       if (a.Hprev) a.Hprev[((size_t)bb * T1) * U + 32 * r + j] = __float2bfloat16_rn(h);
     }
     cst[b * 32 + j] = c;
   }
+  cp_async_wait_all();
   __syncthreads();
   cluster_sync_all();   // barriers initialised everywhere before any st.async
   LSTM_STAMP(0, MAX_T1, 1)
@@ -221,6 +220,11 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   };
   load_x(0);
   const int gid = lane >> 2, tig = lane & 3;
+  // this warp's 16 W_h rows as mma A fragments, register-resident for all steps
+  uint32_t wfrag[16][4];
+#pragma unroll
+  for (int ks = 0; ks < 16; ++ks)
+    ldsm_x4(smem_u32(Ws + (warp * 16 + (lane & 15)) * HP + ks * 16 + (lane >> 4) * 8), wfrag[ks]);
   for (int t = 0; t < T1; ++t) {
     const int cur = t & 1, nbuf = cur ^ 1;
     LSTM_STAMP(0, t, 0)
@@ -241,8 +245,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     const int mi = lane >> 3;
 #pragma unroll
     for (int ks = 0; ks < 16; ++ks) {
-      uint32_t af[4];
-      ldsm_x4(smem_u32(Ws + (warp * 16 + (lane & 15)) * HP + ks * 16 + (lane >> 4) * 8), af);
+      const uint32_t (&af)[4] = wfrag[ks];
       if constexpr (NT == 1) {
         uint32_t b2[2];
         ldsm_x2(smem_u32(hcur + (lane & 7) * HP + ks * 16 + (mi & 1) * 8), b2);
@@ -303,7 +306,8 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
           const uint32_t pv = pack_bf16(h0n, h1n);
           const uint32_t off = (uint32_t)((nbuf * MR * HP + b * HP + col) * 2);
 #pragma unroll
-          for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2) st_async_u32(rh[s2] + off, pv, rbar[nbuf][s2]);
+          for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2)
+            st_async_u32(rh[s2] + off, pv, nbuf ? rbar[1][s2] : rbar[0][s2]);
           if (a.Hprev) *reinterpret_cast<uint32_t*>(a.Hprev + (row + 1) * U + col) = pv;
         } else if (a.hT) {
           const int srow = a.state_rows ? a.state_rows[bb] : bb;
@@ -325,7 +329,8 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
         // rows beyond B still credit the receivers' transaction count (zeros)
         const uint32_t off = (uint32_t)((nbuf * MR * HP + b * HP + 32 * r + j) * 2);
 #pragma unroll
-        for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2) st_async_u32(rh[s2] + off, 0u, rbar[nbuf][s2]);
+        for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2)
+          st_async_u32(rh[s2] + off, 0u, nbuf ? rbar[1][s2] : rbar[0][s2]);
       }
     }
     __syncthreads();   // gpre / cst reuse
@@ -367,6 +372,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   }
   for (int i = tid; i < MR * DP; i += 256) dzs[i] = __float2bfloat16_rn(0.f);
   for (int i = tid; i < MR * 32; i += 256) dcs[i] = 0.f;
+  cp_async_wait_all();
   __syncthreads();
   cluster_sync_all();
   LSTM_STAMP(1, MAX_T1, 1)
@@ -374,14 +380,6 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   // per-thread cell work: NQ (row, unit) items; prefetched per step
   constexpr int NQ = (BBT * 32 + 255) / 256;
   float pdh[NQ], pg[NQ][4], pc[NQ], pcp[NQ];
-  // remote (DSMEM) addresses: reduction buffers and barriers of the 8 CTAs
-  uint32_t rred[LSTM_CLUSTER], rrb[2][LSTM_CLUSTER];
-#pragma unroll
-  for (int s2 = 0; s2 < LSTM_CLUSTER; ++s2) {
-    rred[s2] = mapa_u32(smem_u32(red), s2);
-    rrb[0][s2] = mapa_u32(smem_u32(&rbar[0]), s2);
-    rrb[1][s2] = mapa_u32(smem_u32(&rbar[1]), s2);
-  }
   auto load_in = [&](int t) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -401,6 +399,19 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   };
   load_in(T1 - 1);
   const int gid = lane >> 2, tig = lane & 3;
+  // W_h^T fragments (hidden units of CTA `warp` x this CTA's 128 gate columns),
+  // register-resident for all steps
+  uint32_t wtfrag[8][2][4];
+  {
+    const int mi = lane >> 3;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+        ldsm_x4_t(smem_u32(Ws + (ks * 16 + (mi >> 1) * 8 + (lane & 7)) * HP + 32 * warp + mt * 16 +
+                           (mi & 1) * 8),
+                  wtfrag[ks][mt]);
+  }
   for (int u = 0; u < T1; ++u) {
     const int t = T1 - 1 - u;
     // partials produced at step u land in buffer u&1; consumed at step u+1
@@ -473,12 +484,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
       const int mi = lane >> 3;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        uint32_t af[2][4];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-          ldsm_x4_t(smem_u32(Ws + (ks * 16 + (mi >> 1) * 8 + (lane & 7)) * HP + 32 * warp + mt * 16 +
-                             (mi & 1) * 8),
-                    af[mt]);
+        const uint32_t (&af)[2][4] = wtfrag[ks];
         if constexpr (NT == 1) {
           uint32_t b2[2];
           ldsm_x2(smem_u32(dzs + (lane & 7) * DP + ks * 16 + (mi & 1) * 8), b2);
@@ -499,8 +505,9 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
         }
       }
       // hidden units [32*warp, 32*warp+32) belong to CTA `warp`: its slot r of buffer u&1
-      const uint32_t base = rred[warp] + (uint32_t)(((u & 1) * 8 + r) * MR * RP * 4);
-      const uint32_t rb = rrb[u & 1][warp];
+      // CTA `warp` owns these hidden units (mapa per step: no dynamically indexed arrays)
+      const uint32_t base = mapa_u32(smem_u32(red), warp) + (uint32_t)(((u & 1) * 8 + r) * MR * RP * 4);
+      const uint32_t rb = mapa_u32(smem_u32(&rbar[u & 1]), warp);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
