@@ -42,18 +42,19 @@ const Nccl& nccl() {
 }
 }  // namespace
 
+constexpr int COMM_EVENTS = 4;
 struct seed_comm {
   ncclComm_t comm;
   int rank, world;
   cudaStream_t side;          // all of this comm's collectives inside a learner step
-  cudaEvent_t ev[3];          // fork (bucket 1), fork (bucket 2), join
+  cudaEvent_t ev[COMM_EVENTS];   // bucket forks ..., join
 };
 
 namespace seed {
 seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaEvent_t* ev) {
   if (!c || c->world == 1 || !c->side) return SEED_E_ARG;
   *side = c->side;
-  for (int i = 0; i < 3; ++i) ev[i] = c->ev[i];
+  for (int i = 0; i < COMM_EVENTS; ++i) ev[i] = c->ev[i];
   return SEED_OK;
 }
 int comm_world(const seed_comm* c) { return c ? c->world : 1; }
@@ -79,13 +80,13 @@ extern "C" seed_status seed_comm_get_unique_id(void* id128) {
 
 extern "C" seed_status seed_comm_init(const void* id128, int rank, int world, seed_comm** out) {
   if (!id128 || !out || world < 1 || rank < 0 || rank >= world) return SEED_E_ARG;
-  seed_comm* c = new seed_comm{nullptr, rank, world, nullptr, {nullptr, nullptr, nullptr}};
+  seed_comm* c = new seed_comm{nullptr, rank, world, nullptr, {}};
   if (world > 1) {
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) {
       delete c;
       return SEED_E_CUDA;
     }
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < COMM_EVENTS; ++i)
       if (cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return SEED_E_CUDA;
@@ -108,7 +109,7 @@ extern "C" seed_status seed_comm_init(const void* id128, int rank, int world, se
 extern "C" seed_status seed_comm_destroy(seed_comm* c) {
   if (!c) return SEED_E_ARG;
   if (c->comm && nccl().ok) nccl().destroy(c->comm);
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < COMM_EVENTS; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   if (c->side) cudaStreamDestroy(c->side);
   delete c;

@@ -30,6 +30,10 @@
 
 namespace seed {
 
+seed_status comm_allreduce(seed_comm* comm, float* data, int64_t n, cudaStream_t st);
+seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaEvent_t* ev);
+int comm_world(const seed_comm* c);
+
 struct Trace {
   void** events = nullptr;
   const char** names = nullptr;
@@ -52,6 +56,19 @@ struct StepCtx {
   Trace* tr = nullptr;
   cudaStream_t st;
   int max_ctas = 0;   // > 0 while collectives run concurrently (SMs left for NCCL)
+  // H10 buckets: a gradient range that is final is allreduced on the comm's side
+  // stream while the main stream continues (same bucket order on every rank)
+  seed_comm* comm = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[4] = {};
+  int nbucket = 0;
+  seed_status bucket(float* g, int64_t n) {
+    if (!side || n <= 0 || nbucket >= 3) return SEED_OK;
+    SEED_CUDA_TRY(cudaEventRecord(ev[nbucket], st));
+    SEED_CUDA_TRY(cudaStreamWaitEvent(side, ev[nbucket], 0));
+    ++nbucket;
+    return comm_allreduce(comm, g, n, side);
+  }
   template <class T>
   T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
   // zeroed region after the column-sum partials: [0..15] tickets, then the
@@ -164,6 +181,8 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
     pr.g_wh = grads + p.t[p.i_wh].off;
     SEED_TRY(gemm<128>(c, pr, st, "lstm_wgrad"));
   }
+  // LSTM + heads gradients are final: first DP bucket
+  SEED_TRY(const_cast<StepCtx&>(c).bucket(grads + p.t[p.i_wx].off, p.P - p.t[p.i_wx].off));
   {
     DxFc pr{};
     pr.M = F; pr.N = 256; pr.K = 4 * U; pr.Kxp = p.Kxp;
@@ -178,6 +197,8 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
     pr.g_w = grads + p.t[p.i_fcw].off; pr.g_b = grads + p.t[p.i_fcb].off;
     SEED_TRY(gemm<128>(c, pr, st, "fc_wgrad"));
   }
+  // FC gradients final: second bucket
+  SEED_TRY(const_cast<StepCtx&>(c).bucket(grads + p.t[p.i_fcw].off, p.t[p.i_wx].off - p.t[p.i_fcw].off));
   {
     FcDgrad pr{};
     pr.M = F; pr.N = p.fc_in; pr.K = 256;
@@ -373,9 +394,7 @@ static seed_status mlp_backward(const StepCtx& c, const seed_batch* bt, const fl
   return last_launch();
 }
 
-seed_status comm_allreduce(seed_comm* comm, float* data, int64_t n, cudaStream_t st);
-seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaEvent_t* ev);
-int comm_world(const seed_comm* c);
+
 
 static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
                                      const seed_batch* batch, const seed_train_state* state,
@@ -459,31 +478,21 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
       c.mark("allreduce");
     }
   } else {
-    SEED_TRY(core_backward(c, batch, lowp, params, grads, st));
-    // H10 overlapped with the torso backward: the FC / LSTM / heads gradients
-    // (a contiguous tail of the flat layout, ~99% of the parameters) are final
-    // here; both buckets are reduced on the comm's side stream in the same
-    // order on every rank, and the step joins before the clip.
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev[3];
-    const int64_t tail = p.t[p.i_fcw].off;
+    // H10 overlapped with the rest of the backward: three buckets (LSTM+heads
+    // after the LSTM weight gradient, FC after its weight gradient, the torso at
+    // the end) reduced on the comm's side stream, joined before the clip.
     if (dp) {
-      SEED_TRY(comm_side(comm, &side, ev));
-      SEED_CUDA_TRY(cudaEventRecord(ev[0], st));
-      SEED_CUDA_TRY(cudaStreamWaitEvent(side, ev[0], 0));
-      SEED_TRY(comm_allreduce(comm, grads + tail, p.P - tail, side));
-      // (capping the GEMM grids to leave SMs to NCCL measured slower at N=2)
+      c.comm = comm;
+      SEED_TRY(comm_side(comm, &c.side, c.ev));
     }
+    SEED_TRY(core_backward(c, batch, lowp, params, grads, st));
     if (p.nsec > 0) SEED_TRY(deep_backward(c, batch, lowp, params, grads, st));
     else SEED_TRY(shallow_backward(c, batch, lowp, params, grads, st));
     if (dp) {
-      SEED_CUDA_TRY(cudaEventRecord(ev[1], st));
-      SEED_CUDA_TRY(cudaStreamWaitEvent(side, ev[1], 0));
-      SEED_TRY(comm_allreduce(comm, grads, tail, side));
-      SEED_CUDA_TRY(cudaEventRecord(ev[2], side));
-      SEED_CUDA_TRY(cudaStreamWaitEvent(st, ev[2], 0));
+      SEED_TRY(c.bucket(grads, p.t[p.i_fcw].off));
+      SEED_CUDA_TRY(cudaEventRecord(c.ev[3], c.side));
+      SEED_CUDA_TRY(cudaStreamWaitEvent(st, c.ev[3], 0));
       c.mark("allreduce_tail");
-      c.max_ctas = 0;
     }
   }
 

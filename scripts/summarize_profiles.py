@@ -25,6 +25,9 @@ def short(n):
     m = re.search(r"seed::(\w+)<.*?seed::(\w+)>", n)
     if m:
         return f"{m.group(1)}<{m.group(2)}>"
+    m = re.search(r"(\w+)<([^>]*)>\(", n)
+    if m:
+        return f"{m.group(1)}<{m.group(2).replace('seed::', '').strip()}>"
     m = re.search(r"(\w+)\(", n)
     return m.group(1) if m else n[:60]
 agg = defaultdict(lambda: [0, 0.0])
@@ -39,8 +42,8 @@ for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
 open(f"{outdir}/ncu_launch_list.md", "w").write(
     "# ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n"
     f"Source: `{launches}` from `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 "
-    "python bench.py --steps 3 --warmup 3 --no-cpu-baseline` (cold-cache, serialised launches: "
-    "compare shares, not absolutes; includes the bench's warm-up and V-trace leg).\n\n"
+    "python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra` (cold-cache, serialised "
+    "launches: compare shares, not absolutes; includes the bench's warm-up and e2e steps).\n\n"
     + "\n".join(lines) + "\n")
 
 # ---- full-set capture: per-kernel DRAM traffic and headline metrics
@@ -83,8 +86,9 @@ for r in rr[2:]:
 json.dump(out, open(f"{outdir}/ncu_full.json", "w"), indent=1)
 open(f"{outdir}/ncu_full.md", "w").write(
     "# ncu --set full captures (round 1)\n\n"
-    f"Source: `{rep}` (`ncu --set full --clock-control none --import-source on -k regex:..."
-    " python bench.py --steps 3 --warmup 3 --no-cpu-baseline`).  The DRAM column is the "
+    f"Source: `{rep}` (`ncu --set full --import-source on --clock-control none --launch-skip 25 "
+    "-c 25 python scripts/step_c2.py 2`: every kernel of the second eager c2 learner step, B=32 "
+    "T=20; cold cache per replay).  The DRAM column is the "
     "`traffic` figure bench.py reports for the dominant kernel.\n\n" + "\n".join(md) + "\n")
 print(open(f"{outdir}/ncu_full.md").read())
 print(open(f"{outdir}/ncu_launch_list.md").read()[:3000])
