@@ -219,6 +219,24 @@ seed_status seed_comm_destroy(seed_comm* comm);
 /* In-place sum allreduce of n fp32 device values (metrics, probes). */
 seed_status seed_comm_allreduce_f32(seed_comm* comm, float* data, int64_t n, void* stream);
 
+/* Peer-memory allreduce over NVLink (H10 without NCCL; one process per GPU,
+ * every pair of GPUs peer-capable).  Two-phase setup:
+ *   seed_comm_peer_setup: allocates this rank's exchange buffer (2*max_floats
+ *     fp32 + counters; freed by seed_comm_destroy) and writes its 64-byte CUDA
+ *     IPC handle to handle_out (host);
+ *   the caller all-gathers the handles (rank order) over its process group;
+ *   seed_comm_peer_open: maps every peer's buffer (handles = world*64 bytes,
+ *     host) and switches this comm's allreduce (n <= max_floats) to the peer
+ *     kernel: copy in -> cross-GPU arrival counters -> each rank sums its 1/N
+ *     slice over the ranks in rank order and writes it into every rank's
+ *     buffer -> counters -> copy out.  Results are bit-identical on all ranks.
+ * Waits are bounded (2 s): on timeout the kernel sets a device error flag that
+ * seed_comm_peer_status reports (SEED_E_NCCL) instead of hanging.
+ * All ranks must call every allreduce in the same order. */
+seed_status seed_comm_peer_setup(seed_comm* comm, int64_t max_floats, void* handle_out /* 64 B */);
+seed_status seed_comm_peer_open(seed_comm* comm, const void* handles /* world*64 B */);
+seed_status seed_comm_peer_status(seed_comm* comm);   /* synchronizes; SEED_OK or SEED_E_NCCL */
+
 /* ===========================================================================
  * Centralized inference (H12-H13; "load the recurrent states ... the
  * latest recurrent states are stored").

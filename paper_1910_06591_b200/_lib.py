@@ -71,6 +71,9 @@ _SIGS = {
     "seed_comm_init": (c_int, [c_void_p, c_int, c_int, P(c_void_p)]),
     "seed_comm_destroy": (c_int, [c_void_p]),
     "seed_comm_allreduce_f32": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "seed_comm_peer_setup": (c_int, [c_void_p, c_int64, c_void_p]),
+    "seed_comm_peer_open": (c_int, [c_void_p, c_void_p]),
+    "seed_comm_peer_status": (c_int, [c_void_p]),
     "seed_infer_workspace_size": (c_int, [P(NetSpec), c_int, P(c_size_t)]),
     "seed_infer": (c_int, [P(NetSpec), c_void_p, c_void_p, P(StateTable), c_int, c_void_p,
                            c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint64,

@@ -26,6 +26,8 @@ comm = S.Comm(rank, world)
 L = S.Learner(spec, T, B, params, hp, comm=comm)
 m = L.step({k: torch.from_numpy(v).cuda() for k, v in shards[rank].items()})
 torch.cuda.synchronize()
+if comm.peer:
+    comm.peer_status()   # raises if a peer wait timed out
 np.save(os.path.join(out, f"grads{rank}.npy"), L.grads.cpu().numpy())
 np.save(os.path.join(out, f"params{rank}.npy"), L.params.cpu().numpy())
 np.save(os.path.join(out, f"metrics{rank}.npy"), m.cpu().numpy())

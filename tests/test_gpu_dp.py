@@ -15,12 +15,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs 2 GPUs")
-def test_dp_two_ranks(tmp_path):
+@pytest.mark.parametrize("peer", ["0", "1"])
+def test_dp_two_ranks(tmp_path, peer):
+    """peer=1: the NVLink peer-memory allreduce (seed_comm_peer_*) instead of NCCL."""
     n = 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29533",
+           "--master-addr", "127.0.0.1", "--master-port", "2953" + peer,
            os.path.join(ROOT, "scripts", "dp_check.py"), str(tmp_path)]
-    subprocess.run(cmd, check=True, timeout=600)
+    subprocess.run(cmd, check=True, timeout=600, env=dict(os.environ, SEED_PEER=peer))
     g = [np.load(tmp_path / f"grads{r}.npy") for r in range(n)]
     p = [np.load(tmp_path / f"params{r}.npy") for r in range(n)]
     for r in range(1, n):
