@@ -6,7 +6,11 @@
 
 namespace seed {
 
-constexpr int WC_THREADS = 192;   // warp 0: TMA producer, warp 1: MMA, warps 2-5: epilogue
+constexpr int WC_THREADS = 192;   // wgrad: warp 0 TMA producer, warp 1 MMA, warps 2-5 epilogue
+// forward / dgrad: warp 0 producer, warp 1 MMA, warps 2-9 = two epilogue groups
+// taking alternate tiles (4 TMEM accumulators), so two tiles drain at once
+constexpr int WCF_THREADS = 320;
+constexpr int WCF_ACC = 4;
 constexpr int WC_MAX_STAGES = 8;
 constexpr int WC_SMEM_BUDGET = 200 * 1024;
 constexpr int WG_KS = 256;        // rows per weight-gradient k-stage
@@ -57,17 +61,17 @@ __device__ __forceinline__ int slab_phase(int64_t R0, int rb) {
 
 // ------------------------------------------------------------------ forward / dgrad
 template <class Epi, int RB>
-__global__ void __launch_bounds__(WC_THREADS, 1)
+__global__ void __launch_bounds__(WCF_THREADS, 1)
     win_conv_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes) {
   constexpr int N = Epi::N;
   constexpr uint32_t LAYOUT = swz_layout_code(RB);
   constexpr int WB = 4 * N * RB;
-  constexpr uint32_t TCOLS = 2 * N < 32 ? 32 : 2 * N;
+  constexpr uint32_t TCOLS = WCF_ACC * N < 32 ? 32 : WCF_ACC * N;
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
   uint8_t* Ws = sm;
   uint8_t* slabs = sm + ((WB + 1023) & ~1023);
-  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[2], tempty[2], wbar;
+  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[WCF_ACC], tempty[WCF_ACC], wbar;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int mn = a.off[0], mx = a.off[0];
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   const int64_t tiles = (a.M + 127) / 128;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < WCF_ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     mbar_init(&wbar, 1);
     fence_mbar_init();
   }
@@ -105,9 +109,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       const uint32_t wb = smem_u32(Ws);
       int it = 0;
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-        const int s = it % stages, acc = it & 1;
+        const int s = it % stages, acc = it % WCF_ACC;
         mbar_wait(&full[s], (it / stages) & 1);
-        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&tempty[acc], ((it / WCF_ACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t base =
             smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * 128 + mn, RB);
@@ -124,11 +128,13 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       }
     }
   } else {
-    const int q = warp & 3;   // TMEM lanes [32q, 32q+32) of this warp
+    const int q = warp & 3;            // TMEM lanes [32q, 32q+32) of this warp
+    const int grp = (warp - 2) >> 2;   // epilogue group: tiles it with it % 2 == grp
     int it = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      const int acc = it & 1;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      if ((it & 1) != grp) continue;
+      const int acc = it % WCF_ACC;
+      mbar_wait(&tfull[acc], (it / WCF_ACC) & 1);
       tc_fence_after();
       float v[N];
 #pragma unroll
@@ -167,7 +173,7 @@ seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st)
   }
   const int64_t tiles = (a.M + 127) / 128;
   const int grid = (int)std::min<int64_t>(tiles, 148);
-  return launch_k(win_conv_kernel<Epi, RB>, dim3(grid), dim3(WC_THREADS), smem, st, a, e, stages, slab);
+  return launch_k(win_conv_kernel<Epi, RB>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e, stages, slab);
 }
 
 // ------------------------------------------------------------------ epilogues

@@ -34,6 +34,24 @@ seed_status comm_allreduce(seed_comm* comm, float* data, int64_t n, cudaStream_t
 seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaEvent_t* ev);
 int comm_world(const seed_comm* c);
 
+// The library's second stream (per device, created once) and its event pool.
+// same != nullptr: no second branch (tracing), aux = same.
+static seed_status aux_stream(cudaStream_t same, cudaStream_t* aux, cudaEvent_t* ev6) {
+  static cudaStream_t streams[16] = {};
+  static cudaEvent_t events[16][6] = {};
+  int dev = 0;
+  SEED_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return SEED_E_ARG;
+  if (!streams[dev]) {
+    SEED_CUDA_TRY(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    for (int i = 0; i < 6; ++i)
+      SEED_CUDA_TRY(cudaEventCreateWithFlags(&events[dev][i], cudaEventDisableTiming));
+  }
+  *aux = same ? same : streams[dev];
+  for (int i = 0; i < 6; ++i) ev6[i] = events[dev][i];
+  return SEED_OK;
+}
+
 struct Trace {
   void** events = nullptr;
   const char** names = nullptr;
@@ -62,12 +80,27 @@ struct StepCtx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev[4] = {};
   int nbucket = 0;
-  seed_status bucket(float* g, int64_t n) {
+  seed_status bucket(float* g, int64_t n, cudaStream_t from) {
     if (!side || n <= 0 || nbucket >= 3) return SEED_OK;
-    SEED_CUDA_TRY(cudaEventRecord(ev[nbucket], st));
+    SEED_CUDA_TRY(cudaEventRecord(ev[nbucket], from));
     SEED_CUDA_TRY(cudaStreamWaitEvent(side, ev[nbucket], 0));
     ++nbucket;
     return comm_allreduce(comm, g, n, side);
+  }
+  // Independent backward GEMMs run as a second branch on `aux` (a process-wide
+  // stream of the library; inside a CUDA graph capture the event edges make it a
+  // parallel branch of the graph).  aux == st when the step is traced (phase
+  // marks need one stream) — then the branches simply run in order.
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fev[6] = {};
+  int nfev = 0;
+  seed_status edge(cudaStream_t from, cudaStream_t to) {   // `to` waits for `from`'s work so far
+    if (from == to) return SEED_OK;
+    if (nfev >= 6) return SEED_E_ARG;
+    SEED_CUDA_TRY(cudaEventRecord(fev[nfev], from));
+    SEED_CUDA_TRY(cudaStreamWaitEvent(to, fev[nfev], 0));
+    ++nfev;
+    return SEED_OK;
   }
   template <class T>
   T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -92,7 +125,8 @@ static seed_status gemm(const StepCtx& c, Prob pr, cudaStream_t st, const char* 
   const int s = pick_splits(pr.M, pr.N, BN, pr.K);
   // (the in-kernel last-CTA split reduction, launch_gemm's `cnt`, measured
   // slower here: few tiles -> the fixups serialise on a few SMs)
-  const seed_status r = launch_gemm<BN>(pr, s, st, c.at<float>(c.w.splitk), c.max_ctas);
+  float* part = (st == c.aux && c.aux != c.st) ? c.at<float>(c.w.splitk2) : c.at<float>(c.w.splitk);
+  const seed_status r = launch_gemm<BN>(pr, s, st, part, c.max_ctas);
   c.mark(name, s > 1 ? 2 : 1);
   return r;
 }
@@ -172,6 +206,10 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
   lb.done = bt->done; lb.dH = c.at<float>(w.dH); lb.dG = c.at<bf16>(w.dG);
   SEED_TRY(lstm_backward(lb, st));
   c.mark("lstm_bwd");
+  StepCtx& cc = const_cast<StepCtx&>(c);
+  cudaStream_t ax = c.aux;
+  // branch: LSTM weight gradient (aux) || FC input gradient (main)
+  SEED_TRY(cc.edge(st, ax));
   {
     LstmWgrad pr{};
     pr.M = 4 * U; pr.N = p.Kxp + U; pr.K = F;
@@ -179,10 +217,10 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
     pr.dG = c.at<bf16>(w.dG); pr.X = c.at<bf16>(w.X); pr.Hprev = c.at<bf16>(w.Hprev);
     pr.g_wx = grads + p.t[p.i_wx].off; pr.g_b = grads + p.t[p.i_lb].off;
     pr.g_wh = grads + p.t[p.i_wh].off;
-    SEED_TRY(gemm<128>(c, pr, st, "lstm_wgrad"));
+    SEED_TRY(gemm<128>(c, pr, ax, "lstm_wgrad"));
   }
   // LSTM + heads gradients are final: first DP bucket
-  SEED_TRY(const_cast<StepCtx&>(c).bucket(grads + p.t[p.i_wx].off, p.P - p.t[p.i_wx].off));
+  SEED_TRY(cc.bucket(grads + p.t[p.i_wx].off, p.P - p.t[p.i_wx].off, ax));
   {
     DxFc pr{};
     pr.M = F; pr.N = 256; pr.K = 4 * U; pr.Kxp = p.Kxp;
@@ -190,15 +228,17 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
     pr.dfc = c.at<bf16>(w.dfc);
     SEED_TRY(gemm<128>(c, pr, st, "dx_fc"));
   }
+  // branch: FC weight gradient (aux, after the LSTM weight gradient) || FC data gradient (main)
+  SEED_TRY(cc.edge(st, ax));
   {
     FcWgrad pr{};
     pr.M = 256; pr.N = p.fc_in + 8; pr.K = F; pr.fc_in = p.fc_in;
     pr.dfc = c.at<bf16>(w.dfc); pr.act2 = c.at<bf16>(w.act2);
     pr.g_w = grads + p.t[p.i_fcw].off; pr.g_b = grads + p.t[p.i_fcb].off;
-    SEED_TRY(gemm<128>(c, pr, st, "fc_wgrad"));
+    SEED_TRY(gemm<128>(c, pr, ax, "fc_wgrad"));
   }
   // FC gradients final: second bucket
-  SEED_TRY(const_cast<StepCtx&>(c).bucket(grads + p.t[p.i_fcw].off, p.t[p.i_wx].off - p.t[p.i_fcw].off));
+  SEED_TRY(cc.bucket(grads + p.t[p.i_fcw].off, p.t[p.i_wx].off - p.t[p.i_fcw].off, ax));
   {
     FcDgrad pr{};
     pr.M = F; pr.N = p.fc_in; pr.K = 256;
@@ -220,15 +260,20 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
   const LearnerWs& w = c.w;
   const int F = w.F;
   const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
-  float* part = c.at<float>(w.splitk);
-  SEED_TRY(shallow_s2d_conv2_wgrad(sg, F, c.at<uint8_t>(w.act1), c.at<uint8_t>(w.dY2), part,
-                                   grads + p.t[p.i_conv2w].off, grads + p.t[p.i_conv2b].off, st));
+  StepCtx& cc = const_cast<StepCtx&>(c);
+  cudaStream_t ax = c.aux;
+  // branch: conv2 weight gradient (aux; needs dY2) || conv2 data + conv1 weight gradients (main)
+  SEED_TRY(cc.edge(st, ax));
+  float* part2 = ax != st ? c.at<float>(w.splitk2) : c.at<float>(w.splitk);
+  SEED_TRY(shallow_s2d_conv2_wgrad(sg, F, c.at<uint8_t>(w.act1), c.at<uint8_t>(w.dY2), part2,
+                                   grads + p.t[p.i_conv2w].off, grads + p.t[p.i_conv2b].off, ax));
   c.mark("conv2_wgrad", 2);
   SEED_TRY(shallow_s2d_conv2_dgrad(sg, F, c.at<uint8_t>(w.dY2), lowp + p.im_conv2dg,
                                    c.at<uint8_t>(w.act1), c.at<uint8_t>(w.dY1), st));
   c.mark("conv2_dgrad");
-  SEED_TRY(shallow_s2d_conv1_wgrad(sg, F, c.at<uint8_t>(w.obs_bf16), c.at<uint8_t>(w.dY1), part,
-                                   grads + p.t[p.i_conv1w].off, grads + p.t[p.i_conv1b].off, st));
+  SEED_TRY(shallow_s2d_conv1_wgrad(sg, F, c.at<uint8_t>(w.obs_bf16), c.at<uint8_t>(w.dY1),
+                                   c.at<float>(w.splitk), grads + p.t[p.i_conv1w].off,
+                                   grads + p.t[p.i_conv1b].off, st));
   c.mark("conv1_wgrad", 2);
   return SEED_OK;
 }
@@ -485,11 +530,13 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
       c.comm = comm;
       SEED_TRY(comm_side(comm, &c.side, c.ev));
     }
+    SEED_TRY(aux_stream(tr != nullptr ? st : nullptr, &c.aux, c.fev));
     SEED_TRY(core_backward(c, batch, lowp, params, grads, st));
     if (p.nsec > 0) SEED_TRY(deep_backward(c, batch, lowp, params, grads, st));
     else SEED_TRY(shallow_backward(c, batch, lowp, params, grads, st));
+    SEED_TRY(c.edge(c.aux, st));   // join the aux branch
     if (dp) {
-      SEED_TRY(c.bucket(grads, p.t[p.i_fcw].off));
+      SEED_TRY(c.bucket(grads, p.t[p.i_fcw].off, st));
       SEED_CUDA_TRY(cudaEventRecord(c.ev[3], c.side));
       SEED_CUDA_TRY(cudaStreamWaitEvent(st, c.ev[3], 0));
       c.mark("allreduce_tail");

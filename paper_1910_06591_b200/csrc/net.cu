@@ -268,6 +268,7 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   }
   w->splitk_bytes = sk;
   w->splitk = bump(cur, sk + 16);
+  w->splitk2 = bump(cur, sk + 16);   // partials of the second (aux-stream) backward branch
   w->total = cur;
   return SEED_OK;
 }

@@ -92,7 +92,7 @@ struct LearnerWs {
   size_t total;
   // common
   size_t logits, values, vs, pg, dlogits, dvalues, loss_part, flag, norm_part, step_in, splitk,
-      colsum_part, dH, hpart;
+      colsum_part, dH, hpart, splitk2;
   size_t splitk_bytes;
   // shallow
   size_t obs_bf16, act1, act2, X, xproj, H, Hprev, gates, Cst, dG, dfc, dY2, dY1;
