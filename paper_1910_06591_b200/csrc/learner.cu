@@ -36,19 +36,19 @@ int comm_world(const seed_comm* c);
 
 // The library's second stream (per device, created once) and its event pool.
 // same != nullptr: no second branch (tracing), aux = same.
-static seed_status aux_stream(cudaStream_t same, cudaStream_t* aux, cudaEvent_t* ev6) {
+static seed_status aux_stream(cudaStream_t same, cudaStream_t* aux, cudaEvent_t* ev8) {
   static cudaStream_t streams[16] = {};
-  static cudaEvent_t events[16][6] = {};
+  static cudaEvent_t events[16][8] = {};
   int dev = 0;
   SEED_CUDA_TRY(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 16) return SEED_E_ARG;
   if (!streams[dev]) {
     SEED_CUDA_TRY(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
-    for (int i = 0; i < 6; ++i)
+    for (int i = 0; i < 8; ++i)
       SEED_CUDA_TRY(cudaEventCreateWithFlags(&events[dev][i], cudaEventDisableTiming));
   }
   *aux = same ? same : streams[dev];
-  for (int i = 0; i < 6; ++i) ev6[i] = events[dev][i];
+  for (int i = 0; i < 8; ++i) ev8[i] = events[dev][i];
   return SEED_OK;
 }
 
@@ -92,11 +92,11 @@ struct StepCtx {
   // parallel branch of the graph).  aux == st when the step is traced (phase
   // marks need one stream) — then the branches simply run in order.
   cudaStream_t aux = nullptr;
-  cudaEvent_t fev[6] = {};
+  cudaEvent_t fev[8] = {};
   int nfev = 0;
   seed_status edge(cudaStream_t from, cudaStream_t to) {   // `to` waits for `from`'s work so far
     if (from == to) return SEED_OK;
-    if (nfev >= 6) return SEED_E_ARG;
+    if (nfev >= 8) return SEED_E_ARG;
     SEED_CUDA_TRY(cudaEventRecord(fev[nfev], from));
     SEED_CUDA_TRY(cudaStreamWaitEvent(to, fev[nfev], 0));
     ++nfev;
@@ -164,13 +164,7 @@ static seed_status core_forward(const StepCtx& c, const seed_batch* bt, const bf
     pr.bias = params + p.t[p.i_fcb].off; pr.X = c.at<bf16>(w.X);
     SEED_TRY(gemm<128>(c, pr, st, "fc_fwd"));
   }
-  {
-    const int E = p.Kxp - 256;
-    const int64_t n = (int64_t)F * E;
-    SEED_TRY(launch_k(core_extras_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, F, p.A,
-                      p.Kxp, bt->prev_action, bt->reward, bt->done, c.at<bf16>(w.X)));
-    c.mark("core_extras");
-  }
+  SEED_TRY(const_cast<StepCtx&>(c).edge(c.aux, st));   // join: X extras written
   {
     XprojFwd pr{};
     pr.M = F; pr.N = 4 * p.U; pr.K = p.Kxp;
@@ -488,6 +482,18 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   if (p.kind == SEED_NET_MLP) {
     SEED_TRY(mlp_forward(c, batch, params, st));
   } else {
+    SEED_TRY(aux_stream(tr != nullptr ? st : nullptr, &c.aux, c.fev));
+    // the LSTM-input extras (one-hot, reward, ones column) only read the batch:
+    // an aux-stream branch beside the torso, joined before the input projection
+    SEED_TRY(c.edge(st, c.aux));
+    {
+      const int E = p.Kxp - 256;
+      const int64_t n = (int64_t)c.w.F * E;
+      SEED_TRY(launch_k(core_extras_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, c.aux,
+                        c.w.F, p.A, p.Kxp, batch->prev_action, batch->reward, batch->done,
+                        c.at<bf16>(c.w.X)));
+      c.mark("core_extras");
+    }
     if (p.nsec > 0) SEED_TRY(deep_forward(c, batch, lowp, params, st));
     else SEED_TRY(shallow_forward(c, batch, lowp, params, st));
     SEED_TRY(core_forward(c, batch, lowp, params, st));
@@ -530,7 +536,6 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
       c.comm = comm;
       SEED_TRY(comm_side(comm, &c.side, c.ev));
     }
-    SEED_TRY(aux_stream(tr != nullptr ? st : nullptr, &c.aux, c.fev));
     SEED_TRY(core_backward(c, batch, lowp, params, grads, st));
     if (p.nsec > 0) SEED_TRY(deep_backward(c, batch, lowp, params, grads, st));
     else SEED_TRY(shallow_backward(c, batch, lowp, params, grads, st));

@@ -163,7 +163,7 @@ seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, co
 //  3. all threads write the closed-form output gradients (H7).
 __global__ void __launch_bounds__(256) policy_loss_kernel(const LossArgs a) {
   pdl_wait();
-  __shared__ float s_lse[256], s_tlp[256], s_H[256], s_vs[256], s_pg[256];
+  __shared__ float s_lse[256], s_tlp[256], s_H[256], s_pg[256];
   const int b = blockIdx.x;
   const int T = a.T, T1 = a.T + 1, A = a.A;
   const size_t row0 = (size_t)b * T1;
@@ -211,7 +211,6 @@ __global__ void __launch_bounds__(256) policy_loss_kernel(const LossArgs a) {
       for (int j = 0; j < 4; ++j) {
         const int t = t0 + j;
         if (t >= T) continue;
-        s_vs[t] = vs[j];
         s_pg[t] = pg[j];
         a.vs[(size_t)b * T + t] = vs[j];
         a.pg[(size_t)b * T + t] = pg[j];
