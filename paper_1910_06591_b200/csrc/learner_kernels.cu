@@ -729,6 +729,31 @@ __device__ __forceinline__ int find_img(const uint32_t (*bounds)[2], int nimg, u
   return -1;
 }
 
+constexpr int ADAM_GPT = 2;   // float4 groups per thread, all loads in flight together
+
+struct AdamIn { float4 g, m, v, p; };
+__device__ __forceinline__ AdamIn adam_load(const AdamArgs& a, int64_t gi) {
+  const int64_t i0 = gi * 4;
+  AdamIn r;
+  if (i0 + 3 < a.P) {
+    r.g = reinterpret_cast<const float4*>(a.grads)[gi];
+    r.m = reinterpret_cast<const float4*>(a.m)[gi];
+    r.v = reinterpret_cast<const float4*>(a.v)[gi];
+    r.p = reinterpret_cast<const float4*>(a.params)[gi];
+  } else {
+    float* g = &r.g.x; float* m = &r.m.x; float* v = &r.v.x; float* p = &r.p.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool ok = i0 + q < a.P;
+      g[q] = ok ? a.grads[i0 + q] : 0.f;
+      m[q] = ok ? a.m[i0 + q] : 0.f;
+      v[q] = ok ? a.v[i0 + q] : 0.f;
+      p[q] = ok ? a.params[i0 + q] : 0.f;
+    }
+  }
+  return r;
+}
+
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
   pdl_wait();
   __shared__ uint32_t bounds[8][2];   // source parameter range of each bf16 image
@@ -744,63 +769,57 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
     // the IEEE-division slow path (zero / denormal operands) is kept off the loop
     const float scale = a.coef[0], ibc1 = 1.f / a.coef[1], ibc2 = 1.f / a.coef[2];
     const int64_t ngroups = (a.P + 3) / 4;
-    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ngroups;
-         gi += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t i0 = gi * 4;
-      float g[4], m[4], v[4], p[4];
-      const bool full = i0 + 3 < a.P;
-      if (full) {
-        const float4 G = reinterpret_cast<const float4*>(a.grads)[gi];
-        const float4 M = reinterpret_cast<const float4*>(a.m)[gi];
-        const float4 V = reinterpret_cast<const float4*>(a.v)[gi];
-        const float4 Pp = reinterpret_cast<const float4*>(a.params)[gi];
-        g[0] = G.x; g[1] = G.y; g[2] = G.z; g[3] = G.w;
-        m[0] = M.x; m[1] = M.y; m[2] = M.z; m[3] = M.w;
-        v[0] = V.x; v[1] = V.y; v[2] = V.z; v[3] = V.w;
-        p[0] = Pp.x; p[1] = Pp.y; p[2] = Pp.z; p[3] = Pp.w;
-      } else {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < ngroups; g0 += ADAM_GPT * T) {
+      AdamIn in[ADAM_GPT];
+#pragma unroll
+      for (int k = 0; k < ADAM_GPT; ++k)
+        if (g0 + k * T < ngroups) in[k] = adam_load(a, g0 + k * T);
+#pragma unroll
+      for (int k = 0; k < ADAM_GPT; ++k) {
+        const int64_t gi = g0 + k * T;
+        if (gi >= ngroups) break;
+        const int64_t i0 = gi * 4;
+        float g[4] = {in[k].g.x, in[k].g.y, in[k].g.z, in[k].g.w};
+        float m[4] = {in[k].m.x, in[k].m.y, in[k].m.z, in[k].m.w};
+        float v[4] = {in[k].v.x, in[k].v.y, in[k].v.z, in[k].v.w};
+        float p[4] = {in[k].p.x, in[k].p.y, in[k].p.z, in[k].p.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const bool ok = i0 + q < a.P;
-          g[q] = ok ? a.grads[i0 + q] : 0.f;
-          m[q] = ok ? a.m[i0 + q] : 0.f;
-          v[q] = ok ? a.v[i0 + q] : 0.f;
-          p[q] = ok ? a.params[i0 + q] : 0.f;
+          const float gg = g[q] * scale;
+          m[q] = a.beta1 * m[q] + (1.f - a.beta1) * gg;
+          v[q] = a.beta2 * v[q] + (1.f - a.beta2) * gg * gg;
+          p[q] = p[q] - __fdividef(a.lr * (m[q] * ibc1), sqrtf(v[q] * ibc2) + a.eps);
         }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float gg = g[q] * scale;
-        m[q] = a.beta1 * m[q] + (1.f - a.beta1) * gg;
-        v[q] = a.beta2 * v[q] + (1.f - a.beta2) * gg * gg;
-        p[q] = p[q] - __fdividef(a.lr * (m[q] * ibc1), sqrtf(v[q] * ibc2) + a.eps);
-      }
-      if (full) {
-        reinterpret_cast<float4*>(a.m)[gi] = make_float4(m[0], m[1], m[2], m[3]);
-        reinterpret_cast<float4*>(a.v)[gi] = make_float4(v[0], v[1], v[2], v[3]);
-        reinterpret_cast<float4*>(a.params)[gi] = make_float4(p[0], p[1], p[2], p[3]);
-      } else {
-        for (int q = 0; q < 4 && i0 + q < a.P; ++q) {
-          a.m[i0 + q] = m[q];
-          a.v[i0 + q] = v[q];
-          a.params[i0 + q] = p[q];
-        }
-      }
-      if (a.nimg) {
-        const int k0 = find_img(bounds, a.nimg, (uint32_t)i0);
-        const int k3 = find_img(bounds, a.nimg, (uint32_t)min(i0 + 3, a.P - 1));
-        if (k0 >= 0 && k0 == k3 && a.img[k0].kind == IMG_COPY_PAD) {
-          const LowpImg& im = a.img[k0];
-          uint32_t r, c;
-          img_rc(im, (uint32_t)(i0 - im.src), r, c);
-          if ((int)c + 3 < im.cols) {   // the group stays in one image row
-            __nv_bfloat16* d = a.lowp + im.dst + (int64_t)r * im.ld + c;
-            d[0] = __float2bfloat16_rn(p[0]); d[1] = __float2bfloat16_rn(p[1]);
-            d[2] = __float2bfloat16_rn(p[2]); d[3] = __float2bfloat16_rn(p[3]);
-            continue;
+        if (i0 + 3 < a.P) {
+          reinterpret_cast<float4*>(a.m)[gi] = make_float4(m[0], m[1], m[2], m[3]);
+          reinterpret_cast<float4*>(a.v)[gi] = make_float4(v[0], v[1], v[2], v[3]);
+          reinterpret_cast<float4*>(a.params)[gi] = make_float4(p[0], p[1], p[2], p[3]);
+        } else {
+          for (int q = 0; q < 4 && i0 + q < a.P; ++q) {
+            a.m[i0 + q] = m[q];
+            a.v[i0 + q] = v[q];
+            a.params[i0 + q] = p[q];
           }
         }
-        for (int q = 0; q < 4 && i0 + q < a.P; ++q) lowp_write(a, i0 + q, p[q]);
+        if (a.nimg) {
+          const int k0 = find_img(bounds, a.nimg, (uint32_t)i0);
+          const int k3 = find_img(bounds, a.nimg, (uint32_t)min(i0 + 3, a.P - 1));
+          bool done = false;
+          if (k0 >= 0 && k0 == k3 && a.img[k0].kind == IMG_COPY_PAD) {
+            const LowpImg& im = a.img[k0];
+            uint32_t r, c;
+            img_rc(im, (uint32_t)(i0 - im.src), r, c);
+            if ((int)c + 3 < im.cols) {   // the group stays in one image row
+              __nv_bfloat16* d = a.lowp + im.dst + (int64_t)r * im.ld + c;
+              d[0] = __float2bfloat16_rn(p[0]); d[1] = __float2bfloat16_rn(p[1]);
+              d[2] = __float2bfloat16_rn(p[2]); d[3] = __float2bfloat16_rn(p[3]);
+              done = true;
+            }
+          }
+          if (!done)
+            for (int q = 0; q < 4 && i0 + q < a.P; ++q) lowp_write(a, i0 + q, p[q]);
+        }
       }
     }
   }
@@ -829,8 +848,9 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
 
 seed_status launch_clip_adam(const AdamArgs& a, cudaStream_t st) {
   const int64_t groups = (a.P + 3) / 4;
-  return launch_k(adam_kernel, dim3((unsigned)std::min<int64_t>((groups + 255) / 256, 148 * 4)), dim3(256),
-                  0, st, a);
+  return launch_k(adam_kernel, dim3((unsigned)std::min<int64_t>((groups + 256 * ADAM_GPT - 1) / (256 * ADAM_GPT),
+                                                                 148 * 8)),
+                  dim3(256), 0, st, a);
 }
 
 }  // namespace seed
