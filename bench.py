@@ -477,25 +477,49 @@ def run_ours(args):
     frames = world * B * T * CFG["repeat"]
     value = frames / (ms_per_step / 1e3)
 
-    # ---- e2e through the public API: pinned H2D of the batch + step + D2H of metrics
-    out_pinned = torch.empty(8, dtype=torch.float32).pin_memory()
+    # ---- e2e through the public API: every step copies its batch from pinned host
+    # memory (H2D) and reads its metrics back (D2H) inside the timed region; the
+    # batch is double-buffered on a copy stream so step i's H2D overlaps step
+    # i-1's compute (the way a learner is fed: SEED's prefetch)
     h2d = sum(v.numel() * v.element_size() for v in pinned.values())
-    d2h = out_pinned.numel() * 4
-    Ke = max(3, min(K, 20))
-    es0 = [torch.cuda.Event(enable_timing=True) for _ in range(Ke)]
-    es1 = [torch.cuda.Event(enable_timing=True) for _ in range(Ke)]
+    d2h = 8 * 4
+    torch.cuda.synchronize()
+    ha, hb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ha.record()
+    for _ in range(3):
+        for k, v in pinned.items():
+            dev[k].copy_(v, non_blocking=True)
+    hb.record()
+    torch.cuda.synchronize()
+    h2d_alone_ms = ha.elapsed_time(hb) / 3
+    Ke = max(4, min(K, 20))
+    s_comp = torch.cuda.current_stream()
+    s_copy = torch.cuda.Stream()
+    devs = [dev, {k: torch.empty_like(v) for k, v in dev.items()}]
+    outs = [torch.empty(8, dtype=torch.float32).pin_memory() for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    freed = [torch.cuda.Event() for _ in range(2)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    e0.record(s_comp)
+    s_copy.wait_event(e0)
     for i in range(Ke):
-        es0[i].record()
-        for k, v in pinned.items():
-            dev[k].copy_(v, non_blocking=True)
-        m = learner.step(dev)
-        out_pinned.copy_(m, non_blocking=True)
-        es1[i].record()
-        torch.cuda.synchronize()
-    e2e_ms = sum(a.elapsed_time(b) for a, b in zip(es0, es1)) / Ke
+        b = i % 2
+        with torch.cuda.stream(s_copy):
+            if i >= 2:
+                s_copy.wait_event(freed[b])
+            for k, v in pinned.items():
+                devs[b][k].copy_(v, non_blocking=True)
+            ready[b].record(s_copy)
+        s_comp.wait_event(ready[b])
+        m = learner.step(devs[b])
+        outs[b].copy_(m, non_blocking=True)
+        freed[b].record(s_comp)
+    e1.record(s_comp)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / Ke
     t_e2e = torch.tensor([e2e_ms], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
@@ -554,7 +578,10 @@ def run_ours(args):
         "roofline": roof,
         "vtrace": vt,
         "e2e": {"value": round(e2e_value, 1), "unit": "frames/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": "Learner.step (eager) + pinned copies"},
+                "d2h_bytes_per_step": d2h,
+                "api": "Learner.step (eager): pinned H2D of each step's batch on a copy stream, "
+                       "double-buffered (overlaps the previous step), D2H of the metrics",
+                "h2d_ms_alone": round(h2d_alone_ms, 4)},
         "clocks": clk.summary(),
         **extra,
     }
