@@ -1,0 +1,142 @@
+// conv3w.cuh — the IMPALA-deep torso (configs[2] DMLab, configs[3] GRF; C14)
+// as shifted-window GEMMs on tcgen05 (win_engine.cuh).
+//
+// Section s: conv3x3 'same' (cin -> ch) -> maxpool 3x3/s2 'same' -> 2 x residual
+// [h + conv(relu(conv(relu(h))))]; relu(h) of the last section feeds the FC.
+//
+// Layout ("padded row space"): an activation at resolution H x W is stored as
+// rows g = f*P + Y*Wp + X with Wp = W + 2, P = (H + 2)*Wp, pixel (y, x) at
+// (Y, X) = (y + 1, x + 1); border rows hold zeros, so the 'same' zero padding
+// of a 3x3 conv is read from memory.  A row is the pixel's C channels in bf16
+// (RB = 2C = 32 or 64 bytes), stored pre-swizzled (swz_chunk).  A 3x3 conv is
+// then 9 window GEMMs over the same rows at offsets (ky-1)*Wp + (kx-1)
+// (forward), their negatives with the transposed weights (data gradient), and
+// 3 groups (ky) x atoms (kx, LBO = one row) of the MN-major weight-gradient
+// engine.  Section 0 with C <= 5 input channels (DMLab RGB) uses an x-im2col
+// input instead: row channels (kx, c) (3C <= 16, zero-padded to 16), so the
+// conv is 3 windows at offsets (ky-1)*Wp and its weight gradient 1 group whose
+// atoms are the 3 ky rows (LBO = Wp rows).
+// Epilogues write zeros on border rows (the outputs are the next conv's
+// inputs); the max-pool kernels work on 16-byte chunks of 8 channels.
+#pragma once
+#include "common.cuh"
+#include "win_engine.cuh"
+
+namespace seed {
+
+typedef __nv_bfloat16 bf16;
+
+struct PadGeo {
+  int H, W, Wp, P;       // interior size, padded row width, rows per frame
+  FastDiv fP, fW;        // P, Wp
+  static PadGeo make(int H, int W) {
+    PadGeo g;
+    g.H = H; g.W = W; g.Wp = W + 2; g.P = (H + 2) * (W + 2);
+    g.fP = FastDiv((uint32_t)g.P); g.fW = FastDiv((uint32_t)g.Wp);
+    return g;
+  }
+  // frame and unpadded pixel of row m; false on border rows
+  __device__ __forceinline__ bool split(int64_t m, int& f, int& y, int& x) const {
+    uint32_t uf, r, Y, X;
+    fP.divmod((uint32_t)m, uf, r);
+    fW.divmod(r, Y, X);
+    f = (int)uf; y = (int)Y - 1; x = (int)X - 1;
+    return y >= 0 && x >= 0 && y < H && x < W;
+  }
+  __host__ __device__ int64_t row(int64_t f, int y, int x) const {
+    return f * P + (int64_t)(y + 1) * Wp + (x + 1);
+  }
+};
+
+// obs uint8 [F][H][W][C] -> section-0 input rows (exact 0..255 in bf16):
+//   xim = 0: channels c < C of 16 or 32 (Cp);  xim = 1: channel kx*C + c = pixel x+kx-1
+seed_status conv3_obs(const uint8_t* obs, int64_t F, const PadGeo& g, int C, int Cp, bool xim,
+                      uint8_t* X0, cudaStream_t st);
+
+enum { W3_PLAIN = 0, W3_RELU = 1, W3_RES = 2 };    // forward epilogues
+enum { D3W_PLAIN = 0, D3W_MASK = 1, D3W_RES = 2 };  // data-gradient epilogues
+
+// Forward 3x3 conv (9 windows, or 3 for the x-im2col section-0 input).
+//   W3_PLAIN: out = acc*in_scale + b  (section conv; border rows not written)
+//   W3_RELU:  out = relu(acc + b)
+//   W3_RES:   out = res + acc + b, outr = relu(out), dense (nullable) = relu(out) as
+//             [f][(y*W + x)*ch + c] (the FC input)
+struct Conv3wFwd {
+  int mode, cin_p, ch;    // cin_p = input row channels (16 / 32); ch = 16 / 32
+  bool xim;
+  PadGeo g;
+  int64_t rows;           // F*P
+  float in_scale;
+  const uint8_t* in;      // input rows (cin_p channels)
+  const bf16* wimg;       // window image [NW][ch][cin_p] (pre-swizzled)
+  const float* bias;
+  const uint8_t* res;
+  uint8_t* out;
+  uint8_t* outr;
+  bf16* dense;
+};
+seed_status conv3w_forward(const Conv3wFwd& a, cudaStream_t st);
+
+// Data gradient dX[g][ci] = sum_w dY[g - off_w] . Wdg_w[ci], into rows of cin channels
+//   D3W_PLAIN: dX = acc;  D3W_MASK: dX = acc*(mask > 0);  D3W_RES: dX = dres + acc*(mask > 0)
+struct Conv3wDgrad {
+  int mode, cin, ch;      // dX channels (16 / 32), dY channels
+  PadGeo g;
+  int64_t rows;
+  const uint8_t* dY;
+  const bf16* wimg;       // [9][cin][ch] (pre-swizzled)
+  const uint8_t* mask;
+  const uint8_t* dres;
+  uint8_t* dX;
+};
+seed_status conv3w_dgrad(const Conv3wDgrad& a, cudaStream_t st);
+
+// Weight + bias gradient: dW[co][ky][kx][c] = scale * sum_g X[g + off][c] dY[g][co],
+// db[co] = sum_g dY[g][co] (fixed-order split sum; part = scratch)
+struct Conv3wWgrad {
+  int cin_p, cin, ch;     // X row channels, real input channels, dY channels
+  bool xim;
+  PadGeo g;
+  int64_t rows;
+  float scale;
+  const uint8_t* X;
+  const uint8_t* dY;
+  float* part;
+  float* g_w;             // fp32 [ch][3][3][cin]
+  float* g_b;             // fp32 [ch]
+};
+seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st);
+size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool xim);
+
+// max-pool 3x3 / stride 2 / TF 'same' (top/left pad pt/pl, padding = -inf, first
+// maximum in (ky, kx) order): conv (gi rows) -> h0, hr0 = relu(h0) (go rows) and the
+// window argmax (0..8) per (go row, channel)
+seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
+                            const uint8_t* conv, uint8_t* h0, uint8_t* hr0, uint8_t* arg,
+                            cudaStream_t st);
+// gradient gather into gi rows (borders zero)
+seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
+                            const uint8_t* dout, const uint8_t* arg, uint8_t* din,
+                            cudaStream_t st);
+
+// bf16 weight-image element position of source element e of W[CO][3][3][CI]
+// (net.cuh IMG_WIN3: d0 = mode 0 forward [9][CO][RB] / 1 data gradient [9][CI][RB]
+// / 2 x-im2col forward [3][CO][RB]; d1 = CI, d2 = CO, d3 = RB bytes)
+__host__ __device__ inline int64_t win3_img_pos(int mode, int CI, int CO, int RB, int64_t e64) {
+  const int e = (int)e64;
+  const int c = e % CI;
+  int q = e / CI;
+  const int kx = q % 3; q /= 3;
+  const int ky = q % 3;
+  const int co = q / 3;
+  int row, k;
+  if (mode == 0) { row = (ky * 3 + kx) * CO + co; k = c; }
+  else if (mode == 1) { row = (ky * 3 + kx) * CI + c; k = co; }
+  else { row = ky * CO + co; k = kx * CI + c; }
+  return (int64_t)row * (RB / 2) + swz_chunk(row, RB, k / 8) * 8 + (k % 8);
+}
+inline int64_t win3_img_elems(int mode, int CI, int CO, int RB) {
+  return (int64_t)(mode == 0 ? 9 * CO : mode == 1 ? 9 * CI : 3 * CO) * (RB / 2);
+}
+
+}  // namespace seed

@@ -3,178 +3,9 @@
 // slabs.
 #include <algorithm>
 #include "conv_s2d.cuh"
+#include "win_engine.cuh"
 
 namespace seed {
-
-constexpr int WC_THREADS = 192;   // wgrad: warp 0 TMA producer, warp 1 MMA, warps 2-5 epilogue
-// forward / dgrad: warp 0 producer, warp 1 MMA, warps 2-9 = two epilogue groups
-// taking alternate tiles (4 TMEM accumulators), so two tiles drain at once
-constexpr int WCF_THREADS = 320;
-constexpr int WCF_ACC = 4;
-constexpr int WC_MAX_STAGES = 8;
-constexpr int WC_SMEM_BUDGET = 200 * 1024;
-constexpr int WG_KS = 256;        // rows per weight-gradient k-stage
-
-__device__ __forceinline__ uint4 pack8(const float* o) {
-  uint4 u;
-  u.x = pack_bf16(o[0], o[1]); u.y = pack_bf16(o[2], o[3]);
-  u.z = pack_bf16(o[4], o[5]); u.w = pack_bf16(o[6], o[7]);
-  return u;
-}
-
-// zero rows [z0, z1) of a slab (generic-proxy stores, then made visible to the
-// tensor core's async proxy)
-__device__ __forceinline__ void zero_rows(uint8_t* dst, int rb, int z0, int z1, int lane) {
-  const uint4 z = make_uint4(0, 0, 0, 0);
-  for (int i = z0 * rb / 16 + lane; i < z1 * rb / 16; i += 32) reinterpret_cast<uint4*>(dst)[i] = z;
-}
-
-// Copy global rows [R0, R0 + n) (row bytes rb, pre-swizzled) to `slab` keeping the
-// 1024-byte address phase; rows outside [0, lim) are zero.  Called by one warp;
-// lane 0 arms `bar` (expect_tx) and issues the TMA bulk copy.  Returns the
-// phase offset of row R0 inside the slab.
-__device__ __forceinline__ int load_slab(uint8_t* slab, const uint8_t* src, int rb, int64_t R0, int n,
-                                         int64_t lim, uint64_t* bar, int lane, uint32_t extra_tx) {
-  const int off0 = (int)(((R0 * rb) % 1024 + 1024) % 1024);
-  uint8_t* dst = slab + off0;
-  const int64_t lo = std::max<int64_t>(R0, 0), hi = std::min<int64_t>(R0 + n, lim);
-  const int zlo = (int)std::min<int64_t>(std::max<int64_t>(lo - R0, 0), n);
-  const int zhi = hi > lo ? (int)(hi - R0) : zlo;
-  if (zlo > 0 || zhi < n) {
-    zero_rows(dst, rb, 0, zlo, lane);
-    zero_rows(dst, rb, zhi, n, lane);
-    fence_proxy_async_smem();
-  }
-  __syncwarp();
-  if (lane == 0) {
-    const uint32_t bytes = hi > lo ? (uint32_t)((hi - lo) * rb) : 0u;
-    if (bytes + extra_tx) mbar_expect_tx(bar, bytes + extra_tx);
-    else mbar_arrive(bar);
-    if (bytes) bulk_g2s(smem_u32(dst + (lo - R0) * rb), src + lo * rb, bytes, bar);
-  }
-  return off0;
-}
-
-__device__ __forceinline__ int slab_phase(int64_t R0, int rb) {
-  return (int)(((R0 * rb) % 1024 + 1024) % 1024);
-}
-
-// ------------------------------------------------------------------ forward / dgrad
-template <class Epi, int RB>
-__global__ void __launch_bounds__(WCF_THREADS, 1)
-    win_conv_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes) {
-  constexpr int N = Epi::N;
-  constexpr uint32_t LAYOUT = swz_layout_code(RB);
-  constexpr int WB = 4 * N * RB;
-  constexpr uint32_t TCOLS = WCF_ACC * N < 32 ? 32 : WCF_ACC * N;
-  extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* Ws = sm;
-  uint8_t* slabs = sm + ((WB + 1023) & ~1023);
-  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[WCF_ACC], tempty[WCF_ACC], wbar;
-  __shared__ uint32_t tbase;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int mn = a.off[0], mx = a.off[0];
-#pragma unroll
-  for (int w = 1; w < 4; ++w) { mn = min(mn, a.off[w]); mx = max(mx, a.off[w]); }
-  const int nrows = 128 + mx - mn;
-  const int64_t tiles = (a.M + 127) / 128;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < WCF_ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
-    mbar_init(&wbar, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc(&tbase, TCOLS);
-  __syncthreads();
-  tc_fence_after();
-  pdl_wait();
-  const uint32_t tmem = tbase;
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(&wbar, WB);
-      bulk_g2s(smem_u32(Ws), a.wimg, WB, &wbar);
-    }
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      const int s = it % stages;
-      mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-      load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, t * 128 + mn, nrows, a.src_rows, &full[s],
-                lane, 0);
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      mbar_wait(&wbar, 0);
-      const uint32_t idesc = umma_idesc_bf16(128, N, false, false);
-      const uint32_t wb = smem_u32(Ws);
-      int it = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-        const int s = it % stages, acc = it % WCF_ACC;
-        mbar_wait(&full[s], (it / stages) & 1);
-        mbar_wait(&tempty[acc], ((it / WCF_ACC) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t base =
-            smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * 128 + mn, RB);
-#pragma unroll
-        for (int w = 0; w < 4; ++w)
-#pragma unroll
-          for (int ks = 0; ks < RB / 32; ++ks) {
-            const uint64_t ad = umma_desc(base + (a.off[w] - mn) * RB + ks * 32, 16, 8 * RB, LAYOUT);
-            const uint64_t bd = umma_desc(wb + w * N * RB + ks * 32, 16, 8 * RB, LAYOUT);
-            tc_mma_bf16(tmem + acc * N, ad, bd, idesc, (w | ks) != 0);
-          }
-        tc_commit(&empty[s]);
-        tc_commit(&tfull[acc]);
-      }
-    }
-  } else {
-    const int q = warp & 3;            // TMEM lanes [32q, 32q+32) of this warp
-    const int grp = (warp - 2) >> 2;   // epilogue group: tiles it with it % 2 == grp
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      if ((it & 1) != grp) continue;
-      const int acc = it % WCF_ACC;
-      mbar_wait(&tfull[acc], (it / WCF_ACC) & 1);
-      tc_fence_after();
-      float v[N];
-#pragma unroll
-      for (int c = 0; c < N / 16; ++c)
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * N + c * 16, v + 16 * c);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      const int64_t m = t * 128 + q * 32 + lane;
-      if (m < a.M) e.store(m, v);
-    }
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, TCOLS);
-  }
-}
-
-template <class Epi, int RB>
-seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st) {
-  constexpr int WB = 4 * Epi::N * RB;
-  int mn = a.off[0], mx = a.off[0];
-  for (int w = 1; w < 4; ++w) { mn = std::min(mn, a.off[w]); mx = std::max(mx, a.off[w]); }
-  const int slab = (int)align_up((size_t)(128 + mx - mn) * RB + 1024, 1024);
-  const int wbytes = (int)align_up(WB, 1024);
-  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - wbytes) / slab);
-  if (stages < 2 || a.M <= 0) return a.M == 0 ? SEED_OK : SEED_E_SHAPE;
-  const size_t smem = (size_t)wbytes + (size_t)stages * slab + 1024;
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win_conv_kernel<Epi, RB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       WC_SMEM_BUDGET + 2048));
-    attr = true;
-  }
-  const int64_t tiles = (a.M + 127) / 128;
-  const int grid = (int)std::min<int64_t>(tiles, 148);
-  return launch_k(win_conv_kernel<Epi, RB>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e, stages, slab);
-}
 
 // ------------------------------------------------------------------ epilogues
 __device__ void Conv1S2dEpi::store(int64_t m, float (&v)[N]) const {
@@ -255,185 +86,23 @@ __device__ void Conv2DgradS2dEpi::store(int64_t p, float (&v)[N]) const {
 }
 
 // ------------------------------------------------------------------ weight gradient
-// Per CTA: rows [z*R, min((z+1)*R, M)) in k-stages of 128 rows.  Accumulators
-// (TMEM): tile a (a = 0, 1) = windows (a, 0) and (a, 1) as the two 64-row MN
-// atoms of one M=128 operand (atom stride LBO = 128 bytes = one row), tile 2 =
-// all-ones operand (every row = the column sum of dY = the bias gradient).
-template <int N>
-__global__ void __launch_bounds__(WC_THREADS, 1)
-    win_wgrad_kernel(const WinWgradArgs a, int stages, int a_bytes, int b_bytes) {
-  constexpr int RBY = 2 * N;
-  constexpr uint32_t LB = swz_layout_code(RBY);
-  constexpr uint32_t TCOLS = 4 * N < 32 ? 32 : (4 * N <= 64 ? 64 : 128);
-  extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* ones = sm;                  // 1 KB of bf16 1.0
-  uint8_t* stg = sm + 1024;            // stages x (A slab | B slab)
-  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull;
-  __shared__ uint32_t tbase;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
-  const int64_t r_end = std::min<int64_t>(a.M, r_begin + a.rows_per_cta);
-  const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
-  const int arows = WG_KS + a.wsp + 1;
-  for (int i = threadIdx.x; i < 64; i += blockDim.x)
-    reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-  fence_proxy_async_smem();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(&tfull, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc(&tbase, TCOLS);
-  __syncthreads();
-  tc_fence_after();
-  pdl_wait();
-  const uint32_t tmem = tbase;
-  if (warp == 0) {
-    for (int it = 0; it < nks; ++it) {
-      const int s = it % stages;
-      mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-      const int64_t k0 = r_begin + (int64_t)it * WG_KS;
-      uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
-      // B first (its bytes are credited through the A call's expect_tx)
-      const int64_t blo = k0, bhi = std::min<int64_t>(k0 + WG_KS, r_end);
-      const int boff = slab_phase(k0, RBY);
-      uint8_t* bd = sa + a_bytes + boff;
-      if (bhi - blo < WG_KS) {
-        zero_rows(bd, RBY, (int)(bhi - blo), WG_KS, lane);
-        fence_proxy_async_smem();
-      }
-      __syncwarp();
-      const uint32_t bbytes = (uint32_t)((bhi - blo) * RBY);
-      load_slab(sa, a.src, 128, k0, arows, a.src_rows, &full[s], lane, bbytes);
-      if (lane == 0) bulk_g2s(smem_u32(bd), a.dy + blo * RBY, bbytes, &full[s]);
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = umma_idesc_bf16(128, N, true, true);
-      const uint64_t od = umma_desc(smem_u32(ones), 0, 0, 2);
-      for (int it = 0; it < nks; ++it) {
-        const int s = it % stages;
-        mbar_wait(&full[s], (it / stages) & 1);
-        tc_fence_after();
-        const int64_t k0 = r_begin + (int64_t)it * WG_KS;
-        uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
-        const uint32_t abase = smem_u32(sa) + slab_phase(k0, 128);
-        const uint32_t bbase = smem_u32(sa + a_bytes) + slab_phase(k0, RBY);
-#pragma unroll
-        for (int ks = 0; ks < WG_KS / 16; ++ks) {
-          const uint64_t bdsc = umma_desc(bbase + ks * 16 * RBY, 8 * RBY, 8 * RBY, LB);
-          const uint32_t accf = (it | ks) != 0;
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const uint64_t adsc = umma_desc(abase + (t * a.wsp + ks * 16) * 128, 128, 1024, 2);
-            tc_mma_bf16(tmem + t * N, adsc, bdsc, idesc, accf);
-          }
-          tc_mma_bf16(tmem + 2 * N, od, bdsc, idesc, accf);
-        }
-        tc_commit(&empty[s]);
-      }
-      tc_commit(&tfull);
-    }
-  } else {
-    const int q = warp & 3;
-    float* part = a.part + (size_t)blockIdx.x * 3 * 128 * N;
-    if (nks > 0) {
-      mbar_wait(&tfull, 0);
-      tc_fence_after();
-    }
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      float v[N];
-      if (nks > 0) {
-#pragma unroll
-        for (int c = 0; c < N / 16; ++c)
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + t * N + c * 16, v + 16 * c);
-      } else {
-#pragma unroll
-        for (int c = 0; c < N; ++c) v[c] = 0.f;
-      }
-      const int row = q * 32 + lane;
-      if (t < 2 || row == 0) {
-        float4* dst = reinterpret_cast<float4*>(part + ((size_t)t * 128 + row) * N);
-#pragma unroll
-        for (int c = 0; c < N / 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-      }
-    }
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, TCOLS);
-  }
+// groups a = 0, 1 (window rows a*Ws), atoms b = 0, 1 (window columns, LBO = one
+// 128-byte row): accumulator row i = b*64 + s2d channel
+__device__ void WinWgradFinish::weight(int a, int i, int n, float t) const {
+  const int b = i >> 6, ch = i & 63;
+  const int ky1 = ch / (g.s * g.C), kx1 = (ch / g.C) % g.s, c = ch % g.C;
+  const int K = 2 * g.s, ky = g.s * a + ky1, kx = g.s * b + kx1;
+  g_w[(((size_t)n * K + ky) * K + kx) * g.C + c] = t * scale;
 }
 
-// fixed-order sum of the per-CTA partials; block = 32 outputs x 8 split groups
-__global__ void __launch_bounds__(256) win_wgrad_finish(const float* __restrict__ part, int G, int N,
-                                                        const WinWgradFinish f) {
-  pdl_wait();
-  const int tot = 2 * 128 * N + N;
-  const int o = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
-  __shared__ float sh[8][33];
-  float s = 0.f;
-  size_t idx = 0;
-  if (o < tot) {
-    idx = o < 2 * 128 * N ? (size_t)o : (size_t)2 * 128 * N + (o - 2 * 128 * N);
-    for (int z = g; z < G; z += 8) s += part[(size_t)z * 3 * 128 * N + idx];
-  }
-  sh[g][threadIdx.x & 31] = s;
-  __syncthreads();
-  if (g == 0 && o < tot) {
-    float t = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x & 31];
-    if (o >= 2 * 128 * N) {
-      f.g_b[o - 2 * 128 * N] = t;
-      return;
-    }
-    const S2dGeo& g2 = f.g;
-    const int tile = o / (128 * N), i = (o / N) % 128, n = o % N;
-    const int b = i >> 6, ch = i & 63;
-    const int ky1 = ch / (g2.s * g2.C), kx1 = (ch / g2.C) % g2.s, c = ch % g2.C;
-    const int K = 2 * g2.s, ky = g2.s * tile + ky1, kx = g2.s * b + kx1;
-    f.g_w[(((size_t)n * K + ky) * K + kx) * g2.C + c] = t * f.scale;
-  }
-}
+size_t win_wgrad_part_bytes(int64_t M, int N) { return win_wgrad_part_bytes_g(M, N, 2); }
 
-static int wgrad_grid(int64_t M, int64_t* rows_per_cta) {
-  const int64_t kst = (M + WG_KS - 1) / WG_KS;
-  const int64_t G0 = std::min<int64_t>(148, std::max<int64_t>(kst, 1));
-  const int64_t per = (kst + G0 - 1) / G0;
-  *rows_per_cta = per * WG_KS;
-  return (int)std::max<int64_t>(1, (M + per * WG_KS - 1) / (per * WG_KS));
-}
-
-size_t win_wgrad_part_bytes(int64_t M, int N) {
-  int64_t r;
-  return (size_t)wgrad_grid(M, &r) * 3 * 128 * N * 4;
-}
-
-template <int N>
-seed_status launch_win_wgrad(const WinWgradArgs& a0, const WinWgradFinish& fin, cudaStream_t st) {
-  WinWgradArgs a = a0;
-  const int G = wgrad_grid(a.M, &a.rows_per_cta);
-  const int a_bytes = (int)align_up((size_t)(WG_KS + a.wsp + 1) * 128 + 1024, 1024);
-  const int b_bytes = (int)align_up((size_t)WG_KS * 2 * N + 1024, 1024);
-  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes));
-  if (stages < 2) return SEED_E_SHAPE;
-  const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win_wgrad_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       WC_SMEM_BUDGET + 2048));
-    attr = true;
-  }
-  SEED_TRY(launch_k(win_wgrad_kernel<N>, dim3(G), dim3(WC_THREADS), smem, st, a, stages, a_bytes,
-                    b_bytes));
-  const int tot = 2 * 128 * N + N;
-  return launch_k(win_wgrad_finish, dim3(ceil_div(tot, 32)), dim3(256), 0, st, (const float*)a.part, G,
-                  N, fin);
+static WinWgradArgs s2d_wgrad_args(const uint8_t* src, int64_t rows, const uint8_t* dy, int wsp,
+                                   float* part) {
+  WinWgradArgs a{};
+  a.src = src; a.src_rows = rows; a.dy = dy; a.M = rows; a.part = part;
+  a.ngroup = 2; a.goff[0] = 0; a.goff[1] = wsp; a.astride = 1;
+  return a;
 }
 
 // ------------------------------------------------------------------ obs -> S0
@@ -503,7 +172,7 @@ seed_status shallow_s2d_conv1(const ShallowS2d& sg, int64_t F, const uint8_t* S0
   Conv1S2dEpi e{};
   e.bias = b1; e.S1 = S1; e.P1 = FastDiv(g.P); e.W1 = FastDiv(g.Ws);
   e.Ho = g.Ho; e.Wo = g.Wo; e.W2s = sg.g2.Ws; e.P2 = sg.g2.P;
-  return launch_win_conv<Conv1S2dEpi, 128>(a, e, st);
+  return launch_win_conv<Conv1S2dEpi, 128, 4>(a, e, st);
 }
 
 seed_status shallow_s2d_conv2(const ShallowS2d& sg, int64_t F, const uint8_t* S1, const bf16* w2img,
@@ -516,7 +185,7 @@ seed_status shallow_s2d_conv2(const ShallowS2d& sg, int64_t F, const uint8_t* S1
   Conv2S2dEpi e{};
   e.bias = b2; e.act2 = act2; e.dY2z = dY2z; e.P2 = FastDiv(g.P); e.W2 = FastDiv(g.Ws);
   e.Ho = g.Ho; e.Wo = g.Wo; e.fc_in = sg.fc_in;
-  return launch_win_conv<Conv2S2dEpi, 128>(a, e, st);
+  return launch_win_conv<Conv2S2dEpi, 128, 4>(a, e, st);
 }
 
 seed_status shallow_s2d_forward(const ShallowS2d& sg, int64_t F, const uint8_t* obs,
@@ -531,11 +200,10 @@ seed_status shallow_s2d_forward(const ShallowS2d& sg, int64_t F, const uint8_t* 
 seed_status shallow_s2d_conv2_wgrad(const ShallowS2d& sg, int64_t F, const uint8_t* S1,
                                     const uint8_t* dY2, float* part, float* g_w2, float* g_b2,
                                     cudaStream_t st) {
-  WinWgradArgs a{};
-  a.src = S1; a.src_rows = sg.rows2(F); a.dy = dY2; a.M = sg.rows2(F); a.wsp = sg.g2.Ws; a.part = part;
+  const WinWgradArgs a = s2d_wgrad_args(S1, sg.rows2(F), dY2, sg.g2.Ws, part);
   WinWgradFinish f{};
   f.g = sg.g2; f.scale = 1.f; f.g_w = g_w2; f.g_b = g_b2;
-  return launch_win_wgrad<32>(a, f, st);
+  return launch_win_wgrad<32, 128>(a, f, st);
 }
 
 seed_status shallow_s2d_conv2_dgrad(const ShallowS2d& sg, int64_t F, const uint8_t* dY2,
@@ -549,17 +217,16 @@ seed_status shallow_s2d_conv2_dgrad(const ShallowS2d& sg, int64_t F, const uint8
   Conv2DgradS2dEpi e{};
   e.S1 = S1; e.dY1 = dY1; e.P2 = FastDiv(g.P); e.W2 = FastDiv(g.Ws); e.H2s = g.Hs; e.W2s = g.Ws;
   e.P1 = sg.g1.P; e.W1s = sg.g1.Ws; e.H1s = sg.g1.Hs;
-  return launch_win_conv<Conv2DgradS2dEpi, 64>(a, e, st);
+  return launch_win_conv<Conv2DgradS2dEpi, 64, 4>(a, e, st);
 }
 
 seed_status shallow_s2d_conv1_wgrad(const ShallowS2d& sg, int64_t F, const uint8_t* S0,
                                     const uint8_t* dY1, float* part, float* g_w1, float* g_b1,
                                     cudaStream_t st) {
-  WinWgradArgs a{};
-  a.src = S0; a.src_rows = sg.rows1(F); a.dy = dY1; a.M = sg.rows1(F); a.wsp = sg.g1.Ws; a.part = part;
+  const WinWgradArgs a = s2d_wgrad_args(S0, sg.rows1(F), dY1, sg.g1.Ws, part);
   WinWgradFinish f{};
   f.g = sg.g1; f.scale = 1.f / 255.f; f.g_w = g_w1; f.g_b = g_b1;
-  return launch_win_wgrad<16>(a, f, st);
+  return launch_win_wgrad<16, 128>(a, f, st);
 }
 
 }  // namespace seed

@@ -23,6 +23,7 @@
 // from an all-ones operand) + win_wgrad_finish (fixed-order split sum).
 #pragma once
 #include "common.cuh"
+#include "win_engine.cuh"
 
 namespace seed {
 
@@ -33,15 +34,6 @@ struct S2dGeo {
   int s, C, CO;        // stride, input channels, output channels (s*s*C == 64)
   int Hs, Ws, P;       // s2d image (rows per frame P = Hs*Ws)
   int Ho, Wo;          // valid outputs (Hs-1, Ws-1)
-};
-
-// ---- forward / data-gradient engine
-struct WinConvArgs {
-  const uint8_t* src;    // pre-swizzled rows of RB bytes (1024-aligned base)
-  int64_t src_rows;      // rows that exist (others read as zero)
-  int64_t M;             // output rows
-  int off[4];            // window row offsets (4 windows)
-  const uint8_t* wimg;   // pre-swizzled weight image [4][N][RB] (1024-aligned)
 };
 
 // conv1 epilogue: relu(acc/255 + b) of the valid rows -> S1 (conv2's s2d input)
@@ -77,27 +69,14 @@ struct Conv2DgradS2dEpi {
   __device__ void store(int64_t m, float (&v)[N]) const;
 };
 
-template <class Epi, int RB>
-seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st);
-
-// ---- weight-gradient engine
-struct WinWgradArgs {
-  const uint8_t* src;    // A: pre-swizzled 128-byte rows (64 s2d channels)
-  int64_t src_rows;
-  const uint8_t* dy;     // B: pre-swizzled rows of rby = 2*N bytes
-  int64_t M;             // rows summed over
-  int wsp;               // window pair a starts at row offset a*wsp (b: +1 row)
-  int64_t rows_per_cta;  // multiple of the k-stage (conv_s2d.cu WG_KS)
-  float* part;           // [grid][3][128][N]
-};
 struct WinWgradFinish {
   S2dGeo g;
   float scale;           // weight-gradient scale (1/255 for conv1)
   float* g_w;            // fp32 [CO][2s][2s][C]
   float* g_b;            // fp32 [CO]
+  __device__ void weight(int grp, int i, int n, float v) const;
+  __device__ void bias(int n, float v) const { g_b[n] = v; }
 };
-template <int N>
-seed_status launch_win_wgrad(const WinWgradArgs& a, const WinWgradFinish& fin, cudaStream_t st);
 size_t win_wgrad_part_bytes(int64_t M, int N);
 
 // uint8 obs [F][H][W][4] -> S0 pre-swizzled bf16 rows [F*Hs*Ws][64] (exact 0..255)

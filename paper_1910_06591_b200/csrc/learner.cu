@@ -24,9 +24,9 @@
 #include "learner_kernels.cuh"
 #include "lstm.cuh"
 #include "net.cuh"
-#include "deep_net.cuh"
 #include "shallow_net.cuh"
 #include "conv_s2d.cuh"
+#include "conv3w.cuh"
 
 namespace seed {
 
@@ -241,6 +241,13 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
     if (p.nsec == 0) {   // Atari-shallow: conv2 output space rows (conv_s2d.cuh)
       const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
       pr.dY2s = c.at<uint8_t>(w.dY2); pr.Wo = sg.g2.Wo; pr.W2s = sg.g2.Ws; pr.P2 = sg.g2.P;
+      pr.g0 = 0;
+    } else {             // IMPALA-deep: the last section's padded rows (conv3w.cuh)
+      const DeepSec& d = p.sec[p.nsec - 1];
+      const PadGeo g = PadGeo::make(d.H2, d.W2);
+      pr.dY2s = c.at<uint8_t>(w.dY2); pr.Wo = d.W2; pr.W2s = g.Wp; pr.P2 = g.P; pr.g0 = g.Wp + 1;
+      // border rows are the next convs' zero padding; the GEMM writes interior rows only
+      SEED_CUDA_TRY(cudaMemsetAsync(pr.dY2s, 0, (size_t)w.F * g.P * 64, st));
     }
     SEED_TRY(gemm<128>(c, pr, st, "fc_dgrad"));
   }
@@ -273,131 +280,112 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
 }
 
 // ------------------------------------------------------------------ IMPALA-deep torso
-static Conv3Geo c3geo(int H, int W, int cin, int cout) {
-  return Conv3Geo{H, W, cin, cout, FastDiv((uint32_t)(H * W)), FastDiv((uint32_t)W)};
-}
-static int ilog2(int v) {
-  int l = 0;
-  while ((1 << l) < v) ++l;
-  return l;
-}
-template <int MODE>
-static seed_status conv3_fwd(const StepCtx& c, int BN, int M, Conv3Geo g, const bf16* in,
-                             const bf16* w, const float* bias, const bf16* res, bf16* out,
-                             bf16* outr, float scale, cudaStream_t st, const char* name) {
-  Conv3Fwd<MODE> pr{};
-  pr.M = M; pr.N = g.cout; pr.K = 9 * g.cin; pr.g = g; pr.cshift = ilog2(g.cin);
-  pr.in_scale = scale; pr.in = in; pr.w = w; pr.bias = bias; pr.res = res; pr.out = out;
-  pr.outr = outr;
-  return BN == 16 ? gemm<16>(c, pr, st, name) : gemm<32>(c, pr, st, name);
-}
-template <int MODE>
-static seed_status conv3_dgrad(const StepCtx& c, int M, Conv3Geo g, const bf16* dY,
-                               const bf16* wdg, const bf16* mask, const bf16* dres, bf16* dX,
-                               cudaStream_t st, const char* name) {
-  // g.cin = dY channels (this layer's cout), g.cout = dX channels (this layer's cin)
-  Conv3Dgrad<MODE> pr{};
-  pr.M = M; pr.N = g.cout; pr.K = 9 * g.cin; pr.g = g; pr.cshift = ilog2(g.cin);
-  pr.dY = dY; pr.wdg = wdg; pr.mask = mask; pr.dres = dres; pr.dX = dX;
-  return g.cout == 16 ? gemm<16>(c, pr, st, name) : gemm<32>(c, pr, st, name);
-}
-static seed_status conv3_wgrad(const StepCtx& c, int rows, Conv3Geo g, int creal, float scale,
-                               const bf16* X, const bf16* dY, float* gw, cudaStream_t st,
-                               const char* name) {
-  Conv3Wgrad pr{};
-  pr.M = 9 * g.cin; pr.N = g.cout; pr.K = rows; pr.g = g; pr.cshift = ilog2(g.cin);
-  pr.creal = creal; pr.scale = scale; pr.X = X; pr.dY = dY; pr.g_w = gw;
-  return g.cout == 16 ? gemm<16>(c, pr, st, name) : gemm<32>(c, pr, st, name);
-}
-
+// conv3w.cuh: every activation in its padded row space (zero borders), 3x3
+// convs as shifted-window tcgen05 GEMMs, bias gradients from the weight-gradient
+// engine's all-ones operand.
 static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                 const float* params, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
-  const int F = w.F;
+  const int64_t F = w.F;
   {
     const DeepSec& d = p.sec[0];
-    const int64_t npix = (int64_t)F * d.H * d.W;
-    obs_to_bf16_pad_kernel<<<(int)std::min<int64_t>((npix * d.cinp + 255) / 256, 148 * 16), 256, 0,
-                             st>>>(npix, p.C, d.cinp, (const uint8_t*)bt->obs,
-                                   c.at<bf16>(w.obs_bf16));
+    SEED_TRY(conv3_obs((const uint8_t*)bt->obs, F, PadGeo::make(d.H, d.W), p.C, d.cinp, d.xim,
+                       c.at<uint8_t>(w.obs_bf16), st));
     c.mark("obs_bf16");
   }
   for (int s = 0; s < p.nsec; ++s) {
     const DeepSec& d = p.sec[s];
     const LearnerWs::Sec& b = w.sec[s];
-    const bf16* in = s == 0 ? c.at<bf16>(w.obs_bf16) : c.at<bf16>(w.sec[s - 1].h[2]);
-    SEED_TRY(conv3_fwd<C3_PLAIN>(c, d.ch, F * d.H * d.W, c3geo(d.H, d.W, d.cinp, d.ch), in,
-                                 lowp + d.im_w, params + p.t[d.t_b].off, nullptr,
-                                 c.at<bf16>(b.conv), nullptr, s == 0 ? 1.f / 255.f : 1.f, st,
-                                 "deep_conv_fwd"));
-    const int64_t np = (int64_t)F * d.H2 * d.W2 * d.ch;
-    maxpool_fwd_kernel<<<(int)std::min<int64_t>((np + 255) / 256, 148 * 16), 256, 0, st>>>(
-        np, d.H, d.W, d.H2, d.W2, d.ch, d.pt, d.pl, c.at<bf16>(b.conv), c.at<bf16>(b.h[0]),
-        c.at<bf16>(b.hr[0]), c.at<uint8_t>(b.arg));
+    const PadGeo gi = PadGeo::make(d.H, d.W), go = PadGeo::make(d.H2, d.W2);
+    Conv3wFwd a{};
+    a.mode = W3_PLAIN; a.cin_p = d.cinp; a.ch = d.ch; a.xim = d.xim; a.g = gi; a.rows = F * gi.P;
+    a.in_scale = s == 0 ? 1.f / 255.f : 1.f;
+    a.in = s == 0 ? c.at<uint8_t>(w.obs_bf16) : c.at<uint8_t>(w.sec[s - 1].h[2]);
+    a.wimg = lowp + d.im_w; a.bias = params + p.t[d.t_b].off; a.out = c.at<uint8_t>(b.conv);
+    SEED_TRY(conv3w_forward(a, st));
+    c.mark("deep_conv_fwd");
+    SEED_TRY(conv3w_pool_fwd(F, gi, go, d.ch, d.pt, d.pl, c.at<uint8_t>(b.conv),
+                             c.at<uint8_t>(b.h[0]), c.at<uint8_t>(b.hr[0]), c.at<uint8_t>(b.arg),
+                             st));
     c.mark("deep_pool_fwd");
-    const Conv3Geo gr = c3geo(d.H2, d.W2, d.ch, d.ch);
-    const int Mr = F * d.H2 * d.W2;
     for (int r = 0; r < 2; ++r) {
-      SEED_TRY(conv3_fwd<C3_RELU>(c, d.ch, Mr, gr, c.at<bf16>(b.hr[r]), lowp + d.im_rw[r][0],
-                                  params + p.t[d.t_rb[r][0]].off, nullptr, c.at<bf16>(b.u1[r]),
-                                  nullptr, 1.f, st, "deep_res_fwd0"));
-      SEED_TRY(conv3_fwd<C3_RES>(c, d.ch, Mr, gr, c.at<bf16>(b.u1[r]), lowp + d.im_rw[r][1],
-                                 params + p.t[d.t_rb[r][1]].off, c.at<bf16>(b.h[r]),
-                                 c.at<bf16>(b.h[r + 1]), c.at<bf16>(b.hr[r + 1]), 1.f, st,
-                                 "deep_res_fwd1"));
+      Conv3wFwd a0{};
+      a0.mode = W3_RELU; a0.cin_p = d.ch; a0.ch = d.ch; a0.g = go; a0.rows = F * go.P;
+      a0.in_scale = 1.f; a0.in = c.at<uint8_t>(b.hr[r]); a0.wimg = lowp + d.im_rw[r][0];
+      a0.bias = params + p.t[d.t_rb[r][0]].off; a0.out = c.at<uint8_t>(b.u1[r]);
+      SEED_TRY(conv3w_forward(a0, st));
+      c.mark("deep_res_fwd0");
+      Conv3wFwd a1 = a0;
+      a1.mode = W3_RES; a1.in = c.at<uint8_t>(b.u1[r]); a1.wimg = lowp + d.im_rw[r][1];
+      a1.bias = params + p.t[d.t_rb[r][1]].off; a1.res = c.at<uint8_t>(b.h[r]);
+      a1.out = c.at<uint8_t>(b.h[r + 1]); a1.outr = c.at<uint8_t>(b.hr[r + 1]);
+      a1.dense = (s == p.nsec - 1 && r == 1) ? c.at<bf16>(w.act2) : nullptr;
+      SEED_TRY(conv3w_forward(a1, st));
+      c.mark("deep_res_fwd1");
     }
   }
-  return last_launch();
+  return SEED_OK;
 }
 
 static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                  const float* params, float* grads, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
-  const int F = w.F;
-  float* cpart = c.at<float>(w.colsum_part);
+  const int64_t F = w.F;
+  float* part = c.at<float>(w.splitk);
   for (int s = p.nsec - 1; s >= 0; --s) {
     const DeepSec& d = p.sec[s];
     const LearnerWs::Sec& b = w.sec[s];
-    const Conv3Geo gr = c3geo(d.H2, d.W2, d.ch, d.ch);
-    const int Mr = F * d.H2 * d.W2;
+    const PadGeo gi = PadGeo::make(d.H, d.W), go = PadGeo::make(d.H2, d.W2);
+    const int64_t Mr = F * go.P;
     size_t cur = b.dhA, oth = b.dhB;   // dh of h[2] arrives in dhA
     for (int r = 1; r >= 0; --r) {
       // t1 = conv1(u1): dt1 = dh
-      SEED_TRY(conv3_wgrad(c, Mr, gr, d.ch, 1.f, c.at<bf16>(b.u1[r]), c.at<bf16>(cur),
-                           grads + p.t[d.t_rw[r][1]].off, st, "deep_res_wgrad1"));
-      SEED_TRY(colsum_bf16(c.at<bf16>(cur), Mr, d.ch, cpart, grads + p.t[d.t_rb[r][1]].off, st));
-      c.mark("deep_bias");
-      SEED_TRY(conv3_dgrad<D3_MASK>(c, Mr, gr, c.at<bf16>(cur), lowp + d.im_rdg[r][1],
-                                    c.at<bf16>(b.u1[r]), nullptr, c.at<bf16>(b.dt0), st,
-                                    "deep_res_dgrad1"));
-      // t0 = conv0(u0 = relu(h[r])): dh[r] = dh + dconv0 * (h[r] > 0)
-      SEED_TRY(conv3_wgrad(c, Mr, gr, d.ch, 1.f, c.at<bf16>(b.hr[r]), c.at<bf16>(b.dt0),
-                           grads + p.t[d.t_rw[r][0]].off, st, "deep_res_wgrad0"));
-      SEED_TRY(colsum_bf16(c.at<bf16>(b.dt0), Mr, d.ch, cpart, grads + p.t[d.t_rb[r][0]].off, st));
-      c.mark("deep_bias");
-      SEED_TRY(conv3_dgrad<D3_RES>(c, Mr, gr, c.at<bf16>(b.dt0), lowp + d.im_rdg[r][0],
-                                   c.at<bf16>(b.hr[r]), c.at<bf16>(cur), c.at<bf16>(oth), st,
-                                   "deep_res_dgrad0"));
+      Conv3wWgrad wg{};
+      wg.cin_p = d.ch; wg.cin = d.ch; wg.ch = d.ch; wg.g = go; wg.rows = Mr; wg.scale = 1.f;
+      wg.X = c.at<uint8_t>(b.u1[r]); wg.dY = c.at<uint8_t>(cur); wg.part = part;
+      wg.g_w = grads + p.t[d.t_rw[r][1]].off; wg.g_b = grads + p.t[d.t_rb[r][1]].off;
+      SEED_TRY(conv3w_wgrad(wg, st));
+      c.mark("deep_res_wgrad1", 2);
+      Conv3wDgrad dg{};
+      dg.mode = D3W_MASK; dg.cin = d.ch; dg.ch = d.ch; dg.g = go; dg.rows = Mr;
+      dg.dY = c.at<uint8_t>(cur); dg.wimg = lowp + d.im_rdg[r][1]; dg.mask = c.at<uint8_t>(b.u1[r]);
+      dg.dX = c.at<uint8_t>(b.dt0);
+      SEED_TRY(conv3w_dgrad(dg, st));
+      c.mark("deep_res_dgrad1");
+      // t0 = conv0(relu(h[r])): dh[r] = dh + dconv0 * (h[r] > 0)
+      wg.X = c.at<uint8_t>(b.hr[r]); wg.dY = c.at<uint8_t>(b.dt0);
+      wg.g_w = grads + p.t[d.t_rw[r][0]].off; wg.g_b = grads + p.t[d.t_rb[r][0]].off;
+      SEED_TRY(conv3w_wgrad(wg, st));
+      c.mark("deep_res_wgrad0", 2);
+      Conv3wDgrad d0 = dg;
+      d0.mode = D3W_RES; d0.dY = c.at<uint8_t>(b.dt0); d0.wimg = lowp + d.im_rdg[r][0];
+      d0.mask = c.at<uint8_t>(b.hr[r]); d0.dres = c.at<uint8_t>(cur); d0.dX = c.at<uint8_t>(oth);
+      SEED_TRY(conv3w_dgrad(d0, st));
+      c.mark("deep_res_dgrad0");
       std::swap(cur, oth);
     }
     // max-pool backward into dconv, then the section conv
-    const int64_t nc = (int64_t)F * d.H * d.W * d.ch;
-    maxpool_bwd_kernel<<<(int)std::min<int64_t>((nc + 255) / 256, 148 * 16), 256, 0, st>>>(
-        nc, d.H, d.W, d.H2, d.W2, d.ch, d.pt, d.pl, c.at<bf16>(cur), c.at<uint8_t>(b.arg),
-        c.at<bf16>(b.dconv));
+    SEED_TRY(conv3w_pool_bwd(F, gi, go, d.ch, d.pt, d.pl, c.at<uint8_t>(cur), c.at<uint8_t>(b.arg),
+                             c.at<uint8_t>(b.dconv), st));
     c.mark("deep_pool_bwd");
-    const bf16* in = s == 0 ? c.at<bf16>(w.obs_bf16) : c.at<bf16>(w.sec[s - 1].h[2]);
-    const int Mc = F * d.H * d.W;
-    SEED_TRY(conv3_wgrad(c, Mc, c3geo(d.H, d.W, d.cinp, d.ch), d.cin, s == 0 ? 1.f / 255.f : 1.f,
-                         in, c.at<bf16>(b.dconv), grads + p.t[d.t_w].off, st, "deep_conv_wgrad"));
-    SEED_TRY(colsum_bf16(c.at<bf16>(b.dconv), Mc, d.ch, cpart, grads + p.t[d.t_b].off, st));
-    c.mark("deep_bias");
-    if (s > 0)
-      SEED_TRY(conv3_dgrad<D3_PLAIN>(c, Mc, c3geo(d.H, d.W, d.ch, d.cin), c.at<bf16>(b.dconv),
-                                     lowp + d.im_dg, nullptr, nullptr,
-                                     c.at<bf16>(w.sec[s - 1].dhA), st, "deep_conv_dgrad"));
+    Conv3wWgrad wg{};
+    wg.cin_p = d.cinp; wg.cin = d.cin; wg.ch = d.ch; wg.xim = d.xim; wg.g = gi; wg.rows = F * gi.P;
+    wg.scale = s == 0 ? 1.f / 255.f : 1.f;
+    wg.X = s == 0 ? c.at<uint8_t>(w.obs_bf16) : c.at<uint8_t>(w.sec[s - 1].h[2]);
+    wg.dY = c.at<uint8_t>(b.dconv); wg.part = part;
+    wg.g_w = grads + p.t[d.t_w].off; wg.g_b = grads + p.t[d.t_b].off;
+    SEED_TRY(conv3w_wgrad(wg, st));
+    c.mark("deep_conv_wgrad", 2);
+    if (s > 0) {
+      Conv3wDgrad dg{};
+      dg.mode = D3W_PLAIN; dg.cin = d.cin; dg.ch = d.ch; dg.g = gi; dg.rows = F * gi.P;
+      dg.dY = c.at<uint8_t>(b.dconv); dg.wimg = lowp + d.im_dg;
+      dg.dX = c.at<uint8_t>(w.sec[s - 1].dhA);
+      SEED_TRY(conv3w_dgrad(dg, st));
+      c.mark("deep_conv_dgrad");
+    }
   }
   return SEED_OK;
 }
@@ -649,7 +637,7 @@ extern "C" seed_status seed_learner_debug_buffer(const seed_net_spec* spec, int 
       {"dH", mlp ? 0 : w.dH, F * U * 4}, {"dG", mlp ? 0 : w.dG, F * 4 * U * 2},
       {"dfc", mlp ? 0 : w.dfc, F * 256 * 2}, {"dY2", mlp ? 0 : w.dY2, F * p.fc_in * 2},
       {"dY1", mlp ? 0 : w.dY1, F * p.oh1 * p.ow1 * 16 * 2},
-      {"obs_bf16", w.obs_bf16, 16},
+      {"obs_bf16", w.obs_bf16, p.nsec > 0 ? F * (p.sec[0].H + 2) * (p.sec[0].W + 2) * p.sec[0].cinp * 2 : 16},
       {"h1", mlp ? w.h1 : 0, F * 64 * 4}, {"h2", mlp ? w.h2 : 0, F * 64 * 4},
       {"dh1", mlp ? w.dh1 : 0, F * 64 * 4}, {"dh2", mlp ? w.dh2 : 0, F * 64 * 4}};
   for (const Ent& e : ents)
@@ -663,7 +651,8 @@ extern "C" seed_status seed_learner_debug_buffer(const seed_net_spec* spec, int 
     const int k = name[1] - '0';
     const DeepSec& d = p.sec[k];
     const LearnerWs::Sec& b = w.sec[k];
-    const size_t sc = F * d.H * d.W * d.ch * 2, sp = F * d.H2 * d.W2 * d.ch * 2;
+    // conv3w.cuh padded, pre-swizzled row spaces
+    const size_t sc = F * (d.H + 2) * (d.W + 2) * d.ch * 2, sp = F * (d.H2 + 2) * (d.W2 + 2) * d.ch * 2;
     const char* bn = name + 3;
     struct E2 { const char* n; size_t off, bytes; };
     const E2 e2[] = {{"conv", b.conv, sc}, {"arg", b.arg, sp / 2}, {"h0", b.h[0], sp},

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include "learner_kernels.cuh"
 #include "net.cuh"
+#include "conv3w.cuh"
 
 namespace seed {
 
@@ -726,6 +727,8 @@ __device__ __forceinline__ void lowp_write(const AdamArgs& a, int64_t i, float v
     int64_t dst;
     if (m.kind == IMG_S2D) {
       dst = s2d_img_pos(m, e);
+    } else if (m.kind == IMG_WIN3) {
+      dst = win3_img_pos(m.d0, m.d1, m.d2, m.d3, e);
     } else if (m.kind == IMG_COPY_PAD) {
       uint32_t r, c;
       img_rc(m, (uint32_t)e, r, c);

@@ -5,6 +5,7 @@
 #include "gemm_tc.cuh"
 #include "net.cuh"
 #include "conv_s2d.cuh"
+#include "conv3w.cuh"
 
 namespace seed {
 
@@ -65,7 +66,8 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
       const int ch = chs[sct];
       DeepSec& d = p->sec[sct];
       d.H = h; d.W = w; d.cin = cin; d.ch = ch;
-      d.cinp = cin <= 8 ? 8 : (cin <= 16 ? 16 : (cin <= 32 ? 32 : 64));
+      d.xim = sct == 0 && 3 * cin <= 16;
+      d.cinp = d.xim || cin <= 16 ? 16 : (cin <= 32 ? 32 : 64);
       d.H2 = same_out(h); d.W2 = same_out(w);
       const int ph = std::max((d.H2 - 1) * 2 + 3 - h, 0), pw = std::max((d.W2 - 1) * 2 + 3 - w, 0);
       d.pt = ph / 2; d.pl = pw / 2;
@@ -106,12 +108,6 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
     off = (int64_t)align_up((size_t)off, 64);
     return start;
   };
-  auto dgrad_img = [&](int ti, int co, int k, int ci) {   // [ci][k][k][co]
-    const int64_t at = img(IMG_CONV_DGRAD, ti, ci, k * k * co, k * k * co);
-    LowpImg& m = p->img[p->nimg - 1];
-    m.d0 = co; m.d1 = k; m.d2 = k; m.d3 = ci;
-    return at;
-  };
   if (s->kind == SEED_NET_ATARI_SHALLOW) {
     // space-to-depth window images (conv_s2d.cuh); 1024-byte aligned starts
     auto s2d_img = [&](int ti, int st, int C, int CO, int mode) {
@@ -125,20 +121,27 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
     p->im_conv2 = s2d_img(p->i_conv2w, 2, 16, 32, 0);
     p->im_conv2dg = s2d_img(p->i_conv2w, 2, 16, 32, 1);
   } else {
+    // 3x3 window images (conv3w.cuh), 1024-byte aligned starts
+    auto win3_img = [&](int ti, int mode, int CI, int CO, int RB) {
+      off = (int64_t)align_up((size_t)off, 512);
+      LowpImg& m = p->img[p->nimg++];
+      m.kind = IMG_WIN3; m.src = p->t[ti].off; m.dst = off;
+      m.rows = CO; m.cols = 9 * CI; m.ld = 9 * CI;
+      const FastDiv fd((uint32_t)m.cols);
+      m.cmul = fd.mul; m.cshr = fd.shr;
+      m.d0 = mode; m.d1 = CI; m.d2 = CO; m.d3 = RB;
+      const int64_t start = off;
+      off = (int64_t)align_up((size_t)(off + win3_img_elems(mode, CI, CO, RB)), 64);
+      return start;
+    };
     for (int sct = 0; sct < p->nsec; ++sct) {
       DeepSec& d = p->sec[sct];
-      if (d.cin == d.cinp) {
-        d.im_w = img(IMG_COPY_PAD, d.t_w, d.ch, 9 * d.cin, 9 * d.cin);
-      } else {
-        d.im_w = img(IMG_CHAN_PAD, d.t_w, d.ch, 9 * d.cin, 9 * d.cinp);
-        LowpImg& m = p->img[p->nimg - 1];
-        m.d1 = 9; m.d2 = d.cinp; m.d3 = d.cin;
-      }
-      d.im_dg = sct > 0 ? dgrad_img(d.t_w, d.ch, 3, d.cin) : -1;
+      d.im_w = win3_img(d.t_w, d.xim ? 2 : 0, d.cin, d.ch, d.xim ? 32 : 2 * d.cinp);
+      d.im_dg = sct > 0 ? win3_img(d.t_w, 1, d.cin, d.ch, 2 * d.ch) : -1;
       for (int r = 0; r < 2; ++r)
         for (int j = 0; j < 2; ++j) {
-          d.im_rw[r][j] = img(IMG_COPY_PAD, d.t_rw[r][j], d.ch, 9 * d.ch, 9 * d.ch);
-          d.im_rdg[r][j] = dgrad_img(d.t_rw[r][j], d.ch, 3, d.ch);
+          d.im_rw[r][j] = win3_img(d.t_rw[r][j], 0, d.ch, d.ch, 2 * d.ch);
+          d.im_rdg[r][j] = win3_img(d.t_rw[r][j], 1, d.ch, d.ch, 2 * d.ch);
         }
     }
   }
@@ -152,8 +155,8 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
 bool learner_supported(const NetPlan& p) {
   if (p.kind == SEED_NET_MLP) return true;
   if (p.kind == SEED_NET_ATARI_SHALLOW) return shallow_s2d_supported(p.H, p.W, p.C);
-  if (p.kind == SEED_NET_IMPALA_DEEP || p.kind == SEED_NET_GFOOTBALL)
-    return p.C <= 32 && p.fc_in % 8 == 0;
+  if (p.kind == SEED_NET_IMPALA_DEEP || p.kind == SEED_NET_GFOOTBALL)   // conv3w.cuh
+    return p.C >= 1 && p.C <= 32 && p.sec[p.nsec - 1].ch == 32 && p.fc_in % 8 == 0;
   return false;
 }
 
@@ -205,11 +208,11 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   w->dH = bump(cur, F * U * 4);
   if (p.nsec > 0) {
     const DeepSec& d0 = p.sec[0];
-    w->obs_bf16 = bump(cur, F * d0.H * d0.W * d0.cinp * 2);
+    w->obs_bf16 = bump(cur, F * (d0.H + 2) * (d0.W + 2) * d0.cinp * 2);
     for (int sct = 0; sct < p.nsec; ++sct) {
       const DeepSec& d = p.sec[sct];
       LearnerWs::Sec& b = w->sec[sct];
-      const size_t sc = F * d.H * d.W * d.ch, sp = F * d.H2 * d.W2 * d.ch;
+      const size_t sc = F * (d.H + 2) * (d.W + 2) * d.ch, sp = F * (d.H2 + 2) * (d.W2 + 2) * d.ch;
       b.conv = bump(cur, sc * 2);
       b.arg = bump(cur, sp);
       for (int k = 0; k < 3; ++k) {
@@ -223,9 +226,9 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
       b.dhB = bump(cur, sp * 2);
       b.dt0 = bump(cur, sp * 2);
     }
-    // the FC layer reads relu(h) of the last section and writes its data gradient
-    // into that section's dh buffer
-    w->act2 = w->sec[p.nsec - 1].hr[2];
+    // the FC layer reads dense relu(h) of the last section (written by its last
+    // residual epilogue) and writes its data gradient into that section's dhA
+    w->act2 = bump(cur, F * p.fc_in * 2);
     w->dY2 = w->sec[p.nsec - 1].dhA;
   } else {
     const ShallowS2d sg = shallow_s2d_geometry(p.H, p.W, p.C);
@@ -261,10 +264,10 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
     sk = std::max(sk, win_wgrad_part_bytes(sg.rows1(F), 16));
     sk = std::max(sk, win_wgrad_part_bytes(sg.rows2(F), 32));
   }
-  for (int sct = 0; sct < p.nsec; ++sct) {            // 3x3 weight grads
+  for (int sct = 0; sct < p.nsec; ++sct) {            // 3x3 weight grads (conv3w.cuh)
     const DeepSec& d = p.sec[sct];
-    need(9 * d.cinp, d.ch, d.ch, Fi * d.H * d.W);
-    need(9 * d.ch, d.ch, d.ch, Fi * d.H2 * d.W2);
+    sk = std::max(sk, conv3w_wgrad_part_bytes(F * (d.H + 2) * (d.W + 2), d.ch, d.xim));
+    sk = std::max(sk, conv3w_wgrad_part_bytes(F * (d.H2 + 2) * (d.W2 + 2), d.ch, false));
   }
   w->splitk_bytes = sk;
   w->splitk = bump(cur, sk + 16);
@@ -288,6 +291,10 @@ __global__ void refresh_lowp_multi(const float* __restrict__ params, __nv_bfloat
     float v;
     if (m.kind == IMG_S2D) {   // bijective (s*s*C == 64): iterate the source elements
       lowp[m.dst + s2d_img_pos(m, i)] = __float2bfloat16_rn(params[m.src + i]);
+      continue;
+    }
+    if (m.kind == IMG_WIN3) {  // source elements; padding positions stay zero
+      lowp[m.dst + win3_img_pos(m.d0, m.d1, m.d2, m.d3, i)] = __float2bfloat16_rn(params[m.src + i]);
       continue;
     }
     if (m.kind == IMG_COPY_PAD) {
@@ -358,6 +365,8 @@ extern "C" seed_status seed_net_refresh_lowp(const seed_net_spec* spec, const fl
   SEED_TRY(make_net_plan(spec, &p));
   if (p.nimg == 0) return SEED_OK;
   if (!params || !lowp) return SEED_E_ARG;
+  // image padding (channels, rows) is zero: clear once here, never in the step
+  SEED_CUDA_TRY(cudaMemsetAsync(lowp, 0, (size_t)p.lowp_elems * 2, (cudaStream_t)stream));
   return refresh_lowp(p, params, lowp, (cudaStream_t)stream);
 }
 

@@ -14,7 +14,7 @@ struct PTensor {
 };
 
 // One bf16 operand image inside params_lowp.
-enum { IMG_COPY_PAD = 0, IMG_CONV_DGRAD = 1, IMG_CHAN_PAD = 2, IMG_S2D = 3 };
+enum { IMG_COPY_PAD = 0, IMG_CONV_DGRAD = 1, IMG_CHAN_PAD = 2, IMG_S2D = 3, IMG_WIN3 = 4 };
 struct LowpImg {
   int kind;
   int64_t src;          // fp32 element offset of the source tensor
@@ -26,6 +26,9 @@ struct LowpImg {
                         // S2D: src W[CO=d2][2s][2s][C=d1] (s = d0) -> the pre-swizzled
                         //   space-to-depth window image (conv_s2d.cuh): d3 = 0 forward
                         //   [4][CO][64] (128-byte rows), d3 = 1 data gradient [4][64][CO]
+                        // WIN3: src W[CO=d2][3][3][CI=d1] -> the pre-swizzled 3x3 window
+                        //   image (conv3w.cuh win3_img_pos), mode d0, row bytes d3;
+                        //   rows = CO, cols = ld = 9*CI (source elements)
 };
 
 // IMG_S2D: bf16 element position (inside the image) of source element e.
@@ -55,9 +58,10 @@ __host__ __device__ inline void img_rc(const LowpImg& m, uint32_t e, uint32_t& r
 }
 
 // IMPALA-deep section (C14): conv3x3 (cin -> ch) at H x W, maxpool -> H2 x W2,
-// residual blocks at H2 x W2.
+// residual blocks at H2 x W2 (conv3w.cuh).  cinp = channels of the input rows
+// (16 / 32); xim: section-0 x-im2col input (3 windows).
 struct DeepSec {
-  int H, W, cin, cinp, ch, H2, W2, pt, pl;
+  int H, W, cin, cinp, ch, H2, W2, pt, pl, xim;
   int t_w, t_b, t_rw[2][2], t_rb[2][2];              // tensor indices
   int64_t im_w, im_dg, im_rw[2][2], im_rdg[2][2];    // bf16 image offsets
 };
@@ -99,7 +103,8 @@ struct LearnerWs {
   // shallow (conv_s2d.cuh): obs_bf16 = S0, act1 = S1, dY2 / dY1 pre-swizzled s2d rows
   // mlp
   size_t h1, h2, dh1, dh2;
-  // deep torso, per section
+  // deep torso (conv3w.cuh padded row spaces; obs_bf16 = section-0 input rows,
+  // act2 = dense relu(h) of the last section, dY2 = that section's dhA), per section
   struct Sec {
     size_t conv, arg, h[3], hr[3], u1[2], dconv, dhA, dhB, dt0;
   } sec[4];

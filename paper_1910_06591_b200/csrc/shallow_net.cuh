@@ -179,13 +179,14 @@ struct FcDgrad {
   const bf16* act2;
   bf16* dY2;             // plain [M][N] layout (deep torso), or
   uint8_t* dY2s;         // non-null: Atari-shallow conv2 output space, pre-swizzled
-                         // 64-byte rows g = f*P2 + y*W2s + x (conv_s2d.cuh)
-  int Wo, W2s, P2;
+                         // 64-byte rows g = f*P2 + g0 + y*W2s + x (conv_s2d.cuh; deep
+                         // torso: conv3w.cuh padded rows, g0 = W2s + 1)
+  int Wo, W2s, P2, g0;
   __device__ const void* ptr_a(int m, int k) const { return dfc + (size_t)m * 256 + k; }
   __device__ const void* ptr_b(int k, int n8) const { return w + (size_t)k * N + n8; }
   __device__ uint8_t* s2d_row(int m, int n, int64_t& g) const {
     const int pix = n >> 5;
-    g = (int64_t)m * P2 + (pix / Wo) * W2s + pix % Wo;
+    g = (int64_t)m * P2 + g0 + (pix / Wo) * W2s + pix % Wo;
     return dY2s + g * 64;
   }
   __device__ void store(int m, int n, float v) const {

@@ -1,0 +1,427 @@
+// win_engine.cuh — the shifted-window convolution engine on tcgen05 (templates
+// shared by the Atari-shallow space-to-depth convs, conv_s2d.cu, and the
+// IMPALA-deep 3x3 convs, conv3w.cu).
+//
+// A convolution whose taps are row offsets of one row space (a stride-1
+// convolution over an image stored as rows g = (f, Y, X) of RB bytes, borders
+// included) is a sum of NW GEMMs whose A operands are the SAME rows shifted:
+//   out[g][n] = sum_w sum_k S[g + off_w][k] * Wimg[w][n][k].
+// Forward / data gradient (win_conv_kernel): each 128-row output tile copies
+// one contiguous slab of rows (128 + max off - min off) with a single TMA bulk
+// copy and issues NW x RB/32 tcgen05.mma whose A descriptors start at the
+// shifted rows.  Rows are stored pre-swizzled (the 32B / 64B / 128B swizzle of
+// the row-relative byte address, common.cuh swz_chunk), so a linear copy that
+// keeps the address phase mod 1024 lands every row in the canonical K-major
+// operand layout; a start that is not atom-aligned reads the absolute-address
+// swizzle (verified on hardware: scripts/probe_umma_shift.cu).
+// Weight gradient (win_wgrad_kernel): reduce over rows g,
+//   dW[grp][atom][c][n] = sum_g S[g + goff_grp + atom*astride][c] * dY[g][n]
+// with A = the slab as an MN-major operand of M = 128 = NA atoms x (RB/2)
+// channels whose atoms are rows `astride` apart (atom stride LBO), B = dY rows
+// MN-major, and the bias gradient from an all-ones operand; split over rows
+// with a fixed-order finish (deterministic, C21).
+#pragma once
+#include <algorithm>
+#include "common.cuh"
+
+namespace seed {
+
+constexpr int WC_THREADS = 192;   // wgrad: warp 0 TMA producer, warp 1 MMA, warps 2-5 epilogue
+// forward / dgrad: warp 0 producer, warp 1 MMA, warps 2-9 = two epilogue groups
+// taking alternate tiles (4 TMEM accumulators), so two tiles drain at once
+constexpr int WCF_THREADS = 320;
+constexpr int WCF_ACC = 4;
+constexpr int WC_MAX_STAGES = 8;
+constexpr int WC_SMEM_BUDGET = 200 * 1024;
+constexpr int WG_KS = 256;        // rows per weight-gradient k-stage
+constexpr int WIN_MAX = 9;        // windows per convolution
+constexpr int WG_MAX_GROUPS = 3;  // weight-gradient accumulator groups
+
+struct WinConvArgs {
+  const uint8_t* src;    // pre-swizzled rows of RB bytes
+  int64_t src_rows;      // rows that exist (others read as zero)
+  int64_t M;             // output rows
+  int off[WIN_MAX];      // window row offsets
+  const uint8_t* wimg;   // pre-swizzled weight image [NW][N][RB]
+};
+
+struct WinWgradArgs {
+  const uint8_t* src;    // A: pre-swizzled rows of RBX bytes
+  int64_t src_rows;
+  const uint8_t* dy;     // B: pre-swizzled rows of 2*N bytes
+  int64_t M;             // rows summed over
+  int ngroup;            // accumulator groups (<= 3)
+  int goff[WG_MAX_GROUPS];   // row offset of each group's first atom
+  int astride;           // rows between consecutive atoms of a group
+  int64_t rows_per_cta;  // multiple of WG_KS
+  float* part;           // [grid][ngroup + 1][128][N]
+};
+
+__device__ __forceinline__ uint4 pack8(const float* o) {
+  uint4 u;
+  u.x = pack_bf16(o[0], o[1]); u.y = pack_bf16(o[2], o[3]);
+  u.z = pack_bf16(o[4], o[5]); u.w = pack_bf16(o[6], o[7]);
+  return u;
+}
+__device__ __forceinline__ void unpack8(const uint4 u, float* o) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    o[2 * k] = bf16_lo(w[k]);
+    o[2 * k + 1] = bf16_hi(w[k]);
+  }
+}
+
+// zero rows [z0, z1) of a slab (generic-proxy stores; the caller fences)
+__device__ __forceinline__ void zero_rows(uint8_t* dst, int rb, int z0, int z1, int lane) {
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int i = z0 * rb / 16 + lane; i < z1 * rb / 16; i += 32) reinterpret_cast<uint4*>(dst)[i] = z;
+}
+
+__device__ __forceinline__ int slab_phase(int64_t R0, int rb) {
+  return (int)(((R0 * rb) % 1024 + 1024) % 1024);
+}
+
+// Copy global rows [R0, R0 + n) (row bytes rb, pre-swizzled) to `slab` keeping the
+// 1024-byte address phase; rows outside [0, lim) are zero.  Called by one warp;
+// lane 0 arms `bar` (expect_tx) and issues the TMA bulk copy.
+__device__ __forceinline__ void load_slab(uint8_t* slab, const uint8_t* src, int rb, int64_t R0,
+                                          int n, int64_t lim, uint64_t* bar, int lane,
+                                          uint32_t extra_tx) {
+  uint8_t* dst = slab + slab_phase(R0, rb);
+  const int64_t lo = std::max<int64_t>(R0, 0), hi = std::min<int64_t>(R0 + n, lim);
+  const int zlo = (int)std::min<int64_t>(std::max<int64_t>(lo - R0, 0), n);
+  const int zhi = hi > lo ? (int)(hi - R0) : zlo;
+  if (zlo > 0 || zhi < n) {
+    zero_rows(dst, rb, 0, zlo, lane);
+    zero_rows(dst, rb, zhi, n, lane);
+    fence_proxy_async_smem();
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const uint32_t bytes = hi > lo ? (uint32_t)((hi - lo) * rb) : 0u;
+    if (bytes + extra_tx) mbar_expect_tx(bar, bytes + extra_tx);
+    else mbar_arrive(bar);
+    if (bytes) bulk_g2s(smem_u32(dst + (lo - R0) * rb), src + lo * rb, bytes, bar);
+  }
+}
+
+// ------------------------------------------------------------------ forward / dgrad
+// Epi: static constexpr int N; __device__ void store(int64_t m, float (&v)[N]) const
+template <class Epi, int RB, int NW>
+__global__ void __launch_bounds__(WCF_THREADS, 1)
+    win_conv_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes) {
+  constexpr int N = Epi::N;
+  constexpr uint32_t LAYOUT = swz_layout_code(RB);
+  constexpr int WB = NW * N * RB;
+  constexpr uint32_t TCOLS = WCF_ACC * N < 32 ? 32 : WCF_ACC * N;
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* Ws = sm;
+  uint8_t* slabs = sm + ((WB + 1023) & ~1023);
+  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[WCF_ACC], tempty[WCF_ACC], wbar;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int mn = a.off[0], mx = a.off[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) { mn = min(mn, a.off[w]); mx = max(mx, a.off[w]); }
+  const int nrows = 128 + mx - mn;
+  const int64_t tiles = (a.M + 127) / 128;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int i = 0; i < WCF_ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    mbar_init(&wbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&tbase, TCOLS);
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tmem = tbase;
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(&wbar, WB);
+      bulk_g2s(smem_u32(Ws), a.wimg, WB, &wbar);
+    }
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int s = it % stages;
+      mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+      load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, t * 128 + mn, nrows, a.src_rows, &full[s],
+                lane, 0);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      mbar_wait(&wbar, 0);
+      const uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+      const uint64_t bd0 = umma_desc(smem_u32(Ws), 16, 8 * RB, LAYOUT);
+      int aoff[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) aoff[w] = ((a.off[w] - mn) * RB) >> 4;
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const int s = it % stages, acc = it % WCF_ACC;
+        mbar_wait(&full[s], (it / stages) & 1);
+        mbar_wait(&tempty[acc], ((it / WCF_ACC) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t base =
+            smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * 128 + mn, RB);
+        // descriptors advance linearly with the start address (field = addr >> 4)
+        const uint64_t ad0 = umma_desc(base, 16, 8 * RB, LAYOUT);
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+          for (int ks = 0; ks < RB / 32; ++ks)
+            tc_mma_bf16(tmem + acc * N, ad0 + (uint64_t)(aoff[w] + ks * 2),
+                        bd0 + (uint64_t)((w * N * RB + ks * 32) >> 4), idesc, (w | ks) != 0);
+        tc_commit(&empty[s]);
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int q = warp & 3;            // TMEM lanes [32q, 32q+32) of this warp
+    const int grp = (warp - 2) >> 2;   // epilogue group: tiles it with it % 2 == grp
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      if ((it & 1) != grp) continue;
+      const int acc = it % WCF_ACC;
+      mbar_wait(&tfull[acc], (it / WCF_ACC) & 1);
+      tc_fence_after();
+      float v[N];
+#pragma unroll
+      for (int c = 0; c < N / 16; ++c)
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * N + c * 16, v + 16 * c);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      const int64_t m = t * 128 + q * 32 + lane;
+      if (m < a.M) e.store(m, v);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TCOLS);
+  }
+}
+
+template <class Epi, int RB, int NW>
+seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st) {
+  constexpr int WB = NW * Epi::N * RB;
+  int mn = a.off[0], mx = a.off[0];
+  for (int w = 1; w < NW; ++w) { mn = std::min(mn, a.off[w]); mx = std::max(mx, a.off[w]); }
+  const int slab = (int)align_up((size_t)(128 + mx - mn) * RB + 1024, 1024);
+  const int wbytes = (int)align_up(WB, 1024);
+  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - wbytes) / slab);
+  if (a.M <= 0) return a.M == 0 ? SEED_OK : SEED_E_SHAPE;
+  if (stages < 2) return SEED_E_SHAPE;
+  const size_t smem = (size_t)wbytes + (size_t)stages * slab + 1024;
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win_conv_kernel<Epi, RB, NW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       WC_SMEM_BUDGET + 2048));
+    attr = true;
+  }
+  const int64_t tiles = (a.M + 127) / 128;
+  const int grid = (int)std::min<int64_t>(tiles, 148);
+  return launch_k(win_conv_kernel<Epi, RB, NW>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e,
+                  stages, slab);
+}
+
+// ------------------------------------------------------------------ weight gradient
+// Per CTA: rows [z*R, min((z+1)*R, M)) in k-stages of WG_KS rows.  Accumulator
+// group g (TMEM columns [g*N, g*N+N)) = M=128 MN-major operand whose NA atoms
+// start at rows goff[g] + atom*astride; group `ngroup` = all-ones operand (every
+// row = the column sum of dY = the bias gradient).
+template <int N, int RBX, int NG>
+__global__ void __launch_bounds__(WC_THREADS, 1)
+    win_wgrad_kernel(const WinWgradArgs a, int stages, int a_bytes, int b_bytes) {
+  constexpr int RBY = 2 * N;
+  constexpr uint32_t LA = swz_layout_code(RBX), LB = swz_layout_code(RBY);
+  constexpr int NA = 256 / RBX;   // atoms per M = 128
+  constexpr uint32_t TCOLS = 4 * N < 32 ? 32 : (4 * N <= 64 ? 64 : 128);
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* ones = sm;                  // 1 KB of bf16 1.0
+  uint8_t* stg = sm + 1024;            // stages x (A slab | B slab)
+  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t r_end = std::min<int64_t>(a.M, r_begin + a.rows_per_cta);
+  const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
+  int gmn = a.goff[0], gmx = a.goff[0];
+#pragma unroll
+  for (int g = 1; g < NG; ++g) { gmn = min(gmn, a.goff[g]); gmx = max(gmx, a.goff[g]); }
+  const int arows = WG_KS + gmx - gmn + (NA - 1) * a.astride;
+  for (int i = threadIdx.x; i < 64; i += blockDim.x)
+    reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&tbase, TCOLS);
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tmem = tbase;
+  if (warp == 0) {
+    for (int it = 0; it < nks; ++it) {
+      const int s = it % stages;
+      mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+      const int64_t k0 = r_begin + (int64_t)it * WG_KS;
+      uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
+      // B first (its bytes are credited through the A call's expect_tx)
+      const int64_t blo = k0, bhi = std::min<int64_t>(k0 + WG_KS, r_end);
+      uint8_t* bd = sa + a_bytes + slab_phase(k0, RBY);
+      if (bhi - blo < WG_KS) {
+        zero_rows(bd, RBY, (int)(bhi - blo), WG_KS, lane);
+        fence_proxy_async_smem();
+      }
+      __syncwarp();
+      const uint32_t bbytes = (uint32_t)((bhi - blo) * RBY);
+      load_slab(sa, a.src, RBX, k0 + gmn, arows, a.src_rows, &full[s], lane, bbytes);
+      if (lane == 0) bulk_g2s(smem_u32(bd), a.dy + blo * RBY, bbytes, &full[s]);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(128, N, true, true);
+      const uint64_t od = umma_desc(smem_u32(ones), 0, 0, 2);
+      const uint32_t lbo = (uint32_t)(a.astride * RBX);
+      int goffd[NG];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) goffd[g] = ((a.goff[g] - gmn) * RBX) >> 4;
+      for (int it = 0; it < nks; ++it) {
+        const int s = it % stages;
+        mbar_wait(&full[s], (it / stages) & 1);
+        tc_fence_after();
+        const int64_t k0 = r_begin + (int64_t)it * WG_KS;
+        uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
+        // descriptors advance linearly with the start address (field = addr >> 4)
+        const uint64_t ad0 = umma_desc(smem_u32(sa) + slab_phase(k0 + gmn, RBX), lbo, 8 * RBX, LA);
+        const uint64_t bd0 = umma_desc(smem_u32(sa + a_bytes) + slab_phase(k0, RBY), 8 * RBY, 8 * RBY, LB);
+        const uint32_t acc0 = it != 0;
+#pragma unroll
+        for (int ks = 0; ks < WG_KS / 16; ++ks) {
+          const uint64_t bdsc = bd0 + (uint64_t)((ks * 16 * RBY) >> 4);
+          const uint32_t accf = acc0 | (ks != 0);
+#pragma unroll
+          for (int g = 0; g < NG; ++g)
+            tc_mma_bf16(tmem + g * N, ad0 + (uint64_t)(goffd[g] + ((ks * 16 * RBX) >> 4)), bdsc, idesc,
+                        accf);
+          tc_mma_bf16(tmem + NG * N, od, bdsc, idesc, accf);
+        }
+        tc_commit(&empty[s]);
+      }
+      tc_commit(&tfull);
+    }
+  } else {
+    const int q = warp & 3;
+    const int ng1 = NG + 1;
+    float* part = a.part + (size_t)blockIdx.x * ng1 * 128 * N;
+    if (nks > 0) {
+      mbar_wait(&tfull, 0);
+      tc_fence_after();
+    }
+#pragma unroll
+    for (int t = 0; t < ng1; ++t) {
+      float v[N];
+      if (nks > 0) {
+#pragma unroll
+        for (int c = 0; c < N / 16; ++c)
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + t * N + c * 16, v + 16 * c);
+      } else {
+#pragma unroll
+        for (int c = 0; c < N; ++c) v[c] = 0.f;
+      }
+      const int row = q * 32 + lane;
+      if (t < NG || row == 0) {
+        float4* dst = reinterpret_cast<float4*>(part + ((size_t)t * 128 + row) * N);
+#pragma unroll
+        for (int c = 0; c < N / 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TCOLS);
+  }
+}
+
+// Fixed-order sum of the per-CTA partials; block = 32 outputs x 8 split groups.
+// Fin: __device__ void weight(int grp, int i /*0..127*/, int n, float v) const;
+//      __device__ void bias(int n, float v) const.
+template <class Fin>
+__global__ void __launch_bounds__(256) win_wgrad_finish(const float* __restrict__ part, int G, int N,
+                                                        int ngroup, const Fin f) {
+  pdl_wait();
+  const int ng1 = ngroup + 1;
+  const int tot = ngroup * 128 * N + N;
+  const int o = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
+  __shared__ float sh[8][33];
+  float s = 0.f;
+  if (o < tot) {
+    const size_t idx = (size_t)o;   // bias outputs are row 0 of group `ngroup`
+    for (int z = g; z < G; z += 8) s += part[(size_t)z * ng1 * 128 * N + idx];
+  }
+  sh[g][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (g == 0 && o < tot) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x & 31];
+    if (o >= ngroup * 128 * N) f.bias(o - ngroup * 128 * N, t);
+    else f.weight(o / (128 * N), (o / N) % 128, o % N, t);
+  }
+}
+
+inline int wgrad_grid(int64_t M, int64_t* rows_per_cta) {
+  const int64_t kst = (M + WG_KS - 1) / WG_KS;
+  const int64_t G0 = std::min<int64_t>(148, std::max<int64_t>(kst, 1));
+  const int64_t per = (kst + G0 - 1) / G0;
+  *rows_per_cta = per * WG_KS;
+  return (int)std::max<int64_t>(1, (M + per * WG_KS - 1) / (per * WG_KS));
+}
+
+inline size_t win_wgrad_part_bytes_g(int64_t M, int N, int ngroup) {
+  int64_t r;
+  return (size_t)wgrad_grid(M, &r) * (ngroup + 1) * 128 * N * 4;
+}
+
+template <int N, int RBX, class Fin>
+seed_status launch_win_wgrad(const WinWgradArgs& a0, const Fin& fin, cudaStream_t st) {
+  WinWgradArgs a = a0;
+  if (a.ngroup < 1 || a.ngroup > WG_MAX_GROUPS) return SEED_E_SHAPE;
+  const int G = wgrad_grid(a.M, &a.rows_per_cta);
+  int gmn = a.goff[0], gmx = a.goff[0];
+  for (int g = 1; g < a.ngroup; ++g) { gmn = std::min(gmn, a.goff[g]); gmx = std::max(gmx, a.goff[g]); }
+  const int arows = WG_KS + gmx - gmn + (256 / RBX - 1) * a.astride;
+  const int a_bytes = (int)align_up((size_t)arows * RBX + 1024, 1024);
+  const int b_bytes = (int)align_up((size_t)WG_KS * 2 * N + 1024, 1024);
+  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes));
+  if (stages < 2) return SEED_E_SHAPE;
+  const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win_wgrad_kernel<N, RBX, 1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win_wgrad_kernel<N, RBX, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win_wgrad_kernel<N, RBX, 3>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
+    attr = true;
+  }
+  auto kern = a.ngroup == 1 ? win_wgrad_kernel<N, RBX, 1>
+            : a.ngroup == 2 ? win_wgrad_kernel<N, RBX, 2> : win_wgrad_kernel<N, RBX, 3>;
+  SEED_TRY(launch_k(kern, dim3(G), dim3(WC_THREADS), smem, st, a, stages, a_bytes, b_bytes));
+  const int tot = a.ngroup * 128 * N + N;
+  return launch_k(win_wgrad_finish<Fin>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
+                  (const float*)a.part, G, N, a.ngroup, fin);
+}
+
+}  // namespace seed

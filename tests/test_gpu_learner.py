@@ -206,6 +206,28 @@ def _deep_dims(ospec):
     return out
 
 
+def _padded_rows(L, name, shape):
+    """Decode a deep-torso activation buffer (conv3w.cuh layout: rows of the padded
+    (H+2) x (W+2) space, C bf16 channels per row, 16-byte chunks stored at the
+    32B / 64B swizzled position) into dense (F, H, W, C) float64, and check that
+    the border rows hold zeros."""
+    F_, H, W, C = shape
+    rows, rb = F_ * (H + 2) * (W + 2), 2 * C
+    raw = L.debug_buffer(name, torch.uint8, (rows, rb)).cpu().numpy()
+    g = np.arange(rows)[:, None]
+    j = np.arange(rb // 16)[None, :]
+    phys = j ^ (((g >> 2) & 1) if rb == 32 else ((g >> 1) & 3))
+    chunks = raw.reshape(rows, rb // 16, 16)
+    dense = np.take_along_axis(chunks, phys[:, :, None], axis=1).reshape(rows, rb)
+    v = torch.from_numpy(np.ascontiguousarray(dense)).view(torch.bfloat16).float().numpy()
+    v = v.reshape(F_, H + 2, W + 2, C).astype(np.float64)
+    border = v.copy()
+    border[:, 1:-1, 1:-1, :] = 0
+    if not name.endswith(".conv"):   # the section conv output's border is never read
+        assert not np.any(border), f"{name}: nonzero border rows"
+    return v[:, 1:-1, 1:-1, :]
+
+
 @pytest.mark.parametrize("cfg,B,T", [("c3", 2, 3), ("c4", 2, 2), ("c3", 3, 1)])
 def test_learner_deep_parity(cfg, B, T):
     """configs[2] (DMLab IMPALA-deep, 72x96x3) / configs[3] (GRF SMM 72x96x16), full
@@ -260,7 +282,7 @@ def test_learner_deep_parity(cfg, B, T):
     dims = _deep_dims(ospec)
 
     def buf(s, n, shape):
-        return L.debug_buffer(f"s{s}.{n}", bf, shape).float().cpu().numpy().astype(np.float64)
+        return _padded_rows(L, f"s{s}.{n}", shape)
 
     for s, (H, W, H2, W2, ch) in enumerate(dims):
         bf16_check(buf(s, "conv", (F_, H, W, ch)), cache[f"s{s}.conv"], f"s{s}.conv")
@@ -274,6 +296,8 @@ def test_learner_deep_parity(cfg, B, T):
     H, W, H2, W2, ch = dims[last]
     hr2 = buf(last, "hr2", (F_, H2, W2, ch))
     act2 = hr2.reshape(F_, -1)
+    np.testing.assert_array_equal(
+        L.debug_buffer("act2", bf, (F_, act2.shape[1])).float().cpu().numpy(), act2)
     scaled_check(gt["fc.w"], dfc.T @ act2, 1e-3, "fc.w (teacher-forced)")
     scaled_check(gt["fc.b"], dfc.sum(0), 1e-3, "fc.b (teacher-forced)")
     dh = q((dfc @ Pq["fc.w"]).reshape(F_, H2, W2, ch) * (hr2 > 0))
@@ -291,7 +315,8 @@ def test_learner_deep_parity(cfg, B, T):
             scaled_check(gt[f"s{s}.res{r}.conv0.b"], db0, 5e-3, f"s{s}.res{r}.conv0.b")
             dh = q(dh + du0 * (hr > 0))
         bf16_check(buf(s, "dhA", (F_, H2, W2, ch)), dh, f"s{s}.dh(h0)", tol=1e-2)
-        arg = L.debug_buffer(f"s{s}.arg", torch.uint8, (F_, H2, W2, ch)).cpu().numpy()
+        arg = L.debug_buffer(f"s{s}.arg", torch.uint8, (F_, H2 + 2, W2 + 2, ch)).cpu().numpy()
+        arg = arg[:, 1:-1, 1:-1, :]
         cin = ospec.obs_c if s == 0 else dims[s - 1][4]
         dconv = np.zeros((F_, H, W, ch))
         offs = ((max((H2 - 1) * 2 + 3 - H, 0)) // 2, (max((W2 - 1) * 2 + 3 - W, 0)) // 2)
