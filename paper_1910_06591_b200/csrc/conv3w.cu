@@ -192,66 +192,86 @@ seed_status conv3w_dgrad(const Conv3wDgrad& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ weight gradient
-static WinWgradArgs wgrad_args(const Conv3wWgrad& a) {
-  WinWgradArgs w{};
-  w.src = a.X; w.src_rows = a.rows; w.dy = a.dY; w.M = a.rows; w.part = a.part;
-  if (a.xim) {
-    w.ngroup = 1; w.goff[0] = -a.g.Wp; w.astride = a.g.Wp;
-  } else {
-    w.ngroup = 3;
-    for (int k = 0; k < 3; ++k) w.goff[k] = (k - 1) * a.g.Wp - 1;
-    w.astride = 1;
+// win_engine.cuh win3_wgrad_kernel: D[(kx, c)][(j, co)], tap ky = 2 - j.
+//   9-window input: dW[co][ky][kx][c] = sum_h X[h + kx][c] dY[h + 1 - Wp + j*Wp][co]
+//   x-im2col input: dW[co][ky][(kx, c)] = sum_h X[h][(kx, c)] dY[h - Wp + j*Wp][co] (atom 0)
+struct W3Fin3 {
+  int xim, Cp, CI, CO;
+  float scale;
+  float* g_w;
+  float* g_b;
+  __device__ void weight3(int i, int n, float t) const {
+    const int atom = i / Cp, ch = i % Cp;
+    const int ky = 2 - n / CO, co = n % CO;
+    int kx, c;
+    if (xim) {
+      if (atom != 0 || ch >= 3 * CI) return;
+      kx = ch / CI; c = ch % CI;
+    } else {
+      if (atom >= 3 || ch >= CI) return;
+      kx = atom; c = ch;
+    }
+    g_w[(((size_t)co * 3 + ky) * 3 + kx) * CI + c] = t * scale;
   }
-  return w;
-}
+  __device__ void bias(int n, float t) const { g_b[n] = t; }
+};
 
-size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool xim) {
-  return win_wgrad_part_bytes_g(rows, ch, xim ? 1 : 3);
-}
+size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool) { return win3_wgrad_part_bytes(rows, ch); }
 
 seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
-  const WinWgradArgs w = wgrad_args(a);
-  W3Fin f{};
-  f.xim = a.xim ? 1 : 0; f.Cp = a.cin_p; f.CI = a.cin; f.scale = a.scale; f.g_w = a.g_w;
+  Win3WgradArgs w{};
+  w.X = a.X; w.dy = a.dY; w.M = a.rows; w.part = a.part;
+  w.boff = a.xim ? -a.g.Wp : 1 - a.g.Wp;
+  w.bstride = a.g.Wp;
+  W3Fin3 f{};
+  f.xim = a.xim ? 1 : 0; f.Cp = a.cin_p; f.CI = a.cin; f.CO = a.ch; f.scale = a.scale; f.g_w = a.g_w;
   f.g_b = a.g_b;
-  if (a.ch == 16 && a.cin_p == 16) return launch_win_wgrad<16, 32>(w, f, st);
-  if (a.ch == 32 && a.cin_p == 16) return launch_win_wgrad<32, 32>(w, f, st);
-  if (a.ch == 16 && a.cin_p == 32) return launch_win_wgrad<16, 64>(w, f, st);
-  if (a.ch == 32 && a.cin_p == 32) return launch_win_wgrad<32, 64>(w, f, st);
+  if (a.ch == 16 && a.cin_p == 16) return launch_win3_wgrad<16, 32>(w, f, st);
+  if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, st);
+  if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, st);
+  if (a.ch == 32 && a.cin_p == 32) return launch_win3_wgrad<32, 64>(w, f, st);
   return SEED_E_UNSUPPORTED;
 }
 
-// ------------------------------------------------------------------ obs conversion
-// one thread per (row, 16-byte chunk of 8 channels)
-__global__ void conv3_obs_kernel(int64_t n, PadGeo g, int C, int Cp, int xim,
-                                 const uint8_t* __restrict__ obs, uint8_t* __restrict__ X0) {
+// ------------------------------------------------------------------ row-parallel kernels
+// grid.x = one padded image row (f, Y) of the output space, grid.y * blockDim.x
+// threads over (X, chunk j): no per-thread divisions beyond constant shifts.
+constexpr int ROWK_THREADS = 128;
+
+// obs conversion: thread = (X, chunk of 8 channels)
+template <int NC, int CX>   // chunks per row; CX = compile-time C for the x-im2col path (0 = runtime)
+__global__ void __launch_bounds__(ROWK_THREADS) conv3_obs_kernel(
+    PadGeo g, int C, int xim, const uint8_t* __restrict__ obs, uint8_t* __restrict__ X0) {
   pdl_wait();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int NC = Cp / 8, RB = 2 * Cp;
-  const int j = (int)(i % NC);
-  const int64_t m = i / NC;
-  int f, y, x;
+  constexpr int RB = NC * 16;
+  const int t = blockIdx.y * ROWK_THREADS + threadIdx.x;
+  if (t >= g.Wp * NC) return;
+  const int X = t / NC, j = t % NC;
+  const int Hp = g.H + 2;
+  const int f = blockIdx.x / Hp, Y = blockIdx.x - f * Hp;
+  const int64_t m = (int64_t)blockIdx.x * g.Wp + X;
+  const int y = Y - 1, x = X - 1;
   float v[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) v[k] = 0.f;
-  if (g.split(m, f, y, x)) {
-    const uint8_t* fr = obs + (size_t)f * g.H * g.W * C;
-    if (!xim && C % 8 == 0) {
-      const uint2 u = __ldg(reinterpret_cast<const uint2*>(fr + ((size_t)y * g.W + x) * C + 8 * j));
+  if (y >= 0 && y < g.H && x >= 0 && x < g.W) {
+    const int Cr = CX ? CX : C;
+    const uint8_t* px = obs + (((size_t)f * g.H + y) * g.W + x) * Cr;
+    if (!xim && Cr % 8 == 0) {
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(px + 8 * j));
       const uint32_t w[2] = {u.x, u.y};
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] = (float)((w[k >> 2] >> (8 * (k & 3))) & 0xFF);
+    } else if (!xim) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (8 * j + k < Cr) v[k] = (float)__ldg(px + 8 * j + k);
     } else {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int ch = 8 * j + k;
-        if (!xim) {
-          if (ch < C) v[k] = (float)__ldg(fr + ((size_t)y * g.W + x) * C + ch);
-        } else if (ch < 3 * C) {
-          const int kx = ch / C, c = ch % C, xx = x + kx - 1;
-          if (xx >= 0 && xx < g.W) v[k] = (float)__ldg(fr + ((size_t)y * g.W + xx) * C + c);
-        }
+        const int kx = ch / Cr, c = ch - kx * Cr, xx = x + kx - 1;
+        if (ch < 3 * Cr && xx >= 0 && xx < g.W) v[k] = (float)__ldg(px + (kx - 1) * Cr + c);
       }
     }
   }
@@ -260,50 +280,62 @@ __global__ void conv3_obs_kernel(int64_t n, PadGeo g, int C, int Cp, int xim,
 
 seed_status conv3_obs(const uint8_t* obs, int64_t F, const PadGeo& g, int C, int Cp, bool xim,
                       uint8_t* X0, cudaStream_t st) {
-  const int64_t n = F * g.P * (Cp / 8);
-  if (n == 0) return SEED_OK;
-  return launch_k(conv3_obs_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, n, g, C, Cp,
-                  xim ? 1 : 0, obs, X0);
+  if (F == 0) return SEED_OK;
+  const int NC = Cp / 8;
+  const dim3 grid((unsigned)(F * (g.H + 2)), (unsigned)ceil_div(g.Wp * NC, ROWK_THREADS));
+  if (NC == 2) {
+    if (xim && C == 3) return launch_k(conv3_obs_kernel<2, 3>, grid, dim3(ROWK_THREADS), 0, st, g, C, 1, obs, X0);
+    return launch_k(conv3_obs_kernel<2, 0>, grid, dim3(ROWK_THREADS), 0, st, g, C, xim ? 1 : 0, obs, X0);
+  }
+  if (NC == 4 && !xim)
+    return launch_k(conv3_obs_kernel<4, 0>, grid, dim3(ROWK_THREADS), 0, st, g, C, 0, obs, X0);
+  return SEED_E_UNSUPPORTED;
 }
 
 // ------------------------------------------------------------------ max-pool
-__global__ void conv3w_pool_fwd_kernel(int64_t n, PadGeo gi, PadGeo go, int C, int pt, int pl,
-                                       const uint8_t* __restrict__ conv, uint8_t* __restrict__ h0,
-                                       uint8_t* __restrict__ hr0, uint8_t* __restrict__ arg) {
+template <int NC>
+__global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
+    PadGeo gi, PadGeo go, int pt, int pl, const uint8_t* __restrict__ conv, uint8_t* __restrict__ h0,
+    uint8_t* __restrict__ hr0, uint8_t* __restrict__ arg) {
   pdl_wait();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int NC = C / 8, RB = 2 * C;
-  const int j = (int)(i % NC);
-  const int64_t m = i / NC;
-  int f, oy, ox;
-  if (!go.split(m, f, oy, ox)) {
+  constexpr int C = NC * 8, RB = NC * 16;
+  const int t = blockIdx.y * ROWK_THREADS + threadIdx.x;
+  if (t >= go.Wp * NC) return;
+  const int X = t / NC, j = t % NC;
+  const int Hp = go.H + 2;
+  const int f = blockIdx.x / Hp, Y = blockIdx.x - f * Hp;
+  const int64_t m = (int64_t)blockIdx.x * go.Wp + X;
+  const int oy = Y - 1, ox = X - 1;
+  if (oy < 0 || oy >= go.H || ox < 0 || ox >= go.W) {
     const uint4 z = make_uint4(0, 0, 0, 0);
     *chunk_at(h0, m, RB, j) = z;
     *chunk_at(hr0, m, RB, j) = z;
     return;
   }
+  uint4 in[9];
+  const int64_t fb = (int64_t)f * gi.P;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {   // issue all window loads first
+    const int y = oy * 2 - pt + q / 3, x = ox * 2 - pl + q % 3;
+    const bool ok = y >= 0 && y < gi.H && x >= 0 && x < gi.W;
+    in[q] = ok ? __ldg(chunk_at(conv, fb + (int64_t)(y + 1) * gi.Wp + (x + 1), RB, j))
+               : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);   // -inf
+  }
   float best[8];
   uint32_t barg[8];
+  unpack8(in[0], best);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) { best[k] = -INFINITY; barg[k] = 0; }
+  for (int k = 0; k < 8; ++k) barg[k] = 0;
 #pragma unroll
-  for (int ky = 0; ky < 3; ++ky) {
-    const int y = oy * 2 - pt + ky;
-    if (y < 0 || y >= gi.H) continue;
+  for (int q = 1; q < 9; ++q) {
+    float v[8];
+    unpack8(in[q], v);
 #pragma unroll
-    for (int kx = 0; kx < 3; ++kx) {
-      const int x = ox * 2 - pl + kx;
-      if (x < 0 || x >= gi.W) continue;
-      float v[8];
-      unpack8(__ldg(chunk_at(conv, gi.row(f, y, x), RB, j)), v);
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (v[k] > best[k]) {   // strict: the first maximum in (ky, kx) order wins
-          best[k] = v[k];
-          barg[k] = ky * 3 + kx;
-        }
-    }
+    for (int k = 0; k < 8; ++k)
+      if (v[k] > best[k]) {   // strict: the first maximum in (ky, kx) order wins
+        best[k] = v[k];
+        barg[k] = q;
+      }
   }
   float r[8];
 #pragma unroll
@@ -316,42 +348,48 @@ __global__ void conv3w_pool_fwd_kernel(int64_t n, PadGeo gi, PadGeo go, int C, i
   *reinterpret_cast<uint2*>(arg + m * C + 8 * j) = a;
 }
 
-__global__ void conv3w_pool_bwd_kernel(int64_t n, PadGeo gi, PadGeo go, int C, int pt, int pl,
-                                       const uint8_t* __restrict__ dout,
-                                       const uint8_t* __restrict__ arg, uint8_t* __restrict__ din) {
+template <int NC>
+__global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_bwd_kernel(
+    PadGeo gi, PadGeo go, int pt, int pl, const uint8_t* __restrict__ dout,
+    const uint8_t* __restrict__ arg, uint8_t* __restrict__ din) {
   pdl_wait();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int NC = C / 8, RB = 2 * C;
-  const int j = (int)(i % NC);
-  const int64_t m = i / NC;
-  int f, y, x;
+  constexpr int C = NC * 8, RB = NC * 16;
+  const int t = blockIdx.y * ROWK_THREADS + threadIdx.x;
+  if (t >= gi.Wp * NC) return;
+  const int X = t / NC, j = t % NC;
+  const int Hp = gi.H + 2;
+  const int f = blockIdx.x / Hp, Y = blockIdx.x - f * Hp;
+  const int64_t m = (int64_t)blockIdx.x * gi.Wp + X;
+  const int y = Y - 1, x = X - 1;
   float s[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) s[k] = 0.f;
-  if (gi.split(m, f, y, x)) {
+  if (y >= 0 && y < gi.H && x >= 0 && x < gi.W) {
     // windows (oy, ox) with oy*2 - pt <= y <= oy*2 - pt + 2, in ascending order
     const int oy_hi = (y + pt) >> 1, ox_hi = (x + pl) >> 1;
+    const int64_t fb = (int64_t)f * go.P;
+    uint2 av[4];
+    uint4 dv[4];
+    uint32_t want[4];
 #pragma unroll
-    for (int dy = 0; dy < 2; ++dy) {
-      const int oy = oy_hi - 1 + dy;
-      const int ky = y - (oy * 2 - pt);
-      if (oy < 0 || oy >= go.H || ky < 0 || ky > 2) continue;
+    for (int q = 0; q < 4; ++q) {   // issue all loads first
+      const int oy = oy_hi - 1 + (q >> 1), ox = ox_hi - 1 + (q & 1);
+      const int ky = y - (oy * 2 - pt), kx = x - (ox * 2 - pl);
+      const bool ok = oy >= 0 && oy < go.H && ky >= 0 && ky <= 2 && ox >= 0 && ox < go.W && kx >= 0 &&
+                      kx <= 2;
+      want[q] = ok ? (uint32_t)(ky * 3 + kx) : 0xFFu;
+      const int64_t o = fb + (int64_t)(oy + 1) * go.Wp + (ox + 1);
+      av[q] = ok ? __ldg(reinterpret_cast<const uint2*>(arg + o * C + 8 * j)) : make_uint2(0, 0);
+      dv[q] = ok ? __ldg(chunk_at(dout, o, RB, j)) : make_uint4(0, 0, 0, 0);
+    }
 #pragma unroll
-      for (int dx = 0; dx < 2; ++dx) {
-        const int ox = ox_hi - 1 + dx;
-        const int kx = x - (ox * 2 - pl);
-        if (ox < 0 || ox >= go.W || kx < 0 || kx > 2) continue;
-        const int64_t o = go.row(f, oy, ox);
-        const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + o * C + 8 * j));
-        float d[8];
-        unpack8(__ldg(chunk_at(dout, o, RB, j)), d);
-        const uint32_t want = (uint32_t)(ky * 3 + kx);
+    for (int q = 0; q < 4; ++q) {
+      float d[8];
+      unpack8(dv[q], d);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t ak = ((k < 4 ? a.x : a.y) >> (8 * (k & 3))) & 0xFF;
-          if (ak == want) s[k] += d[k];
-        }
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t ak = ((k < 4 ? av[q].x : av[q].y) >> (8 * (k & 3))) & 0xFF;
+        if (ak == want[q]) s[k] += d[k];
       }
     }
   }
@@ -361,19 +399,27 @@ __global__ void conv3w_pool_bwd_kernel(int64_t n, PadGeo gi, PadGeo go, int C, i
 seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
                             const uint8_t* conv, uint8_t* h0, uint8_t* hr0, uint8_t* arg,
                             cudaStream_t st) {
-  const int64_t n = F * go.P * (C / 8);
-  if (n == 0) return SEED_OK;
-  return launch_k(conv3w_pool_fwd_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, n,
-                  gi, go, C, pt, pl, conv, h0, hr0, arg);
+  if (F == 0) return SEED_OK;
+  const int NC = C / 8;
+  const dim3 grid((unsigned)(F * (go.H + 2)), (unsigned)ceil_div(go.Wp * NC, ROWK_THREADS));
+  if (NC == 2)
+    return launch_k(conv3w_pool_fwd_kernel<2>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, conv, h0, hr0, arg);
+  if (NC == 4)
+    return launch_k(conv3w_pool_fwd_kernel<4>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, conv, h0, hr0, arg);
+  return SEED_E_UNSUPPORTED;
 }
 
 seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
                             const uint8_t* dout, const uint8_t* arg, uint8_t* din,
                             cudaStream_t st) {
-  const int64_t n = F * gi.P * (C / 8);
-  if (n == 0) return SEED_OK;
-  return launch_k(conv3w_pool_bwd_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, n,
-                  gi, go, C, pt, pl, dout, arg, din);
+  if (F == 0) return SEED_OK;
+  const int NC = C / 8;
+  const dim3 grid((unsigned)(F * (gi.H + 2)), (unsigned)ceil_div(gi.Wp * NC, ROWK_THREADS));
+  if (NC == 2)
+    return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, dout, arg, din);
+  if (NC == 4)
+    return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, dout, arg, din);
+  return SEED_E_UNSUPPORTED;
 }
 
 }  // namespace seed

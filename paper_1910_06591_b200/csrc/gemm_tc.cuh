@@ -411,8 +411,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
       }
     }
   } else if (warp == GEMM_MMA_WARP) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (warp-uniform,
+    // one elected lane issues: common.cuh tc_mma_bf16_w)
+    {
       constexpr uint32_t idesc = umma_idesc_bf16(GEMM_BM, BN, Prob::A_MN, Prob::B_MN);
       const uint32_t smem0 = smem_u32(smem);
       int g = 0, it = 0;
@@ -434,12 +435,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = TA::desc(a_base, kk);
             const uint64_t bd = TB::desc(b_base, kk);
-            tc_mma_bf16(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            tc_mma_bf16_w(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit(&empty[s]);
+          tc_commit_w(&empty[s]);
         }
-        if (nkb > 0) tc_commit(&tfull[acc]);
-        else mbar_arrive(&tfull[acc]);
+        if (nkb > 0) tc_commit_w(&tfull[acc]);
+        else if (lane == 0) mbar_arrive(&tfull[acc]);
         GEMM_STAMP(4, it == 0)
       }
     }

@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
       load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, t * 128 + mn, nrows, a.src_rows, &full[s],
                 lane, 0);
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
+  } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
+    {
       mbar_wait(&wbar, 0);
       const uint32_t idesc = umma_idesc_bf16(128, N, false, false);
       const uint64_t bd0 = umma_desc(smem_u32(Ws), 16, 8 * RB, LAYOUT);
@@ -172,10 +172,10 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
         for (int w = 0; w < NW; ++w)
 #pragma unroll
           for (int ks = 0; ks < RB / 32; ++ks)
-            tc_mma_bf16(tmem + acc * N, ad0 + (uint64_t)(aoff[w] + ks * 2),
+            tc_mma_bf16_w(tmem + acc * N, ad0 + (uint64_t)(aoff[w] + ks * 2),
                         bd0 + (uint64_t)((w * N * RB + ks * 32) >> 4), idesc, (w | ks) != 0);
-        tc_commit(&empty[s]);
-        tc_commit(&tfull[acc]);
+        tc_commit_w(&empty[s]);
+        tc_commit_w(&tfull[acc]);
       }
     }
   } else {
@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       load_slab(sa, a.src, RBX, k0 + gmn, arows, a.src_rows, &full[s], lane, bbytes);
       if (lane == 0) bulk_g2s(smem_u32(bd), a.dy + blo * RBY, bbytes, &full[s]);
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
+  } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
+    {
       const uint32_t idesc = umma_idesc_bf16(128, N, true, true);
       const uint64_t od = umma_desc(smem_u32(ones), 0, 0, 2);
       const uint32_t lbo = (uint32_t)(a.astride * RBX);
@@ -310,13 +310,13 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
           const uint32_t accf = acc0 | (ks != 0);
 #pragma unroll
           for (int g = 0; g < NG; ++g)
-            tc_mma_bf16(tmem + g * N, ad0 + (uint64_t)(goffd[g] + ((ks * 16 * RBX) >> 4)), bdsc, idesc,
+            tc_mma_bf16_w(tmem + g * N, ad0 + (uint64_t)(goffd[g] + ((ks * 16 * RBX) >> 4)), bdsc, idesc,
                         accf);
-          tc_mma_bf16(tmem + NG * N, od, bdsc, idesc, accf);
+          tc_mma_bf16_w(tmem + NG * N, od, bdsc, idesc, accf);
         }
-        tc_commit(&empty[s]);
+        tc_commit_w(&empty[s]);
       }
-      tc_commit(&tfull);
+      tc_commit_w(&tfull);
     }
   } else {
     const int q = warp & 3;
@@ -422,6 +422,191 @@ seed_status launch_win_wgrad(const WinWgradArgs& a0, const Fin& fin, cudaStream_
   const int tot = a.ngroup * 128 * N + N;
   return launch_k(win_wgrad_finish<Fin>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
                   (const float*)a.part, G, N, a.ngroup, fin);
+}
+
+
+// ------------------------------------------------------------------ 3x3 weight gradient
+// All nine taps in ONE tcgen05.mma per 16 rows (M = 128, N = 3*CO):
+//   dW[ky][kx][c][co] = sum_h X[h + kx][c] * dY[h + boff + (2-ky)*bstride][co]
+// A = X rows as an MN-major operand of 256/RBX atoms (kx = atom, LBO = one row),
+// B = dY rows as an MN-major operand of 3 atoms (ky = 2 - atom, LBO = bstride rows);
+// a second MMA with an all-ones A and B atom 1 gives the bias gradient (sum of dY
+// over the same rows shifted by boff + bstride, which only moves border / zero rows).
+struct Win3WgradArgs {
+  const uint8_t* X;      // rows of RBX bytes
+  const uint8_t* dy;     // rows of 2*CO bytes
+  int64_t M;             // rows (X and dY share the row space)
+  int boff, bstride;     // B atom j starts at row h + boff + j*bstride
+  int64_t rows_per_cta;
+  float* part;           // [grid][128][4*CO] (cols [0, 3CO) weights, [3CO, 4CO) bias in row 0)
+};
+
+template <int CO, int RBX>
+__global__ void __launch_bounds__(WC_THREADS, 1)
+    win3_wgrad_kernel(const Win3WgradArgs a, int stages, int a_bytes, int b_bytes) {
+  constexpr int RBY = 2 * CO;
+  constexpr int NA = 256 / RBX;           // A atoms per M = 128
+  constexpr int NW = 3 * CO;              // weight columns
+  constexpr uint32_t LA = swz_layout_code(RBX), LB = swz_layout_code(RBY);
+  constexpr uint32_t TCOLS = 4 * CO <= 64 ? 64 : 128;
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* ones = sm;
+  uint8_t* stg = sm + 1024;
+  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t r_end = std::min<int64_t>(a.M, r_begin + a.rows_per_cta);
+  const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
+  const int arows = WG_KS + NA - 1, brows = WG_KS + 2 * a.bstride;
+  for (int i = threadIdx.x; i < 64; i += blockDim.x)
+    reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&tbase, TCOLS);
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tmem = tbase;
+  if (warp == 0) {
+    for (int it = 0; it < nks; ++it) {
+      const int s = it % stages;
+      mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+      const int64_t k0 = r_begin + (int64_t)it * WG_KS;
+      uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
+      // rows_per_cta is a multiple of WG_KS, so only the last CTA has a partial last
+      // stage, and there every K index h >= M reads X rows >= M (zero-filled)
+      const int64_t lo = std::max<int64_t>(k0 + a.boff, 0),
+                    hi = std::min<int64_t>(k0 + a.boff + brows, a.M);
+      const uint32_t bbytes = hi > lo ? (uint32_t)((hi - lo) * RBY) : 0u;
+      // B: zero the out-of-range rows, then one bulk copy (credited via A's expect_tx)
+      uint8_t* bd = sa + a_bytes + slab_phase(k0 + a.boff, RBY);
+      const int zlo = (int)std::min<int64_t>(std::max<int64_t>(lo - (k0 + a.boff), 0), brows);
+      const int zhi = hi > lo ? (int)(hi - (k0 + a.boff)) : zlo;
+      if (zlo > 0 || zhi < brows) {
+        zero_rows(bd, RBY, 0, zlo, lane);
+        zero_rows(bd, RBY, zhi, brows, lane);
+        fence_proxy_async_smem();
+      }
+      __syncwarp();
+      load_slab(sa, a.X, RBX, k0, arows, a.M, &full[s], lane, bbytes);
+      if (lane == 0 && bbytes) bulk_g2s(smem_u32(bd + zlo * RBY), a.dy + lo * RBY, bbytes, &full[s]);
+    }
+  } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
+    const uint32_t idesc = umma_idesc_bf16(128, NW, true, true);
+    const uint32_t idesc_b = umma_idesc_bf16(128, CO, true, true);
+    const uint64_t od = umma_desc(smem_u32(ones), 0, 0, 2);
+    const uint32_t blbo = (uint32_t)(a.bstride * RBY);
+    for (int it = 0; it < nks; ++it) {
+      const int s = it % stages;
+      mbar_wait(&full[s], (it / stages) & 1);
+      tc_fence_after();
+      const int64_t k0 = r_begin + (int64_t)it * WG_KS;
+      uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
+      const uint64_t ad0 = umma_desc(smem_u32(sa) + slab_phase(k0, RBX), RBX, 8 * RBX, LA);
+      const uint64_t bd0 =
+          umma_desc(smem_u32(sa + a_bytes) + slab_phase(k0 + a.boff, RBY), blbo, 8 * RBY, LB);
+      const uint64_t bd1 = bd0 + (uint64_t)(blbo >> 4);
+      const uint32_t acc0 = it != 0;
+#pragma unroll
+      for (int ks = 0; ks < WG_KS / 16; ++ks) {
+        const uint32_t accf = acc0 | (ks != 0);
+        tc_mma_bf16_w(tmem, ad0 + (uint64_t)((ks * 16 * RBX) >> 4), bd0 + (uint64_t)((ks * 16 * RBY) >> 4),
+                      idesc, accf);
+        tc_mma_bf16_w(tmem + NW, od, bd1 + (uint64_t)((ks * 16 * RBY) >> 4), idesc_b, accf);
+      }
+      tc_commit_w(&empty[s]);
+    }
+    tc_commit_w(&tfull);
+  } else {
+    const int q = warp & 3;
+    float* part = a.part + (size_t)blockIdx.x * 128 * 4 * CO;
+    const int row = q * 32 + lane;
+    if (nks > 0) {
+      mbar_wait(&tfull, 0);
+      tc_fence_after();
+    }
+#pragma unroll
+    for (int c0 = 0; c0 < 4 * CO; c0 += 16) {
+      float v[16];
+      if (nks > 0) {
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = 0.f;
+      }
+      if (c0 < NW || row == 0) {
+        float4* dst = reinterpret_cast<float4*>(part + (size_t)row * 4 * CO + c0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TCOLS);
+  }
+}
+
+// fixed-order sum; output o < 128*3CO: (row i, col n) -> Fin::weight3(i, n, v);
+// o >= 128*3CO: bias column -> Fin::bias
+template <int CO, class Fin>
+__global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict__ part, int G,
+                                                         const Fin f) {
+  pdl_wait();
+  constexpr int NW = 3 * CO;
+  const int tot = 128 * NW + CO;
+  const int o = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
+  __shared__ float sh[8][33];
+  float s = 0.f;
+  size_t idx = 0;
+  if (o < tot) {
+    idx = o < 128 * NW ? (size_t)(o / NW) * 4 * CO + (o % NW) : (size_t)NW + (o - 128 * NW);
+    for (int z = g; z < G; z += 8) s += part[(size_t)z * 128 * 4 * CO + idx];
+  }
+  sh[g][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (g == 0 && o < tot) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x & 31];
+    if (o >= 128 * NW) f.bias(o - 128 * NW, t);
+    else f.weight3(o / NW, o % NW, t);
+  }
+}
+
+inline size_t win3_wgrad_part_bytes(int64_t M, int CO) {
+  int64_t r;
+  return (size_t)wgrad_grid(M, &r) * 128 * 4 * CO * 4;
+}
+
+template <int CO, int RBX, class Fin>
+seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, cudaStream_t st) {
+  Win3WgradArgs a = a0;
+  const int G = wgrad_grid(a.M, &a.rows_per_cta);
+  const int a_bytes = (int)align_up((size_t)(WG_KS + 256 / RBX - 1) * RBX + 1024, 1024);
+  const int b_bytes = (int)align_up((size_t)(WG_KS + 2 * a.bstride) * 2 * CO + 1024, 1024);
+  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes));
+  if (stages < 2) return SEED_E_SHAPE;
+  const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);
+  static bool attr = false;
+  if (!attr) {
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
+    attr = true;
+  }
+  SEED_TRY(launch_k(win3_wgrad_kernel<CO, RBX>, dim3(G), dim3(WC_THREADS), smem, st, a, stages, a_bytes,
+                    b_bytes));
+  const int tot = 128 * 3 * CO + CO;
+  return launch_k(win3_wgrad_finish<CO, Fin>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
+                  (const float*)a.part, G, fin);
 }
 
 }  // namespace seed
