@@ -205,6 +205,9 @@ struct W3Fin3 {
     const int ky = 2 - n / CO, co = n % CO;
     int kx, c;
     if (xim) {
+      // channel 3*CI of the x-im2col input is constant 1 (conv3_obs_kernel): its
+      // row of the accumulator against tap ky = 1 (dY unshifted) is the bias gradient
+      if (atom == 0 && ch == 3 * CI && ky == 1) g_b[co] = t;
       if (atom != 0 || ch >= 3 * CI) return;
       kx = ch / CI; c = ch % CI;
     } else {
@@ -226,10 +229,10 @@ seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
   W3Fin3 f{};
   f.xim = a.xim ? 1 : 0; f.Cp = a.cin_p; f.CI = a.cin; f.CO = a.ch; f.scale = a.scale; f.g_w = a.g_w;
   f.g_b = a.g_b;
-  if (a.ch == 16 && a.cin_p == 16) return launch_win3_wgrad<16, 32>(w, f, st);
-  if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, st);
-  if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, st);
-  if (a.ch == 32 && a.cin_p == 32) return launch_win3_wgrad<32, 64>(w, f, st);
+  if (a.ch == 16 && a.cin_p == 16) return launch_win3_wgrad<16, 32>(w, f, !a.xim, st);
+  if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, !a.xim, st);
+  if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, !a.xim, st);
+  if (a.ch == 32 && a.cin_p == 32) return launch_win3_wgrad<32, 64>(w, f, !a.xim, st);
   return SEED_E_UNSUPPORTED;
 }
 
@@ -237,6 +240,7 @@ seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
 // grid.x = one padded image row (f, Y) of the output space, grid.y * blockDim.x
 // threads over (X, chunk j): no per-thread divisions beyond constant shifts.
 constexpr int ROWK_THREADS = 128;
+constexpr int ROWK_RPB = 8;   // padded rows per block (grid.x = F * ceil(Hp / RPB))
 
 // obs conversion: thread = (X, chunk of 8 channels)
 template <int NC, int CX>   // chunks per row; CX = compile-time C for the x-im2col path (0 = runtime)
@@ -247,9 +251,10 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3_obs_kernel(
   const int t = blockIdx.y * ROWK_THREADS + threadIdx.x;
   if (t >= g.Wp * NC) return;
   const int X = t / NC, j = t % NC;
-  const int Hp = g.H + 2;
-  const int f = blockIdx.x / Hp, Y = blockIdx.x - f * Hp;
-  const int64_t m = (int64_t)blockIdx.x * g.Wp + X;
+  const int Hp = g.H + 2, nb = (Hp + ROWK_RPB - 1) / ROWK_RPB;
+  const int f = blockIdx.x / nb, Y0 = (blockIdx.x - f * nb) * ROWK_RPB;
+  for (int Y = Y0; Y < min(Y0 + ROWK_RPB, Hp); ++Y) {
+  const int64_t m = ((int64_t)f * Hp + Y) * g.Wp + X;
   const int y = Y - 1, x = X - 1;
   float v[8];
 #pragma unroll
@@ -275,14 +280,23 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3_obs_kernel(
       }
     }
   }
+  // x-im2col: channel 3C is constant 1 (its weights are zero in the forward image;
+  // the weight-gradient accumulator turns it into the bias gradient, W3Fin3)
+  if (xim) {
+    const int Cr = CX ? CX : C;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (8 * j + k == 3 * Cr) v[k] = 1.f;
+  }
   *chunk_at(X0, m, RB, j) = pack8(v);
+  }
 }
 
 seed_status conv3_obs(const uint8_t* obs, int64_t F, const PadGeo& g, int C, int Cp, bool xim,
                       uint8_t* X0, cudaStream_t st) {
   if (F == 0) return SEED_OK;
   const int NC = Cp / 8;
-  const dim3 grid((unsigned)(F * (g.H + 2)), (unsigned)ceil_div(g.Wp * NC, ROWK_THREADS));
+  const dim3 grid((unsigned)(F * ceil_div(g.H + 2, ROWK_RPB)), (unsigned)ceil_div(g.Wp * NC, ROWK_THREADS));
   if (NC == 2) {
     if (xim && C == 3) return launch_k(conv3_obs_kernel<2, 3>, grid, dim3(ROWK_THREADS), 0, st, g, C, 1, obs, X0);
     return launch_k(conv3_obs_kernel<2, 0>, grid, dim3(ROWK_THREADS), 0, st, g, C, xim ? 1 : 0, obs, X0);
@@ -302,15 +316,16 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
   const int t = blockIdx.y * ROWK_THREADS + threadIdx.x;
   if (t >= go.Wp * NC) return;
   const int X = t / NC, j = t % NC;
-  const int Hp = go.H + 2;
-  const int f = blockIdx.x / Hp, Y = blockIdx.x - f * Hp;
-  const int64_t m = (int64_t)blockIdx.x * go.Wp + X;
+  const int Hp = go.H + 2, nb = (Hp + ROWK_RPB - 1) / ROWK_RPB;
+  const int f = blockIdx.x / nb, Y0 = (blockIdx.x - f * nb) * ROWK_RPB;
+  for (int Y = Y0; Y < min(Y0 + ROWK_RPB, Hp); ++Y) {
+  const int64_t m = ((int64_t)f * Hp + Y) * go.Wp + X;
   const int oy = Y - 1, ox = X - 1;
   if (oy < 0 || oy >= go.H || ox < 0 || ox >= go.W) {
     const uint4 z = make_uint4(0, 0, 0, 0);
     *chunk_at(h0, m, RB, j) = z;
     *chunk_at(hr0, m, RB, j) = z;
-    return;
+    continue;
   }
   uint4 in[9];
   const int64_t fb = (int64_t)f * gi.P;
@@ -321,31 +336,36 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
     in[q] = ok ? __ldg(chunk_at(conv, fb + (int64_t)(y + 1) * gi.Wp + (x + 1), RB, j))
                : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);   // -inf
   }
-  float best[8];
-  uint32_t barg[8];
-  unpack8(in[0], best);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) barg[k] = 0;
+  // packed bf16x2: v > best per half (strict: the first maximum in (ky, kx) order
+  // wins), best / argmax selected through the 16-bit lane masks
+  uint32_t best[4] = {in[0].x, in[0].y, in[0].z, in[0].w};
+  uint32_t barg[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int q = 1; q < 9; ++q) {
-    float v[8];
-    unpack8(in[q], v);
+    const uint32_t v[4] = {in[q].x, in[q].y, in[q].z, in[q].w};
+    const uint32_t qq = (uint32_t)q * 0x00010001u;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (v[k] > best[k]) {   // strict: the first maximum in (ky, kx) order wins
-        best[k] = v[k];
-        barg[k] = q;
-      }
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t gt = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&v[p]),
+                                      *reinterpret_cast<const __nv_bfloat162*>(&best[p]));
+      best[p] = (v[p] & gt) | (best[p] & ~gt);
+      barg[p] = (qq & gt) | (barg[p] & ~gt);
+    }
   }
-  float r[8];
+  uint32_t rl[4];
+  const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) r[k] = fmaxf(best[k], 0.f);
-  *chunk_at(h0, m, RB, j) = pack8(best);
-  *chunk_at(hr0, m, RB, j) = pack8(r);
+  for (int p = 0; p < 4; ++p) {
+    const __nv_bfloat162 r2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&best[p]), zero2);
+    rl[p] = *reinterpret_cast<const uint32_t*>(&r2);
+  }
+  *chunk_at(h0, m, RB, j) = make_uint4(best[0], best[1], best[2], best[3]);
+  *chunk_at(hr0, m, RB, j) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
   uint2 a;
-  a.x = barg[0] | (barg[1] << 8) | (barg[2] << 16) | (barg[3] << 24);
-  a.y = barg[4] | (barg[5] << 8) | (barg[6] << 16) | (barg[7] << 24);
+  a.x = __byte_perm(barg[0], barg[1], 0x6420);
+  a.y = __byte_perm(barg[2], barg[3], 0x6420);
   *reinterpret_cast<uint2*>(arg + m * C + 8 * j) = a;
+  }
 }
 
 template <int NC>
@@ -357,9 +377,10 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_bwd_kernel(
   const int t = blockIdx.y * ROWK_THREADS + threadIdx.x;
   if (t >= gi.Wp * NC) return;
   const int X = t / NC, j = t % NC;
-  const int Hp = gi.H + 2;
-  const int f = blockIdx.x / Hp, Y = blockIdx.x - f * Hp;
-  const int64_t m = (int64_t)blockIdx.x * gi.Wp + X;
+  const int Hp = gi.H + 2, nb = (Hp + ROWK_RPB - 1) / ROWK_RPB;
+  const int f = blockIdx.x / nb, Y0 = (blockIdx.x - f * nb) * ROWK_RPB;
+  for (int Y = Y0; Y < min(Y0 + ROWK_RPB, Hp); ++Y) {
+  const int64_t m = ((int64_t)f * Hp + Y) * gi.Wp + X;
   const int y = Y - 1, x = X - 1;
   float s[8];
 #pragma unroll
@@ -383,17 +404,22 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_bwd_kernel(
       dv[q] = ok ? __ldg(chunk_at(dout, o, RB, j)) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float d[8];
-      unpack8(dv[q], d);
+    for (int q = 0; q < 4; ++q) {   // per-byte argmax match -> 16-bit lane masks on the bf16 pairs
+      const uint32_t w4 = want[q] * 0x01010101u;
+      const uint32_t mx = __vcmpeq4(av[q].x, w4), my = __vcmpeq4(av[q].y, w4);
+      const uint32_t mk[4] = {__byte_perm(mx, 0, 0x1100), __byte_perm(mx, 0, 0x3322),
+                              __byte_perm(my, 0, 0x1100), __byte_perm(my, 0, 0x3322)};
+      const uint32_t dw[4] = {dv[q].x, dv[q].y, dv[q].z, dv[q].w};
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t ak = ((k < 4 ? av[q].x : av[q].y) >> (8 * (k & 3))) & 0xFF;
-        if (ak == want[q]) s[k] += d[k];
+      for (int p = 0; p < 4; ++p) {
+        const uint32_t d = dw[p] & mk[p];
+        s[2 * p] += bf16_lo(d);
+        s[2 * p + 1] += bf16_hi(d);
       }
     }
   }
   *chunk_at(din, m, RB, j) = pack8(s);
+  }
 }
 
 seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
@@ -401,7 +427,7 @@ seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
                             cudaStream_t st) {
   if (F == 0) return SEED_OK;
   const int NC = C / 8;
-  const dim3 grid((unsigned)(F * (go.H + 2)), (unsigned)ceil_div(go.Wp * NC, ROWK_THREADS));
+  const dim3 grid((unsigned)(F * ceil_div(go.H + 2, ROWK_RPB)), (unsigned)ceil_div(go.Wp * NC, ROWK_THREADS));
   if (NC == 2)
     return launch_k(conv3w_pool_fwd_kernel<2>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, conv, h0, hr0, arg);
   if (NC == 4)
@@ -414,7 +440,7 @@ seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
                             cudaStream_t st) {
   if (F == 0) return SEED_OK;
   const int NC = C / 8;
-  const dim3 grid((unsigned)(F * (gi.H + 2)), (unsigned)ceil_div(gi.Wp * NC, ROWK_THREADS));
+  const dim3 grid((unsigned)(F * ceil_div(gi.H + 2, ROWK_RPB)), (unsigned)ceil_div(gi.Wp * NC, ROWK_THREADS));
   if (NC == 2)
     return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, dout, arg, din);
   if (NC == 4)

@@ -441,7 +441,7 @@ struct Win3WgradArgs {
   float* part;           // [grid][128][4*CO] (cols [0, 3CO) weights, [3CO, 4CO) bias in row 0)
 };
 
-template <int CO, int RBX>
+template <int CO, int RBX, bool BIAS>
 __global__ void __launch_bounds__(WC_THREADS, 1)
     win3_wgrad_kernel(const Win3WgradArgs a, int stages, int a_bytes, int b_bytes) {
   constexpr int RBY = 2 * CO;
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
         const uint32_t accf = acc0 | (ks != 0);
         tc_mma_bf16_w(tmem, ad0 + (uint64_t)((ks * 16 * RBX) >> 4), bd0 + (uint64_t)((ks * 16 * RBY) >> 4),
                       idesc, accf);
-        tc_mma_bf16_w(tmem + NW, od, bd1 + (uint64_t)((ks * 16 * RBY) >> 4), idesc_b, accf);
+        if (BIAS) tc_mma_bf16_w(tmem + NW, od, bd1 + (uint64_t)((ks * 16 * RBY) >> 4), idesc_b, accf);
       }
       tc_commit_w(&empty[s]);
     }
@@ -559,10 +559,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
 // o >= 128*3CO: bias column -> Fin::bias
 template <int CO, class Fin>
 __global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict__ part, int G,
-                                                         const Fin f) {
+                                                         int tot, const Fin f) {
   pdl_wait();
   constexpr int NW = 3 * CO;
-  const int tot = 128 * NW + CO;
   const int o = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
   __shared__ float sh[8][33];
   float s = 0.f;
@@ -587,8 +586,10 @@ inline size_t win3_wgrad_part_bytes(int64_t M, int CO) {
   return (size_t)wgrad_grid(M, &r) * 128 * 4 * CO * 4;
 }
 
+// bias = false: no all-ones MMA (the bias gradient is a column of the weight
+// accumulator, e.g. from a constant-1 input channel)
 template <int CO, int RBX, class Fin>
-seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, cudaStream_t st) {
+seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias, cudaStream_t st) {
   Win3WgradArgs a = a0;
   const int G = wgrad_grid(a.M, &a.rows_per_cta);
   const int a_bytes = (int)align_up((size_t)(WG_KS + 256 / RBX - 1) * RBX + 1024, 1024);
@@ -598,15 +599,17 @@ seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, cudaStrea
   const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);
   static bool attr = false;
   if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX>,
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
     attr = true;
   }
-  SEED_TRY(launch_k(win3_wgrad_kernel<CO, RBX>, dim3(G), dim3(WC_THREADS), smem, st, a, stages, a_bytes,
-                    b_bytes));
-  const int tot = 128 * 3 * CO + CO;
+  SEED_TRY(launch_k(bias ? win3_wgrad_kernel<CO, RBX, true> : win3_wgrad_kernel<CO, RBX, false>, dim3(G),
+                    dim3(WC_THREADS), smem, st, a, stages, a_bytes, b_bytes));
+  const int tot = 128 * 3 * CO + (bias ? CO : 0);
   return launch_k(win3_wgrad_finish<CO, Fin>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
-                  (const float*)a.part, G, fin);
+                  (const float*)a.part, G, tot, fin);
 }
 
 }  // namespace seed
