@@ -368,58 +368,81 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
   }
 }
 
+// Backward: thread = (frame, 2x2 block of input pixels (y + pt, x + pl) in
+// {2a, 2a+1} x {2b, 2b+1}, chunk j).  The block's pixels receive gradient only from
+// the 2x2 windows (a-1 | a) x (b-1 | b): an even offset is tap 2 of window a-1 and
+// tap 0 of window a, an odd offset tap 1 of window a.  The four windows' (argmax,
+// dout) are loaded once for the four pixels; sums in ascending window order.
 template <int NC>
 __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_bwd_kernel(
-    PadGeo gi, PadGeo go, int pt, int pl, const uint8_t* __restrict__ dout,
+    PadGeo gi, PadGeo go, int pt, int pl, int nbx, const uint8_t* __restrict__ dout,
     const uint8_t* __restrict__ arg, uint8_t* __restrict__ din) {
   pdl_wait();
   constexpr int C = NC * 8, RB = NC * 16;
   const int t = blockIdx.y * ROWK_THREADS + threadIdx.x;
-  if (t >= gi.Wp * NC) return;
-  const int X = t / NC, j = t % NC;
-  const int Hp = gi.H + 2, nb = (Hp + ROWK_RPB - 1) / ROWK_RPB;
-  const int f = blockIdx.x / nb, Y0 = (blockIdx.x - f * nb) * ROWK_RPB;
-  for (int Y = Y0; Y < min(Y0 + ROWK_RPB, Hp); ++Y) {
-  const int64_t m = ((int64_t)f * Hp + Y) * gi.Wp + X;
-  const int y = Y - 1, x = X - 1;
-  float s[8];
+  if (t >= nbx * NC) return;
+  const int b = t / NC, j = t % NC;
+  const int nby = (gi.H + pt + 1) >> 1;
+  const int f = blockIdx.x / nby, a = blockIdx.x - f * nby;
+  const int64_t fo = (int64_t)f * go.P, fi = (int64_t)f * gi.P;
+  uint2 av[4];
+  uint4 dv[4];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) s[k] = 0.f;
-  if (y >= 0 && y < gi.H && x >= 0 && x < gi.W) {
-    // windows (oy, ox) with oy*2 - pt <= y <= oy*2 - pt + 2, in ascending order
-    const int oy_hi = (y + pt) >> 1, ox_hi = (x + pl) >> 1;
-    const int64_t fb = (int64_t)f * go.P;
-    uint2 av[4];
-    uint4 dv[4];
-    uint32_t want[4];
+  for (int q = 0; q < 4; ++q) {   // windows (a-1, b-1), (a-1, b), (a, b-1), (a, b)
+    const int oy = a - 1 + (q >> 1), ox = b - 1 + (q & 1);
+    const bool ok = oy >= 0 && oy < go.H && ox >= 0 && ox < go.W;
+    const int64_t o = fo + (int64_t)(oy + 1) * go.Wp + (ox + 1);
+    av[q] = ok ? __ldg(reinterpret_cast<const uint2*>(arg + o * C + 8 * j)) : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+    dv[q] = ok ? __ldg(chunk_at(dout, o, RB, j)) : make_uint4(0, 0, 0, 0);
+  }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {   // issue all loads first
-      const int oy = oy_hi - 1 + (q >> 1), ox = ox_hi - 1 + (q & 1);
-      const int ky = y - (oy * 2 - pt), kx = x - (ox * 2 - pl);
-      const bool ok = oy >= 0 && oy < go.H && ky >= 0 && ky <= 2 && ox >= 0 && ox < go.W && kx >= 0 &&
-                      kx <= 2;
-      want[q] = ok ? (uint32_t)(ky * 3 + kx) : 0xFFu;
-      const int64_t o = fb + (int64_t)(oy + 1) * go.Wp + (ox + 1);
-      av[q] = ok ? __ldg(reinterpret_cast<const uint2*>(arg + o * C + 8 * j)) : make_uint2(0, 0);
-      dv[q] = ok ? __ldg(chunk_at(dout, o, RB, j)) : make_uint4(0, 0, 0, 0);
-    }
+  for (int p = 0; p < 4; ++p) {
+    const int dy = p >> 1, dx = p & 1;
+    const int y = 2 * a + dy - pt, x = 2 * b + dx - pl;
+    if (y < 0 || y >= gi.H || x < 0 || x >= gi.W) continue;
+    float s[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {   // per-byte argmax match -> 16-bit lane masks on the bf16 pairs
-      const uint32_t w4 = want[q] * 0x01010101u;
+    for (int k = 0; k < 8; ++k) s[k] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int wy = q >> 1, wx = q & 1;   // window a-1+wy, b-1+wx
+      // tap of this pixel in that window: even offset -> 2 (wy = 0) / 0 (wy = 1); odd -> 1 (wy = 1 only)
+      const int ky = dy == 0 ? (wy == 0 ? 2 : 0) : (wy == 1 ? 1 : -1);
+      const int kx = dx == 0 ? (wx == 0 ? 2 : 0) : (wx == 1 ? 1 : -1);
+      if (ky < 0 || kx < 0) continue;
+      const uint32_t w4 = (uint32_t)(ky * 3 + kx) * 0x01010101u;
       const uint32_t mx = __vcmpeq4(av[q].x, w4), my = __vcmpeq4(av[q].y, w4);
       const uint32_t mk[4] = {__byte_perm(mx, 0, 0x1100), __byte_perm(mx, 0, 0x3322),
                               __byte_perm(my, 0, 0x1100), __byte_perm(my, 0, 0x3322)};
       const uint32_t dw[4] = {dv[q].x, dv[q].y, dv[q].z, dv[q].w};
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const uint32_t d = dw[p] & mk[p];
-        s[2 * p] += bf16_lo(d);
-        s[2 * p + 1] += bf16_hi(d);
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t d = dw[r] & mk[r];
+        s[2 * r] += bf16_lo(d);
+        s[2 * r + 1] += bf16_hi(d);
       }
     }
+    *chunk_at(din, fi + (int64_t)(y + 1) * gi.Wp + (x + 1), RB, j) = pack8(s);
   }
-  *chunk_at(din, m, RB, j) = pack8(s);
-  }
+}
+
+// zero the border rows of a padded row space (per frame: top / bottom rows, and
+// the left / right pixels of the interior rows)
+template <int NC>
+__global__ void __launch_bounds__(ROWK_THREADS) zero_border_kernel(int64_t n, PadGeo g, uint8_t* __restrict__ buf) {
+  pdl_wait();
+  constexpr int RB = NC * 16;
+  const int64_t i = blockIdx.x * (int64_t)ROWK_THREADS + threadIdx.x;
+  if (i >= n) return;
+  const int j = (int)(i % NC);
+  const int64_t r = i / NC;
+  const int per = 2 * g.Wp + 2 * g.H;
+  const int64_t f = r / per;
+  const int k = (int)(r - f * per);
+  int Y, X;
+  if (k < 2 * g.Wp) { Y = k < g.Wp ? 0 : g.H + 1; X = k % g.Wp; }
+  else { Y = 1 + (k - 2 * g.Wp) / 2; X = ((k - 2 * g.Wp) & 1) ? g.W + 1 : 0; }
+  *chunk_at(buf, f * g.P + (int64_t)Y * g.Wp + X, RB, j) = make_uint4(0, 0, 0, 0);
 }
 
 seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
@@ -440,11 +463,20 @@ seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
                             cudaStream_t st) {
   if (F == 0) return SEED_OK;
   const int NC = C / 8;
-  const dim3 grid((unsigned)(F * ceil_div(gi.H + 2, ROWK_RPB)), (unsigned)ceil_div(gi.Wp * NC, ROWK_THREADS));
-  if (NC == 2)
-    return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, dout, arg, din);
-  if (NC == 4)
-    return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, dout, arg, din);
+  const int nby = (gi.H + pt + 1) >> 1, nbx = (gi.W + pl + 1) >> 1;
+  const dim3 grid((unsigned)(F * nby), (unsigned)ceil_div(nbx * NC, ROWK_THREADS));
+  const int64_t nz = F * (2 * gi.Wp + 2 * gi.H) * NC;
+  const dim3 gz((unsigned)((nz + ROWK_THREADS - 1) / ROWK_THREADS));
+  if (NC == 2) {
+    SEED_TRY(launch_k(zero_border_kernel<2>, gz, dim3(ROWK_THREADS), 0, st, nz, gi, din));
+    return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, nbx, dout,
+                    arg, din);
+  }
+  if (NC == 4) {
+    SEED_TRY(launch_k(zero_border_kernel<4>, gz, dim3(ROWK_THREADS), 0, st, nz, gi, din));
+    return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, nbx, dout,
+                    arg, din);
+  }
   return SEED_E_UNSUPPORTED;
 }
 

@@ -369,7 +369,7 @@ static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const b
     // max-pool backward into dconv, then the section conv
     SEED_TRY(conv3w_pool_bwd(F, gi, go, d.ch, d.pt, d.pl, c.at<uint8_t>(cur), c.at<uint8_t>(b.arg),
                              c.at<uint8_t>(b.dconv), st));
-    c.mark("deep_pool_bwd");
+    c.mark("deep_pool_bwd", 2);
     Conv3wWgrad wg{};
     wg.cin_p = d.cinp; wg.cin = d.cin; wg.ch = d.ch; wg.xim = d.xim; wg.g = gi; wg.rows = F * gi.P;
     wg.scale = s == 0 ? 1.f / 255.f : 1.f;
