@@ -130,17 +130,23 @@ struct W3Fin {
 };
 
 // ------------------------------------------------------------------ forward
+// 128-row blocks per window-conv tile (measured per shape, scripts/phases.py
+// PER_LAUNCH=1 at MT = 1 / 2 / 4): 16-channel outputs 4; 32-channel 2, residual
+// forward 1 (its epilogue reads a second input row and writes two)
+template <int MODE, int N, bool FWD>
+constexpr int w3_mt() { return N == 16 ? 4 : (FWD && MODE == W3_RES) ? 1 : 2; }
+// NW = 9: 3 x 3 taps as row windows; NW = 3: x-im2col input, 3 row windows (ky)
 template <int MODE, int N, int RB, int NW>
 static seed_status fwd_t(const Conv3wFwd& a, cudaStream_t st) {
   WinConvArgs w{};
   w.src = a.in; w.src_rows = a.rows; w.M = a.rows;
   w.wimg = reinterpret_cast<const uint8_t*>(a.wimg);
-  for (int k = 0; k < NW; ++k)
-    w.off[k] = NW == 9 ? ((k / 3) - 1) * a.g.Wp + (k % 3) - 1 : (k - 1) * a.g.Wp;
   W3FwdEpi<MODE, N> e{};
   e.g = a.g; e.in_scale = a.in_scale; e.bias = a.bias; e.res = a.res; e.out = a.out;
   e.outr = a.outr; e.dense = a.dense;
-  return launch_win_conv<W3FwdEpi<MODE, N>, RB, NW>(w, e, st);
+  for (int k = 0; k < NW; ++k)
+    w.off[k] = NW == 9 ? ((k / 3) - 1) * a.g.Wp + (k % 3) - 1 : (k - 1) * a.g.Wp;
+  return launch_win_conv<W3FwdEpi<MODE, N>, RB, NW, w3_mt<MODE, N, true>()>(w, e, st);
 }
 
 template <int MODE>
@@ -169,10 +175,13 @@ static seed_status dgrad_t(const Conv3wDgrad& a, cudaStream_t st) {
   WinConvArgs w{};
   w.src = a.dY; w.src_rows = a.rows; w.M = a.rows;
   w.wimg = reinterpret_cast<const uint8_t*>(a.wimg);
-  for (int k = 0; k < 9; ++k) w.off[k] = -(((k / 3) - 1) * a.g.Wp + (k % 3) - 1);
+  // row windows ky at -(ky-1)*Wp; the image stacks the column taps as groups 2 - kx
+  // (win3_img_pos mode 1), so out[g] = D[g-1][grp 0] + D[g][grp 1] + D[g+1][grp 2]
   W3DgradEpi<MODE, N> e{};
   e.g = a.g; e.mask = a.mask; e.dres = a.dres; e.dX = a.dX;
-  return launch_win_conv<W3DgradEpi<MODE, N>, RB, 9>(w, e, st);
+  // 9 windows: tap (ky, kx) at -((ky-1)*Wp + kx-1), image row block ky*3 + 2 - kx
+  for (int k = 0; k < 9; ++k) w.off[k] = -(((k / 3) - 1) * a.g.Wp + 1 - (k % 3));
+  return launch_win_conv<W3DgradEpi<MODE, N>, RB, 9, w3_mt<MODE, N, false>()>(w, e, st);
 }
 
 template <int MODE>

@@ -120,8 +120,8 @@ seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
                             cudaStream_t st);
 
 // bf16 weight-image element position of source element e of W[CO][3][3][CI]
-// (net.cuh IMG_WIN3: d0 = mode 0 forward [9][CO][RB] / 1 data gradient [9][CI][RB]
-// / 2 x-im2col forward [3][CO][RB]; d1 = CI, d2 = CO, d3 = RB bytes)
+// (net.cuh IMG_WIN3: d0 = mode 0 forward [ky][kx][CO][RB] / 1 data gradient
+// [ky][2-kx][CI][RB] / 2 x-im2col forward [ky][CO][RB]; d1 = CI, d2 = CO, d3 = RB bytes)
 __host__ __device__ inline int64_t win3_img_pos(int mode, int CI, int CO, int RB, int64_t e64) {
   const int e = (int)e64;
   const int c = e % CI;
@@ -131,7 +131,7 @@ __host__ __device__ inline int64_t win3_img_pos(int mode, int CI, int CO, int RB
   const int co = q / 3;
   int row, k;
   if (mode == 0) { row = (ky * 3 + kx) * CO + co; k = c; }
-  else if (mode == 1) { row = (ky * 3 + kx) * CI + c; k = co; }
+  else if (mode == 1) { row = (ky * 3 + 2 - kx) * CI + c; k = co; }   // column taps reversed
   else { row = ky * CO + co; k = kx * CI + c; }
   return (int64_t)row * (RB / 2) + swz_chunk(row, RB, k / 8) * 8 + (k % 8);
 }

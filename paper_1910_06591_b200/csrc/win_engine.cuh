@@ -108,13 +108,20 @@ __device__ __forceinline__ void load_slab(uint8_t* slab, const uint8_t* src, int
 
 // ------------------------------------------------------------------ forward / dgrad
 // Epi: static constexpr int N; __device__ void store(int64_t m, float (&v)[N]) const
-template <class Epi, int RB, int NW>
+// A tile is MT x 128 output rows: one slab of MT*128 + (max off - min off) rows, MT
+// accumulators of N columns (bigger tiles re-read fewer halo rows from L2 and pay
+// the per-tile barrier / commit latency once per MT blocks).
+template <class Epi, int RB, int NW, int MT = 1>
 __global__ void __launch_bounds__(WCF_THREADS, 1)
     win_conv_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes) {
   constexpr int N = Epi::N;
+  constexpr int TM = 128 * MT;
   constexpr uint32_t LAYOUT = swz_layout_code(RB);
   constexpr int WB = NW * N * RB;
-  constexpr uint32_t TCOLS = WCF_ACC * N < 32 ? 32 : WCF_ACC * N;
+  constexpr int AC = MT * N;   // TMEM columns per tile accumulator
+  constexpr uint32_t TCOLS = WCF_ACC * AC <= 32 ? 32 : WCF_ACC * AC <= 64 ? 64 : WCF_ACC * AC <= 128 ? 128
+                             : WCF_ACC * AC <= 256 ? 256 : 512;
+  static_assert(WCF_ACC * AC <= 512, "TMEM");
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
   uint8_t* Ws = sm;
@@ -125,8 +132,8 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
   int mn = a.off[0], mx = a.off[0];
 #pragma unroll
   for (int w = 1; w < NW; ++w) { mn = min(mn, a.off[w]); mx = max(mx, a.off[w]); }
-  const int nrows = 128 + mx - mn;
-  const int64_t tiles = (a.M + 127) / 128;
+  const int nrows = TM + mx - mn;
+  const int64_t tiles = (a.M + TM - 1) / TM;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int i = 0; i < WCF_ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
@@ -147,36 +154,36 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int s = it % stages;
       mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-      load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, t * 128 + mn, nrows, a.src_rows, &full[s],
+      load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, t * TM + mn, nrows, a.src_rows, &full[s],
                 lane, 0);
     }
   } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
-    {
-      mbar_wait(&wbar, 0);
-      const uint32_t idesc = umma_idesc_bf16(128, N, false, false);
-      const uint64_t bd0 = umma_desc(smem_u32(Ws), 16, 8 * RB, LAYOUT);
-      int aoff[NW];
+    mbar_wait(&wbar, 0);
+    const uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+    const uint64_t bd0 = umma_desc(smem_u32(Ws), 16, 8 * RB, LAYOUT);
+    int aoff[NW];
 #pragma unroll
-      for (int w = 0; w < NW; ++w) aoff[w] = ((a.off[w] - mn) * RB) >> 4;
-      int it = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-        const int s = it % stages, acc = it % WCF_ACC;
-        mbar_wait(&full[s], (it / stages) & 1);
-        mbar_wait(&tempty[acc], ((it / WCF_ACC) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t base =
-            smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * 128 + mn, RB);
-        // descriptors advance linearly with the start address (field = addr >> 4)
-        const uint64_t ad0 = umma_desc(base, 16, 8 * RB, LAYOUT);
+    for (int w = 0; w < NW; ++w) aoff[w] = ((a.off[w] - mn) * RB) >> 4;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int s = it % stages, acc = it % WCF_ACC;
+      mbar_wait(&full[s], (it / stages) & 1);
+      mbar_wait(&tempty[acc], ((it / WCF_ACC) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t base = smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * TM + mn, RB);
+      // descriptors advance linearly with the start address (field = addr >> 4)
+      const uint64_t ad0 = umma_desc(base, 16, 8 * RB, LAYOUT);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int w = 0; w < NW; ++w)
 #pragma unroll
           for (int ks = 0; ks < RB / 32; ++ks)
-            tc_mma_bf16_w(tmem + acc * N, ad0 + (uint64_t)(aoff[w] + ks * 2),
-                        bd0 + (uint64_t)((w * N * RB + ks * 32) >> 4), idesc, (w | ks) != 0);
-        tc_commit_w(&empty[s]);
-        tc_commit_w(&tfull[acc]);
-      }
+            tc_mma_bf16_w(tmem + acc * AC + mt * N,
+                          ad0 + (uint64_t)(aoff[w] + ((mt * 128 * RB) >> 4) + ks * 2),
+                          bd0 + (uint64_t)((w * N * RB + ks * 32) >> 4), idesc, (w | ks) != 0);
+      tc_commit_w(&empty[s]);
+      tc_commit_w(&tfull[acc]);
     }
   } else {
     const int q = warp & 3;            // TMEM lanes [32q, 32q+32) of this warp
@@ -187,15 +194,25 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
       const int acc = it % WCF_ACC;
       mbar_wait(&tfull[acc], (it / WCF_ACC) & 1);
       tc_fence_after();
-      float v[N];
+      uint32_t vr[MT][N];
 #pragma unroll
-      for (int c = 0; c < N / 16; ++c)
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * N + c * 16, v + 16 * c);
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int c = 0; c < N / 16; ++c)
+          tmem_ld16_nw(tmem + ((uint32_t)(q * 32) << 16) + acc * AC + mt * N + c * 16,
+                       *reinterpret_cast<uint32_t(*)[16]>(&vr[mt][16 * c]));
+      tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      const int64_t m = t * 128 + q * 32 + lane;
-      if (m < a.M) e.store(m, v);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        float v[N];
+#pragma unroll
+        for (int c = 0; c < N; ++c) v[c] = __uint_as_float(vr[mt][c]);
+        const int64_t m = t * TM + mt * 128 + q * 32 + lane;
+        if (m < a.M) e.store(m, v);
+      }
     }
   }
   __syncthreads();
@@ -205,12 +222,13 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
   }
 }
 
-template <class Epi, int RB, int NW>
+template <class Epi, int RB, int NW, int MT = 1>
 seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st) {
   constexpr int WB = NW * Epi::N * RB;
+  constexpr int TM = 128 * MT;
   int mn = a.off[0], mx = a.off[0];
   for (int w = 1; w < NW; ++w) { mn = std::min(mn, a.off[w]); mx = std::max(mx, a.off[w]); }
-  const int slab = (int)align_up((size_t)(128 + mx - mn) * RB + 1024, 1024);
+  const int slab = (int)align_up((size_t)(TM + mx - mn) * RB + 1024, 1024);
   const int wbytes = (int)align_up(WB, 1024);
   const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - wbytes) / slab);
   if (a.M <= 0) return a.M == 0 ? SEED_OK : SEED_E_SHAPE;
@@ -218,14 +236,14 @@ seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st)
   const size_t smem = (size_t)wbytes + (size_t)stages * slab + 1024;
   static bool attr = false;
   if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win_conv_kernel<Epi, RB, NW>,
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win_conv_kernel<Epi, RB, NW, MT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        WC_SMEM_BUDGET + 2048));
     attr = true;
   }
-  const int64_t tiles = (a.M + 127) / 128;
+  const int64_t tiles = (a.M + TM - 1) / TM;
   const int grid = (int)std::min<int64_t>(tiles, 148);
-  return launch_k(win_conv_kernel<Epi, RB, NW>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e,
+  return launch_k(win_conv_kernel<Epi, RB, NW, MT>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e,
                   stages, slab);
 }
 

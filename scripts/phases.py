@@ -73,11 +73,16 @@ for _ in range(reps):
     flush.add_(1)
     g.replay()
     torch.cuda.synchronize()
+    seen = {}
     for j in range(1, nE):
-        if pn[j] not in acc:
-            acc[pn[j]] = 0.0
-            order.append(pn[j])
-        acc[pn[j]] += evs[j - 1].elapsed_time(evs[j])
+        k = pn[j]
+        if os.environ.get("PER_LAUNCH"):
+            seen[k] = seen.get(k, 0) + 1
+            k = f"{k}#{seen[k]}"
+        if k not in acc:
+            acc[k] = 0.0
+            order.append(k)
+        acc[k] += evs[j - 1].elapsed_time(evs[j])
     tot += evs[0].elapsed_time(evs[nE - 1])
 ms = 0.0
 for _ in range(reps):
