@@ -448,8 +448,10 @@ seed_status launch_win_wgrad(const WinWgradArgs& a0, const Fin& fin, cudaStream_
 //   dW[ky][kx][c][co] = sum_h X[h + kx][c] * dY[h + boff + (2-ky)*bstride][co]
 // A = X rows as an MN-major operand of 256/RBX atoms (kx = atom, LBO = one row),
 // B = dY rows as an MN-major operand of 3 atoms (ky = 2 - atom, LBO = bstride rows);
-// a second MMA with an all-ones A and B atom 1 gives the bias gradient (sum of dY
-// over the same rows shifted by boff + bstride, which only moves border / zero rows).
+// the bias gradient (BIAS) is summed from the same B slab by the 4 epilogue warps,
+// idle during the main loop: rows h + boff + bstride (dY shifted by at most one
+// row, which only moves border / zero rows), fixed order, released to the
+// producer through the stage's empty barrier (2 arrivals: MMA commit + epilogue).
 struct Win3WgradArgs {
   const uint8_t* X;      // rows of RBX bytes
   const uint8_t* dy;     // rows of 2*CO bytes
@@ -466,10 +468,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   constexpr int NA = 256 / RBX;           // A atoms per M = 128
   constexpr int NW = 3 * CO;              // weight columns
   constexpr uint32_t LA = swz_layout_code(RBX), LB = swz_layout_code(RBY);
-  constexpr uint32_t TCOLS = 4 * CO <= 64 ? 64 : 128;
+  constexpr uint32_t TCOLS = NW <= 64 ? 64 : 128;
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* ones = sm;
   uint8_t* stg = sm + 1024;
   __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull;
   __shared__ uint32_t tbase;
@@ -478,11 +479,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   const int64_t r_end = std::min<int64_t>(a.M, r_begin + a.rows_per_cta);
   const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
   const int arows = WG_KS + NA - 1, brows = WG_KS + 2 * a.bstride;
-  for (int i = threadIdx.x; i < 64; i += blockDim.x)
-    reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-  fence_proxy_async_smem();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], BIAS ? 2 : 1); }
     mbar_init(&tfull, 1);
     fence_mbar_init();
   }
@@ -517,8 +515,6 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
     }
   } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
     const uint32_t idesc = umma_idesc_bf16(128, NW, true, true);
-    const uint32_t idesc_b = umma_idesc_bf16(128, CO, true, true);
-    const uint64_t od = umma_desc(smem_u32(ones), 0, 0, 2);
     const uint32_t blbo = (uint32_t)(a.bstride * RBY);
     for (int it = 0; it < nks; ++it) {
       const int s = it % stages;
@@ -529,14 +525,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       const uint64_t ad0 = umma_desc(smem_u32(sa) + slab_phase(k0, RBX), RBX, 8 * RBX, LA);
       const uint64_t bd0 =
           umma_desc(smem_u32(sa + a_bytes) + slab_phase(k0 + a.boff, RBY), blbo, 8 * RBY, LB);
-      const uint64_t bd1 = bd0 + (uint64_t)(blbo >> 4);
       const uint32_t acc0 = it != 0;
 #pragma unroll
       for (int ks = 0; ks < WG_KS / 16; ++ks) {
         const uint32_t accf = acc0 | (ks != 0);
         tc_mma_bf16_w(tmem, ad0 + (uint64_t)((ks * 16 * RBX) >> 4), bd0 + (uint64_t)((ks * 16 * RBY) >> 4),
                       idesc, accf);
-        if (BIAS) tc_mma_bf16_w(tmem + NW, od, bd1 + (uint64_t)((ks * 16 * RBY) >> 4), idesc_b, accf);
       }
       tc_commit_w(&empty[s]);
     }
@@ -545,12 +539,52 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
     const int q = warp & 3;
     float* part = a.part + (size_t)blockIdx.x * 128 * 4 * CO;
     const int row = q * 32 + lane;
-    if (nks > 0) {
+    const int et = threadIdx.x - 64;   // 0..127
+    if (BIAS) {
+      // thread = (chunk j of 8 channels, row phase): rows i = rp, rp + 128/NCH, ...
+      constexpr int NCH = CO / 8, RSTEP = 128 / NCH;
+      const int j = et % NCH, rp = et / NCH;
+      float bs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int it = 0; it < nks; ++it) {
+        const int s = it % stages;
+        mbar_wait(&full[s], (it / stages) & 1);
+        const int64_t k0 = r_begin + (int64_t)it * WG_KS;
+        const uint8_t* bsl = stg + (size_t)s * (a_bytes + b_bytes) + a_bytes + slab_phase(k0 + a.boff, RBY);
+#pragma unroll 4
+        for (int i = rp; i < WG_KS; i += RSTEP) {
+          const int lr = i + a.bstride;                        // slab row of dY[h + boff + bstride]
+          const int64_t g = k0 + a.boff + lr;                  // its global row (swizzle phase)
+          float v[8];
+          unpack8(*reinterpret_cast<const uint4*>(bsl + lr * RBY + (swz_chunk(g, RBY, j) << 4)), v);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) bs[k] += v[k];
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) mbar_arrive(&empty[s]);
+      }
+      // fixed-order reduction over the row phases, through shared memory (the
+      // operand ring is idle once tfull has fired)
+      if (nks > 0) {
+        mbar_wait(&tfull, 0);
+        tc_fence_after();
+      }
+      float* red = reinterpret_cast<float*>(stg);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+      for (int k = 0; k < 8; ++k) red[et * 8 + k] = bs[k];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (et < CO) {
+        const int jj = et / 8, kk = et % 8;
+        float t = 0.f;
+        for (int r = 0; r < RSTEP; ++r) t += red[(r * NCH + jj) * 8 + kk];
+        part[NW + et] = t;   // row 0, bias columns
+      }
+    } else if (nks > 0) {
       mbar_wait(&tfull, 0);
       tc_fence_after();
     }
 #pragma unroll
-    for (int c0 = 0; c0 < 4 * CO; c0 += 16) {
+    for (int c0 = 0; c0 < NW; c0 += 16) {
       float v[16];
       if (nks > 0) {
         tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
@@ -558,11 +592,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 16; ++c) v[c] = 0.f;
       }
-      if (c0 < NW || row == 0) {
-        float4* dst = reinterpret_cast<float4*>(part + (size_t)row * 4 * CO + c0);
+      float4* dst = reinterpret_cast<float4*>(part + (size_t)row * 4 * CO + c0);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-      }
+      for (int c = 0; c < 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
     tc_fence_before();
   }
