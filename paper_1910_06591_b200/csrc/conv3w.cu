@@ -301,13 +301,65 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3_obs_kernel(
   }
 }
 
+// x-im2col conversion for C = CX <= 5 (16-channel rows): thread = one padded-row
+// pixel X; its own pixel's C bytes are loaded coalesced, the x-1 / x+1 neighbours
+// come from lanes -+1 (direct loads at warp edges); channel 3C = 1 (see above).
+template <int CX>
+__global__ void __launch_bounds__(ROWK_THREADS) conv3_obs_xim_kernel(
+    PadGeo g, const uint8_t* __restrict__ obs, uint8_t* __restrict__ X0) {
+  pdl_wait();
+  const int X = blockIdx.y * ROWK_THREADS + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int Hp = g.H + 2, nb = (Hp + ROWK_RPB - 1) / ROWK_RPB;
+  const int f = blockIdx.x / nb, Y0 = (blockIdx.x - f * nb) * ROWK_RPB;
+  const int x = X - 1;
+  for (int Y = Y0; Y < min(Y0 + ROWK_RPB, Hp); ++Y) {
+    const int y = Y - 1;
+    const bool rowok = y >= 0 && y < g.H;
+    const uint8_t* pr = obs + ((size_t)f * g.H + (rowok ? y : 0)) * g.W * CX;
+    float me[CX], lf[CX], rt[CX];
+#pragma unroll
+    for (int c = 0; c < CX; ++c) me[c] = (rowok && x >= 0 && x < g.W) ? (float)__ldg(pr + x * CX + c) : 0.f;
+#pragma unroll
+    for (int c = 0; c < CX; ++c) {
+      lf[c] = __shfl_up_sync(0xffffffffu, me[c], 1);
+      rt[c] = __shfl_down_sync(0xffffffffu, me[c], 1);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < CX; ++c) lf[c] = (rowok && x - 1 >= 0 && x - 1 < g.W) ? (float)__ldg(pr + (x - 1) * CX + c) : 0.f;
+    }
+    if (lane == 31) {
+#pragma unroll
+      for (int c = 0; c < CX; ++c) rt[c] = (rowok && x + 1 >= 0 && x + 1 < g.W) ? (float)__ldg(pr + (x + 1) * CX + c) : 0.f;
+    }
+    if (X < g.Wp) {
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = 0.f;
+      const bool in = rowok && x >= 0 && x < g.W;
+      if (in) {
+#pragma unroll
+        for (int c = 0; c < CX; ++c) { v[c] = lf[c]; v[CX + c] = me[c]; v[2 * CX + c] = rt[c]; }
+      }
+      v[3 * CX] = 1.f;
+      const int64_t m = ((int64_t)f * Hp + Y) * g.Wp + X;
+      *chunk_at(X0, m, 32, 0) = pack8(v);
+      *chunk_at(X0, m, 32, 1) = pack8(v + 8);
+    }
+  }
+}
+
 seed_status conv3_obs(const uint8_t* obs, int64_t F, const PadGeo& g, int C, int Cp, bool xim,
                       uint8_t* X0, cudaStream_t st) {
   if (F == 0) return SEED_OK;
   const int NC = Cp / 8;
   const dim3 grid((unsigned)(F * ceil_div(g.H + 2, ROWK_RPB)), (unsigned)ceil_div(g.Wp * NC, ROWK_THREADS));
   if (NC == 2) {
-    if (xim && C == 3) return launch_k(conv3_obs_kernel<2, 3>, grid, dim3(ROWK_THREADS), 0, st, g, C, 1, obs, X0);
+    if (xim && C == 3) {
+      const dim3 gx((unsigned)(F * ceil_div(g.H + 2, ROWK_RPB)), (unsigned)ceil_div(g.Wp, ROWK_THREADS));
+      return launch_k(conv3_obs_xim_kernel<3>, gx, dim3(ROWK_THREADS), 0, st, g, obs, X0);
+    }
     return launch_k(conv3_obs_kernel<2, 0>, grid, dim3(ROWK_THREADS), 0, st, g, C, xim ? 1 : 0, obs, X0);
   }
   if (NC == 4 && !xim)

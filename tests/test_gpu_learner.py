@@ -335,3 +335,34 @@ def test_learner_deep_parity(cfg, B, T):
     dev = {n: np.linalg.norm(gt[n] - rt[n]) / np.linalg.norm(rt[n]) for n in gt}
     print(cfg, "grad relL2 vs emulated (end to end):", {k: f"{v:.1e}" for k, v in dev.items()})
     assert max(dev.values()) < 0.3
+
+
+@pytest.mark.parametrize("cfg,B,T", [("c3", 32, 100), ("c4", 128, 32)])
+def test_learner_deep_full_size_sampled(cfg, B, T):
+    """BASELINE.json configs[2] / configs[3] at their full sizes (the shapes bench.py
+    times: F = 3232 / 4224 frames, 23-31 M padded rows at 72x96): one learner step,
+    then the torso output of sampled frames (relu(h) of the last section, the FC
+    input, and the FC output) against the emulated oracle run on those frames alone
+    (C22), plus finite loss / gradients."""
+    S = _S()
+    spec, ospec = _spec_pair(cfg)
+    params = seedgen.glorot_params(O.param_layout(ospec), seed=31, bias_std=0.1)
+    batch = seedgen.learner_batch((ospec.obs_h, ospec.obs_w, ospec.obs_c), ospec.num_actions, B,
+                                  T, seed=32, smm=(cfg == "c4"))
+    hp = S.HParams(lam=0.95, loss_scale=1.0 / (B * T), lr=1e-4)
+    L = S.Learner(spec, T, B, params, hp)
+    m = L.step(_gpu_batch(batch))
+    torch.cuda.synchronize()
+    assert np.all(np.isfinite(m.cpu().numpy()[:5])) and float(m[5].item()) == 1.0
+    assert bool(torch.isfinite(L.grads).all())
+    F_ = B * (T + 1)
+    frames = batch["obs"].reshape((F_,) + batch["obs"].shape[2:])
+    rng = np.random.default_rng(33)
+    pick = np.sort(rng.choice(F_, 4, replace=False))
+    pick[-1] = F_ - 1                       # the last frame (end of the row space)
+    _, cache = O.torso_forward(ospec, O.unflatten(ospec, params), frames[pick], emu=True)
+    bf = torch.bfloat16
+    act2 = L.debug_buffer("act2", bf, (F_, -1)).float().cpu().numpy().astype(np.float64)
+    bf16_check(act2[pick], cache["flat"], f"{cfg} torso output (sampled frames)")
+    X = L.debug_buffer("X", bf, (F_, -1)).float().cpu().numpy().astype(np.float64)
+    bf16_check(X[pick, :256], cache["fc"], f"{cfg} fc output (sampled frames)")
