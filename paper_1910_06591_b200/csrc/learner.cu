@@ -52,6 +52,19 @@ static seed_status aux_stream(cudaStream_t same, cudaStream_t* aux, cudaEvent_t*
   return SEED_OK;
 }
 
+// DP gradient buckets (H10): 3 = LSTM+heads | FC | torso (default), 2 = core+FC | torso,
+// 1 = one allreduce at the end.  SEED_DP_BUCKETS overrides (measurement; 3 measured
+// best or equal at N=2: profiles/r01/dp_buckets_n2.txt).
+static int dp_buckets() {
+  static int b = -1;
+  if (b < 0) {
+    const char* e = getenv("SEED_DP_BUCKETS");
+    b = e ? atoi(e) : 3;
+    if (b < 1 || b > 3) b = 3;
+  }
+  return b;
+}
+
 struct Trace {
   void** events = nullptr;
   const char** names = nullptr;
@@ -214,7 +227,7 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
     SEED_TRY(gemm<128>(c, pr, ax, "lstm_wgrad"));
   }
   // LSTM + heads gradients are final: first DP bucket
-  SEED_TRY(cc.bucket(grads + p.t[p.i_wx].off, p.P - p.t[p.i_wx].off, ax));
+  if (dp_buckets() >= 3) SEED_TRY(cc.bucket(grads + p.t[p.i_wx].off, p.P - p.t[p.i_wx].off, ax));
   {
     DxFc pr{};
     pr.M = F; pr.N = 256; pr.K = 4 * U; pr.Kxp = p.Kxp;
@@ -232,7 +245,8 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
     SEED_TRY(gemm<128>(c, pr, ax, "fc_wgrad"));
   }
   // FC gradients final: second bucket
-  SEED_TRY(cc.bucket(grads + p.t[p.i_fcw].off, p.t[p.i_wx].off - p.t[p.i_fcw].off, ax));
+  if (dp_buckets() >= 3) SEED_TRY(cc.bucket(grads + p.t[p.i_fcw].off, p.t[p.i_wx].off - p.t[p.i_fcw].off, ax));
+  else if (dp_buckets() == 2) SEED_TRY(cc.bucket(grads + p.t[p.i_fcw].off, p.P - p.t[p.i_fcw].off, ax));
   {
     FcDgrad pr{};
     pr.M = F; pr.N = p.fc_in; pr.K = 256;
@@ -529,7 +543,7 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
     else SEED_TRY(shallow_backward(c, batch, lowp, params, grads, st));
     SEED_TRY(c.edge(c.aux, st));   // join the aux branch
     if (dp) {
-      SEED_TRY(c.bucket(grads, p.t[p.i_fcw].off, st));
+      SEED_TRY(c.bucket(grads, dp_buckets() >= 2 ? p.t[p.i_fcw].off : p.P, st));
       SEED_CUDA_TRY(cudaEventRecord(c.ev[3], c.side));
       SEED_CUDA_TRY(cudaStreamWaitEvent(st, c.ev[3], 0));
       c.mark("allreduce_tail");
