@@ -233,9 +233,10 @@ class Learner:
         self.hp = hp or HParams()
         self.comm = comm
         n = net_param_count(spec)
-        # opt-in peer-memory allreduce (NCCL measured faster inside the step)
+        # opt-in peer-memory allreduce (NCCL measured faster inside the step);
+        # SEED_PEER_MAX caps the bucket size (floats) it takes, larger buckets stay on NCCL
         if comm is not None and comm.world > 1 and os.environ.get("SEED_PEER", "0") == "1":
-            comm.enable_peer(n)
+            comm.enable_peer(min(n, int(os.environ.get("SEED_PEER_MAX", n))))
         params = torch.as_tensor(params, dtype=torch.float32).reshape(-1)
         if params.numel() != n:
             raise ValueError(f"params has {params.numel()} values, net needs {n}")

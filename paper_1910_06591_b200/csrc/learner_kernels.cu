@@ -271,7 +271,6 @@ extern "C" int seed_debug_heads_prof(long long* out) {
 
 __global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS)
     heads_loss_kernel(const LossArgs a) {
-  pdl_wait();
   HL_STAMP(0)
   extern __shared__ float hsm[];
   const int I = a.I, A = a.A, A1 = A + 1, A1p = A1 | 1;
@@ -310,6 +309,9 @@ __global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS)
     Wt[(i + 2) * A1p + o] = w4.z;
     Wt[(i + 3) * A1p + o] = w4.w;
   }
+  // everything above reads the batch and the heads weights (last written by the
+  // previous step's Adam, >= 2 kernels back); H comes from the preceding kernel
+  pdl_wait();
   cluster_sync_all();   // every CTA of the cluster runs before any DSMEM store
   // ---- phase 1: heads forward of this CTA's rows, one (row, output) dot product
   // per thread; results stored into all HL_CL CTAs' sL (DSMEM all-gather)

@@ -132,7 +132,6 @@ struct LstmCfg {
 template <int BBT>
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_fwd_kernel(const LstmFwdArgs a) {
-  pdl_wait();
   LSTM_STAMP(0, MAX_T1, 0)
   using Cfg = LstmCfg<BBT>;
   constexpr int U = LSTM_U, MR = Cfg::MR, NT = Cfg::NT;
@@ -154,7 +153,11 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     mbar_init(&hbar[1], 1);
     fence_mbar_init();
   }
+  // W_h's image was last written by the previous step's Adam (>= 2 kernels back, all of
+  // which waited on their predecessors): start its load before the PDL wait so it
+  // overlaps the preceding kernel's tail
   load_wh_slice(Ws, a.wh, r);   // in flight during the state loads below
+  pdl_wait();
   for (int i = tid; i < BBT * T1; i += 256) {
     const int b = i / T1, t = i % T1;
     dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
@@ -343,7 +346,6 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
 template <int BBT>
 __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     lstm_bwd_kernel(const LstmBwdArgs a) {
-  pdl_wait();
   LSTM_STAMP(1, MAX_T1, 0)
   using Cfg = LstmCfg<BBT>;
   constexpr int U = LSTM_U, MR = Cfg::MR, NT = Cfg::NT;
@@ -365,7 +367,8 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     mbar_init(&rbar[1], 1);
     fence_mbar_init();
   }
-  load_wh_slice(Ws, a.wh, r);
+  load_wh_slice(Ws, a.wh, r);   // before the PDL wait, as in the forward
+  pdl_wait();
   for (int i = tid; i < BBT * T1; i += 256) {
     const int b = i / T1, t = i % T1;
     dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;

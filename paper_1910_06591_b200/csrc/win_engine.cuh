@@ -143,13 +143,16 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
   if (warp == 1) tmem_alloc(&tbase, TCOLS);
   __syncthreads();
   tc_fence_after();
+  // the weight image was last written by the previous step's Adam / image refresh
+  // (many kernels back, each of which waited on its predecessor): fetch it before
+  // the PDL wait, overlapping the preceding kernel's tail
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(&wbar, WB);
+    bulk_g2s(smem_u32(Ws), a.wimg, WB, &wbar);
+  }
   pdl_wait();
   const uint32_t tmem = tbase;
   if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(&wbar, WB);
-      bulk_g2s(smem_u32(Ws), a.wimg, WB, &wbar);
-    }
     int it = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int s = it % stages;
