@@ -492,27 +492,20 @@ __global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS)
   float sb = 0.f;
   if (tid < A1)
     for (int t = rb0; t < rb1; ++t) sb += sL[t * A1p + tid];
-  // the cluster's four partials meet in rank 0's shared memory (DSMEM), overlaying
-  // the now-free Wt | sL | Hc region: gather[cr][o][I+1]
-  cluster_sync_all();   // every CTA is done with its own Wt / sL / Hc
-  const uint32_t g0 = mapa_u32(smem_u32(hsm), 0) + (uint32_t)(cr * A1 * (I + 1)) * 4u;
-  if (col && rg == 0) {
-#pragma unroll
-    for (int o = 0; o < AMAX; ++o)
-      if (o < A1) st_cluster_f32(g0 + (uint32_t)(o * (I + 1) + ci) * 4u, acc[o]);
-  }
-  if (tid < A1) st_cluster_f32(g0 + (uint32_t)(tid * (I + 1) + I) * 4u, sb);
-  cluster_sync_all();
-  if (cr == 0) {   // fixed-order sum over the cluster ranks -> one partial per trajectory
+  // one partial per (trajectory, cluster rank), written straight to global (a DSMEM
+  // gather into rank 0 cost two cluster barriers and ~5K remote stores per CTA);
+  // heads_wgrad_finish sums them in (b, rank) order
+  {
     const int n = A1 * (I + 1);
-    float* wp = a.wpart + (size_t)b * n;
-    for (int q = tid; q < n; q += HL_THREADS) {
-      float v = 0.f;
+    float* wp = a.wpart + ((size_t)b * HL_CL + cr) * n;
+    if (col && rg == 0) {
 #pragma unroll
-      for (int r = 0; r < HL_CL; ++r) v += hsm[r * n + q];
-      wp[q] = v;
+      for (int o = 0; o < AMAX; ++o)
+        if (o < A1) wp[o * (I + 1) + ci] = acc[o];
     }
+    if (tid < A1) wp[tid * (I + 1) + I] = sb;
   }
+  // (the last DSMEM access, phase 1's all-gather, completed at its cluster barrier)
   HL_STAMP(6)
 }
 
@@ -545,11 +538,9 @@ __global__ void __launch_bounds__(256) heads_wgrad_finish(int NP, int A1, int I,
 seed_status launch_heads_loss(const LossArgs& a, cudaStream_t st) {
   if (a.T > 256 || a.A > 32 || a.I > 256 || (a.I & 3)) return SEED_E_SHAPE;
   const int A1p = (a.A + 1) | 1;
-  // Hc holds HL_RC rows of H, later the [A+1][I] row-parity partials (A+1 <= HL_RC+1);
-  // at the end the region holds the cluster gather [HL_CL][A+1][I+1]
-  const size_t smem = std::max(((((size_t)a.I * A1p + (size_t)(a.T + 1) * A1p + 3) & ~(size_t)3) +
-                                (size_t)(HL_RC + 1) * a.I) * 4,
-                               (size_t)HL_CL * (a.A + 1) * (a.I + 1) * 4);
+  // Hc holds HL_RC rows of H, later the [A+1][I] row-parity partials (A+1 <= HL_RC+1)
+  const size_t smem = ((((size_t)a.I * A1p + (size_t)(a.T + 1) * A1p + 3) & ~(size_t)3) +
+                       (size_t)(HL_RC + 1) * a.I) * 4;
   static bool attr = false;
   if (!attr) {
     SEED_CUDA_TRY(cudaFuncSetAttribute(heads_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -559,7 +550,7 @@ seed_status launch_heads_loss(const LossArgs& a, cudaStream_t st) {
   }
   SEED_TRY(launch_k(heads_loss_kernel, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
   const int n = (a.A + 1) * (a.I + 1);
-  return launch_k(heads_wgrad_finish, dim3(ceil_div(n, 32)), dim3(256), 0, st, a.B, a.A + 1,
+  return launch_k(heads_wgrad_finish, dim3(ceil_div(n, 32)), dim3(256), 0, st, a.B * HL_CL, a.A + 1,
                   a.I, (const float*)a.wpart, a.g_w, a.g_b);
 }
 

@@ -57,12 +57,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ float sigm(float x) { return rcp_approx(1.f + __expf(-x)); }
+// Activations on the SFU's tanh.approx.f32 (one MUFU op; max rel. error ~2^-11, far
+// inside the bf16 tolerance C22): sigmoid(x) = 0.5 * tanh(0.5 x) + 0.5.  The cell
+// does 5 activations per element, so MUFU issue (16 / clk / SM) bounds the step's
+// cell phase: 1 op each instead of ex2 + rcp (2) halves it.
 __device__ __forceinline__ float tanh_fast(float x) {
-  const float e = __expf(-2.f * fabsf(x));
-  const float t = (1.f - e) * rcp_approx(1.f + e);
-  return copysignf(t, x);
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
+__device__ __forceinline__ float sigm(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
 
 // CTA r's W_h slice: local row lc = gate*32 + j  <-  global row gate*U + 32r + j.
 // cp.async (16 B, L2 only), 16 chunks per thread (blockDim 256), left in flight:
