@@ -106,36 +106,38 @@ static WinWgradArgs s2d_wgrad_args(const uint8_t* src, int64_t rows, const uint8
 }
 
 // ------------------------------------------------------------------ obs -> S0
-// 8 threads per S0 row, one 16-byte output chunk each (chunk j = obs row 4Y + j/2,
-// pixels 4X + 2(j%2) .. +1, 4 channels = 8 input bytes): a warp writes 4 whole rows
+// 4 threads per S0 row, one obs row each: 16 input bytes (4 pixels x 4 channels,
+// one load; a warp reads 128 contiguous bytes of each of 4 obs rows) -> output
+// chunks 2r, 2r+1 of the row (a warp writes 8 whole rows, 1 KB contiguous)
 __global__ void s2d_obs_kernel(int64_t nrows, FastDiv P, FastDiv Wd, int H, int W,
                                const uint8_t* __restrict__ obs, uint8_t* __restrict__ S0) {
   pdl_wait();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t g = t >> 3;
+  const int64_t g = t >> 2;
   if (g >= nrows) return;
-  const int j = (int)(t & 7);
+  const int r = (int)(t & 3);
   uint32_t f, rem, Y, X;
   P.divmod((uint32_t)g, f, rem);
   Wd.divmod(rem, Y, X);
-  const uint2 u = __ldg(reinterpret_cast<const uint2*>(
-      obs + (((size_t)f * H + 4 * Y + (j >> 1)) * W + 4 * X + 2 * (j & 1)) * 4));
-  const uint32_t w[2] = {u.x, u.y};
-  uint32_t o[4];
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(obs + (((size_t)f * H + 4 * Y + r) * W + 4 * X) * 4));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  uint32_t o[8];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {   // bytes -> bf16 (exact): the float's high half
+  for (int k = 0; k < 4; ++k) {   // bytes -> bf16 (exact): the float's high half
     const uint32_t b0 = w[k] & 0xFF, b1 = (w[k] >> 8) & 0xFF, b2 = (w[k] >> 16) & 0xFF, b3 = w[k] >> 24;
     o[2 * k] = (__float_as_uint((float)b0) >> 16) | (__float_as_uint((float)b1) & 0xFFFF0000u);
     o[2 * k + 1] = (__float_as_uint((float)b2) >> 16) | (__float_as_uint((float)b3) & 0xFFFF0000u);
   }
-  *reinterpret_cast<uint4*>(S0 + g * 128 + (swz_chunk(g, 128, j) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+  uint8_t* row = S0 + g * 128;
+  *reinterpret_cast<uint4*>(row + (swz_chunk(g, 128, 2 * r) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+  *reinterpret_cast<uint4*>(row + (swz_chunk(g, 128, 2 * r + 1) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
 }
 
 seed_status s2d_obs(const uint8_t* obs, int64_t F, int H, int W, uint8_t* S0, cudaStream_t st) {
   const int Hs = H / 4, Ws = W / 4;
   const int64_t n = F * Hs * Ws;
   if (n == 0) return SEED_OK;
-  return launch_k(s2d_obs_kernel, dim3((unsigned)((n * 8 + 255) / 256)), dim3(256), 0, st, n,
+  return launch_k(s2d_obs_kernel, dim3((unsigned)((n * 4 + 255) / 256)), dim3(256), 0, st, n,
                   FastDiv(Hs * Ws), FastDiv(Ws), H, W, obs, S0);
 }
 
