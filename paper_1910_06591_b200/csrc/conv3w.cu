@@ -350,6 +350,35 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3_obs_xim_kernel(
   }
 }
 
+// direct conversion for C = 16 (GRF SMM planes): thread = one padded-row pixel, one
+// 16-byte load of its 16 channel bytes, two 16-byte chunk stores
+__global__ void __launch_bounds__(ROWK_THREADS) conv3_obs_c16_kernel(
+    PadGeo g, const uint8_t* __restrict__ obs, uint8_t* __restrict__ X0) {
+  pdl_wait();
+  const int X = blockIdx.y * ROWK_THREADS + threadIdx.x;
+  if (X >= g.Wp) return;
+  const int Hp = g.H + 2, nb = (Hp + ROWK_RPB - 1) / ROWK_RPB;
+  const int f = blockIdx.x / nb, Y0 = (blockIdx.x - f * nb) * ROWK_RPB;
+  const int x = X - 1;
+  for (int Y = Y0; Y < min(Y0 + ROWK_RPB, Hp); ++Y) {
+    const int y = Y - 1;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (y >= 0 && y < g.H && x >= 0 && x < g.W)
+      u = __ldg(reinterpret_cast<const uint4*>(obs + (((size_t)f * g.H + y) * g.W + x) * 16));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {   // bytes -> bf16 (exact): the float's high half
+      const uint32_t b0 = w[k] & 0xFF, b1 = (w[k] >> 8) & 0xFF, b2 = (w[k] >> 16) & 0xFF, b3 = w[k] >> 24;
+      o[2 * k] = (__float_as_uint((float)b0) >> 16) | (__float_as_uint((float)b1) & 0xFFFF0000u);
+      o[2 * k + 1] = (__float_as_uint((float)b2) >> 16) | (__float_as_uint((float)b3) & 0xFFFF0000u);
+    }
+    const int64_t m = ((int64_t)f * Hp + Y) * g.Wp + X;
+    *chunk_at(X0, m, 32, 0) = make_uint4(o[0], o[1], o[2], o[3]);
+    *chunk_at(X0, m, 32, 1) = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
 seed_status conv3_obs(const uint8_t* obs, int64_t F, const PadGeo& g, int C, int Cp, bool xim,
                       uint8_t* X0, cudaStream_t st) {
   if (F == 0) return SEED_OK;
@@ -359,6 +388,10 @@ seed_status conv3_obs(const uint8_t* obs, int64_t F, const PadGeo& g, int C, int
     if (xim && C == 3) {
       const dim3 gx((unsigned)(F * ceil_div(g.H + 2, ROWK_RPB)), (unsigned)ceil_div(g.Wp, ROWK_THREADS));
       return launch_k(conv3_obs_xim_kernel<3>, gx, dim3(ROWK_THREADS), 0, st, g, obs, X0);
+    }
+    if (!xim && C == 16 && (reinterpret_cast<uintptr_t>(obs) & 15) == 0) {
+      const dim3 gx((unsigned)(F * ceil_div(g.H + 2, ROWK_RPB)), (unsigned)ceil_div(g.Wp, ROWK_THREADS));
+      return launch_k(conv3_obs_c16_kernel, gx, dim3(ROWK_THREADS), 0, st, g, obs, X0);
     }
     return launch_k(conv3_obs_kernel<2, 0>, grid, dim3(ROWK_THREADS), 0, st, g, C, xim ? 1 : 0, obs, X0);
   }
