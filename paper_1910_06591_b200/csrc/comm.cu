@@ -15,6 +15,7 @@ typedef int (*GetUid_t)(NcclUid*);
 typedef int (*InitRank_t)(ncclComm_t*, int, NcclUid, int);
 typedef int (*AllReduce_t)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef int (*Destroy_t)(ncclComm_t);
+typedef int (*Split_t)(ncclComm_t, int, int, ncclComm_t*, void*);
 constexpr int kNcclFloat32 = 7, kNcclSum = 0;
 
 struct Nccl {
@@ -23,6 +24,7 @@ struct Nccl {
   InitRank_t init_rank = nullptr;
   AllReduce_t all_reduce = nullptr;
   Destroy_t destroy = nullptr;
+  Split_t split = nullptr;   // optional (NCCL >= 2.18)
 };
 
 const Nccl& nccl() {
@@ -37,6 +39,7 @@ const Nccl& nccl() {
       n.init_rank = (InitRank_t)dlsym(h, "ncclCommInitRank");
       n.all_reduce = (AllReduce_t)dlsym(h, "ncclAllReduce");
       n.destroy = (Destroy_t)dlsym(h, "ncclCommDestroy");
+      n.split = (Split_t)dlsym(h, "ncclCommSplit");
       n.ok = n.get_uid && n.init_rank && n.all_reduce && n.destroy;
     }
   }
@@ -44,7 +47,7 @@ const Nccl& nccl() {
 }
 }  // namespace
 
-constexpr int COMM_EVENTS = 4;
+constexpr int COMM_EVENTS = 6;
 constexpr int PEER_MAX = 8;
 // 128 x 256 measured best standalone (4.9 MB in 31-33 us at N=2 vs NCCL's 39 us);
 // inside the learner step it still loses to NCCL (its CTAs compete with the
@@ -64,7 +67,12 @@ struct seed_comm {
   ncclComm_t comm;
   int rank, world;
   cudaStream_t side;          // all of this comm's collectives inside a learner step
-  cudaEvent_t ev[COMM_EVENTS];   // bucket forks ..., join
+  cudaEvent_t ev[COMM_EVENTS];   // bucket forks ..., joins
+  // a second communicator (ncclCommSplit of the first) on its own side stream, so
+  // two gradient buckets reduce concurrently (NCCL serialises one communicator's
+  // collectives); null when the split is unavailable or SEED_DP_COMMS=1
+  ncclComm_t comm2 = nullptr;
+  cudaStream_t side2 = nullptr;
   // peer-memory allreduce
   int64_t peer_max = 0;
   uint8_t* peer_local = nullptr;            // this rank's buffer (cudaMalloc)
@@ -224,11 +232,21 @@ static bool aligned_f4(const float* p) { return (reinterpret_cast<uintptr_t>(p) 
 }
 
 namespace seed {
-seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaEvent_t* ev) {
+seed_status comm_allreduce(seed_comm* c, float* data, int64_t n, cudaStream_t st);
+seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaStream_t* side2, cudaEvent_t* ev) {
   if (!c || c->world == 1 || !c->side) return SEED_E_ARG;
   *side = c->side;
+  *side2 = c->comm2 ? c->side2 : nullptr;
   for (int i = 0; i < COMM_EVENTS; ++i) ev[i] = c->ev[i];
   return SEED_OK;
+}
+seed_status comm_allreduce2(seed_comm* c, float* data, int64_t n, cudaStream_t st) {
+  if (!c || !data) return SEED_E_ARG;
+  if (c->world == 1) return SEED_OK;
+  if (!c->comm2) return comm_allreduce(c, data, n, st);
+  return nccl().all_reduce(data, data, (size_t)n, kNcclFloat32, kNcclSum, c->comm2, st) == 0
+             ? SEED_OK
+             : SEED_E_NCCL;
 }
 int comm_world(const seed_comm* c) { return c ? c->world : 1; }
 
@@ -290,6 +308,12 @@ extern "C" seed_status seed_comm_init(const void* id128, int rank, int world, se
       delete c;
       return SEED_E_NCCL;
     }
+    const char* e = getenv("SEED_DP_COMMS");   // collective decision: same env on every rank
+    if (nccl().split && !(e && e[0] == '1')) {
+      if (nccl().split(c->comm, 0, rank, &c->comm2, nullptr) != 0 ||
+          cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking) != cudaSuccess)
+        c->comm2 = nullptr;
+    }
   }
   *out = c;
   return SEED_OK;
@@ -297,7 +321,9 @@ extern "C" seed_status seed_comm_init(const void* id128, int rank, int world, se
 
 extern "C" seed_status seed_comm_destroy(seed_comm* c) {
   if (!c) return SEED_E_ARG;
+  if (c->comm2 && nccl().ok) nccl().destroy(c->comm2);
   if (c->comm && nccl().ok) nccl().destroy(c->comm);
+  if (c->side2) cudaStreamDestroy(c->side2);
   for (int r = 0; r < c->world && r < PEER_MAX; ++r)
     if (c->peer_map[r] && c->peer_map[r] != c->peer_local) cudaIpcCloseMemHandle(c->peer_map[r]);
   if (c->peer_local) cudaFree(c->peer_local);

@@ -31,7 +31,8 @@
 namespace seed {
 
 seed_status comm_allreduce(seed_comm* comm, float* data, int64_t n, cudaStream_t st);
-seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaEvent_t* ev);
+seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaStream_t* side2, cudaEvent_t* ev);
+seed_status comm_allreduce2(seed_comm* comm, float* data, int64_t n, cudaStream_t st);
 int comm_world(const seed_comm* c);
 
 // The library's second stream (per device, created once) and its event pool.
@@ -89,16 +90,20 @@ struct StepCtx {
   int max_ctas = 0;   // > 0 while collectives run concurrently (SMs left for NCCL)
   // H10 buckets: a gradient range that is final is allreduced on the comm's side
   // stream while the main stream continues (same bucket order on every rank)
+  // The second bucket goes to a second communicator on its own stream (side2) when
+  // the comm has one, so it reduces concurrently with the first.
   seed_comm* comm = nullptr;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev[4] = {};
+  cudaStream_t side = nullptr, side2 = nullptr;
+  cudaEvent_t ev[6] = {};
   int nbucket = 0;
   seed_status bucket(float* g, int64_t n, cudaStream_t from) {
     if (!side || n <= 0 || nbucket >= 3) return SEED_OK;
+    const bool second = side2 && nbucket == 1;
+    cudaStream_t s = second ? side2 : side;
     SEED_CUDA_TRY(cudaEventRecord(ev[nbucket], from));
-    SEED_CUDA_TRY(cudaStreamWaitEvent(side, ev[nbucket], 0));
+    SEED_CUDA_TRY(cudaStreamWaitEvent(s, ev[nbucket], 0));
     ++nbucket;
-    return comm_allreduce(comm, g, n, side);
+    return second ? comm_allreduce2(comm, g, n, s) : comm_allreduce(comm, g, n, s);
   }
   // Independent backward GEMMs run as a second branch on `aux` (a process-wide
   // stream of the library; inside a CUDA graph capture the event edges make it a
@@ -536,7 +541,7 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
     // the end) reduced on the comm's side stream, joined before the clip.
     if (dp) {
       c.comm = comm;
-      SEED_TRY(comm_side(comm, &c.side, c.ev));
+      SEED_TRY(comm_side(comm, &c.side, &c.side2, c.ev));
     }
     SEED_TRY(core_backward(c, batch, lowp, params, grads, st));
     if (p.nsec > 0) SEED_TRY(deep_backward(c, batch, lowp, params, grads, st));
@@ -546,6 +551,10 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
       SEED_TRY(c.bucket(grads, dp_buckets() >= 2 ? p.t[p.i_fcw].off : p.P, st));
       SEED_CUDA_TRY(cudaEventRecord(c.ev[3], c.side));
       SEED_CUDA_TRY(cudaStreamWaitEvent(st, c.ev[3], 0));
+      if (c.side2) {
+        SEED_CUDA_TRY(cudaEventRecord(c.ev[4], c.side2));
+        SEED_CUDA_TRY(cudaStreamWaitEvent(st, c.ev[4], 0));
+      }
       c.mark("allreduce_tail");
     }
   }
