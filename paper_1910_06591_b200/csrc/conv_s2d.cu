@@ -95,15 +95,25 @@ __device__ void WinWgradFinish::weight(int a, int i, int n, float t) const {
   g_w[(((size_t)n * K + ky) * K + kx) * g.C + c] = t * scale;
 }
 
-size_t win_wgrad_part_bytes(int64_t M, int N) { return win_wgrad_part_bytes_g(M, N, 2); }
+size_t win_wgrad_part_bytes(int64_t M, int N) { return win3_wgrad_part_bytes(M, N, 2); }
 
-static WinWgradArgs s2d_wgrad_args(const uint8_t* src, int64_t rows, const uint8_t* dy, int wsp,
-                                   float* part) {
-  WinWgradArgs a{};
-  a.src = src; a.src_rows = rows; a.dy = dy; a.M = rows; a.part = part;
-  a.ngroup = 2; a.goff[0] = 0; a.goff[1] = wsp; a.astride = 1;
+// Both window rows in one MMA (win3_wgrad_kernel with 2 B atoms): D[(b, ch)][(j, n)] =
+// sum_h S[h + b][ch] dY[h - Ws + j*Ws][n], window row a = 1 - j; the bias gradient
+// from the epilogue warps' column sums of dY (B atom 1 = dY[h])
+struct S2dFin2 {
+  WinWgradFinish f;
+  int CO;
+  __device__ void weight3(int i, int n, float t) const { f.weight(1 - n / CO, i, n % CO, t); }
+  __device__ void bias(int n, float t) const { f.bias(n, t); }
+};
+static Win3WgradArgs s2d_wgrad3_args(const uint8_t* src, int64_t rows, const uint8_t* dy, int wsp,
+                                     float* part) {
+  Win3WgradArgs a{};
+  a.X = src; a.dy = dy; a.M = rows; a.part = part;
+  a.boff = -wsp; a.bstride = wsp;
   return a;
 }
+
 
 // ------------------------------------------------------------------ obs -> S0
 // 4 threads per S0 row, one obs row each: 16 input bytes (4 pixels x 4 channels,
@@ -202,10 +212,10 @@ seed_status shallow_s2d_forward(const ShallowS2d& sg, int64_t F, const uint8_t* 
 seed_status shallow_s2d_conv2_wgrad(const ShallowS2d& sg, int64_t F, const uint8_t* S1,
                                     const uint8_t* dY2, float* part, float* g_w2, float* g_b2,
                                     cudaStream_t st) {
-  const WinWgradArgs a = s2d_wgrad_args(S1, sg.rows2(F), dY2, sg.g2.Ws, part);
-  WinWgradFinish f{};
-  f.g = sg.g2; f.scale = 1.f; f.g_w = g_w2; f.g_b = g_b2;
-  return launch_win_wgrad<32, 128>(a, f, st);
+  const Win3WgradArgs a = s2d_wgrad3_args(S1, sg.rows2(F), dY2, sg.g2.Ws, part);
+  S2dFin2 f{};
+  f.f.g = sg.g2; f.f.scale = 1.f; f.f.g_w = g_w2; f.f.g_b = g_b2; f.CO = 32;
+  return launch_win3_wgrad<32, 128, S2dFin2, 2>(a, f, true, st);
 }
 
 seed_status shallow_s2d_conv2_dgrad(const ShallowS2d& sg, int64_t F, const uint8_t* dY2,
@@ -225,10 +235,10 @@ seed_status shallow_s2d_conv2_dgrad(const ShallowS2d& sg, int64_t F, const uint8
 seed_status shallow_s2d_conv1_wgrad(const ShallowS2d& sg, int64_t F, const uint8_t* S0,
                                     const uint8_t* dY1, float* part, float* g_w1, float* g_b1,
                                     cudaStream_t st) {
-  const WinWgradArgs a = s2d_wgrad_args(S0, sg.rows1(F), dY1, sg.g1.Ws, part);
-  WinWgradFinish f{};
-  f.g = sg.g1; f.scale = 1.f / 255.f; f.g_w = g_w1; f.g_b = g_b1;
-  return launch_win_wgrad<16, 128>(a, f, st);
+  const Win3WgradArgs a = s2d_wgrad3_args(S0, sg.rows1(F), dY1, sg.g1.Ws, part);
+  S2dFin2 f{};
+  f.f.g = sg.g1; f.f.scale = 1.f / 255.f; f.f.g_w = g_w1; f.f.g_b = g_b1; f.CO = 16;
+  return launch_win3_wgrad<16, 128, S2dFin2, 2>(a, f, true, st);
 }
 
 }  // namespace seed

@@ -18,9 +18,11 @@
 //
 // Kernels: s2d_obs_kernel (uint8 obs -> S0), win_conv_kernel (forward /
 // data-gradient: persistent, TMA slab ring, double-buffered TMEM accumulators),
-// win_wgrad_kernel (weight + bias gradient: split-K over rows, A = MN-major
-// slab with the b-shift expressed as the atom stride LBO = 128 bytes, bias
-// from an all-ones operand) + win_wgrad_finish (fixed-order split sum).
+// win3_wgrad_kernel with 2 B atoms (weight + bias gradient: split over rows, one
+// MMA per 16 rows — A = MN-major slab whose two 64-channel atoms are the window
+// columns b (LBO = one 128-byte row), B = dY rows whose two atoms are the window
+// rows a (LBO = Ws rows); bias from the epilogue warps' column sums of dY) +
+// win3_wgrad_finish (fixed-order split sum).
 #pragma once
 #include "common.cuh"
 #include "win_engine.cuh"

@@ -14,12 +14,11 @@
 // keeps the address phase mod 1024 lands every row in the canonical K-major
 // operand layout; a start that is not atom-aligned reads the absolute-address
 // swizzle (verified on hardware: scripts/probe_umma_shift.cu).
-// Weight gradient (win_wgrad_kernel): reduce over rows g,
-//   dW[grp][atom][c][n] = sum_g S[g + goff_grp + atom*astride][c] * dY[g][n]
-// with A = the slab as an MN-major operand of M = 128 = NA atoms x (RB/2)
-// channels whose atoms are rows `astride` apart (atom stride LBO), B = dY rows
-// MN-major, and the bias gradient from an all-ones operand; split over rows
-// with a fixed-order finish (deterministic, C21).
+// Weight gradient (win3_wgrad_kernel): reduce over rows, all taps in one MMA per
+// 16 rows — A = input rows as an MN-major operand whose atoms are column shifts,
+// B = dY rows as an MN-major operand whose atoms are row-window shifts; bias from
+// column sums of the dY slab; split over rows with a fixed-order finish
+// (deterministic, C21).
 #pragma once
 #include <algorithm>
 #include "common.cuh"
@@ -35,7 +34,6 @@ constexpr int WC_MAX_STAGES = 8;
 constexpr int WC_SMEM_BUDGET = 200 * 1024;
 constexpr int WG_KS = 256;        // rows per weight-gradient k-stage
 constexpr int WIN_MAX = 9;        // windows per convolution
-constexpr int WG_MAX_GROUPS = 3;  // weight-gradient accumulator groups
 
 struct WinConvArgs {
   const uint8_t* src;    // pre-swizzled rows of RB bytes
@@ -45,17 +43,6 @@ struct WinConvArgs {
   const uint8_t* wimg;   // pre-swizzled weight image [NW][N][RB]
 };
 
-struct WinWgradArgs {
-  const uint8_t* src;    // A: pre-swizzled rows of RBX bytes
-  int64_t src_rows;
-  const uint8_t* dy;     // B: pre-swizzled rows of 2*N bytes
-  int64_t M;             // rows summed over
-  int ngroup;            // accumulator groups (<= 3)
-  int goff[WG_MAX_GROUPS];   // row offset of each group's first atom
-  int astride;           // rows between consecutive atoms of a group
-  int64_t rows_per_cta;  // multiple of WG_KS
-  float* part;           // [grid][ngroup + 1][128][N]
-};
 
 __device__ __forceinline__ uint4 pack8(const float* o) {
   uint4 u;
@@ -250,157 +237,6 @@ seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st)
                   stages, slab);
 }
 
-// ------------------------------------------------------------------ weight gradient
-// Per CTA: rows [z*R, min((z+1)*R, M)) in k-stages of WG_KS rows.  Accumulator
-// group g (TMEM columns [g*N, g*N+N)) = M=128 MN-major operand whose NA atoms
-// start at rows goff[g] + atom*astride; group `ngroup` = all-ones operand (every
-// row = the column sum of dY = the bias gradient).
-template <int N, int RBX, int NG>
-__global__ void __launch_bounds__(WC_THREADS, 1)
-    win_wgrad_kernel(const WinWgradArgs a, int stages, int a_bytes, int b_bytes) {
-  constexpr int RBY = 2 * N;
-  constexpr uint32_t LA = swz_layout_code(RBX), LB = swz_layout_code(RBY);
-  constexpr int NA = 256 / RBX;   // atoms per M = 128
-  constexpr uint32_t TCOLS = 4 * N < 32 ? 32 : (4 * N <= 64 ? 64 : 128);
-  extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* ones = sm;                  // 1 KB of bf16 1.0
-  uint8_t* stg = sm + 1024;            // stages x (A slab | B slab)
-  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull;
-  __shared__ uint32_t tbase;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
-  const int64_t r_end = std::min<int64_t>(a.M, r_begin + a.rows_per_cta);
-  const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
-  int gmn = a.goff[0], gmx = a.goff[0];
-#pragma unroll
-  for (int g = 1; g < NG; ++g) { gmn = min(gmn, a.goff[g]); gmx = max(gmx, a.goff[g]); }
-  const int arows = WG_KS + gmx - gmn + (NA - 1) * a.astride;
-  for (int i = threadIdx.x; i < 64; i += blockDim.x)
-    reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-  fence_proxy_async_smem();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(&tfull, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc(&tbase, TCOLS);
-  __syncthreads();
-  tc_fence_after();
-  pdl_wait();
-  const uint32_t tmem = tbase;
-  if (warp == 0) {
-    for (int it = 0; it < nks; ++it) {
-      const int s = it % stages;
-      mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-      const int64_t k0 = r_begin + (int64_t)it * WG_KS;
-      uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
-      // B first (its bytes are credited through the A call's expect_tx)
-      const int64_t blo = k0, bhi = std::min<int64_t>(k0 + WG_KS, r_end);
-      uint8_t* bd = sa + a_bytes + slab_phase(k0, RBY);
-      if (bhi - blo < WG_KS) {
-        zero_rows(bd, RBY, (int)(bhi - blo), WG_KS, lane);
-        fence_proxy_async_smem();
-      }
-      __syncwarp();
-      const uint32_t bbytes = (uint32_t)((bhi - blo) * RBY);
-      load_slab(sa, a.src, RBX, k0 + gmn, arows, a.src_rows, &full[s], lane, bbytes);
-      if (lane == 0) bulk_g2s(smem_u32(bd), a.dy + blo * RBY, bbytes, &full[s]);
-    }
-  } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
-    {
-      const uint32_t idesc = umma_idesc_bf16(128, N, true, true);
-      const uint64_t od = umma_desc(smem_u32(ones), 0, 0, 2);
-      const uint32_t lbo = (uint32_t)(a.astride * RBX);
-      int goffd[NG];
-#pragma unroll
-      for (int g = 0; g < NG; ++g) goffd[g] = ((a.goff[g] - gmn) * RBX) >> 4;
-      for (int it = 0; it < nks; ++it) {
-        const int s = it % stages;
-        mbar_wait(&full[s], (it / stages) & 1);
-        tc_fence_after();
-        const int64_t k0 = r_begin + (int64_t)it * WG_KS;
-        uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
-        // descriptors advance linearly with the start address (field = addr >> 4)
-        const uint64_t ad0 = umma_desc(smem_u32(sa) + slab_phase(k0 + gmn, RBX), lbo, 8 * RBX, LA);
-        const uint64_t bd0 = umma_desc(smem_u32(sa + a_bytes) + slab_phase(k0, RBY), 8 * RBY, 8 * RBY, LB);
-        const uint32_t acc0 = it != 0;
-#pragma unroll
-        for (int ks = 0; ks < WG_KS / 16; ++ks) {
-          const uint64_t bdsc = bd0 + (uint64_t)((ks * 16 * RBY) >> 4);
-          const uint32_t accf = acc0 | (ks != 0);
-#pragma unroll
-          for (int g = 0; g < NG; ++g)
-            tc_mma_bf16_w(tmem + g * N, ad0 + (uint64_t)(goffd[g] + ((ks * 16 * RBX) >> 4)), bdsc, idesc,
-                        accf);
-          tc_mma_bf16_w(tmem + NG * N, od, bdsc, idesc, accf);
-        }
-        tc_commit_w(&empty[s]);
-      }
-      tc_commit_w(&tfull);
-    }
-  } else {
-    const int q = warp & 3;
-    const int ng1 = NG + 1;
-    float* part = a.part + (size_t)blockIdx.x * ng1 * 128 * N;
-    if (nks > 0) {
-      mbar_wait(&tfull, 0);
-      tc_fence_after();
-    }
-#pragma unroll
-    for (int t = 0; t < ng1; ++t) {
-      float v[N];
-      if (nks > 0) {
-#pragma unroll
-        for (int c = 0; c < N / 16; ++c)
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + t * N + c * 16, v + 16 * c);
-      } else {
-#pragma unroll
-        for (int c = 0; c < N; ++c) v[c] = 0.f;
-      }
-      const int row = q * 32 + lane;
-      if (t < NG || row == 0) {
-        float4* dst = reinterpret_cast<float4*>(part + ((size_t)t * 128 + row) * N);
-#pragma unroll
-        for (int c = 0; c < N / 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-      }
-    }
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, TCOLS);
-  }
-}
-
-// Fixed-order sum of the per-CTA partials; block = 32 outputs x 8 split groups.
-// Fin: __device__ void weight(int grp, int i /*0..127*/, int n, float v) const;
-//      __device__ void bias(int n, float v) const.
-template <class Fin>
-__global__ void __launch_bounds__(256) win_wgrad_finish(const float* __restrict__ part, int G, int N,
-                                                        int ngroup, const Fin f) {
-  pdl_wait();
-  const int ng1 = ngroup + 1;
-  const int tot = ngroup * 128 * N + N;
-  const int o = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
-  __shared__ float sh[8][33];
-  float s = 0.f;
-  if (o < tot) {
-    const size_t idx = (size_t)o;   // bias outputs are row 0 of group `ngroup`
-    for (int z = g; z < G; z += 8) s += part[(size_t)z * ng1 * 128 * N + idx];
-  }
-  sh[g][threadIdx.x & 31] = s;
-  __syncthreads();
-  if (g == 0 && o < tot) {
-    float t = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x & 31];
-    if (o >= ngroup * 128 * N) f.bias(o - ngroup * 128 * N, t);
-    else f.weight(o / (128 * N), (o / N) % 128, o % N, t);
-  }
-}
-
 inline int wgrad_grid(int64_t M, int64_t* rows_per_cta) {
   const int64_t kst = (M + WG_KS - 1) / WG_KS;
   const int64_t G0 = std::min<int64_t>(148, std::max<int64_t>(kst, 1));
@@ -408,43 +244,6 @@ inline int wgrad_grid(int64_t M, int64_t* rows_per_cta) {
   *rows_per_cta = per * WG_KS;
   return (int)std::max<int64_t>(1, (M + per * WG_KS - 1) / (per * WG_KS));
 }
-
-inline size_t win_wgrad_part_bytes_g(int64_t M, int N, int ngroup) {
-  int64_t r;
-  return (size_t)wgrad_grid(M, &r) * (ngroup + 1) * 128 * N * 4;
-}
-
-template <int N, int RBX, class Fin>
-seed_status launch_win_wgrad(const WinWgradArgs& a0, const Fin& fin, cudaStream_t st) {
-  WinWgradArgs a = a0;
-  if (a.ngroup < 1 || a.ngroup > WG_MAX_GROUPS) return SEED_E_SHAPE;
-  const int G = wgrad_grid(a.M, &a.rows_per_cta);
-  int gmn = a.goff[0], gmx = a.goff[0];
-  for (int g = 1; g < a.ngroup; ++g) { gmn = std::min(gmn, a.goff[g]); gmx = std::max(gmx, a.goff[g]); }
-  const int arows = WG_KS + gmx - gmn + (256 / RBX - 1) * a.astride;
-  const int a_bytes = (int)align_up((size_t)arows * RBX + 1024, 1024);
-  const int b_bytes = (int)align_up((size_t)WG_KS * 2 * N + 1024, 1024);
-  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes));
-  if (stages < 2) return SEED_E_SHAPE;
-  const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win_wgrad_kernel<N, RBX, 1>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win_wgrad_kernel<N, RBX, 2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win_wgrad_kernel<N, RBX, 3>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
-    attr = true;
-  }
-  auto kern = a.ngroup == 1 ? win_wgrad_kernel<N, RBX, 1>
-            : a.ngroup == 2 ? win_wgrad_kernel<N, RBX, 2> : win_wgrad_kernel<N, RBX, 3>;
-  SEED_TRY(launch_k(kern, dim3(G), dim3(WC_THREADS), smem, st, a, stages, a_bytes, b_bytes));
-  const int tot = a.ngroup * 128 * N + N;
-  return launch_k(win_wgrad_finish<Fin>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
-                  (const float*)a.part, G, N, a.ngroup, fin);
-}
-
 
 // ------------------------------------------------------------------ 3x3 weight gradient
 // All nine taps in ONE tcgen05.mma per 16 rows (M = 128, N = 3*CO):
@@ -464,12 +263,13 @@ struct Win3WgradArgs {
   float* part;           // [grid][128][4*CO] (cols [0, 3CO) weights, [3CO, 4CO) bias in row 0)
 };
 
-template <int CO, int RBX, bool BIAS>
+template <int CO, int RBX, bool BIAS, int NB = 3>
 __global__ void __launch_bounds__(WC_THREADS, 1)
     win3_wgrad_kernel(const Win3WgradArgs a, int stages, int a_bytes, int b_bytes) {
   constexpr int RBY = 2 * CO;
   constexpr int NA = 256 / RBX;           // A atoms per M = 128
-  constexpr int NW = 3 * CO;              // weight columns
+  constexpr int NW = NB * CO;             // weight columns (NB B atoms)
+  constexpr int PC = (NB + 1) * CO;       // partial row: weights | bias
   constexpr uint32_t LA = swz_layout_code(RBX), LB = swz_layout_code(RBY);
   constexpr uint32_t TCOLS = NW <= 64 ? 64 : 128;
   extern __shared__ uint8_t smraw[];
@@ -481,7 +281,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t r_end = std::min<int64_t>(a.M, r_begin + a.rows_per_cta);
   const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
-  const int arows = WG_KS + NA - 1, brows = WG_KS + 2 * a.bstride;
+  const int arows = WG_KS + NA - 1, brows = WG_KS + (NB - 1) * a.bstride;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], BIAS ? 2 : 1); }
     mbar_init(&tfull, 1);
@@ -540,7 +340,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
     tc_commit_w(&tfull);
   } else {
     const int q = warp & 3;
-    float* part = a.part + (size_t)blockIdx.x * 128 * 4 * CO;
+    float* part = a.part + (size_t)blockIdx.x * 128 * PC;
     const int row = q * 32 + lane;
     const int et = threadIdx.x - 64;   // 0..127
     if (BIAS) {
@@ -595,7 +395,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 16; ++c) v[c] = 0.f;
       }
-      float4* dst = reinterpret_cast<float4*>(part + (size_t)row * 4 * CO + c0);
+      float4* dst = reinterpret_cast<float4*>(part + (size_t)row * PC + c0);
 #pragma unroll
       for (int c = 0; c < 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
@@ -610,18 +410,18 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
 
 // fixed-order sum; output o < 128*3CO: (row i, col n) -> Fin::weight3(i, n, v);
 // o >= 128*3CO: bias column -> Fin::bias
-template <int CO, class Fin>
+template <int CO, class Fin, int NB = 3>
 __global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict__ part, int G,
                                                          int tot, const Fin f) {
   pdl_wait();
-  constexpr int NW = 3 * CO;
+  constexpr int NW = NB * CO, PC = (NB + 1) * CO;
   const int o = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
   __shared__ float sh[8][33];
   float s = 0.f;
   size_t idx = 0;
   if (o < tot) {
-    idx = o < 128 * NW ? (size_t)(o / NW) * 4 * CO + (o % NW) : (size_t)NW + (o - 128 * NW);
-    for (int z = g; z < G; z += 8) s += part[(size_t)z * 128 * 4 * CO + idx];
+    idx = o < 128 * NW ? (size_t)(o / NW) * PC + (o % NW) : (size_t)NW + (o - 128 * NW);
+    for (int z = g; z < G; z += 8) s += part[(size_t)z * 128 * PC + idx];
   }
   sh[g][threadIdx.x & 31] = s;
   __syncthreads();
@@ -634,34 +434,34 @@ __global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict
   }
 }
 
-inline size_t win3_wgrad_part_bytes(int64_t M, int CO) {
+inline size_t win3_wgrad_part_bytes(int64_t M, int CO, int NB = 3) {
   int64_t r;
-  return (size_t)wgrad_grid(M, &r) * 128 * 4 * CO * 4;
+  return (size_t)wgrad_grid(M, &r) * 128 * (NB + 1) * CO * 4;
 }
 
 // bias = false: no all-ones MMA (the bias gradient is a column of the weight
 // accumulator, e.g. from a constant-1 input channel)
-template <int CO, int RBX, class Fin>
+template <int CO, int RBX, class Fin, int NB = 3>
 seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias, cudaStream_t st) {
   Win3WgradArgs a = a0;
   const int G = wgrad_grid(a.M, &a.rows_per_cta);
   const int a_bytes = (int)align_up((size_t)(WG_KS + 256 / RBX - 1) * RBX + 1024, 1024);
-  const int b_bytes = (int)align_up((size_t)(WG_KS + 2 * a.bstride) * 2 * CO + 1024, 1024);
+  const int b_bytes = (int)align_up((size_t)(WG_KS + (NB - 1) * a.bstride) * 2 * CO + 1024, 1024);
   const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes));
   if (stages < 2) return SEED_E_SHAPE;
   const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);
   static bool attr = false;
   if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX, true>,
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX, true, NB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX, false>,
+    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX, false, NB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
     attr = true;
   }
-  SEED_TRY(launch_k(bias ? win3_wgrad_kernel<CO, RBX, true> : win3_wgrad_kernel<CO, RBX, false>, dim3(G),
+  SEED_TRY(launch_k(bias ? win3_wgrad_kernel<CO, RBX, true, NB> : win3_wgrad_kernel<CO, RBX, false, NB>, dim3(G),
                     dim3(WC_THREADS), smem, st, a, stages, a_bytes, b_bytes));
-  const int tot = 128 * 3 * CO + (bias ? CO : 0);
-  return launch_k(win3_wgrad_finish<CO, Fin>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
+  const int tot = 128 * NB * CO + (bias ? CO : 0);
+  return launch_k(win3_wgrad_finish<CO, Fin, NB>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
                   (const float*)a.part, G, tot, fin);
 }
 
