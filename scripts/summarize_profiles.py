@@ -86,8 +86,8 @@ for r in rr[2:]:
 json.dump(out, open(f"{outdir}/ncu_full.json", "w"), indent=1)
 open(f"{outdir}/ncu_full.md", "w").write(
     "# ncu --set full captures (round 1)\n\n"
-    f"Source: `{rep}` (`ncu --set full --import-source on --clock-control none --launch-skip 25 "
-    "-c 25 python scripts/step_c2.py 2`: every kernel of the second eager c2 learner step, B=32 "
+    f"Source: `{rep}` (`ncu --set full --import-source on --clock-control none --launch-skip 24 "
+    "-c 24 python scripts/step_c2.py 2`: every kernel of the second eager c2 learner step, B=32 "
     "T=20; cold cache per replay).  The DRAM column is the "
     "`traffic` figure bench.py reports for the dominant kernel.\n\n" + "\n".join(md) + "\n")
 print(open(f"{outdir}/ncu_full.md").read())
