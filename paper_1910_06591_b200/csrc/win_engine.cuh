@@ -421,7 +421,9 @@ __global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict
   size_t idx = 0;
   if (o < tot) {
     idx = o < 128 * NW ? (size_t)(o / NW) * PC + (o % NW) : (size_t)NW + (o - 128 * NW);
-    for (int z = g; z < G; z += 8) s += part[(size_t)z * 128 * PC + idx];
+    // unrolled: the loads issue back to back, the adds stay in z order
+#pragma unroll 8
+    for (int z = g; z < G; z += 8) s += __ldcg(part + (size_t)z * 128 * PC + idx);
   }
   sh[g][threadIdx.x & 31] = s;
   __syncthreads();
