@@ -12,13 +12,12 @@
 //            the unroll store, C19), core-input extras onehot(prev a), clip(r),
 //            zeroed on done (C15)
 //   torso    obs -> bf16, conv1, conv2, fc on the tcgen05 engine (shallow_net.cuh)
-//   core     LSTM input projection GEMM + the cluster LSTM kernel with T+1 = 1,
-//            reading (h, c) from the table rows (reset on done) and writing the
-//            new state back to the same rows
-//   heads    logits / value (fp32)
-//   sample   warp per request: softmax, CDF, a = min{j : u < CDF_j} (C18),
-//            behaviour log-prob; u from the caller or Philox4x32-10
-//            keyed (seed, counter, actor id)
+//   core     one GEMM for the single LSTM step: [x | h_{t-1}] . [W_x | W_h]^T + b
+//            (h_{t-1} from the table rows, reset on done)
+//   cell+heads+sample  one CTA per request: the cell (new (h, c) written back to
+//            the table row), logits / value (fp32), then softmax, CDF,
+//            a = min{j : u < CDF_j} (C18) and the behaviour log-prob; u from the
+//            caller or Philox4x32-10 keyed (seed, counter, actor id)
 //   record   (optional) obs/action/reward/done/log-prob into each actor's
 //            current unroll buffer; a completed unroll (T+1 slots) is pushed to
 //            the ready ring at a position given by a block-wide prefix sum in
@@ -34,7 +33,7 @@ namespace seed {
 
 struct InferWs {
   int n;
-  size_t total, obs_bf16, act1, act2, X, xproj, H, logits, values, hpre, cpre, prev, splitk;
+  size_t total, obs_bf16, act1, act2, X, xproj, H, logits, values, hpre, cpre, prev, splitk, hb;
 };
 
 static size_t ibump(size_t& cur, size_t bytes) {
@@ -60,13 +59,14 @@ static seed_status make_infer_ws(const NetPlan& p, int n, InferWs* w) {
   w->hpre = ibump(cur, N * p.U * 4);
   w->cpre = ibump(cur, N * p.U * 4);
   w->prev = ibump(cur, N * 4);
+  w->hb = ibump(cur, N * p.U * 2);
   size_t sk = 0;
   auto need = [&](int M, int Nn, int BN, int K) {
     const int s = pick_splits(M, Nn, BN, K);
     if (s > 1) sk = std::max(sk, (size_t)s * M * Nn * 4);
   };
   need(n, 256, 128, p.fc_in);
-  need(n, 4 * p.U, 128, p.Kxp);
+  need(n, 4 * p.U, 128, p.Kxp + p.U);
   w->splitk = ibump(cur, sk + 16);
   w->total = cur;
   return SEED_OK;
@@ -78,7 +78,7 @@ __global__ void infer_pre_kernel(int n, int A, int U, int Kxp, const int32_t* __
                                  const float* __restrict__ th, const float* __restrict__ tc,
                                  const int32_t* __restrict__ tla, float* __restrict__ hpre,
                                  float* __restrict__ cpre, int32_t* __restrict__ prev,
-                                 __nv_bfloat16* __restrict__ X) {
+                                 __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ hb) {
   const int E = Kxp - 256;
   const int per = U + E;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -86,8 +86,10 @@ __global__ void infer_pre_kernel(int n, int A, int U, int Kxp, const int32_t* __
   const int i = (int)(idx / per), j = (int)(idx % per);
   const int a = ids[i];
   if (j < U) {
-    hpre[(size_t)i * U + j] = th[(size_t)a * U + j];
+    const float h = th[(size_t)a * U + j];
+    hpre[(size_t)i * U + j] = h;
     cpre[(size_t)i * U + j] = tc[(size_t)a * U + j];
+    hb[(size_t)i * U + j] = __float2bfloat16_rn(done[i] ? 0.f : h);   // reset on done (C15)
     return;
   }
   const int e = j - U;
@@ -114,42 +116,108 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
-// ------------------------------------------------------------------ sample
-// warp per request; lane j holds action j (A <= 32)
-__global__ void infer_sample_kernel(int n, int A, const float* __restrict__ logits,
-                                    const float* __restrict__ uniforms, uint64_t seed,
-                                    uint64_t counter, const int32_t* __restrict__ ids,
-                                    int32_t* __restrict__ action_out, float* __restrict__ blp_out,
-                                    int32_t* __restrict__ tla) {
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i >= n) return;
-  const float z = lane < A ? logits[(size_t)i * A + lane] : -INFINITY;
-  const float mx = warp_max(z);
-  const float e = lane < A ? expf(z - mx) : 0.f;
-  const float se = warp_sum(e);
-  // inclusive prefix sum of probabilities (CDF), fp32, in action order
-  float cdf = e / se;
+// ------------------------------------------------------------------ core + heads + sample
+// The single-step LSTM as one GEMM: gates = [x | h_{t-1}] . [W_x | W_h]^T + b
+// (K = Kxp + U; both operand rows are read through the engine's gather, so no
+// concatenated copy exists), then one CTA per request runs the cell, writes the
+// new state into its table row, the heads (fp32) and the sampling.
+struct GatesFwd {
+  static constexpr bool ASYNC = true;
+  const void* dummy = k_ones_chunk;
+  static constexpr bool A_MN = false, B_MN = false;
+  int M, N, K, kb_per_split;
+  int Kxp, U;
+  const bf16* X;         // [n][Kxp]: fc | onehot(prev a) | clip(r) | 1 | 0-pad
+  const bf16* hb;        // [n][U]: h_{t-1}, zero on done
+  const bf16* wx;        // [4U][Kxp]
+  const bf16* wh;        // [4U][U]
+  const float* bias;
+  float* out;            // [n][4U] pre-activation gates
+  __device__ const void* ptr_a(int m, int k) const {
+    return k < Kxp ? X + (size_t)m * Kxp + k : hb + (size_t)m * U + (k - Kxp);
+  }
+  __device__ const void* ptr_b(int n, int k) const {
+    return k < Kxp ? wx + (size_t)n * Kxp + k : wh + (size_t)n * U + (k - Kxp);
+  }
+  __device__ void store(int m, int n, float v) const { out[(size_t)m * N + n] = v + bias[n]; }
+  static constexpr bool ROW_OUT = true;
+  __device__ float* out_row(int m) const { return out + (size_t)m * N; }
+  __device__ float post(int, int n, float v) const { return v + bias[n]; }
+  static constexpr bool VEC_STORE = true;
+  __device__ void store16(int m, int n0, float (&v)[16]) const {
+    float4* o = reinterpret_cast<float4*>(out + (size_t)m * N + n0);
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const float t = __shfl_up_sync(0xffffffffu, cdf, o);
-    if (lane >= o) cdf += t;
+    for (int q = 0; q < 4; ++q)
+      o[q] = make_float4(v[4 * q] + bias[n0 + 4 * q], v[4 * q + 1] + bias[n0 + 4 * q + 1],
+                         v[4 * q + 2] + bias[n0 + 4 * q + 2], v[4 * q + 3] + bias[n0 + 4 * q + 3]);
   }
-  float u;
-  if (uniforms) {
-    u = uniforms[i];
-  } else {
-    const uint4 r = philox4x32_10(
-        make_uint4((uint32_t)counter, (uint32_t)(counter >> 32), (uint32_t)ids[i], 0u),
-        make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-    u = (float)(r.x >> 8) * (1.f / 16777216.f);
+};
+
+constexpr int ICH_THREADS = 256;   // = LSTM_U: thread j owns hidden unit j
+
+// CTA i = request i: cell (gate order i, f, g, o; c reset on done, C15), new (h, c)
+// into table row ids[i]; logits | value = W h + b (fp32, fixed-order block sum);
+// warp 0 samples a = min{j : u < CDF_j} (C18) and writes the behaviour log-prob.
+__global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
+    int A, const float* __restrict__ gates, const float* __restrict__ cpre,
+    const uint8_t* __restrict__ done, const int32_t* __restrict__ ids, const float* __restrict__ hw,
+    const float* __restrict__ hbias, const float* __restrict__ uniforms, uint64_t seed,
+    uint64_t counter, float* __restrict__ th, float* __restrict__ tc, int32_t* __restrict__ tla,
+    int32_t* __restrict__ action_out, float* __restrict__ blp_out, float* __restrict__ logits_out) {
+  constexpr int U = LSTM_U, NW = ICH_THREADS / 32;
+  const int i = blockIdx.x, j = threadIdx.x, warp = j >> 5, lane = j & 31;
+  const int A1 = A + 1;
+  __shared__ float red[NW][33];
+  __shared__ float lg[33];
+  const float* g = gates + (size_t)i * 4 * U;
+  const float c0 = done[i] ? 0.f : cpre[(size_t)i * U + j];
+  const float gi = sigm(g[j]), gf = sigm(g[U + j]), gg = tanh_fast(g[2 * U + j]), go = sigm(g[3 * U + j]);
+  const float c = gf * c0 + gi * gg;
+  const float h = go * tanh_fast(c);
+  const int a = ids[i];
+  th[(size_t)a * U + j] = h;
+  tc[(size_t)a * U + j] = c;
+  for (int o = 0; o < A1; ++o) {
+    const float v = warp_sum(h * __ldg(hw + (size_t)o * U + j));
+    if (lane == 0) red[warp][o] = v;
   }
-  const unsigned hit = __ballot_sync(0xffffffffu, lane < A && u < cdf);
-  const int a = hit ? (__ffs(hit) - 1) : A - 1;
-  const float za = __shfl_sync(0xffffffffu, z, a);
-  if (lane == 0) {
-    action_out[i] = a;
-    blp_out[i] = za - mx - logf(se);
-    tla[ids[i]] = a;
+  __syncthreads();
+  if (j < A1) {
+    float t = __ldg(hbias + j);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += red[w][j];   // fixed order
+    lg[j] = t;
+    if (logits_out && j < A) logits_out[(size_t)i * A + j] = t;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const float z = lane < A ? lg[lane] : -INFINITY;
+    const float mx = warp_max(z);
+    const float e = lane < A ? expf(z - mx) : 0.f;
+    const float se = warp_sum(e);
+    float cdf = e / se;   // inclusive prefix sum of the probabilities, fp32, action order
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float t = __shfl_up_sync(0xffffffffu, cdf, o);
+      if (lane >= o) cdf += t;
+    }
+    float u;
+    if (uniforms) {
+      u = uniforms[i];
+    } else {
+      const uint4 r = philox4x32_10(
+          make_uint4((uint32_t)counter, (uint32_t)(counter >> 32), (uint32_t)a, 0u),
+          make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+      u = (float)(r.x >> 8) * (1.f / 16777216.f);
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, lane < A && u < cdf);
+    const int act = hit ? (__ffs(hit) - 1) : A - 1;
+    const float za = __shfl_sync(0xffffffffu, z, act);
+    if (lane == 0) {
+      action_out[i] = act;
+      blp_out[i] = za - mx - logf(se);
+      tla[a] = act;
+    }
   }
 }
 
@@ -318,7 +386,8 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
     const int64_t tot = (int64_t)n * (U + p.Kxp - 256);
     infer_pre_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(
         n, A, U, p.Kxp, actor_ids, reward, done, table->h, table->c, table->last_action,
-        (float*)at(w.hpre), (float*)at(w.cpre), (int32_t*)at(w.prev), (bf16*)at(w.X));
+        (float*)at(w.hpre), (float*)at(w.cpre), (int32_t*)at(w.prev), (bf16*)at(w.X),
+        (bf16*)at(w.hb));
   }
   SEED_TRY(shallow_s2d_forward(shallow_s2d_geometry(p.H, p.W, p.C), n, obs, lowp + p.im_conv1,
                                params + p.t[p.i_conv1b].off, lowp + p.im_conv2,
@@ -332,28 +401,17 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
     SEED_TRY(launch_gemm<128>(pr, pick_splits(pr.M, pr.N, 128, pr.K), st, splitk));
   }
   {
-    XprojFwd pr{};
-    pr.M = n; pr.N = 4 * U; pr.K = p.Kxp;
-    pr.X = (const bf16*)at(w.X); pr.w = lowp + p.im_wx;
+    GatesFwd pr{};
+    pr.M = n; pr.N = 4 * U; pr.K = p.Kxp + U; pr.Kxp = p.Kxp; pr.U = U;
+    pr.X = (const bf16*)at(w.X); pr.hb = (const bf16*)at(w.hb);
+    pr.wx = lowp + p.im_wx; pr.wh = lowp + p.im_wh;
     pr.bias = params + p.t[p.i_lb].off; pr.out = (float*)at(w.xproj);
     SEED_TRY(launch_gemm<128>(pr, pick_splits(pr.M, pr.N, 128, pr.K), st, splitk));
   }
-  {
-    LstmFwdArgs la{};
-    la.B = n; la.T1 = 1;
-    la.xproj = (const float*)at(w.xproj);
-    la.wh = lowp + p.im_wh;
-    la.h0 = table->h; la.c0 = table->c; la.state_rows = actor_ids;
-    la.done = done;
-    la.H = (float*)at(w.H);
-    la.hT = table->h; la.cT = table->c;
-    SEED_TRY(lstm_forward(la, st));
-  }
-  float* logits = logits_out ? logits_out : (float*)at(w.logits);
-  SEED_TRY(launch_dense_fwd(n, U, A + 1, (const float*)at(w.H), params + p.t[p.i_hw].off,
-                            params + p.t[p.i_hb].off, logits, A, (float*)at(w.values), 0, st));
-  infer_sample_kernel<<<ceil_div(n * 32, 256), 256, 0, st>>>(
-      n, A, logits, uniforms, seed, counter, actor_ids, action_out, blp_out, table->last_action);
+  infer_cell_heads_kernel<<<n, ICH_THREADS, 0, st>>>(
+      A, (const float*)at(w.xproj), (const float*)at(w.cpre), done, actor_ids,
+      params + p.t[p.i_hw].off, params + p.t[p.i_hb].off, uniforms, seed, counter, table->h, table->c,
+      table->last_action, action_out, blp_out, logits_out);
   if (store) {
     const int64_t obs16 = (int64_t)p.H * p.W * p.C / 16;
     infer_store_obs_kernel<<<(int)std::min<int64_t>((n * obs16 + 255) / 256, 148 * 8), 256, 0,

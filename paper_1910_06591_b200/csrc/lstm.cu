@@ -48,26 +48,6 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-// ex2 / rcp.approx activations (MUFU.EX2 + MUFU.RCP, no IEEE-division slow
-// path on the serial critical path); the cell is fp32 and these are within a
-// few ulp of the libm versions (relative 2^-15 for |x| << 1 in tanh), far below
-// the bf16 rounding of the recurrent operands.
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-// Activations on the SFU's tanh.approx.f32 (one MUFU op; max rel. error ~2^-11, far
-// inside the bf16 tolerance C22): sigmoid(x) = 0.5 * tanh(0.5 x) + 0.5.  The cell
-// does 5 activations per element, so MUFU issue (16 / clk / SM) bounds the step's
-// cell phase: 1 op each instead of ex2 + rcp (2) halves it.
-__device__ __forceinline__ float tanh_fast(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float sigm(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
-
 // CTA r's W_h slice: local row lc = gate*32 + j  <-  global row gate*U + 32r + j.
 // cp.async (16 B, L2 only), 16 chunks per thread (blockDim 256), left in flight:
 // the caller overlaps its other setup loads and calls cp_async_wait_all().

@@ -36,6 +36,17 @@ struct LstmBwdArgs {
   __nv_bfloat16* dG;           // out [B*T1][4U] dL/d(pre-activation gates), bf16
 };
 
+// Activations on the SFU's tanh.approx.f32 (one MUFU op; max rel. error ~2^-11, far
+// inside the bf16 tolerance C22): sigmoid(x) = 0.5 * tanh(0.5 x) + 0.5.  Shared by
+// the cluster kernels and the inference cell (infer.cu), so the policy that acts
+// and the learner's recomputation use the same cell arithmetic.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigm(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
+
 seed_status lstm_forward(const LstmFwdArgs& a, cudaStream_t st);
 seed_status lstm_backward(const LstmBwdArgs& a, cudaStream_t st);
 
