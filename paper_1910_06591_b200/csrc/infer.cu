@@ -79,6 +79,7 @@ __global__ void infer_pre_kernel(int n, int A, int U, int Kxp, const int32_t* __
                                  const int32_t* __restrict__ tla, float* __restrict__ hpre,
                                  float* __restrict__ cpre, int32_t* __restrict__ prev,
                                  __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ hb) {
+  pdl_wait();
   const int E = Kxp - 256;
   const int per = U + E;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
     const float* __restrict__ hbias, const float* __restrict__ uniforms, uint64_t seed,
     uint64_t counter, float* __restrict__ th, float* __restrict__ tc, int32_t* __restrict__ tla,
     int32_t* __restrict__ action_out, float* __restrict__ blp_out, float* __restrict__ logits_out) {
+  pdl_wait();
   constexpr int U = LSTM_U, NW = ICH_THREADS / 32;
   const int i = blockIdx.x, j = threadIdx.x, warp = j >> 5, lane = j & 31;
   const int A1 = A + 1;
@@ -384,10 +386,10 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
   float* splitk = (float*)at(w.splitk);
   {
     const int64_t tot = (int64_t)n * (U + p.Kxp - 256);
-    infer_pre_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(
-        n, A, U, p.Kxp, actor_ids, reward, done, table->h, table->c, table->last_action,
-        (float*)at(w.hpre), (float*)at(w.cpre), (int32_t*)at(w.prev), (bf16*)at(w.X),
-        (bf16*)at(w.hb));
+    SEED_TRY(launch_k(infer_pre_kernel, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, n, A, U,
+                      p.Kxp, actor_ids, reward, done, (const float*)table->h, (const float*)table->c,
+                      (const int32_t*)table->last_action, (float*)at(w.hpre), (float*)at(w.cpre),
+                      (int32_t*)at(w.prev), (bf16*)at(w.X), (bf16*)at(w.hb)));
   }
   SEED_TRY(shallow_s2d_forward(shallow_s2d_geometry(p.H, p.W, p.C), n, obs, lowp + p.im_conv1,
                                params + p.t[p.i_conv1b].off, lowp + p.im_conv2,
@@ -408,10 +410,10 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
     pr.bias = params + p.t[p.i_lb].off; pr.out = (float*)at(w.xproj);
     SEED_TRY(launch_gemm<128>(pr, pick_splits(pr.M, pr.N, 128, pr.K), st, splitk));
   }
-  infer_cell_heads_kernel<<<n, ICH_THREADS, 0, st>>>(
-      A, (const float*)at(w.xproj), (const float*)at(w.cpre), done, actor_ids,
-      params + p.t[p.i_hw].off, params + p.t[p.i_hb].off, uniforms, seed, counter, table->h, table->c,
-      table->last_action, action_out, blp_out, logits_out);
+  SEED_TRY(launch_k(infer_cell_heads_kernel, dim3(n), dim3(ICH_THREADS), 0, st, A,
+                    (const float*)at(w.xproj), (const float*)at(w.cpre), done, actor_ids,
+                    params + p.t[p.i_hw].off, params + p.t[p.i_hb].off, uniforms, seed, counter,
+                    table->h, table->c, table->last_action, action_out, blp_out, logits_out));
   if (store) {
     const int64_t obs16 = (int64_t)p.H * p.W * p.C / 16;
     infer_store_obs_kernel<<<(int)std::min<int64_t>((n * obs16 + 255) / 256, 148 * 8), 256, 0,
