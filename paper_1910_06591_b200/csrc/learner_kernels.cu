@@ -576,72 +576,6 @@ __global__ void core_extras_kernel(int F, int A, int Kxp, const int32_t* __restr
   X[(size_t)f * Kxp + 256 + j] = __float2bfloat16_rn(v);
 }
 
-// ------------------------------------------------------------------ column sums
-// out[c] = sum_r X[r][c] (bf16 X, C in {16, 32}): each block sums a contiguous row
-// range with 16-byte loads (8 columns per thread), writes its partial, and the
-// last block to finish (integer ticket) adds the partials in block order —
-// deterministic, one launch.
-__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ X, int64_t R,
-                                                     int C, float* __restrict__ part,
-                                                     unsigned* ticket, float* __restrict__ out) {
-  pdl_wait();
-  const int G = C / 8;                         // 16-byte groups per row
-  const int RL = 256 / G;                      // rows in flight per block
-  const int grp = threadIdx.x % G, rl = threadIdx.x / G;
-  const int64_t per = (R + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = blockIdx.x * per, r1 = min(R, r0 + per);
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int64_t r = r0 + rl; r < r1; r += RL) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(X + r * C) + grp);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      acc[2 * q] += bf16_lo(w[q]);
-      acc[2 * q + 1] += bf16_hi(w[q]);
-    }
-  }
-  __shared__ float sh[256][9];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) sh[threadIdx.x][q] = acc[q];
-  __syncthreads();
-  if (threadIdx.x < C) {
-    const int c = threadIdx.x, g0 = c / 8, e = c % 8;
-    float t = 0.f;
-    for (int k = 0; k < RL; ++k) t += sh[k * G + g0][e];
-    part[blockIdx.x * C + c] = t;
-  }
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    // thread (g, c): partials k = g, g+RG, ... of column c; then RG group sums in order
-    const int RG = 256 / C, g2 = threadIdx.x / C, c2 = threadIdx.x % C;
-    float t = 0.f;
-    for (int k = g2; k < (int)gridDim.x; k += RG) t += part[k * C + c2];
-    __shared__ float red[256];
-    red[threadIdx.x] = t;
-    __syncthreads();
-    if (threadIdx.x < C) {
-      float u = 0.f;
-      for (int k = 0; k < RG; ++k) u += red[k * C + threadIdx.x];
-      out[threadIdx.x] = u;
-      if (threadIdx.x == 0) *ticket = 0;   // re-arm for the next use
-    }
-  }
-}
-
-seed_status colsum_bf16(const __nv_bfloat16* X, int64_t R, int C, float* part, float* out,
-                        cudaStream_t st) {
-  if (C % 8 || C > 64) return SEED_E_SHAPE;
-  unsigned* ticket = reinterpret_cast<unsigned*>(part + COLSUM_BLOCKS * 64);
-  colsum_kernel<<<COLSUM_BLOCKS, 256, 0, st>>>(X, R, C, part, ticket, out);
-  return last_launch();
-}
 
 // ------------------------------------------------------------------ K9 clip + Adam
 __device__ __forceinline__ double block_sum_double(double v, double* sh8) {

@@ -69,9 +69,6 @@ __global__ void core_extras_kernel(int F, int A, int Kxp, const int32_t* __restr
                                    const float* __restrict__ reward,
                                    const uint8_t* __restrict__ done, __nv_bfloat16* X);
 
-// out[c] = sum_r X[r][c] (bf16 input), deterministic two-phase.
-seed_status colsum_bf16(const __nv_bfloat16* X, int64_t R, int C, float* part, float* out,
-                        cudaStream_t st);
 
 struct AdamArgs {
   int64_t P;

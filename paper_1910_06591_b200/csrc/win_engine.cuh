@@ -163,7 +163,9 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
       const uint32_t base = smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * TM + mn, RB);
       // descriptors advance linearly with the start address (field = addr >> 4)
       const uint64_t ad0 = umma_desc(base, 16, 8 * RB, LAYOUT);
-#pragma unroll
+      // fully unrolled unless that would exceed 36 MMAs (register spills)
+      constexpr int MT_UNROLL = MT * NW * (RB / 32) > 36 ? 1 : MT;
+#pragma unroll MT_UNROLL
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int w = 0; w < NW; ++w)
