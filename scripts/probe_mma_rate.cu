@@ -56,7 +56,7 @@ __global__ void rate_w(int layout_a, int rb_a, int reps, int nacc, long long* ou
   if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc(tbase, 256); }
 }
 
-template <int N>
+template <int N, int M = 128>
 __global__ void rate(int layout_a, int rb_a, int a_mn, int reps, long long* out) {
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
@@ -70,7 +70,7 @@ __global__ void rate(int layout_a, int rb_a, int a_mn, int reps, long long* out)
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0) {
-    const uint32_t idesc = umma_idesc_bf16(128, N, a_mn != 0, false);
+    const uint32_t idesc = umma_idesc_bf16(M, N, a_mn != 0, false);
     const uint32_t A = smem_u32(sm), Bm = smem_u32(sm + 32768);
     // A: K-major: SBO = 8 rows * rb; MN-major: LBO = atom stride (rb * 1 row, the
     // shifted-window pattern), SBO = 8 k-rows * rb
@@ -91,18 +91,68 @@ __global__ void rate(int layout_a, int rb_a, int a_mn, int reps, long long* out)
   if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc(tbase, 256); }
 }
 
-template <int N>
+template <int N, int M = 128>
 void run(const char* name, int layout, int rb, int mn, long long* d) {
   const int reps = 512;
-  cudaFuncSetAttribute(rate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  rate<N><<<148, 128, 100 * 1024>>>(layout, rb, mn, reps, d);
+  cudaFuncSetAttribute(rate<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  rate<N, M><<<148, 128, 100 * 1024>>>(layout, rb, mn, reps, d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double s = 0;
   for (int i = 0; i < 148; ++i) s += h[i];
-  printf("%-14s N=%3d: %7.1f cycles / MMA  (%s)\n", name, N, s / 148 / (reps * 8.0),
+  printf("%-14s M=%3d N=%3d: %7.1f cycles / MMA  (%s)\n", name, M, N, s / 148 / (reps * 8.0),
          e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+}
+
+// NI issuing warps, each one elected lane issuing into its own accumulator
+template <int N, int NI>
+__global__ void rate_multi(int reps, long long* out) {
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar[4];
+  __shared__ uint32_t tbase;
+  for (int i = threadIdx.x; i < 64 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sm)[i] = make_uint4(0x3F803F80u, 0, 0x3F803F80u, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1); fence_mbar_init(); }
+  if (threadIdx.x < 32) tmem_alloc(&tbase, 256);
+  __syncthreads();
+  tc_fence_after();
+  const int warp = threadIdx.x >> 5;
+  long long t0 = clock64();
+  if (warp < NI) {
+    const uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+    const uint32_t A = smem_u32(sm + warp * 8192), Bm = smem_u32(sm + 40960);
+    const uint64_t ad = umma_desc(A, 16, 8 * 32, 6);
+    const uint64_t bd = umma_desc(Bm, 16, 1024, 2);
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        tc_mma_bf16_w(tbase + (uint32_t)(warp * 64), ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, 1);
+    }
+    tc_commit_w(&bar[warp]);
+    mbar_wait(&bar[warp], 0);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  __syncthreads();
+  if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc(tbase, 256); }
+}
+
+template <int N, int NI>
+void run_multi(long long* d) {
+  const int reps = 512;
+  cudaFuncSetAttribute(rate_multi<N, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  rate_multi<N, NI><<<148, 128, 100 * 1024>>>(reps, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double s = 0;
+  for (int i = 0; i < 148; ++i) s += h[i];
+  printf("issuers=%d N=%3d: %7.1f cycles per MMA (all issuers)  (%s)\n", NI, N,
+         s / 148 / (reps * 8.0 * NI), e == cudaSuccess ? "ok" : cudaGetErrorString(e));
 }
 
 template <int N>
@@ -138,6 +188,15 @@ int main() {
   run<64>("K SW128", 2, 128, 0, d);
   run<128>("K SW128", 2, 128, 0, d);
   run<256>("K SW128", 2, 128, 0, d);
+  run_multi<16, 1>(d);
+  run_multi<16, 2>(d);
+  run_multi<16, 4>(d);
+  run_multi<48, 2>(d);
+  run<48>("MN SW32", 6, 32, 1, d);
+  run<48, 64>("MN SW32", 6, 32, 1, d);
+  run<96>("MN SW64", 4, 64, 1, d);
+  run<96, 64>("MN SW64", 4, 64, 1, d);
+  run<16, 64>("K SW32", 6, 32, 0, d);
   run_w<16>("K SW32", 6, 32, 1, d);
   run_w<16>("K SW32", 6, 32, 2, d);
   run_w<16>("K SW32", 6, 32, 4, d);
