@@ -22,8 +22,14 @@
  * Layout:    batch-major, trajectory-contiguous, row-major: [B][T] and
  *            [B][T+1][...]; bootstrap values separate [B].  16-byte aligned
  *            pointers are required (torch allocations satisfy this).
- * Threads:   no global mutable state; calls on different streams with disjoint
- *            buffers are independent.
+ * Threads:   no global mutable state: the second stream and events a learner step
+ *            branches onto belong to a caller-owned seed_exec, the NCCL comms to a
+ *            caller-owned seed_comm.  The only process-wide data are idempotent
+ *            per-device caches (kernel shared-memory opt-ins, SM counts) and
+ *            read-once environment switches (SEED_PDL, SEED_DP_BUCKETS).  Calls on
+ *            different streams with disjoint buffers (and distinct seed_exec /
+ *            seed_comm handles) are independent; one process may drive several
+ *            devices (each call runs on the device current at the call).
  */
 #ifndef SEED_H_
 #define SEED_H_
@@ -90,8 +96,9 @@ seed_status seed_vtrace(int T, int B,
  *      heads.w[A+1][U] heads.b[A+1]       (rows 0..A-1 logits, row A value)
  *  SEED_NET_IMPALA_DEEP / SEED_NET_GFOOTBALL (configs[2]/[3]): per section s
  *      s{s}.conv.w[ch][3][3][cin] .b, then res{0,1}.conv{0,1}.w[ch][3][3][ch] .b;
- *      then fc / lstm / heads as above.  (Declared; this build returns
- *      SEED_E_UNSUPPORTED for their learner/infer calls.)
+ *      then fc / lstm / heads as above.  seed_learner_step supports every
+ *      kind; seed_infer supports SEED_NET_ATARI_SHALLOW (configs[4]) and returns
+ *      SEED_E_UNSUPPORTED for the others.
  *  Observations enter as obs/255 (uint8 nets).  LSTM core input
  *  x_t = [fc_t, onehot(prev_action_t), clip(reward_t,-1,1)], one-hot and reward
  *  zeroed when done_t, and (h,c) reset to 0 before step t when done_t
@@ -157,6 +164,14 @@ typedef struct {
   const float* c0;             /* [B][U]                                        */
 } seed_batch;
 
+/* params, grads, adam_m, adam_v, params_lowp and obs must be 16-byte aligned
+ * (float4 / bulk-copy accesses); SEED_E_ARG otherwise.
+ * params_lowp is rewritten in place by every applied update (inside the clip +
+ * Adam kernel, on `stream`).  A seed_infer reading the same params_lowp on
+ * another stream must be ordered against the step by the caller; for
+ * inference running concurrently with training use the versioned snapshot
+ * (seed_param_publish / seed_param_acquire below), which never exposes a
+ * half-written update. */
 typedef struct {
   float* params;       /* [P] fp32 master (flat layout above)          */
   float* grads;        /* [P] fp32: receives the (allreduced, unclipped) grads */
@@ -167,6 +182,17 @@ typedef struct {
 } seed_train_state;
 
 typedef struct seed_comm seed_comm;  /* wraps an ncclComm_t */
+
+/* Execution context of a learner step (caller-owned; create on the device the
+ * steps run on): a second CUDA stream of that device and the events of the
+ * fork / join edges, onto which the step branches its independent backward
+ * GEMMs (inside a CUDA-graph capture the edges become parallel graph branches).
+ * One seed_exec must not be used by two steps at the same time.
+ * seed_learner_step == seed_learner_step_ex with exec = NULL: everything on
+ * `stream`, in order (same results; no overlap of the branches). */
+typedef struct seed_exec seed_exec;
+seed_status seed_exec_create(seed_exec** out);
+seed_status seed_exec_destroy(seed_exec* exec);
 
 seed_status seed_learner_workspace_size(const seed_net_spec* spec, int T, int B,
                                         size_t* bytes_out);
@@ -180,6 +206,11 @@ seed_status seed_learner_step(const seed_net_spec* spec, int T, int B,
                               const seed_hparams* hp, seed_comm* comm,
                               void* workspace, size_t ws_bytes, float* metrics,
                               void* stream);
+seed_status seed_learner_step_ex(const seed_net_spec* spec, int T, int B,
+                                 const seed_batch* batch, const seed_train_state* state,
+                                 const seed_hparams* hp, seed_comm* comm, seed_exec* exec,
+                                 void* workspace, size_t ws_bytes, float* metrics,
+                                 void* stream);
 /* Bench / profiling hook: identical to seed_learner_step, and additionally
  * records events[0] (cudaEvent_t as void*) before the first kernel and
  * events[i] after the i-th phase of the step (a phase = one kernel, or a
@@ -230,8 +261,10 @@ seed_status seed_comm_allreduce_f32(seed_comm* comm, float* data, int64_t n, voi
  *     kernel: copy in -> cross-GPU arrival counters -> each rank sums its 1/N
  *     slice over the ranks in rank order and writes it into every rank's
  *     buffer -> counters -> copy out.  Results are bit-identical on all ranks.
- * Waits are bounded (2 s): on timeout the kernel sets a device error flag that
- * seed_comm_peer_status reports (SEED_E_NCCL) instead of hanging.
+ * Waits are bounded (2 s): on timeout the kernel sets a sticky device error flag
+ * that seed_comm_peer_status reports (SEED_E_NCCL) instead of hanging, and
+ * poisons the (partial) result with NaN, so a learner step's global norm is
+ * non-finite and the update is skipped (metrics[7] = 1).
  * All ranks must call every allreduce in the same order. */
 seed_status seed_comm_peer_setup(seed_comm* comm, int64_t max_floats, void* handle_out /* 64 B */);
 seed_status seed_comm_peer_open(seed_comm* comm, const void* handles /* world*64 B */);
@@ -250,6 +283,10 @@ seed_status seed_comm_peer_status(seed_comm* comm);   /* synchronizes; SEED_OK o
  * store: nullable unroll store; each step is recorded (C17, C19) and completed
  *   unrolls (T+1 slots, slot T copied into slot 0 of the next) are pushed to
  *   the ready ring.
+ * actor_ids: must be unique within a call.  An id outside [0, num_actors) is
+ *   reported on the device, not trusted: that request reads no table row,
+ *   writes nothing (table, store), and gets action_out = -1, behaviour_logp_out
+ *   (and its logits_out row) = NaN.
  * ======================================================================== */
 typedef struct {
   float* h;              /* [num_actors][U] */
@@ -272,9 +309,21 @@ typedef struct {
   int32_t* fill;           /* [num_actors]  slots filled in the current buffer */
   int32_t* cur;            /* [num_actors]  current buffer 0/1                */
   int32_t* ready_ring;     /* [ring_capacity] entries actor*2 + buffer        */
-  int32_t* ready_count;    /* device int32[2]: {pushed total, consumed total} */
+  int32_t* ready_count;    /* device int32[4]: {pushed total, consumed total,
+                              stale unrolls assembled, short assembles}       */
   int ring_capacity;
+  int32_t* gen;            /* [num_actors][2] buffer generations (zeroed)     */
+  int32_t* ready_gen;      /* [ring_capacity] generation of each ring entry   */
 } seed_unroll_store;
+/* Lifetime (C29): each actor has two unroll buffers.  A completed unroll stays
+ * valid until the actor completes its NEXT unroll (T more steps): from then on
+ * its buffer is refilled.  The learner must assemble it before that, and the
+ * ring must not wrap over unconsumed entries (ring_capacity >= the number of
+ * unrolls pushed but not yet assembled).  seed_assemble_batch checks both on the
+ * device: an entry whose buffer was reused since it was pushed (generation
+ * mismatch) increments ready_count[2]; asking for more unrolls than are pushed
+ * and unconsumed increments ready_count[3].  The batch is still written (the
+ * counters are the report; nothing forces a host sync). */
 
 seed_status seed_infer_workspace_size(const seed_net_spec* spec, int max_n, size_t* bytes_out);
 seed_status seed_infer(const seed_net_spec* spec, const void* params_lowp, const float* params,
@@ -290,6 +339,41 @@ seed_status seed_infer(const seed_net_spec* spec, const void* params_lowp, const
  * unrolls already pushed (host-visible count). */
 seed_status seed_assemble_batch(const seed_unroll_store* store, int obs_bytes, int lstm_units,
                                 int B, const seed_batch* out, void* stream);
+
+/* ===========================================================================
+ * Versioned parameter snapshots: inference concurrent with training (SURVEY
+ * §8(f) row 2; P:98, P:111 inference with the latest parameters
+ * inference on cores of its own while the learner trains; S:37-42 the version
+ * is ParamSnapshot.version, S:109 / S:465 single-copy semantics).
+ * A single-producer (learner) / single-consumer (inference) triple buffer in
+ * device memory: three slots of seed_param_snapshot_bytes() bytes each (the
+ * params_lowp image, then the fp32 params), their versions, and an index word.
+ * seed_param_publish (producer's stream, after seed_learner_step): copies
+ *   params_lowp + params into the producer's slot, stamps version = *step,
+ *   and hands the slot over with one atomic exchange.
+ * seed_param_acquire (consumer's stream, before seed_infer): takes the latest
+ *   handed-over slot with one atomic exchange when there is a newer one, and
+ *   copies it into the consumer's private lowp_out / params_out (which
+ *   seed_infer then reads) when it changed (always if force_copy != 0);
+ *   *version_out (nullable, device int64) = the version now held.
+ * Neither side waits for the other; a slot the consumer can read is never
+ * written, so inference always runs on one whole update (never a torn one)
+ * and on the newest one published before its acquire.  One producer stream and
+ * one consumer stream per snapshot.  Call seed_param_snapshot_init once
+ * (version -1 = nothing published yet).
+ * ======================================================================== */
+typedef struct {
+  void* slots[3];          /* device, seed_param_snapshot_bytes() each, 16-B aligned */
+  int32_t* state;          /* device int32[4] (library-private index word)        */
+  int64_t* version;        /* device int64[3]: version held by each slot           */
+} seed_param_snapshot;
+seed_status seed_param_snapshot_bytes(const seed_net_spec* spec, size_t* slot_bytes);
+seed_status seed_param_snapshot_init(seed_param_snapshot* snap, void* stream);
+seed_status seed_param_publish(const seed_net_spec* spec, const seed_train_state* state,
+                               seed_param_snapshot* snap, void* stream);
+seed_status seed_param_acquire(const seed_net_spec* spec, seed_param_snapshot* snap,
+                               void* lowp_out, float* params_out, int64_t* version_out,
+                               int force_copy, void* stream);
 
 /* ===========================================================================
  * Test / benchmark hooks (not part of the method):

@@ -42,7 +42,12 @@ class UnrollStore(C.Structure):
     _fields_ = [("T", c_int), ("num_actors", c_int)] + \
         [(n, c_void_p) for n in ("obs", "action", "prev_action", "reward", "done",
                                  "behaviour_logp", "h0", "c0", "fill", "cur", "ready_ring",
-                                 "ready_count")] + [("ring_capacity", c_int)]
+                                 "ready_count")] + [("ring_capacity", c_int), ("gen", c_void_p),
+                                                    ("ready_gen", c_void_p)]
+
+
+class ParamSnapshot(C.Structure):
+    _fields_ = [("slots", c_void_p * 3), ("state", c_void_p), ("version", c_void_p)]
 
 
 _SIGS = {
@@ -59,6 +64,16 @@ _SIGS = {
     "seed_learner_step": (c_int, [P(NetSpec), c_int, c_int, P(Batch), P(TrainState),
                                   P(HParams), c_void_p, c_void_p, c_size_t, c_void_p,
                                   c_void_p]),
+    "seed_exec_create": (c_int, [P(c_void_p)]),
+    "seed_exec_destroy": (c_int, [c_void_p]),
+    "seed_learner_step_ex": (c_int, [P(NetSpec), c_int, c_int, P(Batch), P(TrainState),
+                                     P(HParams), c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
+                                     c_void_p]),
+    "seed_param_snapshot_bytes": (c_int, [P(NetSpec), P(c_size_t)]),
+    "seed_param_snapshot_init": (c_int, [P(ParamSnapshot), c_void_p]),
+    "seed_param_publish": (c_int, [P(NetSpec), P(TrainState), P(ParamSnapshot), c_void_p]),
+    "seed_param_acquire": (c_int, [P(NetSpec), P(ParamSnapshot), c_void_p, c_void_p, c_void_p,
+                                   c_int, c_void_p]),
     "seed_learner_step_traced": (c_int, [P(NetSpec), c_int, c_int, P(Batch), P(TrainState),
                                          P(HParams), c_void_p, c_void_p, c_size_t, c_void_p,
                                          c_void_p, P(c_void_p), c_int, P(C.c_char_p), P(c_int),

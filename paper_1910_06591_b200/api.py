@@ -253,7 +253,21 @@ class Learner:
         self.ws = torch.empty(max(nb.value, 16), dtype=torch.uint8, device=device)
         self.metrics = torch.zeros(8, dtype=torch.float32, device=device)
         self._spec_c = spec.c()
+        # caller-owned execution context (second stream + fork/join events) on this device
+        h = C.c_void_p()
+        with torch.cuda.device(self.params.device):
+            L.check(lib.seed_exec_create(C.byref(h)), "seed_exec_create")
+        self._exec = h
         self.refresh_lowp()
+
+    def __del__(self):
+        h = getattr(self, "_exec", None)
+        if h is not None and h.value:
+            try:
+                L.load().seed_exec_destroy(h)
+            except Exception:  # noqa: BLE001 (interpreter shutdown)
+                pass
+            self._exec = None
 
     def refresh_lowp(self, stream=None):
         L.check(L.load().seed_net_refresh_lowp(C.byref(self._spec_c), _ptr(self.params),
@@ -278,19 +292,30 @@ class Learner:
         return L.Batch(*(_ptr(batch.get(k)) for k in ("obs", "action", "prev_action", "reward",
                                                       "done", "behaviour_logp", "h0", "c0")))
 
+    def _train_state(self):
+        return L.TrainState(_ptr(self.params), _ptr(self.grads), _ptr(self.m), _ptr(self.v),
+                            _ptr(self.lowp), _ptr(self.step_counter))
+
     def step(self, batch, stream=None):
-        """One seed_learner_step (asynchronous); returns the device metrics[8]."""
+        """One seed_learner_step_ex (asynchronous); returns the device metrics[8]."""
         cb = self._batch(batch)
-        ts = L.TrainState(_ptr(self.params), _ptr(self.grads), _ptr(self.m), _ptr(self.v),
-                          _ptr(self.lowp), _ptr(self.step_counter))
+        ts = self._train_state()
         hp = self.hp.c()
-        st = L.load().seed_learner_step(C.byref(self._spec_c), self.T, self.B, C.byref(cb),
-                                        C.byref(ts), C.byref(hp),
-                                        self.comm.handle if self.comm else None,
-                                        _ptr(self.ws), self.ws.numel(), _ptr(self.metrics),
-                                        _stream(stream))
-        L.check(st, "seed_learner_step")
+        st = L.load().seed_learner_step_ex(C.byref(self._spec_c), self.T, self.B, C.byref(cb),
+                                           C.byref(ts), C.byref(hp),
+                                           self.comm.handle if self.comm else None, self._exec,
+                                           _ptr(self.ws), self.ws.numel(), _ptr(self.metrics),
+                                           _stream(stream))
+        L.check(st, "seed_learner_step_ex")
         return self.metrics
+
+    def publish(self, snapshot, stream=None):
+        """seed_param_publish: hand the current parameters (version = step counter)
+        to a ParamSnapshot's consumer, on `stream` after the step."""
+        ts = self._train_state()
+        L.check(L.load().seed_param_publish(C.byref(self._spec_c), C.byref(ts),
+                                            C.byref(snapshot.c), _stream(stream)),
+                "seed_param_publish")
 
     def debug_buffer(self, name, dtype, shape):
         """Test hook: a torch view of an internal workspace buffer (seed_learner_debug_buffer)."""
@@ -321,12 +346,29 @@ class Learner:
                 view(ptrs[3], (B, T1 - 1)))
 
 
+class ParamSnapshot:
+    """Device triple buffer for versioned parameter publication (include/seed.h
+    seed_param_*): one producer (Learner.publish) and one consumer
+    (InferenceServer with snapshot=...)."""
+
+    def __init__(self, spec, device="cuda", stream=None):
+        lib = L.load()
+        nb = C.c_size_t()
+        L.check(lib.seed_param_snapshot_bytes(C.byref(spec.c()), C.byref(nb)), "snapshot_bytes")
+        self.slots = [torch.zeros(nb.value, dtype=torch.uint8, device=device) for _ in range(3)]
+        self.state = torch.zeros(4, dtype=torch.int32, device=device)
+        self.version = torch.zeros(3, dtype=torch.int64, device=device)
+        self.c = L.ParamSnapshot((C.c_void_p * 3)(*[t.data_ptr() for t in self.slots]),
+                                 _ptr(self.state), _ptr(self.version))
+        L.check(lib.seed_param_snapshot_init(C.byref(self.c), _stream(stream)), "snapshot_init")
+
+
 class InferenceServer:
     """Centralized batched inference (seed_infer) with the per-actor recurrent
     state table and the device unroll store."""
 
     def __init__(self, spec, num_actors, max_n, learner=None, T=None, ring_capacity=None,
-                 device="cuda"):
+                 device="cuda", snapshot=None):
         lib = L.load()
         self.spec, self.num_actors, self.max_n = spec, num_actors, max_n
         U = max(spec.lstm_units, 1)
@@ -340,6 +382,15 @@ class InferenceServer:
         self.ws = torch.empty(max(nb.value, 16), dtype=torch.uint8, device=device)
         self.learner = learner
         self._spec_c = spec.c()
+        # concurrent serving: a private copy of the latest published parameters,
+        # refreshed from the snapshot at the start of every call
+        self.snapshot = snapshot
+        if snapshot is not None:
+            nb = C.c_size_t()
+            L.check(lib.seed_net_lowp_bytes(C.byref(spec.c()), C.byref(nb)), "lowp_bytes")
+            self.lowp = torch.zeros(max(nb.value, 16), dtype=torch.uint8, device=device)
+            self.params = torch.zeros(net_param_count(spec), dtype=torch.float32, device=device)
+            self.version = torch.full((1,), -1, dtype=torch.int64, device=device)
         self.store = None
         if T is not None:
             self._make_store(T, ring_capacity or 4 * num_actors, device)
@@ -357,12 +408,13 @@ class InferenceServer:
                        behaviour_logp=z(NA, 2, T1, dt=torch.float32),
                        h0=z(NA, 2, U, dt=torch.float32), c0=z(NA, 2, U, dt=torch.float32),
                        fill=z(NA, dt=torch.int32), cur=z(NA, dt=torch.int32),
-                       ready_ring=z(cap, dt=torch.int32), ready_count=z(2, dt=torch.int32))
+                       ready_ring=z(cap, dt=torch.int32), ready_count=z(4, dt=torch.int32),
+                       gen=z(NA, 2, dt=torch.int32), ready_gen=z(cap, dt=torch.int32))
         s = self.st
         self.T = T
         self.store = L.UnrollStore(T, NA, *(_ptr(s[k]) for k in (
             "obs", "action", "prev_action", "reward", "done", "behaviour_logp", "h0", "c0",
-            "fill", "cur", "ready_ring", "ready_count")), cap)
+            "fill", "cur", "ready_ring", "ready_count")), cap, _ptr(s["gen"]), _ptr(s["ready_gen"]))
 
     def infer(self, actor_ids, obs, reward, done, uniforms=None, seed=0, counter=0,
               action_out=None, blp_out=None, logits_out=None, stream=None):
@@ -378,8 +430,15 @@ class InferenceServer:
         dev = actor_ids.device
         a = action_out if action_out is not None else torch.empty(n, dtype=torch.int32, device=dev)
         blp = blp_out if blp_out is not None else torch.empty(n, dtype=torch.float32, device=dev)
-        lr = self.learner
-        st = L.load().seed_infer(C.byref(self._spec_c), _ptr(lr.lowp), _ptr(lr.params),
+        lib = L.load()
+        if self.snapshot is not None:
+            L.check(lib.seed_param_acquire(C.byref(self._spec_c), C.byref(self.snapshot.c),
+                                           _ptr(self.lowp), _ptr(self.params), _ptr(self.version),
+                                           0, _stream(stream)), "seed_param_acquire")
+            lowp, params = self.lowp, self.params
+        else:
+            lowp, params = self.learner.lowp, self.learner.params
+        st = lib.seed_infer(C.byref(self._spec_c), _ptr(lowp), _ptr(params),
                                  C.byref(self.table), n, _ptr(actor_ids), _ptr(obs), _ptr(reward),
                                  _ptr(done), _ptr(uniforms), seed, counter, _ptr(a), _ptr(blp),
                                  _ptr(logits_out), C.byref(self.store) if self.store else None,

@@ -27,11 +27,10 @@ struct Nccl {
   Split_t split = nullptr;   // optional (NCCL >= 2.18)
 };
 
-const Nccl& nccl() {
-  static Nccl n;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+// resolved once per process (thread-safe static initialisation)
+static Nccl load_nccl() {
+  Nccl n;
+  {
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (h) {
@@ -43,6 +42,10 @@ const Nccl& nccl() {
       n.ok = n.get_uid && n.init_rank && n.all_reduce && n.destroy;
     }
   }
+  return n;
+}
+const Nccl& nccl() {
+  static const Nccl n = load_nccl();
   return n;
 }
 }  // namespace
@@ -223,6 +226,13 @@ __global__ void __launch_bounds__(PEER_THREADS) peer_allreduce_kernel(const Peer
     for (int u = 0; u < 4; ++u) if (i + u * stride < n4) w4[i + u * stride] = t[u];
   }
   for (int64_t i = 4 * n4 + tid; i < a.n; i += stride) a.data[i] = __ldcv(peer_out(a, a.me) + i);
+  // a barrier timeout (this call or an earlier one: the flag is sticky) leaves the
+  // sum partial: each block poisons the first value it wrote with NaN, so the global
+  // norm is non-finite and clip + Adam skip the update (metrics[7] = 1)
+  if (threadIdx.x == 0 && *(volatile unsigned*)&peer_ctrl(a, a.me)->error) {
+    if (tid < n4) a.data[4 * tid] = __int_as_float(0x7fffffff);
+    else if (4 * n4 + tid < a.n) a.data[4 * n4 + tid] = __int_as_float(0x7fffffff);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) peer_ctrl(a, a.me)->epoch = ep + 1;   // all blocks read ep
 }
 }  // namespace seed

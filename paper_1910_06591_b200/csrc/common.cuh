@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <atomic>
 #include "../../include/seed.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -31,6 +32,45 @@ static inline seed_status last_launch() {
 }
 
 static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------- per-device one-time setup
+// A kernel's dynamic shared-memory opt-in (cudaFuncSetAttribute) applies to the
+// device that is current when it is set, so the "already set" flag is kept per
+// device (bit d of a mask); the SM count is cached per device the same way.  These
+// idempotent caches are the library's only process-wide state (include/seed.h).
+constexpr int SEED_MAX_DEVICES = 64;
+struct PerDevice {
+  std::atomic<uint64_t> mask{0};
+  bool done(int dev) const { return (mask.load(std::memory_order_acquire) >> dev) & 1u; }
+  void set(int dev) { mask.fetch_or(1ull << dev, std::memory_order_acq_rel); }
+};
+static inline int current_device() {
+  int d = 0;
+  return cudaGetDevice(&d) == cudaSuccess ? d : -1;
+}
+template <class Kern>
+static inline seed_status smem_optin(PerDevice& flag, Kern kern, size_t bytes) {
+  const int dev = current_device();
+  if (dev < 0 || dev >= SEED_MAX_DEVICES) return SEED_E_CUDA;
+  if (!flag.done(dev)) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+      return SEED_E_CUDA;
+    flag.set(dev);
+  }
+  return SEED_OK;
+}
+static inline int sm_count() {
+  static std::atomic<int> cache[SEED_MAX_DEVICES];
+  const int dev = current_device();
+  if (dev < 0 || dev >= SEED_MAX_DEVICES) return 148;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
 
 // ---------------------------------------------------------------- programmatic dependent launch
 // Kernels launched through launch_k() carry the programmatic-stream-

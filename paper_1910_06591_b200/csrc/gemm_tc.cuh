@@ -516,16 +516,9 @@ seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullp
   if (splits > nkb) splits = nkb > 0 ? nkb : 1;
   p.kb_per_split = (nkb + splits - 1) / splits;
   splits = nkb > 0 ? (nkb + p.kb_per_split - 1) / p.kb_per_split : 1;
-  static int sms = 0;
-  if (!sms) {
-    if (cudaFuncSetAttribute(gemm_tc_kernel<BN, Prob>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg::SMEM) != cudaSuccess)
-      return SEED_E_CUDA;
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    sms = n;
-  }
+  static PerDevice attr;
+  SEED_TRY(smem_optin(attr, gemm_tc_kernel<BN, Prob>, Cfg::SMEM));
+  const int sms = sm_count();
   if (splits > 1 && !part) return SEED_E_WORKSPACE;
   const int tiles = ceil_div(p.M, GEMM_BM) * ceil_div(p.N, BN);
   if (tiles > GEMM_COUNTERS) cnt = nullptr;

@@ -73,7 +73,8 @@ static seed_status make_infer_ws(const NetPlan& p, int n, InferWs* w) {
 }
 
 // ------------------------------------------------------------------ pre
-__global__ void infer_pre_kernel(int n, int A, int U, int Kxp, const int32_t* __restrict__ ids,
+__global__ void infer_pre_kernel(int n, int A, int U, int Kxp, int num_actors,
+                                 const int32_t* __restrict__ ids,
                                  const float* __restrict__ reward, const uint8_t* __restrict__ done,
                                  const float* __restrict__ th, const float* __restrict__ tc,
                                  const int32_t* __restrict__ tla, float* __restrict__ hpre,
@@ -86,16 +87,19 @@ __global__ void infer_pre_kernel(int n, int A, int U, int Kxp, const int32_t* __
   if (idx >= (int64_t)n * per) return;
   const int i = (int)(idx / per), j = (int)(idx % per);
   const int a = ids[i];
+  // an out-of-range actor id reads no table row (zero state, no previous action);
+  // the cell kernel reports it (action -1, NaN log-prob) and writes nothing
+  const bool valid = a >= 0 && a < num_actors;
   if (j < U) {
-    const float h = th[(size_t)a * U + j];
+    const float h = valid ? th[(size_t)a * U + j] : 0.f;
     hpre[(size_t)i * U + j] = h;
-    cpre[(size_t)i * U + j] = tc[(size_t)a * U + j];
+    cpre[(size_t)i * U + j] = valid ? tc[(size_t)a * U + j] : 0.f;
     hb[(size_t)i * U + j] = __float2bfloat16_rn(done[i] ? 0.f : h);   // reset on done (C15)
     return;
   }
   const int e = j - U;
   const bool dn = done[i] != 0;
-  const int pa = tla[a];
+  const int pa = valid ? tla[a] : -1;
   if (e == 0) prev[i] = pa;
   float v = 0.f;
   if (e < A) v = (!dn && pa == e) ? 1.f : 0.f;
@@ -164,7 +168,8 @@ __global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
     const uint8_t* __restrict__ done, const int32_t* __restrict__ ids, const float* __restrict__ hw,
     const float* __restrict__ hbias, const float* __restrict__ uniforms, uint64_t seed,
     uint64_t counter, float* __restrict__ th, float* __restrict__ tc, int32_t* __restrict__ tla,
-    int32_t* __restrict__ action_out, float* __restrict__ blp_out, float* __restrict__ logits_out) {
+    int32_t* __restrict__ action_out, float* __restrict__ blp_out, float* __restrict__ logits_out,
+    int num_actors) {
   pdl_wait();
   constexpr int U = LSTM_U, NW = ICH_THREADS / 32;
   const int i = blockIdx.x, j = threadIdx.x, warp = j >> 5, lane = j & 31;
@@ -177,6 +182,14 @@ __global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
   const float c = gf * c0 + gi * gg;
   const float h = go * tanh_fast(c);
   const int a = ids[i];
+  if (a < 0 || a >= num_actors) {   // out-of-range actor id: reported, nothing written
+    if (j == 0) {
+      action_out[i] = -1;
+      blp_out[i] = __int_as_float(0x7fffffff);
+    }
+    if (logits_out && j < A) logits_out[(size_t)i * A + j] = __int_as_float(0x7fffffff);
+    return;
+  }
   th[(size_t)a * U + j] = h;
   tc[(size_t)a * U + j] = c;
   for (int o = 0; o < A1; ++o) {
@@ -233,6 +246,7 @@ __global__ void infer_store_obs_kernel(int n, int64_t obs16, const uint8_t* __re
     const int i = (int)(idx / obs16);
     const int64_t q = idx % obs16;
     const int a = ids[i];
+    if (a < 0 || a >= st.num_actors) continue;
     const int buf = st.cur[a], slot = st.fill[a];
     const uint4 v = reinterpret_cast<const uint4*>(obs)[idx];
     uint4* base = reinterpret_cast<uint4*>(st.obs);
@@ -254,7 +268,8 @@ __global__ void infer_store_record_kernel(int n, int U, const int32_t* __restric
   const int T1 = st.T + 1;
   int a = 0, buf = 0, slot = 0;
   bool completed = false;
-  if (i < n) {
+  const bool valid = i < n && ids[i] >= 0 && ids[i] < st.num_actors;
+  if (valid) {
     a = ids[i];
     buf = st.cur[a];
     slot = st.fill[a];
@@ -271,7 +286,7 @@ __global__ void infer_store_record_kernel(int n, int U, const int32_t* __restric
   __syncthreads();
   int before = 0;
   for (int w = 0; w < wid; ++w) before += warp_tot[w];
-  if (i < n) {
+  if (valid) {
     const int64_t s0 = ((int64_t)a * 2 + buf) * T1 + slot;
     st.action[s0] = action[i];
     st.prev_action[s0] = prev[i];
@@ -285,8 +300,14 @@ __global__ void infer_store_record_kernel(int n, int U, const int32_t* __restric
       }
     }
     if (completed) {
-      st.ready_ring[(base_pos + before + within) % st.ring_capacity] = a * 2 + buf;
+      const int pos = (base_pos + before + within) % st.ring_capacity;
+      st.ready_ring[pos] = a * 2 + buf;
       const int nb = 1 - buf;
+      // buffer generations: the entry carries buf's generation; nb is
+      // being reused from here on (its slot 0 is written below), so its generation
+      // advances and a not-yet-assembled entry of nb becomes detectably stale
+      st.ready_gen[pos] = st.gen[a * 2 + buf];
+      st.gen[a * 2 + nb] += 1;
       const int64_t d0 = ((int64_t)a * 2 + nb) * T1;
       st.action[d0] = action[i];
       st.prev_action[d0] = prev[i];
@@ -316,8 +337,15 @@ __global__ void assemble_kernel(seed_unroll_store st, int64_t obs16, int U, int 
   const int b = blockIdx.y;
   const int T1 = st.T + 1;
   const int consumed = st.ready_count[1];
-  const int e = st.ready_ring[(consumed + b) % st.ring_capacity];
+  const int pos = (consumed + b) % st.ring_capacity;
+  const int e = st.ready_ring[pos];
   const int a = e >> 1, buf = e & 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // the unroll's buffer was reused (refilled) after it was pushed: stale
+    if (st.gen[e] != st.ready_gen[pos]) atomicAdd(&st.ready_count[2], 1);
+    // fewer than B unrolls pushed and not yet consumed
+    if (b == 0 && st.ready_count[0] - consumed < B) atomicAdd(&st.ready_count[3], 1);
+  }
   const int64_t src = ((int64_t)a * 2 + buf) * T1;
   const uint4* so = reinterpret_cast<const uint4*>(st.obs) + src * obs16;
   uint4* dob = reinterpret_cast<uint4*>(const_cast<void*>(out.obs)) + (int64_t)b * T1 * obs16;
@@ -371,6 +399,10 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
   SEED_TRY(make_net_plan(spec, &p));
   if (p.kind != SEED_NET_ATARI_SHALLOW || !learner_supported(p)) return SEED_E_UNSUPPORTED;
   if (n < 1 || n > 1024) return SEED_E_SHAPE;
+  if (table && table->num_actors < 1) return SEED_E_ARG;
+  if (store && (!store->gen || !store->ready_gen || store->num_actors != table->num_actors ||
+                store->ring_capacity < 1))
+    return SEED_E_ARG;
   if (!params_lowp || !params || !table || !actor_ids || !obs || !reward || !done ||
       !action_out || !blp_out || !ws || !table->h || !table->c || !table->last_action)
     return SEED_E_ARG;
@@ -387,7 +419,7 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
   {
     const int64_t tot = (int64_t)n * (U + p.Kxp - 256);
     SEED_TRY(launch_k(infer_pre_kernel, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, n, A, U,
-                      p.Kxp, actor_ids, reward, done, (const float*)table->h, (const float*)table->c,
+                      p.Kxp, table->num_actors, actor_ids, reward, done, (const float*)table->h, (const float*)table->c,
                       (const int32_t*)table->last_action, (float*)at(w.hpre), (float*)at(w.cpre),
                       (int32_t*)at(w.prev), (bf16*)at(w.X), (bf16*)at(w.hb)));
   }
@@ -413,7 +445,8 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
   SEED_TRY(launch_k(infer_cell_heads_kernel, dim3(n), dim3(ICH_THREADS), 0, st, A,
                     (const float*)at(w.xproj), (const float*)at(w.cpre), done, actor_ids,
                     params + p.t[p.i_hw].off, params + p.t[p.i_hb].off, uniforms, seed, counter,
-                    table->h, table->c, table->last_action, action_out, blp_out, logits_out));
+                    table->h, table->c, table->last_action, action_out, blp_out, logits_out,
+                    table->num_actors));
   if (store) {
     const int64_t obs16 = (int64_t)p.H * p.W * p.C / 16;
     infer_store_obs_kernel<<<(int)std::min<int64_t>((n * obs16 + 255) / 256, 148 * 8), 256, 0,
@@ -428,7 +461,8 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
 extern "C" seed_status seed_assemble_batch(const seed_unroll_store* store, int obs_bytes,
                                            int lstm_units, int B, const seed_batch* out,
                                            void* stream) {
-  if (!store || !out || B < 1 || obs_bytes <= 0 || obs_bytes % 16 || lstm_units < 1)
+  if (!store || !out || B < 1 || obs_bytes <= 0 || obs_bytes % 16 || lstm_units < 1 ||
+      !store->gen || !store->ready_gen || store->ring_capacity < 1)
     return SEED_E_ARG;
   if (!out->obs || !out->action || !out->prev_action || !out->reward || !out->done ||
       !out->behaviour_logp || !out->h0 || !out->c0)

@@ -35,21 +35,58 @@ seed_status comm_side(seed_comm* c, cudaStream_t* side, cudaStream_t* side2, cud
 seed_status comm_allreduce2(seed_comm* comm, float* data, int64_t n, cudaStream_t st);
 int comm_world(const seed_comm* c);
 
-// The library's second stream (per device, created once) and its event pool.
-// same != nullptr: no second branch (tracing), aux = same.
-static seed_status aux_stream(cudaStream_t same, cudaStream_t* aux, cudaEvent_t* ev8) {
-  static cudaStream_t streams[16] = {};
-  static cudaEvent_t events[16][8] = {};
-  int dev = 0;
-  SEED_CUDA_TRY(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 16) return SEED_E_ARG;
-  if (!streams[dev]) {
-    SEED_CUDA_TRY(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
-    for (int i = 0; i < 8; ++i)
-      SEED_CUDA_TRY(cudaEventCreateWithFlags(&events[dev][i], cudaEventDisableTiming));
+}  // namespace seed
+
+// Caller-owned execution context (include/seed.h seed_exec): the second stream the
+// independent backward GEMMs branch onto and the events of the fork / join edges.
+// A step captured into a CUDA graph turns the edges into parallel graph branches.
+struct seed_exec {
+  int device;
+  cudaStream_t aux;
+  cudaEvent_t ev[8];
+};
+
+extern "C" seed_status seed_exec_create(seed_exec** out) {
+  if (!out) return SEED_E_ARG;
+  *out = nullptr;
+  seed_exec* e = new seed_exec{};
+  if (cudaGetDevice(&e->device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&e->aux, cudaStreamNonBlocking) != cudaSuccess) {
+    delete e;
+    return SEED_E_CUDA;
   }
-  *aux = same ? same : streams[dev];
-  for (int i = 0; i < 8; ++i) ev8[i] = events[dev][i];
+  for (int i = 0; i < 8; ++i)
+    if (cudaEventCreateWithFlags(&e->ev[i], cudaEventDisableTiming) != cudaSuccess) {
+      for (int k = 0; k < i; ++k) cudaEventDestroy(e->ev[k]);
+      cudaStreamDestroy(e->aux);
+      delete e;
+      return SEED_E_CUDA;
+    }
+  *out = e;
+  return SEED_OK;
+}
+
+extern "C" seed_status seed_exec_destroy(seed_exec* e) {
+  if (!e) return SEED_OK;
+  for (int i = 0; i < 8; ++i) cudaEventDestroy(e->ev[i]);
+  cudaStreamDestroy(e->aux);
+  delete e;
+  return SEED_OK;
+}
+
+namespace seed {
+
+// The step's second branch: the context's stream and events; without a context
+// (or when tracing: phase marks need one stream) aux = st and no edges are made.
+static seed_status aux_stream(const seed_exec* ex, cudaStream_t st, bool single, cudaStream_t* aux,
+                              cudaEvent_t* ev8) {
+  if (!ex || single) {
+    *aux = st;
+    return SEED_OK;
+  }
+  if (ex->device != current_device()) return SEED_E_ARG;
+  *aux = ex->aux;
+  for (int i = 0; i < 8; ++i) ev8[i] = ex->ev[i];
   return SEED_OK;
 }
 
@@ -105,10 +142,10 @@ struct StepCtx {
     ++nbucket;
     return second ? comm_allreduce2(comm, g, n, s) : comm_allreduce(comm, g, n, s);
   }
-  // Independent backward GEMMs run as a second branch on `aux` (a process-wide
-  // stream of the library; inside a CUDA graph capture the event edges make it a
-  // parallel branch of the graph).  aux == st when the step is traced (phase
-  // marks need one stream) — then the branches simply run in order.
+  // Independent backward GEMMs run as a second branch on `aux` (the caller's
+  // seed_exec stream; inside a CUDA graph capture the event edges make it a
+  // parallel branch of the graph).  aux == st without a seed_exec or when the step
+  // is traced (phase marks need one stream) — then the branches simply run in order.
   cudaStream_t aux = nullptr;
   cudaEvent_t fev[8] = {};
   int nfev = 0;
@@ -444,8 +481,9 @@ static seed_status mlp_backward(const StepCtx& c, const seed_batch* bt, const fl
 
 static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
                                      const seed_batch* batch, const seed_train_state* state,
-                                     const seed_hparams* hp, seed_comm* comm, void* ws,
-                                     size_t ws_bytes, float* metrics, void* stream, Trace* tr) {
+                                     const seed_hparams* hp, seed_comm* comm, const seed_exec* ex,
+                                     void* ws, size_t ws_bytes, float* metrics, void* stream,
+                                     Trace* tr) {
   NetPlan p;
   SEED_TRY(make_net_plan(spec, &p));
   if (!learner_supported(p)) return SEED_E_UNSUPPORTED;
@@ -454,9 +492,13 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   if (!batch->obs || !batch->action || !batch->reward || !batch->done || !batch->behaviour_logp ||
       !state->params || !state->grads || !state->adam_m || !state->adam_v || !state->step)
     return SEED_E_ARG;
+  // fp32 master / grads / moments are read and written with float4 accesses
+  if (!aligned16(state->params) || !aligned16(state->grads) || !aligned16(state->adam_m) ||
+      !aligned16(state->adam_v) || !aligned16(ws))
+    return SEED_E_ARG;
   if (p.kind != SEED_NET_MLP &&
       (!batch->prev_action || !batch->h0 || !batch->c0 || !state->params_lowp ||
-       !aligned16(batch->obs) || !aligned16(ws) || !aligned16(state->params_lowp)))
+       !aligned16(batch->obs) || !aligned16(state->params_lowp)))
     return SEED_E_ARG;
   if (!(hp->c_bar > 0.f) || !(hp->rho_bar >= hp->c_bar) || !(hp->lambda >= 0.f && hp->lambda <= 1.f) ||
       !(hp->max_grad_norm > 0.f))
@@ -489,7 +531,7 @@ static seed_status learner_step_impl(const seed_net_spec* spec, int T, int B,
   if (p.kind == SEED_NET_MLP) {
     SEED_TRY(mlp_forward(c, batch, params, st));
   } else {
-    SEED_TRY(aux_stream(tr != nullptr ? st : nullptr, &c.aux, c.fev));
+    SEED_TRY(aux_stream(ex, st, tr != nullptr, &c.aux, c.fev));
     // the LSTM-input extras (one-hot, reward, ones column) only read the batch:
     // an aux-stream branch beside the torso, joined before the input projection
     SEED_TRY(c.edge(st, c.aux));
@@ -594,7 +636,15 @@ extern "C" seed_status seed_learner_step(const seed_net_spec* spec, int T, int B
                                          const seed_batch* batch, const seed_train_state* state,
                                          const seed_hparams* hp, seed_comm* comm, void* ws,
                                          size_t ws_bytes, float* metrics, void* stream) {
-  return seed::learner_step_impl(spec, T, B, batch, state, hp, comm, ws, ws_bytes, metrics,
+  return seed::learner_step_impl(spec, T, B, batch, state, hp, comm, nullptr, ws, ws_bytes, metrics,
+                                 stream, nullptr);
+}
+
+extern "C" seed_status seed_learner_step_ex(const seed_net_spec* spec, int T, int B,
+                                            const seed_batch* batch, const seed_train_state* state,
+                                            const seed_hparams* hp, seed_comm* comm, seed_exec* exec,
+                                            void* ws, size_t ws_bytes, float* metrics, void* stream) {
+  return seed::learner_step_impl(spec, T, B, batch, state, hp, comm, exec, ws, ws_bytes, metrics,
                                  stream, nullptr);
 }
 
@@ -610,8 +660,8 @@ extern "C" seed_status seed_learner_step_traced(const seed_net_spec* spec, int T
   tr.events = events;
   tr.names = names_out;
   tr.max = events ? max_events : 0;
-  const seed_status r = seed::learner_step_impl(spec, T, B, batch, state, hp, comm, ws, ws_bytes,
-                                                metrics, stream, &tr);
+  const seed_status r = seed::learner_step_impl(spec, T, B, batch, state, hp, comm, nullptr, ws,
+                                                ws_bytes, metrics, stream, &tr);
   if (n_events_out) *n_events_out = tr.n;
   if (n_launches_out) *n_launches_out = tr.launches;
   return r;

@@ -130,13 +130,9 @@ __global__ void __launch_bounds__(256) dense_wgrad_f32(int R, int I, int O, cons
 seed_status launch_dense_fwd(int R, int I, int O, const float* X, const float* W, const float* b,
                              float* Y, int ldy, float* Yv, int relu, cudaStream_t st) {
   if (I > 256 || O > 64) return SEED_E_SHAPE;
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(dense_fwd_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (256 * 64 + 8 * 256) * 4));
-    attr = true;
-  }
-  const size_t smem = (size_t)(I * O + 8 * I) * 4;
+  static PerDevice attr;
+  SEED_TRY(smem_optin(attr, dense_fwd_f32, (256 * 64 + 8 * 256) * 4));
+    const size_t smem = (size_t)(I * O + 8 * I) * 4;
   const int blocks = std::min(ceil_div(R, 8), 148 * 4);
   return launch_k(dense_fwd_f32, dim3(blocks), dim3(256), smem, st, R, I, O, X, W, b, Y, ldy, Yv, relu);
 }
@@ -144,13 +140,9 @@ seed_status launch_dense_fwd(int R, int I, int O, const float* X, const float* W
 seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, const float* dv,
                                const float* W, const float* mask, float* dX, cudaStream_t st) {
   if (I > 256 || O > 64) return SEED_E_SHAPE;
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(dense_dgrad_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (256 * 64 + DG_ROWS * 64) * 4));
-    attr = true;
-  }
-  const size_t smem = (size_t)(O * I + DG_ROWS * O) * 4;
+  static PerDevice attr;
+  SEED_TRY(smem_optin(attr, dense_dgrad_f32, (256 * 64 + DG_ROWS * 64) * 4));
+    const size_t smem = (size_t)(O * I + DG_ROWS * O) * 4;
   return launch_k(dense_dgrad_f32, dim3(ceil_div(R, DG_ROWS)), dim3(256), smem, st, R, I, O, dy, ldy, dv,
                   W, mask, dX);
 }
@@ -541,14 +533,9 @@ seed_status launch_heads_loss(const LossArgs& a, cudaStream_t st) {
   // Hc holds HL_RC rows of H, later the [A+1][I] row-parity partials (A+1 <= HL_RC+1)
   const size_t smem = ((((size_t)a.I * A1p + (size_t)(a.T + 1) * A1p + 3) & ~(size_t)3) +
                        (size_t)(HL_RC + 1) * a.I) * 4;
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(heads_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::max<size_t>((256 * 33 + 257 * 33 + 4 + (HL_RC + 1) * 256) * 4,
-                                                             (size_t)HL_CL * 33 * 257 * 4)));
-    attr = true;
-  }
-  SEED_TRY(launch_k(heads_loss_kernel, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
+  static PerDevice attr;
+  SEED_TRY(smem_optin(attr, heads_loss_kernel, (int)std::max<size_t>((256 * 33 + 257 * 33 + 4 + (HL_RC + 1) * 256) * 4, (size_t)HL_CL * 33 * 257 * 4)));
+    SEED_TRY(launch_k(heads_loss_kernel, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
   const int n = (a.A + 1) * (a.I + 1);
   return launch_k(heads_wgrad_finish, dim3(ceil_div(n, 32)), dim3(256), 0, st, a.B * HL_CL, a.A + 1,
                   a.I, (const float*)a.wpart, a.g_w, a.g_b);

@@ -515,26 +515,16 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
 
 template <int BBT>
 static seed_status launch_fwd(const LstmFwdArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel<BBT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       LstmCfg<BBT>::FWD_SMEM));
-    attr = true;
-  }
-  return launch_k(lstm_fwd_kernel<BBT>, dim3(ceil_div(a.B, BBT) * LSTM_CLUSTER), dim3(256),
+  static PerDevice attr;
+  SEED_TRY(smem_optin(attr, lstm_fwd_kernel<BBT>, LstmCfg<BBT>::FWD_SMEM));
+    return launch_k(lstm_fwd_kernel<BBT>, dim3(ceil_div(a.B, BBT) * LSTM_CLUSTER), dim3(256),
                   (size_t)LstmCfg<BBT>::FWD_SMEM, st, a);
 }
 template <int BBT>
 static seed_status launch_bwd(const LstmBwdArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(lstm_bwd_kernel<BBT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       LstmCfg<BBT>::BWD_SMEM));
-    attr = true;
-  }
-  return launch_k(lstm_bwd_kernel<BBT>, dim3(ceil_div(a.B, BBT) * LSTM_CLUSTER), dim3(256),
+  static PerDevice attr;
+  SEED_TRY(smem_optin(attr, lstm_bwd_kernel<BBT>, LstmCfg<BBT>::BWD_SMEM));
+    return launch_k(lstm_bwd_kernel<BBT>, dim3(ceil_div(a.B, BBT) * LSTM_CLUSTER), dim3(256),
                   (size_t)LstmCfg<BBT>::BWD_SMEM, st, a);
 }
 

@@ -355,7 +355,7 @@ extern "C" seed_status seed_net_lowp_bytes(const seed_net_spec* spec, size_t* by
   if (!bytes) return SEED_E_ARG;
   NetPlan p;
   SEED_TRY(make_net_plan(spec, &p));
-  *bytes = (size_t)p.lowp_elems * 2;
+  *bytes = align_up((size_t)p.lowp_elems * 2, 16);   // whole 16-byte chunks
   return SEED_OK;
 }
 

@@ -226,14 +226,9 @@ seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st)
   if (a.M <= 0) return a.M == 0 ? SEED_OK : SEED_E_SHAPE;
   if (stages < 2) return SEED_E_SHAPE;
   const size_t smem = (size_t)wbytes + (size_t)stages * slab + 1024;
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win_conv_kernel<Epi, RB, NW, MT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       WC_SMEM_BUDGET + 2048));
-    attr = true;
-  }
-  const int64_t tiles = (a.M + TM - 1) / TM;
+  static PerDevice attr;
+  SEED_TRY(smem_optin(attr, win_conv_kernel<Epi, RB, NW, MT>, WC_SMEM_BUDGET + 2048));
+    const int64_t tiles = (a.M + TM - 1) / TM;
   const int grid = (int)std::min<int64_t>(tiles, 148);
   return launch_k(win_conv_kernel<Epi, RB, NW, MT>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e,
                   stages, slab);
@@ -454,15 +449,11 @@ seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias
   const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes));
   if (stages < 2) return SEED_E_SHAPE;
   const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);
-  static bool attr = false;
-  if (!attr) {
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX, true, NB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
-    SEED_CUDA_TRY(cudaFuncSetAttribute(win3_wgrad_kernel<CO, RBX, false, NB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WC_SMEM_BUDGET + 2048));
-    attr = true;
-  }
-  SEED_TRY(launch_k(bias ? win3_wgrad_kernel<CO, RBX, true, NB> : win3_wgrad_kernel<CO, RBX, false, NB>, dim3(G),
+  static PerDevice attr0;
+  SEED_TRY(smem_optin(attr0, win3_wgrad_kernel<CO, RBX, true, NB>, WC_SMEM_BUDGET + 2048));
+  static PerDevice attr1;
+  SEED_TRY(smem_optin(attr1, win3_wgrad_kernel<CO, RBX, false, NB>, WC_SMEM_BUDGET + 2048));
+    SEED_TRY(launch_k(bias ? win3_wgrad_kernel<CO, RBX, true, NB> : win3_wgrad_kernel<CO, RBX, false, NB>, dim3(G),
                     dim3(WC_THREADS), smem, st, a, stages, a_bytes, b_bytes));
   const int tot = 128 * NB * CO + (bias ? CO : 0);
   return launch_k(win3_wgrad_finish<CO, Fin, NB>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,

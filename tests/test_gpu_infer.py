@@ -169,3 +169,110 @@ def test_behaviour_fidelity_self_consistency():
     tlp = np.take_along_axis(logp, act[:, :, None], 2)[:, :, 0]
     blp = out["behaviour_logp"].cpu().numpy()
     assert np.max(np.abs(tlp - blp)) < 1e-4, np.max(np.abs(tlp - blp))
+
+
+def test_infer_bench_shape_n1024_store():
+    """The bench's c5 shape: 4096 actors, n = 1024 requests per call (the split-K /
+    tiling of the big-n path), unroll store on.  Logits, actions, log-probs and the
+    state table against the emulated oracle; actors not in the call untouched
+    (bitwise); every called actor's first unroll slot and h0 / c0 recorded exactly."""
+    import paper_1910_06591_b200 as S
+    NA4, n = 4096, 1024
+    spec = S.spec_for_config("c5")
+    ospec = O.spec_c2()
+    params = seedgen.glorot_params(O.param_layout(ospec), seed=51, bias_std=0.1)
+    learner = S.Learner(spec, T, 2, params)
+    srv = S.InferenceServer(spec, NA4, n, learner=learner, T=T)
+    g = seedgen.rng(52)
+    th = (0.5 * g.standard_normal((NA4, 256))).astype(np.float32)
+    tc = (0.5 * g.standard_normal((NA4, 256))).astype(np.float32)
+    tla = g.integers(-1, A, NA4).astype(np.int32)
+    srv.h.copy_(torch.from_numpy(th))
+    srv.c.copy_(torch.from_numpy(tc))
+    srv.last_action.copy_(torch.from_numpy(tla))
+    req = seedgen.infer_requests((84, 84, 4), A, NA4, n, seed=53)
+    a, blp, logits = _call(srv, req)
+    ra, rblp, rlg, rth, rtc, rtla = O.infer(ospec, params, th, tc, tla, req["actor_ids"],
+                                            req["obs"], req["reward"], req["done"],
+                                            req["uniforms"], emu=True)
+    assert _relL2(logits, rlg) < 2e-2
+    nb = _near_boundary(rlg, req["uniforms"].astype(np.float64))
+    assert np.all((a == ra) | nb), np.nonzero((a != ra) & ~nb)
+    ok = a == ra
+    np.testing.assert_allclose(blp[ok], rblp[ok], atol=2e-2 * max(1.0, np.abs(rblp).max()))
+    ids = req["actor_ids"]
+    h_gpu, c_gpu = srv.h.cpu().numpy(), srv.c.cpu().numpy()
+    assert _relL2(h_gpu[ids], rth[ids]) < 2e-2
+    assert _relL2(c_gpu[ids], rtc[ids]) < 2e-2
+    others = np.setdiff1d(np.arange(NA4), ids)
+    np.testing.assert_array_equal(h_gpu[others], th[others])
+    np.testing.assert_array_equal(c_gpu[others], tc[others])
+    np.testing.assert_array_equal(srv.last_action.cpu().numpy()[ids], a)
+    np.testing.assert_array_equal(srv.last_action.cpu().numpy()[others], tla[others])
+    # unroll store: slot 0 of buffer 0 of each called actor (C17, C19)
+    st = {k: v.cpu().numpy() for k, v in srv.st.items()}
+    np.testing.assert_array_equal(st["fill"][ids], 1)
+    np.testing.assert_array_equal(st["fill"][others], 0)
+    np.testing.assert_array_equal(st["obs"][ids, 0, 0], req["obs"].reshape(n, -1))
+    np.testing.assert_array_equal(st["action"][ids, 0, 0], a)
+    np.testing.assert_array_equal(st["behaviour_logp"][ids, 0, 0], blp)
+    np.testing.assert_array_equal(st["reward"][ids, 0, 0], req["reward"])
+    np.testing.assert_array_equal(st["done"][ids, 0, 0], req["done"])
+    np.testing.assert_array_equal(st["prev_action"][ids, 0, 0], tla[ids])
+    np.testing.assert_array_equal(st["h0"][ids, 0], th[ids])
+    np.testing.assert_array_equal(st["c0"][ids, 0], tc[ids])
+
+
+def test_infer_out_of_range_actor_ids():
+    """An actor id outside [0, num_actors) is reported on the device (action -1,
+    NaN log-prob and logits), reads and writes nothing; the valid requests of the
+    same call are unaffected."""
+    S, srv, ospec, params = _setup(store=True, max_n=16)
+    th, tc, tla = (srv.h.cpu().numpy(), srv.c.cpu().numpy(), srv.last_action.cpu().numpy())
+    req = seedgen.infer_requests((84, 84, 4), A, NA, 8, seed=71)
+    bad = np.array([3, 5])
+    req["actor_ids"][3] = NA + 5
+    req["actor_ids"][5] = -2
+    a, blp, logits = _call(srv, req)
+    assert np.all(a[bad] == -1) and np.all(np.isnan(blp[bad])) and np.all(np.isnan(logits[bad]))
+    ok = np.setdiff1d(np.arange(8), bad)
+    ids = req["actor_ids"][ok]
+    sub = {k: v[ok] for k, v in req.items()}
+    ra, rblp, rlg, rth, rtc, _ = O.infer(ospec, params, th, tc, tla, ids, sub["obs"], sub["reward"],
+                                         sub["done"], sub["uniforms"], emu=True)
+    assert _relL2(logits[ok], rlg) < 2e-2
+    nb = _near_boundary(rlg, sub["uniforms"].astype(np.float64))
+    assert np.all((a[ok] == ra) | nb)
+    others = np.setdiff1d(np.arange(NA), ids)
+    np.testing.assert_array_equal(srv.h.cpu().numpy()[others], th[others])
+    np.testing.assert_array_equal(srv.last_action.cpu().numpy()[others], tla[others])
+    fill = srv.st["fill"].cpu().numpy()
+    np.testing.assert_array_equal(fill[ids], 1)
+    np.testing.assert_array_equal(fill[others], 0)
+
+
+def test_store_stale_and_short_assemble_reported():
+    """an unroll whose buffer was reused before it was assembled
+    (the actor completed its next unroll) is counted in ready_count[2]; asking for
+    more unrolls than are pushed and unconsumed is counted in ready_count[3]."""
+    S, srv, ospec, params = _setup(store=True, max_n=NA)
+    call = 0
+    for _ in range(T + 1):                        # every actor completes unroll 0
+        _call(srv, seedgen.infer_requests((84, 84, 4), A, NA, NA, seed=72, call_index=call))
+        call += 1
+    out = _batch_bufs(NA // 2)
+    srv.assemble(NA // 2, out)                    # fresh: nothing stale
+    torch.cuda.synchronize()
+    assert srv.st["ready_count"].cpu().numpy()[2:].tolist() == [0, 0]
+    for _ in range(T):                            # unroll 1 completes: unroll 0 buffers reused
+        _call(srv, seedgen.infer_requests((84, 84, 4), A, NA, NA, seed=72, call_index=call))
+        call += 1
+    srv.assemble(NA // 2, out)                    # the other half of unroll 0: all stale
+    torch.cuda.synchronize()
+    rc = srv.st["ready_count"].cpu().numpy()
+    assert rc[2] == NA // 2 and rc[3] == 0, rc
+    big = _batch_bufs(NA + 1)
+    srv.assemble(NA + 1, big)                     # NA pushed and unconsumed (unroll 1) < NA + 1
+    torch.cuda.synchronize()
+    rc = srv.st["ready_count"].cpu().numpy()
+    assert rc[3] == 1, rc

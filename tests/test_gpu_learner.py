@@ -43,6 +43,23 @@ def bf16_check(gpu, ref, what="", tol=2e-2):
     return rel
 
 
+def exact_bound_check(gpu, exact, emu, what="", floor=2e-2, factor=1.25):
+    """Parity against the plain fp64 definition: the kernel may be no
+    further from the exact oracle than bf16 rounding itself puts the oracle, i.e.
+    ||gpu - exact|| / ||exact|| <= max(floor, factor * ||emu - exact|| / ||exact||)
+    per tensor, where emu is the oracle taking its bf16 roundings at the kernels'
+    rounding points (C26).  Returns (rel_gpu, rel_emu)."""
+    gpu = np.asarray(gpu, np.float64).ravel()
+    exact = np.asarray(exact, np.float64).ravel()
+    emu = np.asarray(emu, np.float64).ravel()
+    n = max(np.linalg.norm(exact), 1e-30)
+    rg = np.linalg.norm(gpu - exact) / n
+    re = np.linalg.norm(emu - exact) / n
+    assert rg <= max(floor, factor * re), \
+        f"{what}: gpu-vs-exact relL2 {rg:.3g} > max({floor}, {factor} x emu-vs-exact {re:.3g})"
+    return rg, re
+
+
 def _spec_pair(cfg):
     S = _S()
     spec = S.spec_for_config(cfg)
@@ -163,9 +180,13 @@ def test_learner_c2_atari_parity(B, T, seed):
         except AssertionError as e:
             errs[name] = "FAIL " + str(e)
     print("per-tensor grad relL2 (vs emulated):", errs)
-    print("per-tensor grad relL2 (vs exact fp64):",
-          {n: f"{np.linalg.norm(gt[n] - ex[n]) / np.linalg.norm(ex[n]):.2e}" for n in ex})
     assert not any(v.startswith("FAIL") for v in errs.values()), errs
+    # every gradient tensor against the exact definition (C26, C31)
+    ex_rel = {}
+    for name, _ in O.param_layout(ospec):
+        rg, re = exact_bound_check(gt[name], ex[name], rt[name], f"grad {name} vs exact")
+        ex_rel[name] = f"{rg:.2e} (emu {re:.2e})"
+    print("per-tensor grad relL2 vs exact, gpu (emu):", ex_rel)
     _check_k2_and_adam(ospec, params, batch, hp, g)
 
 
@@ -317,6 +338,13 @@ def test_learner_deep_parity(cfg, B, T):
         bf16_check(buf(s, "dhA", (F_, H2, W2, ch)), dh, f"s{s}.dh(h0)", tol=1e-2)
         arg = L.debug_buffer(f"s{s}.arg", torch.uint8, (F_, H2 + 2, W2 + 2, ch)).cpu().numpy()
         arg = arg[:, 1:-1, 1:-1, :]
+        # max-pool argmax is index work: bit-exact against the oracle's max-pool run on
+        # the GPU's own conv output (first maximum in (ky, kx) order, -inf padding)
+        gconv = buf(s, "conv", (F_, H, W, ch))
+        ry, rarg, _ = O.maxpool_same(gconv)
+        np.testing.assert_array_equal(arg.astype(np.int64), rarg, err_msg=f"s{s} pool argmax")
+        np.testing.assert_array_equal(buf(s, "h0", (F_, H2, W2, ch)), ry,
+                                      err_msg=f"s{s} pooled values")
         cin = ospec.obs_c if s == 0 else dims[s - 1][4]
         dconv = np.zeros((F_, H, W, ch))
         offs = ((max((H2 - 1) * 2 + 3 - H, 0)) // 2, (max((W2 - 1) * 2 + 3 - W, 0)) // 2)
@@ -331,10 +359,44 @@ def test_learner_deep_parity(cfg, B, T):
         scaled_check(gt[f"s{s}.conv.b"], db, 5e-3, f"s{s}.conv.b")
         if s > 0:
             dh = q(dxin)
-    # end-to-end deviation of the gradients from the emulated oracle (reported; sanity bound)
-    dev = {n: np.linalg.norm(gt[n] - rt[n]) / np.linalg.norm(rt[n]) for n in gt}
-    print(cfg, "grad relL2 vs emulated (end to end):", {k: f"{v:.1e}" for k, v in dev.items()})
-    assert max(dev.values()) < 0.3
+    # end to end, every gradient tensor against the exact fp64 definition (C31)
+    exact = O.learner_step(ospec, params, np.zeros(params.size), np.zeros(params.size), 0, batch,
+                           hp.as_oracle())
+    ex = O.unflatten(ospec, exact["grads"])
+    _deep_exact_checks(cfg, g, gt, ex, rt, exact, ref)
+
+
+def _deep_exact_checks(cfg, g, gt, ex, rt, exact, ref):
+    """IMPALA-deep torsos (15-20 stacked bf16 convs, C31): the kernel and the emulated
+    oracle are two bf16 evaluations whose ReLU-mask / argmax flips are different
+    samples of the same rounding noise, so per tensor their distances to the exact
+    definition agree only up to sampling spread (measured 0.7-1.3x at F = 202).
+    Criterion: the whole gradient vector within 1.25x of the emulated oracle's
+    distance, every tensor within 1.5x (floor 2e-2), logits / values within 1.25x."""
+    allg = np.concatenate([np.ravel(gt[n]) for n in gt])
+    alle = np.concatenate([np.ravel(ex[n]) for n in gt])
+    allr = np.concatenate([np.ravel(rt[n]) for n in gt])
+    rows, bad = {}, []
+    try:
+        rg, re = exact_bound_check(allg, alle, allr, "whole gradient")
+        rows["(all)"] = f"{rg:.2e} (emu {re:.2e})"
+    except AssertionError as e:
+        bad.append(str(e))
+    for n in gt:
+        try:
+            rg, re = exact_bound_check(gt[n], ex[n], rt[n], n, factor=1.5)
+        except AssertionError as e:
+            bad.append(str(e))
+            rg = np.linalg.norm(gt[n] - ex[n]) / np.linalg.norm(ex[n])
+            re = np.linalg.norm(rt[n] - ex[n]) / np.linalg.norm(ex[n])
+        rows[n] = f"{rg:.2e} (emu {re:.2e})"
+    for what in ("logits", "values"):
+        try:
+            exact_bound_check(g[what], exact[what], ref[what], what)
+        except AssertionError as e:
+            bad.append(str(e))
+    print(cfg, "grad relL2 vs exact, gpu (emu):", rows)
+    assert not bad, bad
 
 
 @pytest.mark.parametrize("cfg,B,T", [("c3", 32, 100), ("c4", 128, 32)])
@@ -366,3 +428,30 @@ def test_learner_deep_full_size_sampled(cfg, B, T):
     bf16_check(act2[pick], cache["flat"], f"{cfg} torso output (sampled frames)")
     X = L.debug_buffer("X", bf, (F_, -1)).float().cpu().numpy().astype(np.float64)
     bf16_check(X[pick, :256], cache["fc"], f"{cfg} fc output (sampled frames)")
+
+
+def test_learner_c3_bptt_T100():
+    """configs[2] at its full unroll length T = 100 (101 serial LSTM steps forward and
+    backward) and full image size, B = 2: logits, values and the LSTM / heads
+    gradients against the emulated oracle (C22) and every gradient tensor end to end
+    against the exact fp64 definition (C31).  One forced episode boundary mid-unroll
+    (the BPTT chain is cut there), otherwise done ~ Bern(1/200)."""
+    S = _S()
+    B, T = 2, 100
+    spec, ospec = _spec_pair("c3")
+    params = seedgen.glorot_params(O.param_layout(ospec), seed=41, bias_std=0.1)
+    batch = seedgen.learner_batch((ospec.obs_h, ospec.obs_w, ospec.obs_c), ospec.num_actions, B,
+                                  T, seed=42, done_p=1.0 / 200, force_done=((1, 57),))
+    hp = S.HParams(lam=0.95, loss_scale=1.0 / (B * T), lr=1e-3)
+    g = _run_gpu(S, spec, params, batch, hp, B, T)
+    z = np.zeros(params.size)
+    ref = O.learner_step(ospec, params, z, z, 0, batch, hp.as_oracle(), emu=True)
+    exact = O.learner_step(ospec, params, z, z, 0, batch, hp.as_oracle())
+    bf16_check(g["logits"], ref["logits"], "logits")
+    bf16_check(g["values"], ref["values"], "values")
+    gt, rt = _per_tensor(ospec, g["grads"]), _per_tensor(ospec, ref["grads"])
+    ex = O.unflatten(ospec, exact["grads"])
+    for n in ("heads.w", "heads.b", "lstm.wx", "lstm.wh", "lstm.b"):
+        bf16_check(gt[n], rt[n], f"{n} (T=100 BPTT)")
+    _check_k2_and_adam(ospec, params, batch, hp, g)
+    _deep_exact_checks("c3 T=100", g, gt, ex, rt, exact, ref)

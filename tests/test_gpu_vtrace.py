@@ -85,3 +85,19 @@ def test_vtrace_full_size_sampled():
     _tol_check(vs[idx], vs_r)
     _tol_check(pg[idx], pg_r)
     assert flag == 0
+
+
+@pytest.mark.parametrize("name", ["vtrace_S145.json", "vtrace_cbar_hand.json"])
+def test_vtrace_golden_values(name):
+    """The kernel on the printed / hand-derived examples (tests/golden): values fixed by
+    the paper's recursion, not by the oracle (fp32 inputs: 1e-5 relative)."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", name)) as f:
+        g = json.load(f)
+    x = {k: np.asarray(g[k], np.float32) for k in ("behaviour_logp", "target_logp", "rewards",
+                                                   "discounts", "values", "bootstrap")}
+    vs, pg, flag = _run(x, g["rho_bar"], g["c_bar"], g["lambda"])
+    _tol_check(vs, np.asarray(g["vs"], np.float64))
+    _tol_check(pg, np.asarray(g["pg_advantages"], np.float64))
+    assert flag == 0

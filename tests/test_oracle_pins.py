@@ -35,6 +35,41 @@ def test_vtrace_worked_example_S145():
     assert not bad
 
 
+def test_vtrace_cbar_lambda_hand_golden():
+    """c_bar and lambda pinned by a hand-derived example (tests/golden/vtrace_cbar_hand.json,
+    S:140 with rho_bar != c_bar and lambda < 1): the direct sum repeats the recursion's
+    formula for c_t, and the enumeration / lambda-return pins are blind to c_bar."""
+    g = _gold("vtrace_cbar_hand.json")
+    vs, pg, bad = O.vtrace(g["behaviour_logp"], g["target_logp"], g["rewards"], g["discounts"],
+                           g["values"], g["bootstrap"], g["rho_bar"], g["c_bar"], g["lambda"])
+    np.testing.assert_allclose(vs, g["vs"], atol=1e-9)
+    np.testing.assert_allclose(pg, g["pg_advantages"], atol=1e-9)
+    assert not bad
+
+
+def test_vtrace_monotone_clipping_S161():
+    """with rho_bar' <= rho_bar and identical inputs, the outputs differ only
+    through the clipped ratios.  Pre-clipping every ratio to rho_bar' (target log-prob
+    rewritten as log mu + log min(ratio, rho_bar')) and running with rho_bar must give
+    exactly the rho_bar' result: rho' = min(rho_bar, ratio') = min(ratio, rho_bar') and,
+    for c_bar <= rho_bar', c' = lambda min(c_bar, ratio') = lambda min(c_bar, ratio)."""
+    x = seedgen.vtrace_inputs(16, 24, seed=17)
+    blp = x["behaviour_logp"].astype(np.float64)
+    tlp = blp + 1.2 * seedgen.rng(18).standard_normal(blp.shape)   # ratios well above / below 1
+    for rb, rb2, cb, lam in ((2.0, 1.0, 1.0, 0.95), (np.inf, 1.5, 0.7, 0.9), (3.0, 0.8, 0.5, 1.0)):
+        base = dict(rewards=x["rewards"], discounts=x["discounts"], values=x["values"],
+                    bootstrap=x["bootstrap"])
+        vs2, pg2, _ = O.vtrace(blp, tlp, **base, rho_bar=rb2, c_bar=cb, lam=lam)
+        ratio = np.exp(tlp - blp)
+        tlp_c = blp + np.log(np.minimum(ratio, rb2))
+        vs1, pg1, _ = O.vtrace(blp, tlp_c, **base, rho_bar=rb, c_bar=cb, lam=lam)
+        np.testing.assert_allclose(vs1, vs2, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(pg1, pg2, rtol=1e-12, atol=1e-12)
+        # and the looser clip really differs where some ratio exceeds rho_bar'
+        vs0, _, _ = O.vtrace(blp, tlp, **base, rho_bar=rb, c_bar=cb, lam=lam)
+        assert np.max(np.abs(vs0 - vs2)) > 1e-3
+
+
 def test_vtrace_fully_clipped_S146():
     x = seedgen.vtrace_inputs(4, 7, seed=3)
     tlp = x["behaviour_logp"] - 1e4            # ratio underflows to 0 -> rho = c = 0
@@ -140,7 +175,7 @@ def test_vtrace_exact_enumeration_fixed_point(rho_bar, c_bar, lam):
         assert abs(expect - Vst[x0]) < 1e-12, (x0, expect, Vst[x0])
 
 
-def test_vtrace_episode_isolation_and_monotone_clip_S161_S162():
+def test_vtrace_episode_isolation_S162():
     x = seedgen.vtrace_inputs(4, 12, seed=9, done_p=0.0)
     x["discounts"][:, 5] = 0.0                       # episode boundary after step 5
     vs1, _, _ = O.vtrace(**x, rho_bar=1.0, c_bar=1.0, lam=0.95)
