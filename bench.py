@@ -4,17 +4,21 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One "step" = one seed_learner_step (H0-H11 of SURVEY.md §8(a)) of the
-BASELINE.json configs[1] workload — Atari IMPALA-shallow CNN + LSTM(256),
-84x84x4 uint8 obs, 18 actions, T=20, B=32 per GPU — on synthetic seeded inputs
-already resident in HBM; N>1 = one process per GPU (torchrun), data-parallel
-with the NCCL gradient allreduce inside the step (weak scaling).
-Metric: learner frames/s (frames = B*T*4, action repeat 4: P:163; C16).
-The same JSON line carries the V-trace bandwidth leg (seed_vtrace at T=100,
-B=2^17, 367 MB > L2), the per-phase breakdown, the roofline of the dominant
-kernel, the e2e number through the public API with pinned H2D/D2H copies,
-clocks, and the CPU oracle baseline.
+headline workload, BASELINE.json configs[3] — Google Research Football SMM,
+IMPALA-deep torso (16, 32, 32, 32) + LSTM(256), 72x96x16 uint8 obs, 19 actions,
+T=32, B=128 per GPU (the largest single-GPU config, the one BASELINE.json
+scales over 1/2/4/8 GPUs) — on synthetic seeded inputs already resident in HBM;
+N>1 = one process per GPU (torchrun), data-parallel with the NCCL gradient
+allreduce inside the step (weak scaling).
+Metric: learner frames/s (frames = B*T*repeat; repeat 1 for GRF; 4 for
+Atari / DMLab; C16).  The same JSON line carries the per-launch
+breakdown, the roofline of the dominant kernel, the e2e number through the
+public API (pinned H2D of every step's batch, D2H of the metrics), clocks, the
+CPU oracle baseline, the V-trace bandwidth leg (T=100, B=2^17, 367 MB > L2),
+inference steps/s (configs[4], on every rank), and the configs[1] / configs[2]
+learner steps with their own rooflines.
 --impl reference: the CPU oracle (oracle/, fp64 numpy) on a bounded sample of
-the same workload (rank 0 only) — the reference arm for this tier.
+the headline workload (rank 0 only) — the reference arm for this tier.
 """
 import argparse
 import json
@@ -30,7 +34,19 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-CFG = dict(name="c2", T=20, B=32, A=18, repeat=4)
+CONFIGS = {
+    "c2": dict(T=20, B=32, A=18, repeat=4, batch_kw={},
+               workload="c2 Atari IMPALA-shallow CNN + LSTM256 learner step (BASELINE.json "
+                        "configs[1]): 84x84x4 uint8, A=18, T=20, B=32/GPU"),
+    "c3": dict(T=100, B=32, A=15, repeat=4, batch_kw={},
+               workload="c3 DMLab IMPALA-deep ResNet (16,32,32) + LSTM256 learner step "
+                        "(BASELINE.json configs[2]): 72x96x3 uint8, A=15, T=100, B=32/GPU"),
+    "c4": dict(T=32, B=128, A=19, repeat=1, batch_kw=dict(smm=True),
+               workload="c4 Google Research Football SMM, IMPALA-deep (16,32,32,32) + LSTM256 "
+                        "learner step (BASELINE.json configs[3]): 72x96x16 uint8, A=19, T=32, "
+                        "B=128/GPU"),
+}
+HEAD = "c4"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK = dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0)
 
@@ -53,71 +69,124 @@ def dist_env():
     return world, rank, local
 
 
-# ---------------------------------------------------------------- algorithmic work per phase
-def phase_work(T, B, A):
-    """Algorithmic FLOPs and bytes of each step phase.  Convs count
-    the forward-equivalent MACs (no zero taps); bytes are compulsory HBM traffic
-    (every input read once, every output written once)."""
-    F = B * (T + 1)
-    P1, P2 = F * 400, F * 81
-    obs = F * 84 * 84 * 4
-    a1, a2 = P1 * 16 * 2, P2 * 32 * 2
-    Kxp, U = 288, 256
+# ---------------------------------------------------------------- algorithmic work per launch
+def deep_geometry(cfg):
+    """IMPALA-deep sections (C14): (H, W, cin, cin_rows, ch, H2, W2) per section."""
+    H, W, C = 72, 96, (3 if cfg == "c3" else 16)
+    chans = (16, 32, 32) if cfg == "c3" else (16, 32, 32, 32)
+    out, cin, cinp = [], C, 16
+    for ch in chans:
+        H2, W2 = (H + 1) // 2, (W + 1) // 2
+        out.append((H, W, cin, cinp, ch, H2, W2))
+        H, W, cin, cinp = H2, W2, ch, ch
+    return out
+
+
+def core_work(F, B, T, A, fc_in, P):
+    """FC / LSTM / heads / optimizer launches: algorithmic FLOPs and
+    compulsory HBM bytes (every input read once, every output written once)."""
+    Kxp = ((256 + A + 1 + 1 + 31) // 32) * 32
     X = F * Kxp * 2
     w = {}
-    w["obs_s2d"] = (0, obs * 3)          # uint8 obs -> space-to-depth bf16 S0
-    w["conv1_fwd"] = (2 * P1 * 16 * 256, obs * 2 + a1 + 16 * 256 * 2)
-    w["conv2_fwd"] = (2 * P2 * 32 * 256, a1 + a2 + 32 * 256 * 2)
-    w["fc_fwd"] = (2 * F * 256 * 2592, a2 + 256 * 2592 * 2 + F * 256 * 2)
-    w["core_extras"] = (0, F * 32 * 2 + F * 9)
-    w["xproj_fwd"] = (2 * F * 1024 * 275, X + 1024 * Kxp * 2 + F * 1024 * 4)
-    w["lstm_fwd"] = (2 * F * 1024 * 256, F * 1024 * 4 + 1024 * 256 * 2 + F * (256 * 4 * 2 + 1024 * 4 + 256 * 2))
-    # heads forward + policy loss + heads backward (one kernel + the weight-grad sum):
-    # H read, logits/values/dlogits written, dH written, per-trajectory partials
-    w["heads_loss"] = (6 * F * (A + 1) * 256,
-                       2 * F * 256 * 4 + 2 * F * (A + 1) * 4 + F * 9 + B * T * 8 + 2 * B * (A + 1) * 257 * 4)
+    w["core_extras"] = (0, F * (Kxp - 256) * 2 + F * 9)
+    w["fc_fwd"] = (2 * F * 256 * fc_in, F * fc_in * 2 + 256 * fc_in * 2 + F * 256 * 2)
+    w["xproj_fwd"] = (2 * F * 1024 * (256 + A + 1), X + 1024 * Kxp * 2 + F * 1024 * 4)
+    w["lstm_fwd"] = (2 * F * 1024 * 256, F * 1024 * 4 + 1024 * 256 * 2 +
+                     F * (256 * 4 * 2 + 1024 * 4 + 256 * 2))
+    w["heads_loss"] = (6 * F * (A + 1) * 256, 2 * F * 256 * 4 + 2 * F * (A + 1) * 4 + F * 9 +
+                       B * T * 8 + 2 * B * (A + 1) * 257 * 4)
     w["lstm_bwd"] = (2 * F * 1024 * 256, F * (1024 * 4 + 256 * 4 * 2 + 256 * 4 + 1024 * 2))
-    w["lstm_wgrad"] = (2 * 1024 * (275 + 1 + 256) * F, F * 1024 * 2 + X + F * 256 * 2 + 1024 * 532 * 4)
+    w["lstm_wgrad"] = (2 * 1024 * (256 + A + 2 + 256) * F,
+                       F * 1024 * 2 + X + F * 256 * 2 + 1024 * (Kxp + 256) * 4)
     w["dx_fc"] = (2 * F * 256 * 1024, F * 1024 * 2 + 1024 * Kxp * 2 + F * 256 * 2 * 2)
-    w["fc_wgrad"] = (2 * 256 * 2593 * F, F * 256 * 2 + a2 + 256 * 2593 * 4)
-    w["fc_dgrad"] = (2 * F * 2592 * 256, F * 256 * 2 + 256 * 2592 * 2 + 2 * a2)
-    w["conv2_wgrad"] = (2 * 256 * 32 * P2, a1 + a2 + 257 * 32 * 4)   # + bias row
-    w["conv2_dgrad"] = (2 * P2 * 32 * 256, a2 + 2 * a1 + 16 * 512 * 2)
-    w["conv1_wgrad"] = (2 * 256 * 16 * P1, obs * 2 + a1 + 257 * 16 * 4)
-    Pn = 1225795
-    w["grad_norm"] = (0, Pn * 4)
-    w["clip_adam"] = (0, Pn * 28)
-    w["lowp_refresh"] = (0, Pn * 6)
-    w["allreduce"] = (0, Pn * 4 * 2)
-    w["allreduce_tail"] = (0, 12336 * 4 * 2)
+    w["fc_wgrad"] = (2 * 256 * (fc_in + 1) * F, F * 256 * 2 + F * fc_in * 2 + 256 * (fc_in + 1) * 4)
+    w["fc_dgrad"] = (2 * F * fc_in * 256, F * 256 * 2 + 256 * fc_in * 2 + 2 * F * fc_in * 2)
+    w["grad_norm"] = (0, P * 4)
+    w["clip_adam"] = (0, P * 28)
+    w["lowp_refresh"] = (0, P * 6)
+    w["allreduce"] = (0, P * 4 * 2)
+    w["allreduce_tail"] = (0, P * 4 * 2)
     return w
 
 
+def launch_work(cfg, T, B, A, P, names):
+    """(FLOPs, bytes) of every traced launch, in order.  Convolutions count the
+    MACs of the definition (no padding taps); bytes are the op's compulsory
+    traffic on unpadded tensors (bf16 activations, uint8 obs)."""
+    F = B * (T + 1)
+    out = []
+    if cfg == "c2":
+        P1, P2 = F * 400, F * 81
+        obs = F * 84 * 84 * 4
+        a1, a2 = P1 * 16 * 2, P2 * 32 * 2
+        tw = {"obs_s2d": (0, obs * 3),
+              "conv1_fwd": (2 * P1 * 16 * 256, obs * 2 + a1 + 16 * 256 * 2),
+              "conv2_fwd": (2 * P2 * 32 * 256, a1 + a2 + 32 * 256 * 2),
+              "conv2_wgrad": (2 * 256 * 32 * P2, a1 + a2 + 257 * 32 * 4),
+              "conv2_dgrad": (2 * P2 * 32 * 256, a2 + 2 * a1 + 16 * 512 * 2),
+              "conv1_wgrad": (2 * 256 * 16 * P1, obs * 2 + a1 + 257 * 16 * 4)}
+        tw.update(core_work(F, B, T, A, 2592, P))
+        return [tw.get(n, (0, 0)) for n in names]
+    geo = deep_geometry(cfg)
+    ns = len(geo)
+    tw = core_work(F, B, T, A, geo[-1][5] * geo[-1][6] * geo[-1][4], P)
+    seen = {}
+    for n in names:
+        k = seen.get(n, 0)
+        seen[n] = k + 1
+        if not n.startswith("deep_") and n != "obs_bf16":
+            out.append(tw.get(n, (0, 0)))
+            continue
+        fwd = "_fwd" in n
+        if n == "obs_bf16":
+            H, W, cin, cinp = geo[0][0], geo[0][1], geo[0][2], geo[0][3]
+            out.append((0, F * H * W * (cin + cinp * 2)))
+            continue
+        if n.startswith("deep_res"):
+            s = k // 2 if fwd else ns - 1 - k // 2
+        else:
+            s = k if fwd else ns - 1 - k
+            if n == "deep_conv_dgrad":
+                s = ns - 1 - k
+        H, W, cin, cinp, ch, H2, W2 = geo[s]
+        Ai, Ao = F * H * W, F * H2 * W2
+        xin = Ai * (cinp * 2 if s == 0 else cin * 2)
+        if n == "deep_conv_fwd":
+            w = (2 * Ai * ch * 9 * cin, xin + Ai * ch * 2)
+        elif n == "deep_pool_fwd":
+            w = (0, Ai * ch * 2 + 2 * Ao * ch * 2 + Ao * ch)
+        elif n == "deep_res_fwd0":
+            w = (2 * Ao * ch * 9 * ch, 2 * Ao * ch * 2)
+        elif n == "deep_res_fwd1":
+            w = (2 * Ao * ch * 9 * ch, 4 * Ao * ch * 2)
+        elif n.startswith("deep_res_wgrad"):
+            w = (2 * Ao * 9 * ch * ch, 2 * Ao * ch * 2)
+        elif n == "deep_res_dgrad1":
+            w = (2 * Ao * 9 * ch * ch, 3 * Ao * ch * 2)
+        elif n == "deep_res_dgrad0":
+            w = (2 * Ao * 9 * ch * ch, 4 * Ao * ch * 2)
+        elif n == "deep_pool_bwd":
+            w = (0, Ao * ch * 2 + Ao * ch + Ai * ch * 2)
+        elif n == "deep_conv_wgrad":
+            w = (2 * Ai * 9 * cin * ch, xin + Ai * ch * 2)
+        elif n == "deep_conv_dgrad":
+            w = (2 * Ai * 9 * cin * ch, Ai * ch * 2 + Ai * cin * 2)
+        else:
+            w = (0, 0)
+        out.append(w)
+    return out
+
+
 # ---------------------------------------------------------------- committed ncu evidence
-PHASE_KERNEL = {"obs_s2d": "s2d_obs_kernel", "conv1_fwd": "Conv1S2dEpi", "conv2_fwd": "Conv2S2dEpi",
-                "fc_fwd": "FcFwd",
-                "xproj_fwd": "XprojFwd", "lstm_fwd": "lstm_fwd_kernel", "lstm_bwd": "lstm_bwd_kernel",
-                "lstm_wgrad": "LstmWgrad", "dx_fc": "DxFc", "fc_wgrad": "FcWgrad",
-                "fc_dgrad": "FcDgrad", "conv2_wgrad": "win_wgrad_kernel<32>",
-                "conv2_dgrad": "Conv2DgradS2dEpi", "conv1_wgrad": "win_wgrad_kernel<16>",
-                "heads_loss": "heads_loss_kernel",
-                "clip_adam": "adam_kernel"}
-
-
-def ncu_traffic(phase):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's main
-    kernel from the committed `ncu --set full` capture (profiles/r01/ncu_full.json)."""
-    key = PHASE_KERNEL.get(phase)
-    path = os.path.join(ROOT, "profiles", "r01", "ncu_full.json")
-    if not key or not os.path.exists(path):
+def ncu_traffic(label):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the launch `label` (phase#k)
+    from the committed `ncu --set full` summary (profiles/r02/ncu_traffic.json)."""
+    path = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
+    if not os.path.exists(path):
         return None
     with open(path) as f:
         d = json.load(f)
-    for name, ents in d.items():
-        if key in name and "splitk" not in name:
-            v = [e["dram_bytes"] for e in ents if e.get("dram_bytes") is not None]
-            return round(sum(v) / len(v)) if v else None
-    return None
+    return d.get(HEAD, {}).get(label)
 
 
 # ---------------------------------------------------------------- clocks (NVML)
@@ -169,12 +238,21 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU oracle baseline
-def oracle_step_time(B_sample, T, seed=0):
+# (B, T) of one bounded oracle step: the reference arm times one such step per
+# --steps (a few minutes for 25 steps); cpu_baseline one step of ORACLE_BASELINE
+# (10-30 s of CPU work)
+ORACLE_SAMPLE = dict(c2=(4, 20), c3=(1, 20), c4=(1, 32))
+ORACLE_BASELINE = dict(c2=(32, 20), c3=(4, 20), c4=(8, 32))
+
+
+def oracle_step_time(cfg, B_sample, T, seed=0):
     import oracle as O
     import seedgen
-    spec = O.spec_c2()
+    spec = {"c2": O.spec_c2, "c3": O.spec_c3, "c4": O.spec_c4}[cfg]()
+    obs_shape = (spec.obs_h, spec.obs_w, spec.obs_c)
     params = seedgen.glorot_params(O.param_layout(spec), seed=seed)
-    batch = seedgen.learner_batch((84, 84, 4), 18, B_sample, T, seed=seed)
+    batch = seedgen.learner_batch(obs_shape, spec.num_actions, B_sample, T, seed=seed,
+                                  **CONFIGS[cfg]["batch_kw"])
     hp = dict(discount=0.99, rho_bar=1.0, c_bar=1.0, vf_coef=0.5, ent_coef=0.01,
               loss_scale=1.0 / (B_sample * T), lr=3e-4, beta1=0.9, beta2=0.999, eps=1e-5,
               max_grad_norm=40.0, **{"lambda": 1.0})
@@ -193,37 +271,49 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(T):
-    B_s = 4
-    t = oracle_step_time(B_s, T)
-    frames = B_s * T * CFG["repeat"]
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(cfg):
+    B_s, T_s = ORACLE_BASELINE[cfg]
+    t = oracle_step_time(cfg, B_s, T_s)
+    frames = B_s * T_s * CONFIGS[cfg]["repeat"]
     return {"value": round(frames / t, 2), "unit": "learner frames/s", "cores": blas_threads(),
-            "kind": "oracle",
-            "sample": f"1 oracle learner step (fp64 numpy) of the c2 workload at B={B_s} "
-                      f"(of 32), T={T}: {t:.2f} s"}
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "kind": "oracle",
+            "sample": f"1 oracle learner step (fp64 numpy) of the {cfg} network at B={B_s}, "
+                      f"T={T_s} (of B={CONFIGS[cfg]['B']}, T={CONFIGS[cfg]['T']}): {t:.2f} s"}
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    T = CFG["T"]
-    B_s = 4
+    cfg = HEAD
+    B_s, T_s = ORACLE_SAMPLE[cfg]
     for _ in range(args.warmup):
-        oracle_step_time(B_s, T)
-    ts = [oracle_step_time(B_s, T, seed=i) for i in range(args.steps)]
+        oracle_step_time(cfg, B_s, T_s)
+    ts = [oracle_step_time(cfg, B_s, T_s, seed=i) for i in range(args.steps)]
     t = sum(ts) / len(ts)
-    frames = B_s * T * CFG["repeat"]
+    frames = B_s * T_s * CONFIGS[cfg]["repeat"]
     v = frames / t
     line = {"impl": "reference", "metric": "learner frames/sec", "value": round(v, 3),
             "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t * 1e3, 2), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"c2 Atari IMPALA-shallow + LSTM256 learner step, T={T}, "
-                                   f"B={B_s} sample of B=32 (CPU oracle)"},
+            "config": {"workload": CONFIGS[cfg]["workload"] +
+                       f" — CPU oracle on a B={B_s}, T={T_s} sample per step"},
             "cpu_baseline": {"value": round(v, 3), "unit": "frames/s", "cores": blas_threads(),
+                             "host_cpus": os.cpu_count(), "cpu_model": cpu_model(),
                              "kind": "oracle",
-                             "sample": f"{args.steps} oracle steps at B={B_s}, T={T}"},
+                             "sample": f"{args.steps} oracle steps at B={B_s}, T={T_s}"},
             "e2e": {"value": round(v, 3), "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -257,24 +347,32 @@ def vtrace_leg(S, torch, T=100, B=1 << 17, iters=20):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / iters
     nbytes = 28 * B * T + 4 * B
-    return {"T": T, "B": B, "bytes": nbytes, "us": round(us, 2), "GBs": round(nbytes / us / 1e3, 1)}
+    return {"T": T, "B": B, "bytes": nbytes, "us": round(us, 2), "GBs": round(nbytes / us / 1e3, 1),
+            "working_set": "367.5 MB > 126 MB L2 (20 back-to-back calls in one graph)"}
 
 
 # ---------------------------------------------------------------- inference leg (c5)
-def inference_leg(S, torch, iters=20):
-    """configs[4]: 4096 actors, per-actor LSTM state table, Atari net; one
-    seed_infer call per step over n actor ids (device-resident requests, CUDA
-    graph per n) and host-fed (pinned H2D of the n observations inside the timed
-    region).  steps/s = n / call time."""
+def inference_leg(S, torch, world, rank, dist, iters=20):
+    """configs[4]: 4096 actors per GPU, per-actor LSTM state table, Atari net; one
+    seed_infer call per step over n actor ids (device-resident requests, CUDA graph
+    per n) and host-fed (pinned H2D of the n observations + D2H of the actions
+    inside the timed region).  steps/s = N * n / (max over ranks of the call time)."""
     import seedgen
     NA = 4096
     spec = S.spec_for_config("c5")
     params = seedgen.glorot_params(S.net_param_layout(spec), seed=0)
     learner = S.Learner(spec, 1, 1, params)
     srv = S.InferenceServer(spec, NA, 1024, learner=learner)
-    out = {"actors": NA, "sweep": []}
+    out = {"actors_per_gpu": NA, "n_gpus": world, "sweep": []}
+
+    def tmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     for n in (64, 128, 256, 512, 1024):
-        req = seedgen.infer_requests((84, 84, 4), 18, NA, n, seed=0)
+        req = seedgen.infer_requests((84, 84, 4), 18, NA, n, seed=rank)
         d = {k: torch.from_numpy(v).cuda() for k, v in req.items()}
         a = torch.empty(n, dtype=torch.int32, device="cuda")
         blp = torch.empty(n, device="cuda")
@@ -299,12 +397,22 @@ def inference_leg(S, torch, iters=20):
             g.replay()
         e1.record()
         torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / iters
-        row = {"n": n, "us_per_call": round(us, 2), "steps_per_s": round(n / us * 1e6, 1)}
+        us = tmax(e0.elapsed_time(e1) * 1e3 / iters)
+        row = {"n": n, "us_per_call": round(us, 2), "steps_per_s": round(world * n / us * 1e6, 1)}
         if n == 1024:   # host-fed: pinned H2D of the requests + D2H of the actions
             hobs = torch.from_numpy(req["obs"]).pin_memory()
             hact = torch.empty(n, dtype=torch.int32).pin_memory()
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # same-job pinned H2D probe of the same bytes: the PCIe denominator
+            tp0, tp1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d["obs"].copy_(hobs, non_blocking=True)
+            torch.cuda.synchronize()
+            tp0.record()
+            for _ in range(iters):
+                d["obs"].copy_(hobs, non_blocking=True)
+            tp1.record()
+            torch.cuda.synchronize()
+            h2d_us = tp0.elapsed_time(tp1) * 1e3 / iters
             tot = 0.0
             for _ in range(iters):
                 t0.record()
@@ -314,173 +422,183 @@ def inference_leg(S, torch, iters=20):
                 t1.record()
                 torch.cuda.synchronize()
                 tot += t0.elapsed_time(t1)
-            hus = tot * 1e3 / iters
-            row.update(host_fed_us=round(hus, 2), host_fed_steps_per_s=round(n / hus * 1e6, 1),
-                       h2d_bytes=int(hobs.numel()))
+            hus = tmax(tot * 1e3 / iters)
+            row.update(host_fed_us=round(hus, 2),
+                       host_fed_steps_per_s=round(world * n / hus * 1e6, 1),
+                       h2d_bytes=int(hobs.numel()), h2d_probe_us=round(h2d_us, 2),
+                       h2d_probe_GBs=round(hobs.numel() / h2d_us / 1e3, 2),
+                       host_fed_vs_probe=round(hus / max(h2d_us + us, 1e-9), 3))
         out["sweep"].append(row)
+    del srv, learner
     return out
 
 
-def other_configs_leg(S, torch, steps=3):
-    """Learner-step timing of the other BASELINE.json configs (CUDA graph, L2
-    flushed between steps): c1 MLP fp32 (T=20, B=8), c3 DMLab IMPALA-deep
-    (T=100, B=32), c4 GRF SMM (T=32, B=128, repeat 1)."""
+# ---------------------------------------------------------------- one learner config
+def make_learner(S, torch, cfg, world, rank, comm):
     import seedgen
-    res = {}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for cfg, T, B, rep, kw in (("c1", 20, 8, 1, dict(float_obs=True, lstm_units=0)),
-                               ("c3", 100, 32, 4, {}), ("c4", 32, 128, 1, dict(smm=True))):
-        spec = S.spec_for_config(cfg)
-        params = seedgen.glorot_params(S.net_param_layout(spec), seed=0,
-                                       lstm_units=max(spec.lstm_units, 1))
-        L = S.Learner(spec, T, B, params, S.HParams(loss_scale=1.0 / (B * T)))
-        host = seedgen.learner_batch(spec.obs_shape, spec.num_actions, B, T, seed=1, **kw)
-        dev = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
-        L.step(dev)
-        torch.cuda.synchronize()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            L.step(dev, stream=s)
-        torch.cuda.synchronize()
-        g.replay()
-        ms = 0.0
-        for _ in range(steps):
-            flush.add_(1)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            g.replay()
-            e1.record()
-            torch.cuda.synchronize()
-            ms += e0.elapsed_time(e1)
-        ms /= steps
-        res[cfg] = {"T": T, "B": B, "ms_per_step": round(ms, 3),
-                    "learner_frames_per_s": round(B * T * rep / (ms / 1e3), 1),
-                    "env_steps_per_s": round(B * T / (ms / 1e3), 1)}
-        del L, dev, g
-        torch.cuda.empty_cache()
-    return res
-
-
-# ---------------------------------------------------------------- ours
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-
-    import paper_1910_06591_b200 as S
-    import seedgen
-    from paper_1910_06591_b200 import _lib as L
-
-    world, rank, local = dist_env()
-    assert torch.cuda.is_available(), "bench.py needs a GPU"
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("gloo", init_method="env://", rank=rank, world_size=world)
-    T, B, A = CFG["T"], CFG["B"], CFG["A"]
-    spec = S.spec_for_config("c2")
-    layout = S.net_param_layout(spec)
-    params = seedgen.glorot_params(layout, seed=0)  # identical on every rank
-    hp = S.HParams(lam=1.0, loss_scale=1.0 / (world * B * T))
-    comm = S.Comm(rank, world) if world > 1 else None
-    learner = S.Learner(spec, T, B, params, hp, comm=comm)
-    host = seedgen.learner_batch((84, 84, 4), A, B, T, seed=1000 + rank)
+    c = CONFIGS[cfg]
+    spec = S.spec_for_config(cfg)
+    params = seedgen.glorot_params(S.net_param_layout(spec), seed=0)   # identical on every rank
+    hp = S.HParams(lam=1.0, loss_scale=1.0 / (world * c["B"] * c["T"]))
+    L = S.Learner(spec, c["T"], c["B"], params, hp, comm=comm)
+    host = seedgen.learner_batch(spec.obs_shape, spec.num_actions, c["B"], c["T"],
+                                 seed=1000 + rank, **c["batch_kw"])
     pinned = {k: torch.from_numpy(v).pin_memory() for k, v in host.items()}
     dev = {k: v.cuda() for k, v in pinned.items()}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    return spec, L, pinned, dev
 
-    # ---- warm-up (sets kernel attributes; eager)
-    for _ in range(max(args.warmup, 3)):
-        learner.step(dev)
-    torch.cuda.synchronize()
 
-    # ---- capture the traced step in a CUDA graph (events after every phase)
-    MAXE = 64
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(MAXE)]
+def traced_graph(S, torch, L, spec, dev, comm, maxe=160):
+    """A CUDA graph of the step with an event node after every launch group
+    (seed_learner_step_traced) -> per-launch times; the plain graph is separate."""
+    import ctypes as C
+    from paper_1910_06591_b200 import _lib as Lb
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(maxe)]
     for e in evs:
         e.record()
     torch.cuda.synchronize()
-    ev_arr = (L.c_void_p * MAXE)(*[e.cuda_event for e in evs])
-    names = (L.C.c_char_p * MAXE)()
-    n_ev, n_launch = L.c_int(), L.c_int()
-    import ctypes as C
-    spec_c = spec.c()
-    hp_c = hp.c()
-    cb = learner._batch(dev)
-    ts = L.TrainState(*(C.c_void_p(t.data_ptr()) for t in (learner.params, learner.grads,
-                                                             learner.m, learner.v)),
-                      C.c_void_p(learner.lowp.data_ptr()), C.c_void_p(learner.step_counter.data_ptr()))
+    ev_arr = (Lb.c_void_p * maxe)(*[e.cuda_event for e in evs])
+    names = (Lb.C.c_char_p * maxe)()
+    n_ev, n_launch = Lb.c_int(), Lb.c_int()
+    spec_c, hp_c = spec.c(), L.hp.c()
+    cb = L._batch(dev)
+    ts = L._train_state()
 
     def traced(stream):
-        st = L.load().seed_learner_step_traced(
-            C.byref(spec_c), T, B, C.byref(cb), C.byref(ts), C.byref(hp_c),
-            comm.handle if comm else None, C.c_void_p(learner.ws.data_ptr()), learner.ws.numel(),
-            C.c_void_p(learner.metrics.data_ptr()), C.c_void_p(stream.cuda_stream), ev_arr, MAXE,
+        st = Lb.load().seed_learner_step_traced(
+            C.byref(spec_c), L.T, L.B, C.byref(cb), C.byref(ts), C.byref(hp_c),
+            comm.handle if comm else None, C.c_void_p(L.ws.data_ptr()), L.ws.numel(),
+            C.c_void_p(L.metrics.data_ptr()), C.c_void_p(stream.cuda_stream), ev_arr, maxe,
             names, C.byref(n_ev), C.byref(n_launch))
-        L.check(st, "seed_learner_step_traced")
+        Lb.check(st, "seed_learner_step_traced")
 
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
-        traced(s)   # eager once on the capture stream
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=s):
         traced(s)
     torch.cuda.synchronize()
-    # the same step without event nodes (headline timing)
-    plain = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(plain, stream=s):
-        learner.step(dev, stream=s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        traced(s)
     torch.cuda.synchronize()
     nE = n_ev.value
-    phase_names = [names[i].decode() for i in range(nE)]
-    launches_per_step = n_launch.value
-    for _ in range(2):
-        graph.replay()
-    torch.cuda.synchronize()
+    return g, evs, [names[i].decode() for i in range(nE)], n_launch.value
 
+
+def measure_learner(S, torch, dist, cfg, steps, warmup, world, rank, local, comm, clocks=True,
+                    e2e=True):
+    c = CONFIGS[cfg]
+    T, B, A = c["T"], c["B"], c["A"]
+    spec, L, pinned, dev = make_learner(S, torch, cfg, world, rank, comm)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    for _ in range(max(warmup, 3)):
+        L.step(dev)
+    torch.cuda.synchronize()
+    tgraph, evs, names, launches = traced_graph(S, torch, L, spec, dev, comm)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    plain = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(plain, stream=s):
+        L.step(dev, stream=s)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        plain.replay()
+        tgraph.replay()
+    torch.cuda.synchronize()
     # ---- timed region: K replays of the plain step graph, L2 flushed between
-    K = args.steps
+    K = steps
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     e1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     flush.random_()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for i in range(K):
-            flush.add_(1)                      # L2 flush, outside the timed events
-            e0[i].record()
-            plain.replay()
-            e1[i].record()
-        torch.cuda.synchronize()
+    clk = ClockSampler(local) if clocks else None
+    if clk:
+        clk.__enter__()
+    for i in range(K):
+        flush.add_(1)                      # L2 flush, outside the timed events
+        e0[i].record()
+        plain.replay()
+        e1[i].record()
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(e0, e1)]
-    # ---- per-phase breakdown: the traced graph (an event node after every phase)
-    phase_ms = {n: 0.0 for n in phase_names[1:]}
-    traced_ms = 0.0
-    for i in range(K):
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total.item()) / K
+    # ---- per-launch breakdown from the traced graph (event node after every launch group)
+    nE = len(names)
+    Kt = max(2, min(K, 10))
+    per = [0.0] * nE
+    for _ in range(Kt):
         flush.add_(1)
-        graph.replay()
+        tgraph.replay()
         torch.cuda.synchronize()
         for j in range(1, nE):
-            phase_ms[phase_names[j]] += evs[j - 1].elapsed_time(evs[j])
-        traced_ms += evs[0].elapsed_time(evs[nE - 1])
-    total_ms = sum(step_ms)
-    t_local = torch.tensor([total_ms], dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    total_ms = float(t_local.item())
-    ms_per_step = total_ms / K
-    frames = world * B * T * CFG["repeat"]
-    value = frames / (ms_per_step / 1e3)
+            per[j] += evs[j - 1].elapsed_time(evs[j])
+    per = [p / Kt for p in per]
+    work = launch_work(cfg, T, B, A, int(L.params.numel()), names[1:])
+    seen, kernels = {}, []
+    for j in range(1, nE):
+        n = names[j]
+        k = seen.get(n, 0) + 1
+        seen[n] = k
+        f, b = work[j - 1]
+        us = per[j] * 1e3
+        kernels.append({"launch": f"{n}#{k}", "us": round(us, 2),
+                        "share": round(per[j] / ms_per_step, 4),
+                        "TFLOPs": round(f / (us * 1e-6) / 1e12, 2) if f and us > 0 else None,
+                        "GBs": round(b / (us * 1e-6) / 1e9, 1) if b and us > 0 else None,
+                        "flops": f, "bytes": b})
+    frames = world * B * T * c["repeat"]
+    out = {"cfg": cfg, "ms_per_step": ms_per_step, "frames_per_step": frames,
+           "value": frames / (ms_per_step / 1e3), "env_steps_per_s": world * B * T / (ms_per_step / 1e3),
+           "gpu_launches_per_step": launches, "kernels": kernels,
+           "traced_ms_per_step": sum(per[1:]),
+           "clocks": clk.summary() if clk else None,
+           "step_ms_p10_p50_p90": [round(float(np.percentile(step_ms, q)), 4) for q in (10, 50, 90)]}
+    out["roofline"] = roofline_of(kernels, cfg)
+    if e2e:
+        out["e2e"] = e2e_leg(torch, dist, L, dev, pinned, steps, world, frames)
+    del L, dev, pinned, tgraph, plain, flush
+    torch.cuda.empty_cache()
+    return out
 
-    # ---- e2e through the public API: every step copies its batch from pinned host
-    # memory (H2D) and reads its metrics back (D2H) inside the timed region; the
-    # batch is double-buffered on a copy stream so step i's H2D overlaps step
-    # i-1's compute (the way a learner is fed: SEED's prefetch, P:125)
+
+def roofline_of(kernels, cfg):
+    """Roofline of the dominant launch: algorithmic FLOPs (or bytes) ÷ its measured
+    average duration, against the measured tensor-core (or HBM) peak."""
+    pk = peaks()
+    dom = max(kernels, key=lambda k: k["us"])
+    ridge = pk["bf16_tflops_sustained"] * 1e12 / (pk["hbm_gbs"] * 1e9)
+    t_s = dom["us"] * 1e-6
+    f, b = dom["flops"], dom["bytes"]
+    if f and f / max(b, 1) >= ridge:
+        roof = {"bound": "tensor", "achieved": round(f / t_s / 1e12, 3),
+                "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": round(b / t_s / 1e9, 2), "peak": pk["hbm_gbs"],
+                "unit": "GB/s"}
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["traffic"] = ncu_traffic(dom["launch"]) if cfg == HEAD else None
+    roof["kernel"] = dom["launch"]
+    roof["us_per_launch"] = dom["us"]
+    roof["algorithmic"] = {"flops": f, "bytes": b}
+    roof["peak_source"] = pk["source"] + (" sustained bf16" if roof["bound"] == "tensor" else "")
+    return roof
+
+
+def e2e_leg(torch, dist, L, dev, pinned, steps, world, frames):
+    """The same metric through the public API (Learner.step, eager): every step
+    copies its batch from pinned host memory (H2D) and reads its metrics back
+    (D2H) inside the timed region; the batch is double-buffered on a copy stream
+    so step i's H2D overlaps step i-1's compute (the way a learner is fed:
+    SEED's prefetch)."""
     h2d = sum(v.numel() * v.element_size() for v in pinned.values())
     d2h = 8 * 4
     torch.cuda.synchronize()
@@ -492,7 +610,7 @@ def run_ours(args):
     hb.record()
     torch.cuda.synchronize()
     h2d_alone_ms = ha.elapsed_time(hb) / 3
-    Ke = max(4, min(K, 20))
+    Ke = max(4, min(steps, 20))
     s_comp = torch.cuda.current_stream()
     s_copy = torch.cuda.Stream()
     devs = [dev, {k: torch.empty_like(v) for k, v in dev.items()}]
@@ -514,80 +632,87 @@ def run_ours(args):
                 devs[b][k].copy_(v, non_blocking=True)
             ready[b].record(s_copy)
         s_comp.wait_event(ready[b])
-        m = learner.step(devs[b])
+        m = L.step(devs[b])
         outs[b].copy_(m, non_blocking=True)
         freed[b].record(s_comp)
     e1.record(s_comp)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / Ke
-    t_e2e = torch.tensor([e2e_ms], dtype=torch.float64)
+    t = torch.tensor([e2e_ms], dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = frames / (float(t_e2e.item()) / 1e3)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    del devs
+    return {"value": round(frames / (float(t.item()) / 1e3), 1), "unit": "frames/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(float(t.item()), 4),
+            "api": "Learner.step (eager): pinned H2D of each step's batch on a copy stream, "
+                   "double-buffered (overlaps the previous step), D2H of the metrics",
+            "h2d_ms_alone": round(h2d_alone_ms, 4),
+            "h2d_GBs_alone": round(h2d / (h2d_alone_ms * 1e-3) / 1e9, 2)}
 
-    if rank != 0:
-        if world > 1:
-            dist.barrier()
-        return
-    # ---- roofline of the dominant phase
-    pk = peaks()
-    work = phase_work(T, B, A)
-    per_phase = {n: phase_ms[n] / K for n in phase_ms}
-    dom = max(per_phase, key=per_phase.get)
-    flops, nbytes = work.get(dom, (0, 0))
-    ridge = pk["bf16_tflops_sustained"] * 1e12 / (pk["hbm_gbs"] * 1e9)
-    t_s = per_phase[dom] / 1e3
-    if flops and flops / max(nbytes, 1) >= ridge:
-        roof = {"bound": "tensor", "achieved": round(flops / t_s / 1e12, 3),
-                "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s"}
-    else:
-        roof = {"bound": "hbm", "achieved": round(nbytes / t_s / 1e9, 2), "peak": pk["hbm_gbs"],
-                "unit": "GB/s"}
-    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
-    roof["traffic"] = ncu_traffic(dom)
-    roof["kernel"] = dom
-    roof["us_per_launch"] = round(per_phase[dom] * 1e3, 2)
-    roof["peak_source"] = pk["source"]
-    kernels = []
-    for n in phase_names[1:]:
-        f, b = work.get(n, (0, 0))
-        us = per_phase[n] * 1e3
-        kernels.append({"phase": n, "us": round(us, 2), "share": round(per_phase[n] / ms_per_step, 4),
-                        "TFLOPs": round(f / (us * 1e-6) / 1e12, 3) if f else None,
-                        "GBs": round(b / (us * 1e-6) / 1e9, 1) if b else None})
-    vt = vtrace_leg(S, torch)
-    vt["frac"] = round(vt["GBs"] / pk["hbm_gbs"], 4)
+
+# ---------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_06591_b200 as S
+
+    world, rank, local = dist_env()
+    assert torch.cuda.is_available(), "bench.py needs a GPU"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://", rank=rank, world_size=world)
+    comm = S.Comm(rank, world) if world > 1 else None
+    head = measure_learner(S, torch, dist, HEAD, args.steps, args.warmup, world, rank, local,
+                           comm)
     extra = {}
-    if world == 1 and not args.no_extra:
-        extra["inference"] = inference_leg(S, torch)
-        extra["other_configs"] = other_configs_leg(S, torch)
-    line = {
-        "metric": "learner frames/sec", "value": round(value, 1), "unit": "frames/s",
-        "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic",
-        "config": {"workload": "c2 Atari IMPALA-shallow CNN + LSTM256 learner step "
-                               "(BASELINE.json configs[1]): 84x84x4 uint8, A=18, T=20, B=32/GPU",
-                   "global_batch": world * B, "seq_len": T + 1, "parallelism": f"dp{world}",
-                   "frames_per_step": frames, "l2": "flushed (256 MiB write) between timed steps",
-                   "timing": "CUDA-graph replay, CUDA events per step, max over ranks"},
-        "env_steps_per_s": round(value / CFG["repeat"], 1),
-        "gpu_launches": launches_per_step * K,
-        "traced_ms_per_step": round(traced_ms / K, 4),
-        "kernels": kernels,
-        "roofline": roof,
-        "vtrace": vt,
-        "e2e": {"value": round(e2e_value, 1), "unit": "frames/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
-                "api": "Learner.step (eager): pinned H2D of each step's batch on a copy stream, "
-                       "double-buffered (overlaps the previous step), D2H of the metrics",
-                "h2d_ms_alone": round(h2d_alone_ms, 4)},
-        "clocks": clk.summary(),
-        **extra,
-    }
-    if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(T)
-    print(json.dumps(line), flush=True)
+    if not args.no_extra:
+        # the other learner configs (fewer timed steps) and inference, on every rank
+        for cfg, k in (("c2", max(20, min(args.steps, 100))), ("c3", max(5, min(args.steps, 20)))):
+            r = measure_learner(S, torch, dist, cfg, k, 3, world, rank, local, comm, clocks=False,
+                                e2e=False)
+            extra[cfg] = {"workload": CONFIGS[cfg]["workload"], "steps": k,
+                          "ms_per_step": round(r["ms_per_step"], 4),
+                          "learner_frames_per_s": round(r["value"], 1),
+                          "env_steps_per_s": round(r["env_steps_per_s"], 1),
+                          "gpu_launches_per_step": r["gpu_launches_per_step"],
+                          "roofline": r["roofline"],
+                          "top_kernels": sorted(r["kernels"], key=lambda x: -x["us"])[:8]}
+        inf = inference_leg(S, torch, world, rank, dist)
+    c = CONFIGS[HEAD]
+    if rank == 0:
+        vt = vtrace_leg(S, torch)
+        vt["frac"] = round(vt["GBs"] / peaks()["hbm_gbs"], 4)
+        line = {
+            "metric": "learner frames/sec", "value": round(head["value"], 1), "unit": "frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(head["ms_per_step"], 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": c["workload"], "global_batch": world * c["B"],
+                       "seq_len": c["T"] + 1, "parallelism": f"dp{world}",
+                       "frames_per_step": head["frames_per_step"],
+                       "l2": "flushed (256 MiB write) between timed steps; the 467 MB obs batch "
+                             "alone exceeds the 126 MB L2",
+                       "timing": "CUDA-graph replay, CUDA events per step, max over ranks"},
+            "env_steps_per_s": round(head["env_steps_per_s"], 1),
+            "gpu_launches": head["gpu_launches_per_step"] * args.steps,
+            "step_ms_p10_p50_p90": head["step_ms_p10_p50_p90"],
+            "traced_ms_per_step": round(head["traced_ms_per_step"], 4),
+            "roofline": head["roofline"],
+            "e2e": head["e2e"],
+            "clocks": head["clocks"],
+            "kernels": [{k: v for k, v in x.items() if k not in ("flops", "bytes")}
+                        for x in head["kernels"]],
+            "vtrace": vt,
+        }
+        if not args.no_extra:
+            line["other_configs"] = extra
+            line["inference"] = inf
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(HEAD)
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
 
@@ -595,11 +720,12 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the inference / other-config legs")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the other-config / inference legs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -53,6 +53,9 @@ typedef enum {
 } seed_status;
 
 const char* seed_status_string(int status);
+/* Diagnostics: the CUDA error string behind the last SEED_E_CUDA returned to
+ * this thread (thread-local; "no error" if none). */
+const char* seed_last_cuda_error(void);
 /* Library ABI version (this header): 1. */
 int seed_abi_version(void);
 

@@ -89,9 +89,21 @@ def spec_c3(num_actions=15):
     return NetSpec(NET_IMPALA_DEEP, 72, 96, 3, num_actions, sections=(16, 32, 32))
 
 
-def spec_c4(num_actions=19):
-    """BJ configs[3]: GRF SMM 72x96x16, IMPALA-deep block (16,32,32,32) + LSTM256."""
-    return NetSpec(NET_GFOOTBALL, 72, 96, 16, num_actions, sections=(16, 32, 32, 32))
+def spec_c4(num_actions=19, obs_h=72, obs_w=96):
+    """BJ configs[3]: GRF SMM 72x96x16, IMPALA-deep block (16,32,32,32) + LSTM256.
+    P:358: the SMM is 96 x 72 by default, Medium 120 x 90, Large 144 x 108
+    (width x height)."""
+    return NetSpec(NET_GFOOTBALL, obs_h, obs_w, 16, num_actions, sections=(16, 32, 32, 32))
+
+
+def spec_c4_medium(num_actions=19):
+    """P:358 Medium SMM: 120 x 90 (W x H)."""
+    return spec_c4(num_actions, obs_h=90, obs_w=120)
+
+
+def spec_c4_large(num_actions=19):
+    """P:358 Large SMM: 144 x 108 (W x H)."""
+    return spec_c4(num_actions, obs_h=108, obs_w=144)
 
 
 def _same_out(n, s):

@@ -53,6 +53,7 @@ class ParamSnapshot(C.Structure):
 _SIGS = {
     "seed_status_string": (C.c_char_p, [c_int]),
     "seed_abi_version": (c_int, []),
+    "seed_last_cuda_error": (C.c_char_p, []),
     "seed_vtrace": (c_int, [c_int, c_int] + [c_void_p] * 6 + [c_float] * 3 +
                     [c_void_p, c_void_p, c_void_p, c_void_p]),
     "seed_net_param_count": (c_int, [P(NetSpec), P(c_int64)]),
@@ -128,4 +129,6 @@ def load():
 def check(status, what=""):
     if status != 0:
         msg = load().seed_status_string(status).decode()
+        if status == 4:   # SEED_E_CUDA: the CUDA error behind it
+            msg += f" [{load().seed_last_cuda_error().decode()}]"
         raise SeedError(f"{what}: {msg} ({status})")

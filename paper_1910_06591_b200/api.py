@@ -97,13 +97,16 @@ class NetSpec:
 
 
 def spec_for_config(cfg):
-    """BASELINE.json configs -> NetSpec (c1..c5)."""
+    """BASELINE.json configs -> NetSpec (c1..c5; c4m / c4l the larger Football SMMs)."""
     return {
         "c1": NetSpec(NET_MLP, 1, 1, 16, 4, 0),
         "c2": NetSpec(NET_ATARI_SHALLOW, 84, 84, 4, 18, 256),
         "c3": NetSpec(NET_IMPALA_DEEP, 72, 96, 3, 15, 256),
         "c4": NetSpec(NET_GFOOTBALL, 72, 96, 16, 19, 256),
         "c5": NetSpec(NET_ATARI_SHALLOW, 84, 84, 4, 18, 256),
+        # SURVEY §8(f) row 3, P:358: Football SMM Medium 120x90 / Large 144x108 (W x H)
+        "c4m": NetSpec(NET_GFOOTBALL, 90, 120, 16, 19, 256),
+        "c4l": NetSpec(NET_GFOOTBALL, 108, 144, 16, 19, 256),
     }[cfg]
 
 

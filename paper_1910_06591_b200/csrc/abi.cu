@@ -16,3 +16,12 @@ extern "C" const char* seed_status_string(int s) {
 }
 
 extern "C" int seed_abi_version(void) { return 1; }
+
+namespace seed {
+static thread_local cudaError_t g_last_cuda_error = cudaSuccess;
+void note_cuda_error(cudaError_t e) { g_last_cuda_error = e; }
+}  // namespace seed
+
+extern "C" const char* seed_last_cuda_error(void) {
+  return cudaGetErrorString(seed::g_last_cuda_error);
+}

@@ -13,10 +13,15 @@
 #error "libseed is sm_100a-only"
 #endif
 
+namespace seed { void note_cuda_error(cudaError_t e); }
+
 #define SEED_CUDA_TRY(expr)                                   \
   do {                                                        \
     cudaError_t _e = (expr);                                  \
-    if (_e != cudaSuccess) return SEED_E_CUDA;                \
+    if (_e != cudaSuccess) {                                  \
+      ::seed::note_cuda_error(_e);                            \
+      return SEED_E_CUDA;                                     \
+    }                                                         \
   } while (0)
 
 #define SEED_TRY(expr)                                        \
@@ -27,8 +32,13 @@
 
 namespace seed {
 
+// Diagnostics: note_cuda_error keeps the last CUDA error a library call of this
+// thread saw (seed_last_cuda_error in include/seed.h).
+
 static inline seed_status last_launch() {
-  return cudaGetLastError() == cudaSuccess ? SEED_OK : SEED_E_CUDA;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) note_cuda_error(e);
+  return e == cudaSuccess ? SEED_OK : SEED_E_CUDA;
 }
 
 static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -53,8 +63,11 @@ static inline seed_status smem_optin(PerDevice& flag, Kern kern, size_t bytes) {
   const int dev = current_device();
   if (dev < 0 || dev >= SEED_MAX_DEVICES) return SEED_E_CUDA;
   if (!flag.done(dev)) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) {
+      note_cuda_error(e);
       return SEED_E_CUDA;
+    }
     flag.set(dev);
   }
   return SEED_OK;
@@ -105,7 +118,9 @@ inline seed_status launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args...) == cudaSuccess ? SEED_OK : SEED_E_CUDA;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, kern, args...);
+  if (err != cudaSuccess) note_cuda_error(err);
+  return err == cudaSuccess ? SEED_OK : SEED_E_CUDA;
 }
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

@@ -17,6 +17,7 @@ template <int MODE, int NN>
 struct W3FwdEpi {
   static constexpr int N = NN;
   static constexpr int RB = 2 * NN;
+  static constexpr int PRE = MODE == W3_RES ? N / 8 : 0;   // the residual row
   PadGeo g;
   float in_scale;
   const float* bias;
@@ -24,7 +25,15 @@ struct W3FwdEpi {
   uint8_t* out;
   uint8_t* outr;
   bf16* dense;
-  __device__ void store(int64_t m, float (&v)[N]) const {
+  __device__ void pre(int64_t m, uint4 (&p)[PRE > 0 ? PRE : 1]) const {
+#pragma unroll
+    for (int j = 0; j < PRE; ++j) p[j] = __ldg(chunk_at(res, m, RB, j));
+  }
+  __device__ void store(int64_t m, float (&v)[N]) const {   // PRE == 0 modes
+    const uint4 p[1] = {make_uint4(0, 0, 0, 0)};
+    store(m, v, p);
+  }
+  __device__ void store(int64_t m, float (&v)[N], const uint4 (&p)[PRE > 0 ? PRE : 1]) const {
     int f, y, x;
     if (!g.split(m, f, y, x)) {
       if (MODE != W3_PLAIN) {
@@ -46,7 +55,7 @@ struct W3FwdEpi {
 #pragma unroll
       for (int j = 0; j < N / 8; ++j) {
         float r[8];
-        unpack8(*chunk_at(res, m, RB, j), r);
+        unpack8(p[j], r);
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[8 * j + k] += r[k];
       }
@@ -72,11 +81,26 @@ template <int MODE, int NN>
 struct W3DgradEpi {
   static constexpr int N = NN;
   static constexpr int RB = 2 * NN;
+  // the mask row, then (D3W_RES) the incoming residual-gradient row
+  static constexpr int PRE = MODE == D3W_PLAIN ? 0 : (MODE == D3W_MASK ? N / 8 : N / 4);
   PadGeo g;
   const uint8_t* mask;
   const uint8_t* dres;
   uint8_t* dX;
-  __device__ void store(int64_t m, float (&v)[N]) const {
+  __device__ void pre(int64_t m, uint4 (&p)[PRE > 0 ? PRE : 1]) const {
+    if (MODE == D3W_PLAIN) return;
+#pragma unroll
+    for (int j = 0; j < N / 8; ++j) p[j] = __ldg(chunk_at(mask, m, RB, j));
+    if (MODE == D3W_RES) {
+#pragma unroll
+      for (int j = 0; j < N / 8; ++j) p[N / 8 + j] = __ldg(chunk_at(dres, m, RB, j));
+    }
+  }
+  __device__ void store(int64_t m, float (&v)[N]) const {   // PRE == 0 modes
+    const uint4 p[1] = {make_uint4(0, 0, 0, 0)};
+    store(m, v, p);
+  }
+  __device__ void store(int64_t m, float (&v)[N], const uint4 (&p)[PRE > 0 ? PRE : 1]) const {
     int f, y, x;
     if (!g.split(m, f, y, x)) {
       const uint4 z = make_uint4(0, 0, 0, 0);
@@ -88,7 +112,7 @@ struct W3DgradEpi {
 #pragma unroll
       for (int j = 0; j < N / 8; ++j) {
         float mk[8];
-        unpack8(*chunk_at(mask, m, RB, j), mk);
+        unpack8(p[j], mk);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           if (!(mk[k] > 0.f)) v[8 * j + k] = 0.f;
@@ -98,7 +122,7 @@ struct W3DgradEpi {
 #pragma unroll
       for (int j = 0; j < N / 8; ++j) {
         float r[8];
-        unpack8(*chunk_at(dres, m, RB, j), r);
+        unpack8(p[N / 8 + j], r);
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[8 * j + k] += r[k];
       }
@@ -131,11 +155,28 @@ struct W3Fin {
 
 // ------------------------------------------------------------------ forward
 // 128-row blocks per window-conv tile (measured per shape, scripts/phases.py
-// PER_LAUNCH=1 at MT = 1 / 2 / 4): 16-channel outputs 4; 32-channel 2, residual
-// forward 1 (its epilogue reads a second input row and writes two)
+// PER_LAUNCH=1 at MT = 1 / 2 / 4): 16-channel outputs 4; 32-channel 2 (the
+// residual forward's second input row is prefetched before the accumulator wait)
 template <int MODE, int N, bool FWD>
-constexpr int w3_mt() { return N == 16 ? 4 : (FWD && MODE == W3_RES) ? 1 : 2; }
+constexpr int w3_mt() { return N == 16 ? 4 : 2; }
 // NW = 9: 3 x 3 taps as row windows; NW = 3: x-im2col input, 3 row windows (ky)
+// Column-tap-stacked kernels (win_engine.cuh win_conv_kx_kernel: 3 MMAs of
+// N = 3*out per 128 rows, neighbour-row combine in the epilogue) vs the 9-window
+// kernels (9 MMAs of N = out, no combine).  Measured per launch at c4
+// (profiles/r02/kx_vs_9window.md): the combine's shuffles cost more than the six
+// saved ~45-cycle MMAs everywhere except when K = 32 input channels feed 16
+// outputs (RB = 64, N = 16: 18 -> 6 MMAs per 128 rows; 205 -> 165 us), so that is
+// the only shape that takes it.  SEED_KX=1 forces it for every 3x3 conv,
+// SEED_KX=0 never (A/B measurement).
+template <int N, int RB>
+static bool kx_stacked() {
+  static const int env = [] {
+    const char* e = getenv("SEED_KX");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  return env >= 0 ? env == 1 : (RB == 64 && N == 16);
+}
+
 template <int MODE, int N, int RB, int NW>
 static seed_status fwd_t(const Conv3wFwd& a, cudaStream_t st) {
   WinConvArgs w{};
@@ -144,6 +185,10 @@ static seed_status fwd_t(const Conv3wFwd& a, cudaStream_t st) {
   W3FwdEpi<MODE, N> e{};
   e.g = a.g; e.in_scale = a.in_scale; e.bias = a.bias; e.res = a.res; e.out = a.out;
   e.outr = a.outr; e.dense = a.dense;
+  if (NW == 9 && kx_stacked<N, RB>()) {   // 3 row windows ky, column taps stacked on N
+    for (int k = 0; k < 3; ++k) w.off[k] = (k - 1) * a.g.Wp;
+    return launch_win_conv_kx<W3FwdEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
+  }
   for (int k = 0; k < NW; ++k)
     w.off[k] = NW == 9 ? ((k / 3) - 1) * a.g.Wp + (k % 3) - 1 : (k - 1) * a.g.Wp;
   return launch_win_conv<W3FwdEpi<MODE, N>, RB, NW, w3_mt<MODE, N, true>()>(w, e, st);
@@ -179,6 +224,10 @@ static seed_status dgrad_t(const Conv3wDgrad& a, cudaStream_t st) {
   // (win3_img_pos mode 1), so out[g] = D[g-1][grp 0] + D[g][grp 1] + D[g+1][grp 2]
   W3DgradEpi<MODE, N> e{};
   e.g = a.g; e.mask = a.mask; e.dres = a.dres; e.dX = a.dX;
+  if (kx_stacked<N, RB>()) {   // 3 row windows at -(ky-1)*Wp, column taps stacked on N
+    for (int k = 0; k < 3; ++k) w.off[k] = -(k - 1) * a.g.Wp;
+    return launch_win_conv_kx<W3DgradEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
+  }
   // 9 windows: tap (ky, kx) at -((ky-1)*Wp + kx-1), image row block ky*3 + 2 - kx
   for (int k = 0; k < 9; ++k) w.off[k] = -(((k / 3) - 1) * a.g.Wp + 1 - (k % 3));
   return launch_win_conv<W3DgradEpi<MODE, N>, RB, 9, w3_mt<MODE, N, false>()>(w, e, st);

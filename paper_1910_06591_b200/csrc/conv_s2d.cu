@@ -41,15 +41,20 @@ __device__ void Conv2S2dEpi::store(int64_t m, float (&v)[N]) const {
   }
 }
 
-__device__ void Conv2DgradS2dEpi::store(int64_t p, float (&v)[N]) const {
+__device__ void Conv2DgradS2dEpi::pre(int64_t p, uint4 (&pr)[PRE]) const {
+  const uint8_t* srow = S1 + p * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) pr[j] = __ldg(reinterpret_cast<const uint4*>(srow + (swz_chunk(p, 128, j) << 4)));
+}
+
+__device__ void Conv2DgradS2dEpi::store(int64_t p, float (&v)[N], const uint4 (&pr)[PRE]) const {
   uint32_t f, rem, Y, X;
   P2.divmod((uint32_t)p, f, rem);
   W2.divmod(rem, Y, X);
-  // ReLU mask of act1 (S1 row p, 64 channels = 4 conv1 pixels x 16)
-  const uint8_t* srow = S1 + p * 128;
+  // ReLU mask of act1 (S1 row p, 64 channels = 4 conv1 pixels x 16; prefetched)
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const uint4 u = *reinterpret_cast<const uint4*>(srow + (swz_chunk(p, 128, j) << 4));
+    const uint4 u = pr[j];
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {

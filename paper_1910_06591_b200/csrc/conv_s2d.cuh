@@ -63,12 +63,14 @@ struct Conv2S2dEpi {
 // padding rows of conv1 output space receive zeros
 struct Conv2DgradS2dEpi {
   static constexpr int N = 64;
+  static constexpr int PRE = 8;   // the S1 row (ReLU mask), prefetched by the engine
   const uint8_t* S1;
   uint8_t* dY1;
   FastDiv P2, W2;        // 100, 10
   int H2s, W2s;          // 10, 10
   int P1, W1s, H1s;      // 441, 21, 21 (conv1 output rows, padded numbering)
-  __device__ void store(int64_t m, float (&v)[N]) const;
+  __device__ void pre(int64_t m, uint4 (&p)[PRE]) const;
+  __device__ void store(int64_t m, float (&v)[N], const uint4 (&p)[PRE]) const;
 };
 
 struct WinWgradFinish {

@@ -21,6 +21,7 @@
 // (deterministic, C21).
 #pragma once
 #include <algorithm>
+#include <type_traits>
 #include "common.cuh"
 
 namespace seed {
@@ -95,9 +96,22 @@ __device__ __forceinline__ void load_slab(uint8_t* slab, const uint8_t* src, int
 
 // ------------------------------------------------------------------ forward / dgrad
 // Epi: static constexpr int N; __device__ void store(int64_t m, float (&v)[N]) const
+// An epilogue that reads other rows of global memory (residual input, ReLU mask)
+// declares static constexpr int PRE = uint4 chunks per output row and
+//   __device__ void pre(int64_t m, uint4 (&p)[PRE]) const   (issue the loads)
+//   __device__ void store(int64_t m, float (&v)[N], const uint4 (&p)[PRE]) const
+// The engine issues pre() for all of a tile's rows BEFORE waiting for the tile's
+// accumulator, so those loads are in flight during the MMAs instead of being
+// dependent loads inside the epilogue (measured: the residual / masked epilogues
+// were latency-bound on them, profiles/r02/ncu_c4_deep.md).
 // A tile is MT x 128 output rows: one slab of MT*128 + (max off - min off) rows, MT
 // accumulators of N columns (bigger tiles re-read fewer halo rows from L2 and pay
 // the per-tile barrier / commit latency once per MT blocks).
+template <class E, class = void>
+struct EpiPre { static constexpr int n = 0; };
+template <class E>
+struct EpiPre<E, std::void_t<decltype(E::PRE)>> { static constexpr int n = E::PRE; };
+
 template <class Epi, int RB, int NW, int MT = 1>
 __global__ void __launch_bounds__(WCF_THREADS, 1)
     win_conv_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes) {
@@ -184,6 +198,15 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       if ((it & 1) != grp) continue;
       const int acc = it % WCF_ACC;
+      constexpr int PN = EpiPre<Epi>::n > 0 ? EpiPre<Epi>::n : 1;
+      uint4 pre[MT][PN];
+      if constexpr (EpiPre<Epi>::n > 0) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int64_t m = t * TM + mt * 128 + q * 32 + lane;
+          if (m < a.M) e.pre(m, pre[mt]);
+        }
+      }
       mbar_wait(&tfull[acc], (it / WCF_ACC) & 1);
       tc_fence_after();
       uint32_t vr[MT][N];
@@ -203,7 +226,11 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < N; ++c) v[c] = __uint_as_float(vr[mt][c]);
         const int64_t m = t * TM + mt * 128 + q * 32 + lane;
-        if (m < a.M) e.store(m, v);
+        if constexpr (EpiPre<Epi>::n > 0) {
+          if (m < a.M) e.store(m, v, pre[mt]);
+        } else {
+          if (m < a.M) e.store(m, v);
+        }
       }
     }
   }
@@ -231,6 +258,216 @@ seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st)
     const int64_t tiles = (a.M + TM - 1) / TM;
   const int grid = (int)std::min<int64_t>(tiles, 148);
   return launch_k(win_conv_kernel<Epi, RB, NW, MT>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e,
+                  stages, slab);
+}
+
+// ------------------------------------------------------------------ column-tap-stacked 3x3
+// A 3x3 conv over the padded row space with the three column taps (kx) stacked on
+// N: one MMA per row window ky (N = 3*NO, K = RB/2 channels) computes
+//   D[g][j*NO + o] = sum_ky sum_k S[g + off_ky][k] * Wimg[ky][j*NO + o][k]
+// and the epilogue combines neighbouring rows:
+//   out[g][o] = D[g-1][0*NO + o] + D[g][1*NO + o] + D[g+1][2*NO + o]
+// (forward: j = kx, off_ky = (ky-1)*Wp; data gradient: j = 2-kx with the mode-1
+// image, off_ky = -(ky-1)*Wp — the same combination).  3 MMAs per 128 rows instead
+// of 9: the 16/32-channel convs were bound by the ~45-cycle floor of each small
+// tcgen05.mma (profiles/r01/mma_rate_probe.txt), not by HBM.
+// Tiles of TM = 128*MT MMA rows overlap by 2 rows: tile t computes rows
+// [t*TS - 1, t*TS - 1 + TM) and outputs [t*TS, t*TS + TS), TS = TM - 2, so every
+// output row's neighbours are in its own tile.  Inside a tile, rows g-1 / g+1 come
+// from the neighbouring lane (warp shuffle) or, at the 32-row warp-quarter edges,
+// through a shared-memory exchange (one named barrier per tile and group).
+constexpr int WKX_ACC = 2;   // one TMEM accumulator per epilogue group
+
+template <class Epi, int RB, int MT>
+__global__ void __launch_bounds__(WCF_THREADS, 1)
+    win_conv_kx_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes) {
+  constexpr int NO = Epi::N;          // output channels
+  constexpr int N = 3 * NO;           // MMA N: kx-stacked
+  constexpr int TM = 128 * MT, TS = TM - 2;
+  constexpr uint32_t LAYOUT = swz_layout_code(RB);
+  constexpr int WB = 3 * N * RB;
+  constexpr int AC = MT * N;          // TMEM columns per tile accumulator
+  constexpr uint32_t TCOLS = WKX_ACC * AC <= 128 ? 128 : WKX_ACC * AC <= 256 ? 256 : 512;
+  static_assert(WKX_ACC * AC <= 512, "TMEM");
+  static_assert(NO % 16 == 0, "NO");
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* Ws = sm;
+  uint8_t* slabs = sm + ((WB + 1023) & ~1023);
+  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[WKX_ACC], tempty[WKX_ACC], wbar;
+  __shared__ uint32_t tbase;
+  // edge exchange per group: [MT*4 quarters][0: last row's part 0 | 1: first row's part 2][NO]
+  __shared__ __align__(16) float xch[2][MT * 4][2][NO];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mn = min(a.off[0], min(a.off[1], a.off[2]));
+  const int mx = max(a.off[0], max(a.off[1], a.off[2]));
+  const int nrows = TM + mx - mn;
+  const int64_t tiles = (a.M + TS - 1) / TS;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int i = 0; i < WKX_ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    mbar_init(&wbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&tbase, TCOLS);
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(&wbar, WB);
+    bulk_g2s(smem_u32(Ws), a.wimg, WB, &wbar);
+  }
+  pdl_wait();
+  const uint32_t tmem = tbase;
+  if (warp == 0) {
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int s = it % stages;
+      mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+      load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, t * TS - 1 + mn, nrows, a.src_rows,
+                &full[s], lane, 0);
+    }
+  } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
+    mbar_wait(&wbar, 0);
+    const uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+    const uint64_t bd0 = umma_desc(smem_u32(Ws), 16, 8 * RB, LAYOUT);
+    int aoff[3];
+#pragma unroll
+    for (int w = 0; w < 3; ++w) aoff[w] = ((a.off[w] - mn) * RB) >> 4;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int s = it % stages, acc = it % WKX_ACC;
+      mbar_wait(&full[s], (it / stages) & 1);
+      mbar_wait(&tempty[acc], ((it / WKX_ACC) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t base = smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * TS - 1 + mn, RB);
+      const uint64_t ad0 = umma_desc(base, 16, 8 * RB, LAYOUT);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int w = 0; w < 3; ++w)
+#pragma unroll
+          for (int ks = 0; ks < RB / 32; ++ks)
+            tc_mma_bf16_w(tmem + acc * AC + mt * N,
+                          ad0 + (uint64_t)(aoff[w] + ((mt * 128 * RB) >> 4) + ks * 2),
+                          bd0 + (uint64_t)((w * N * RB + ks * 32) >> 4), idesc, (w | ks) != 0);
+      tc_commit_w(&empty[s]);
+      tc_commit_w(&tfull[acc]);
+    }
+  } else {
+    const int q = warp & 3;            // TMEM lanes [32q, 32q+32) of this warp
+    const int grp = (warp - 2) >> 2;   // epilogue group: tiles it with it % 2 == grp
+    constexpr int PN = EpiPre<Epi>::n > 0 ? EpiPre<Epi>::n : 1;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      if ((it & 1) != grp) continue;
+      const int acc = it % WKX_ACC;
+      const int64_t g0 = t * TS - 1;   // global row of MMA row 0
+      uint4 pre[MT][PN];
+      if constexpr (EpiPre<Epi>::n > 0) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = mt * 128 + q * 32 + lane;
+          const int64_t m = g0 + r;
+          if (r >= 1 && r <= TM - 2 && m < a.M) e.pre(m, pre[mt]);
+        }
+      }
+      mbar_wait(&tfull[acc], (it / WKX_ACC) & 1);
+      tc_fence_after();
+      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + acc * AC;
+      // pass 1: the quarter-edge rows' parts for the neighbouring quarters
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+        for (int c = 0; c < NO / 16; ++c) {
+          uint32_t p0[16], p2[16];
+          tmem_ld16_nw(tb + mt * N + c * 16, p0);
+          tmem_ld16_nw(tb + mt * N + 2 * NO + c * 16, p2);
+          tmem_wait_ld();
+          if (lane == 31 || lane == 0) {
+            const uint32_t* src = lane == 31 ? p0 : p2;
+            float4* dst = reinterpret_cast<float4*>(&xch[grp][mt * 4 + q][lane == 31 ? 0 : 1][c * 16]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              dst[k] = make_float4(__uint_as_float(src[4 * k]), __uint_as_float(src[4 * k + 1]),
+                                   __uint_as_float(src[4 * k + 2]), __uint_as_float(src[4 * k + 3]));
+          }
+        }
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+      // pass 2: combine and store.  Branch-free: every lane issues the shuffles and
+      // the (broadcast) exchange reads; lanes 0 / 31 select the exchanged values.
+      // (unrolled: the prefetched rows pre[mt] stay in registers)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int r = mt * 128 + q * 32 + lane;
+        const int slot = mt * 4 + q;
+        const int su = slot > 0 ? slot - 1 : 0, sd = slot < MT * 4 - 1 ? slot + 1 : slot;
+        float v[NO];
+#pragma unroll
+        for (int c = 0; c < NO / 16; ++c) {
+          uint32_t p0[16], p1[16], p2[16];
+          tmem_ld16_nw(tb + mt * N + c * 16, p0);
+          tmem_ld16_nw(tb + mt * N + NO + c * 16, p1);
+          tmem_ld16_nw(tb + mt * N + 2 * NO + c * 16, p2);
+          float eu[16], ed[16];
+          const float4* xu = reinterpret_cast<const float4*>(&xch[grp][su][0][c * 16]);
+          const float4* xd = reinterpret_cast<const float4*>(&xch[grp][sd][1][c * 16]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 a4 = xu[k], b4 = xd[k];
+            eu[4 * k] = a4.x; eu[4 * k + 1] = a4.y; eu[4 * k + 2] = a4.z; eu[4 * k + 3] = a4.w;
+            ed[4 * k] = b4.x; ed[4 * k + 1] = b4.y; ed[4 * k + 2] = b4.z; ed[4 * k + 3] = b4.w;
+          }
+          tmem_wait_ld();
+          float up[16], dn[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            up[k] = __shfl_up_sync(0xffffffffu, __uint_as_float(p0[k]), 1);     // D[r-1] part 0
+            dn[k] = __shfl_down_sync(0xffffffffu, __uint_as_float(p2[k]), 1);   // D[r+1] part 2
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            v[c * 16 + k] = (lane == 0 ? eu[k] : up[k]) + __uint_as_float(p1[k]) +
+                            (lane == 31 ? ed[k] : dn[k]);
+        }
+        const int64_t m = g0 + r;
+        if (r >= 1 && r <= TM - 2 && m < a.M) {
+          if constexpr (EpiPre<Epi>::n > 0) e.store(m, v, pre[mt]);
+          else e.store(m, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      // the exchange buffer is rewritten by this group's next tile only after all
+      // four warps have read it
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TCOLS);
+  }
+}
+
+template <class Epi, int RB, int MT>
+seed_status launch_win_conv_kx(const WinConvArgs& a, const Epi& e, cudaStream_t st) {
+  constexpr int WB = 3 * 3 * Epi::N * RB;
+  constexpr int TM = 128 * MT, TS = TM - 2;
+  const int mn = std::min(a.off[0], std::min(a.off[1], a.off[2]));
+  const int mx = std::max(a.off[0], std::max(a.off[1], a.off[2]));
+  const int slab = (int)align_up((size_t)(TM + mx - mn) * RB + 1024, 1024);
+  const int wbytes = (int)align_up(WB, 1024);
+  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - wbytes) / slab);
+  if (a.M <= 0) return a.M == 0 ? SEED_OK : SEED_E_SHAPE;
+  if (stages < 2) return SEED_E_SHAPE;
+  const size_t smem = (size_t)wbytes + (size_t)stages * slab + 1024;
+  static PerDevice attr;
+  SEED_TRY(smem_optin(attr, win_conv_kx_kernel<Epi, RB, MT>, WC_SMEM_BUDGET + 2048));
+  const int64_t tiles = (a.M + TS - 1) / TS;
+  const int grid = (int)std::min<int64_t>(tiles, sm_count());
+  return launch_k(win_conv_kx_kernel<Epi, RB, MT>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e,
                   stages, slab);
 }
 

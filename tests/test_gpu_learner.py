@@ -63,11 +63,12 @@ def exact_bound_check(gpu, exact, emu, what="", floor=2e-2, factor=1.25):
 def _spec_pair(cfg):
     S = _S()
     spec = S.spec_for_config(cfg)
-    ospec = {"c1": O.spec_c1, "c2": O.spec_c2, "c3": O.spec_c3, "c4": O.spec_c4}[cfg]()
+    ospec = {"c1": O.spec_c1, "c2": O.spec_c2, "c3": O.spec_c3, "c4": O.spec_c4,
+             "c4m": O.spec_c4_medium, "c4l": O.spec_c4_large}[cfg]()
     return spec, ospec
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c4m", "c4l"])
 def test_param_layout_matches_oracle(cfg):
     S = _S()
     spec, ospec = _spec_pair(cfg)
@@ -249,7 +250,8 @@ def _padded_rows(L, name, shape):
     return v[:, 1:-1, 1:-1, :]
 
 
-@pytest.mark.parametrize("cfg,B,T", [("c3", 2, 3), ("c4", 2, 2), ("c3", 3, 1)])
+@pytest.mark.parametrize("cfg,B,T", [("c3", 2, 3), ("c4", 2, 2), ("c3", 3, 1), ("c4m", 2, 2),
+                                     ("c4l", 1, 2)])
 def test_learner_deep_parity(cfg, B, T):
     """configs[2] (DMLab IMPALA-deep, 72x96x3) / configs[3] (GRF SMM 72x96x16), full
     image size: 3x3 'same' convs, max-pool, residual blocks (C14).
@@ -267,7 +269,7 @@ def test_learner_deep_parity(cfg, B, T):
     spec, ospec = _spec_pair(cfg)
     params = seedgen.glorot_params(O.param_layout(ospec), seed=21, bias_std=0.1)
     batch = seedgen.learner_batch((ospec.obs_h, ospec.obs_w, ospec.obs_c), ospec.num_actions, B,
-                                  T, seed=22, done_p=0.2, smm=(cfg == "c4"))
+                                  T, seed=22, done_p=0.2, smm=cfg.startswith("c4"))
     hp = S.HParams(lam=0.95, loss_scale=1.0 / (B * T), lr=1e-3)
     g = _run_gpu(S, spec, params, batch, hp, B, T)
     L = g["L"]
@@ -399,7 +401,7 @@ def _deep_exact_checks(cfg, g, gt, ex, rt, exact, ref):
     assert not bad, bad
 
 
-@pytest.mark.parametrize("cfg,B,T", [("c3", 32, 100), ("c4", 128, 32)])
+@pytest.mark.parametrize("cfg,B,T", [("c3", 32, 100), ("c4", 128, 32), ("c4l", 128, 32)])
 def test_learner_deep_full_size_sampled(cfg, B, T):
     """BASELINE.json configs[2] / configs[3] at their full sizes (the shapes bench.py
     times: F = 3232 / 4224 frames, 23-31 M padded rows at 72x96): one learner step,
@@ -410,7 +412,7 @@ def test_learner_deep_full_size_sampled(cfg, B, T):
     spec, ospec = _spec_pair(cfg)
     params = seedgen.glorot_params(O.param_layout(ospec), seed=31, bias_std=0.1)
     batch = seedgen.learner_batch((ospec.obs_h, ospec.obs_w, ospec.obs_c), ospec.num_actions, B,
-                                  T, seed=32, smm=(cfg == "c4"))
+                                  T, seed=32, smm=cfg.startswith("c4"))
     hp = S.HParams(lam=0.95, loss_scale=1.0 / (B * T), lr=1e-4)
     L = S.Learner(spec, T, B, params, hp)
     m = L.step(_gpu_batch(batch))
