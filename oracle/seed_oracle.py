@@ -718,3 +718,105 @@ def philox_uniforms(seed, counter, actor_ids):
     x = philox4x32_10([counter & 0xFFFFFFFF, counter >> 32, ids, 0],
                       [seed & 0xFFFFFFFF, seed >> 32])
     return (x[0] >> 8).astype(np.float64) * (1.0 / 16777216.0)
+
+
+# --------------------------------------------------------------------------
+# R2D2 on SEED (hyper-parameters table
+# `r2d2_params` P:586-622; SPEC qlearn S:187-245 and replay S:287-333).
+# --------------------------------------------------------------------------
+def value_rescale(x, eps=1e-3):
+    """h(x) = sign(x)(sqrt(|x| + 1) - 1) + eps x (value function rescaling)."""
+    x = np.asarray(x, np.float64)
+    return np.sign(x) * (np.sqrt(np.abs(x) + 1.0) - 1.0) + eps * x
+
+
+def value_rescale_inv(y, eps=1e-3):
+    """h^-1(y) = sign(y)(((sqrt(1 + 4 eps (|y| + 1 + eps)) - 1) / (2 eps))^2 - 1) (S:204,
+    the closed-form inverse of P:611's h)."""
+    y = np.asarray(y, np.float64)
+    return np.sign(y) * (((np.sqrt(1.0 + 4.0 * eps * (np.abs(y) + 1.0 + eps)) - 1.0) /
+                          (2.0 * eps)) ** 2 - 1.0)
+
+
+def r2d2_targets(q_online, q_target, actions, rewards, discounts, n=5, eta=0.9, eps=1e-3):
+    """n-step double-Q targets with value rescaling and sequence priorities
+    (P:149 double Q-learning, multi-step targets, value rescaling; P:613 n = 5;
+    P:615 p = eta max_i delta_i + (1 - eta) mean delta).
+
+    q_online, q_target: [B][T+1][A] rescaled action values of the online / target
+    network at the T+1 observations of the trained part (after burn-in);
+    actions [B][T+1] (a_t taken at observation t), rewards [B][T] (r_t received
+    after a_t), discounts [B][T] (gamma_t = gamma (1 - done_{t+1}), the V-trace
+    convention C5).  For t = 0..T-1, with m = min(n, T - t) (reading C32: the
+    sequence end shortens the window; an episode end inside it zeroes the rest
+    through gamma_t = 0):
+      a* = argmax_a q_online[t+m][a]            (double Q: online selects, first max)
+      G  = sum_{k<m} (prod_{j<k} gamma_{t+j}) r_{t+k}
+           + (prod_{j<m} gamma_{t+j}) h^-1(q_target[t+m][a*])
+      y_t = h(G);  delta_t = y_t - q_online[t][a_t]
+    priority_b = eta max_t |delta_t| + (1 - eta) mean_t |delta_t|.
+    Returns (y [B][T], delta [B][T], priority [B])."""
+    qo = np.asarray(q_online, np.float64)
+    qt = np.asarray(q_target, np.float64)
+    a = np.asarray(actions).astype(np.int64)
+    r = np.asarray(rewards, np.float64)
+    g = np.asarray(discounts, np.float64)
+    B, T = r.shape
+    y = np.zeros((B, T))
+    for b in range(B):
+        for t in range(T):
+            m = min(n, T - t)
+            G, disc = 0.0, 1.0
+            for k in range(m):
+                G += disc * r[b, t + k]
+                disc *= g[b, t + k]
+            astar = int(np.argmax(qo[b, t + m]))
+            G += disc * value_rescale_inv(qt[b, t + m, astar], eps)
+            y[b, t] = value_rescale(G, eps)
+    q_taken = np.take_along_axis(qo[:, :T], a[:, :T, None], axis=2)[:, :, 0]
+    delta = y - q_taken
+    ad = np.abs(delta)
+    prio = eta * ad.max(axis=1) + (1.0 - eta) * ad.mean(axis=1)
+    return y, delta, prio
+
+
+def r2d2_loss_grad(q_online, actions, y, is_weights, scale):
+    """L = scale sum_b w_b sum_t 1/2 (q_online[t][a_t] - y_t)^2 with y a constant
+    (importance-weighted squared TD error); dL/dq_online is nonzero only at
+    a_t: scale w_b (q - y).  Returns (loss, dq [B][T+1][A], row T zero)."""
+    qo = np.asarray(q_online, np.float64)
+    a = np.asarray(actions).astype(np.int64)
+    B, T1, A = qo.shape
+    T = T1 - 1
+    w = np.asarray(is_weights, np.float64)
+    dq = np.zeros_like(qo)
+    loss = 0.0
+    for b in range(B):
+        for t in range(T):
+            d = qo[b, t, a[b, t]] - y[b, t]
+            loss += scale * w[b] * 0.5 * d * d
+            dq[b, t, a[b, t]] = scale * w[b] * d
+    return loss, dq
+
+
+def replay_probabilities(priorities, alpha=0.9):
+    """P(i) = p_i^alpha / sum_j p_j^alpha (P:602 priority exponent)."""
+    p = np.asarray(priorities, np.float64) ** alpha
+    return p / p.sum()
+
+
+def replay_sample(priorities, uniforms, alpha=0.9, beta=0.6, size=None):
+    """Proportional prioritized sampling by inverse CDF (the sum-tree's definition):
+    draw i = min{ i : u * sum_j p_j^alpha < sum_{j<=i} p_j^alpha } for each uniform
+    u in [0, 1); importance weights w_i = (N P(i))^-beta / max_batch w (P:603
+    exponent 0.6; S:313, S:325 normalisation by the batch max), N = number of
+    stored sequences (`size`, default len(priorities))."""
+    pa = np.asarray(priorities, np.float64) ** alpha
+    c = np.cumsum(pa)
+    u = np.asarray(uniforms, np.float64)
+    idx = np.searchsorted(c, u * c[-1], side="right")
+    idx = np.minimum(idx, len(pa) - 1)
+    N = len(pa) if size is None else size
+    P = pa[idx] / c[-1]
+    w = (N * P) ** (-beta)
+    return idx, w / w.max()

@@ -17,10 +17,13 @@ out = sys.argv[1]
 world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
 dist.init_process_group("gloo")
-T, B = 5, 4
-spec = S.spec_for_config("c2")
-params = seedgen.glorot_params(O.param_layout(O.spec_c2()), seed=2, bias_std=0.1)
-shards = [seedgen.learner_batch((84, 84, 4), 18, B, T, seed=60 + r, done_p=0.1) for r in range(world)]
+cfg = os.environ.get("CFG", "c2")
+T, B = (5, 4) if cfg == "c2" else (4, 2)
+spec = S.spec_for_config(cfg)
+ospec = {"c2": O.spec_c2, "c3": O.spec_c3, "c4": O.spec_c4}[cfg]()
+params = seedgen.glorot_params(O.param_layout(ospec), seed=2, bias_std=0.1)
+shards = [seedgen.learner_batch(spec.obs_shape, spec.num_actions, B, T, seed=60 + r, done_p=0.1,
+                                smm=(cfg == "c4")) for r in range(world)]
 hp = S.HParams(lam=0.95, loss_scale=1.0 / (world * B * T), lr=1e-3)
 comm = S.Comm(rank, world)
 L = S.Learner(spec, T, B, params, hp, comm=comm)

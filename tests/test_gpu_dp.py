@@ -15,14 +15,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs 2 GPUs")
-@pytest.mark.parametrize("peer", ["0", "1"])
-def test_dp_two_ranks(tmp_path, peer):
-    """peer=1: the NVLink peer-memory allreduce (seed_comm_peer_*) instead of NCCL."""
+@pytest.mark.parametrize("cfg,peer", [("c2", "0"), ("c2", "1"), ("c4", "0")])
+def test_dp_two_ranks(tmp_path, cfg, peer):
+    """peer=1: the NVLink peer-memory allreduce (seed_comm_peer_*) instead of NCCL;
+    c4 = the GRF deep net (BASELINE.json configs[3], the config it scales 1/2/4/8)."""
     n = 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "2953" + peer,
+           "--master-addr", "127.0.0.1", "--master-port", str(29530 + int(peer) + (10 if cfg == "c4" else 0)),
            os.path.join(ROOT, "scripts", "dp_check.py"), str(tmp_path)]
-    subprocess.run(cmd, check=True, timeout=600, env=dict(os.environ, SEED_PEER=peer))
+    subprocess.run(cmd, check=True, timeout=600, env=dict(os.environ, SEED_PEER=peer, CFG=cfg))
     g = [np.load(tmp_path / f"grads{r}.npy") for r in range(n)]
     p = [np.load(tmp_path / f"params{r}.npy") for r in range(n)]
     for r in range(1, n):
