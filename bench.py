@@ -351,6 +351,60 @@ def vtrace_leg(S, torch, T=100, B=1 << 17, iters=20):
             "working_set": "367.5 MB > 126 MB L2 (20 back-to-back calls in one graph)"}
 
 
+# ---------------------------------------------------------------- R2D2 leg
+def r2d2_leg(S, torch, iters=20):
+    """seed_r2d2_targets at the paper's trained-sequence shape (80 steps after the
+    40-step burn-in of 120; 18 actions; n = 5) over B = 2^14 sequences
+    (> L2), as HBM GB/s of its compulsory traffic; and the replay at the paper's
+    10^5 sequences: one training iteration's sample (B = 64) +
+    priority update (+ tree rebuilds), device time per iteration."""
+    B, T, A = 1 << 14, 80, 18
+    g = torch.Generator(device="cuda").manual_seed(0)
+    qo = torch.randn(B, T + 1, A, device="cuda", generator=g)
+    qt = torch.randn(B, T + 1, A, device="cuda", generator=g)
+    a = torch.randint(0, A, (B, T + 1), device="cuda", dtype=torch.int32, generator=g)
+    r = torch.randn(B, T, device="cuda", generator=g)
+    disc = torch.full((B, T), 0.997, device="cuda")
+    w = torch.rand(B, device="cuda", generator=g)
+    call = lambda: S.r2d2_targets(qo, qt, a, r, disc, n=5, is_weights=w, want_grad=True)
+    for _ in range(3):
+        call()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / iters
+    # compulsory bytes: q_online read + q_target rows read (~1/A of it: one value per
+    # step, but whole rows for the argmax are q_online's) + actions, rewards,
+    # discounts, weights read; y, delta, priority, loss written; dq written
+    nbytes = 4 * (B * (T + 1) * A + B * (T + 1) + 2 * B * T + B + B * (T + 1) * A +
+                  2 * B * T + 2 * B) + 4 * B * T
+    out = {"targets": {"B": B, "T": T, "A": A, "n": 5, "us": round(us, 2),
+                       "GBs": round(nbytes / us / 1e3, 1), "bytes": nbytes}}
+    N, Bs = 100000, 64
+    R = S.PrioritizedReplay(N, 16)
+    recs = torch.zeros(1024, 16, dtype=torch.uint8, device="cuda")
+    for k in range(0, N, 1024):
+        R.insert(recs[:min(1024, N - k)])
+    torch.cuda.synchronize()
+    pr = torch.rand(Bs, device="cuda", generator=g)
+    e0.record()
+    for i in range(iters):
+        sl, gn, ww = R.sample(Bs, seed=1, counter=i)
+        R.update(sl, gn, pr)
+    e1.record()
+    torch.cuda.synchronize()
+    out["replay"] = {"sequences": N, "tree_leaves": R.capacity, "batch": Bs,
+                     "us_per_sample_and_update": round(e0.elapsed_time(e1) * 1e3 / iters, 2),
+                     "launches_per_iteration": 3}
+    del R, qo, qt
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- inference leg (c5)
 def inference_leg(S, torch, world, rank, dist, iters=20):
     """configs[4]: 4096 actors per GPU, per-actor LSTM state table, Atari net; one
@@ -501,10 +555,15 @@ def measure_learner(S, torch, dist, cfg, steps, warmup, world, rank, local, comm
     with torch.cuda.graph(plain, stream=s):
         L.step(dev, stream=s)
     torch.cuda.synchronize()
+    # warm replays (first replays of a graph with NCCL inside carry one-time setup);
+    # every rank replays the same count, in step
     for _ in range(2):
-        plain.replay()
         tgraph.replay()
+    for _ in range(max(warmup, 3)):
+        plain.replay()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     # ---- timed region: K replays of the plain step graph, L2 flushed between
     K = steps
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
@@ -528,7 +587,11 @@ def measure_learner(S, torch, dist, cfg, steps, warmup, world, rank, local, comm
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(e0, e1)]
     total = torch.tensor([sum(step_ms)], dtype=torch.float64)
+    per_rank = [sum(step_ms) / K]
     if world > 1:
+        allr = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allr, total)
+        per_rank = [float(x.item()) / K for x in allr]
         dist.all_reduce(total, op=dist.ReduceOp.MAX)
     ms_per_step = float(total.item()) / K
     # ---- per-launch breakdown from the traced graph (event node after every launch group)
@@ -561,7 +624,8 @@ def measure_learner(S, torch, dist, cfg, steps, warmup, world, rank, local, comm
            "gpu_launches_per_step": launches, "kernels": kernels,
            "traced_ms_per_step": sum(per[1:]),
            "clocks": clk.summary() if clk else None,
-           "step_ms_p10_p50_p90": [round(float(np.percentile(step_ms, q)), 4) for q in (10, 50, 90)]}
+           "step_ms_p10_p50_p90": [round(float(np.percentile(step_ms, q)), 4) for q in (10, 50, 90)],
+           "ms_per_step_per_rank": [round(x, 4) for x in per_rank]}
     out["roofline"] = roofline_of(kernels, cfg)
     if e2e:
         out["e2e"] = e2e_leg(torch, dist, L, dev, pinned, steps, world, frames)
@@ -680,6 +744,7 @@ def run_ours(args):
                           "roofline": r["roofline"],
                           "top_kernels": sorted(r["kernels"], key=lambda x: -x["us"])[:8]}
         inf = inference_leg(S, torch, world, rank, dist)
+        r2 = r2d2_leg(S, torch) if rank == 0 else None
     c = CONFIGS[HEAD]
     if rank == 0:
         vt = vtrace_leg(S, torch)
@@ -699,6 +764,7 @@ def run_ours(args):
             "env_steps_per_s": round(head["env_steps_per_s"], 1),
             "gpu_launches": head["gpu_launches_per_step"] * args.steps,
             "step_ms_p10_p50_p90": head["step_ms_p10_p50_p90"],
+            "ms_per_step_per_rank": head["ms_per_step_per_rank"],
             "traced_ms_per_step": round(head["traced_ms_per_step"], 4),
             "roofline": head["roofline"],
             "e2e": head["e2e"],
@@ -710,6 +776,7 @@ def run_ours(args):
         if not args.no_extra:
             line["other_configs"] = extra
             line["inference"] = inf
+            line["r2d2"] = r2
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(HEAD)
         print(json.dumps(line), flush=True)

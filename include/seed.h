@@ -379,6 +379,84 @@ seed_status seed_param_acquire(const seed_net_spec* spec, seed_param_snapshot* s
                                int force_copy, void* stream);
 
 /* ===========================================================================
+ * R2D2 on SEED ("fully implementing R2D2",
+ * hyper-parameters P:586-622).
+ *
+ * seed_r2d2_targets — n-step double-Q targets with value rescaling (P:149, P:611,
+ * P:613), TD errors, sequence priorities and the importance-weighted
+ * squared-TD loss gradient, one warp per sequence:
+ *   h(x) = sign(x)(sqrt(|x|+1) - 1) + eps x,  h^-1 its closed-form inverse
+ *   for t < T, m = min(n, T - t):  a* = argmax_a q_online[t+m][a] (first maximum)
+ *     G_t = sum_{k<m} (prod_{j<k} gamma_{t+j}) r_{t+k}
+ *           + (prod_{j<m} gamma_{t+j}) h^-1(q_target[t+m][a*])
+ *     y_t = h(G_t);  delta_t = y_t - q_online[t][a_t]
+ *   priority_b = eta max_t |delta_t| + (1 - eta) mean_t |delta_t|
+ *   loss_part_b = loss_scale w_b sum_t delta_t^2 / 2;
+ *   dq[b][t][a_t] = loss_scale w_b (q_online[t][a_t] - y_t), 0 elsewhere, row T zero.
+ * Arguments: q_online, q_target [B][T+1][A] fp32 (rescaled values of the trained
+ *   part, after burn-in); actions [B][T+1] int32; rewards, discounts [B][T]
+ *   (gamma_t = gamma (1 - done_{t+1}), C5 — an episode end zeroes the rest of the
+ *   window, the sequence end shortens it: reading C32); is_weights nullable [B]
+ *   (1 if NULL); dq, loss_part nullable.  T, B >= 1, 2 <= A <= 4096, n >= 1 else
+ *   SEED_E_SHAPE; eps > 0, 0 <= eta <= 1 else SEED_E_ARG.
+ * ======================================================================== */
+seed_status seed_r2d2_targets(int T, int B, int A, int n, const float* q_online,
+                              const float* q_target, const int32_t* actions,
+                              const float* rewards, const float* discounts, float eta,
+                              float rescale_eps, const float* is_weights, float loss_scale,
+                              float* y, float* delta, float* priority, float* dq,
+                              float* loss_part, void* stream);
+
+/* Learner-resident prioritized sequence replay ("keep the replay buffer on
+ * the learner"; priority exponent alpha P:602, importance exponent beta P:603;
+ * S:287-333), entirely in HBM: a sum tree over p_i^alpha (leaves tree[C + i],
+ * root tree[1]; rebuilt in fixed pairwise order after every change — exact per
+ * level, deterministic), FIFO slots, and per-slot generations so that priority
+ * updates for a sequence evicted since its sample are skipped.  All fields are
+ * caller-owned device memory, zero-initialised before first use. */
+typedef struct {
+  int capacity;            /* sum-tree leaves C: power of two >= slots, C/2048 <= 2048 */
+  int slots;               /* sequences held (FIFO ring)                               */
+  float* tree;             /* device fp32 [2*C]                                        */
+  float* max_priority;     /* device fp32 [1]: max priority seen (new sequences')     */
+  int32_t* size;           /* device int32 [4]: {stored, next slot, rejected
+                              priorities (negative / non-finite), 0}                  */
+  int32_t* gen;            /* device int32 [slots]: generation of each slot           */
+  unsigned* ticket;        /* device uint32 [1]                                       */
+} seed_replay;
+/* SEED_OK if the descriptor is well-formed (host check only). */
+seed_status seed_replay_check(const seed_replay* replay);
+/* n (<= 1024) new sequences take the next FIFO slots (evicting the oldest) at the
+ * max priority seen so far (1 before any update); out_slots / out_gens (nullable
+ * device [n]) receive their slots and generations — the caller then writes the
+ * sequence payload into those slots. */
+seed_status seed_replay_insert(const seed_replay* replay, int n, float alpha,
+                               int32_t* out_slots, int32_t* out_gens, void* stream);
+/* New raw priorities p (>= 0, finite) for n (<= 1024) sampled sequences; an entry
+ * whose generation differs from the slot's current one (gens non-NULL) is skipped;
+ * invalid priorities are skipped and counted in size[2]; the max priority is
+ * raised to the largest applied p. */
+seed_status seed_replay_update(const seed_replay* replay, int n, const int32_t* slots,
+                               const int32_t* gens, const float* priorities, float alpha,
+                               void* stream);
+/* B (<= 1024) i.i.d. proportional draws: x = u * root, descend the tree (left if
+ * x < left sum, else subtract it and go right); u from `uniforms` (nullable [B]) or
+ * Philox4x32-10 keyed (seed) with counter (counter, draw index, 1);
+ * out_weights[b] = (N P(slot))^-beta / max over the batch, N = stored sequences.
+ * Requires at least one positive priority (stored > 0). */
+seed_status seed_replay_sample(const seed_replay* replay, int B, float beta,
+                               const float* uniforms, uint64_t seed, uint64_t counter,
+                               int32_t* out_slots, int32_t* out_gens, float* out_weights,
+                               void* stream);
+/* dst[b] = src[slots[b]] for slot_bytes-sized records (multiple of 16, 16-B aligned
+ * pointers): the sampled sequences' payload into a contiguous training batch. */
+seed_status seed_replay_gather(const void* src, size_t slot_bytes, const int32_t* slots, int B,
+                               void* dst, void* stream);
+/* The inverse: dst[slots[b]] = src[b] (the payload of sequences just inserted). */
+seed_status seed_replay_scatter(const void* src, size_t slot_bytes, const int32_t* slots, int B,
+                                void* dst, void* stream);
+
+/* ===========================================================================
  * Test / benchmark hooks (not part of the method):
  * seed_debug_gemm: D[M][N] (fp32, row-major) = A . B^T with A [M][K], B [N][K]
  * bf16 row-major (a_t / b_t != 0: A given as [K][M] / B as [K][N]), on the

@@ -46,6 +46,11 @@ class UnrollStore(C.Structure):
                                                     ("ready_gen", c_void_p)]
 
 
+class Replay(C.Structure):
+    _fields_ = [("capacity", c_int), ("slots", c_int)] + \
+        [(n, c_void_p) for n in ("tree", "max_priority", "size", "gen", "ticket")]
+
+
 class ParamSnapshot(C.Structure):
     _fields_ = [("slots", c_void_p * 3), ("state", c_void_p), ("version", c_void_p)]
 
@@ -75,6 +80,16 @@ _SIGS = {
     "seed_param_publish": (c_int, [P(NetSpec), P(TrainState), P(ParamSnapshot), c_void_p]),
     "seed_param_acquire": (c_int, [P(NetSpec), P(ParamSnapshot), c_void_p, c_void_p, c_void_p,
                                    c_int, c_void_p]),
+    "seed_r2d2_targets": (c_int, [c_int, c_int, c_int, c_int] + [c_void_p] * 5 +
+                          [c_float, c_float, c_void_p, c_float] + [c_void_p] * 6),
+    "seed_replay_check": (c_int, [P(Replay)]),
+    "seed_replay_insert": (c_int, [P(Replay), c_int, c_float, c_void_p, c_void_p, c_void_p]),
+    "seed_replay_update": (c_int, [P(Replay), c_int, c_void_p, c_void_p, c_void_p, c_float,
+                                   c_void_p]),
+    "seed_replay_sample": (c_int, [P(Replay), c_int, c_float, c_void_p, c_uint64, c_uint64,
+                                   c_void_p, c_void_p, c_void_p, c_void_p]),
+    "seed_replay_gather": (c_int, [c_void_p, c_size_t, c_void_p, c_int, c_void_p, c_void_p]),
+    "seed_replay_scatter": (c_int, [c_void_p, c_size_t, c_void_p, c_int, c_void_p, c_void_p]),
     "seed_learner_step_traced": (c_int, [P(NetSpec), c_int, c_int, P(Batch), P(TrainState),
                                          P(HParams), c_void_p, c_void_p, c_size_t, c_void_p,
                                          c_void_p, P(c_void_p), c_int, P(C.c_char_p), P(c_int),

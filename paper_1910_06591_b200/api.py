@@ -57,6 +57,99 @@ def vtrace(behaviour_logp, target_logp, rewards, discounts, values, bootstrap, r
     return vs, pg_advantages
 
 
+# --------------------------------------------------------------------------- R2D2
+def r2d2_targets(q_online, q_target, actions, rewards, discounts, n=5, eta=0.9, rescale_eps=1e-3,
+                 is_weights=None, loss_scale=1.0, want_grad=False, stream=None):
+    """seed_r2d2_targets: q_online / q_target [B][T+1][A], actions [B][T+1] int32,
+    rewards / discounts [B][T] -> (y, delta [B][T], priority [B], dq or None,
+    loss_part or None)."""
+    B, T1, A = q_online.shape
+    T = T1 - 1
+    _need(q_online, torch.float32, "q_online")
+    _need(q_target, torch.float32, "q_target")
+    _need(actions, torch.int32, "actions")
+    _need(rewards, torch.float32, "rewards")
+    _need(discounts, torch.float32, "discounts")
+    if tuple(q_target.shape) != (B, T1, A) or tuple(actions.shape) != (B, T1) or \
+            tuple(rewards.shape) != (B, T) or tuple(discounts.shape) != (B, T):
+        raise ValueError("r2d2_targets: shapes")
+    dev = q_online.device
+    y = torch.empty(B, T, device=dev)
+    delta = torch.empty(B, T, device=dev)
+    prio = torch.empty(B, device=dev)
+    dq = torch.empty(B, T1, A, device=dev) if want_grad else None
+    loss = torch.empty(B, device=dev) if want_grad else None
+    if is_weights is not None:
+        _need(is_weights, torch.float32, "is_weights")
+    L.check(L.load().seed_r2d2_targets(T, B, A, int(n), _ptr(q_online), _ptr(q_target),
+                                       _ptr(actions), _ptr(rewards), _ptr(discounts), float(eta),
+                                       float(rescale_eps), _ptr(is_weights), float(loss_scale),
+                                       _ptr(y), _ptr(delta), _ptr(prio), _ptr(dq), _ptr(loss),
+                                       _stream(stream)), "seed_r2d2_targets")
+    return y, delta, prio, dq, loss
+
+
+class PrioritizedReplay:
+    """Learner-resident prioritized sequence replay in HBM (include/seed.h
+    seed_replay_*): `slots` sequences of `record_bytes` each (the payload lives in
+    self.data, one row per slot), a sum tree over p^alpha."""
+
+    def __init__(self, slots, record_bytes, alpha=0.9, beta=0.6, device="cuda"):
+        C = 1
+        while C < slots:
+            C *= 2
+        self.slots, self.capacity, self.alpha, self.beta = slots, C, alpha, beta
+        self.record_bytes = record_bytes
+        z = lambda n, dt: torch.zeros(n, dtype=dt, device=device)
+        self.tree = z(2 * C, torch.float32)
+        self.max_priority = z(1, torch.float32)
+        self.size = z(4, torch.int32)
+        self.gen = z(slots, torch.int32)
+        self.ticket = z(1, torch.int32)
+        self.data = torch.zeros(slots, record_bytes, dtype=torch.uint8, device=device)
+        self.c = L.Replay(C, slots, _ptr(self.tree), _ptr(self.max_priority), _ptr(self.size),
+                          _ptr(self.gen), _ptr(self.ticket))
+        L.check(L.load().seed_replay_check(self._cref()), "seed_replay_check")
+
+    def _cref(self):
+        return C.byref(self.c)
+
+    def insert(self, records, stream=None):
+        """records: uint8 [n][record_bytes] on the device -> (slots, gens)."""
+        n = records.shape[0]
+        slots = torch.empty(n, dtype=torch.int32, device=records.device)
+        gens = torch.empty(n, dtype=torch.int32, device=records.device)
+        L.check(L.load().seed_replay_insert(self._cref(), n, float(self.alpha), _ptr(slots),
+                                            _ptr(gens), _stream(stream)), "seed_replay_insert")
+        _need(records, torch.uint8, "records")
+        L.check(L.load().seed_replay_scatter(_ptr(records), self.record_bytes, _ptr(slots), n,
+                                             _ptr(self.data), _stream(stream)), "seed_replay_scatter")
+        return slots, gens
+
+    def update(self, slots, gens, priorities, stream=None):
+        L.check(L.load().seed_replay_update(self._cref(), slots.numel(), _ptr(slots), _ptr(gens),
+                                            _ptr(priorities), float(self.alpha), _stream(stream)),
+                "seed_replay_update")
+
+    def sample(self, B, uniforms=None, seed=0, counter=0, stream=None):
+        dev = self.tree.device
+        slots = torch.empty(B, dtype=torch.int32, device=dev)
+        gens = torch.empty(B, dtype=torch.int32, device=dev)
+        w = torch.empty(B, dtype=torch.float32, device=dev)
+        L.check(L.load().seed_replay_sample(self._cref(), B, float(self.beta), _ptr(uniforms), seed,
+                                            counter, _ptr(slots), _ptr(gens), _ptr(w),
+                                            _stream(stream)), "seed_replay_sample")
+        return slots, gens, w
+
+    def gather(self, slots, out=None, stream=None):
+        B = slots.numel()
+        out = out if out is not None else torch.empty(B, self.record_bytes, dtype=torch.uint8,
+                                                      device=self.data.device)
+        L.check(L.load().seed_replay_gather(_ptr(self.data), self.record_bytes, _ptr(slots), B,
+                                            _ptr(out), _stream(stream)), "seed_replay_gather")
+        return out
+
+
 def debug_gemm(A, B, a_t=False, b_t=False, bn=64, splits=1, out=None, stream=None):
     """Test hook: D = A @ B^T on the tcgen05 engine (bf16 in, fp32 out)."""
     _need(A, torch.bfloat16, "A")

@@ -501,7 +501,13 @@ template <int CO, int RBX, bool BIAS, int NB = 3>
 __global__ void __launch_bounds__(WC_THREADS, 1)
     win3_wgrad_kernel(const Win3WgradArgs a, int stages, int a_bytes, int b_bytes) {
   constexpr int RBY = 2 * CO;
-  constexpr int NA = 256 / RBX;           // A atoms per M = 128
+  // M = 64 when the rows are 16 channels (32 B): 4 atoms (kx = 0..2 used of 4)
+  // instead of 8 — half the shared-memory operand reads per MMA for the same
+  // ~45-cycle issue (the weight gradients were bound by those reads;
+  // profiles/r02/wgrad_m64.md).  TMEM layout of M = 64 (scripts/probe_umma_m64.cu):
+  // row m at lane (m / 16) * 32 + m % 16.
+  constexpr int MM = RBX == 32 ? 64 : 128;
+  constexpr int NA = 2 * MM / RBX;        // A atoms per MMA
   constexpr int NW = NB * CO;             // weight columns (NB B atoms)
   constexpr int PC = (NB + 1) * CO;       // partial row: weights | bias
   constexpr uint32_t LA = swz_layout_code(RBX), LB = swz_layout_code(RBY);
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       if (lane == 0 && bbytes) bulk_g2s(smem_u32(bd + zlo * RBY), a.dy + lo * RBY, bbytes, &full[s]);
     }
   } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
-    const uint32_t idesc = umma_idesc_bf16(128, NW, true, true);
+    const uint32_t idesc = umma_idesc_bf16(MM, NW, true, true);
     const uint32_t blbo = (uint32_t)(a.bstride * RBY);
     for (int it = 0; it < nks; ++it) {
       const int s = it % stages;
@@ -575,7 +581,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   } else {
     const int q = warp & 3;
     float* part = a.part + (size_t)blockIdx.x * 128 * PC;
-    const int row = q * 32 + lane;
+    // accumulator row of this thread's TMEM lane (M = 64: lanes 0-15 of each quarter)
+    const int row = MM == 128 ? q * 32 + lane : q * 16 + lane;
+    const bool row_ok = MM == 128 || lane < 16;
     const int et = threadIdx.x - 64;   // 0..127
     if (BIAS) {
       // thread = (chunk j of 8 channels, row phase): rows i = rp, rp + 128/NCH, ...
@@ -630,8 +638,10 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
         for (int c = 0; c < 16; ++c) v[c] = 0.f;
       }
       float4* dst = reinterpret_cast<float4*>(part + (size_t)row * PC + c0);
+      if (row_ok) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        for (int c = 0; c < 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
     }
     tc_fence_before();
   }

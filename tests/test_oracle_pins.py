@@ -534,3 +534,121 @@ def test_philox4x32_10_known_answers():
         assert [int(x) for x in out] == [int(x, 16) for x in v["out"]]
     u = O.philox_uniforms(7, 3, np.arange(1000))
     assert np.all((u >= 0) & (u < 1)) and abs(u.mean() - 0.5) < 0.05
+
+
+# ------------------------------------------------------------------ R2D2
+def test_value_rescale_golden_S206_and_roundtrip():
+    """S:206-207 printed values rescale(3) = 1.003, rescale(-3) = -1.003, rescale(0) = 0;
+    S:238 invariant h^-1(h(x)) = x over |x| <= 1e4 (the two functions checked
+    against each other, h increasing and odd)."""
+    assert O.value_rescale(0.0) == 0.0
+    assert abs(O.value_rescale(3.0) - 1.003) < 1e-12
+    assert abs(O.value_rescale(-3.0) + 1.003) < 1e-12
+    x = np.concatenate([np.linspace(-1e4, 1e4, 20001), seedgen.rng(5).normal(0, 30, 1000)])
+    assert np.max(np.abs(O.value_rescale_inv(O.value_rescale(x)) - x)) < 1e-5
+    h = O.value_rescale(np.sort(x))
+    assert np.all(np.diff(h) >= 0) and np.allclose(O.value_rescale(-x), -O.value_rescale(x))
+
+
+def _r2d2_case(B, T, A, seed, done_p=0.1):
+    g = seedgen.rng(seed)
+    qo = g.normal(0, 1.5, (B, T + 1, A))
+    qt = g.normal(0, 1.5, (B, T + 1, A))
+    a = g.integers(0, A, (B, T + 1))
+    r = g.normal(0, 1, (B, T)) * (g.random((B, T)) < 0.3)
+    disc = 0.997 * (g.random((B, T)) >= done_p)
+    return qo, qt, a, r, disc
+
+
+def test_r2d2_targets_terminal_and_priority_goldens_S218_S227():
+    """S:218: terminal step (discount 0) with r = 1 -> y = rescale(1) = 0.41521;
+    S:227: |delta| = [1, 3], eta = 0.9 -> priority 2.9."""
+    qo = np.zeros((1, 2, 3))
+    qt = np.full((1, 2, 3), 7.0)                 # never used: the bootstrap is discounted away
+    y, d, p = O.r2d2_targets(qo, qt, np.zeros((1, 2), int), np.array([[1.0]]),
+                             np.array([[0.0]]), n=5)
+    assert abs(y[0, 0] - 0.41521356237309515) < 1e-12
+    # two steps, both terminal, rewards r: y_t = h(r_t); q chosen so delta = [1, -3]
+    r = np.array([[2.0, -5.0]])
+    qo = np.zeros((1, 3, 2))
+    qo[0, 0, 0] = O.value_rescale(2.0) - 1.0
+    qo[0, 1, 1] = O.value_rescale(-5.0) + 3.0
+    y, d, p = O.r2d2_targets(qo, qo, np.array([[0, 1, 0]]), r, np.zeros((1, 2)), n=5, eta=0.9)
+    np.testing.assert_allclose(d, [[1.0, -3.0]], atol=1e-12)
+    assert abs(p[0] - 2.9) < 1e-12
+
+
+def test_r2d2_targets_geometric_closed_form():
+    """Constant reward r, constant gamma, no episode end, all Q = 0: the n-step return
+    is the geometric sum r (1 - gamma^m) / (1 - gamma), m = min(n, T - t), and h^-1(0) = 0."""
+    B, T, A, n, gam, rv = 2, 9, 4, 5, 0.97, 0.7
+    z = np.zeros((B, T + 1, A))
+    y, _, _ = O.r2d2_targets(z, z, np.zeros((B, T + 1), int), np.full((B, T), rv),
+                             np.full((B, T), gam), n=n)
+    for t in range(T):
+        m = min(n, T - t)
+        np.testing.assert_allclose(y[:, t], O.value_rescale(rv * (1 - gam ** m) / (1 - gam)),
+                                   rtol=1e-12)
+
+
+def test_r2d2_double_q_decoupling_S241():
+    """Perturbing q_target at actions other than the online argmax leaves y unchanged;
+    perturbing it at the argmax changes y (double Q: online selects, target evaluates)."""
+    qo, qt, a, r, disc = _r2d2_case(3, 12, 6, seed=3)
+    y0, _, _ = O.r2d2_targets(qo, qt, a, r, disc, n=5)
+    amax = qo.argmax(-1)
+    mask = np.ones_like(qt, bool)
+    np.put_along_axis(mask, amax[..., None], False, axis=2)
+    y1, _, _ = O.r2d2_targets(qo, np.where(mask, qt + 9.0, qt), a, r, disc, n=5)
+    np.testing.assert_array_equal(y0, y1)
+    y2, _, _ = O.r2d2_targets(qo, np.where(mask, qt, qt + 1.0), a, r, disc, n=5)
+    assert np.mean(np.abs(y2 - y0) > 0) > 0.5     # (zero only where an episode end drops it)
+
+
+def test_r2d2_nstep_recursion_equals_window_sum():
+    """The n-step return as the recursion G^(k)_t = r_t + gamma_t G^(k-1)_{t+1},
+    G^(0)_s = h^-1(q_target[s][argmax q_online[s]]) (written here independently of
+    the oracle's forward window sum) gives the same y."""
+    qo, qt, a, r, disc = _r2d2_case(2, 11, 5, seed=4)
+    n = 4
+    y, _, _ = O.r2d2_targets(qo, qt, a, r, disc, n=n)
+    B, T = r.shape
+    boot = O.value_rescale_inv(np.take_along_axis(qt, qo.argmax(-1)[..., None], 2)[..., 0])
+
+    def G(b, t, k):
+        return boot[b, t] if k == 0 else r[b, t] + disc[b, t] * G(b, t + 1, k - 1)
+    for b in range(B):
+        for t in range(T):
+            assert abs(O.value_rescale(G(b, t, min(n, T - t))) - y[b, t]) < 1e-12
+
+
+def test_r2d2_loss_grad_vs_autograd():
+    qo, qt, a, r, disc = _r2d2_case(2, 6, 4, seed=6)
+    y, _, _ = O.r2d2_targets(qo, qt, a, r, disc, n=3)
+    w = np.array([0.7, 1.0])
+    loss, dq = O.r2d2_loss_grad(qo, a, y, w, 0.25)
+    q = torch.tensor(qo, requires_grad=True)
+    taken = torch.gather(q[:, :-1], 2, torch.tensor(a[:, :-1])[..., None])[..., 0]
+    L = 0.25 * (torch.tensor(w)[:, None] * 0.5 * (taken - torch.tensor(y)) ** 2).sum()
+    L.backward()
+    assert abs(L.item() - loss) < 1e-12
+    np.testing.assert_allclose(dq, q.grad.numpy(), atol=1e-14)
+
+
+def test_replay_probabilities_golden_S313_and_sampling():
+    """priorities [1, 16], alpha = 0.9 -> P ~ [0.0762, 0.9238]; equal priorities ->
+    all weights 1; a zero priority is never drawn; 100k inverse-CDF draws pass a
+    chi-square goodness-of-fit against p^alpha / sum (significance 0.001)."""
+    P = O.replay_probabilities([1.0, 16.0], 0.9)
+    np.testing.assert_allclose(P, [0.0762, 0.9238], atol=5e-5)
+    idx, w = O.replay_sample([2.0] * 5, np.linspace(0, 0.999, 50), 0.9, 0.6)
+    np.testing.assert_allclose(w, 1.0)
+    assert set(idx) == set(range(5))
+    idx, _ = O.replay_sample([0.0, 1.0], seedgen.rng(1).random(1000))
+    assert np.all(idx == 1)
+    from scipy.stats import chisquare
+    pr = seedgen.rng(2).random(40) * 5
+    idx, _ = O.replay_sample(pr, seedgen.rng(3).random(100000), 0.9, 0.6)
+    obs = np.bincount(idx, minlength=40)
+    exp = O.replay_probabilities(pr, 0.9) * 100000
+    assert chisquare(obs, exp).pvalue > 1e-3
