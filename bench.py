@@ -150,14 +150,16 @@ def launch_work(cfg, T, B, A, P, names):
                 s = ns - 1 - k
         H, W, cin, cinp, ch, H2, W2 = geo[s]
         Ai, Ao = F * H * W, F * H2 * W2
-        xin = Ai * (cinp * 2 if s == 0 else cin * 2)
+        # section 0 of the GRF net reads the uint8 obs directly; DMLab's conv reads
+        # the converted x-im2col rows (obs_bf16)
+        xin = Ai * (cin if cfg == "c4" else cinp * 2) if s == 0 else Ai * cin * 2
         if n == "deep_conv_fwd":
             w = (2 * Ai * ch * 9 * cin, xin + Ai * ch * 2)
-        elif n == "deep_pool_fwd":
+        elif n == "deep_pool_fwd":     # conv read, pooled h, relu(h) + argmax written
             w = (0, Ai * ch * 2 + 2 * Ao * ch * 2 + Ao * ch)
         elif n == "deep_res_fwd0":
             w = (2 * Ao * ch * 9 * ch, 2 * Ao * ch * 2)
-        elif n == "deep_res_fwd1":
+        elif n == "deep_res_fwd1":     # u1 + residual read, h and relu(h) written
             w = (2 * Ao * ch * 9 * ch, 4 * Ao * ch * 2)
         elif n.startswith("deep_res_wgrad"):
             w = (2 * Ao * 9 * ch * ch, 2 * Ao * ch * 2)
@@ -453,11 +455,27 @@ def inference_leg(S, torch, world, rank, dist, iters=20):
         torch.cuda.synchronize()
         us = tmax(e0.elapsed_time(e1) * 1e3 / iters)
         row = {"n": n, "us_per_call": round(us, 2), "steps_per_s": round(world * n / us * 1e6, 1)}
-        if n == 1024:   # host-fed: pinned H2D of the requests + D2H of the actions
-            hobs = torch.from_numpy(req["obs"]).pin_memory()
+        if n == 1024:
+            # host-fed: the actors' latest frames sit in per-actor host buffers; every
+            # call packs the n requests into pinned staging (seed_stage_requests: the
+            # library's host worker threads, chunked copies overlapping the packing),
+            # runs the inference graph on the staged buffers and reads the actions back
+            frames = np.random.default_rng(rank).integers(0, 256, size=(NA, 84 * 84 * 4),
+                                                          dtype=np.uint8)
+            ids = req["actor_ids"]
+            obs_list = [frames[i] for i in ids]
             hact = torch.empty(n, dtype=torch.int32).pin_memory()
+            sd = srv.stage_requests(obs_list, ids, req["reward"], req["done"], threads=8,
+                                    chunk=128, stream=s)
+            torch.cuda.synchronize()
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2, stream=s):
+                srv.infer(sd[0], sd[1], sd[2], sd[3], d["uniforms"], action_out=a, blp_out=blp,
+                          stream=s)
+            torch.cuda.synchronize()
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             # same-job pinned H2D probe of the same bytes: the PCIe denominator
+            hobs = torch.from_numpy(frames[ids].reshape(req["obs"].shape)).pin_memory()
             tp0, tp1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             d["obs"].copy_(hobs, non_blocking=True)
             torch.cuda.synchronize()
@@ -467,19 +485,24 @@ def inference_leg(S, torch, world, rank, dist, iters=20):
             tp1.record()
             torch.cuda.synchronize()
             h2d_us = tp0.elapsed_time(tp1) * 1e3 / iters
+            cur = torch.cuda.current_stream()
             tot = 0.0
             for _ in range(iters):
-                t0.record()
-                d["obs"].copy_(hobs, non_blocking=True)
-                g.replay()
+                t0.record(cur)
+                srv.stage_requests(obs_list, ids, req["reward"], req["done"], stream=cur)
+                g2.replay()
                 hact.copy_(a, non_blocking=True)
-                t1.record()
+                t1.record(cur)
                 torch.cuda.synchronize()
                 tot += t0.elapsed_time(t1)
             hus = tmax(tot * 1e3 / iters)
             row.update(host_fed_us=round(hus, 2),
                        host_fed_steps_per_s=round(world * n / hus * 1e6, 1),
                        h2d_bytes=int(hobs.numel()), h2d_probe_us=round(h2d_us, 2),
+                       host_fed_api="InferenceServer.stage_requests (seed_stage_requests: 8 "
+                                    "host threads pack per-actor frames into pinned staging, "
+                                    "128-request chunks copied as packed) + graph replay + "
+                                    "D2H of the actions",
                        h2d_probe_GBs=round(hobs.numel() / h2d_us / 1e3, 2),
                        host_fed_vs_probe=round(hus / max(h2d_us + us, 1e-9), 3))
         out["sweep"].append(row)

@@ -336,6 +336,26 @@ seed_status seed_infer(const seed_net_spec* spec, const void* params_lowp, const
                        int32_t* action_out, float* behaviour_logp_out, float* logits_out,
                        const seed_unroll_store* store, void* workspace, size_t ws_bytes,
                        void* stream);
+/* Host side of the inference batch (H12).  A seed_stager
+ * is a caller-owned pool of `threads` host worker threads.  seed_stage_requests
+ * packs the n requests' observations — obs_ptrs[i] (host) points to request i's
+ * obs_bytes bytes wherever the transport left them — into contiguous pinned
+ * staging (pinned_obs, n*obs_bytes page-locked host bytes), chunk by chunk
+ * (`chunk` requests, <= 0: 128), and issues each chunk's host->device copy into
+ * dev_obs on `stream` as soon as the chunk is packed, so the copies overlap the
+ * packing of later chunks.  Optional metadata (all three host arrays non-NULL or
+ * all NULL) goes in one copy into dev_meta (9n bytes, 16-B aligned): int32 actor
+ * ids at byte 0, fp32 rewards at byte 4n, uint8 dones at byte 8n — the seed_infer
+ * argument layouts.  Returns once every copy is issued; the staging must stay
+ * untouched until the stream reaches them.  One call at a time per stager. */
+typedef struct seed_stager seed_stager;
+seed_status seed_stager_create(int threads, seed_stager** out);
+seed_status seed_stager_destroy(seed_stager* stager);
+seed_status seed_stage_requests(seed_stager* stager, int n, const uint8_t* const* obs_ptrs,
+                                size_t obs_bytes, const int32_t* actor_ids, const float* rewards,
+                                const uint8_t* dones, uint8_t* pinned_obs, uint8_t* pinned_meta,
+                                uint8_t* dev_obs, uint8_t* dev_meta, int chunk, void* stream);
+
 /* Gather B completed unrolls (entries ready_ring[consumed .. consumed+B)) into
  * the seed_batch layout buffers given in `out` (device pointers, cast away
  * const), and advance the consumed counter.  The caller must only ask for

@@ -110,6 +110,10 @@ _SIGS = {
                            c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint64,
                            c_void_p, c_void_p, c_void_p, P(UnrollStore), c_void_p, c_size_t,
                            c_void_p]),
+    "seed_stager_create": (c_int, [c_int, P(c_void_p)]),
+    "seed_stager_destroy": (c_int, [c_void_p]),
+    "seed_stage_requests": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "seed_assemble_batch": (c_int, [P(UnrollStore), c_int, c_int, c_int, P(Batch), c_void_p]),
     "seed_debug_gemm": (c_int, [c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_int,
                                 c_void_p, c_int, c_int, c_void_p, c_void_p]),

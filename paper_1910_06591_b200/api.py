@@ -542,6 +542,50 @@ class InferenceServer:
         L.check(st, "seed_infer")
         return a, blp
 
+    def stage_requests(self, obs_list, actor_ids, rewards, dones, threads=8, chunk=128,
+                       stream=None):
+        if getattr(self, "_stager", None) is None:
+            h = C.c_void_p()
+            L.check(L.load().seed_stager_create(threads, C.byref(h)), "seed_stager_create")
+            self._stager = h
+        return self._stage(obs_list, actor_ids, rewards, dones, chunk, stream)
+
+    def __del__(self):
+        h = getattr(self, "_stager", None)
+        if h is not None and h.value:
+            try:
+                L.load().seed_stager_destroy(h)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stager = None
+
+    def _stage(self, obs_list, actor_ids, rewards, dones, chunk, stream):
+        """Host-fed requests (seed_stage_requests): obs_list = n host uint8 arrays
+        (one per request, e.g. the actors' latest frames), actor_ids / rewards / dones
+        host numpy arrays -> device (actor_ids, obs, reward, done) views of this
+        server's staging buffers, filled asynchronously on `stream`."""
+        import numpy as np
+        n = len(obs_list)
+        ob = int(obs_list[0].nbytes)
+        if getattr(self, "_stage_n", 0) < n or getattr(self, "_stage_ob", 0) != ob:
+            self._pin_obs = torch.empty(n * ob, dtype=torch.uint8).pin_memory()
+            self._pin_meta = torch.empty(9 * n + 16, dtype=torch.uint8).pin_memory()
+            self._dev_obs = torch.empty(n * ob, dtype=torch.uint8, device=self.h.device)
+            self._dev_meta = torch.empty(9 * n + 16, dtype=torch.uint8, device=self.h.device)
+            self._stage_n, self._stage_ob = n, ob
+        ptrs = (C.c_void_p * n)(*[o.ctypes.data for o in obs_list])
+        ids = np.ascontiguousarray(actor_ids, np.int32)
+        rw = np.ascontiguousarray(rewards, np.float32)
+        dn = np.ascontiguousarray(dones, np.uint8)
+        L.check(L.load().seed_stage_requests(self._stager, n, ptrs, ob, ids.ctypes.data,
+                                             rw.ctypes.data, dn.ctypes.data, _ptr(self._pin_obs),
+                                             _ptr(self._pin_meta), _ptr(self._dev_obs),
+                                             _ptr(self._dev_meta), chunk, _stream(stream)),
+                "seed_stage_requests")
+        m = self._dev_meta
+        return (m[:4 * n].view(torch.int32), self._dev_obs[:n * ob].view(n, ob),
+                m[4 * n:8 * n].view(torch.float32), m[8 * n:9 * n])
+
     def assemble(self, B, out, stream=None):
         cb = L.Batch(*(_ptr(out.get(k)) for k in ("obs", "action", "prev_action", "reward",
                                                   "done", "behaviour_logp", "h0", "c0")))

@@ -41,7 +41,7 @@ struct W3FwdEpi {
 #pragma unroll
         for (int j = 0; j < N / 8; ++j) {
           *chunk_at(out, m, RB, j) = z;
-          if (MODE == W3_RES) *chunk_at(outr, m, RB, j) = z;
+          if (MODE == W3_RES && outr) *chunk_at(outr, m, RB, j) = z;
         }
       }
       return;
@@ -66,8 +66,10 @@ struct W3FwdEpi {
       float r[N];
 #pragma unroll
       for (int q = 0; q < N; ++q) r[q] = fmaxf(__bfloat162float(__float2bfloat16_rn(v[q])), 0.f);
+      if (outr) {
 #pragma unroll
-      for (int j = 0; j < N / 8; ++j) *chunk_at(outr, m, RB, j) = pack8(r + 8 * j);
+        for (int j = 0; j < N / 8; ++j) *chunk_at(outr, m, RB, j) = pack8(r + 8 * j);
+      }
       if (dense) {
         uint4* d = reinterpret_cast<uint4*>(dense + ((int64_t)f * g.H * g.W + (int64_t)y * g.W + x) * N);
 #pragma unroll
@@ -177,25 +179,43 @@ static bool kx_stacked() {
   return env >= 0 ? env == 1 : (RB == 64 && N == 16);
 }
 
-template <int MODE, int N, int RB, int NW>
+static U8Rows u8_rows(const uint8_t* obs, const PadGeo& g) {
+  U8Rows u{};
+  u.obs = obs; u.H = g.H; u.W = g.W; u.Wp = g.Wp; u.P = g.P;
+  u.fP = FastDiv((uint32_t)g.P); u.fWp = FastDiv((uint32_t)g.Wp);
+  return u;
+}
+
+template <int MODE, int N, int RB, int NW, int XF = XF_NONE>
 static seed_status fwd_t(const Conv3wFwd& a, cudaStream_t st) {
   WinConvArgs w{};
   w.src = a.in; w.src_rows = a.rows; w.M = a.rows;
   w.wimg = reinterpret_cast<const uint8_t*>(a.wimg);
+  if (XF == XF_U8) w.u8 = u8_rows(a.obs_u8, a.g);
   W3FwdEpi<MODE, N> e{};
   e.g = a.g; e.in_scale = a.in_scale; e.bias = a.bias; e.res = a.res; e.out = a.out;
   e.outr = a.outr; e.dense = a.dense;
-  if (NW == 9 && kx_stacked<N, RB>()) {   // 3 row windows ky, column taps stacked on N
+  if (NW == 9 && XF == XF_NONE && kx_stacked<N, RB>()) {   // 3 row windows ky, column taps stacked on N
     for (int k = 0; k < 3; ++k) w.off[k] = (k - 1) * a.g.Wp;
     return launch_win_conv_kx<W3FwdEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
   }
   for (int k = 0; k < NW; ++k)
     w.off[k] = NW == 9 ? ((k / 3) - 1) * a.g.Wp + (k % 3) - 1 : (k - 1) * a.g.Wp;
-  return launch_win_conv<W3FwdEpi<MODE, N>, RB, NW, w3_mt<MODE, N, true>()>(w, e, st);
+  return launch_win_conv<W3FwdEpi<MODE, N>, RB, NW, w3_mt<MODE, N, true>(), XF>(w, e, st);
 }
 
 template <int MODE>
 static seed_status fwd_mode(const Conv3wFwd& a, cudaStream_t st) {
+  if (a.xf == XF_U8) {   // section 0 of the GRF net: 16 uint8 planes
+    if (MODE == W3_PLAIN && !a.xim && a.ch == 16 && a.cin_p == 16 && a.obs_u8)
+      return fwd_t<MODE, 16, 32, 9, XF_U8>(a, st);
+    return SEED_E_UNSUPPORTED;
+  }
+  if (a.xf == XF_RELU) {   // residual conv0: relu of the residual stream in shared memory
+    if (MODE == W3_RELU && !a.xim && a.ch == 16 && a.cin_p == 16) return fwd_t<MODE, 16, 32, 9, XF_RELU>(a, st);
+    if (MODE == W3_RELU && !a.xim && a.ch == 32 && a.cin_p == 32) return fwd_t<MODE, 32, 64, 9, XF_RELU>(a, st);
+    return SEED_E_UNSUPPORTED;
+  }
   if (a.xim) {
     if (a.ch == 16 && a.cin_p == 16) return fwd_t<MODE, 16, 32, 3>(a, st);
     return SEED_E_UNSUPPORTED;
@@ -282,11 +302,22 @@ size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool) { return win3_wgrad_p
 seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
   Win3WgradArgs w{};
   w.X = a.X; w.dy = a.dY; w.M = a.rows; w.part = a.part;
+  if (a.xf == XF_U8) w.u8 = u8_rows(a.obs_u8, a.g);
   w.boff = a.xim ? -a.g.Wp : 1 - a.g.Wp;
   w.bstride = a.g.Wp;
   W3Fin3 f{};
   f.xim = a.xim ? 1 : 0; f.Cp = a.cin_p; f.CI = a.cin; f.CO = a.ch; f.scale = a.scale; f.g_w = a.g_w;
   f.g_b = a.g_b;
+  if (a.xf == XF_U8) {
+    if (a.ch == 16 && a.cin_p == 16 && !a.xim && a.obs_u8)
+      return launch_win3_wgrad<16, 32, W3Fin3, 3, XF_U8>(w, f, true, st);
+    return SEED_E_UNSUPPORTED;
+  }
+  if (a.xf == XF_RELU) {
+    if (a.ch == 16 && a.cin_p == 16 && !a.xim) return launch_win3_wgrad<16, 32, W3Fin3, 3, XF_RELU>(w, f, true, st);
+    if (a.ch == 32 && a.cin_p == 32 && !a.xim) return launch_win3_wgrad<32, 64, W3Fin3, 3, XF_RELU>(w, f, true, st);
+    return SEED_E_UNSUPPORTED;
+  }
   if (a.ch == 16 && a.cin_p == 16) return launch_win3_wgrad<16, 32>(w, f, !a.xim, st);
   if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, !a.xim, st);
   if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, !a.xim, st);
@@ -467,7 +498,7 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
   if (oy < 0 || oy >= go.H || ox < 0 || ox >= go.W) {
     const uint4 z = make_uint4(0, 0, 0, 0);
     *chunk_at(h0, m, RB, j) = z;
-    *chunk_at(hr0, m, RB, j) = z;
+    if (hr0) *chunk_at(hr0, m, RB, j) = z;
     continue;
   }
   uint4 in[9];
@@ -503,7 +534,7 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
     rl[p] = *reinterpret_cast<const uint32_t*>(&r2);
   }
   *chunk_at(h0, m, RB, j) = make_uint4(best[0], best[1], best[2], best[3]);
-  *chunk_at(hr0, m, RB, j) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+  if (hr0) *chunk_at(hr0, m, RB, j) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
   uint2 a;
   a.x = __byte_perm(barg[0], barg[1], 0x6420);
   a.y = __byte_perm(barg[2], barg[3], 0x6420);

@@ -59,11 +59,16 @@ enum { D3W_PLAIN = 0, D3W_MASK = 1, D3W_RES = 2 };  // data-gradient epilogues
 // Forward 3x3 conv (9 windows, or 3 for the x-im2col section-0 input).
 //   W3_PLAIN: out = acc*in_scale + b  (section conv; border rows not written)
 //   W3_RELU:  out = relu(acc + b)
-//   W3_RES:   out = res + acc + b, outr = relu(out), dense (nullable) = relu(out) as
-//             [f][(y*W + x)*ch + c] (the FC input)
+//   W3_RES:   out = res + acc + b, outr (nullable) = relu(out), dense (nullable) =
+//             relu(out) as [f][(y*W + x)*ch + c] (the FC input)
+// xf (win_engine.cuh): XF_RELU = the conv reads relu(in) (relu applied to the slab in
+// shared memory); XF_U8 = `in` is ignored and the input rows are the uint8 obs
+// [F][H][W][16] `obs_u8` expanded in shared memory (section 0 of the GRF net)
 struct Conv3wFwd {
   int mode, cin_p, ch;    // cin_p = input row channels (16 / 32); ch = 16 / 32
   bool xim;
+  int xf;
+  const uint8_t* obs_u8;
   PadGeo g;
   int64_t rows;           // F*P
   float in_scale;
@@ -92,10 +97,13 @@ struct Conv3wDgrad {
 seed_status conv3w_dgrad(const Conv3wDgrad& a, cudaStream_t st);
 
 // Weight + bias gradient: dW[co][ky][kx][c] = scale * sum_g X[g + off][c] dY[g][co],
-// db[co] = sum_g dY[g][co] (fixed-order split sum; part = scratch)
+// db[co] = sum_g dY[g][co] (fixed-order split sum; part = scratch); xf as Conv3wFwd
+// (XF_RELU: X = relu(rows), XF_U8: X from obs_u8)
 struct Conv3wWgrad {
   int cin_p, cin, ch;     // X row channels, real input channels, dY channels
   bool xim;
+  int xf;
+  const uint8_t* obs_u8;
   PadGeo g;
   int64_t rows;
   float scale;
@@ -109,8 +117,8 @@ seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st);
 size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool xim);
 
 // max-pool 3x3 / stride 2 / TF 'same' (top/left pad pt/pl, padding = -inf, first
-// maximum in (ky, kx) order): conv (gi rows) -> h0, hr0 = relu(h0) (go rows) and the
-// window argmax (0..8) per (go row, channel)
+// maximum in (ky, kx) order): conv (gi rows) -> h0, hr0 = relu(h0) (nullable; go rows)
+// and the window argmax (0..8) per (go row, channel)
 seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
                             const uint8_t* conv, uint8_t* h0, uint8_t* hr0, uint8_t* arg,
                             cudaStream_t st);

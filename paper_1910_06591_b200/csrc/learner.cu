@@ -339,12 +339,32 @@ static seed_status shallow_backward(const StepCtx& c, const seed_batch* bt, cons
 // conv3w.cuh: every activation in its padded row space (zero borders), 3x3
 // convs as shifted-window tcgen05 GEMMs, bias gradients from the weight-gradient
 // engine's all-ones operand.
+// Section 0 reads the uint8 obs directly (converted to bf16 rows in shared memory,
+// XF_U8) when they are 16 planes (GRF SMM); other inputs (DMLab RGB: the x-im2col
+// rows) go through one conversion pass.  (Applying the residual stream's relu in
+// shared memory instead of storing hr = relu(h), XF_RELU, was measured and is not
+// used: the 16/32-channel convs are bound by shared-memory operand reads, and the
+// in-place pass cost them more than the saved HBM writes: profiles/r02/xf_modes.md.)
+// Measured slower (conv_fwd s0 432 -> 839 us, conv_wgrad s0 410 -> 938 us with the
+// obs_bf16 pass (235 us) gone: the 16-channel convs are bound by shared-memory
+// operand reads and the expansion's staging traffic and ALU work land on the same
+// SMs; profiles/r02/xf_modes.md), so it is opt-in: SEED_XF_U8=1 (A/B measurement;
+// parity-tested in tests/test_gpu_learner.py::test_learner_c4_u8_source_parity).
+static bool deep_u8_input(const NetPlan& p) {
+  static const bool on = [] {
+    const char* e = getenv("SEED_XF_U8");
+    return e && e[0] == '1';
+  }();
+  return on && !p.sec[0].xim && p.C == 16 && p.sec[0].cinp == 16;
+}
+
 static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                 const float* params, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
   const int64_t F = w.F;
-  {
+  const bool u8in = deep_u8_input(p);
+  if (!u8in) {
     const DeepSec& d = p.sec[0];
     SEED_TRY(conv3_obs((const uint8_t*)bt->obs, F, PadGeo::make(d.H, d.W), p.C, d.cinp, d.xim,
                        c.at<uint8_t>(w.obs_bf16), st));
@@ -358,6 +378,10 @@ static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf
     a.mode = W3_PLAIN; a.cin_p = d.cinp; a.ch = d.ch; a.xim = d.xim; a.g = gi; a.rows = F * gi.P;
     a.in_scale = s == 0 ? 1.f / 255.f : 1.f;
     a.in = s == 0 ? c.at<uint8_t>(w.obs_bf16) : c.at<uint8_t>(w.sec[s - 1].h[2]);
+    if (s == 0 && u8in) {
+      a.xf = XF_U8;
+      a.obs_u8 = (const uint8_t*)bt->obs;
+    }
     a.wimg = lowp + d.im_w; a.bias = params + p.t[d.t_b].off; a.out = c.at<uint8_t>(b.conv);
     SEED_TRY(conv3w_forward(a, st));
     c.mark("deep_conv_fwd");
@@ -373,7 +397,7 @@ static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf
       SEED_TRY(conv3w_forward(a0, st));
       c.mark("deep_res_fwd0");
       Conv3wFwd a1 = a0;
-      a1.mode = W3_RES; a1.in = c.at<uint8_t>(b.u1[r]); a1.wimg = lowp + d.im_rw[r][1];
+      a1.mode = W3_RES; a1.xf = XF_NONE; a1.in = c.at<uint8_t>(b.u1[r]); a1.wimg = lowp + d.im_rw[r][1];
       a1.bias = params + p.t[d.t_rb[r][1]].off; a1.res = c.at<uint8_t>(b.h[r]);
       a1.out = c.at<uint8_t>(b.h[r + 1]); a1.outr = c.at<uint8_t>(b.hr[r + 1]);
       a1.dense = (s == p.nsec - 1 && r == 1) ? c.at<bf16>(w.act2) : nullptr;
@@ -430,6 +454,10 @@ static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const b
     wg.cin_p = d.cinp; wg.cin = d.cin; wg.ch = d.ch; wg.xim = d.xim; wg.g = gi; wg.rows = F * gi.P;
     wg.scale = s == 0 ? 1.f / 255.f : 1.f;
     wg.X = s == 0 ? c.at<uint8_t>(w.obs_bf16) : c.at<uint8_t>(w.sec[s - 1].h[2]);
+    if (s == 0 && deep_u8_input(p)) {
+      wg.xf = XF_U8;
+      wg.obs_u8 = (const uint8_t*)bt->obs;
+    }
     wg.dY = c.at<uint8_t>(b.dconv); wg.part = part;
     wg.g_w = grads + p.t[d.t_w].off; wg.g_b = grads + p.t[d.t_b].off;
     SEED_TRY(conv3w_wgrad(wg, st));

@@ -36,14 +36,47 @@ constexpr int WC_SMEM_BUDGET = 200 * 1024;
 constexpr int WG_KS = 256;        // rows per weight-gradient k-stage
 constexpr int WIN_MAX = 9;        // windows per convolution
 
+// uint8 source of a 16-channel padded row space (XF_U8): obs [F][H][W][16] bytes
+// whose padded row g = f*P + Y*Wp + X holds pixel (Y-1, X-1) (zero borders)
+struct U8Rows {
+  const uint8_t* obs;
+  int H, W, Wp, P;
+  FastDiv fP, fWp;
+  // interior pixels before padded row g (g < 2^31): the obs pixel index of g if
+  // g is interior; consecutive rows map to a contiguous obs range
+  __device__ __forceinline__ int64_t idx(int64_t g) const {
+    uint32_t f, r, Y, X;
+    fP.divmod((uint32_t)g, f, r);
+    fWp.divmod(r, Y, X);
+    const int y = min(max((int)Y - 1, 0), H);
+    const int x = ((int)Y >= 1 && (int)Y <= H) ? min(max((int)X - 1, 0), W) : 0;
+    return (int64_t)f * H * W + (int64_t)y * W + x;
+  }
+  __device__ __forceinline__ bool interior(int64_t g) const {
+    uint32_t f, r, Y, X;
+    fP.divmod((uint32_t)g, f, r);
+    fWp.divmod(r, Y, X);
+    return Y >= 1 && (int)Y <= H && X >= 1 && (int)X <= W;
+  }
+};
+
+// slab transforms between the TMA and the MMA (done by two extra converter warps):
+//   XF_NONE  the slab is the MMA operand as copied;
+//   XF_RELU  relu in place (the input is h, the conv reads relu(h): the relu copy
+//            hr of the residual stream is never stored);
+//   XF_U8    the TMA brings the raw uint8 pixels (U8Rows) into a staging buffer and
+//            the converters expand them into the bf16 row slab (0..255 exact in
+//            bf16), zero borders included — no converted copy of the obs in HBM.
+enum { XF_NONE = 0, XF_RELU = 1, XF_U8 = 2 };
+
 struct WinConvArgs {
   const uint8_t* src;    // pre-swizzled rows of RB bytes
   int64_t src_rows;      // rows that exist (others read as zero)
   int64_t M;             // output rows
   int off[WIN_MAX];      // window row offsets
   const uint8_t* wimg;   // pre-swizzled weight image [NW][N][RB]
+  U8Rows u8;             // XF_U8 source
 };
-
 
 __device__ __forceinline__ uint4 pack8(const float* o) {
   uint4 u;
@@ -94,6 +127,107 @@ __device__ __forceinline__ void load_slab(uint8_t* slab, const uint8_t* src, int
   }
 }
 
+// bf16 bits of 8 bytes (values 0..255, exact): the float's high half
+__device__ __forceinline__ uint4 u8x8_to_bf16(uint32_t lo, uint32_t hi) {
+  const uint32_t w[2] = {lo, hi};
+  uint32_t o[4];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    // (0x4B000000 | b) as float = 2^23 + b exactly; minus 2^23 -> b (FADD, no I2F)
+    const float b0 = __uint_as_float(0x4B000000u | (w[k] & 0xFF)) - 8388608.f;
+    const float b1 = __uint_as_float(0x4B000000u | ((w[k] >> 8) & 0xFF)) - 8388608.f;
+    const float b2 = __uint_as_float(0x4B000000u | ((w[k] >> 16) & 0xFF)) - 8388608.f;
+    const float b3 = __uint_as_float(0x4B000000u | (w[k] >> 24)) - 8388608.f;
+    o[2 * k] = __byte_perm(__float_as_uint(b0), __float_as_uint(b1), 0x7632);
+    o[2 * k + 1] = __byte_perm(__float_as_uint(b2), __float_as_uint(b3), 0x7632);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// Converter warps (XF_CW of them) of a stage: expand / transform slab rows [0, n)
+// whose first row is global row R0.  XF_U8 (rows of 32 bytes = 16 bf16 channels):
+// warp cw takes the contiguous row block [cw*n/XF_CW, (cw+1)*n/XF_CW) with its
+// lanes striding 32 rows, tracking each lane's (frame, Y, X) incrementally (one
+// division per stage, not per row).
+constexpr int XF_CW = 4;
+template <int XF, int RB>
+__device__ __forceinline__ void convert_slab(uint8_t* slab, const uint8_t* stg, int64_t R0, int n,
+                                             int64_t lim, const U8Rows& u, int64_t p_lo, int cw,
+                                             int lane) {
+  uint8_t* dst = slab + slab_phase(R0, RB);
+  if constexpr (XF == XF_RELU) {
+    const __nv_bfloat162 z2 = __floats2bfloat162_rn(0.f, 0.f);
+    uint4* p = reinterpret_cast<uint4*>(dst);
+    for (int i = cw * 32 + lane; i < n * RB / 16; i += 32 * XF_CW) {
+      uint4 v = p[i];
+      uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const __nv_bfloat162 r = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]), z2);
+        w[k] = *reinterpret_cast<const uint32_t*>(&r);
+      }
+      p[i] = v;
+    }
+  } else if constexpr (XF == XF_U8) {
+    static_assert(RB == 32, "XF_U8: 16-channel rows");
+    const int i0 = (int)((int64_t)n * cw / XF_CW), i1 = (int)((int64_t)n * (cw + 1) / XF_CW);
+    int i = i0 + lane;
+    int64_t g = R0 + i;
+    // (frame, Y, X) of row g (rows < 0 clamp to frame 0; they are zeroed below)
+    uint32_t f = 0, Y = 0, X = 0;
+    {
+      uint32_t r;
+      u.fP.divmod((uint32_t)max(g, (int64_t)0), f, r);
+      u.fWp.divmod(r, Y, X);
+    }
+    const int Hp = u.H + 2;
+    const int64_t HW = (int64_t)u.H * u.W;
+    for (; i < i1; i += 32, g += 32) {
+      uint4 c0 = make_uint4(0, 0, 0, 0), c1 = c0;
+      if (g >= 0 && g < lim && Y >= 1 && (int)Y <= u.H && X >= 1 && (int)X <= u.W) {
+        const int64_t pix = (int64_t)f * HW + (int64_t)(Y - 1) * u.W + (X - 1);
+        const uint4 b = *reinterpret_cast<const uint4*>(stg + (pix - p_lo) * 16);
+        c0 = u8x8_to_bf16(b.x, b.y);
+        c1 = u8x8_to_bf16(b.z, b.w);
+      }
+      uint8_t* row = dst + (size_t)i * 32;
+      const int sw = (int)((g >> 2) & 1);   // swz_chunk(g, 32, j) = j ^ ((g >> 2) & 1)
+      *reinterpret_cast<uint4*>(row + ((0 ^ sw) << 4)) = c0;
+      *reinterpret_cast<uint4*>(row + ((1 ^ sw) << 4)) = c1;
+      if (g >= 0) {   // advance 32 rows
+        X += 32;
+        while ((int)X >= u.Wp) {
+          X -= u.Wp;
+          if ((int)++Y == Hp) { Y = 0; ++f; }
+        }
+      } else if (g + 32 >= 0) {
+        uint32_t r;
+        u.fP.divmod((uint32_t)(g + 32), f, r);
+        u.fWp.divmod(r, Y, X);
+      }
+    }
+  }
+}
+
+// XF_U8 producer: the contiguous obs pixel range of padded rows [R0, R0 + n) into
+// the staging buffer (one bulk copy, credited to `bar`); returns its first pixel
+// (*plo_out is written before the barrier arrival, whose release orders it for the
+// converters waiting on `bar`)
+__device__ __forceinline__ void load_u8_rows(uint8_t* stg, const U8Rows& u, int64_t R0, int n,
+                                             int64_t lim, uint64_t* bar, int lane, uint32_t extra_tx,
+                                             int64_t* plo_out) {
+  const int64_t lo = max(R0, (int64_t)0), hi = min(R0 + n, lim);
+  const int64_t p_lo = hi > lo ? u.idx(lo) : 0, p_hi = hi > lo ? u.idx(hi) : 0;
+  if (lane == 0) {
+    *plo_out = p_lo;
+    const uint32_t bytes = (uint32_t)((p_hi - p_lo) * 16);
+    if (bytes + extra_tx) mbar_expect_tx(bar, bytes + extra_tx);
+    else mbar_arrive(bar);
+    if (bytes) bulk_g2s(smem_u32(stg), u.obs + p_lo * 16, bytes, bar);
+  }
+}
+
+
 // ------------------------------------------------------------------ forward / dgrad
 // Epi: static constexpr int N; __device__ void store(int64_t m, float (&v)[N]) const
 // An epilogue that reads other rows of global memory (residual input, ReLU mask)
@@ -112,9 +246,9 @@ struct EpiPre { static constexpr int n = 0; };
 template <class E>
 struct EpiPre<E, std::void_t<decltype(E::PRE)>> { static constexpr int n = E::PRE; };
 
-template <class Epi, int RB, int NW, int MT = 1>
-__global__ void __launch_bounds__(WCF_THREADS, 1)
-    win_conv_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes) {
+template <class Epi, int RB, int NW, int MT = 1, int XF = XF_NONE>
+__global__ void __launch_bounds__(WCF_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0), 1)
+    win_conv_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes, int stg_bytes) {
   constexpr int N = Epi::N;
   constexpr int TM = 128 * MT;
   constexpr uint32_t LAYOUT = swz_layout_code(RB);
@@ -127,7 +261,10 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
   uint8_t* Ws = sm;
   uint8_t* slabs = sm + ((WB + 1023) & ~1023);
+  uint8_t* stgs = slabs + (size_t)stages * slab_bytes;   // XF_U8 staging, stg_bytes each
   __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[WCF_ACC], tempty[WCF_ACC], wbar;
+  __shared__ uint64_t ready[WC_MAX_STAGES];   // XF: converters done (count XF_CW)
+  __shared__ int64_t plo[WC_MAX_STAGES];      // XF_U8: first pixel of each stage's staging
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int mn = a.off[0], mx = a.off[0];
@@ -136,7 +273,11 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
   const int nrows = TM + mx - mn;
   const int64_t tiles = (a.M + TM - 1) / TM;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&ready[s], XF_CW);
+    }
     for (int i = 0; i < WCF_ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     mbar_init(&wbar, 1);
     fence_mbar_init();
@@ -158,8 +299,25 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int s = it % stages;
       mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-      load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, t * TM + mn, nrows, a.src_rows, &full[s],
-                lane, 0);
+      if constexpr (XF == XF_U8) {
+        load_u8_rows(stgs + (size_t)s * stg_bytes, a.u8, t * TM + mn, nrows, a.src_rows, &full[s], lane, 0,
+                     &plo[s]);
+      } else {
+        load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, t * TM + mn, nrows, a.src_rows, &full[s],
+                  lane, 0);
+      }
+    }
+  } else if (XF != XF_NONE && warp >= 10) {   // slab converters
+    const int cw = warp - 10;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int s = it % stages;
+      mbar_wait(&full[s], (it / stages) & 1);
+      convert_slab<XF, RB>(slabs + (size_t)s * slab_bytes, stgs + (size_t)s * stg_bytes, t * TM + mn, nrows,
+                           a.src_rows, a.u8, XF == XF_U8 ? plo[s] : 0, cw, lane);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ready[s]);
     }
   } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
     mbar_wait(&wbar, 0);
@@ -171,7 +329,7 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
     int it = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int s = it % stages, acc = it % WCF_ACC;
-      mbar_wait(&full[s], (it / stages) & 1);
+      mbar_wait(XF != XF_NONE ? &ready[s] : &full[s], (it / stages) & 1);
       mbar_wait(&tempty[acc], ((it / WCF_ACC) & 1) ^ 1);
       tc_fence_after();
       const uint32_t base = smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * TM + mn, RB);
@@ -191,7 +349,7 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
       tc_commit_w(&empty[s]);
       tc_commit_w(&tfull[acc]);
     }
-  } else {
+  } else if (warp < 10) {
     const int q = warp & 3;            // TMEM lanes [32q, 32q+32) of this warp
     const int grp = (warp - 2) >> 2;   // epilogue group: tiles it with it % 2 == grp
     int it = 0;
@@ -241,24 +399,27 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
   }
 }
 
-template <class Epi, int RB, int NW, int MT = 1>
+template <class Epi, int RB, int NW, int MT = 1, int XF = XF_NONE>
 seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st) {
   constexpr int WB = NW * Epi::N * RB;
   constexpr int TM = 128 * MT;
   int mn = a.off[0], mx = a.off[0];
   for (int w = 1; w < NW; ++w) { mn = std::min(mn, a.off[w]); mx = std::max(mx, a.off[w]); }
   const int slab = (int)align_up((size_t)(TM + mx - mn) * RB + 1024, 1024);
+  // XF_U8 staging: the slab's pixels as uint8 (16 bytes each)
+  const int stg = XF == XF_U8 ? (int)align_up((size_t)(TM + mx - mn) * 16 + 16, 1024) : 0;
   const int wbytes = (int)align_up(WB, 1024);
-  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - wbytes) / slab);
+  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - wbytes) / (slab + stg));
   if (a.M <= 0) return a.M == 0 ? SEED_OK : SEED_E_SHAPE;
   if (stages < 2) return SEED_E_SHAPE;
-  const size_t smem = (size_t)wbytes + (size_t)stages * slab + 1024;
+  const size_t smem = (size_t)wbytes + (size_t)stages * (slab + stg) + 1024;
   static PerDevice attr;
-  SEED_TRY(smem_optin(attr, win_conv_kernel<Epi, RB, NW, MT>, WC_SMEM_BUDGET + 2048));
-    const int64_t tiles = (a.M + TM - 1) / TM;
-  const int grid = (int)std::min<int64_t>(tiles, 148);
-  return launch_k(win_conv_kernel<Epi, RB, NW, MT>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e,
-                  stages, slab);
+  SEED_TRY(smem_optin(attr, win_conv_kernel<Epi, RB, NW, MT, XF>, WC_SMEM_BUDGET + 2048));
+  const int64_t tiles = (a.M + TM - 1) / TM;
+  const int grid = (int)std::min<int64_t>(tiles, sm_count());
+  const int threads = WCF_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0);
+  return launch_k(win_conv_kernel<Epi, RB, NW, MT, XF>, dim3(grid), dim3(threads), smem, st, a, e,
+                  stages, slab, stg);
 }
 
 // ------------------------------------------------------------------ column-tap-stacked 3x3
@@ -489,17 +650,18 @@ inline int wgrad_grid(int64_t M, int64_t* rows_per_cta) {
 // row, which only moves border / zero rows), fixed order, released to the
 // producer through the stage's empty barrier (2 arrivals: MMA commit + epilogue).
 struct Win3WgradArgs {
-  const uint8_t* X;      // rows of RBX bytes
+  const uint8_t* X;      // rows of RBX bytes (XF_U8: unused, the rows come from u8)
   const uint8_t* dy;     // rows of 2*CO bytes
   int64_t M;             // rows (X and dY share the row space)
   int boff, bstride;     // B atom j starts at row h + boff + j*bstride
   int64_t rows_per_cta;
   float* part;           // [grid][128][4*CO] (cols [0, 3CO) weights, [3CO, 4CO) bias in row 0)
+  U8Rows u8;             // XF_U8 source of the X rows
 };
 
-template <int CO, int RBX, bool BIAS, int NB = 3>
-__global__ void __launch_bounds__(WC_THREADS, 1)
-    win3_wgrad_kernel(const Win3WgradArgs a, int stages, int a_bytes, int b_bytes) {
+template <int CO, int RBX, bool BIAS, int NB = 3, int XF = XF_NONE>
+__global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0), 1)
+    win3_wgrad_kernel(const Win3WgradArgs a, int stages, int a_bytes, int b_bytes, int stg_bytes) {
   constexpr int RBY = 2 * CO;
   // M = 64 when the rows are 16 channels (32 B): 4 atoms (kx = 0..2 used of 4)
   // instead of 8 — half the shared-memory operand reads per MMA for the same
@@ -515,7 +677,10 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
   uint8_t* stg = sm + 1024;
+  const size_t sst = (size_t)a_bytes + b_bytes + stg_bytes;   // stage stride
   __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull;
+  __shared__ uint64_t ready[WC_MAX_STAGES];   // XF: A slab transformed (converter warps 6..)
+  __shared__ int64_t plo[WC_MAX_STAGES];
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
@@ -523,7 +688,11 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
   const int arows = WG_KS + NA - 1, brows = WG_KS + (NB - 1) * a.bstride;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], BIAS ? 2 : 1); }
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], BIAS ? 2 : 1);
+      mbar_init(&ready[s], XF_CW);
+    }
     mbar_init(&tfull, 1);
     fence_mbar_init();
   }
@@ -537,7 +706,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       const int s = it % stages;
       mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
       const int64_t k0 = r_begin + (int64_t)it * WG_KS;
-      uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
+      uint8_t* sa = stg + (size_t)s * sst;
       // rows_per_cta is a multiple of WG_KS, so only the last CTA has a partial last
       // stage, and there every K index h >= M reads X rows >= M (zero-filled)
       const int64_t lo = std::max<int64_t>(k0 + a.boff, 0),
@@ -553,18 +722,33 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
         fence_proxy_async_smem();
       }
       __syncwarp();
-      load_slab(sa, a.X, RBX, k0, arows, a.M, &full[s], lane, bbytes);
+      if constexpr (XF == XF_U8)
+        load_u8_rows(sa + a_bytes + b_bytes, a.u8, k0, arows, a.M, &full[s], lane, bbytes, &plo[s]);
+      else
+        load_slab(sa, a.X, RBX, k0, arows, a.M, &full[s], lane, bbytes);
       if (lane == 0 && bbytes) bulk_g2s(smem_u32(bd + zlo * RBY), a.dy + lo * RBY, bbytes, &full[s]);
+    }
+  } else if (XF != XF_NONE && warp >= 6) {   // A-slab converters
+    for (int it = 0; it < nks; ++it) {
+      const int s = it % stages;
+      mbar_wait(&full[s], (it / stages) & 1);
+      const int64_t k0 = r_begin + (int64_t)it * WG_KS;
+      uint8_t* sa = stg + (size_t)s * sst;
+      convert_slab<XF, RBX>(sa, sa + a_bytes + b_bytes, k0, arows, a.M, a.u8, XF == XF_U8 ? plo[s] : 0,
+                            warp - 6, lane);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ready[s]);
     }
   } else if (warp == 1) {   // MMA issue: warp-uniform, one elected lane issues
     const uint32_t idesc = umma_idesc_bf16(MM, NW, true, true);
     const uint32_t blbo = (uint32_t)(a.bstride * RBY);
     for (int it = 0; it < nks; ++it) {
       const int s = it % stages;
-      mbar_wait(&full[s], (it / stages) & 1);
+      mbar_wait(XF != XF_NONE ? &ready[s] : &full[s], (it / stages) & 1);
       tc_fence_after();
       const int64_t k0 = r_begin + (int64_t)it * WG_KS;
-      uint8_t* sa = stg + (size_t)s * (a_bytes + b_bytes);
+      uint8_t* sa = stg + (size_t)s * sst;
       const uint64_t ad0 = umma_desc(smem_u32(sa) + slab_phase(k0, RBX), RBX, 8 * RBX, LA);
       const uint64_t bd0 =
           umma_desc(smem_u32(sa + a_bytes) + slab_phase(k0 + a.boff, RBY), blbo, 8 * RBY, LB);
@@ -578,7 +762,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       tc_commit_w(&empty[s]);
     }
     tc_commit_w(&tfull);
-  } else {
+  } else if (warp < 6) {
     const int q = warp & 3;
     float* part = a.part + (size_t)blockIdx.x * 128 * PC;
     // accumulator row of this thread's TMEM lane (M = 64: lanes 0-15 of each quarter)
@@ -594,7 +778,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
         const int s = it % stages;
         mbar_wait(&full[s], (it / stages) & 1);
         const int64_t k0 = r_begin + (int64_t)it * WG_KS;
-        const uint8_t* bsl = stg + (size_t)s * (a_bytes + b_bytes) + a_bytes + slab_phase(k0 + a.boff, RBY);
+        const uint8_t* bsl = stg + (size_t)s * sst + a_bytes + slab_phase(k0 + a.boff, RBY);
 #pragma unroll 4
         for (int i = rp; i < WG_KS; i += RSTEP) {
           const int lr = i + a.bstride;                        // slab row of dY[h + boff + bstride]
@@ -687,21 +871,24 @@ inline size_t win3_wgrad_part_bytes(int64_t M, int CO, int NB = 3) {
 
 // bias = false: no all-ones MMA (the bias gradient is a column of the weight
 // accumulator, e.g. from a constant-1 input channel)
-template <int CO, int RBX, class Fin, int NB = 3>
+template <int CO, int RBX, class Fin, int NB = 3, int XF = XF_NONE>
 seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias, cudaStream_t st) {
   Win3WgradArgs a = a0;
   const int G = wgrad_grid(a.M, &a.rows_per_cta);
-  const int a_bytes = (int)align_up((size_t)(WG_KS + 256 / RBX - 1) * RBX + 1024, 1024);
+  const int arows = WG_KS + 256 / RBX - 1;
+  const int a_bytes = (int)align_up((size_t)arows * RBX + 1024, 1024);
   const int b_bytes = (int)align_up((size_t)(WG_KS + (NB - 1) * a.bstride) * 2 * CO + 1024, 1024);
-  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes));
+  const int stg_bytes = XF == XF_U8 ? (int)align_up((size_t)arows * 16 + 16, 1024) : 0;
+  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - 1024) / (a_bytes + b_bytes + stg_bytes));
   if (stages < 2) return SEED_E_SHAPE;
-  const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes);
+  const size_t smem = 2048 + (size_t)stages * (a_bytes + b_bytes + stg_bytes);
   static PerDevice attr0;
-  SEED_TRY(smem_optin(attr0, win3_wgrad_kernel<CO, RBX, true, NB>, WC_SMEM_BUDGET + 2048));
+  SEED_TRY(smem_optin(attr0, win3_wgrad_kernel<CO, RBX, true, NB, XF>, WC_SMEM_BUDGET + 2048));
   static PerDevice attr1;
-  SEED_TRY(smem_optin(attr1, win3_wgrad_kernel<CO, RBX, false, NB>, WC_SMEM_BUDGET + 2048));
-    SEED_TRY(launch_k(bias ? win3_wgrad_kernel<CO, RBX, true, NB> : win3_wgrad_kernel<CO, RBX, false, NB>, dim3(G),
-                    dim3(WC_THREADS), smem, st, a, stages, a_bytes, b_bytes));
+  SEED_TRY(smem_optin(attr1, win3_wgrad_kernel<CO, RBX, false, NB, XF>, WC_SMEM_BUDGET + 2048));
+  const int threads = WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0);
+  SEED_TRY(launch_k(bias ? win3_wgrad_kernel<CO, RBX, true, NB, XF> : win3_wgrad_kernel<CO, RBX, false, NB, XF>,
+                    dim3(G), dim3(threads), smem, st, a, stages, a_bytes, b_bytes, stg_bytes));
   const int tot = 128 * NB * CO + (bias ? CO : 0);
   return launch_k(win3_wgrad_finish<CO, Fin, NB>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
                   (const float*)a.part, G, tot, fin);

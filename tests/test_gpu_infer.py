@@ -276,3 +276,30 @@ def test_store_stale_and_short_assemble_reported():
     torch.cuda.synchronize()
     rc = srv.st["ready_count"].cpu().numpy()
     assert rc[3] == 1, rc
+
+
+def test_stage_requests_host_fed_equals_device_fed():
+    """H12 host side (seed_stage_requests): the requests' observations gathered from
+    per-actor host buffers into pinned staging by the stager's threads and copied in
+    chunks give exactly the device-fed call's results (bit-exact staging)."""
+    S, srv, ospec, params = _setup(store=False, max_n=16)
+    S2, srv2, _, _ = _setup(store=False, max_n=16)
+    g = seedgen.rng(81)
+    frames = g.integers(0, 256, size=(NA, 84 * 84 * 4), dtype=np.uint8)   # the actors' latest obs
+    req = seedgen.infer_requests((84, 84, 4), A, NA, 16, seed=82)
+    ids = req["actor_ids"]
+    ids_d, obs_d, rw_d, dn_d = srv.stage_requests([frames[i] for i in ids], ids, req["reward"],
+                                                  req["done"], threads=4, chunk=5)
+    u = torch.from_numpy(req["uniforms"]).cuda()
+    a1, b1 = srv.infer(ids_d, obs_d, rw_d, dn_d, u)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(obs_d.cpu().numpy(), frames[ids])
+    np.testing.assert_array_equal(ids_d.cpu().numpy(), ids)
+    np.testing.assert_array_equal(rw_d.cpu().numpy(), req["reward"])
+    np.testing.assert_array_equal(dn_d.cpu().numpy(), req["done"])
+    dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in req.items()}
+    a2, b2 = srv2.infer(dev["actor_ids"], torch.from_numpy(frames[ids]).cuda(), dev["reward"],
+                        dev["done"], u)
+    torch.cuda.synchronize()
+    assert torch.equal(a1, a2) and torch.equal(b1, b2)
+    assert torch.equal(srv.h, srv2.h) and torch.equal(srv.c, srv2.c)

@@ -457,3 +457,34 @@ def test_learner_c3_bptt_T100():
         bf16_check(gt[n], rt[n], f"{n} (T=100 BPTT)")
     _check_k2_and_adam(ospec, params, batch, hp, g)
     _deep_exact_checks("c3 T=100", g, gt, ex, rt, exact, ref)
+
+
+def test_learner_c4_u8_source_parity(tmp_path):
+    """The opt-in XF_U8 path (SEED_XF_U8=1: section 0 reads the uint8 obs and expands
+    them to bf16 rows in shared memory, no obs_bf16 pass) gives the same learner step
+    as the default path: identical logits / values and gradients within fp32
+    accumulation-order noise (run in a subprocess: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle as O, seedgen, paper_1910_06591_b200 as S
+B, T = 2, 3
+spec = S.spec_for_config("c4")
+params = seedgen.glorot_params(O.param_layout(O.spec_c4()), seed=21, bias_std=0.1)
+batch = seedgen.learner_batch((72, 96, 16), 19, B, T, seed=22, done_p=0.2, smm=True)
+L = S.Learner(spec, T, B, params, S.HParams(lam=0.95, loss_scale=1.0 / (B * T), lr=1e-3))
+L.step({k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in batch.items()})
+torch.cuda.synchronize()
+np.save(sys.argv[1], np.concatenate([L.outputs()[0].cpu().numpy().ravel(), L.grads.cpu().numpy()]))
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("0", "1"):
+        f = tmp_path / f"o{flag}.npy"
+        subprocess.run([sys.executable, "-c", code, str(f)], check=True, timeout=300,
+                       env=dict(os.environ, SEED_XF_U8=flag))
+        outs.append(np.load(f).astype(np.float64))
+    rel = np.linalg.norm(outs[1] - outs[0]) / np.linalg.norm(outs[0])
+    assert rel < 1e-3, rel
