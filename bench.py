@@ -150,9 +150,10 @@ def launch_work(cfg, T, B, A, P, names):
                 s = ns - 1 - k
         H, W, cin, cinp, ch, H2, W2 = geo[s]
         Ai, Ao = F * H * W, F * H2 * W2
-        # section 0 of the GRF net reads the uint8 obs directly; DMLab's conv reads
-        # the converted x-im2col rows (obs_bf16)
-        xin = Ai * (cin if cfg == "c4" else cinp * 2) if s == 0 else Ai * cin * 2
+        # section 0 reads the converted bf16 rows (obs_bf16: 16 planes, or DMLab's
+        # x-im2col rows); with SEED_XF_U8=1 the GRF net reads the uint8 obs directly
+        u8 = cfg == "c4" and os.environ.get("SEED_XF_U8") == "1"
+        xin = Ai * (cin if u8 else cinp * 2) if s == 0 else Ai * cin * 2
         if n == "deep_conv_fwd":
             w = (2 * Ai * ch * 9 * cin, xin + Ai * ch * 2)
         elif n == "deep_pool_fwd":     # conv read, pooled h, relu(h) + argmax written
@@ -404,6 +405,44 @@ def r2d2_leg(S, torch, iters=20):
                      "launches_per_iteration": 3}
     del R, qo, qt
     torch.cuda.empty_cache()
+    # one R2D2 learner update at the paper's shape: 64 sequences of
+    # 120 Atari frames, the first 40 burn-in, on the configs[1] network with dueling
+    # heads; CUDA-graph replays, L2 flushed between them
+    import seedgen
+    spec = S.spec_for_config("c2")
+    Bq, bi, Tq = 64, 40, 79
+    params = seedgen.glorot_params(S.net_param_layout(spec), seed=0)
+    Lq = S.R2d2Learner(spec, bi, Tq, Bq, params, S.R2d2HParams(loss_scale=1.0 / (Bq * Tq)))
+    full = seedgen.learner_batch(spec.obs_shape, spec.num_actions, Bq, bi + Tq, seed=5)
+    L1 = bi + Tq + 1
+    cut = lambda a, b: {k: torch.from_numpy(np.ascontiguousarray(v[:, a:b] if v.ndim >= 2 and v.shape[1] == L1
+                                                                  else v)).cuda() for k, v in full.items()}
+    burn, train = cut(0, bi), cut(bi, L1)
+    w = torch.rand(Bq, device="cuda", generator=g)
+    for _ in range(3):
+        Lq.step(train, burn=burn, is_weights=w)
+    sq = torch.cuda.Stream()
+    sq.wait_stream(torch.cuda.current_stream())
+    gq = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gq, stream=sq):
+        Lq.step(train, burn=burn, is_weights=w, stream=sq)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    tot = 0.0
+    for _ in range(iters):
+        flush.add_(1)
+        e0.record()
+        gq.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    ms = tot / iters
+    out["learner_step"] = {"net": "configs[1] Atari net + LSTM256, dueling heads", "B": Bq,
+                           "burn_in": bi, "trained_steps": Tq, "ms_per_update": round(ms, 4),
+                           "updates_per_s": round(1e3 / ms, 1),
+                           "trained_frames_per_s": round(Bq * Tq * 4 / (ms / 1e3), 1)}
+    del Lq, gq, flush
+    torch.cuda.empty_cache()
     return out
 
 
@@ -546,7 +585,7 @@ def traced_graph(S, torch, L, spec, dev, comm, maxe=160):
             C.byref(spec_c), L.T, L.B, C.byref(cb), C.byref(ts), C.byref(hp_c),
             comm.handle if comm else None, C.c_void_p(L.ws.data_ptr()), L.ws.numel(),
             C.c_void_p(L.metrics.data_ptr()), C.c_void_p(stream.cuda_stream), ev_arr, maxe,
-            names, C.byref(n_ev), C.byref(n_launch))
+            names, C.byref(n_ev), C.byref(n_launch), None)
         Lb.check(st, "seed_learner_step_traced")
 
     s = torch.cuda.Stream()

@@ -220,14 +220,16 @@ seed_status seed_learner_step_ex(const seed_net_spec* spec, int T, int B,
  * split-K GEMM + its fixed-order reduction).  names_out (host, nullable,
  * max_events entries) receives static phase names (names_out[i] ends at
  * events[i]); *n_events_out (host) the number of events recorded and
- * *n_launches_out (host, nullable) the number of kernels the step launched. */
+ * *n_launches_out (host, nullable) the number of kernels the step launched;
+ * launch_counts_out (host, nullable, max_events entries) the number of kernels of
+ * each phase (launch_counts_out[i] for the phase ending at events[i]). */
 seed_status seed_learner_step_traced(const seed_net_spec* spec, int T, int B,
                                      const seed_batch* batch, const seed_train_state* state,
                                      const seed_hparams* hp, seed_comm* comm,
                                      void* workspace, size_t ws_bytes, float* metrics,
                                      void* stream, void** events, int max_events,
                                      const char** names_out, int* n_events_out,
-                                     int* n_launches_out);
+                                     int* n_launches_out, int* launch_counts_out);
 /* Views into a workspace after seed_learner_step (for tests / metrics):
  * logits [B][T+1][A], values [B][T+1], vs [B][T], pg_adv [B][T] (fp32). */
 seed_status seed_learner_outputs(const seed_net_spec* spec, int T, int B, void* workspace,
@@ -426,6 +428,43 @@ seed_status seed_r2d2_targets(int T, int B, int A, int n, const float* q_online,
                               float rescale_eps, const float* is_weights, float loss_scale,
                               float* y, float* delta, float* priority, float* dq,
                               float* loss_part, void* stream);
+
+/* seed_r2d2_learner_step — one R2D2 learner update:
+ *   burn-in: the sequences' stored (h0, c0) warmed over their first burn_in steps
+ *      by the online and by the target network, with no gradient;
+ *   trained window [B][T+1]: online and target forward passes, dueling heads read
+ *     from the net's A+1 outputs (Q(a) = V + A_a - mean_j A_j; reading C35),
+ *     seed_r2d2_targets (n-step double Q, value rescaling, priorities -> priorities_out,
+ *     IS-weighted squared-TD gradient), the dueling / heads / core / torso backward,
+ *     the optional DP allreduce (comm), global-norm clip (80) and Adam
+ *     (lr 1e-4, eps 1e-3) of the online parameters; version += 1 if finite.
+ * The target parameters (target_params fp32 [P] + target_lowp image) are read only;
+ * the caller copies the online parameters into them every 2500 updates.
+ * burn: [B][burn_in] frames (obs, prev_action, reward, done, h0 / c0 = the stored
+ *   state at the sequence start); NULL iff burn_in == 0 (then train's h0 / c0).
+ * train: [B][T+1] frames (obs, action, prev_action, reward, done); trained step t
+ *   uses reward[t+1] and discount gamma (1 - done[t+1]) (C5).
+ * is_weights: nullable [B] importance weights (seed_replay_sample).
+ * metrics: device float[8] as seed_learner_step (loss in [0] and [1]).
+ * Supports the conv nets (not SEED_NET_MLP). */
+typedef struct {
+  float discount;        /* gamma (.997)                         */
+  int n;                 /* n-step (5)                           */
+  float eta;             /* priority mixing (.9)                 */
+  float rescale_eps;     /* value rescaling epsilon (1e-3)       */
+  float loss_scale;      /* e.g. 1/(N*B*T)                              */
+  float lr, beta1, beta2, eps;   /* Adam                                */
+  float max_grad_norm;   /* 80                                   */
+} seed_r2d2_hparams;
+seed_status seed_r2d2_workspace_size(const seed_net_spec* spec, int burn_in, int T, int B,
+                                     size_t* bytes_out);
+seed_status seed_r2d2_learner_step(const seed_net_spec* spec, int burn_in, int T, int B,
+                                   const seed_batch* burn, const seed_batch* train,
+                                   const seed_train_state* online, const float* target_params,
+                                   const void* target_lowp, const float* is_weights,
+                                   const seed_r2d2_hparams* hp, seed_comm* comm, seed_exec* exec,
+                                   void* workspace, size_t ws_bytes, float* priorities_out,
+                                   float* metrics, void* stream);
 
 /* Learner-resident prioritized sequence replay ("keep the replay buffer on
  * the learner"; priority exponent alpha P:602, importance exponent beta P:603;

@@ -820,3 +820,56 @@ def replay_sample(priorities, uniforms, alpha=0.9, beta=0.6, size=None):
     P = pa[idx] / c[-1]
     w = (N * P) ** (-beta)
     return idx, w / w.max()
+
+
+def dueling_q(logits, values):
+    """Dueling heads ("dueling heads"): Q(a) = V + A_a - mean_j A_j, with the
+    net's A+1 outputs read as A advantages and 1 value (reading C35)."""
+    adv = np.asarray(logits, np.float64)
+    return np.asarray(values, np.float64)[..., None] + adv - adv.mean(axis=-1, keepdims=True)
+
+
+def r2d2_warm_state(spec, P, burn, emu=False):
+    """Burn-in: run the network over the sequence's first burn_in steps from
+    the stored state; the state entering the trained window (no gradient)."""
+    _, _, cache = network_forward(spec, P, burn, emu)
+    B, T1 = cache["B"], cache["T1"]
+    H = cache["H"].reshape(B, T1, -1)
+    return H[:, -1].copy(), cache["lstm"]["c"][:, -1].copy()
+
+
+def r2d2_learner_step(spec, params, target_params, m, v, step, burn, train, is_weights, hp,
+                      emu=False):
+    """One R2D2 learner update: burn-in of the
+    stored state by the online and the target network (no gradient), forward of the
+    trained window [B][T+1] by both, dueling Q, n-step double-Q targets with value
+    rescaling and priorities (r2d2_targets; trained step t uses reward[t+1] and
+    gamma (1 - done[t+1]), C5), the IS-weighted squared-TD loss, its gradient through
+    the dueling heads and the online network, clip + Adam.
+    hp: dict(discount, n, eta, rescale_eps, loss_scale, lr, beta1, beta2, eps,
+    max_grad_norm).  burn: None when burn_in = 0 (train's h0 / c0 are used)."""
+    P = unflatten(spec, params)
+    Pt = unflatten(spec, target_params)
+    tr_o, tr_t = dict(train), dict(train)
+    if burn is not None:
+        tr_o["h0"], tr_o["c0"] = r2d2_warm_state(spec, P, burn, emu)
+        tr_t["h0"], tr_t["c0"] = r2d2_warm_state(spec, Pt, burn, emu)
+    lo, vo, cache = network_forward(spec, P, tr_o, emu)
+    lt, vt, _ = network_forward(spec, Pt, tr_t, emu)
+    qo, qt = dueling_q(lo, vo), dueling_q(lt, vt)
+    rew = np.asarray(train["reward"], np.float64)[:, 1:]
+    disc = hp["discount"] * (1.0 - np.asarray(train["done"], np.float64)[:, 1:])
+    y, delta, prio = r2d2_targets(qo, qt, train["action"], rew, disc, hp["n"], hp["eta"],
+                                  hp["rescale_eps"])
+    w = np.ones(qo.shape[0]) if is_weights is None else np.asarray(is_weights, np.float64)
+    loss, dq = r2d2_loss_grad(qo, train["action"], y, w, hp["loss_scale"])
+    dA = dq - dq.sum(axis=-1, keepdims=True) / dq.shape[-1]
+    dV = dq.sum(axis=-1)
+    grads = network_backward(spec, P, tr_o, cache, dA, dV)
+    gflat = flatten(spec, grads)
+    p2, m2, v2, step2, norm, applied = clip_adam(np.asarray(params, np.float64), gflat,
+                                                 np.asarray(m, np.float64),
+                                                 np.asarray(v, np.float64), step, hp)
+    return dict(q_online=qo, q_target=qt, y=y, delta=delta, priorities=prio, loss=loss,
+                grads=gflat, params=p2, m=m2, v=v2, step=step2, grad_norm=norm, applied=applied,
+                warm=(tr_o.get("h0"), tr_o.get("c0")))

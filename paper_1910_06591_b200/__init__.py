@@ -6,6 +6,7 @@ used for device memory, streams and process groups.
 """
 from ._lib import SeedError, load  # noqa: F401
 from .api import (  # noqa: F401
-    HParams, Learner, InferenceServer, NetSpec, ParamSnapshot, PrioritizedReplay, r2d2_targets, debug_gemm, net_param_count, net_param_layout,
+    HParams, Learner, InferenceServer, NetSpec, ParamSnapshot, PrioritizedReplay, r2d2_targets,
+    R2d2HParams, R2d2Learner, debug_gemm, net_param_count, net_param_layout,
     spec_for_config, vtrace, Comm,
 )

@@ -51,6 +51,12 @@ class Replay(C.Structure):
         [(n, c_void_p) for n in ("tree", "max_priority", "size", "gen", "ticket")]
 
 
+class R2d2HParams(C.Structure):
+    _fields_ = [("discount", c_float), ("n", c_int), ("eta", c_float), ("rescale_eps", c_float),
+                ("loss_scale", c_float), ("lr", c_float), ("beta1", c_float), ("beta2", c_float),
+                ("eps", c_float), ("max_grad_norm", c_float)]
+
+
 class ParamSnapshot(C.Structure):
     _fields_ = [("slots", c_void_p * 3), ("state", c_void_p), ("version", c_void_p)]
 
@@ -82,6 +88,11 @@ _SIGS = {
                                    c_int, c_void_p]),
     "seed_r2d2_targets": (c_int, [c_int, c_int, c_int, c_int] + [c_void_p] * 5 +
                           [c_float, c_float, c_void_p, c_float] + [c_void_p] * 6),
+    "seed_r2d2_workspace_size": (c_int, [P(NetSpec), c_int, c_int, c_int, P(c_size_t)]),
+    "seed_r2d2_learner_step": (c_int, [P(NetSpec), c_int, c_int, c_int, c_void_p, P(Batch),
+                                       P(TrainState), c_void_p, c_void_p, c_void_p,
+                                       P(R2d2HParams), c_void_p, c_void_p, c_void_p, c_size_t,
+                                       c_void_p, c_void_p, c_void_p]),
     "seed_replay_check": (c_int, [P(Replay)]),
     "seed_replay_insert": (c_int, [P(Replay), c_int, c_float, c_void_p, c_void_p, c_void_p]),
     "seed_replay_update": (c_int, [P(Replay), c_int, c_void_p, c_void_p, c_void_p, c_float,
@@ -93,7 +104,7 @@ _SIGS = {
     "seed_learner_step_traced": (c_int, [P(NetSpec), c_int, c_int, P(Batch), P(TrainState),
                                          P(HParams), c_void_p, c_void_p, c_size_t, c_void_p,
                                          c_void_p, P(c_void_p), c_int, P(C.c_char_p), P(c_int),
-                                         P(c_int)]),
+                                         P(c_int), c_void_p]),
     "seed_learner_outputs": (c_int, [P(NetSpec), c_int, c_int, c_void_p, P(c_void_p),
                                      P(c_void_p), P(c_void_p), P(c_void_p)]),
     "seed_learner_debug_buffer": (c_int, [P(NetSpec), c_int, c_int, c_void_p, C.c_char_p,

@@ -442,6 +442,79 @@ class Learner:
                 view(ptrs[3], (B, T1 - 1)))
 
 
+@dataclass
+class R2d2HParams:
+    """R2D2 hyper-parameters (P:586-622 table r2d2_params)."""
+    discount: float = 0.997
+    n: int = 5
+    eta: float = 0.9
+    rescale_eps: float = 1e-3
+    loss_scale: float = 1.0
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-3
+    max_grad_norm: float = 80.0
+
+    def c(self):
+        return L.R2d2HParams(self.discount, int(self.n), self.eta, self.rescale_eps,
+                             self.loss_scale, self.lr, self.beta1, self.beta2, self.eps,
+                             self.max_grad_norm)
+
+
+class R2d2Learner(Learner):
+    """Online network train state (Learner) + the target network's parameters
+    (fp32 + bf16 image) and the workspace of seed_r2d2_learner_step."""
+
+    def __init__(self, spec, burn_in, T, B, params, hp=None, comm=None, device="cuda"):
+        super().__init__(spec, T, B, params, HParams(), comm=comm, device=device)
+        self.burn_in = burn_in
+        self.r2hp = hp or R2d2HParams()
+        self.target_params = self.params.clone()
+        self.target_lowp = self.lowp.clone()
+        nb = C.c_size_t()
+        L.check(L.load().seed_r2d2_workspace_size(C.byref(spec.c()), burn_in, T, B, C.byref(nb)),
+                "seed_r2d2_workspace_size")
+        self.ws = torch.empty(max(nb.value, 16), dtype=torch.uint8, device=device)
+        self.priorities = torch.zeros(B, dtype=torch.float32, device=device)
+
+    def sync_target(self, stream=None):
+        """The target network takes the online parameters (every 2500 updates)."""
+        self.target_params.copy_(self.params)
+        self.target_lowp.copy_(self.lowp)
+
+    def step(self, train, burn=None, is_weights=None, stream=None):
+        """One seed_r2d2_learner_step; returns (metrics[8], priorities[B])."""
+        ct = self._batch_r2d2(train, self.T + 1, need_h0=self.burn_in == 0)
+        cb = self._batch_r2d2(burn, self.burn_in, need_h0=True) if self.burn_in > 0 else None
+        ts = self._train_state()
+        hp = self.r2hp.c()
+        if is_weights is not None:
+            _need(is_weights, torch.float32, "is_weights")
+        st = L.load().seed_r2d2_learner_step(
+            C.byref(self._spec_c), self.burn_in, self.T, self.B,
+            C.byref(cb) if cb is not None else None, C.byref(ct), C.byref(ts),
+            _ptr(self.target_params), _ptr(self.target_lowp), _ptr(is_weights), C.byref(hp),
+            self.comm.handle if self.comm else None, self._exec, _ptr(self.ws), self.ws.numel(),
+            _ptr(self.priorities), _ptr(self.metrics), _stream(stream))
+        L.check(st, "seed_r2d2_learner_step")
+        return self.metrics, self.priorities
+
+    def _batch_r2d2(self, b, T1, need_h0):
+        _need(b["obs"], self.spec.obs_dtype, "obs")
+        if tuple(b["obs"].shape[:2]) != (self.B, T1):
+            raise ValueError(f"obs must be [B][{T1}][...]")
+        for k, dt in (("action", torch.int32), ("prev_action", torch.int32),
+                      ("reward", torch.float32), ("done", torch.uint8)):
+            if k in b:
+                _need(b[k], dt, k)
+        if need_h0:
+            _need(b["h0"], torch.float32, "h0")
+            _need(b["c0"], torch.float32, "c0")
+        return L.Batch(*(_ptr(b.get(k)) for k in ("obs", "action", "prev_action", "reward", "done",
+                                                  "behaviour_logp", "h0", "c0")))
+
+
 class ParamSnapshot:
     """Device triple buffer for versioned parameter publication (include/seed.h
     seed_param_*): one producer (Learner.publish) and one consumer

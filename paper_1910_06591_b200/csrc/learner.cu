@@ -106,6 +106,7 @@ static int dp_buckets() {
 struct Trace {
   void** events = nullptr;
   const char** names = nullptr;
+  int* counts = nullptr;   // kernel launches of each phase (nullable)
   int max = 0, n = 0, launches = 0;
   bool capturing = false;
 };
@@ -170,6 +171,7 @@ struct StepCtx {
     if (tr->events && tr->n < tr->max) {
       trace_record(tr, tr->events[tr->n], st);
       if (tr->names) tr->names[tr->n] = name;
+      if (tr->counts) tr->counts[tr->n] = k;
       tr->n++;
     }
   }
@@ -683,10 +685,11 @@ extern "C" seed_status seed_learner_step_traced(const seed_net_spec* spec, int T
                                                 void* ws, size_t ws_bytes, float* metrics,
                                                 void* stream, void** events, int max_events,
                                                 const char** names_out, int* n_events_out,
-                                                int* n_launches_out) {
+                                                int* n_launches_out, int* launch_counts_out) {
   seed::Trace tr;
   tr.events = events;
   tr.names = names_out;
+  tr.counts = launch_counts_out;
   tr.max = events ? max_events : 0;
   const seed_status r = seed::learner_step_impl(spec, T, B, batch, state, hp, comm, nullptr, ws,
                                                 ws_bytes, metrics, stream, &tr);
@@ -769,4 +772,314 @@ extern "C" seed_status seed_learner_debug_buffer(const seed_net_spec* spec, int 
       }
   }
   return SEED_E_ARG;
+}
+
+// ============================================================================
+// R2D2 learner step (hyper-parameters
+// P:586-622): burn-in, online / target forward passes, n-step double-Q targets
+// with value rescaling and priorities (seed_r2d2_targets), dueling heads, the
+// importance-weighted squared-TD backward, clip (80) + Adam.  The network is the
+// configured one (seed_net_spec) with dueling heads read from its A+1 outputs:
+// Q(a) = V + A_a - mean_j A_j (C35).
+// ============================================================================
+extern "C" seed_status seed_r2d2_targets(int T, int B, int A, int n, const float* q_online,
+                                         const float* q_target, const int32_t* actions,
+                                         const float* rewards, const float* discounts, float eta,
+                                         float rescale_eps, const float* is_weights, float loss_scale,
+                                         float* y, float* delta, float* priority, float* dq,
+                                         float* loss_part, void* stream);
+
+namespace seed {
+
+// trained step t of a [B][T+1] window uses reward[t+1] and gamma (1 - done[t+1]) (C5)
+__global__ void r2d2_rewards_kernel(int B, int T, float gamma, const float* __restrict__ reward,
+                                    const uint8_t* __restrict__ done, float* __restrict__ r,
+                                    float* __restrict__ disc) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * T) return;
+  const int b = i / T, t = i % T;
+  const int s = b * (T + 1) + t + 1;
+  r[i] = reward[s];
+  disc[i] = done[s] ? 0.f : gamma;
+}
+
+// dueling combine: Q[f][a] = V[f] + A[f][a] - mean_j A[f][j]  (warp per row)
+__global__ void dueling_q_kernel(int F, int A, const float* __restrict__ adv, const float* __restrict__ val,
+                                 float* __restrict__ q) {
+  pdl_wait();
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (f >= F) return;
+  float s = 0.f;
+  for (int j = lane; j < A; j += 32) s += adv[(size_t)f * A + j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / (float)A, v = val[f];
+  for (int j = lane; j < A; j += 32) q[(size_t)f * A + j] = v + adv[(size_t)f * A + j] - mean;
+}
+
+// its backward: dV = sum_a dQ_a, dA_j = dQ_j - (1/A) sum_a dQ_a
+__global__ void dueling_bwd_kernel(int F, int A, const float* __restrict__ dq, float* __restrict__ dadv,
+                                   float* __restrict__ dval) {
+  pdl_wait();
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (f >= F) return;
+  float s = 0.f;
+  for (int j = lane; j < A; j += 32) s += dq[(size_t)f * A + j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  for (int j = lane; j < A; j += 32) dadv[(size_t)f * A + j] = dq[(size_t)f * A + j] - s / (float)A;
+  if (lane == 0) dval[f] = s;
+}
+
+// last LSTM state of each burn-in window -> the trained window's initial state
+__global__ void last_state_kernel(int B, int T1, int U, const float* __restrict__ H,
+                                  const float* __restrict__ C, float* __restrict__ h0,
+                                  float* __restrict__ c0) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * U) return;
+  const int b = i / U, u = i % U;
+  const size_t r = ((size_t)b * T1 + T1 - 1) * U + u;
+  h0[i] = H[r];
+  c0[i] = C[r];
+}
+
+// R2D2 loss partials in the clip + Adam kernel's [B][4] layout: {loss_b, 0, 0, nonfinite}
+__global__ void r2d2_loss_part_kernel(int B, const float* __restrict__ loss, float* __restrict__ part) {
+  pdl_wait();
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const float l = loss[b];
+  part[b * 4 + 0] = l;
+  part[b * 4 + 1] = 0.f;
+  part[b * 4 + 2] = 0.f;
+  part[b * 4 + 3] = isfinite(l) ? 0.f : 1.f;
+}
+
+// workspace: [burn-in online | burn-in target | trained online | trained target |
+//             R2D2 extras]
+struct R2d2Ws {
+  LearnerWs wbo, wbt, wto, wtt;
+  size_t obo, obt, oto, ott;
+  size_t qo, qt, adv, val, y, delta, dq, dadv, dval, loss, lpart, r, disc, h0o, c0o, h0t, c0t;
+  size_t total;
+};
+
+static seed_status make_r2d2_ws(const NetPlan& p, int burn_in, int T, int B, R2d2Ws* w) {
+  size_t cur = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = cur;
+    cur = align_up(cur + bytes, 256);
+    return at;
+  };
+  if (burn_in > 0) {
+    SEED_TRY(make_learner_ws(p, burn_in - 1, B, &w->wbo));
+    w->wbt = w->wbo;
+    w->obo = take(w->wbo.total);
+    w->obt = take(w->wbt.total);
+  }
+  SEED_TRY(make_learner_ws(p, T, B, &w->wto));
+  w->wtt = w->wto;
+  w->oto = take(w->wto.total);
+  w->ott = take(w->wtt.total);
+  const size_t F = (size_t)B * (T + 1), A = p.A, U = p.U;
+  w->qo = take(F * A * 4); w->qt = take(F * A * 4);
+  w->adv = take(F * A * 4); w->val = take(F * 4);
+  w->y = take((size_t)B * T * 4); w->delta = take((size_t)B * T * 4);
+  w->dq = take(F * A * 4); w->dadv = take(F * A * 4); w->dval = take(F * 4);
+  w->loss = take((size_t)B * 4); w->lpart = take((size_t)B * 16);
+  w->r = take((size_t)B * T * 4); w->disc = take((size_t)B * T * 4);
+  w->h0o = take((size_t)B * U * 4); w->c0o = take((size_t)B * U * 4);
+  w->h0t = take((size_t)B * U * 4); w->c0t = take((size_t)B * U * 4);
+  w->total = cur;
+  return SEED_OK;
+}
+
+// torso + core forward of one [B][T+1] window into a workspace (no loss): the LSTM
+// outputs H / C rows, and (heads) A advantages + 1 value per row
+static seed_status r2d2_forward(const NetPlan& p, const LearnerWs& lw, uint8_t* wsb, int T, int B,
+                                const seed_batch* bt, const bf16* lowp, const float* params,
+                                cudaStream_t st) {
+  StepCtx c;
+  c.p = &p;
+  c.w = lw;
+  c.ws = wsb;
+  c.g = Geo{p.H, p.W, p.C, p.oh1, p.ow1, p.oh2, p.ow2, p.fc_in, p.Kx, p.Kxp,
+            FastDiv((uint32_t)(p.oh1 * p.ow1)), FastDiv((uint32_t)p.ow1),
+            FastDiv((uint32_t)(p.oh2 * p.ow2)), FastDiv((uint32_t)p.ow2)};
+  c.st = st;
+  c.aux = st;
+  SEED_CUDA_TRY(cudaMemsetAsync(c.tickets(), 0, 64 + GEMM_COUNTERS * 4, st));
+  {
+    const int E = p.Kxp - 256;
+    const int64_t n = (int64_t)lw.F * E;
+    SEED_TRY(launch_k(core_extras_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, lw.F, p.A,
+                      p.Kxp, bt->prev_action, bt->reward, bt->done, c.at<bf16>(lw.X)));
+  }
+  if (p.nsec > 0) SEED_TRY(deep_forward(c, bt, lowp, params, st));
+  else SEED_TRY(shallow_forward(c, bt, lowp, params, st));
+  return core_forward(c, bt, lowp, params, st);
+}
+
+static seed_status r2d2_step_impl(const seed_net_spec* spec, int burn_in, int T, int B,
+                                  const seed_batch* burn, const seed_batch* train,
+                                  const seed_train_state* state, const float* tparams,
+                                  const void* tlowp, const float* is_weights,
+                                  const seed_r2d2_hparams* hp, seed_comm* comm, const seed_exec* ex,
+                                  void* ws, size_t ws_bytes, float* prio_out, float* metrics,
+                                  void* stream) {
+  NetPlan p;
+  SEED_TRY(make_net_plan(spec, &p));
+  if (p.kind == SEED_NET_MLP || !learner_supported(p)) return SEED_E_UNSUPPORTED;
+  if (T < 1 || T > 256 || B < 1 || B > 1024 || burn_in < 0 || burn_in > 256) return SEED_E_SHAPE;
+  if (!train || !state || !hp || !ws || !metrics || !prio_out || !tparams || !tlowp) return SEED_E_ARG;
+  if (burn_in > 0 && (!burn || !burn->obs || !burn->prev_action || !burn->reward || !burn->done ||
+                      !burn->h0 || !burn->c0 || !aligned16(burn->obs)))
+    return SEED_E_ARG;
+  if (!train->obs || !train->action || !train->prev_action || !train->reward || !train->done ||
+      !aligned16(train->obs) || (burn_in == 0 && (!train->h0 || !train->c0)))
+    return SEED_E_ARG;
+  if (!state->params || !state->grads || !state->adam_m || !state->adam_v || !state->step ||
+      !state->params_lowp || !aligned16(state->params) || !aligned16(state->grads) ||
+      !aligned16(state->adam_m) || !aligned16(state->adam_v) || !aligned16(state->params_lowp) ||
+      !aligned16(tlowp) || !aligned16(ws))
+    return SEED_E_ARG;
+  if (!(hp->max_grad_norm > 0.f) || hp->n < 1 || !(hp->rescale_eps > 0.f) || !(hp->eta >= 0.f && hp->eta <= 1.f))
+    return SEED_E_ARG;
+  R2d2Ws w;
+  SEED_TRY(make_r2d2_ws(p, burn_in, T, B, &w));
+  if (ws_bytes < w.total) return SEED_E_WORKSPACE;
+  uint8_t* base = (uint8_t*)ws;
+  auto at = [&](size_t off) { return base + off; };
+  cudaStream_t st = (cudaStream_t)stream;
+  const bf16* lowp = (const bf16*)state->params_lowp;
+  const bf16* tl = (const bf16*)tlowp;
+  const float* params = state->params;
+  float* grads = state->grads;
+  const int U = p.U, A = p.A, F = B * (T + 1);
+  // 1. burn-in (no gradient): the stored state warmed over the first burn_in steps,
+  //    by the online and by the target network
+  seed_batch to = *train, tt = *train;
+  if (burn_in > 0) {
+    SEED_TRY(r2d2_forward(p, w.wbo, at(w.obo), burn_in - 1, B, burn, lowp, params, st));
+    SEED_TRY(r2d2_forward(p, w.wbt, at(w.obt), burn_in - 1, B, burn, tl, tparams, st));
+    const int n = B * U;
+    SEED_TRY(launch_k(last_state_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, st, B, burn_in, U,
+                      (const float*)at(w.obo + w.wbo.H), (const float*)at(w.obo + w.wbo.Cst),
+                      (float*)at(w.h0o), (float*)at(w.c0o)));
+    SEED_TRY(launch_k(last_state_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, st, B, burn_in, U,
+                      (const float*)at(w.obt + w.wbt.H), (const float*)at(w.obt + w.wbt.Cst),
+                      (float*)at(w.h0t), (float*)at(w.c0t)));
+    to.h0 = (const float*)at(w.h0o); to.c0 = (const float*)at(w.c0o);
+    tt.h0 = (const float*)at(w.h0t); tt.c0 = (const float*)at(w.c0t);
+  }
+  // 2. trained window: online and target forward, dueling heads
+  SEED_TRY(r2d2_forward(p, w.wto, at(w.oto), T, B, &to, lowp, params, st));
+  SEED_TRY(r2d2_forward(p, w.wtt, at(w.ott), T, B, &tt, tl, tparams, st));
+  const float* Ho = (const float*)at(w.oto + w.wto.H);
+  const float* Ht = (const float*)at(w.ott + w.wtt.H);
+  const int64_t hw = p.t[p.i_hw].off, hb = p.t[p.i_hb].off;
+  const unsigned rows_blocks = (unsigned)ceil_div(F * 32, 256);
+  SEED_TRY(launch_dense_fwd(F, U, A + 1, Ho, params + hw, params + hb, (float*)at(w.adv), A,
+                            (float*)at(w.val), 0, st));
+  SEED_TRY(launch_k(dueling_q_kernel, dim3(rows_blocks), dim3(256), 0, st, F, A, (const float*)at(w.adv),
+                    (const float*)at(w.val), (float*)at(w.qo)));
+  SEED_TRY(launch_dense_fwd(F, U, A + 1, Ht, tparams + hw, tparams + hb, (float*)at(w.adv), A,
+                            (float*)at(w.val), 0, st));
+  SEED_TRY(launch_k(dueling_q_kernel, dim3(rows_blocks), dim3(256), 0, st, F, A, (const float*)at(w.adv),
+                    (const float*)at(w.val), (float*)at(w.qt)));
+  // 3. targets, TD errors, priorities, IS-weighted loss gradient
+  SEED_TRY(launch_k(r2d2_rewards_kernel, dim3((unsigned)ceil_div(B * T, 256)), dim3(256), 0, st, B, T,
+                    hp->discount, train->reward, train->done, (float*)at(w.r), (float*)at(w.disc)));
+  SEED_TRY(seed_r2d2_targets(T, B, A, hp->n, (const float*)at(w.qo), (const float*)at(w.qt),
+                             train->action, (const float*)at(w.r), (const float*)at(w.disc), hp->eta,
+                             hp->rescale_eps, is_weights, hp->loss_scale, (float*)at(w.y),
+                             (float*)at(w.delta), prio_out, (float*)at(w.dq), (float*)at(w.loss), st));
+  // 4. dueling + heads backward (the heads forward of the online net is recomputed
+  //    into adv / val above only for the target; H is the online core output)
+  SEED_TRY(launch_k(dueling_bwd_kernel, dim3(rows_blocks), dim3(256), 0, st, F, A, (const float*)at(w.dq),
+                    (float*)at(w.dadv), (float*)at(w.dval)));
+  dense_wgrad_f32<<<dim3(A + 1, ceil_div(U + 1, 32)), 256, 0, st>>>(
+      F, U, A + 1, (const float*)at(w.dadv), A, (const float*)at(w.dval), Ho, grads + hw, grads + hb);
+  SEED_TRY(launch_dense_dgrad(F, U, A + 1, (const float*)at(w.dadv), A, (const float*)at(w.dval),
+                              params + hw, nullptr, (float*)at(w.oto + w.wto.dH), st));
+  // 5. core + torso backward on the online workspace, then the optimizer
+  StepCtx c;
+  c.p = &p;
+  c.w = w.wto;
+  c.ws = at(w.oto);
+  c.g = Geo{p.H, p.W, p.C, p.oh1, p.ow1, p.oh2, p.ow2, p.fc_in, p.Kx, p.Kxp,
+            FastDiv((uint32_t)(p.oh1 * p.ow1)), FastDiv((uint32_t)p.ow1),
+            FastDiv((uint32_t)(p.oh2 * p.ow2)), FastDiv((uint32_t)p.ow2)};
+  c.st = st;
+  SEED_TRY(aux_stream(ex, st, false, &c.aux, c.fev));
+  const bool dp = comm && comm_world(comm) > 1;
+  if (dp) {
+    c.comm = comm;
+    SEED_TRY(comm_side(comm, &c.side, &c.side2, c.ev));
+  }
+  SEED_TRY(core_backward(c, &to, lowp, params, grads, st));
+  if (p.nsec > 0) SEED_TRY(deep_backward(c, &to, lowp, params, grads, st));
+  else SEED_TRY(shallow_backward(c, &to, lowp, params, grads, st));
+  SEED_TRY(c.edge(c.aux, st));
+  if (dp) {
+    SEED_TRY(c.bucket(grads, dp_buckets() >= 2 ? p.t[p.i_fcw].off : p.P, st));
+    SEED_CUDA_TRY(cudaEventRecord(c.ev[3], c.side));
+    SEED_CUDA_TRY(cudaStreamWaitEvent(st, c.ev[3], 0));
+    if (c.side2) {
+      SEED_CUDA_TRY(cudaEventRecord(c.ev[4], c.side2));
+      SEED_CUDA_TRY(cudaStreamWaitEvent(st, c.ev[4], 0));
+    }
+  }
+  SEED_TRY(launch_k(r2d2_loss_part_kernel, dim3((unsigned)ceil_div(B, 256)), dim3(256), 0, st, B,
+                    (const float*)at(w.loss), (float*)at(w.lpart)));
+  double* npart = c.at<double>(c.w.norm_part);
+  NormArgs na{};
+  na.g = grads; na.P = p.P; na.part = npart;
+  na.coef = reinterpret_cast<float*>(npart + NORM_BLOCKS); na.norm = npart + NORM_BLOCKS + 2;
+  na.ticket = c.tickets() + 1;
+  na.step = state->step; na.step_in = c.at<int64_t>(c.w.step_in);
+  na.beta1 = hp->beta1; na.beta2 = hp->beta2; na.max_norm = hp->max_grad_norm;
+  SEED_TRY(launch_k(grad_norm_kernel, dim3(NORM_BLOCKS), dim3(256), 0, st, na));
+  AdamArgs aa{};
+  aa.P = p.P; aa.params = state->params; aa.grads = grads; aa.m = state->adam_m;
+  aa.v = state->adam_v; aa.step = state->step; aa.step_in = c.at<int64_t>(c.w.step_in);
+  aa.coef = na.coef; aa.norm = na.norm;
+  aa.lr = hp->lr; aa.beta1 = hp->beta1; aa.beta2 = hp->beta2; aa.eps = hp->eps;
+  aa.max_norm = hp->max_grad_norm; aa.loss_part = (const float*)at(w.lpart); aa.B = B;
+  aa.metrics = metrics;
+  aa.lowp = (bf16*)state->params_lowp;
+  const bool fused_lowp = p.nimg <= 8;
+  aa.nimg = fused_lowp ? p.nimg : 0;
+  for (int k = 0; k < aa.nimg; ++k) aa.img[k] = p.img[k];
+  SEED_TRY(launch_clip_adam(aa, st));
+  if (!fused_lowp) SEED_TRY(refresh_lowp(p, state->params, state->params_lowp, st));
+  return last_launch();
+}
+
+}  // namespace seed
+
+extern "C" seed_status seed_r2d2_workspace_size(const seed_net_spec* spec, int burn_in, int T, int B,
+                                                size_t* bytes) {
+  if (!bytes) return SEED_E_ARG;
+  NetPlan p;
+  SEED_TRY(make_net_plan(spec, &p));
+  if (p.kind == SEED_NET_MLP || !learner_supported(p)) return SEED_E_UNSUPPORTED;
+  if (T < 1 || T > 256 || B < 1 || B > 1024 || burn_in < 0 || burn_in > 256) return SEED_E_SHAPE;
+  R2d2Ws w;
+  SEED_TRY(make_r2d2_ws(p, burn_in, T, B, &w));
+  *bytes = w.total;
+  return SEED_OK;
+}
+
+extern "C" seed_status seed_r2d2_learner_step(const seed_net_spec* spec, int burn_in, int T, int B,
+                                              const seed_batch* burn, const seed_batch* train,
+                                              const seed_train_state* online, const float* target_params,
+                                              const void* target_lowp, const float* is_weights,
+                                              const seed_r2d2_hparams* hp, seed_comm* comm,
+                                              seed_exec* exec, void* ws, size_t ws_bytes,
+                                              float* priorities_out, float* metrics, void* stream) {
+  return seed::r2d2_step_impl(spec, burn_in, T, B, burn, train, online, target_params, target_lowp,
+                              is_weights, hp, comm, exec, ws, ws_bytes, priorities_out, metrics, stream);
 }

@@ -48,7 +48,7 @@ def traced(stream):
         C.byref(spec_c), T, B, C.byref(cb), C.byref(ts), C.byref(hp_c), None,
         C.c_void_p(learner.ws.data_ptr()), learner.ws.numel(),
         C.c_void_p(learner.metrics.data_ptr()), C.c_void_p(stream.cuda_stream), ev_arr, MAXE,
-        names, C.byref(n_ev), C.byref(n_launch)), "traced")
+        names, C.byref(n_ev), C.byref(n_launch), None), "traced")
 
 
 s = torch.cuda.Stream()

@@ -652,3 +652,41 @@ def test_replay_probabilities_golden_S313_and_sampling():
     obs = np.bincount(idx, minlength=40)
     exp = O.replay_probabilities(pr, 0.9) * 100000
     assert chisquare(obs, exp).pvalue > 1e-3
+
+
+def test_r2d2_learner_step_finite_differences():
+    """The R2D2 learner-step oracle's gradient = central differences of its loss with
+    the targets y and the burn-in states held constant (stop-gradient targets;
+    burn-in without gradient), on the Atari net (fp64, h = 1e-6), at sampled
+    coordinates of every layer type — pins the dueling backward and the gradient
+    cut at the burn-in boundary."""
+    spec = O.spec_c2(num_actions=5)
+    layout = O.param_layout(spec)
+    params = seedgen.glorot_params(layout, seed=3, bias_std=0.1).astype(np.float64)
+    tparams = seedgen.glorot_params(layout, seed=4, bias_std=0.1).astype(np.float64)
+    B, bi, T = 2, 3, 4
+    full = seedgen.learner_batch((84, 84, 4), 5, B, bi + T, seed=5, done_p=0.1)
+    burn = {k: (v[:, :bi] if v.ndim >= 2 and v.shape[1] == bi + T + 1 else v) for k, v in full.items()}
+    train = {k: (v[:, bi:] if v.ndim >= 2 and v.shape[1] == bi + T + 1 else v) for k, v in full.items()}
+    hp = dict(discount=0.997, n=3, eta=0.9, rescale_eps=1e-3, loss_scale=1.0 / (B * T), lr=1e-4,
+              beta1=0.9, beta2=0.999, eps=1e-3, max_grad_norm=80.0)
+    w = np.array([0.6, 1.0])
+    z = np.zeros(params.size)
+    ref = O.r2d2_learner_step(spec, params, tparams, z, z, 0, burn, train, w, hp)
+    h0, c0 = ref["warm"]
+    y = ref["y"]
+    tr = dict(train, h0=h0, c0=c0)
+
+    def loss(pv):
+        lo, vo, _ = O.network_forward(spec, O.unflatten(spec, pv), tr)
+        return O.r2d2_loss_grad(O.dueling_q(lo, vo), train["action"], y, w, hp["loss_scale"])[0]
+    offs = {n: o for (n, _), o in zip(layout, np.cumsum([0] + [int(np.prod(s)) for _, s in layout])[:-1])}
+    g = seedgen.rng(6)
+    for name in ("heads.w", "heads.b", "lstm.wh", "lstm.wx", "lstm.b", "fc.w", "conv2.w", "conv1.b"):
+        size = int(np.prod(dict(layout)[name]))
+        for k in g.choice(size, 2, replace=False):
+            i = offs[name] + k
+            e = np.zeros(params.size)
+            e[i] = 1e-6
+            fd = (loss(params + e) - loss(params - e)) / 2e-6
+            assert abs(fd - ref["grads"][i]) <= 1e-6 + 1e-4 * abs(fd), (name, k, fd, ref["grads"][i])
