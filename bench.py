@@ -46,6 +46,14 @@ CONFIGS = {
                         "learner step (BASELINE.json configs[3]): 72x96x16 uint8, A=19, T=32, "
                         "B=128/GPU"),
 }
+# SURVEY §8(f) row 3 (larger torsos): reported as extra legs
+CONFIGS["c3m"] = dict(T=100, B=32, A=15, repeat=4, batch_kw={},
+                      workload="c3m DMLab IMPALA-deep Medium (2x filters: 32,64,64) + LSTM256 learner "
+                               "step (P:411): 72x96x3 uint8, A=15, T=100, B=32/GPU")
+CONFIGS["c4l"] = dict(T=32, B=128, A=19, repeat=1, batch_kw=dict(smm=True),
+                      workload="c4l Google Research Football Large SMM 144x108 (P:358), IMPALA-deep "
+                               "(16,32,32,32) + LSTM256 learner step: 108x144x16 uint8, A=19, T=32, "
+                               "B=128/GPU")
 HEAD = "c4"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK = dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0)
@@ -72,8 +80,9 @@ def dist_env():
 # ---------------------------------------------------------------- algorithmic work per launch
 def deep_geometry(cfg):
     """IMPALA-deep sections (C14): (H, W, cin, cin_rows, ch, H2, W2) per section."""
-    H, W, C = 72, 96, (3 if cfg == "c3" else 16)
-    chans = (16, 32, 32) if cfg == "c3" else (16, 32, 32, 32)
+    H, W = (108, 144) if cfg == "c4l" else (72, 96)
+    C = 3 if cfg.startswith("c3") else 16
+    chans = ((32, 64, 64) if cfg == "c3m" else (16, 32, 32)) if cfg.startswith("c3") else (16, 32, 32, 32)
     out, cin, cinp = [], C, 16
     for ch in chans:
         H2, W2 = (H + 1) // 2, (W + 1) // 2
@@ -289,10 +298,20 @@ def cpu_baseline(cfg):
     B_s, T_s = ORACLE_BASELINE[cfg]
     t = oracle_step_time(cfg, B_s, T_s)
     frames = B_s * T_s * CONFIGS[cfg]["repeat"]
-    return {"value": round(frames / t, 2), "unit": "learner frames/s", "cores": blas_threads(),
-            "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "kind": "oracle",
-            "sample": f"1 oracle learner step (fp64 numpy) of the {cfg} network at B={B_s}, "
-                      f"T={T_s} (of B={CONFIGS[cfg]['B']}, T={CONFIGS[cfg]['T']}): {t:.2f} s"}
+    out = {"value": round(frames / t, 2), "unit": "learner frames/s", "cores": blas_threads(),
+           "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "kind": "oracle",
+           "sample": f"1 oracle learner step (fp64 numpy) of the {cfg} network at B={B_s}, "
+                     f"T={T_s} (of B={CONFIGS[cfg]['B']}, T={CONFIGS[cfg]['T']}): {t:.2f} s"}
+    try:   # the same oracle on one core (BLAS limited to 1 thread), a B=1 sample
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            t1 = oracle_step_time(cfg, 1, T_s)
+        out["value_1thread"] = round(1 * T_s * CONFIGS[cfg]["repeat"] / t1, 2)
+        out["sample_1thread"] = f"B=1, T={T_s}, 1 BLAS thread: {t1:.2f} s"
+    except Exception as e:  # noqa: BLE001
+        out["value_1thread"] = None
+        out["sample_1thread"] = f"unavailable: {e}"
+    return out
 
 
 def run_reference(args):
@@ -689,6 +708,15 @@ def measure_learner(S, torch, dist, cfg, steps, warmup, world, rank, local, comm
            "step_ms_p10_p50_p90": [round(float(np.percentile(step_ms, q)), 4) for q in (10, 50, 90)],
            "ms_per_step_per_rank": [round(x, 4) for x in per_rank]}
     out["roofline"] = roofline_of(kernels, cfg)
+    # the step's roofline floor: every launch at max(FLOPs / sustained bf16, bytes / HBM)
+    pk = peaks()
+    floor_us = sum(max(k["flops"] / (pk["bf16_tflops_sustained"] * 1e6),
+                       k["bytes"] / (pk["hbm_gbs"] * 1e3)) for k in kernels)
+    out["step_floor"] = {"ms": round(floor_us / 1e3, 4),
+                         "frac_of_measured": round(floor_us / 1e3 / ms_per_step, 4),
+                         "model": "sum over launches of max(algorithmic FLOPs / sustained bf16 "
+                                  "peak, algorithmic bytes / measured HBM) — ignores the serial "
+                                  "LSTM latency and per-MMA issue floors"}
     if e2e:
         out["e2e"] = e2e_leg(torch, dist, L, dev, pinned, steps, world, frames)
     del L, dev, pinned, tgraph, plain, flush
@@ -795,7 +823,8 @@ def run_ours(args):
     extra = {}
     if not args.no_extra:
         # the other learner configs (fewer timed steps) and inference, on every rank
-        for cfg, k in (("c2", max(20, min(args.steps, 100))), ("c3", max(5, min(args.steps, 20)))):
+        for cfg, k in (("c2", max(20, min(args.steps, 100))), ("c3", max(5, min(args.steps, 20))),
+                       ("c3m", 5), ("c4l", 5)):
             r = measure_learner(S, torch, dist, cfg, k, 3, world, rank, local, comm, clocks=False,
                                 e2e=False)
             extra[cfg] = {"workload": CONFIGS[cfg]["workload"], "steps": k,
@@ -803,7 +832,7 @@ def run_ours(args):
                           "learner_frames_per_s": round(r["value"], 1),
                           "env_steps_per_s": round(r["env_steps_per_s"], 1),
                           "gpu_launches_per_step": r["gpu_launches_per_step"],
-                          "roofline": r["roofline"],
+                          "roofline": r["roofline"], "step_floor": r["step_floor"],
                           "top_kernels": sorted(r["kernels"], key=lambda x: -x["us"])[:8]}
         inf = inference_leg(S, torch, world, rank, dist)
         r2 = r2d2_leg(S, torch) if rank == 0 else None
@@ -829,6 +858,7 @@ def run_ours(args):
             "ms_per_step_per_rank": head["ms_per_step_per_rank"],
             "traced_ms_per_step": round(head["traced_ms_per_step"], 4),
             "roofline": head["roofline"],
+            "step_floor": head["step_floor"],
             "e2e": head["e2e"],
             "clocks": head["clocks"],
             "kernels": [{k: v for k, v in x.items() if k not in ("flops", "bytes")}

@@ -115,6 +115,9 @@ typedef struct {
   int obs_h, obs_w, obs_c;        /* MLP: 1, 1, D                                */
   int num_actions;                /* A >= 2                               */
   int lstm_units;                 /* 0 for the MLP; 256 for the conv nets        */
+  int torso_width;                /* IMPALA-deep channel multiplier: 0/1 = (16, 32,
+                                     32[, 32]), 2 = DMLab "Medium 2x" (32, 64, 64)
+                                     (P:411); others SEED_E_UNSUPPORTED */
 } seed_net_spec;
 
 seed_status seed_net_param_count(const seed_net_spec* spec, int64_t* n_out /* host */);

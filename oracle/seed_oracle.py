@@ -84,9 +84,16 @@ def spec_c2(num_actions=18):
     return NetSpec(NET_ATARI_SHALLOW, 84, 84, 4, num_actions)
 
 
-def spec_c3(num_actions=15):
-    """BJ configs[2]: DMLab IMPALA deep ResNet (16,32,32) + LSTM256, 72x96x3."""
-    return NetSpec(NET_IMPALA_DEEP, 72, 96, 3, num_actions, sections=(16, 32, 32))
+def spec_c3(num_actions=15, width=1):
+    """BJ configs[2]: DMLab IMPALA deep ResNet (16,32,32) + LSTM256, 72x96x3; width 2 =
+    the "Medium 2x" filters (32, 64, 64) of P:411."""
+    return NetSpec(NET_IMPALA_DEEP, 72, 96, 3, num_actions,
+                   sections=tuple(width * c for c in (16, 32, 32)))
+
+
+def spec_c3_medium(num_actions=15):
+    """P:411 DMLab Medium: 2x filters."""
+    return spec_c3(num_actions, width=2)
 
 
 def spec_c4(num_actions=19, obs_h=72, obs_w=96):

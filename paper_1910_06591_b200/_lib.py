@@ -14,7 +14,7 @@ P = C.POINTER
 
 class NetSpec(C.Structure):
     _fields_ = [("kind", c_int), ("obs_h", c_int), ("obs_w", c_int), ("obs_c", c_int),
-                ("num_actions", c_int), ("lstm_units", c_int)]
+                ("num_actions", c_int), ("lstm_units", c_int), ("torso_width", c_int)]
 
 
 class HParams(C.Structure):

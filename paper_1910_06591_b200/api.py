@@ -174,10 +174,11 @@ class NetSpec:
     obs_c: int
     num_actions: int
     lstm_units: int = 256
+    torso_width: int = 1
 
     def c(self):
         return L.NetSpec(self.kind, self.obs_h, self.obs_w, self.obs_c, self.num_actions,
-                         self.lstm_units)
+                         self.lstm_units, self.torso_width)
 
     @property
     def obs_shape(self):
@@ -200,6 +201,8 @@ def spec_for_config(cfg):
         # Football SMM Medium 120x90 / Large 144x108 (W x H)
         "c4m": NetSpec(NET_GFOOTBALL, 90, 120, 16, 19, 256),
         "c4l": NetSpec(NET_GFOOTBALL, 108, 144, 16, 19, 256),
+        # DMLab ResNet "Medium 2x" filters (32, 64, 64)
+        "c3m": NetSpec(NET_IMPALA_DEEP, 72, 96, 3, 15, 256, 2),
     }[cfg]
 
 

@@ -160,7 +160,7 @@ struct W3Fin {
 // PER_LAUNCH=1 at MT = 1 / 2 / 4): 16-channel outputs 4; 32-channel 2 (the
 // residual forward's second input row is prefetched before the accumulator wait)
 template <int MODE, int N, bool FWD>
-constexpr int w3_mt() { return N == 16 ? 4 : 2; }
+constexpr int w3_mt() { return N == 16 ? 4 : N == 32 ? 2 : 1; }
 // NW = 9: 3 x 3 taps as row windows; NW = 3: x-im2col input, 3 row windows (ky)
 // Column-tap-stacked kernels (win_engine.cuh win_conv_kx_kernel: 3 MMAs of
 // N = 3*out per 128 rows, neighbour-row combine in the epilogue) vs the 9-window
@@ -195,9 +195,11 @@ static seed_status fwd_t(const Conv3wFwd& a, cudaStream_t st) {
   W3FwdEpi<MODE, N> e{};
   e.g = a.g; e.in_scale = a.in_scale; e.bias = a.bias; e.res = a.res; e.out = a.out;
   e.outr = a.outr; e.dense = a.dense;
-  if (NW == 9 && XF == XF_NONE && kx_stacked<N, RB>()) {   // 3 row windows ky, column taps stacked on N
-    for (int k = 0; k < 3; ++k) w.off[k] = (k - 1) * a.g.Wp;
-    return launch_win_conv_kx<W3FwdEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
+  if constexpr (NW == 9 && XF == XF_NONE && N <= 32) {
+    if (kx_stacked<N, RB>()) {   // 3 row windows ky, column taps stacked on N
+      for (int k = 0; k < 3; ++k) w.off[k] = (k - 1) * a.g.Wp;
+      return launch_win_conv_kx<W3FwdEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
+    }
   }
   for (int k = 0; k < NW; ++k)
     w.off[k] = NW == 9 ? ((k / 3) - 1) * a.g.Wp + (k % 3) - 1 : (k - 1) * a.g.Wp;
@@ -218,12 +220,15 @@ static seed_status fwd_mode(const Conv3wFwd& a, cudaStream_t st) {
   }
   if (a.xim) {
     if (a.ch == 16 && a.cin_p == 16) return fwd_t<MODE, 16, 32, 3>(a, st);
+    if (a.ch == 32 && a.cin_p == 16) return fwd_t<MODE, 32, 32, 3>(a, st);
     return SEED_E_UNSUPPORTED;
   }
   if (a.ch == 16 && a.cin_p == 16) return fwd_t<MODE, 16, 32, 9>(a, st);
   if (a.ch == 32 && a.cin_p == 16) return fwd_t<MODE, 32, 32, 9>(a, st);
   if (a.ch == 16 && a.cin_p == 32) return fwd_t<MODE, 16, 64, 9>(a, st);
   if (a.ch == 32 && a.cin_p == 32) return fwd_t<MODE, 32, 64, 9>(a, st);
+  if (a.ch == 64 && a.cin_p == 32) return fwd_t<MODE, 64, 64, 9>(a, st);    // DMLab Medium (2x)
+  if (a.ch == 64 && a.cin_p == 64) return fwd_t<MODE, 64, 128, 9>(a, st);
   return SEED_E_UNSUPPORTED;
 }
 
@@ -244,9 +249,11 @@ static seed_status dgrad_t(const Conv3wDgrad& a, cudaStream_t st) {
   // (win3_img_pos mode 1), so out[g] = D[g-1][grp 0] + D[g][grp 1] + D[g+1][grp 2]
   W3DgradEpi<MODE, N> e{};
   e.g = a.g; e.mask = a.mask; e.dres = a.dres; e.dX = a.dX;
-  if (kx_stacked<N, RB>()) {   // 3 row windows at -(ky-1)*Wp, column taps stacked on N
-    for (int k = 0; k < 3; ++k) w.off[k] = -(k - 1) * a.g.Wp;
-    return launch_win_conv_kx<W3DgradEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
+  if constexpr (N <= 32) {
+    if (kx_stacked<N, RB>()) {   // 3 row windows at -(ky-1)*Wp, column taps stacked on N
+      for (int k = 0; k < 3; ++k) w.off[k] = -(k - 1) * a.g.Wp;
+      return launch_win_conv_kx<W3DgradEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
+    }
   }
   // 9 windows: tap (ky, kx) at -((ky-1)*Wp + kx-1), image row block ky*3 + 2 - kx
   for (int k = 0; k < 9; ++k) w.off[k] = -(((k / 3) - 1) * a.g.Wp + 1 - (k % 3));
@@ -259,6 +266,8 @@ static seed_status dgrad_mode(const Conv3wDgrad& a, cudaStream_t st) {
   if (a.cin == 16 && a.ch == 32) return dgrad_t<MODE, 16, 64>(a, st);
   if (a.cin == 32 && a.ch == 16) return dgrad_t<MODE, 32, 32>(a, st);
   if (a.cin == 32 && a.ch == 32) return dgrad_t<MODE, 32, 64>(a, st);
+  if (a.cin == 32 && a.ch == 64) return dgrad_t<MODE, 32, 128>(a, st);   // DMLab Medium (2x)
+  if (a.cin == 64 && a.ch == 64) return dgrad_t<MODE, 64, 128>(a, st);
   return SEED_E_UNSUPPORTED;
 }
 
@@ -297,7 +306,9 @@ struct W3Fin3 {
   __device__ void bias(int n, float t) const { g_b[n] = t; }
 };
 
-size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool) { return win3_wgrad_part_bytes(rows, ch); }
+size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool) {
+  return win3_wgrad_part_bytes(rows, ch, 3, ch == 64 ? 128 : 64);   // 64-ch inputs: 256 partial rows
+}
 
 seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
   Win3WgradArgs w{};
@@ -322,6 +333,8 @@ seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
   if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, !a.xim, st);
   if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, !a.xim, st);
   if (a.ch == 32 && a.cin_p == 32) return launch_win3_wgrad<32, 64>(w, f, !a.xim, st);
+  if (a.ch == 64 && a.cin_p == 32) return launch_win3_wgrad<64, 64>(w, f, !a.xim, st);
+  if (a.ch == 64 && a.cin_p == 64) return launch_win3_wgrad<64, 128>(w, f, !a.xim, st);
   return SEED_E_UNSUPPORTED;
 }
 
@@ -629,6 +642,8 @@ seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
     return launch_k(conv3w_pool_fwd_kernel<2>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, conv, h0, hr0, arg);
   if (NC == 4)
     return launch_k(conv3w_pool_fwd_kernel<4>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, conv, h0, hr0, arg);
+  if (NC == 8)
+    return launch_k(conv3w_pool_fwd_kernel<8>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, conv, h0, hr0, arg);
   return SEED_E_UNSUPPORTED;
 }
 
@@ -649,6 +664,11 @@ seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
   if (NC == 4) {
     SEED_TRY(launch_k(zero_border_kernel<4>, gz, dim3(ROWK_THREADS), 0, st, nz, gi, din));
     return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, nbx, dout,
+                    arg, din);
+  }
+  if (NC == 8) {
+    SEED_TRY(launch_k(zero_border_kernel<8>, gz, dim3(ROWK_THREADS), 0, st, nz, gi, din));
+    return launch_k(conv3w_pool_bwd_kernel<8>, grid, dim3(ROWK_THREADS), 0, st, gi, go, pt, pl, nbx, dout,
                     arg, din);
   }
   return SEED_E_UNSUPPORTED;

@@ -304,8 +304,9 @@ static seed_status core_backward(const StepCtx& c, const seed_batch* bt, const b
       const DeepSec& d = p.sec[p.nsec - 1];
       const PadGeo g = PadGeo::make(d.H2, d.W2);
       pr.dY2s = c.at<uint8_t>(w.dY2); pr.Wo = d.W2; pr.W2s = g.Wp; pr.P2 = g.P; pr.g0 = g.Wp + 1;
+      pr.CH = d.ch;
       // border rows are the next convs' zero padding; the GEMM writes interior rows only
-      SEED_CUDA_TRY(cudaMemsetAsync(pr.dY2s, 0, (size_t)w.F * g.P * 64, st));
+      SEED_CUDA_TRY(cudaMemsetAsync(pr.dY2s, 0, (size_t)w.F * g.P * d.ch * 2, st));
     }
     SEED_TRY(gemm<128>(c, pr, st, "fc_dgrad"));
   }

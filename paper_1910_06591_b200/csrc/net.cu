@@ -58,7 +58,9 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
     fh = p->oh2; fw = p->ow2; fc = 32;
   } else if (s->kind == SEED_NET_IMPALA_DEEP || s->kind == SEED_NET_GFOOTBALL) {
     const int ns = s->kind == SEED_NET_IMPALA_DEEP ? 3 : 4;
-    const int chs[4] = {16, 32, 32, 32};
+    const int wm = s->torso_width <= 1 ? 1 : s->torso_width;
+    if (wm != 1 && wm != 2) return SEED_E_UNSUPPORTED;
+    const int chs[4] = {16 * wm, 32 * wm, 32 * wm, 32 * wm};
     int cin = p->C, h = p->H, w = p->W;
     char nm[32];
     p->nsec = ns;
@@ -156,7 +158,8 @@ bool learner_supported(const NetPlan& p) {
   if (p.kind == SEED_NET_MLP) return true;
   if (p.kind == SEED_NET_ATARI_SHALLOW) return shallow_s2d_supported(p.H, p.W, p.C);
   if (p.kind == SEED_NET_IMPALA_DEEP || p.kind == SEED_NET_GFOOTBALL)   // conv3w.cuh
-    return p.C >= 1 && p.C <= 32 && p.sec[p.nsec - 1].ch == 32 && p.fc_in % 8 == 0;
+    return p.C >= 1 && p.C <= 32 && (p.sec[p.nsec - 1].ch == 32 || p.sec[p.nsec - 1].ch == 64) &&
+           p.fc_in % 8 == 0;
   return false;
 }
 

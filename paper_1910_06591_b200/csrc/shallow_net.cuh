@@ -179,15 +179,16 @@ struct FcDgrad {
   const bf16* act2;
   bf16* dY2;             // plain [M][N] layout (deep torso), or
   uint8_t* dY2s;         // non-null: Atari-shallow conv2 output space, pre-swizzled
-                         // 64-byte rows g = f*P2 + g0 + y*W2s + x (conv_s2d.cuh; deep
-                         // torso: conv3w.cuh padded rows, g0 = W2s + 1)
+                         // rows of 2*CH bytes g = f*P2 + g0 + y*W2s + x (conv_s2d.cuh;
+                         // deep torso: conv3w.cuh padded rows, g0 = W2s + 1)
   int Wo, W2s, P2, g0;
+  int CH = 32;           // channels per dY2s row (32; 64 for the 2x DMLab torso)
   __device__ const void* ptr_a(int m, int k) const { return dfc + (size_t)m * 256 + k; }
   __device__ const void* ptr_b(int k, int n8) const { return w + (size_t)k * N + n8; }
   __device__ uint8_t* s2d_row(int m, int n, int64_t& g) const {
-    const int pix = n >> 5;
+    const int pix = n / CH;
     g = (int64_t)m * P2 + g0 + (pix / Wo) * W2s + pix % Wo;
-    return dY2s + g * 64;
+    return dY2s + g * (2 * CH);
   }
   __device__ void store(int m, int n, float v) const {
     const size_t i = (size_t)m * N + n;
@@ -195,8 +196,8 @@ struct FcDgrad {
     if (dY2s) {
       int64_t g;
       uint8_t* row = s2d_row(m, n, g);
-      const int c = n & 31;
-      *reinterpret_cast<bf16*>(row + (swz_chunk(g, 64, c >> 3) << 4) + (c & 7) * 2) = o;
+      const int c = n % CH;
+      *reinterpret_cast<bf16*>(row + (swz_chunk(g, 2 * CH, c >> 3) << 4) + (c & 7) * 2) = o;
     } else {
       dY2[i] = o;
     }
@@ -208,14 +209,14 @@ struct FcDgrad {
     if (dY2s) {
       int64_t g;
       uint8_t* row = s2d_row(m, n0, g);
-      const int j0 = (n0 & 31) >> 3;
+      const int j0 = (n0 % CH) >> 3;
       uint4 a, b;
       a.x = pack_bf16(v[0], v[1]); a.y = pack_bf16(v[2], v[3]);
       a.z = pack_bf16(v[4], v[5]); a.w = pack_bf16(v[6], v[7]);
       b.x = pack_bf16(v[8], v[9]); b.y = pack_bf16(v[10], v[11]);
       b.z = pack_bf16(v[12], v[13]); b.w = pack_bf16(v[14], v[15]);
-      *reinterpret_cast<uint4*>(row + (swz_chunk(g, 64, j0) << 4)) = a;
-      *reinterpret_cast<uint4*>(row + (swz_chunk(g, 64, j0 + 1) << 4)) = b;
+      *reinterpret_cast<uint4*>(row + (swz_chunk(g, 2 * CH, j0) << 4)) = a;
+      *reinterpret_cast<uint4*>(row + (swz_chunk(g, 2 * CH, j0 + 1) << 4)) = b;
     } else {
       st_bf16x16(dY2 + i, v);
     }

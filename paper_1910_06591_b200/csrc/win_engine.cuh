@@ -35,6 +35,9 @@ constexpr int WC_MAX_STAGES = 8;
 constexpr int WC_SMEM_BUDGET = 200 * 1024;
 constexpr int WG_KS = 256;        // rows per weight-gradient k-stage
 constexpr int WIN_MAX = 9;        // windows per convolution
+// weight-gradient partial rows per CTA: 128, or 256 when 64-channel rows (128 B:
+// 2 atoms per MMA) need two MMAs for 3 column taps
+constexpr int wgrad_prows(int rbx, int nb) { return rbx == 128 && nb >= 3 ? 256 : 128; }
 
 // uint8 source of a 16-channel padded row space (XF_U8): obs [F][H][W][16] bytes
 // whose padded row g = f*P + Y*Wp + X holds pixel (Y-1, X-1) (zero borders)
@@ -670,10 +673,16 @@ __global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0),
   // row m at lane (m / 16) * 32 + m % 16.
   constexpr int MM = RBX == 32 ? 64 : 128;
   constexpr int NA = 2 * MM / RBX;        // A atoms per MMA
+  // 64-channel rows (RBX = 128): 2 atoms per M = 128, so the three kx taps take two
+  // MMAs per 16 rows (atoms kx 0-1, and kx 2-3 from two rows further), two accumulators
+  constexpr int NMMA = NA >= NB ? 1 : 2;   // (NB = the kernel's side: column taps too)
+  constexpr int PROWS = wgrad_prows(RBX, NB);   // partial rows per CTA (= NMMA * MM, >= 128)
+  static_assert(PROWS >= NMMA * MM, "partial rows");
   constexpr int NW = NB * CO;             // weight columns (NB B atoms)
   constexpr int PC = (NB + 1) * CO;       // partial row: weights | bias
   constexpr uint32_t LA = swz_layout_code(RBX), LB = swz_layout_code(RBY);
-  constexpr uint32_t TCOLS = NW <= 64 ? 64 : 128;
+  constexpr int ACOL = NW <= 64 ? 64 : NW <= 128 ? 128 : 256;   // columns per accumulator
+  constexpr uint32_t TCOLS = NMMA * ACOL <= 64 ? 64 : NMMA * ACOL <= 128 ? 128 : NMMA * ACOL <= 256 ? 256 : 512;
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
   uint8_t* stg = sm + 1024;
@@ -686,7 +695,7 @@ __global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0),
   const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t r_end = std::min<int64_t>(a.M, r_begin + a.rows_per_cta);
   const int nks = r_end > r_begin ? (int)((r_end - r_begin + WG_KS - 1) / WG_KS) : 0;
-  const int arows = WG_KS + NA - 1, brows = WG_KS + (NB - 1) * a.bstride;
+  const int arows = WG_KS + NA * NMMA - 1, brows = WG_KS + (NB - 1) * a.bstride;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
@@ -756,15 +765,17 @@ __global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0),
 #pragma unroll
       for (int ks = 0; ks < WG_KS / 16; ++ks) {
         const uint32_t accf = acc0 | (ks != 0);
-        tc_mma_bf16_w(tmem, ad0 + (uint64_t)((ks * 16 * RBX) >> 4), bd0 + (uint64_t)((ks * 16 * RBY) >> 4),
-                      idesc, accf);
+#pragma unroll
+        for (int mi = 0; mi < NMMA; ++mi)
+          tc_mma_bf16_w(tmem + mi * ACOL, ad0 + (uint64_t)((ks * 16 * RBX + mi * NA * RBX) >> 4),
+                        bd0 + (uint64_t)((ks * 16 * RBY) >> 4), idesc, accf);
       }
       tc_commit_w(&empty[s]);
     }
     tc_commit_w(&tfull);
   } else if (warp < 6) {
     const int q = warp & 3;
-    float* part = a.part + (size_t)blockIdx.x * 128 * PC;
+    float* part = a.part + (size_t)blockIdx.x * PROWS * PC;
     // accumulator row of this thread's TMEM lane (M = 64: lanes 0-15 of each quarter)
     const int row = MM == 128 ? q * 32 + lane : q * 16 + lane;
     const bool row_ok = MM == 128 || lane < 16;
@@ -813,20 +824,21 @@ __global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0),
       tc_fence_after();
     }
 #pragma unroll
-    for (int c0 = 0; c0 < NW; c0 += 16) {
-      float v[16];
-      if (nks > 0) {
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
-      } else {
+    for (int mi = 0; mi < NMMA; ++mi)
+      for (int c0 = 0; c0 < NW; c0 += 16) {
+        float v[16];
+        if (nks > 0) {
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + mi * ACOL + c0, v);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = 0.f;
-      }
-      float4* dst = reinterpret_cast<float4*>(part + (size_t)row * PC + c0);
-      if (row_ok) {
+          for (int c = 0; c < 16; ++c) v[c] = 0.f;
+        }
+        float4* dst = reinterpret_cast<float4*>(part + (size_t)(mi * MM + row) * PC + c0);
+        if (row_ok) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          for (int c = 0; c < 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        }
       }
-    }
     tc_fence_before();
   }
   __syncthreads();
@@ -838,7 +850,7 @@ __global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0),
 
 // fixed-order sum; output o < 128*3CO: (row i, col n) -> Fin::weight3(i, n, v);
 // o >= 128*3CO: bias column -> Fin::bias
-template <int CO, class Fin, int NB = 3>
+template <int CO, class Fin, int NB = 3, int PROWS = 128>
 __global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict__ part, int G,
                                                          int tot, const Fin f) {
   pdl_wait();
@@ -848,10 +860,10 @@ __global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict
   float s = 0.f;
   size_t idx = 0;
   if (o < tot) {
-    idx = o < 128 * NW ? (size_t)(o / NW) * PC + (o % NW) : (size_t)NW + (o - 128 * NW);
+    idx = o < PROWS * NW ? (size_t)(o / NW) * PC + (o % NW) : (size_t)NW + (o - PROWS * NW);
     // unrolled: the loads issue back to back, the adds stay in z order
 #pragma unroll 8
-    for (int z = g; z < G; z += 8) s += __ldcg(part + (size_t)z * 128 * PC + idx);
+    for (int z = g; z < G; z += 8) s += __ldcg(part + (size_t)z * PROWS * PC + idx);
   }
   sh[g][threadIdx.x & 31] = s;
   __syncthreads();
@@ -859,14 +871,14 @@ __global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict
     float t = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x & 31];
-    if (o >= 128 * NW) f.bias(o - 128 * NW, t);
+    if (o >= PROWS * NW) f.bias(o - PROWS * NW, t);
     else f.weight3(o / NW, o % NW, t);
   }
 }
 
-inline size_t win3_wgrad_part_bytes(int64_t M, int CO, int NB = 3) {
+inline size_t win3_wgrad_part_bytes(int64_t M, int CO, int NB = 3, int rbx = 128) {
   int64_t r;
-  return (size_t)wgrad_grid(M, &r) * 128 * (NB + 1) * CO * 4;
+  return (size_t)wgrad_grid(M, &r) * wgrad_prows(rbx, NB) * (NB + 1) * CO * 4;
 }
 
 // bias = false: no all-ones MMA (the bias gradient is a column of the weight
@@ -875,7 +887,7 @@ template <int CO, int RBX, class Fin, int NB = 3, int XF = XF_NONE>
 seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias, cudaStream_t st) {
   Win3WgradArgs a = a0;
   const int G = wgrad_grid(a.M, &a.rows_per_cta);
-  const int arows = WG_KS + 256 / RBX - 1;
+  const int arows = WG_KS + 256 / RBX - 1 + (wgrad_prows(RBX, NB) == 256 ? 2 : 0);   // + the second MMA's rows
   const int a_bytes = (int)align_up((size_t)arows * RBX + 1024, 1024);
   const int b_bytes = (int)align_up((size_t)(WG_KS + (NB - 1) * a.bstride) * 2 * CO + 1024, 1024);
   const int stg_bytes = XF == XF_U8 ? (int)align_up((size_t)arows * 16 + 16, 1024) : 0;
@@ -889,8 +901,9 @@ seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias
   const int threads = WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0);
   SEED_TRY(launch_k(bias ? win3_wgrad_kernel<CO, RBX, true, NB, XF> : win3_wgrad_kernel<CO, RBX, false, NB, XF>,
                     dim3(G), dim3(threads), smem, st, a, stages, a_bytes, b_bytes, stg_bytes));
-  const int tot = 128 * NB * CO + (bias ? CO : 0);
-  return launch_k(win3_wgrad_finish<CO, Fin, NB>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
+  constexpr int PROWS = wgrad_prows(RBX, NB);
+  const int tot = PROWS * NB * CO + (bias ? CO : 0);
+  return launch_k(win3_wgrad_finish<CO, Fin, NB, PROWS>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
                   (const float*)a.part, G, tot, fin);
 }
 

@@ -64,11 +64,11 @@ def _spec_pair(cfg):
     S = _S()
     spec = S.spec_for_config(cfg)
     ospec = {"c1": O.spec_c1, "c2": O.spec_c2, "c3": O.spec_c3, "c4": O.spec_c4,
-             "c4m": O.spec_c4_medium, "c4l": O.spec_c4_large}[cfg]()
+             "c4m": O.spec_c4_medium, "c4l": O.spec_c4_large, "c3m": O.spec_c3_medium}[cfg]()
     return spec, ospec
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c4m", "c4l"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c4m", "c4l", "c3m"])
 def test_param_layout_matches_oracle(cfg):
     S = _S()
     spec, ospec = _spec_pair(cfg)
@@ -238,7 +238,7 @@ def _padded_rows(L, name, shape):
     raw = L.debug_buffer(name, torch.uint8, (rows, rb)).cpu().numpy()
     g = np.arange(rows)[:, None]
     j = np.arange(rb // 16)[None, :]
-    phys = j ^ (((g >> 2) & 1) if rb == 32 else ((g >> 1) & 3))
+    phys = j ^ (((g >> 2) & 1) if rb == 32 else ((g >> 1) & 3) if rb == 64 else (g & 7))
     chunks = raw.reshape(rows, rb // 16, 16)
     dense = np.take_along_axis(chunks, phys[:, :, None], axis=1).reshape(rows, rb)
     v = torch.from_numpy(np.ascontiguousarray(dense)).view(torch.bfloat16).float().numpy()
@@ -251,7 +251,7 @@ def _padded_rows(L, name, shape):
 
 
 @pytest.mark.parametrize("cfg,B,T", [("c3", 2, 3), ("c4", 2, 2), ("c3", 3, 1), ("c4m", 2, 2),
-                                     ("c4l", 1, 2)])
+                                     ("c4l", 1, 2), ("c3m", 2, 3)])
 def test_learner_deep_parity(cfg, B, T):
     """configs[2] (DMLab IMPALA-deep, 72x96x3) / configs[3] (GRF SMM 72x96x16), full
     image size: 3x3 'same' convs, max-pool, residual blocks (C14).
@@ -401,7 +401,8 @@ def _deep_exact_checks(cfg, g, gt, ex, rt, exact, ref):
     assert not bad, bad
 
 
-@pytest.mark.parametrize("cfg,B,T", [("c3", 32, 100), ("c4", 128, 32), ("c4l", 128, 32)])
+@pytest.mark.parametrize("cfg,B,T", [("c3", 32, 100), ("c4", 128, 32), ("c4l", 128, 32),
+                                     ("c3m", 32, 100)])
 def test_learner_deep_full_size_sampled(cfg, B, T):
     """BASELINE.json configs[2] / configs[3] at their full sizes (the shapes bench.py
     times: F = 3232 / 4224 frames, 23-31 M padded rows at 72x96): one learner step,
