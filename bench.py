@@ -146,7 +146,7 @@ def launch_work(cfg, T, B, A, P, names):
         if not n.startswith("deep_") and n != "obs_bf16":
             out.append(tw.get(n, (0, 0)))
             continue
-        fwd = "_fwd" in n
+        fwd = "_fwd" in n or n == "deep_conv_pool"
         if n == "obs_bf16":
             H, W, cin, cinp = geo[0][0], geo[0][1], geo[0][2], geo[0][3]
             out.append((0, F * H * W * (cin + cinp * 2)))
@@ -165,6 +165,8 @@ def launch_work(cfg, T, B, A, P, names):
         xin = Ai * (cin if u8 else cinp * 2) if s == 0 else Ai * cin * 2
         if n == "deep_conv_fwd":
             w = (2 * Ai * ch * 9 * cin, xin + Ai * ch * 2)
+        elif n == "deep_conv_pool":    # fused: input read, pooled h, relu(h) + argmax written
+            w = (2 * Ai * ch * 9 * cin, xin + 2 * Ao * ch * 2 + Ao * ch)
         elif n == "deep_pool_fwd":     # conv read, pooled h, relu(h) + argmax written
             w = (0, Ai * ch * 2 + 2 * Ao * ch * 2 + Ao * ch)
         elif n == "deep_res_fwd0":

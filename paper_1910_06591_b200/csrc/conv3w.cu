@@ -523,34 +523,11 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
     in[q] = ok ? __ldg(chunk_at(conv, fb + (int64_t)(y + 1) * gi.Wp + (x + 1), RB, j))
                : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);   // -inf
   }
-  // packed bf16x2: v > best per half (strict: the first maximum in (ky, kx) order
-  // wins), best / argmax selected through the 16-bit lane masks
-  uint32_t best[4] = {in[0].x, in[0].y, in[0].z, in[0].w};
-  uint32_t barg[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-  for (int q = 1; q < 9; ++q) {
-    const uint32_t v[4] = {in[q].x, in[q].y, in[q].z, in[q].w};
-    const uint32_t qq = (uint32_t)q * 0x00010001u;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const uint32_t gt = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&v[p]),
-                                      *reinterpret_cast<const __nv_bfloat162*>(&best[p]));
-      best[p] = (v[p] & gt) | (best[p] & ~gt);
-      barg[p] = (qq & gt) | (barg[p] & ~gt);
-    }
-  }
-  uint32_t rl[4];
-  const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const __nv_bfloat162 r2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&best[p]), zero2);
-    rl[p] = *reinterpret_cast<const uint32_t*>(&r2);
-  }
-  *chunk_at(h0, m, RB, j) = make_uint4(best[0], best[1], best[2], best[3]);
-  if (hr0) *chunk_at(hr0, m, RB, j) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+  uint4 best, rl;
   uint2 a;
-  a.x = __byte_perm(barg[0], barg[1], 0x6420);
-  a.y = __byte_perm(barg[2], barg[3], 0x6420);
+  pool_max9(in, best, rl, a);
+  *chunk_at(h0, m, RB, j) = best;
+  if (hr0) *chunk_at(hr0, m, RB, j) = rl;
   *reinterpret_cast<uint2*>(arg + m * C + 8 * j) = a;
   }
 }

@@ -122,6 +122,49 @@ size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool xim);
 seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
                             const uint8_t* conv, uint8_t* h0, uint8_t* hr0, uint8_t* arg,
                             cudaStream_t st);
+// the 3x3 window max of 8 channels (one 16-byte chunk per tap, taps in (ky, kx)
+// order, -inf for padding): packed bf16x2 v > best per half (strict: the first
+// maximum wins), best / argmax selected through the 16-bit lane masks; rl =
+// relu(best), arg = the 8 argmax bytes
+__device__ __forceinline__ void pool_max9(const uint4 (&in)[9], uint4& best_o, uint4& rl_o, uint2& arg_o) {
+  uint32_t best[4] = {in[0].x, in[0].y, in[0].z, in[0].w};
+  uint32_t barg[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int q = 1; q < 9; ++q) {
+    const uint32_t v[4] = {in[q].x, in[q].y, in[q].z, in[q].w};
+    const uint32_t qq = (uint32_t)q * 0x00010001u;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t gt = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&v[p]),
+                                      *reinterpret_cast<const __nv_bfloat162*>(&best[p]));
+      best[p] = (v[p] & gt) | (best[p] & ~gt);
+      barg[p] = (qq & gt) | (barg[p] & ~gt);
+    }
+  }
+  uint32_t rl[4];
+  const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const __nv_bfloat162 r2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&best[p]), zero2);
+    rl[p] = *reinterpret_cast<const uint32_t*>(&r2);
+  }
+  best_o = make_uint4(best[0], best[1], best[2], best[3]);
+  rl_o = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+  arg_o.x = __byte_perm(barg[0], barg[1], 0x6420);
+  arg_o.y = __byte_perm(barg[2], barg[3], 0x6420);
+}
+constexpr uint32_t BF16X2_NEG_INF = 0xFF80FF80u;
+
+// Section conv + max-pool in one kernel (conv3w_pool.cu): the conv of a band of
+// whole image rows (or of several whole frames) accumulates in TMEM, is stored
+// as bf16 into shared memory by the epilogue warps, which then pool it there and
+// write h0 / hr0 / arg (borders zero) — the full-resolution conv output never
+// goes to HBM.  `a` is the W3_PLAIN section conv; conv_dbg (nullable) also
+// receives the conv rows (border rows unspecified) for the parity tests.
+// SEED_E_UNSUPPORTED when the shape has no fused instantiation or does not fit
+// (the caller then runs conv3w_forward + conv3w_pool_fwd).
+seed_status conv3w_conv_pool(const Conv3wFwd& a, const PadGeo& go, int pt, int pl, uint8_t* h0,
+                             uint8_t* hr0, uint8_t* arg, uint8_t* conv_dbg, cudaStream_t st);
 // gradient gather into gi rows (borders zero)
 seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
                             const uint8_t* dout, const uint8_t* arg, uint8_t* din,

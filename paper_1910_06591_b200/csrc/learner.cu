@@ -361,6 +361,22 @@ static bool deep_u8_input(const NetPlan& p) {
   return on && !p.sec[0].xim && p.C == 16 && p.sec[0].cinp == 16;
 }
 
+// Section conv + max-pool fused (conv3w_pool.cu; the full-resolution conv output
+// is not stored) unless SEED_FUSE_POOL=0 (A/B measurement).  SEED_STORE_CONV=1
+// (read per call: the parity tests flip it) makes the fused kernel also write
+// the conv rows to the workspace's "s<k>.conv" buffer.
+static bool fuse_conv_pool() {
+  static const bool on = [] {
+    const char* e = getenv("SEED_FUSE_POOL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static bool store_conv_rows() {
+  const char* e = getenv("SEED_STORE_CONV");
+  return e && e[0] == '1';
+}
+
 static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                 const float* params, cudaStream_t st) {
   const NetPlan& p = *c.p;
@@ -386,12 +402,21 @@ static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf
       a.obs_u8 = (const uint8_t*)bt->obs;
     }
     a.wimg = lowp + d.im_w; a.bias = params + p.t[d.t_b].off; a.out = c.at<uint8_t>(b.conv);
-    SEED_TRY(conv3w_forward(a, st));
-    c.mark("deep_conv_fwd");
-    SEED_TRY(conv3w_pool_fwd(F, gi, go, d.ch, d.pt, d.pl, c.at<uint8_t>(b.conv),
-                             c.at<uint8_t>(b.h[0]), c.at<uint8_t>(b.hr[0]), c.at<uint8_t>(b.arg),
-                             st));
-    c.mark("deep_pool_fwd");
+    seed_status fs = SEED_E_UNSUPPORTED;
+    if (fuse_conv_pool() && a.xf == XF_NONE) {
+      fs = conv3w_conv_pool(a, go, d.pt, d.pl, c.at<uint8_t>(b.h[0]), c.at<uint8_t>(b.hr[0]),
+                            c.at<uint8_t>(b.arg), store_conv_rows() ? c.at<uint8_t>(b.conv) : nullptr, st);
+      if (fs != SEED_E_UNSUPPORTED) SEED_TRY(fs);
+      if (fs == SEED_OK) c.mark("deep_conv_pool");
+    }
+    if (fs == SEED_E_UNSUPPORTED) {
+      SEED_TRY(conv3w_forward(a, st));
+      c.mark("deep_conv_fwd");
+      SEED_TRY(conv3w_pool_fwd(F, gi, go, d.ch, d.pt, d.pl, c.at<uint8_t>(b.conv),
+                               c.at<uint8_t>(b.h[0]), c.at<uint8_t>(b.hr[0]), c.at<uint8_t>(b.arg),
+                               st));
+      c.mark("deep_pool_fwd");
+    }
     for (int r = 0; r < 2; ++r) {
       Conv3wFwd a0{};
       a0.mode = W3_RELU; a0.cin_p = d.ch; a0.ch = d.ch; a0.g = go; a0.rows = F * go.P;

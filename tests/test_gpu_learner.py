@@ -252,7 +252,7 @@ def _padded_rows(L, name, shape):
 
 @pytest.mark.parametrize("cfg,B,T", [("c3", 2, 3), ("c4", 2, 2), ("c3", 3, 1), ("c4m", 2, 2),
                                      ("c4l", 1, 2), ("c3m", 2, 3)])
-def test_learner_deep_parity(cfg, B, T):
+def test_learner_deep_parity(cfg, B, T, monkeypatch):
     """configs[2] (DMLab IMPALA-deep, 72x96x3) / configs[3] (GRF SMM 72x96x16), full
     image size: 3x3 'same' convs, max-pool, residual blocks (C14).
 
@@ -271,6 +271,9 @@ def test_learner_deep_parity(cfg, B, T):
     batch = seedgen.learner_batch((ospec.obs_h, ospec.obs_w, ospec.obs_c), ospec.num_actions, B,
                                   T, seed=22, done_p=0.2, smm=cfg.startswith("c4"))
     hp = S.HParams(lam=0.95, loss_scale=1.0 / (B * T), lr=1e-3)
+    # the fused section conv + max-pool (conv3w_pool.cu) keeps the conv output on
+    # chip; this makes it also store the conv rows for the checks below
+    monkeypatch.setenv("SEED_STORE_CONV", "1")
     g = _run_gpu(S, spec, params, batch, hp, B, T)
     L = g["L"]
     ref = O.learner_step(ospec, params, np.zeros(params.size), np.zeros(params.size), 0, batch,
