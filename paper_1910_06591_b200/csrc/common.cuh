@@ -154,6 +154,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 1024-aligned start of the dynamic shared memory as a shared-space pointer:
+// arithmetic on the extern __shared__ array (not an integer round trip through
+// uintptr_t), so direct loads / stores through it compile to LDS / STS instead of
+// generic LD / ST with a memory descriptor each
+__device__ __forceinline__ uint8_t* smem_align1024(uint8_t* base) {
+  return base + ((1024u - (smem_u32(base) & 1023u)) & 1023u);
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }

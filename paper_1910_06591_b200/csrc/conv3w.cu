@@ -46,10 +46,23 @@ struct W3FwdEpi {
       }
       return;
     }
+    if ((reinterpret_cast<uintptr_t>(bias) & 15) == 0) {   // 16-byte bias loads (the torso's
+#pragma unroll                                              // parameter offsets are multiples of 4)
+      for (int q = 0; q < N / 4; ++q) {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias) + q);
+        const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-    for (int q = 0; q < N; ++q) {
-      v[q] = v[q] * in_scale + __ldg(bias + q);
-      if (MODE == W3_RELU) v[q] = fmaxf(v[q], 0.f);
+        for (int k = 0; k < 4; ++k) {
+          v[4 * q + k] = v[4 * q + k] * in_scale + bb[k];
+          if (MODE == W3_RELU) v[4 * q + k] = fmaxf(v[4 * q + k], 0.f);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        v[q] = v[q] * in_scale + __ldg(bias + q);
+        if (MODE == W3_RELU) v[q] = fmaxf(v[q], 0.f);
+      }
     }
     if (MODE == W3_RES) {
 #pragma unroll
@@ -198,7 +211,7 @@ static seed_status fwd_t(const Conv3wFwd& a, cudaStream_t st) {
   if constexpr (NW == 9 && XF == XF_NONE && N <= 32) {
     if (kx_stacked<N, RB>()) {   // 3 row windows ky, column taps stacked on N
       for (int k = 0; k < 3; ++k) w.off[k] = (k - 1) * a.g.Wp;
-      return launch_win_conv_kx<W3FwdEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
+      return launch_win_conv_kx<W3FwdEpi<MODE, N>, RB, N == 16 ? 2 : 1, 3>(w, e, st);
     }
   }
   for (int k = 0; k < NW; ++k)
@@ -252,7 +265,7 @@ static seed_status dgrad_t(const Conv3wDgrad& a, cudaStream_t st) {
   if constexpr (N <= 32) {
     if (kx_stacked<N, RB>()) {   // 3 row windows at -(ky-1)*Wp, column taps stacked on N
       for (int k = 0; k < 3; ++k) w.off[k] = -(k - 1) * a.g.Wp;
-      return launch_win_conv_kx<W3DgradEpi<MODE, N>, RB, N == 16 ? 4 : 2>(w, e, st);
+      return launch_win_conv_kx<W3DgradEpi<MODE, N>, RB, N == 16 ? 2 : 1, 3>(w, e, st);
     }
   }
   // 9 windows: tap (ky, kx) at -((ky-1)*Wp + kx-1), image row block ky*3 + 2 - kx

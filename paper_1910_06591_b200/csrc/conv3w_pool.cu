@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
   constexpr int WB = NW * N * RB;
   constexpr int AC = 256;   // TMEM columns per accumulator (2 accumulators)
   extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_align1024(smraw);
   uint8_t* Ws = sm;
   uint8_t* slabs = sm + ((WB + 1023) & ~1023);
   uint8_t* bandbuf = slabs + (size_t)stages * slab_bytes;

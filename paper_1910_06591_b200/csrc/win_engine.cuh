@@ -248,6 +248,11 @@ template <class E, class = void>
 struct EpiPre { static constexpr int n = 0; };
 template <class E>
 struct EpiPre<E, std::void_t<decltype(E::PRE)>> { static constexpr int n = E::PRE; };
+template <class E, class P>
+__device__ __forceinline__ void epi_store(const E& e, int64_t m, float (&v)[E::N], const P& pre) {
+  if constexpr (EpiPre<E>::n > 0) e.store(m, v, pre);
+  else e.store(m, v);
+}
 
 template <class Epi, int RB, int NW, int MT = 1, int XF = XF_NONE>
 __global__ void __launch_bounds__(WCF_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0), 1)
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(WCF_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0)
                              : WCF_ACC * AC <= 256 ? 256 : 512;
   static_assert(WCF_ACC * AC <= 512, "TMEM");
   extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_align1024(smraw);
   uint8_t* Ws = sm;
   uint8_t* slabs = sm + ((WB + 1023) & ~1023);
   uint8_t* stgs = slabs + (size_t)stages * slab_bytes;   // XF_U8 staging, stg_bytes each
@@ -387,11 +392,7 @@ __global__ void __launch_bounds__(WCF_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0)
 #pragma unroll
         for (int c = 0; c < N; ++c) v[c] = __uint_as_float(vr[mt][c]);
         const int64_t m = t * TM + mt * 128 + q * 32 + lane;
-        if constexpr (EpiPre<Epi>::n > 0) {
-          if (m < a.M) e.store(m, v, pre[mt]);
-        } else {
-          if (m < a.M) e.store(m, v);
-        }
+        if (m < a.M) epi_store(e, m, v, pre[mt]);
       }
     }
   }
@@ -433,35 +434,42 @@ seed_status launch_win_conv(const WinConvArgs& a, const Epi& e, cudaStream_t st)
 //   out[g][o] = D[g-1][0*NO + o] + D[g][1*NO + o] + D[g+1][2*NO + o]
 // (forward: j = kx, off_ky = (ky-1)*Wp; data gradient: j = 2-kx with the mode-1
 // image, off_ky = -(ky-1)*Wp — the same combination).  3 MMAs per 128 rows instead
-// of 9: the 16/32-channel convs were bound by the ~45-cycle floor of each small
-// tcgen05.mma (profiles/r01/mma_rate_probe.txt), not by HBM.
+// of 9, reading the A rows 3 times instead of 9: the 16/32-channel convs are bound
+// by the shared-memory operand reads of their small tcgen05.mma
+// (profiles/r02/conv_pool_fused.md), not by HBM.
 // Tiles of TM = 128*MT MMA rows overlap by 2 rows: tile t computes rows
 // [t*TS - 1, t*TS - 1 + TM) and outputs [t*TS, t*TS + TS), TS = TM - 2, so every
-// output row's neighbours are in its own tile.  Inside a tile, rows g-1 / g+1 come
-// from the neighbouring lane (warp shuffle) or, at the 32-row warp-quarter edges,
-// through a shared-memory exchange (one named barrier per tile and group).
-constexpr int WKX_ACC = 2;   // one TMEM accumulator per epilogue group
-
-template <class Epi, int RB, int MT>
-__global__ void __launch_bounds__(WCF_THREADS, 1)
+// output row's neighbours are in its own tile.  Epilogue: NG groups of 4 warps take
+// tiles round robin (one TMEM accumulator each).  A warp drains each 32-row block
+// of its TMEM lane quarter once (three 16-column loads per 16 outputs) and takes
+// rows r-1 / r+1 from the neighbouring lanes (shuffles); lanes 31 / 0 leave the
+// part the neighbouring quarter's edge row needs in a shared-memory exchange
+// (double-buffered per group) and, after one named barrier, lanes 0 / 31 add it
+// and the whole warp stores (the tile's sums stay in registers across the
+// barrier: MT*NO <= 32).  Edge rows sum D[g-1] + (D[g] + D[g+1]) /
+// (D[g-1] + D[g]) + D[g+1], interior rows (D[g-1] + D[g]) + D[g+1].
+// (A non-finite D of a quarter's edge row times the 0 mask would poison that row
+// with NaN; the D here are finite bf16-operand sums.)
+template <class Epi, int RB, int MT, int NG>
+__global__ void __launch_bounds__(64 + 128 * NG, 1)
     win_conv_kx_kernel(const WinConvArgs a, const Epi e, int stages, int slab_bytes) {
   constexpr int NO = Epi::N;          // output channels
   constexpr int N = 3 * NO;           // MMA N: kx-stacked
   constexpr int TM = 128 * MT, TS = TM - 2;
   constexpr uint32_t LAYOUT = swz_layout_code(RB);
   constexpr int WB = 3 * N * RB;
-  constexpr int AC = MT * N;          // TMEM columns per tile accumulator
-  constexpr uint32_t TCOLS = WKX_ACC * AC <= 128 ? 128 : WKX_ACC * AC <= 256 ? 256 : 512;
-  static_assert(WKX_ACC * AC <= 512, "TMEM");
+  constexpr int AC = MT * N;          // TMEM columns per tile accumulator (one per group)
+  constexpr uint32_t TCOLS = NG * AC <= 128 ? 128 : NG * AC <= 256 ? 256 : 512;
+  static_assert(NG * AC <= 512, "TMEM");
   static_assert(NO % 16 == 0, "NO");
   extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_align1024(smraw);
   uint8_t* Ws = sm;
   uint8_t* slabs = sm + ((WB + 1023) & ~1023);
-  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[WKX_ACC], tempty[WKX_ACC], wbar;
+  // exchange [group][buffer][slot = mt*4 + quarter][ 0: D0 of lane 31 | 1: D2 of lane 0 ][NO]
+  float* xch = reinterpret_cast<float*>(slabs + (size_t)stages * slab_bytes);
+  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[NG], tempty[NG], wbar;
   __shared__ uint32_t tbase;
-  // edge exchange per group: [MT*4 quarters][0: last row's part 0 | 1: first row's part 2][NO]
-  __shared__ __align__(16) float xch[2][MT * 4][2][NO];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mn = min(a.off[0], min(a.off[1], a.off[2]));
   const int mx = max(a.off[0], max(a.off[1], a.off[2]));
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
   const int64_t tiles = (a.M + TS - 1) / TS;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < WKX_ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < NG; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     mbar_init(&wbar, 1);
     fence_mbar_init();
   }
@@ -499,9 +507,9 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
     for (int w = 0; w < 3; ++w) aoff[w] = ((a.off[w] - mn) * RB) >> 4;
     int it = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      const int s = it % stages, acc = it % WKX_ACC;
+      const int s = it % stages, acc = it % NG;
       mbar_wait(&full[s], (it / stages) & 1);
-      mbar_wait(&tempty[acc], ((it / WKX_ACC) & 1) ^ 1);
+      mbar_wait(&tempty[acc], ((it / NG) & 1) ^ 1);
       tc_fence_after();
       const uint32_t base = smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(t * TS - 1 + mn, RB);
       const uint64_t ad0 = umma_desc(base, 16, 8 * RB, LAYOUT);
@@ -519,12 +527,12 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
     }
   } else {
     const int q = warp & 3;            // TMEM lanes [32q, 32q+32) of this warp
-    const int grp = (warp - 2) >> 2;   // epilogue group: tiles it with it % 2 == grp
+    const int grp = (warp - 2) >> 2;   // epilogue group: tiles it with it % NG == grp
     constexpr int PN = EpiPre<Epi>::n > 0 ? EpiPre<Epi>::n : 1;
-    int it = 0;
+    const float m_up = lane == 0 ? 0.f : 1.f, m_dn = lane == 31 ? 0.f : 1.f;
+    int it = 0, gt = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      if ((it & 1) != grp) continue;
-      const int acc = it % WKX_ACC;
+      if (it % NG != grp) continue;
       const int64_t g0 = t * TS - 1;   // global row of MMA row 0
       uint4 pre[MT][PN];
       if constexpr (EpiPre<Epi>::n > 0) {
@@ -535,77 +543,76 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
           if (r >= 1 && r <= TM - 2 && m < a.M) e.pre(m, pre[mt]);
         }
       }
-      mbar_wait(&tfull[acc], (it / WKX_ACC) & 1);
+      mbar_wait(&tfull[grp], (it / NG) & 1);
       tc_fence_after();
-      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + acc * AC;
-      // pass 1: the quarter-edge rows' parts for the neighbouring quarters
+      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + grp * AC;
+      float* xb = xch + (size_t)(grp * 2 + (gt & 1)) * MT * 4 * 2 * NO;
+      float v[MT][NO];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-#pragma unroll
-        for (int c = 0; c < NO / 16; ++c) {
-          uint32_t p0[16], p2[16];
-          tmem_ld16_nw(tb + mt * N + c * 16, p0);
-          tmem_ld16_nw(tb + mt * N + 2 * NO + c * 16, p2);
-          tmem_wait_ld();
-          if (lane == 31 || lane == 0) {
-            const uint32_t* src = lane == 31 ? p0 : p2;
-            float4* dst = reinterpret_cast<float4*>(&xch[grp][mt * 4 + q][lane == 31 ? 0 : 1][c * 16]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              dst[k] = make_float4(__uint_as_float(src[4 * k]), __uint_as_float(src[4 * k + 1]),
-                                   __uint_as_float(src[4 * k + 2]), __uint_as_float(src[4 * k + 3]));
-          }
-        }
-      }
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-      // pass 2: combine and store.  Branch-free: every lane issues the shuffles and
-      // the (broadcast) exchange reads; lanes 0 / 31 select the exchanged values.
-      // (unrolled: the prefetched rows pre[mt] stay in registers)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int r = mt * 128 + q * 32 + lane;
         const int slot = mt * 4 + q;
-        const int su = slot > 0 ? slot - 1 : 0, sd = slot < MT * 4 - 1 ? slot + 1 : slot;
-        float v[NO];
 #pragma unroll
         for (int c = 0; c < NO / 16; ++c) {
           uint32_t p0[16], p1[16], p2[16];
           tmem_ld16_nw(tb + mt * N + c * 16, p0);
           tmem_ld16_nw(tb + mt * N + NO + c * 16, p1);
           tmem_ld16_nw(tb + mt * N + 2 * NO + c * 16, p2);
-          float eu[16], ed[16];
-          const float4* xu = reinterpret_cast<const float4*>(&xch[grp][su][0][c * 16]);
-          const float4* xd = reinterpret_cast<const float4*>(&xch[grp][sd][1][c * 16]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float4 a4 = xu[k], b4 = xd[k];
-            eu[4 * k] = a4.x; eu[4 * k + 1] = a4.y; eu[4 * k + 2] = a4.z; eu[4 * k + 3] = a4.w;
-            ed[4 * k] = b4.x; ed[4 * k + 1] = b4.y; ed[4 * k + 2] = b4.z; ed[4 * k + 3] = b4.w;
-          }
           tmem_wait_ld();
-          float up[16], dn[16];
+          // (up + D1) + dn with the lane-0 up / lane-31 dn masked out by an exact
+          // multiply by 0 (one FFMA each instead of a select and an add)
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
-            up[k] = __shfl_up_sync(0xffffffffu, __uint_as_float(p0[k]), 1);     // D[r-1] part 0
-            dn[k] = __shfl_down_sync(0xffffffffu, __uint_as_float(p2[k]), 1);   // D[r+1] part 2
+            const float up = __shfl_up_sync(0xffffffffu, __uint_as_float(p0[k]), 1);     // D[r-1] part 0
+            const float dn = __shfl_down_sync(0xffffffffu, __uint_as_float(p2[k]), 1);   // D[r+1] part 2
+            v[mt][c * 16 + k] = fmaf(dn, m_dn, fmaf(up, m_up, __uint_as_float(p1[k])));
           }
+          // the part the neighbouring quarter's edge row needs
+          if (lane == 31) {
+            float4* dst = reinterpret_cast<float4*>(xb + (slot * 2 + 0) * NO + c * 16);
 #pragma unroll
-          for (int k = 0; k < 16; ++k)
-            v[c * 16 + k] = (lane == 0 ? eu[k] : up[k]) + __uint_as_float(p1[k]) +
-                            (lane == 31 ? ed[k] : dn[k]);
-        }
-        const int64_t m = g0 + r;
-        if (r >= 1 && r <= TM - 2 && m < a.M) {
-          if constexpr (EpiPre<Epi>::n > 0) e.store(m, v, pre[mt]);
-          else e.store(m, v);
+            for (int k = 0; k < 4; ++k)
+              dst[k] = make_float4(__uint_as_float(p0[4 * k]), __uint_as_float(p0[4 * k + 1]),
+                                   __uint_as_float(p0[4 * k + 2]), __uint_as_float(p0[4 * k + 3]));
+          }
+          if (lane == 0) {
+            float4* dst = reinterpret_cast<float4*>(xb + (slot * 2 + 1) * NO + c * 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              dst[k] = make_float4(__uint_as_float(p2[4 * k]), __uint_as_float(p2[4 * k + 1]),
+                                   __uint_as_float(p2[4 * k + 2]), __uint_as_float(p2[4 * k + 3]));
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      // the exchange buffer is rewritten by this group's next tile only after all
-      // four warps have read it
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+      if (lane == 0) mbar_arrive(&tempty[grp]);
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // exchange written
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int r = mt * 128 + q * 32 + lane;
+        const int slot = mt * 4 + q;
+        const int64_t m = g0 + r;
+        if (!(r >= 1 && r <= TM - 2 && m < a.M)) continue;   // also slot 0 lane 0 / last slot lane 31
+        if (lane == 0) {   // edge rows: D[g-1] + partial / partial + D[g+1]
+          const float4* nb = reinterpret_cast<const float4*>(xb + ((slot - 1) * 2 + 0) * NO);
+#pragma unroll
+          for (int k = 0; k < NO / 4; ++k) {
+            const float4 y = nb[k];
+            v[mt][4 * k] = y.x + v[mt][4 * k]; v[mt][4 * k + 1] = y.y + v[mt][4 * k + 1];
+            v[mt][4 * k + 2] = y.z + v[mt][4 * k + 2]; v[mt][4 * k + 3] = y.w + v[mt][4 * k + 3];
+          }
+        }
+        if (lane == 31) {
+          const float4* nb = reinterpret_cast<const float4*>(xb + ((slot + 1) * 2 + 1) * NO);
+#pragma unroll
+          for (int k = 0; k < NO / 4; ++k) {
+            const float4 y = nb[k];
+            v[mt][4 * k] += y.x; v[mt][4 * k + 1] += y.y; v[mt][4 * k + 2] += y.z; v[mt][4 * k + 3] += y.w;
+          }
+        }
+        epi_store(e, m, v[mt], pre[mt]);
+      }
+      ++gt;
     }
   }
   __syncthreads();
@@ -615,7 +622,7 @@ __global__ void __launch_bounds__(WCF_THREADS, 1)
   }
 }
 
-template <class Epi, int RB, int MT>
+template <class Epi, int RB, int MT, int NG>
 seed_status launch_win_conv_kx(const WinConvArgs& a, const Epi& e, cudaStream_t st) {
   constexpr int WB = 3 * 3 * Epi::N * RB;
   constexpr int TM = 128 * MT, TS = TM - 2;
@@ -623,15 +630,16 @@ seed_status launch_win_conv_kx(const WinConvArgs& a, const Epi& e, cudaStream_t 
   const int mx = std::max(a.off[0], std::max(a.off[1], a.off[2]));
   const int slab = (int)align_up((size_t)(TM + mx - mn) * RB + 1024, 1024);
   const int wbytes = (int)align_up(WB, 1024);
-  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - wbytes) / slab);
+  const int xbytes = NG * 2 * MT * 4 * 2 * Epi::N * 4;   // exchange
+  const int stages = std::min(WC_MAX_STAGES, (WC_SMEM_BUDGET - wbytes - xbytes) / slab);
   if (a.M <= 0) return a.M == 0 ? SEED_OK : SEED_E_SHAPE;
   if (stages < 2) return SEED_E_SHAPE;
-  const size_t smem = (size_t)wbytes + (size_t)stages * slab + 1024;
+  const size_t smem = (size_t)wbytes + (size_t)stages * slab + xbytes + 1024;
   static PerDevice attr;
-  SEED_TRY(smem_optin(attr, win_conv_kx_kernel<Epi, RB, MT>, WC_SMEM_BUDGET + 2048));
+  SEED_TRY(smem_optin(attr, win_conv_kx_kernel<Epi, RB, MT, NG>, WC_SMEM_BUDGET + 2048));
   const int64_t tiles = (a.M + TS - 1) / TS;
   const int grid = (int)std::min<int64_t>(tiles, sm_count());
-  return launch_k(win_conv_kx_kernel<Epi, RB, MT>, dim3(grid), dim3(WCF_THREADS), smem, st, a, e,
+  return launch_k(win_conv_kx_kernel<Epi, RB, MT, NG>, dim3(grid), dim3(64 + 128 * NG), smem, st, a, e,
                   stages, slab);
 }
 
@@ -684,7 +692,7 @@ __global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0),
   constexpr int ACOL = NW <= 64 ? 64 : NW <= 128 ? 128 : 256;   // columns per accumulator
   constexpr uint32_t TCOLS = NMMA * ACOL <= 64 ? 64 : NMMA * ACOL <= 128 ? 128 : NMMA * ACOL <= 256 ? 256 : 512;
   extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_align1024(smraw);
   uint8_t* stg = sm + 1024;
   const size_t sst = (size_t)a_bytes + b_bytes + stg_bytes;   // stage stride
   __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull;
