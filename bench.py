@@ -50,6 +50,10 @@ CONFIGS = {
 CONFIGS["c3m"] = dict(T=100, B=32, A=15, repeat=4, batch_kw={},
                       workload="c3m DMLab IMPALA-deep Medium (2x filters: 32,64,64) + LSTM256 learner "
                                "step (P:411): 72x96x3 uint8, A=15, T=100, B=32/GPU")
+CONFIGS["c3l"] = dict(T=100, B=32, A=15, repeat=4, batch_kw={},
+                      workload="c3l DMLab IMPALA-deep Large (4x filters: 64,128,128; 128-channel "
+                               "tensors as two 64-channel planes) + LSTM256 learner step (P:411, "
+                               "P:434): 72x96x3 uint8, A=15, T=100, B=32/GPU")
 CONFIGS["c4l"] = dict(T=32, B=128, A=19, repeat=1, batch_kw=dict(smm=True),
                       workload="c4l Google Research Football Large SMM 144x108 (P:358), IMPALA-deep "
                                "(16,32,32,32) + LSTM256 learner step: 108x144x16 uint8, A=19, T=32, "
@@ -82,7 +86,8 @@ def deep_geometry(cfg):
     """IMPALA-deep sections (C14): (H, W, cin, cin_rows, ch, H2, W2) per section."""
     H, W = (108, 144) if cfg == "c4l" else (72, 96)
     C = 3 if cfg.startswith("c3") else 16
-    chans = ((32, 64, 64) if cfg == "c3m" else (16, 32, 32)) if cfg.startswith("c3") else (16, 32, 32, 32)
+    chans = {"c3m": (32, 64, 64), "c3l": (64, 128, 128)}.get(cfg, (16, 32, 32)) if cfg.startswith("c3") \
+        else (16, 32, 32, 32)
     out, cin, cinp = [], C, 16
     for ch in chans:
         H2, W2 = (H + 1) // 2, (W + 1) // 2
@@ -139,6 +144,36 @@ def launch_work(cfg, T, B, A, P, names):
     geo = deep_geometry(cfg)
     ns = len(geo)
     tw = core_work(F, B, T, A, geo[-1][5] * geo[-1][6] * geo[-1][4], P)
+    # the (section, fraction of its work) of each launch of a phase name, in launch
+    # order: sections ascending forward, descending backward; 128-channel sections
+    # run as 64-channel plane pairs (learner.cu plane_section_*), each launch a
+    # 1/(planes) share of the section's op
+    fuse = os.environ.get("SEED_FUSE_POOL") != "0"
+    seq = {}
+
+    def add(name, s, n):
+        seq.setdefault(name, []).extend([(s, 1.0 / n)] * n)
+    for s, (H, W, cin, cinp, ch, H2, W2) in enumerate(geo):
+        npo, npi = (2 if ch > 64 else 1), (2 if cinp > 64 else 1)
+        fused = fuse and ch <= 32 and cinp <= 32
+        if fused:
+            add("deep_conv_pool", s, 1)
+        else:
+            add("deep_conv_fwd", s, npo * npi)
+            add("deep_pool_fwd", s, npo)
+        for _ in range(2):
+            add("deep_res_fwd0", s, npo * npo)
+            add("deep_res_fwd1", s, npo * npo)
+    for s in range(ns - 1, -1, -1):
+        H, W, cin, cinp, ch, H2, W2 = geo[s]
+        npo, npi = (2 if ch > 64 else 1), (2 if cinp > 64 else 1)
+        for _ in range(2):
+            for nm in ("deep_res_wgrad1", "deep_res_dgrad1", "deep_res_wgrad0", "deep_res_dgrad0"):
+                add(nm, s, npo * npo)
+        add("deep_pool_bwd", s, npo)
+        add("deep_conv_wgrad", s, npo * npi)
+        if s > 0:
+            add("deep_conv_dgrad", s, npo * npi)
     seen = {}
     for n in names:
         k = seen.get(n, 0)
@@ -146,17 +181,14 @@ def launch_work(cfg, T, B, A, P, names):
         if not n.startswith("deep_") and n != "obs_bf16":
             out.append(tw.get(n, (0, 0)))
             continue
-        fwd = "_fwd" in n or n == "deep_conv_pool"
         if n == "obs_bf16":
             H, W, cin, cinp = geo[0][0], geo[0][1], geo[0][2], geo[0][3]
             out.append((0, F * H * W * (cin + cinp * 2)))
             continue
-        if n.startswith("deep_res"):
-            s = k // 2 if fwd else ns - 1 - k // 2
-        else:
-            s = k if fwd else ns - 1 - k
-            if n == "deep_conv_dgrad":
-                s = ns - 1 - k
+        if n not in seq or k >= len(seq[n]):
+            out.append((0, 0))
+            continue
+        s, frac = seq[n][k]
         H, W, cin, cinp, ch, H2, W2 = geo[s]
         Ai, Ao = F * H * W, F * H2 * W2
         # section 0 reads the converted bf16 rows (obs_bf16: 16 planes, or DMLab's
@@ -187,7 +219,7 @@ def launch_work(cfg, T, B, A, P, names):
             w = (2 * Ai * 9 * cin * ch, Ai * ch * 2 + Ai * cin * 2)
         else:
             w = (0, 0)
-        out.append(w)
+        out.append((w[0] * frac, w[1] * frac))
     return out
 
 
@@ -826,7 +858,7 @@ def run_ours(args):
     if not args.no_extra:
         # the other learner configs (fewer timed steps) and inference, on every rank
         for cfg, k in (("c2", max(20, min(args.steps, 100))), ("c3", max(5, min(args.steps, 20))),
-                       ("c3m", 5), ("c4l", 5)):
+                       ("c3m", 5), ("c3l", 3), ("c4l", 5)):
             r = measure_learner(S, torch, dist, cfg, k, 3, world, rank, local, comm, clocks=False,
                                 e2e=False)
             extra[cfg] = {"workload": CONFIGS[cfg]["workload"], "steps": k,

@@ -116,8 +116,9 @@ typedef struct {
   int num_actions;                /* A >= 2                               */
   int lstm_units;                 /* 0 for the MLP; 256 for the conv nets        */
   int torso_width;                /* IMPALA-deep channel multiplier: 0/1 = (16, 32,
-                                     32[, 32]), 2 = DMLab "Medium 2x" (32, 64, 64)
-                                     (P:411); others SEED_E_UNSUPPORTED */
+                                     32[, 32]), 2 = DMLab "Medium 2x" (32, 64, 64),
+                                     4 = DMLab "Large 4x" (64, 128, 128; P:411,
+                                     P:432-434); others SEED_E_UNSUPPORTED        */
 } seed_net_spec;
 
 seed_status seed_net_param_count(const seed_net_spec* spec, int64_t* n_out /* host */);

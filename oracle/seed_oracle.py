@@ -96,6 +96,11 @@ def spec_c3_medium(num_actions=15):
     return spec_c3(num_actions, width=2)
 
 
+def spec_c3_large(num_actions=15):
+    """P:411, P:434 DMLab Large: 4x filters (64, 128, 128)."""
+    return spec_c3(num_actions, width=4)
+
+
 def spec_c4(num_actions=19, obs_h=72, obs_w=96):
     """BJ configs[3]: GRF SMM 72x96x16, IMPALA-deep block (16,32,32,32) + LSTM256.
     P:358: the SMM is 96 x 72 by default, Medium 120 x 90, Large 144 x 108

@@ -203,6 +203,8 @@ def spec_for_config(cfg):
         "c4l": NetSpec(NET_GFOOTBALL, 108, 144, 16, 19, 256),
         # DMLab ResNet "Medium 2x" filters (32, 64, 64)
         "c3m": NetSpec(NET_IMPALA_DEEP, 72, 96, 3, 15, 256, 2),
+        # DMLab ResNet "Large 4x" filters (64, 128, 128)
+        "c3l": NetSpec(NET_IMPALA_DEEP, 72, 96, 3, 15, 256, 4),
     }[cfg]
 
 

@@ -25,6 +25,9 @@ struct W3FwdEpi {
   uint8_t* out;
   uint8_t* outr;
   bf16* dense;
+  int dense_ct, dense_off;
+  float* part_out;
+  const float* part_in;
   __device__ void pre(int64_t m, uint4 (&p)[PRE > 0 ? PRE : 1]) const {
 #pragma unroll
     for (int j = 0; j < PRE; ++j) p[j] = __ldg(chunk_at(res, m, RB, j));
@@ -34,6 +37,14 @@ struct W3FwdEpi {
     store(m, v, p);
   }
   __device__ void store(int64_t m, float (&v)[N], const uint4 (&p)[PRE > 0 ? PRE : 1]) const {
+    if constexpr (MODE == W3_PART) {   // the first input plane's fp32 sum (every row)
+      float4* d = reinterpret_cast<float4*>(part_out + m * N);
+#pragma unroll
+      for (int q = 0; q < N / 4; ++q)
+        d[q] = make_float4(v[4 * q] * in_scale, v[4 * q + 1] * in_scale, v[4 * q + 2] * in_scale,
+                           v[4 * q + 3] * in_scale);
+      return;
+    }
     int f, y, x;
     if (!g.split(m, f, y, x)) {
       if (MODE != W3_PLAIN) {
@@ -46,6 +57,16 @@ struct W3FwdEpi {
       }
       return;
     }
+    if (part_in) {   // the other input plane's fp32 sum
+      const float4* ps = reinterpret_cast<const float4*>(part_in + m * N);
+#pragma unroll
+      for (int q = 0; q < N / 4; ++q) {
+        const float4 t = __ldg(ps + q);
+        v[4 * q] = fmaf(v[4 * q], in_scale, t.x); v[4 * q + 1] = fmaf(v[4 * q + 1], in_scale, t.y);
+        v[4 * q + 2] = fmaf(v[4 * q + 2], in_scale, t.z); v[4 * q + 3] = fmaf(v[4 * q + 3], in_scale, t.w);
+      }
+    }
+    const float isc = part_in ? 1.f : in_scale;
     if ((reinterpret_cast<uintptr_t>(bias) & 15) == 0) {   // 16-byte bias loads (the torso's
 #pragma unroll                                              // parameter offsets are multiples of 4)
       for (int q = 0; q < N / 4; ++q) {
@@ -53,14 +74,14 @@ struct W3FwdEpi {
         const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          v[4 * q + k] = v[4 * q + k] * in_scale + bb[k];
+          v[4 * q + k] = v[4 * q + k] * isc + bb[k];
           if (MODE == W3_RELU) v[4 * q + k] = fmaxf(v[4 * q + k], 0.f);
         }
       }
     } else {
 #pragma unroll
       for (int q = 0; q < N; ++q) {
-        v[q] = v[q] * in_scale + __ldg(bias + q);
+        v[q] = v[q] * isc + __ldg(bias + q);
         if (MODE == W3_RELU) v[q] = fmaxf(v[q], 0.f);
       }
     }
@@ -84,7 +105,8 @@ struct W3FwdEpi {
         for (int j = 0; j < N / 8; ++j) *chunk_at(outr, m, RB, j) = pack8(r + 8 * j);
       }
       if (dense) {
-        uint4* d = reinterpret_cast<uint4*>(dense + ((int64_t)f * g.H * g.W + (int64_t)y * g.W + x) * N);
+        const int ct = dense_ct > 0 ? dense_ct : N;
+        uint4* d = reinterpret_cast<uint4*>(dense + ((int64_t)f * g.H * g.W + (int64_t)y * g.W + x) * ct + dense_off);
 #pragma unroll
         for (int j = 0; j < N / 8; ++j) d[j] = pack8(r + 8 * j);
       }
@@ -97,13 +119,15 @@ struct W3DgradEpi {
   static constexpr int N = NN;
   static constexpr int RB = 2 * NN;
   // the mask row, then (D3W_RES) the incoming residual-gradient row
-  static constexpr int PRE = MODE == D3W_PLAIN ? 0 : (MODE == D3W_MASK ? N / 8 : N / 4);
+  static constexpr int PRE = (MODE == D3W_PLAIN || MODE == D3W_PART) ? 0 : (MODE == D3W_MASK ? N / 8 : N / 4);
   PadGeo g;
   const uint8_t* mask;
   const uint8_t* dres;
   uint8_t* dX;
+  float* part_out;
+  const float* part_in;
   __device__ void pre(int64_t m, uint4 (&p)[PRE > 0 ? PRE : 1]) const {
-    if (MODE == D3W_PLAIN) return;
+    if (MODE == D3W_PLAIN || MODE == D3W_PART) return;
 #pragma unroll
     for (int j = 0; j < N / 8; ++j) p[j] = __ldg(chunk_at(mask, m, RB, j));
     if (MODE == D3W_RES) {
@@ -116,12 +140,26 @@ struct W3DgradEpi {
     store(m, v, p);
   }
   __device__ void store(int64_t m, float (&v)[N], const uint4 (&p)[PRE > 0 ? PRE : 1]) const {
+    if constexpr (MODE == D3W_PART) {   // the first dY plane's fp32 sum (every row)
+      float4* d = reinterpret_cast<float4*>(part_out + m * N);
+#pragma unroll
+      for (int q = 0; q < N / 4; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      return;
+    }
     int f, y, x;
     if (!g.split(m, f, y, x)) {
       const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int j = 0; j < N / 8; ++j) *chunk_at(dX, m, RB, j) = z;
       return;
+    }
+    if (part_in) {
+      const float4* ps = reinterpret_cast<const float4*>(part_in + m * N);
+#pragma unroll
+      for (int q = 0; q < N / 4; ++q) {
+        const float4 t = __ldg(ps + q);
+        v[4 * q] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
+      }
     }
     if (MODE != D3W_PLAIN) {
 #pragma unroll
@@ -207,7 +245,8 @@ static seed_status fwd_t(const Conv3wFwd& a, cudaStream_t st) {
   if (XF == XF_U8) w.u8 = u8_rows(a.obs_u8, a.g);
   W3FwdEpi<MODE, N> e{};
   e.g = a.g; e.in_scale = a.in_scale; e.bias = a.bias; e.res = a.res; e.out = a.out;
-  e.outr = a.outr; e.dense = a.dense;
+  e.outr = a.outr; e.dense = a.dense; e.dense_ct = a.dense_ct; e.dense_off = a.dense_off;
+  e.part_out = a.part_out; e.part_in = a.part_in;
   if constexpr (NW == 9 && XF == XF_NONE && N <= 32) {
     if (kx_stacked<N, RB>()) {   // 3 row windows ky, column taps stacked on N
       for (int k = 0; k < 3; ++k) w.off[k] = (k - 1) * a.g.Wp;
@@ -234,6 +273,7 @@ static seed_status fwd_mode(const Conv3wFwd& a, cudaStream_t st) {
   if (a.xim) {
     if (a.ch == 16 && a.cin_p == 16) return fwd_t<MODE, 16, 32, 3>(a, st);
     if (a.ch == 32 && a.cin_p == 16) return fwd_t<MODE, 32, 32, 3>(a, st);
+    if (a.ch == 64 && a.cin_p == 16) return fwd_t<MODE, 64, 32, 3>(a, st);   // DMLab 4x
     return SEED_E_UNSUPPORTED;
   }
   if (a.ch == 16 && a.cin_p == 16) return fwd_t<MODE, 16, 32, 9>(a, st);
@@ -249,6 +289,8 @@ seed_status conv3w_forward(const Conv3wFwd& a, cudaStream_t st) {
   if (a.mode == W3_PLAIN) return fwd_mode<W3_PLAIN>(a, st);
   if (a.mode == W3_RELU && !a.xim) return fwd_mode<W3_RELU>(a, st);
   if (a.mode == W3_RES && !a.xim) return fwd_mode<W3_RES>(a, st);
+  if (a.mode == W3_PART && !a.xim && a.xf == XF_NONE && a.ch == 64 && a.cin_p == 64 && a.part_out)
+    return fwd_t<W3_PART, 64, 128, 9>(a, st);   // plane pairs of the 4x torso
   return SEED_E_UNSUPPORTED;
 }
 
@@ -261,7 +303,7 @@ static seed_status dgrad_t(const Conv3wDgrad& a, cudaStream_t st) {
   // row windows ky at -(ky-1)*Wp; the image stacks the column taps as groups 2 - kx
   // (win3_img_pos mode 1), so out[g] = D[g-1][grp 0] + D[g][grp 1] + D[g+1][grp 2]
   W3DgradEpi<MODE, N> e{};
-  e.g = a.g; e.mask = a.mask; e.dres = a.dres; e.dX = a.dX;
+  e.g = a.g; e.mask = a.mask; e.dres = a.dres; e.dX = a.dX; e.part_out = a.part_out; e.part_in = a.part_in;
   if constexpr (N <= 32) {
     if (kx_stacked<N, RB>()) {   // 3 row windows at -(ky-1)*Wp, column taps stacked on N
       for (int k = 0; k < 3; ++k) w.off[k] = -(k - 1) * a.g.Wp;
@@ -288,6 +330,7 @@ seed_status conv3w_dgrad(const Conv3wDgrad& a, cudaStream_t st) {
   if (a.mode == D3W_PLAIN) return dgrad_mode<D3W_PLAIN>(a, st);
   if (a.mode == D3W_MASK) return dgrad_mode<D3W_MASK>(a, st);
   if (a.mode == D3W_RES) return dgrad_mode<D3W_RES>(a, st);
+  if (a.mode == D3W_PART && a.cin == 64 && a.ch == 64 && a.part_out) return dgrad_t<D3W_PART, 64, 128>(a, st);
   return SEED_E_UNSUPPORTED;
 }
 
@@ -297,6 +340,7 @@ seed_status conv3w_dgrad(const Conv3wDgrad& a, cudaStream_t st) {
 //   x-im2col input: dW[co][ky][(kx, c)] = sum_h X[h][(kx, c)] dY[h - Wp + j*Wp][co] (atom 0)
 struct W3Fin3 {
   int xim, Cp, CI, CO;
+  int ci_full, co_off, c_off;   // the [co_off..][3][3][c_off..] block of a [..][3][3][ci_full] tensor
   float scale;
   float* g_w;
   float* g_b;
@@ -314,7 +358,7 @@ struct W3Fin3 {
       if (atom >= 3 || ch >= CI) return;
       kx = atom; c = ch;
     }
-    g_w[(((size_t)co * 3 + ky) * 3 + kx) * CI + c] = t * scale;
+    g_w[(((size_t)(co_off + co) * 3 + ky) * 3 + kx) * ci_full + c_off + c] = t * scale;
   }
   __device__ void bias(int n, float t) const { g_b[n] = t; }
 };
@@ -332,6 +376,9 @@ seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
   W3Fin3 f{};
   f.xim = a.xim ? 1 : 0; f.Cp = a.cin_p; f.CI = a.cin; f.CO = a.ch; f.scale = a.scale; f.g_w = a.g_w;
   f.g_b = a.g_b;
+  f.ci_full = a.ci_full > 0 ? a.ci_full : a.cin; f.co_off = a.co_off; f.c_off = a.c_off;
+  const bool bias = !a.xim && a.g_b;
+  if (a.xim && !a.g_b) return SEED_E_ARG;   // x-im2col: the bias comes with the weights
   if (a.xf == XF_U8) {
     if (a.ch == 16 && a.cin_p == 16 && !a.xim && a.obs_u8)
       return launch_win3_wgrad<16, 32, W3Fin3, 3, XF_U8>(w, f, true, st);
@@ -342,12 +389,13 @@ seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
     if (a.ch == 32 && a.cin_p == 32 && !a.xim) return launch_win3_wgrad<32, 64, W3Fin3, 3, XF_RELU>(w, f, true, st);
     return SEED_E_UNSUPPORTED;
   }
-  if (a.ch == 16 && a.cin_p == 16) return launch_win3_wgrad<16, 32>(w, f, !a.xim, st);
-  if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, !a.xim, st);
-  if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, !a.xim, st);
-  if (a.ch == 32 && a.cin_p == 32) return launch_win3_wgrad<32, 64>(w, f, !a.xim, st);
-  if (a.ch == 64 && a.cin_p == 32) return launch_win3_wgrad<64, 64>(w, f, !a.xim, st);
-  if (a.ch == 64 && a.cin_p == 64) return launch_win3_wgrad<64, 128>(w, f, !a.xim, st);
+  if (a.ch == 16 && a.cin_p == 16) return launch_win3_wgrad<16, 32>(w, f, bias, st);
+  if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, bias, st);
+  if (a.ch == 64 && a.cin_p == 16) return launch_win3_wgrad<64, 32>(w, f, bias, st);   // DMLab 4x s0
+  if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, bias, st);
+  if (a.ch == 32 && a.cin_p == 32) return launch_win3_wgrad<32, 64>(w, f, bias, st);
+  if (a.ch == 64 && a.cin_p == 32) return launch_win3_wgrad<64, 64>(w, f, bias, st);
+  if (a.ch == 64 && a.cin_p == 64) return launch_win3_wgrad<64, 128>(w, f, bias, st);
   return SEED_E_UNSUPPORTED;
 }
 

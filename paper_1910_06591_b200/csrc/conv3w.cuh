@@ -53,14 +53,25 @@ struct PadGeo {
 seed_status conv3_obs(const uint8_t* obs, int64_t F, const PadGeo& g, int C, int Cp, bool xim,
                       uint8_t* X0, cudaStream_t st);
 
-enum { W3_PLAIN = 0, W3_RELU = 1, W3_RES = 2 };    // forward epilogues
-enum { D3W_PLAIN = 0, D3W_MASK = 1, D3W_RES = 2 };  // data-gradient epilogues
+enum { W3_PLAIN = 0, W3_RELU = 1, W3_RES = 2, W3_PART = 3 };    // forward epilogues
+enum { D3W_PLAIN = 0, D3W_MASK = 1, D3W_RES = 2, D3W_PART = 3 };  // data-gradient epilogues
+
+// 128-channel tensors (the DMLab 4x torso) are stored as two 64-channel planes,
+// each a padded row space of 128-byte rows (plane q at base + q * rows * 128); a
+// 3x3 conv between such tensors is the sum over input planes p of the 64 -> 64
+// convs into each output plane q.  The first input plane's conv stores its fp32
+// accumulator (W3_PART / D3W_PART, `part_out`, [rows][64]); the second adds it
+// (`part_in`) before its epilogue — one fp32 sum, one bf16 rounding, as a single
+// conv over 128 input channels.
 
 // Forward 3x3 conv (9 windows, or 3 for the x-im2col section-0 input).
 //   W3_PLAIN: out = acc*in_scale + b  (section conv; border rows not written)
 //   W3_RELU:  out = relu(acc + b)
 //   W3_RES:   out = res + acc + b, outr (nullable) = relu(out), dense (nullable) =
-//             relu(out) as [f][(y*W + x)*ch + c] (the FC input)
+//             relu(out) as [f][(y*W + x)*dense_ct + dense_off + c] (the FC input;
+//             dense_ct 0 = ch)
+//   W3_PART:  part_out[g][c] = acc*in_scale (fp32, every row); other modes add
+//             part_in[g][c] (nullable) to acc*in_scale before the bias
 // xf (win_engine.cuh): XF_RELU = the conv reads relu(in) (relu applied to the slab in
 // shared memory); XF_U8 = `in` is ignored and the input rows are the uint8 obs
 // [F][H][W][16] `obs_u8` expanded in shared memory (section 0 of the GRF net)
@@ -79,11 +90,15 @@ struct Conv3wFwd {
   uint8_t* out;
   uint8_t* outr;
   bf16* dense;
+  int dense_ct, dense_off;
+  float* part_out;
+  const float* part_in;
 };
 seed_status conv3w_forward(const Conv3wFwd& a, cudaStream_t st);
 
 // Data gradient dX[g][ci] = sum_w dY[g - off_w] . Wdg_w[ci], into rows of cin channels
 //   D3W_PLAIN: dX = acc;  D3W_MASK: dX = acc*(mask > 0);  D3W_RES: dX = dres + acc*(mask > 0)
+//   D3W_PART: part_out[g][c] = acc; other modes: acc += part_in[g][c] (nullable) first
 struct Conv3wDgrad {
   int mode, cin, ch;      // dX channels (16 / 32), dY channels
   PadGeo g;
@@ -93,6 +108,8 @@ struct Conv3wDgrad {
   const uint8_t* mask;
   const uint8_t* dres;
   uint8_t* dX;
+  float* part_out;
+  const float* part_in;
 };
 seed_status conv3w_dgrad(const Conv3wDgrad& a, cudaStream_t st);
 
@@ -110,8 +127,10 @@ struct Conv3wWgrad {
   const uint8_t* X;
   const uint8_t* dY;
   float* part;
-  float* g_w;             // fp32 [ch][3][3][cin]
-  float* g_b;             // fp32 [ch]
+  float* g_w;             // fp32 [ch][3][3][cin] (or the block [co_off..][..][..][c_off..] of
+                          // a [..][3][3][ci_full] tensor: plane pairs of the 4x torso)
+  float* g_b;             // fp32 [ch] (nullptr: no bias gradient)
+  int ci_full, co_off, c_off;
 };
 seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st);
 size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool xim);
@@ -186,8 +205,30 @@ __host__ __device__ inline int64_t win3_img_pos(int mode, int CI, int CO, int RB
   else { row = ky * CO + co; k = kx * CI + c; }
   return (int64_t)row * (RB / 2) + swz_chunk(row, RB, k / 8) * 8 + (k % 8);
 }
-inline int64_t win3_img_elems(int mode, int CI, int CO, int RB) {
+__host__ __device__ inline int64_t win3_img_elems(int mode, int CI, int CO, int RB) {
   return (int64_t)(mode == 0 ? 9 * CO : mode == 1 ? 9 * CI : 3 * CO) * (RB / 2);
+}
+// Plane-pair images of a conv with more than 64 input or output channels: the
+// 64 -> 64 sub-images (q = output plane, p = input plane) one after another, each
+// 1024-byte aligned, sub-image (q, p) at index q * npi + p (mode 1 (data gradient)
+// uses the same index: the dX plane p sums over the dY planes q).  RB = the
+// sub-conv's row bytes (128).
+__host__ __device__ inline int64_t win3p_sub_elems(int mode, int CI, int CO, int RB) {
+  const int ci = CI > 64 ? 64 : CI, co = CO > 64 ? 64 : CO;
+  return (win3_img_elems(mode, ci, co, RB) + 511) & ~(int64_t)511;
+}
+__host__ __device__ inline int64_t win3p_img_pos(int mode, int CI, int CO, int RB, int64_t e) {
+  if (CI <= 64 && CO <= 64) return win3_img_pos(mode, CI, CO, RB, e);
+  const int c = (int)(e % CI);
+  const int64_t r = e / CI;
+  const int k = (int)(r % 9), co = (int)(r / 9);
+  const int ci_s = CI > 64 ? 64 : CI, co_s = CO > 64 ? 64 : CO, npi = CI > 64 ? 2 : 1;
+  const int64_t es = ((int64_t)(co % 64) * 9 + k) * ci_s + c % 64;
+  return ((co / 64) * npi + c / 64) * win3p_sub_elems(mode, CI, CO, RB) +
+         win3_img_pos(mode, ci_s, co_s, RB, es);
+}
+inline int64_t win3p_img_elems(int mode, int CI, int CO, int RB) {
+  return (int64_t)(CI > 64 ? 2 : 1) * (CO > 64 ? 2 : 1) * win3p_sub_elems(mode, CI, CO, RB);
 }
 
 }  // namespace seed

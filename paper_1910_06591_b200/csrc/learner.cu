@@ -377,6 +377,142 @@ static bool store_conv_rows() {
   return e && e[0] == '1';
 }
 
+// ---- 128-channel sections (DMLab 4x torso): two 64-channel planes per tensor
+// (conv3w.cuh); every conv is the plane-pair 64 -> 64 convs, the first input plane's
+// fp32 sum carried to the second (W3_PART / D3W_PART, workspace part3).
+static uint8_t* plane_at(const StepCtx& c, size_t off, int q, int64_t rows) {
+  return c.at<uint8_t>(off) + (size_t)q * rows * 128;   // 64 bf16 channels per row
+}
+static int64_t w3_sub(const DeepSec& d, int mode, bool res) {
+  const int ci = res ? d.ch : d.cin;
+  const int rb = 2 * std::min(mode == 1 ? d.ch : (res ? d.ch : d.cinp), 64);
+  return win3p_sub_elems(mode, ci, d.ch, rb);
+}
+
+static seed_status plane_section_forward(const StepCtx& c, int s, const bf16* lowp, const float* params,
+                                         cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int64_t F = w.F;
+  const DeepSec& d = p.sec[s];
+  const LearnerWs::Sec& b = w.sec[s];
+  const PadGeo gi = PadGeo::make(d.H, d.W), go = PadGeo::make(d.H2, d.W2);
+  const int64_t ri = F * gi.P, ro = F * go.P;
+  const int npo = d.ch > 64 ? 2 : 1, npi = d.cinp > 64 ? 2 : 1;
+  const int cpi = std::min(d.cinp, 64);
+  float* part = c.at<float>(w.part3);
+  if (d.xim || !part) return SEED_E_UNSUPPORTED;
+  for (int q = 0; q < npo; ++q) {
+    for (int pi = 0; pi < npi; ++pi) {
+      Conv3wFwd a{};
+      a.mode = pi + 1 < npi ? W3_PART : W3_PLAIN; a.cin_p = cpi; a.ch = 64; a.g = gi; a.rows = ri;
+      a.in_scale = 1.f;
+      a.in = npi > 1 ? plane_at(c, w.sec[s - 1].h[2], pi, ri) : c.at<uint8_t>(w.sec[s - 1].h[2]);
+      a.wimg = lowp + d.im_w + (q * npi + pi) * w3_sub(d, 0, false);
+      a.bias = params + p.t[d.t_b].off + 64 * q;
+      a.out = plane_at(c, b.conv, q, ri);
+      a.part_out = part; a.part_in = pi > 0 ? part : nullptr;
+      SEED_TRY(conv3w_forward(a, st));
+      c.mark("deep_conv_fwd");
+    }
+    SEED_TRY(conv3w_pool_fwd(F, gi, go, 64, d.pt, d.pl, plane_at(c, b.conv, q, ri), plane_at(c, b.h[0], q, ro),
+                             plane_at(c, b.hr[0], q, ro), c.at<uint8_t>(b.arg) + (size_t)q * ro * 64, st));
+    c.mark("deep_pool_fwd");
+  }
+  for (int r = 0; r < 2; ++r) {
+    for (int j = 0; j < 2; ++j)   // conv0: relu(h) -> u1 (W3_RELU); conv1: u1 -> h + conv (W3_RES)
+      for (int q = 0; q < npo; ++q)
+        for (int pi = 0; pi < npo; ++pi) {
+          Conv3wFwd a{};
+          a.mode = pi + 1 < npo ? W3_PART : (j == 0 ? W3_RELU : W3_RES);
+          a.cin_p = 64; a.ch = 64; a.g = go; a.rows = ro; a.in_scale = 1.f;
+          a.in = plane_at(c, j == 0 ? b.hr[r] : b.u1[r], pi, ro);
+          a.wimg = lowp + d.im_rw[r][j] + (q * npo + pi) * w3_sub(d, 0, true);
+          a.bias = params + p.t[d.t_rb[r][j]].off + 64 * q;
+          a.part_out = part; a.part_in = pi > 0 ? part : nullptr;
+          if (j == 0) {
+            a.out = plane_at(c, b.u1[r], q, ro);
+          } else {
+            a.res = plane_at(c, b.h[r], q, ro);
+            a.out = plane_at(c, b.h[r + 1], q, ro); a.outr = plane_at(c, b.hr[r + 1], q, ro);
+            if (s == p.nsec - 1 && r == 1) { a.dense = c.at<bf16>(w.act2); a.dense_ct = d.ch; a.dense_off = 64 * q; }
+          }
+          SEED_TRY(conv3w_forward(a, st));
+          c.mark(j == 0 ? "deep_res_fwd0" : "deep_res_fwd1");
+        }
+  }
+  return SEED_OK;
+}
+
+static seed_status plane_section_backward(const StepCtx& c, int s, const bf16* lowp, const float* params,
+                                          float* grads, cudaStream_t st) {
+  const NetPlan& p = *c.p;
+  const LearnerWs& w = c.w;
+  const int64_t F = w.F;
+  const DeepSec& d = p.sec[s];
+  const LearnerWs::Sec& b = w.sec[s];
+  const PadGeo gi = PadGeo::make(d.H, d.W), go = PadGeo::make(d.H2, d.W2);
+  const int64_t ri = F * gi.P, ro = F * go.P;
+  const int npo = d.ch > 64 ? 2 : 1, npi = d.cinp > 64 ? 2 : 1;
+  const int cpi = std::min(d.cinp, 64);
+  float* part = c.at<float>(w.part3);
+  float* wpart = c.at<float>(w.splitk);
+  size_t cur = b.dhA, oth = b.dhB;
+  auto wgrad = [&](const uint8_t* X, int xplanes, int cinp, const uint8_t* dY, int64_t rows, const PadGeo& g,
+                   int ci_full, int ti_w, int ti_b, const char* name) -> seed_status {
+    for (int q = 0; q < npo; ++q)
+      for (int pi = 0; pi < xplanes; ++pi) {
+        Conv3wWgrad wg{};
+        wg.cin_p = cinp; wg.cin = cinp; wg.ch = 64; wg.g = g; wg.rows = rows; wg.scale = 1.f;
+        wg.X = X + (size_t)pi * rows * 2 * cinp; wg.dY = dY + (size_t)q * rows * 128; wg.part = wpart;
+        wg.g_w = grads + p.t[ti_w].off; wg.ci_full = ci_full; wg.co_off = 64 * q; wg.c_off = cinp * pi;
+        wg.g_b = pi == 0 ? grads + p.t[ti_b].off + 64 * q : nullptr;
+        SEED_TRY(conv3w_wgrad(wg, st));
+        c.mark(name, 2);
+      }
+    return SEED_OK;
+  };
+  // dX plane pi = sum over dY planes q (D3W_PART then the final mode)
+  auto dgrad = [&](int mode, const uint8_t* dY, int64_t rows, const PadGeo& g, int64_t im, int64_t sub,
+                   int xplanes, const uint8_t* mask, const uint8_t* dres, uint8_t* dX, const char* name) -> seed_status {
+    for (int pi = 0; pi < xplanes; ++pi)
+      for (int q = 0; q < npo; ++q) {
+        Conv3wDgrad dg{};
+        dg.mode = q + 1 < npo ? D3W_PART : mode; dg.cin = 64; dg.ch = 64; dg.g = g; dg.rows = rows;
+        dg.dY = dY + (size_t)q * rows * 128; dg.wimg = lowp + im + (q * xplanes + pi) * sub;
+        dg.mask = mask ? mask + (size_t)pi * rows * 128 : nullptr;
+        dg.dres = dres ? dres + (size_t)pi * rows * 128 : nullptr;
+        dg.dX = dX + (size_t)pi * rows * 128;
+        dg.part_out = part; dg.part_in = q > 0 ? part : nullptr;
+        SEED_TRY(conv3w_dgrad(dg, st));
+        c.mark(name);
+      }
+    return SEED_OK;
+  };
+  for (int r = 1; r >= 0; --r) {
+    SEED_TRY(wgrad(c.at<uint8_t>(b.u1[r]), npo, 64, c.at<uint8_t>(cur), ro, go, d.ch, d.t_rw[r][1], d.t_rb[r][1],
+                   "deep_res_wgrad1"));
+    SEED_TRY(dgrad(D3W_MASK, c.at<uint8_t>(cur), ro, go, d.im_rdg[r][1], w3_sub(d, 1, true), npo,
+                   c.at<uint8_t>(b.u1[r]), nullptr, c.at<uint8_t>(b.dt0), "deep_res_dgrad1"));
+    SEED_TRY(wgrad(c.at<uint8_t>(b.hr[r]), npo, 64, c.at<uint8_t>(b.dt0), ro, go, d.ch, d.t_rw[r][0], d.t_rb[r][0],
+                   "deep_res_wgrad0"));
+    SEED_TRY(dgrad(D3W_RES, c.at<uint8_t>(b.dt0), ro, go, d.im_rdg[r][0], w3_sub(d, 1, true), npo,
+                   c.at<uint8_t>(b.hr[r]), c.at<uint8_t>(cur), c.at<uint8_t>(oth), "deep_res_dgrad0"));
+    std::swap(cur, oth);
+  }
+  for (int q = 0; q < npo; ++q) {
+    SEED_TRY(conv3w_pool_bwd(F, gi, go, 64, d.pt, d.pl, plane_at(c, cur, q, ro),
+                             c.at<uint8_t>(b.arg) + (size_t)q * ro * 64, plane_at(c, b.dconv, q, ri), st));
+    c.mark("deep_pool_bwd", 2);
+  }
+  if (s == 0 || d.xim) return SEED_E_UNSUPPORTED;   // plane sections follow a 64-channel section
+  SEED_TRY(wgrad(c.at<uint8_t>(w.sec[s - 1].h[2]), npi, cpi, c.at<uint8_t>(b.dconv), ri, gi, d.cin, d.t_w, d.t_b,
+                 "deep_conv_wgrad"));
+  SEED_TRY(dgrad(D3W_PLAIN, c.at<uint8_t>(b.dconv), ri, gi, d.im_dg, w3_sub(d, 1, false), npi, nullptr, nullptr,
+                 c.at<uint8_t>(w.sec[s - 1].dhA), "deep_conv_dgrad"));
+  return SEED_OK;
+}
+
 static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                 const float* params, cudaStream_t st) {
   const NetPlan& p = *c.p;
@@ -393,6 +529,10 @@ static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf
     const DeepSec& d = p.sec[s];
     const LearnerWs::Sec& b = w.sec[s];
     const PadGeo gi = PadGeo::make(d.H, d.W), go = PadGeo::make(d.H2, d.W2);
+    if (d.ch > 64) {
+      SEED_TRY(plane_section_forward(c, s, lowp, params, st));
+      continue;
+    }
     Conv3wFwd a{};
     a.mode = W3_PLAIN; a.cin_p = d.cinp; a.ch = d.ch; a.xim = d.xim; a.g = gi; a.rows = F * gi.P;
     a.in_scale = s == 0 ? 1.f / 255.f : 1.f;
@@ -446,6 +586,10 @@ static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const b
     const DeepSec& d = p.sec[s];
     const LearnerWs::Sec& b = w.sec[s];
     const PadGeo gi = PadGeo::make(d.H, d.W), go = PadGeo::make(d.H2, d.W2);
+    if (d.ch > 64) {
+      SEED_TRY(plane_section_backward(c, s, lowp, params, grads, st));
+      continue;
+    }
     const int64_t Mr = F * go.P;
     size_t cur = b.dhA, oth = b.dhB;   // dh of h[2] arrives in dhA
     for (int r = 1; r >= 0; --r) {

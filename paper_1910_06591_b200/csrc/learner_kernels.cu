@@ -642,7 +642,7 @@ __device__ __forceinline__ void lowp_write(const AdamArgs& a, int64_t i, float v
     if (m.kind == IMG_S2D) {
       dst = s2d_img_pos(m, e);
     } else if (m.kind == IMG_WIN3) {
-      dst = win3_img_pos(m.d0, m.d1, m.d2, m.d3, e);
+      dst = win3p_img_pos(m.d0, m.d1, m.d2, m.d3, e);
     } else if (m.kind == IMG_COPY_PAD) {
       uint32_t r, c;
       img_rc(m, (uint32_t)e, r, c);

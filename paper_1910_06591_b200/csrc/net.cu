@@ -59,7 +59,7 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
   } else if (s->kind == SEED_NET_IMPALA_DEEP || s->kind == SEED_NET_GFOOTBALL) {
     const int ns = s->kind == SEED_NET_IMPALA_DEEP ? 3 : 4;
     const int wm = s->torso_width <= 1 ? 1 : s->torso_width;
-    if (wm != 1 && wm != 2) return SEED_E_UNSUPPORTED;
+    if (wm != 1 && wm != 2 && wm != 4) return SEED_E_UNSUPPORTED;
     const int chs[4] = {16 * wm, 32 * wm, 32 * wm, 32 * wm};
     int cin = p->C, h = p->H, w = p->W;
     char nm[32];
@@ -69,7 +69,9 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
       DeepSec& d = p->sec[sct];
       d.H = h; d.W = w; d.cin = cin; d.ch = ch;
       d.xim = sct == 0 && 3 * cin <= 16;
-      d.cinp = d.xim || cin <= 16 ? 16 : (cin <= 32 ? 32 : 64);
+      // input row channels; 128 = two 64-channel planes (conv3w.cuh)
+      d.cinp = d.xim || cin <= 16 ? 16 : (cin <= 32 ? 32 : cin <= 64 ? 64 : 128);
+      if (cin > 64 && cin != 128) return SEED_E_UNSUPPORTED;
       d.H2 = same_out(h); d.W2 = same_out(w);
       const int ph = std::max((d.H2 - 1) * 2 + 3 - h, 0), pw = std::max((d.W2 - 1) * 2 + 3 - w, 0);
       d.pt = ph / 2; d.pl = pw / 2;
@@ -133,17 +135,19 @@ seed_status make_net_plan(const seed_net_spec* s, NetPlan* p) {
       m.cmul = fd.mul; m.cshr = fd.shr;
       m.d0 = mode; m.d1 = CI; m.d2 = CO; m.d3 = RB;
       const int64_t start = off;
-      off = (int64_t)align_up((size_t)(off + win3_img_elems(mode, CI, CO, RB)), 64);
+      off = (int64_t)align_up((size_t)(off + win3p_img_elems(mode, CI, CO, RB)), 64);
       return start;
     };
+    // (more than 64 channels: plane-pair sub-images of 64 -> 64 convs, conv3w.cuh)
     for (int sct = 0; sct < p->nsec; ++sct) {
       DeepSec& d = p->sec[sct];
-      d.im_w = win3_img(d.t_w, d.xim ? 2 : 0, d.cin, d.ch, d.xim ? 32 : 2 * d.cinp);
-      d.im_dg = sct > 0 ? win3_img(d.t_w, 1, d.cin, d.ch, 2 * d.ch) : -1;
+      const int ci_rb = 2 * std::min(d.cinp, 64), ch_rb = 2 * std::min(d.ch, 64);
+      d.im_w = win3_img(d.t_w, d.xim ? 2 : 0, d.cin, d.ch, d.xim ? 32 : ci_rb);
+      d.im_dg = sct > 0 ? win3_img(d.t_w, 1, d.cin, d.ch, ch_rb) : -1;
       for (int r = 0; r < 2; ++r)
         for (int j = 0; j < 2; ++j) {
-          d.im_rw[r][j] = win3_img(d.t_rw[r][j], 0, d.ch, d.ch, 2 * d.ch);
-          d.im_rdg[r][j] = win3_img(d.t_rw[r][j], 1, d.ch, d.ch, 2 * d.ch);
+          d.im_rw[r][j] = win3_img(d.t_rw[r][j], 0, d.ch, d.ch, ch_rb);
+          d.im_rdg[r][j] = win3_img(d.t_rw[r][j], 1, d.ch, d.ch, ch_rb);
         }
     }
   }
@@ -158,7 +162,8 @@ bool learner_supported(const NetPlan& p) {
   if (p.kind == SEED_NET_MLP) return true;
   if (p.kind == SEED_NET_ATARI_SHALLOW) return shallow_s2d_supported(p.H, p.W, p.C);
   if (p.kind == SEED_NET_IMPALA_DEEP || p.kind == SEED_NET_GFOOTBALL)   // conv3w.cuh
-    return p.C >= 1 && p.C <= 32 && (p.sec[p.nsec - 1].ch == 32 || p.sec[p.nsec - 1].ch == 64) &&
+    return p.C >= 1 && p.C <= 32 &&
+           (p.sec[p.nsec - 1].ch == 32 || p.sec[p.nsec - 1].ch == 64 || p.sec[p.nsec - 1].ch == 128) &&
            p.fc_in % 8 == 0;
   return false;
 }
@@ -229,6 +234,15 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
       b.dhB = bump(cur, sp * 2);
       b.dt0 = bump(cur, sp * 2);
     }
+    // fp32 partial sums of the plane-pair convs (128-channel sections): the largest
+    // row space with two input planes
+    size_t prow = 0;
+    for (int sct = 0; sct < p.nsec; ++sct) {
+      const DeepSec& d = p.sec[sct];
+      if (d.cinp > 64 || d.ch > 64) prow = std::max(prow, (size_t)F * (d.H + 2) * (d.W + 2));
+      if (d.ch > 64) prow = std::max(prow, (size_t)F * (d.H2 + 2) * (d.W2 + 2));
+    }
+    w->part3 = prow ? bump(cur, prow * 64 * 4) : 0;
     // the FC layer reads dense relu(h) of the last section (written by its last
     // residual epilogue) and writes its data gradient into that section's dhA
     w->act2 = bump(cur, F * p.fc_in * 2);
@@ -297,7 +311,7 @@ __global__ void refresh_lowp_multi(const float* __restrict__ params, __nv_bfloat
       continue;
     }
     if (m.kind == IMG_WIN3) {  // source elements; padding positions stay zero
-      lowp[m.dst + win3_img_pos(m.d0, m.d1, m.d2, m.d3, i)] = __float2bfloat16_rn(params[m.src + i]);
+      lowp[m.dst + win3p_img_pos(m.d0, m.d1, m.d2, m.d3, i)] = __float2bfloat16_rn(params[m.src + i]);
       continue;
     }
     if (m.kind == IMG_COPY_PAD) {

@@ -59,7 +59,7 @@ __host__ __device__ inline void img_rc(const LowpImg& m, uint32_t e, uint32_t& r
 
 // IMPALA-deep section (C14): conv3x3 (cin -> ch) at H x W, maxpool -> H2 x W2,
 // residual blocks at H2 x W2 (conv3w.cuh).  cinp = channels of the input rows
-// (16 / 32); xim: section-0 x-im2col input (3 windows).
+// (16 / 32 / 64; 128 = two 64-channel planes); xim: section-0 x-im2col input (3 windows).
 struct DeepSec {
   int H, W, cin, cinp, ch, H2, W2, pt, pl, xim;
   int t_w, t_b, t_rw[2][2], t_rb[2][2];              // tensor indices
@@ -108,6 +108,7 @@ struct LearnerWs {
   struct Sec {
     size_t conv, arg, h[3], hr[3], u1[2], dconv, dhA, dhB, dt0;
   } sec[4];
+  size_t part3;   // fp32 [rows][64] partial sums of the plane-pair convs (0: none)
 };
 constexpr int NORM_BLOCKS = 296;
 constexpr int COLSUM_BLOCKS = 148;

@@ -182,22 +182,26 @@ struct FcDgrad {
                          // rows of 2*CH bytes g = f*P2 + g0 + y*W2s + x (conv_s2d.cuh;
                          // deep torso: conv3w.cuh padded rows, g0 = W2s + 1)
   int Wo, W2s, P2, g0;
-  int CH = 32;           // channels per dY2s row (32; 64 for the 2x DMLab torso)
+  int CH = 32;           // channels per dY2s pixel (32; 64 for the 2x DMLab torso; 128
+                         // for the 4x: two planes of 64-channel rows, conv3w.cuh)
   __device__ const void* ptr_a(int m, int k) const { return dfc + (size_t)m * 256 + k; }
   __device__ const void* ptr_b(int k, int n8) const { return w + (size_t)k * N + n8; }
+  // the row holding channel n % CH of pixel n / CH (its plane's row for CH = 128)
   __device__ uint8_t* s2d_row(int m, int n, int64_t& g) const {
     const int pix = n / CH;
     g = (int64_t)m * P2 + g0 + (pix / Wo) * W2s + pix % Wo;
+    if (CH > 64) return dY2s + (size_t)((n % CH) >> 6) * M * P2 * 128 + g * 128;
     return dY2s + g * (2 * CH);
   }
+  __device__ int row_bytes() const { return CH > 64 ? 128 : 2 * CH; }
   __device__ void store(int m, int n, float v) const {
     const size_t i = (size_t)m * N + n;
     const bf16 o = to_bf(bf2f(act2[i]) > 0.f ? v : 0.f);
     if (dY2s) {
       int64_t g;
       uint8_t* row = s2d_row(m, n, g);
-      const int c = n % CH;
-      *reinterpret_cast<bf16*>(row + (swz_chunk(g, 2 * CH, c >> 3) << 4) + (c & 7) * 2) = o;
+      const int c = (n % CH) & (row_bytes() / 2 - 1);
+      *reinterpret_cast<bf16*>(row + (swz_chunk(g, row_bytes(), c >> 3) << 4) + (c & 7) * 2) = o;
     } else {
       dY2[i] = o;
     }
@@ -209,14 +213,14 @@ struct FcDgrad {
     if (dY2s) {
       int64_t g;
       uint8_t* row = s2d_row(m, n0, g);
-      const int j0 = (n0 % CH) >> 3;
+      const int j0 = ((n0 % CH) & (row_bytes() / 2 - 1)) >> 3;
       uint4 a, b;
       a.x = pack_bf16(v[0], v[1]); a.y = pack_bf16(v[2], v[3]);
       a.z = pack_bf16(v[4], v[5]); a.w = pack_bf16(v[6], v[7]);
       b.x = pack_bf16(v[8], v[9]); b.y = pack_bf16(v[10], v[11]);
       b.z = pack_bf16(v[12], v[13]); b.w = pack_bf16(v[14], v[15]);
-      *reinterpret_cast<uint4*>(row + (swz_chunk(g, 2 * CH, j0) << 4)) = a;
-      *reinterpret_cast<uint4*>(row + (swz_chunk(g, 2 * CH, j0 + 1) << 4)) = b;
+      *reinterpret_cast<uint4*>(row + (swz_chunk(g, row_bytes(), j0) << 4)) = a;
+      *reinterpret_cast<uint4*>(row + (swz_chunk(g, row_bytes(), j0 + 1) << 4)) = b;
     } else {
       st_bf16x16(dY2 + i, v);
     }

@@ -18,7 +18,7 @@ cfg = os.environ.get("CFG", "c3")
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 T, B, kw = {"c1": (20, 8, dict(float_obs=True, lstm_units=0)), "c2": (20, 32, {}),
             "c3": (100, 32, {}), "c4": (32, 128, dict(smm=True)), "c3m": (100, 32, {}),
-            "c4m": (32, 128, dict(smm=True)), "c4l": (32, 128, dict(smm=True))}[cfg]
+            "c4m": (32, 128, dict(smm=True)), "c4l": (32, 128, dict(smm=True)), "c3l": (100, 32, {})}[cfg]
 T = int(os.environ.get("T", T))
 B = int(os.environ.get("B", B))
 spec = S.spec_for_config(cfg)
