@@ -57,7 +57,7 @@ struct W3FwdEpi {
       }
       return;
     }
-    if (part_in) {   // the other input plane's fp32 sum
+    if (N == 64 && part_in) {   // the other input plane's fp32 sum (plane pairs: 64-ch only)
       const float4* ps = reinterpret_cast<const float4*>(part_in + m * N);
 #pragma unroll
       for (int q = 0; q < N / 4; ++q) {
@@ -66,7 +66,7 @@ struct W3FwdEpi {
         v[4 * q + 2] = fmaf(v[4 * q + 2], in_scale, t.z); v[4 * q + 3] = fmaf(v[4 * q + 3], in_scale, t.w);
       }
     }
-    const float isc = part_in ? 1.f : in_scale;
+    const float isc = (N == 64 && part_in) ? 1.f : in_scale;
     if ((reinterpret_cast<uintptr_t>(bias) & 15) == 0) {   // 16-byte bias loads (the torso's
 #pragma unroll                                              // parameter offsets are multiples of 4)
       for (int q = 0; q < N / 4; ++q) {
@@ -85,31 +85,32 @@ struct W3FwdEpi {
         if (MODE == W3_RELU) v[q] = fmaxf(v[q], 0.f);
       }
     }
-    if (MODE == W3_RES) {
+    if constexpr (MODE == W3_RES) {
+      // per 8-channel chunk: + residual, h, relu(h) (of the rounded h), dense relu(h)
+      uint4* d = nullptr;
+      if (dense) {
+        const int ct = dense_ct > 0 ? dense_ct : N;
+        d = reinterpret_cast<uint4*>(dense + ((int64_t)f * g.H * g.W + (int64_t)y * g.W + x) * ct + dense_off);
+      }
 #pragma unroll
       for (int j = 0; j < N / 8; ++j) {
         float r[8];
         unpack8(p[j], r);
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[8 * j + k] += r[k];
+        const uint4 hv = pack8(v + 8 * j);
+        *chunk_at(out, m, RB, j) = hv;
+        float h8[8];
+        unpack8(hv, h8);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) h8[k] = fmaxf(h8[k], 0.f);
+        const uint4 rv = pack8(h8);
+        if (outr) *chunk_at(outr, m, RB, j) = rv;
+        if (d) d[j] = rv;
       }
-    }
+    } else {
 #pragma unroll
-    for (int j = 0; j < N / 8; ++j) *chunk_at(out, m, RB, j) = pack8(v + 8 * j);
-    if (MODE == W3_RES) {
-      float r[N];
-#pragma unroll
-      for (int q = 0; q < N; ++q) r[q] = fmaxf(__bfloat162float(__float2bfloat16_rn(v[q])), 0.f);
-      if (outr) {
-#pragma unroll
-        for (int j = 0; j < N / 8; ++j) *chunk_at(outr, m, RB, j) = pack8(r + 8 * j);
-      }
-      if (dense) {
-        const int ct = dense_ct > 0 ? dense_ct : N;
-        uint4* d = reinterpret_cast<uint4*>(dense + ((int64_t)f * g.H * g.W + (int64_t)y * g.W + x) * ct + dense_off);
-#pragma unroll
-        for (int j = 0; j < N / 8; ++j) d[j] = pack8(r + 8 * j);
-      }
+      for (int j = 0; j < N / 8; ++j) *chunk_at(out, m, RB, j) = pack8(v + 8 * j);
     }
   }
 };
@@ -153,7 +154,7 @@ struct W3DgradEpi {
       for (int j = 0; j < N / 8; ++j) *chunk_at(dX, m, RB, j) = z;
       return;
     }
-    if (part_in) {
+    if (N == 64 && part_in) {   // plane pairs: 64-ch only
       const float4* ps = reinterpret_cast<const float4*>(part_in + m * N);
 #pragma unroll
       for (int q = 0; q < N / 4; ++q) {

@@ -429,7 +429,7 @@ def _deep_exact_checks(cfg, g, gt, ex, rt, exact, ref):
 
 
 @pytest.mark.parametrize("cfg,B,T", [("c3", 32, 100), ("c4", 128, 32), ("c4l", 128, 32),
-                                     ("c3m", 32, 100)])
+                                     ("c3m", 32, 100), ("c3l", 32, 100)])
 def test_learner_deep_full_size_sampled(cfg, B, T):
     """BASELINE.json configs[2] / configs[3] at their full sizes (the shapes bench.py
     times: F = 3232 / 4224 frames, 23-31 M padded rows at 72x96): one learner step,
