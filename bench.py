@@ -408,6 +408,76 @@ def vtrace_leg(S, torch, T=100, B=1 << 17, iters=20):
 
 
 # ---------------------------------------------------------------- R2D2 leg
+def wire_leg(S, torch, actors=16, envs=2, steps=30):
+    """f4: actors (threads, one TCP connection each, SEEDWire v1
+    uint8 StepRequests) -> the library's batching server (max batch 32, 1 ms
+    deadline) -> seed_infer on the configs[4] net -> ActionResponses routed back.
+    Reports env steps/s through the whole loop and the actor-observed round-trip
+    latency (send -> action) percentiles.  Host networking on loopback; the actors
+    are Python threads, so this measures the library's path under a light load."""
+    import threading
+    import numpy as np
+    import seedgen
+    from paper_1910_06591_b200 import wire as Wr
+    spec = S.spec_for_config("c5")
+    params = seedgen.glorot_params(S.net_param_layout(spec), seed=0)
+    learner = S.Learner(spec, 1, 1, params)
+    rows = actors * envs
+    srv = S.InferenceServer(spec, rows, 32, learner=learner)
+    obs_bytes = 84 * 84 * 4
+    ws = Wr.WireServer(obs_bytes, rows, max_batch=32, max_wait_us=1000)
+    lat, errors = [], []
+    frame = np.random.default_rng(0).integers(0, 256, obs_bytes, dtype=np.uint8)
+
+    def actor(aid):
+        try:
+            c = Wr.ActorClient(ws.port, aid, envs)
+            for step in range(steps):
+                t0 = time.perf_counter()
+                for e in range(envs):
+                    c.send_step(e, 0.0, step == 0, frame)
+                for _ in range(envs):
+                    c.recv()
+                lat.append((time.perf_counter() - t0) * 1e3)
+            c.close()
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+    dev = {k: torch.empty(32, dtype=dt, device="cuda") for k, dt in
+           (("ids", torch.int32), ("rew", torch.float32), ("done", torch.uint8), ("u", torch.float32))}
+    dobs = torch.empty(32, 84, 84, 4, dtype=torch.uint8, device="cuda")
+    dev["u"].uniform_()
+    threads = [threading.Thread(target=actor, args=(i,)) for i in range(actors)]
+    t0 = time.perf_counter()
+    for t in threads:
+        t.start()
+    served, batches = 0, 0
+    while served < rows * steps and time.perf_counter() - t0 < 120:
+        obs, ids, rew, done = ws.next_batch(timeout_us=100000)
+        n = len(ids)
+        if n == 0:
+            continue
+        dobs[:n].copy_(torch.from_numpy(obs.reshape(n, 84, 84, 4)))
+        dev["ids"][:n].copy_(torch.from_numpy(ids))
+        dev["rew"][:n].copy_(torch.from_numpy(rew))
+        dev["done"][:n].copy_(torch.from_numpy(done))
+        a, _ = srv.infer(dev["ids"][:n], dobs[:n], dev["rew"][:n], dev["done"][:n], dev["u"][:n])
+        ws.reply(ids, a.cpu().numpy())
+        served += n
+        batches += 1
+    dt = time.perf_counter() - t0
+    for t in threads:
+        t.join(timeout=30)
+    st = ws.stats()
+    ws.close()
+    lat = np.sort(np.asarray(lat)) if lat else np.zeros(1)
+    return {"actors": actors, "envs_per_actor": envs, "steps": served, "batches": batches,
+            "mean_batch": round(served / max(batches, 1), 2), "env_steps_per_s": round(served / dt, 1),
+            "round_trip_ms_p50_p99": [round(float(np.percentile(lat, 50)), 3),
+                                      round(float(np.percentile(lat, 99)), 3)],
+            "batch_triggers": {k: st[k] for k in ("by_size", "by_deadline", "by_timeout")},
+            "errors": errors[:3]}
+
+
 def r2d2_leg(S, torch, iters=20):
     """seed_r2d2_targets at the paper's trained-sequence shape (80 steps after the
     40-step burn-in of 120; 18 actions; n = 5) over B = 2^14 sequences
@@ -870,6 +940,7 @@ def run_ours(args):
                           "top_kernels": sorted(r["kernels"], key=lambda x: -x["us"])[:8]}
         inf = inference_leg(S, torch, world, rank, dist)
         r2 = r2d2_leg(S, torch) if rank == 0 else None
+        wl = wire_leg(S, torch) if rank == 0 else None
     c = CONFIGS[HEAD]
     if rank == 0:
         vt = vtrace_leg(S, torch)
@@ -903,6 +974,7 @@ def run_ours(args):
             line["other_configs"] = extra
             line["inference"] = inf
             line["r2d2"] = r2
+            line["actor_transport"] = wl
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(HEAD)
         print(json.dumps(line), flush=True)

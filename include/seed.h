@@ -362,6 +362,37 @@ seed_status seed_stage_requests(seed_stager* stager, int n, const uint8_t* const
                                 const uint8_t* dones, uint8_t* pinned_obs, uint8_t* pinned_meta,
                                 uint8_t* dev_obs, uint8_t* dev_meta, int chunk, void* stream);
 
+/* Actor transport + server-side batching ("the
+ * connection from actor to learner is kept open and metadata sent only once",
+ * P:136 the batching module; wire format SEEDWire v1: frames =
+ * u32 LE length (of type byte + payload) | u8 type | payload; Hello 0x01 (u32
+ * actor_id, u32 num_envs), StepRequest 0x02 (u32 env_id, f32 reward, u8 done, u32
+ * obs_count, obs_count f32 — rounded and clamped to 0..255 bytes), ActionResponse
+ * 0x03 (u32 env_id, u32 action), Error 0x00 (u16 code, u16 length, UTF-8); plus
+ * StepRequest-u8 0x04 = StepRequest with obs_count uint8 pixels; max frame 16 MiB).
+ * Host-only: a TCP server on 127.0.0.1:port (0 = any free port, returned in
+ * *port_out) whose I/O thread accepts actors, gives each Hello num_envs consecutive
+ * state-table rows (at most max_rows in all), and queues StepRequests (obs_count
+ * must equal obs_bytes; one in-flight request per (actor, env), else Error +
+ * close).  seed_wire_next_batch blocks until max_batch requests are queued, or the
+ * oldest has waited max_wait_us, or timeout_us passes, and copies up to max_batch
+ * of them in arrival order into host buffers (obs_out [n][obs_bytes], rows_out =
+ * state-table rows for seed_infer's actor_ids, reward_out, done_out; *n_out may
+ * be 0).  seed_wire_reply sends each request's action to its connection (exactly
+ * once; SEED_E_ARG for a row with no request waiting).  stats6: batches, requests,
+ * batches by size / deadline / timeout trigger, protocol errors.  The server's
+ * calls are thread-safe; destroy joins the I/O thread and closes every socket. */
+typedef struct seed_wire_server seed_wire_server;
+seed_status seed_wire_server_create(int port, int max_batch, int max_wait_us, int obs_bytes, int max_rows,
+                                    seed_wire_server** out, int* port_out);
+seed_status seed_wire_server_destroy(seed_wire_server* server);
+seed_status seed_wire_next_batch(seed_wire_server* server, int timeout_us, uint8_t* obs_out /* host */,
+                                 int32_t* rows_out, float* reward_out, uint8_t* done_out, int* n_out);
+seed_status seed_wire_reply(seed_wire_server* server, int n, const int32_t* rows /* host */,
+                            const int32_t* actions /* host */);
+seed_status seed_wire_server_stats(seed_wire_server* server, int64_t* stats6 /* host */,
+                                   int* rows_assigned);
+
 /* Gather B completed unrolls (entries ready_ring[consumed .. consumed+B)) into
  * the seed_batch layout buffers given in `out` (device pointers, cast away
  * const), and advance the consumed counter.  The caller must only ask for

@@ -126,6 +126,11 @@ _SIGS = {
     "seed_stage_requests": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "seed_assemble_batch": (c_int, [P(UnrollStore), c_int, c_int, c_int, P(Batch), c_void_p]),
+    "seed_wire_server_create": (c_int, [c_int, c_int, c_int, c_int, c_int, P(c_void_p), P(c_int)]),
+    "seed_wire_server_destroy": (c_int, [c_void_p]),
+    "seed_wire_next_batch": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, P(c_int)]),
+    "seed_wire_reply": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "seed_wire_server_stats": (c_int, [c_void_p, c_void_p, P(c_int)]),
     "seed_debug_gemm": (c_int, [c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_int,
                                 c_void_p, c_int, c_int, c_void_p, c_void_p]),
 }
