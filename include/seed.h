@@ -26,7 +26,11 @@
  *            branches onto belong to a caller-owned seed_exec, the NCCL comms to a
  *            caller-owned seed_comm.  The only process-wide data are idempotent
  *            per-device caches (kernel shared-memory opt-ins, SM counts) and
- *            read-once environment switches (SEED_PDL, SEED_DP_BUCKETS).  Calls on
+ *            environment switches for A/B measurement, read once (SEED_PDL,
+ *            SEED_DP_BUCKETS, SEED_DP_COMMS, SEED_FUSE_POOL=0 unfused section conv +
+ *            max-pool, SEED_KX, SEED_XF_U8, SEED_PEER_DEBUG) or per call
+ *            (SEED_STORE_CONV=1: the fused section conv + max-pool also stores the
+ *            conv rows, a test hook).  Calls on
  *            different streams with disjoint buffers (and distinct seed_exec /
  *            seed_comm handles) are independent; one process may drive several
  *            devices (each call runs on the device current at the call).
