@@ -506,9 +506,11 @@ __global__ void __launch_bounds__(256) splitk_finish(const Prob p, const float* 
 // caller workspace); with `cnt` (GEMM_COUNTERS zeroed unsigned, left zeroed)
 // the last CTA of each tile reduces in-kernel, otherwise the fixed-order
 // splitk_finish kernel follows.  max_ctas > 0 caps the persistent grid.
+// run_finish = false: with splits > 1 the caller reduces `part` itself (e.g. the
+// consumer kernel sums the splits in z order while loading)
 template <int BN, class Prob>
 seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullptr,
-                        int max_ctas = 0, unsigned* cnt = nullptr) {
+                        int max_ctas = 0, unsigned* cnt = nullptr, bool run_finish = true) {
   using Cfg = GemmCfg<BN, Prob::A_MN, Prob::B_MN>;
   if (p.M <= 0 || p.N <= 0) return SEED_OK;
   const int nkb = (p.K + GEMM_BK - 1) / GEMM_BK;
@@ -526,7 +528,7 @@ seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullp
   const int grid = std::min(items, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   SEED_TRY(launch_k(gemm_tc_kernel<BN, Prob>, dim3(grid), dim3(GEMM_THREADS), (size_t)Cfg::SMEM, st, p,
                     part, splits, splits > 1 ? cnt : (unsigned*)nullptr));
-  if (splits > 1 && !cnt) {
+  if (splits > 1 && !cnt && run_finish) {
     const size_t MN = (size_t)p.M * p.N;
     const int blocks = (int)std::min<size_t>((MN / 4 + 255) / 256 + 1, 148 * 8);
     SEED_TRY(launch_k(splitk_finish<Prob>, dim3(blocks), dim3(256), 0, st, p, (const float*)part, splits));

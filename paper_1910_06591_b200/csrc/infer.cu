@@ -163,8 +163,12 @@ constexpr int ICH_THREADS = 256;   // = LSTM_U: thread j owns hidden unit j
 // CTA i = request i: cell (gate order i, f, g, o; c reset on done, C15), new (h, c)
 // into table row ids[i]; logits | value = W h + b (fp32, fixed-order block sum);
 // warp 0 samples a = min{j : u < CDF_j} (C18) and writes the behaviour log-prob.
+// With `part` (the gates GEMM's split-K partials [splits][n][4U]) the pre-activation
+// gates are summed here, splits in z order, then + bias — the arithmetic of the
+// GEMM's fixed-order finish, without its launch.
 __global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
-    int A, const float* __restrict__ gates, const float* __restrict__ cpre,
+    int A, const float* __restrict__ gates, const float* __restrict__ part, int splits,
+    const float* __restrict__ gbias, const float* __restrict__ cpre,
     const uint8_t* __restrict__ done, const int32_t* __restrict__ ids, const float* __restrict__ hw,
     const float* __restrict__ hbias, const float* __restrict__ uniforms, uint64_t seed,
     uint64_t counter, float* __restrict__ th, float* __restrict__ tc, int32_t* __restrict__ tla,
@@ -176,9 +180,24 @@ __global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
   const int A1 = A + 1;
   __shared__ float red[NW][33];
   __shared__ float lg[33];
-  const float* g = gates + (size_t)i * 4 * U;
+  float gv[4];
+  if (part) {
+    const size_t MN = (size_t)gridDim.x * 4 * U;
+    const float* pz = part + (size_t)i * 4 * U + j;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gv[k] = 0.f;
+    for (int z = 0; z < splits; ++z)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gv[k] += __ldcs(pz + (size_t)z * MN + k * U);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gv[k] += __ldg(gbias + k * U + j);
+  } else {
+    const float* g = gates + (size_t)i * 4 * U;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gv[k] = g[k * U + j];
+  }
   const float c0 = done[i] ? 0.f : cpre[(size_t)i * U + j];
-  const float gi = sigm(g[j]), gf = sigm(g[U + j]), gg = tanh_fast(g[2 * U + j]), go = sigm(g[3 * U + j]);
+  const float gi = sigm(gv[0]), gf = sigm(gv[1]), gg = tanh_fast(gv[2]), go = sigm(gv[3]);
   const float c = gf * c0 + gi * gg;
   const float h = go * tanh_fast(c);
   const int a = ids[i];
@@ -434,16 +453,19 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
     pr.bias = params + p.t[p.i_fcb].off; pr.X = (bf16*)at(w.X);
     SEED_TRY(launch_gemm<128>(pr, pick_splits(pr.M, pr.N, 128, pr.K), st, splitk));
   }
+  int gsplits = 1;
   {
     GatesFwd pr{};
     pr.M = n; pr.N = 4 * U; pr.K = p.Kxp + U; pr.Kxp = p.Kxp; pr.U = U;
     pr.X = (const bf16*)at(w.X); pr.hb = (const bf16*)at(w.hb);
     pr.wx = lowp + p.im_wx; pr.wh = lowp + p.im_wh;
     pr.bias = params + p.t[p.i_lb].off; pr.out = (float*)at(w.xproj);
-    SEED_TRY(launch_gemm<128>(pr, pick_splits(pr.M, pr.N, 128, pr.K), st, splitk));
+    gsplits = gemm_effective_splits(pr.K, pick_splits(pr.M, pr.N, 128, pr.K));
+    SEED_TRY(launch_gemm<128>(pr, gsplits, st, splitk, 0, nullptr, /*run_finish=*/false));
   }
   SEED_TRY(launch_k(infer_cell_heads_kernel, dim3(n), dim3(ICH_THREADS), 0, st, A,
-                    (const float*)at(w.xproj), (const float*)at(w.cpre), done, actor_ids,
+                    (const float*)at(w.xproj), gsplits > 1 ? (const float*)splitk : nullptr, gsplits,
+                    params + p.t[p.i_lb].off, (const float*)at(w.cpre), done, actor_ids,
                     params + p.t[p.i_hw].off, params + p.t[p.i_hb].off, uniforms, seed, counter,
                     table->h, table->c, table->last_action, action_out, blp_out, logits_out,
                     table->num_actors));
