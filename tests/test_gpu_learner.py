@@ -489,9 +489,10 @@ def test_learner_c3_bptt_T100():
 
 def test_learner_c4_u8_source_parity(tmp_path):
     """The opt-in XF_U8 path (SEED_XF_U8=1: section 0 reads the uint8 obs and expands
-    them to bf16 rows in shared memory, no obs_bf16 pass) gives the same learner step
-    as the default path: identical logits / values and gradients within fp32
-    accumulation-order noise (run in a subprocess: the switch is read once)."""
+    them to bf16 rows in shared memory, no obs_bf16 pass) and the unfused section
+    conv + max-pool (SEED_FUSE_POOL=0) give the same learner step as the default
+    path: logits / values and gradients within fp32 accumulation-order noise (run in
+    subprocesses: the switches are read once)."""
     import os
     import subprocess
     import sys
@@ -509,10 +510,12 @@ torch.cuda.synchronize()
 np.save(sys.argv[1], np.concatenate([L.outputs()[0].cpu().numpy().ravel(), L.grads.cpu().numpy()]))
 ''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for flag in ("0", "1"):
-        f = tmp_path / f"o{flag}.npy"
+    # default; XF_U8 section 0; every section conv + max-pool unfused (SEED_FUSE_POOL=0)
+    for name, env in (("d", {}), ("u8", {"SEED_XF_U8": "1"}), ("nofuse", {"SEED_FUSE_POOL": "0"})):
+        f = tmp_path / f"o_{name}.npy"
         subprocess.run([sys.executable, "-c", code, str(f)], check=True, timeout=300,
-                       env=dict(os.environ, SEED_XF_U8=flag))
+                       env=dict(os.environ, **env))
         outs.append(np.load(f).astype(np.float64))
-    rel = np.linalg.norm(outs[1] - outs[0]) / np.linalg.norm(outs[0])
-    assert rel < 1e-3, rel
+    for o in outs[1:]:
+        rel = np.linalg.norm(o - outs[0]) / np.linalg.norm(outs[0])
+        assert rel < 1e-3, rel
