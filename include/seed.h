@@ -346,6 +346,25 @@ seed_status seed_infer(const seed_net_spec* spec, const void* params_lowp, const
                        int32_t* action_out, float* behaviour_logp_out, float* logits_out,
                        const seed_unroll_store* store, void* workspace, size_t ws_bytes,
                        void* stream);
+/* R2D2 actors (P:591 dueling heads, P:614 per-actor
+ * epsilon-greedy): the same batched step (state table, unroll store, workspace as
+ * seed_infer), but the net's A+1 outputs are read as dueling heads (C35: A advantages
+ * then the value), Q_a = V + A_a - mean_j A_j (written to q_out [n][A] if non-NULL),
+ * and the action is epsilon-greedy with epsilon_i = eps_base^(1 + eps_alpha * i /
+ * (num_actors_eps - 1)) for table row i (0.4, 7; num_actors_eps = 1: eps_base):
+ * uniforms [n][2] (device, or NULL: Philox4x32-10 keyed by seed, counter and the row,
+ * outputs x, y): explore when uniforms[r][0] < epsilon_i, then action =
+ * floor(uniforms[r][1] * A) (clamped to A-1), else the first maximum of Q.
+ * behaviour_logp_out = log(epsilon_i / A + (1 - epsilon_i) [action = greedy]).
+ * SEED_E_ARG for eps_base outside [0, 1], eps_alpha < 0 or num_actors_eps < 1. */
+seed_status seed_infer_eps_greedy(const seed_net_spec* spec, const void* params_lowp, const float* params,
+                                  const seed_state_table* table, int n, const int32_t* actor_ids,
+                                  const uint8_t* obs, const float* reward, const uint8_t* done,
+                                  const float* uniforms, uint64_t seed, uint64_t counter,
+                                  float eps_base, float eps_alpha, int num_actors_eps,
+                                  int32_t* action_out, float* behaviour_logp_out, float* q_out,
+                                  const seed_unroll_store* store, void* workspace, size_t ws_bytes,
+                                  void* stream);
 /* Host side of the inference batch (H12).  A seed_stager
  * is a caller-owned pool of `threads` host worker threads.  seed_stage_requests
  * packs the n requests' observations — obs_ptrs[i] (host) points to request i's

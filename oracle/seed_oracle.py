@@ -643,10 +643,10 @@ def sample_inverse_cdf(logits, u):
     return idx
 
 
-def infer(spec, params, table_h, table_c, table_last_action, actor_ids, obs, reward, done,
-          uniforms, emu=False):
-    """One batched inference call.  Returns (action, behaviour_logp, logits, new table
-    arrays).  Actors not in actor_ids are untouched."""
+def _infer_net(spec, params, table_h, table_c, table_last_action, actor_ids, obs, reward, done,
+               emu=False):
+    """The network part of a batched inference step: the A+1 head outputs
+    of each request and the new (h, c) rows of the state table."""
     P = unflatten(spec, params)
     ids = np.asarray(actor_ids).astype(np.int64)
     d = np.asarray(done).astype(bool)
@@ -660,13 +660,42 @@ def infer(spec, params, table_h, table_c, table_last_action, actor_ids, obs, rew
         h1, c1 = H[:, 0], lc["c"][:, 0]
         th[ids], tc[ids] = h1, c1
         feat = h1
-    out = feat @ P["heads.w"].T + P["heads.b"]
+    return feat @ P["heads.w"].T + P["heads.b"], ids, th, tc, tla
+
+
+def infer(spec, params, table_h, table_c, table_last_action, actor_ids, obs, reward, done,
+          uniforms, emu=False):
+    """One batched inference call.  Returns (action, behaviour_logp, logits, new table
+    arrays).  Actors not in actor_ids are untouched."""
+    out, ids, th, tc, tla = _infer_net(spec, params, table_h, table_c, table_last_action, actor_ids,
+                                       obs, reward, done, emu)
     A = spec.num_actions
     logits = out[:, :A]
     a = sample_inverse_cdf(logits, np.asarray(uniforms, np.float64))
     blp = np.take_along_axis(log_softmax(logits), a[:, None], axis=1)[:, 0]
     tla[ids] = a
     return a, blp, logits, th, tc, tla
+
+
+def infer_eps_greedy(spec, params, table_h, table_c, table_last_action, actor_ids, obs, reward, done,
+                     uniforms2, n_actors, base=0.4, alpha=7.0, emu=False):
+    """R2D2 actors (P:591 dueling heads, P:614 per-actor epsilon-greedy): the same
+    network step, Q from the A+1 outputs (dueling_q), the action epsilon-greedy with
+    epsilon of the request's actor (table row).  Returns (action, behaviour_logp, Q,
+    new table arrays)."""
+    out, ids, th, tc, tla = _infer_net(spec, params, table_h, table_c, table_last_action, actor_ids,
+                                       obs, reward, done, emu)
+    A = spec.num_actions
+    q = dueling_q(out[:, :A], out[:, A])
+    u = np.asarray(uniforms2, np.float64)
+    acts, blp = [], []
+    for r, i in enumerate(ids):
+        a, p = eps_greedy_action(q[r], actor_epsilon(int(i), n_actors, base, alpha), u[r, 0], u[r, 1])
+        acts.append(a)
+        blp.append(np.log(p))
+    a = np.asarray(acts, np.int64)
+    tla[ids] = a
+    return a, np.asarray(blp), q, th, tc, tla
 
 
 @dataclass
@@ -839,6 +868,24 @@ def dueling_q(logits, values):
     net's A+1 outputs read as A advantages and 1 value (reading C35)."""
     adv = np.asarray(logits, np.float64)
     return np.asarray(values, np.float64)[..., None] + adv - adv.mean(axis=-1, keepdims=True)
+
+
+def actor_epsilon(i, n_actors, base=0.4, alpha=7.0):
+    """the i-th of N actors explores with epsilon_i = 0.4^(1 + 7 i / (N - 1))."""
+    if n_actors <= 1:
+        return float(base)
+    return float(base) ** (1.0 + float(alpha) * i / (n_actors - 1))
+
+
+def eps_greedy_action(q, eps, u_explore, u_action):
+    """Epsilon-greedy over Q: with probability eps a uniformly random action
+    (floor(u_action * A)), else the greedy one (first maximum); returns the action and
+    its behaviour probability eps / A + (1 - eps) [a = greedy]."""
+    q = np.asarray(q, np.float64)
+    A = q.shape[-1]
+    greedy = int(np.argmax(q))
+    a = min(int(np.floor(u_action * A)), A - 1) if u_explore < eps else greedy
+    return a, eps / A + ((1.0 - eps) if a == greedy else 0.0)
 
 
 def r2d2_warm_state(spec, P, burn, emu=False):

@@ -121,6 +121,11 @@ _SIGS = {
                            c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint64,
                            c_void_p, c_void_p, c_void_p, P(UnrollStore), c_void_p, c_size_t,
                            c_void_p]),
+    "seed_infer_eps_greedy": (c_int, [P(NetSpec), c_void_p, c_void_p, P(StateTable), c_int, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint64,
+                                      c_float, c_float, c_int,
+                                      c_void_p, c_void_p, c_void_p, P(UnrollStore), c_void_p, c_size_t,
+                                      c_void_p]),
     "seed_stager_create": (c_int, [c_int, P(c_void_p)]),
     "seed_stager_destroy": (c_int, [c_void_p]),
     "seed_stage_requests": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,

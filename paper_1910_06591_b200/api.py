@@ -620,6 +620,40 @@ class InferenceServer:
         L.check(st, "seed_infer")
         return a, blp
 
+    def infer_eps_greedy(self, actor_ids, obs, reward, done, uniforms=None, seed=0, counter=0,
+                         eps_base=0.4, eps_alpha=7.0, num_actors_eps=None, action_out=None,
+                         blp_out=None, q_out=None, stream=None):
+        """R2D2 actors (seed_infer_eps_greedy): dueling Q from the net's
+        A+1 outputs, per-actor epsilon-greedy; uniforms [n][2] (explore, action) or
+        None (Philox).  num_actors_eps defaults to the state table's actor count."""
+        n = actor_ids.numel()
+        if n > self.max_n:
+            raise ValueError("n > max_n")
+        _need(actor_ids, torch.int32, "actor_ids")
+        _need(obs, torch.uint8, "obs")
+        _need(reward, torch.float32, "reward")
+        _need(done, torch.uint8, "done")
+        if uniforms is not None:
+            _need(uniforms, torch.float32, "uniforms")
+        dev = actor_ids.device
+        a = action_out if action_out is not None else torch.empty(n, dtype=torch.int32, device=dev)
+        blp = blp_out if blp_out is not None else torch.empty(n, dtype=torch.float32, device=dev)
+        lib = L.load()
+        if self.snapshot is not None:
+            L.check(lib.seed_param_acquire(C.byref(self._spec_c), C.byref(self.snapshot.c),
+                                           _ptr(self.lowp), _ptr(self.params), _ptr(self.version),
+                                           0, _stream(stream)), "seed_param_acquire")
+            lowp, params = self.lowp, self.params
+        else:
+            lowp, params = self.learner.lowp, self.learner.params
+        st = lib.seed_infer_eps_greedy(
+            C.byref(self._spec_c), _ptr(lowp), _ptr(params), C.byref(self.table), n, _ptr(actor_ids),
+            _ptr(obs), _ptr(reward), _ptr(done), _ptr(uniforms), seed, counter, float(eps_base),
+            float(eps_alpha), int(num_actors_eps or self.num_actors), _ptr(a), _ptr(blp), _ptr(q_out),
+            C.byref(self.store) if self.store else None, _ptr(self.ws), self.ws.numel(), _stream(stream))
+        L.check(st, "seed_infer_eps_greedy")
+        return a, blp
+
     def stage_requests(self, obs_list, actor_ids, rewards, dones, threads=8, chunk=128,
                        stream=None):
         if getattr(self, "_stager", None) is None:

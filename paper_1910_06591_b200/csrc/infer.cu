@@ -166,8 +166,20 @@ constexpr int ICH_THREADS = 256;   // = LSTM_U: thread j owns hidden unit j
 // With `part` (the gates GEMM's split-K partials [splits][n][4U]) the pre-activation
 // gates are summed here, splits in z order, then + bias — the arithmetic of the
 // GEMM's fixed-order finish, without its launch.
+// R2D2 actors: the A+1 outputs are dueling heads (C35:
+// advantages 0..A-1, value A), Q_a = V + A_a - mean_j A_j, and the action is
+// epsilon-greedy with the per-actor epsilon_i = base^(1 + alpha * i / (N - 1)) of
+// actor i of N (0.4, 7).  u0 = uniforms[2r] (explore if u0 < epsilon_i),
+// u1 = uniforms[2r+1] (the random action floor(u1 * A)); the greedy action is the
+// first maximum of Q; the behaviour log-prob is log(eps/A + (1 - eps)[a = greedy]).
+struct EpsGreedy {
+  int on;
+  float base, alpha;
+  int n_eps;
+};
+
 __global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
-    int A, const float* __restrict__ gates, const float* __restrict__ part, int splits,
+    EpsGreedy eg, int A, const float* __restrict__ gates, const float* __restrict__ part, int splits,
     const float* __restrict__ gbias, const float* __restrict__ cpre,
     const uint8_t* __restrict__ done, const int32_t* __restrict__ ids, const float* __restrict__ hw,
     const float* __restrict__ hbias, const float* __restrict__ uniforms, uint64_t seed,
@@ -224,7 +236,33 @@ __global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
     if (logits_out && j < A) logits_out[(size_t)i * A + j] = t;
   }
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 0 && eg.on) {
+    const float adv = lane < A ? lg[lane] : 0.f;
+    const float mean = warp_sum(adv) / (float)A;
+    const float q = lane < A ? (lg[A] + adv) - mean : -INFINITY;
+    if (logits_out && lane < A) logits_out[(size_t)i * A + lane] = q;
+    const float qmax = warp_max(q);
+    const unsigned ism = __ballot_sync(0xffffffffu, lane < A && q == qmax);
+    const int greedy = ism ? __ffs(ism) - 1 : 0;
+    float u0, u1;
+    if (uniforms) {
+      u0 = uniforms[2 * i];
+      u1 = uniforms[2 * i + 1];
+    } else {
+      const uint4 r = philox4x32_10(
+          make_uint4((uint32_t)counter, (uint32_t)(counter >> 32), (uint32_t)a, 0u),
+          make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+      u0 = (float)(r.x >> 8) * (1.f / 16777216.f);
+      u1 = (float)(r.y >> 8) * (1.f / 16777216.f);
+    }
+    const float eps = eg.n_eps > 1 ? powf(eg.base, 1.f + eg.alpha * (float)a / (float)(eg.n_eps - 1)) : eg.base;
+    const int act = u0 < eps ? min((int)(u1 * (float)A), A - 1) : greedy;
+    if (lane == 0) {
+      action_out[i] = act;
+      blp_out[i] = logf(eps / (float)A + (act == greedy ? 1.f - eps : 0.f));
+      tla[a] = act;
+    }
+  } else if (warp == 0) {
     const float z = lane < A ? lg[lane] : -INFINITY;
     const float mx = warp_max(z);
     const float e = lane < A ? expf(z - mx) : 0.f;
@@ -406,14 +444,14 @@ extern "C" seed_status seed_infer_workspace_size(const seed_net_spec* spec, int 
   return SEED_OK;
 }
 
-extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_lowp,
-                                  const float* params, const seed_state_table* table, int n,
-                                  const int32_t* actor_ids, const uint8_t* obs,
-                                  const float* reward, const uint8_t* done,
-                                  const float* uniforms, uint64_t seed, uint64_t counter,
-                                  int32_t* action_out, float* blp_out, float* logits_out,
-                                  const seed_unroll_store* store, void* ws, size_t ws_bytes,
-                                  void* stream) {
+static seed_status infer_impl(const seed_net_spec* spec, const void* params_lowp,
+                              const float* params, const seed_state_table* table, int n,
+                              const int32_t* actor_ids, const uint8_t* obs,
+                              const float* reward, const uint8_t* done,
+                              const float* uniforms, uint64_t seed, uint64_t counter,
+                              int32_t* action_out, float* blp_out, float* logits_out,
+                              const seed_unroll_store* store, void* ws, size_t ws_bytes,
+                              void* stream, const EpsGreedy& eg) {
   NetPlan p;
   SEED_TRY(make_net_plan(spec, &p));
   if (p.kind != SEED_NET_ATARI_SHALLOW || !learner_supported(p)) return SEED_E_UNSUPPORTED;
@@ -463,7 +501,7 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
     gsplits = gemm_effective_splits(pr.K, pick_splits(pr.M, pr.N, 128, pr.K));
     SEED_TRY(launch_gemm<128>(pr, gsplits, st, splitk, 0, nullptr, /*run_finish=*/false));
   }
-  SEED_TRY(launch_k(infer_cell_heads_kernel, dim3(n), dim3(ICH_THREADS), 0, st, A,
+  SEED_TRY(launch_k(infer_cell_heads_kernel, dim3(n), dim3(ICH_THREADS), 0, st, eg, A,
                     (const float*)at(w.xproj), gsplits > 1 ? (const float*)splitk : nullptr, gsplits,
                     params + p.t[p.i_lb].off, (const float*)at(w.cpre), done, actor_ids,
                     params + p.t[p.i_hw].off, params + p.t[p.i_hb].off, uniforms, seed, counter,
@@ -478,6 +516,34 @@ extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_
         (const float*)at(w.hpre), (const float*)at(w.cpre), *store);
   }
   return last_launch();
+}
+
+extern "C" seed_status seed_infer(const seed_net_spec* spec, const void* params_lowp,
+                                  const float* params, const seed_state_table* table, int n,
+                                  const int32_t* actor_ids, const uint8_t* obs,
+                                  const float* reward, const uint8_t* done,
+                                  const float* uniforms, uint64_t seed, uint64_t counter,
+                                  int32_t* action_out, float* blp_out, float* logits_out,
+                                  const seed_unroll_store* store, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  const EpsGreedy off{0, 0.f, 0.f, 0};
+  return infer_impl(spec, params_lowp, params, table, n, actor_ids, obs, reward, done, uniforms, seed,
+                    counter, action_out, blp_out, logits_out, store, ws, ws_bytes, stream, off);
+}
+
+extern "C" seed_status seed_infer_eps_greedy(const seed_net_spec* spec, const void* params_lowp,
+                                             const float* params, const seed_state_table* table, int n,
+                                             const int32_t* actor_ids, const uint8_t* obs,
+                                             const float* reward, const uint8_t* done,
+                                             const float* uniforms, uint64_t seed, uint64_t counter,
+                                             float eps_base, float eps_alpha, int num_actors_eps,
+                                             int32_t* action_out, float* blp_out, float* q_out,
+                                             const seed_unroll_store* store, void* ws, size_t ws_bytes,
+                                             void* stream) {
+  if (!(eps_base >= 0.f && eps_base <= 1.f) || !(eps_alpha >= 0.f) || num_actors_eps < 1) return SEED_E_ARG;
+  const EpsGreedy eg{1, eps_base, eps_alpha, num_actors_eps};
+  return infer_impl(spec, params_lowp, params, table, n, actor_ids, obs, reward, done, uniforms, seed,
+                    counter, action_out, blp_out, q_out, store, ws, ws_bytes, stream, eg);
 }
 
 extern "C" seed_status seed_assemble_batch(const seed_unroll_store* store, int obs_bytes,

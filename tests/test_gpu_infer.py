@@ -365,3 +365,48 @@ def test_wire_actors_to_inference_and_back():
     for req, a in log:   # replay on the fresh server: the same actions, bit for bit
         a2, _, _ = _call(srv2, req)
         np.testing.assert_array_equal(a2, a)
+
+
+def test_infer_eps_greedy_r2d2_actors():
+    """R2D2 actors (seed_infer_eps_greedy; P:591 dueling heads, P:614 per-actor
+    epsilon-greedy): Q vs the oracle (C22), the explore / greedy decisions bit-exact
+    (greedy = first maximum of the kernel's own Q; explore = floor(u1 * A)), the
+    behaviour log-probs and the state table against the oracle; the Philox path is
+    reproducible."""
+    S, srv, ospec, params = _setup(store=False)
+    th, tc, tla = (srv.h.cpu().numpy(), srv.c.cpu().numpy(), srv.last_action.cpu().numpy())
+    n = 16
+    req = seedgen.infer_requests((84, 84, 4), A, NA, n, seed=11)
+    req["done"][:2] = 1
+    g = np.random.default_rng(3)
+    u = np.stack([np.where(np.arange(n) % 2 == 0, 0.0, 1.0), g.random(n)], axis=1).astype(np.float32)
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in req.items()}
+    q = torch.empty(n, A, device="cuda")
+    a, blp = srv.infer_eps_greedy(d["actor_ids"], d["obs"], d["reward"], d["done"],
+                                  torch.from_numpy(u).cuda(), num_actors_eps=NA, q_out=q)
+    torch.cuda.synchronize()
+    a, blp, q = a.cpu().numpy(), blp.cpu().numpy(), q.cpu().numpy()
+    ra, rblp, rq, rth, rtc, rtla = O.infer_eps_greedy(ospec, params, th, tc, tla, req["actor_ids"],
+                                                       req["obs"], req["reward"], req["done"], u, NA,
+                                                       emu=True)
+    assert _relL2(q, rq) < 2e-2
+    ids = req["actor_ids"]
+    explore = u[:, 0] < np.array([O.actor_epsilon(int(i), NA) for i in ids])
+    assert explore.sum() == n // 2
+    np.testing.assert_array_equal(a[explore], np.minimum(np.floor(u[explore, 1] * A), A - 1))
+    np.testing.assert_array_equal(a[~explore], np.argmax(q[~explore], axis=1))   # first maximum
+    np.testing.assert_array_equal(a, ra)
+    eps = np.array([O.actor_epsilon(int(i), NA) for i in ids])
+    greedy = np.argmax(q, axis=1)
+    np.testing.assert_allclose(blp, np.log(eps / A + (1 - eps) * (a == greedy)), rtol=1e-5, atol=1e-6)
+    assert _relL2(srv.h.cpu().numpy()[ids], rth[ids]) < 2e-2
+    np.testing.assert_array_equal(srv.last_action.cpu().numpy()[ids], a)
+    # Philox draws: same (seed, counter, state) -> same actions
+    S2, srv2, _, _ = _setup(store=False)
+    S3, srv3, _, _ = _setup(store=False)
+    outs = []
+    for s in (srv2, srv3):
+        aa, _ = s.infer_eps_greedy(d["actor_ids"], d["obs"], d["reward"], d["done"], None, seed=5,
+                                   counter=9, num_actors_eps=NA)
+        outs.append(aa.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])

@@ -690,3 +690,34 @@ def test_r2d2_learner_step_finite_differences():
             e[i] = 1e-6
             fd = (loss(params + e) - loss(params - e)) / 2e-6
             assert abs(fd - ref["grads"][i]) <= 1e-6 + 1e-4 * abs(fd), (name, k, fd, ref["grads"][i])
+
+
+def test_actor_epsilon_P614_and_eps_greedy():
+    """epsilon_i = 0.4^(1 + 7 i / (N - 1)) — the first actor explores at 0.4, the
+    last at 0.4^8; epsilon-greedy: the behaviour probabilities of one state sum to 1
+    over the actions (enumerated through the uniform draws), the greedy action gets
+    1 - eps + eps/A, ties go to the first maximum."""
+    assert O.actor_epsilon(0, 610) == pytest.approx(0.4, abs=0)
+    assert O.actor_epsilon(609, 610) == pytest.approx(0.4 ** 8, rel=1e-15)
+    assert O.actor_epsilon(0, 1) == 0.4
+    assert O.actor_epsilon(3, 7) == pytest.approx(0.4 ** (1 + 7 * 3 / 6), rel=1e-15)
+    q = np.array([0.5, 2.0, -1.0, 2.0])
+    eps = 0.3
+    # greedy branch: first maximum
+    a, p = O.eps_greedy_action(q, eps, u_explore=0.9, u_action=0.0)
+    assert a == 1 and p == pytest.approx(eps / 4 + 1 - eps)
+    # explore branch: floor(u * A), clamped
+    assert O.eps_greedy_action(q, eps, 0.1, 0.0)[0] == 0
+    assert O.eps_greedy_action(q, eps, 0.1, 0.74)[0] == 2
+    assert O.eps_greedy_action(q, eps, 0.1, 1.0)[0] == 3
+    # the behaviour distribution, enumerated over a fine grid of (u0, u1), sums to 1 and
+    # matches the returned probabilities
+    g = (np.arange(200) + 0.5) / 200
+    freq = np.zeros(4)
+    for u0 in g:
+        for u1 in g:
+            freq[O.eps_greedy_action(q, eps, u0, u1)[0]] += 1
+    freq /= freq.sum()
+    probs = np.array([eps / 4 + (1 - eps) * (k == 1) for k in range(4)])
+    np.testing.assert_allclose(freq, probs, atol=1e-12)
+    assert probs.sum() == pytest.approx(1.0)
