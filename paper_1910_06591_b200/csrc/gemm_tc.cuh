@@ -35,9 +35,54 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <type_traits>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "common.cuh"
 
 namespace seed {
+
+// ---------------------------------------------------------------- TMA tensor maps
+// A Problem whose A and B are plain K-major bf16 matrices ([rows][K], row stride
+// ld elements) may declare `static constexpr bool TMA = true` with CUtensorMap
+// members ta / tb (filled by its host method tmaps()): one producer thread then
+// moves each 128x64 / BNx64 tile with one cp.async.bulk.tensor (UTMALDG) into the
+// same 128-byte-swizzled layout the cp.async path writes (TileMap K-major), the
+// tensor unit zero-filling rows >= M / N and k >= K.
+inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+// K-major bf16 [rows][K] (row stride ld elements, 16-byte aligned base and stride)
+// with a box of 64 k x box_rows rows, 128-byte swizzle
+inline bool tmap_kmajor(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc || ((uintptr_t)base & 15) || (ld * 2) % 16) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+template <class P, class = void>
+struct HasTma : std::false_type {};
+template <class P>
+struct HasTma<P, std::void_t<decltype(P::TMA)>> : std::integral_constant<bool, P::TMA> {};
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
@@ -290,14 +335,16 @@ __device__ long long g_gemm_prof[8];
 #endif
 
 template <int BN, class Prob>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, float* __restrict__ part,
-                                                                  int splits, unsigned* cnt) {
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ Prob p,
+                                                                  float* __restrict__ part, int splits,
+                                                                  unsigned* cnt) {
   GEMM_STAMP(0, threadIdx.x == 0)
   using Cfg = GemmCfg<BN, Prob::A_MN, Prob::B_MN>;
   using TA = typename Cfg::TA;
   using TB = typename Cfg::TB;
   constexpr int BK = GEMM_BK, S = Cfg::STAGES;
   constexpr bool ASYNC = IsAsync<Prob>::value;
+  constexpr bool TMA = HasTma<Prob>::value;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
   uint64_t* empty = full + S;
@@ -314,7 +361,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], GEMM_PRODUCERS);
+      mbar_init(&full[s], TMA ? 1 : GEMM_PRODUCERS);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -352,7 +399,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const Prob p, 
         if (g >= S) mbar_wait(&empty[s], ((g / S) - 1) & 1);
         const int k0 = (kb0 + i) * BK;
         const uint32_t sa = smem0 + s * Cfg::STAGE_BYTES, sb = sa + Cfg::A_BYTES;
-        if constexpr (ASYNC) {
+        if constexpr (TMA) {   // one thread: two tensor copies credited to the stage
+          if (tid == 0) {
+            mbar_expect_tx(&full[s], (uint32_t)(GEMM_BM + BN) * BK * 2);
+            tma_load_2d(sa, &p.ta, k0, m0, &full[s]);
+            tma_load_2d(sb, &p.tb, k0, n0, &full[s]);
+          }
+        } else if constexpr (ASYNC) {
           // zero chunks (padding, transposed-conv zero taps) are plain shared
           // stores: a zero-fill cp.async would still send a request to memory
           bool zeroed = false;
@@ -518,6 +571,9 @@ seed_status launch_gemm(Prob p, int splits, cudaStream_t st, float* part = nullp
   if (splits > nkb) splits = nkb > 0 ? nkb : 1;
   p.kb_per_split = (nkb + splits - 1) / splits;
   splits = nkb > 0 ? (nkb + p.kb_per_split - 1) / p.kb_per_split : 1;
+  if constexpr (HasTma<Prob>::value) {
+    if (!p.tmaps(BN)) return SEED_E_ARG;   // base / stride not 16-byte aligned, or no driver entry point
+  }
   static PerDevice attr;
   SEED_TRY(smem_optin(attr, gemm_tc_kernel<BN, Prob>, Cfg::SMEM));
   const int sms = sm_count();

@@ -51,6 +51,8 @@ __device__ __forceinline__ void relu_mask16(const bf16* src, float (&v)[16]) {
 // fc: X[f][0:256] = relu(act2[f] . Wfc^T + b)
 struct FcFwd {
   static constexpr bool ASYNC = true;
+  static constexpr bool TMA = true;   // plain K-major A [M][K] and B [N][K]: tensor-map tiles
+  CUtensorMap ta, tb;
   const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = false;
   int M, N, K, kb_per_split;
@@ -59,6 +61,7 @@ struct FcFwd {
   const bf16* w;
   const float* bias;
   bf16* X;
+  bool tmaps(int bn) { return tmap_kmajor(&ta, act2, M, K, K, 128) && tmap_kmajor(&tb, w, N, K, K, bn); }
   __device__ const void* ptr_a(int m, int k) const { return act2 + (size_t)m * K + k; }
   __device__ const void* ptr_b(int n, int k) const { return w + (size_t)n * K + k; }
   __device__ void store(int m, int n, float v) const {
@@ -75,6 +78,8 @@ struct FcFwd {
 // LSTM input projection: xproj[f][n] = X[f] . Wx[n] + b[n]
 struct XprojFwd {
   static constexpr bool ASYNC = true;
+  static constexpr bool TMA = true;   // plain K-major A [M][K] and B [N][K]: tensor-map tiles
+  CUtensorMap ta, tb;
   const void* dummy = k_ones_chunk;
   static constexpr bool A_MN = false, B_MN = false;
   int M, N, K, kb_per_split;
@@ -82,6 +87,7 @@ struct XprojFwd {
   const bf16* w;
   const float* bias;
   float* out;
+  bool tmaps(int bn) { return tmap_kmajor(&ta, X, M, K, K, 128) && tmap_kmajor(&tb, w, N, K, K, bn); }
   __device__ const void* ptr_a(int m, int k) const { return X + (size_t)m * K + k; }
   __device__ const void* ptr_b(int n, int k) const { return w + (size_t)n * K + k; }
   __device__ void store(int m, int n, float v) const { out[(size_t)m * N + n] = v + bias[n]; }
