@@ -261,7 +261,11 @@ extern "C" int seed_debug_heads_prof(long long* out) {
 #define HL_STAMP(I)
 #endif
 
-__global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS)
+// MINB = 2 (64 registers, two CTAs per SM) when the trajectories' clusters exceed one
+// wave of 148 SMs at one CTA each (c4: B = 128 -> 512 CTAs, 81 -> 69 us); below that
+// the 99-register form is faster (c2: 24 vs 27 us)
+template <int MINB>
+__global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS, MINB)
     heads_loss_kernel(const LossArgs a) {
   HL_STAMP(0)
   extern __shared__ float hsm[];
@@ -533,9 +537,17 @@ seed_status launch_heads_loss(const LossArgs& a, cudaStream_t st) {
   // Hc holds HL_RC rows of H, later the [A+1][I] row-parity partials (A+1 <= HL_RC+1)
   const size_t smem = ((((size_t)a.I * A1p + (size_t)(a.T + 1) * A1p + 3) & ~(size_t)3) +
                        (size_t)(HL_RC + 1) * a.I) * 4;
-  static PerDevice attr;
-  SEED_TRY(smem_optin(attr, heads_loss_kernel, (int)std::max<size_t>((256 * 33 + 257 * 33 + 4 + (HL_RC + 1) * 256) * 4, (size_t)HL_CL * 33 * 257 * 4)));
-    SEED_TRY(launch_k(heads_loss_kernel, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
+  const int smax = (int)std::max<size_t>((256 * 33 + 257 * 33 + 4 + (HL_RC + 1) * 256) * 4,
+                                          (size_t)HL_CL * 33 * 257 * 4);
+  if (a.B * HL_CL > 148) {
+    static PerDevice attr2;
+    SEED_TRY(smem_optin(attr2, heads_loss_kernel<2>, smax));
+    SEED_TRY(launch_k(heads_loss_kernel<2>, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
+  } else {
+    static PerDevice attr1;
+    SEED_TRY(smem_optin(attr1, heads_loss_kernel<1>, smax));
+    SEED_TRY(launch_k(heads_loss_kernel<1>, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
+  }
   const int n = (a.A + 1) * (a.I + 1);
   return launch_k(heads_wgrad_finish, dim3(ceil_div(n, 32)), dim3(256), 0, st, a.B * HL_CL, a.A + 1,
                   a.I, (const float*)a.wpart, a.g_w, a.g_b);
