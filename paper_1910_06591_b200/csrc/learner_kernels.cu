@@ -264,15 +264,17 @@ extern "C" int seed_debug_heads_prof(long long* out) {
 // MINB = 2 (64 registers, two CTAs per SM) when the trajectories' clusters exceed one
 // wave of 148 SMs at one CTA each (c4: B = 128 -> 512 CTAs, 81 -> 69 us); below that
 // the 99-register form is faster (c2: 24 vs 27 us)
-template <int MINB>
-__global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS, MINB)
+// CL = CTAs (cluster) per trajectory: 4, or 2 when B is large enough that 4 would
+// need more than one wave even at two CTAs per SM
+template <int MINB, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(HL_THREADS, MINB)
     heads_loss_kernel(const LossArgs a) {
   HL_STAMP(0)
   extern __shared__ float hsm[];
   const int I = a.I, A = a.A, A1 = A + 1, A1p = A1 | 1;
-  const int T = a.T, T1 = T + 1, b = blockIdx.x / HL_CL;
+  const int T = a.T, T1 = T + 1, b = blockIdx.x / CL;
   const int cr = (int)cluster_rank();
-  const int Rr = (T1 + HL_CL - 1) / HL_CL, rb0 = min(T1, cr * Rr), rb1 = min(T1, rb0 + Rr);
+  const int Rr = (T1 + CL - 1) / CL, rb0 = min(T1, cr * Rr), rb1 = min(T1, rb0 + Rr);
   const size_t row0 = (size_t)b * T1;
   float* Wt = hsm;                  // [I][A1p]
   float* sL = Wt + I * A1p;         // [T1][A1p]: logits | value, then their gradients
@@ -310,7 +312,7 @@ __global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS, MINB
   pdl_wait();
   cluster_sync_all();   // every CTA of the cluster runs before any DSMEM store
   // ---- phase 1: heads forward of this CTA's rows, one (row, output) dot product
-  // per thread; results stored into all HL_CL CTAs' sL (DSMEM all-gather)
+  // per thread; results stored into all CL CTAs' sL (DSMEM all-gather)
   for (int r0 = rb0; r0 < rb1; r0 += HL_RC) {
     const int nr = min(HL_RC, rb1 - r0);
     __syncthreads();
@@ -333,7 +335,7 @@ __global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS, MINB
       const int t = r0 + rr;
       const uint32_t la = smem_u32(sL + t * A1p + o);
 #pragma unroll
-      for (int d = 0; d < HL_CL; ++d) st_cluster_f32(mapa_u32(la, d), y);
+      for (int d = 0; d < CL; ++d) st_cluster_f32(mapa_u32(la, d), y);
       if (o < A) a.logits[(row0 + t) * A + o] = y;
       else a.values[row0 + t] = y;
     }
@@ -493,7 +495,7 @@ __global__ void __cluster_dims__(HL_CL, 1, 1) __launch_bounds__(HL_THREADS, MINB
   // heads_wgrad_finish sums them in (b, rank) order
   {
     const int n = A1 * (I + 1);
-    float* wp = a.wpart + ((size_t)b * HL_CL + cr) * n;
+    float* wp = a.wpart + ((size_t)b * CL + cr) * n;
     if (col && rg == 0) {
 #pragma unroll
       for (int o = 0; o < AMAX; ++o)
@@ -539,17 +541,23 @@ seed_status launch_heads_loss(const LossArgs& a, cudaStream_t st) {
                        (size_t)(HL_RC + 1) * a.I) * 4;
   const int smax = (int)std::max<size_t>((256 * 33 + 257 * 33 + 4 + (HL_RC + 1) * 256) * 4,
                                           (size_t)HL_CL * 33 * 257 * 4);
-  if (a.B * HL_CL > 148) {
+  int cl = HL_CL;
+  if (a.B * HL_CL > 2 * 148) {          // more than one wave at two CTAs per SM
+    cl = 2;
+    static PerDevice attr;
+    SEED_TRY(smem_optin(attr, heads_loss_kernel<2, 2>, smax));
+    SEED_TRY(launch_k(heads_loss_kernel<2, 2>, dim3(a.B * 2), dim3(HL_THREADS), smem, st, a));
+  } else if (a.B * HL_CL > 148) {
     static PerDevice attr2;
-    SEED_TRY(smem_optin(attr2, heads_loss_kernel<2>, smax));
-    SEED_TRY(launch_k(heads_loss_kernel<2>, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
+    SEED_TRY(smem_optin(attr2, heads_loss_kernel<2, HL_CL>, smax));
+    SEED_TRY(launch_k(heads_loss_kernel<2, HL_CL>, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
   } else {
     static PerDevice attr1;
-    SEED_TRY(smem_optin(attr1, heads_loss_kernel<1>, smax));
-    SEED_TRY(launch_k(heads_loss_kernel<1>, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
+    SEED_TRY(smem_optin(attr1, heads_loss_kernel<1, HL_CL>, smax));
+    SEED_TRY(launch_k(heads_loss_kernel<1, HL_CL>, dim3(a.B * HL_CL), dim3(HL_THREADS), smem, st, a));
   }
   const int n = (a.A + 1) * (a.I + 1);
-  return launch_k(heads_wgrad_finish, dim3(ceil_div(n, 32)), dim3(256), 0, st, a.B * HL_CL, a.A + 1,
+  return launch_k(heads_wgrad_finish, dim3(ceil_div(n, 32)), dim3(256), 0, st, a.B * cl, a.A + 1,
                   a.I, (const float*)a.wpart, a.g_w, a.g_b);
 }
 
