@@ -599,17 +599,35 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
 // the 2x2 windows (a-1 | a) x (b-1 | b): an even offset is tap 2 of window a-1 and
 // tap 0 of window a, an odd offset tap 1 of window a.  The four windows' (argmax,
 // dout) are loaded once for the four pixels; sums in ascending window order.
+// chunk i of the border rows of a padded row space (per frame: top / bottom rows,
+// and the left / right pixels of the interior rows) <- 0
+__device__ __forceinline__ void zero_border_chunk(int64_t i, int NC, int RB, const PadGeo& g, uint8_t* buf) {
+  const int j = (int)(i % NC);
+  const int64_t r = i / NC;
+  const int per = 2 * g.Wp + 2 * g.H;
+  const int64_t f = r / per;
+  const int k = (int)(r - f * per);
+  int Y, X;
+  if (k < 2 * g.Wp) { Y = k < g.Wp ? 0 : g.H + 1; X = k % g.Wp; }
+  else { Y = 1 + (k - 2 * g.Wp) / 2; X = ((k - 2 * g.Wp) & 1) ? g.W + 1 : 0; }
+  *chunk_at(buf, f * g.P + (int64_t)Y * g.Wp + X, RB, j) = make_uint4(0, 0, 0, 0);
+}
+
 template <int NC>
 __global__ void __launch_bounds__(256) conv3w_pool_bwd_kernel(
-    PadGeo gi, PadGeo go, int pt, int pl, int64_t total, FastDiv frow, FastDiv fnby,
+    PadGeo gi, PadGeo go, int pt, int pl, int64_t total, int64_t nz, FastDiv frow, FastDiv fnby,
     const uint8_t* __restrict__ dout, const uint8_t* __restrict__ arg, uint8_t* __restrict__ din) {
   pdl_wait();
   constexpr int C = NC * 8, RB = NC * 16;
   // flat thread index -> (frame f, block row a, block column b, chunk j): full 256-thread
   // blocks instead of one 2-row strip per block (measured: 4.0 TB/s at c4 s0 with
-  // strip blocks of 98 active threads)
+  // strip blocks of 98 active threads); threads past `total` zero the border rows
+  // of din (formerly a separate launch)
   const int64_t tt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (tt >= total) return;
+  if (tt >= total) {
+    if (tt < total + nz) zero_border_chunk(tt - total, NC, RB, gi, din);
+    return;
+  }
   uint32_t fa, rem, f32, a32;
   frow.divmod((uint32_t)tt, fa, rem);
   fnby.divmod(fa, f32, a32);
@@ -659,22 +677,6 @@ __global__ void __launch_bounds__(256) conv3w_pool_bwd_kernel(
 
 // zero the border rows of a padded row space (per frame: top / bottom rows, and
 // the left / right pixels of the interior rows)
-template <int NC>
-__global__ void __launch_bounds__(ROWK_THREADS) zero_border_kernel(int64_t n, PadGeo g, uint8_t* __restrict__ buf) {
-  pdl_wait();
-  constexpr int RB = NC * 16;
-  const int64_t i = blockIdx.x * (int64_t)ROWK_THREADS + threadIdx.x;
-  if (i >= n) return;
-  const int j = (int)(i % NC);
-  const int64_t r = i / NC;
-  const int per = 2 * g.Wp + 2 * g.H;
-  const int64_t f = r / per;
-  const int k = (int)(r - f * per);
-  int Y, X;
-  if (k < 2 * g.Wp) { Y = k < g.Wp ? 0 : g.H + 1; X = k % g.Wp; }
-  else { Y = 1 + (k - 2 * g.Wp) / 2; X = ((k - 2 * g.Wp) & 1) ? g.W + 1 : 0; }
-  *chunk_at(buf, f * g.P + (int64_t)Y * g.Wp + X, RB, j) = make_uint4(0, 0, 0, 0);
-}
 
 seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
                             const uint8_t* conv, uint8_t* h0, uint8_t* hr0, uint8_t* arg,
@@ -698,26 +700,19 @@ seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
   const int NC = C / 8;
   const int nby = (gi.H + pt + 1) >> 1, nbx = (gi.W + pl + 1) >> 1;
   const int64_t total = F * nby * nbx * NC;
-  if (total >= (1ll << 31)) return SEED_E_SHAPE;
-  const FastDiv frow((uint32_t)(nbx * NC)), fnby((uint32_t)nby);
-  const dim3 grid((unsigned)((total + 255) / 256));
   const int64_t nz = F * (2 * gi.Wp + 2 * gi.H) * NC;
-  const dim3 gz((unsigned)((nz + ROWK_THREADS - 1) / ROWK_THREADS));
-  if (NC == 2) {
-    SEED_TRY(launch_k(zero_border_kernel<2>, gz, dim3(ROWK_THREADS), 0, st, nz, gi, din));
-    return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(256), 0, st, gi, go, pt, pl, total, frow, fnby,
+  if (total + nz >= (1ll << 31)) return SEED_E_SHAPE;
+  const FastDiv frow((uint32_t)(nbx * NC)), fnby((uint32_t)nby);
+  const dim3 grid((unsigned)((total + nz + 255) / 256));
+  if (NC == 2)
+    return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(256), 0, st, gi, go, pt, pl, total, nz, frow, fnby,
                     dout, arg, din);
-  }
-  if (NC == 4) {
-    SEED_TRY(launch_k(zero_border_kernel<4>, gz, dim3(ROWK_THREADS), 0, st, nz, gi, din));
-    return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(256), 0, st, gi, go, pt, pl, total, frow, fnby,
+  if (NC == 4)
+    return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(256), 0, st, gi, go, pt, pl, total, nz, frow, fnby,
                     dout, arg, din);
-  }
-  if (NC == 8) {
-    SEED_TRY(launch_k(zero_border_kernel<8>, gz, dim3(ROWK_THREADS), 0, st, nz, gi, din));
-    return launch_k(conv3w_pool_bwd_kernel<8>, grid, dim3(256), 0, st, gi, go, pt, pl, total, frow, fnby,
+  if (NC == 8)
+    return launch_k(conv3w_pool_bwd_kernel<8>, grid, dim3(256), 0, st, gi, go, pt, pl, total, nz, frow, fnby,
                     dout, arg, din);
-  }
   return SEED_E_UNSUPPORTED;
 }
 

@@ -503,7 +503,7 @@ static seed_status plane_section_backward(const StepCtx& c, int s, const bf16* l
   for (int q = 0; q < npo; ++q) {
     SEED_TRY(conv3w_pool_bwd(F, gi, go, 64, d.pt, d.pl, plane_at(c, cur, q, ro),
                              c.at<uint8_t>(b.arg) + (size_t)q * ro * 64, plane_at(c, b.dconv, q, ri), st));
-    c.mark("deep_pool_bwd", 2);
+    c.mark("deep_pool_bwd");
   }
   if (s == 0 || d.xim) return SEED_E_UNSUPPORTED;   // plane sections follow a 64-channel section
   SEED_TRY(wgrad(c.at<uint8_t>(w.sec[s - 1].h[2]), npi, cpi, c.at<uint8_t>(b.dconv), ri, gi, d.cin, d.t_w, d.t_b,
@@ -621,7 +621,7 @@ static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const b
     // max-pool backward into dconv, then the section conv
     SEED_TRY(conv3w_pool_bwd(F, gi, go, d.ch, d.pt, d.pl, c.at<uint8_t>(cur), c.at<uint8_t>(b.arg),
                              c.at<uint8_t>(b.dconv), st));
-    c.mark("deep_pool_bwd", 2);
+    c.mark("deep_pool_bwd");
     Conv3wWgrad wg{};
     wg.cin_p = d.cinp; wg.cin = d.cin; wg.ch = d.ch; wg.xim = d.xim; wg.g = gi; wg.rows = F * gi.P;
     wg.scale = s == 0 ? 1.f / 255.f : 1.f;
