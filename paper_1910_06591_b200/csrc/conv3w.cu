@@ -85,8 +85,32 @@ struct W3FwdEpi {
         if (MODE == W3_RELU) v[q] = fmaxf(v[q], 0.f);
       }
     }
-    if constexpr (MODE == W3_RES) {
-      // per 8-channel chunk: + residual, h, relu(h) (of the rounded h), dense relu(h)
+    if constexpr (MODE == W3_RES && N <= 32) {   // (measured faster than the chunked form at N <= 32)
+#pragma unroll
+      for (int j = 0; j < N / 8; ++j) {
+        float r[8];
+        unpack8(p[j], r);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[8 * j + k] += r[k];
+      }
+#pragma unroll
+      for (int j = 0; j < N / 8; ++j) *chunk_at(out, m, RB, j) = pack8(v + 8 * j);
+      float r[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) r[q] = fmaxf(__bfloat162float(__float2bfloat16_rn(v[q])), 0.f);
+      if (outr) {
+#pragma unroll
+        for (int j = 0; j < N / 8; ++j) *chunk_at(outr, m, RB, j) = pack8(r + 8 * j);
+      }
+      if (dense) {
+        const int ct = dense_ct > 0 ? dense_ct : N;
+        uint4* d = reinterpret_cast<uint4*>(dense + ((int64_t)f * g.H * g.W + (int64_t)y * g.W + x) * ct + dense_off);
+#pragma unroll
+        for (int j = 0; j < N / 8; ++j) d[j] = pack8(r + 8 * j);
+      }
+    } else if constexpr (MODE == W3_RES) {
+      // 64 channels, per 8-channel chunk (no second N-float array: the array form spills):
+      // + residual, h, relu(h) (of the rounded h), dense relu(h)
       uint4* d = nullptr;
       if (dense) {
         const int ct = dense_ct > 0 ? dense_ct : N;
