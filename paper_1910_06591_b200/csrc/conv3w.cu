@@ -143,8 +143,11 @@ template <int MODE, int NN>
 struct W3DgradEpi {
   static constexpr int N = NN;
   static constexpr int RB = 2 * NN;
-  // the mask row, then (D3W_RES) the incoming residual-gradient row
-  static constexpr int PRE = (MODE == D3W_PLAIN || MODE == D3W_PART) ? 0 : (MODE == D3W_MASK ? N / 8 : N / 4);
+  // the mask row, then (D3W_RES) the incoming residual-gradient row (at 64 channels
+  // the residual row is read in the store instead: prefetching both spills)
+  static constexpr bool DRES_PRE = N <= 32;
+  static constexpr int PRE = (MODE == D3W_PLAIN || MODE == D3W_PART) ? 0
+                             : (MODE == D3W_MASK || !DRES_PRE) ? N / 8 : N / 4;
   PadGeo g;
   const uint8_t* mask;
   const uint8_t* dres;
@@ -155,7 +158,7 @@ struct W3DgradEpi {
     if (MODE == D3W_PLAIN || MODE == D3W_PART) return;
 #pragma unroll
     for (int j = 0; j < N / 8; ++j) p[j] = __ldg(chunk_at(mask, m, RB, j));
-    if (MODE == D3W_RES) {
+    if constexpr (MODE == D3W_RES && DRES_PRE) {
 #pragma unroll
       for (int j = 0; j < N / 8; ++j) p[N / 8 + j] = __ldg(chunk_at(dres, m, RB, j));
     }
@@ -200,7 +203,8 @@ struct W3DgradEpi {
 #pragma unroll
       for (int j = 0; j < N / 8; ++j) {
         float r[8];
-        unpack8(p[N / 8 + j], r);
+        if constexpr (DRES_PRE) unpack8(p[N / 8 + j], r);
+        else unpack8(__ldg(chunk_at(dres, m, RB, j)), r);
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[8 * j + k] += r[k];
       }
