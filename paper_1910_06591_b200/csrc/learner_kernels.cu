@@ -781,15 +781,27 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
       }
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double l0 = 0, l1 = 0, l2 = 0;
-    float nonfin = finite ? 0.f : 1.f;
-    for (int b = 0; b < a.B; ++b) {
-      l0 += a.loss_part[b * 4 + 0];
-      l1 += a.loss_part[b * 4 + 1];
-      l2 += a.loss_part[b * 4 + 2];
-      if (a.loss_part[b * 4 + 3] != 0.f) nonfin = 1.f;
+  if (blockIdx.x == 0) {
+    // per-trajectory loss partials: strided over the block's threads, then a
+    // fixed-order block reduction (was one thread looping over B: the kernel's
+    // straggler at B = 128)
+    double q0 = 0, q1 = 0, q2 = 0;
+    int nf = 0;
+    for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
+      q0 += a.loss_part[b * 4 + 0];
+      q1 += a.loss_part[b * 4 + 1];
+      q2 += a.loss_part[b * 4 + 2];
+      nf |= a.loss_part[b * 4 + 3] != 0.f;
     }
+    __shared__ double sh8[8];
+    const double l0 = block_sum_double(q0, sh8);
+    __syncthreads();
+    const double l1 = block_sum_double(q1, sh8);
+    __syncthreads();
+    const double l2 = block_sum_double(q2, sh8);
+    const int anynf = __syncthreads_or(nf);
+    if (threadIdx.x != 0) return;
+    const float nonfin = (finite && !anynf) ? 0.f : 1.f;
     const int64_t ver = *a.step_in + (finite ? 1 : 0);
     const double norm = *a.norm;
     a.metrics[0] = (float)(l0 + l1 + l2);
