@@ -85,10 +85,52 @@ __device__ __forceinline__ Band band_of(const CpArgs& a, int64_t bi) {
   return b;
 }
 
-template <int N, int RB, int NW>
-__global__ void __launch_bounds__(CP_THREADS, 1)
+// The max-pool of one band from the shared-memory band buffer (epilogue thread et
+// of CP_EPI): output padded rows Y of each frame (with the top / bottom border row
+// in the first / last band of a frame), all columns X, 8-channel chunks j.
+template <int N, int EPI = CP_EPI>
+__device__ __forceinline__ void pool_band(const CpArgs& a, const Band& b, const uint8_t* bandbuf, int et) {
+  constexpr int RBO = 2 * N, NC = N / 8;
+  const int Ylo = b.oy0 == 0 ? 0 : b.oy0 + 1;
+  const int Yhi = b.oy1 == a.go.H ? a.go.H + 1 : b.oy1;
+  const int total = b.nf * (Yhi - Ylo + 1) * (int)a.fRow.d;
+  for (int i = et; i < total; i += EPI) {
+    uint32_t fl = 0, rem = (uint32_t)i, Yr, c2;
+    if (a.G > 0) a.fFrame.divmod((uint32_t)i, fl, rem);
+    a.fRow.divmod(rem, Yr, c2);
+    const int X = (int)(c2 / NC), j = (int)(c2 % NC);
+    const int Y = Ylo + (int)Yr;
+    const int64_t g = (b.f0 + fl) * a.go.P + (int64_t)Y * a.go.Wp + X;
+    uint4* ph = reinterpret_cast<uint4*>(a.h0 + g * RBO + (swz_chunk(g, RBO, j) << 4));
+    uint4* pr = reinterpret_cast<uint4*>(a.hr0 + g * RBO + (swz_chunk(g, RBO, j) << 4));
+    if (Y == 0 || Y == a.go.H + 1 || X == 0 || X == a.go.W + 1) {
+      *ph = make_uint4(0, 0, 0, 0);
+      *pr = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    // tap (ky, kx) of output (Y-1, X-1): conv pixel (2(Y-1) - pt + ky, 2(X-1) - pl + kx),
+    // band row fl*P + (y+1)*Wp + (x+1) - base
+    const int r0 = (int)fl * a.gi.P + (2 * Y - 1 - a.pt) * a.gi.Wp + 2 * X - 1 - a.pl - b.base;
+    uint4 in[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int r = r0 + (t / 3) * a.gi.Wp + t % 3;
+      in[t] = *reinterpret_cast<const uint4*>(bandbuf + (size_t)r * RBO + (swz_chunk(r, RBO, j) << 4));
+    }
+    uint4 best, rl;
+    uint2 am;
+    pool_max9(in, best, rl, am);
+    *ph = best;
+    *pr = rl;
+    *reinterpret_cast<uint2*>(a.arg + g * N + 8 * j) = am;
+  }
+}
+
+template <int N, int RB, int NW, int EW = CP_EW>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
     conv_pool_kernel(const CpArgs a, int stages, int slab_bytes, int band_bytes) {
   constexpr int RBO = 2 * N, NC = N / 8;
+  constexpr int EPI = 32 * EW;
   constexpr uint32_t LAYOUT = swz_layout_code(RB);
   constexpr int WB = NW * N * RB;
   constexpr int AC = 256;   // TMEM columns per accumulator (2 accumulators)
@@ -105,7 +147,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
   for (int w = 1; w < NW; ++w) { mn = min(mn, a.off[w]); mx = max(mx, a.off[w]); }
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], CP_EW); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EW); }
     mbar_init(&wbar, 1);
     fence_mbar_init();
   }
@@ -157,8 +199,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
     }
   } else {
     const int q = warp & 3;                      // TMEM lanes [32q, 32q + 32)
-    const int part = (warp - 2) >> 2;            // 128-row blocks mt with mt % (CP_EW / 4) == part
-    const int et = threadIdx.x - 64;
+    const int part = (warp - 2) >> 2;            // 128-row blocks mt with mt % (EW / 4) == part
     float bias[N];
 #pragma unroll
     for (int c = 0; c < N; ++c) bias[c] = __ldg(a.bias + c);
@@ -170,7 +211,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
       const int nblk = (b.R + 127) >> 7;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      for (int mt = part; mt < nblk; mt += CP_EW / 4) {
+      for (int mt = part; mt < nblk; mt += EW / 4) {
         uint32_t vr[N];
 #pragma unroll
         for (int c = 0; c < N / 16; ++c)
@@ -201,43 +242,9 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      asm volatile("bar.sync 1, %0;" ::"n"(CP_EPI) : "memory");   // band buffer complete
-      // pool: output padded rows Y of each frame (with the top / bottom border row
-      // in the first / last band of a frame), all columns X, chunks j
-      const int Ylo = b.oy0 == 0 ? 0 : b.oy0 + 1;
-      const int Yhi = b.oy1 == a.go.H ? a.go.H + 1 : b.oy1;
-      const int total = b.nf * (Yhi - Ylo + 1) * (int)a.fRow.d;
-      for (int i = et; i < total; i += CP_EPI) {
-        uint32_t fl = 0, rem = (uint32_t)i, Yr, c2;
-        if (a.G > 0) a.fFrame.divmod((uint32_t)i, fl, rem);
-        a.fRow.divmod(rem, Yr, c2);
-        const int X = (int)(c2 / NC), j = (int)(c2 % NC);
-        const int Y = Ylo + (int)Yr;
-        const int64_t g = (b.f0 + fl) * a.go.P + (int64_t)Y * a.go.Wp + X;
-        uint4* ph = reinterpret_cast<uint4*>(a.h0 + g * RBO + (swz_chunk(g, RBO, j) << 4));
-        uint4* pr = reinterpret_cast<uint4*>(a.hr0 + g * RBO + (swz_chunk(g, RBO, j) << 4));
-        if (Y == 0 || Y == a.go.H + 1 || X == 0 || X == a.go.W + 1) {
-          *ph = make_uint4(0, 0, 0, 0);
-          *pr = make_uint4(0, 0, 0, 0);
-          continue;
-        }
-        // tap (ky, kx) of output (Y-1, X-1): conv pixel (2(Y-1) - pt + ky, 2(X-1) - pl + kx),
-        // band row fl*P + (y+1)*Wp + (x+1) - base
-        const int r0 = (int)fl * a.gi.P + (2 * Y - 1 - a.pt) * a.gi.Wp + 2 * X - 1 - a.pl - b.base;
-        uint4 in[9];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          const int r = r0 + (t / 3) * a.gi.Wp + t % 3;
-          in[t] = *reinterpret_cast<const uint4*>(bandbuf + (size_t)r * RBO + (swz_chunk(r, RBO, j) << 4));
-        }
-        uint4 best, rl;
-        uint2 am;
-        pool_max9(in, best, rl, am);
-        *ph = best;
-        *pr = rl;
-        *reinterpret_cast<uint2*>(a.arg + g * N + 8 * j) = am;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(CP_EPI) : "memory");   // band buffer free
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI) : "memory");   // band buffer complete
+      pool_band<N, EPI>(a, b, bandbuf, threadIdx.x - 64);
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI) : "memory");   // band buffer free
     }
   }
   __syncthreads();
@@ -247,10 +254,213 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
   }
 }
 
-template <int N, int RB, int NW>
+// Column-tap-stacked variant (win_engine.cuh win_conv_kx_kernel's MMA form): per
+// 128-row block 3 MMAs (one per kernel row ky, window offset (ky-1)*Wp) of
+// N = 3*NO — the three column taps' weights side by side on N (the 9-window weight
+// image read as 3 windows of 3*NO rows) — instead of 9 MMAs of N = NO; the small
+// tcgen05.mma costs ~45 cycles up to N = 48 (profiles/r01/mma_rate_probe.txt), so
+// the tensor side is ~3x cheaper.  The conv output of band row r is
+//   D_0[r-1] + D_1[r] + D_2[r+1]
+// (D_kx: the kx part of the accumulator; the neighbouring rows are the adjacent
+// TMEM lanes).  A band's 128-row blocks stream through a ring of NSLOT TMEM slots
+// of 3*NO columns (per-slot full / empty barriers), so bands are as large as in the
+// 9-window kernel although one block's accumulator is 3x wider.  Each block is
+// drained by one epilogue warp per TMEM lane quarter (blocks round robin over the
+// CP_EW / 4 warps of a quarter): three 8-column TMEM loads per 8-channel chunk, the
+// r-1 / r+1 parts by warp shuffles, interior rows (lanes 1..30) stored to the band
+// buffer at once; the quarter-edge rows (lanes 0 / 31) leave their partial sum and
+// the part their neighbour needs in a shared-memory exchange and are finished after
+// one barrier.  The band's first / last rows are frame border columns (-inf), so no
+// row needs a neighbour outside the band.
+template <int NO, int RB>
+__global__ void __launch_bounds__(CP_THREADS, 1)
+    conv_pool_kx_kernel(const CpArgs a, int stages, int slab_bytes, int band_bytes) {
+  constexpr int NN = 3 * NO, RBO = 2 * NO, NC = NO / 8;
+  constexpr uint32_t LAYOUT = swz_layout_code(RB);
+  constexpr int WB = 3 * NN * RB;
+  constexpr int NSLOT = 512 / NN;           // TMEM slots of one 128-row block each
+  constexpr int XG = 4 * NO;                // exchange floats per 32-row group
+  constexpr int EP = CP_EW / 4;             // epilogue warps per lane quarter
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = smem_align1024(smraw);
+  uint8_t* Ws = sm;
+  uint8_t* slabs = sm + ((WB + 1023) & ~1023);
+  uint8_t* bandbuf = slabs + (size_t)stages * slab_bytes;
+  // exchange per 32-row group g: [0, NO) D_0 of lane 31 | [NO, 2NO) D_2 of lane 0 |
+  // [2NO, 3NO) partial of lane 0 | [3NO, 4NO) partial of lane 31
+  float* xch = reinterpret_cast<float*>(bandbuf + band_bytes);
+  __shared__ uint64_t full[WC_MAX_STAGES], empty[WC_MAX_STAGES], tfull[NSLOT], tempty[NSLOT], wbar;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mn = min(a.off[0], min(a.off[1], a.off[2]));
+  const int mx = max(a.off[0], max(a.off[1], a.off[2]));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int i = 0; i < NSLOT; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    mbar_init(&wbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&tbase, 512);
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(&wbar, WB);
+    bulk_g2s(smem_u32(Ws), a.wimg, WB, &wbar);
+  }
+  pdl_wait();
+  const uint32_t tmem = tbase;
+  if (warp == 0) {
+    int it = 0;
+    for (int64_t bi = blockIdx.x; bi < a.nbands; bi += gridDim.x, ++it) {
+      const int s = it % stages;
+      const Band b = band_of(a, bi);
+      const int nblk = (b.R + 127) >> 7;
+      mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+      load_slab(slabs + (size_t)s * slab_bytes, a.src, RB, b.row0 + mn, nblk * 128 + mx - mn, a.src_rows,
+                &full[s], lane, 0);
+    }
+  } else if (warp == 1) {
+    mbar_wait(&wbar, 0);
+    const uint32_t idesc = umma_idesc_bf16(128, NN, false, false);
+    const uint64_t bd0 = umma_desc(smem_u32(Ws), 16, 8 * RB, LAYOUT);
+    int aoff[3];
+#pragma unroll
+    for (int w = 0; w < 3; ++w) aoff[w] = ((a.off[w] - mn) * RB) >> 4;
+    int it = 0;
+    uint32_t cb = 0;   // blocks issued before this band
+    for (int64_t bi = blockIdx.x; bi < a.nbands; bi += gridDim.x, ++it) {
+      const int s = it % stages;
+      const Band b = band_of(a, bi);
+      const int nblk = (b.R + 127) >> 7;
+      mbar_wait(&full[s], (it / stages) & 1);
+      const uint32_t base = smem_u32(slabs + (size_t)s * slab_bytes) + slab_phase(b.row0 + mn, RB);
+      const uint64_t ad0 = umma_desc(base, 16, 8 * RB, LAYOUT);
+      for (int mt = 0; mt < nblk; ++mt) {
+        const uint32_t idx = cb + mt, slot = idx % NSLOT;
+        mbar_wait(&tempty[slot], ((idx / NSLOT) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int w = 0; w < 3; ++w)
+#pragma unroll
+          for (int ks = 0; ks < RB / 32; ++ks)
+            tc_mma_bf16_w(tmem + slot * NN, ad0 + (uint64_t)(aoff[w] + ((mt * 128 * RB) >> 4) + ks * 2),
+                          bd0 + (uint64_t)((w * NN * RB + ks * 32) >> 4), idesc, (w | ks) != 0);
+        tc_commit_w(&tfull[slot]);
+      }
+      tc_commit_w(&empty[s]);
+      cb += nblk;
+    }
+  } else {
+    const int q = warp & 3;                      // TMEM lanes [32q, 32q + 32)
+    const int part = (warp - 2) >> 2;            // blocks mt with mt % EP == part
+    const int et = threadIdx.x - 64;
+    const float m_up = lane == 0 ? 0.f : 1.f, m_dn = lane == 31 ? 0.f : 1.f;
+    const uint4 ninf = make_uint4(BF16X2_NEG_INF, BF16X2_NEG_INF, BF16X2_NEG_INF, BF16X2_NEG_INF);
+    float bias[NO];
+#pragma unroll
+    for (int c = 0; c < NO; ++c) bias[c] = __ldg(a.bias + c);
+    auto is_border = [&](const Band& b, int r) {
+      uint32_t fl, rem, Y, X;
+      a.fP.divmod((uint32_t)(r + b.base), fl, rem);
+      a.fWp.divmod(rem, Y, X);
+      return Y == 0 || (int)Y == a.gi.H + 1 || X == 0 || (int)X == a.gi.W + 1;
+    };
+    // conv row r of the band, chunk j -> band buffer (bf16, -inf at frame borders), debug
+    // copy; bias b8 = the chunk's 8 biases
+    auto put = [&](const Band& b, int r, int j, bool border, const float* v, const float* b8) {
+      float o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = fmaf(v[k], a.in_scale, b8[k]);
+      const uint4 u = pack8(o);
+      *reinterpret_cast<uint4*>(bandbuf + (size_t)r * RBO + (swz_chunk(r, RBO, j) << 4)) = border ? ninf : u;
+      if (a.conv_dbg) {
+        const int64_t g = b.row0 + r;
+        *reinterpret_cast<uint4*>(a.conv_dbg + g * RBO + (swz_chunk(g, RBO, j) << 4)) = u;
+      }
+    };
+    uint32_t cb = 0;
+    for (int64_t bi = blockIdx.x; bi < a.nbands; bi += gridDim.x) {
+      const Band b = band_of(a, bi);
+      const int nblk = (b.R + 127) >> 7;
+      for (int mt = part; mt < nblk; mt += EP) {
+        const uint32_t idx = cb + mt, slot = idx % NSLOT;
+        const int grp = mt * 4 + q;
+        const int r = grp * 32 + lane;
+        const bool border = r < b.R ? is_border(b, r) : true;
+        mbar_wait(&tfull[slot], (idx / NSLOT) & 1);
+        tc_fence_after();
+        const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + slot * NN;
+        uint32_t p0[NO], p1[NO], p2[NO];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          tmem_ld8_nw(tb + j * 8, *reinterpret_cast<uint32_t(*)[8]>(&p0[8 * j]));
+          tmem_ld8_nw(tb + NO + j * 8, *reinterpret_cast<uint32_t(*)[8]>(&p1[8 * j]));
+          tmem_ld8_nw(tb + 2 * NO + j * 8, *reinterpret_cast<uint32_t(*)[8]>(&p2[8 * j]));
+        }
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[slot]);   // the slot's columns are in registers
+        float v[NO];
+#pragma unroll
+        for (int k = 0; k < NO; ++k) {
+          const float up = __shfl_up_sync(0xffffffffu, __uint_as_float(p0[k]), 1);     // D_0[r-1]
+          const float dn = __shfl_down_sync(0xffffffffu, __uint_as_float(p2[k]), 1);   // D_2[r+1]
+          v[k] = fmaf(dn, m_dn, fmaf(up, m_up, __uint_as_float(p1[k])));
+        }
+        if (lane == 0 || lane == 31) {
+          float4* xg = reinterpret_cast<float4*>(xch + grp * XG);
+          const uint32_t* pp = lane == 0 ? p2 : p0;
+          const int dp = (lane == 0 ? 2 : 3) * NO / 4, dn = (lane == 0 ? 1 : 0) * NO / 4;
+#pragma unroll
+          for (int k = 0; k < NO / 4; ++k) {
+            xg[dp + k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            xg[dn + k] = make_float4(__uint_as_float(pp[4 * k]), __uint_as_float(pp[4 * k + 1]),
+                                     __uint_as_float(pp[4 * k + 2]), __uint_as_float(pp[4 * k + 3]));
+          }
+        } else if (r < b.R) {
+#pragma unroll
+          for (int j = 0; j < NC; ++j) put(b, r, j, border, v + 8 * j, bias + 8 * j);
+        }
+      }
+      cb += nblk;
+      asm volatile("bar.sync 1, %0;" ::"n"(CP_EPI) : "memory");   // interior rows + exchange written
+      // quarter-edge rows: lane-0 row of group g adds D_0 of group g-1's lane 31,
+      // lane-31 row adds D_2 of group g+1's lane 0
+      const int ng = nblk * 4;
+      for (int i = et; i < ng * 2 * NC; i += CP_EPI) {
+        const int g = i / (2 * NC), side = (i / NC) & 1, j = i % NC;
+        const int r = g * 32 + (side ? 31 : 0);
+        if (r >= b.R) continue;
+        const float* pv = xch + g * XG + (2 + side) * NO + j * 8;
+        const float* nb = side ? (g + 1 < ng ? xch + (g + 1) * XG + NO + j * 8 : nullptr)
+                               : (g > 0 ? xch + (g - 1) * XG + j * 8 : nullptr);
+        float v[8], b8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[k] = nb ? pv[k] + nb[k] : pv[k];
+          b8[k] = __ldg(a.bias + j * 8 + k);
+        }
+        put(b, r, j, is_border(b, r), v, b8);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(CP_EPI) : "memory");   // band buffer complete
+      pool_band<NO>(a, b, bandbuf, et);
+      asm volatile("bar.sync 1, %0;" ::"n"(CP_EPI) : "memory");   // band buffer / exchange free
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// KX: the column-tap-stacked kernel (NW = 9 only): 3 windows, N = 3*out per block
+template <int N, int RB, int NW, bool KX = false, int EW = CP_EW>
 seed_status launch_conv_pool(CpArgs a, cudaStream_t st) {
+  static_assert(!KX || NW == 9, "KX");
   constexpr int WB = NW * N * RB;
-  const int cap = (256 / N) * 128;   // rows per accumulator
+  const int cap = (256 / N) * 128;   // rows per band (9-window: per TMEM accumulator)
   const PadGeo& gi = a.gi;
   int Rmax;
   if (gi.P <= cap) {
@@ -273,21 +483,47 @@ seed_status launch_conv_pool(CpArgs a, cudaStream_t st) {
   a.fP = FastDiv((uint32_t)gi.P); a.fWp = FastDiv((uint32_t)gi.Wp);
   a.fRow = FastDiv((uint32_t)(a.go.Wp * (N / 8)));
   a.fFrame = FastDiv((uint32_t)((a.go.H + 2) * a.go.Wp * (N / 8)));
+  if (KX)
+    for (int k = 0; k < 3; ++k) a.off[k] = (k - 1) * gi.Wp;
+  const int nw = KX ? 3 : NW;
   int mn = a.off[0], mx = a.off[0];
-  for (int w = 1; w < NW; ++w) { mn = std::min(mn, a.off[w]); mx = std::max(mx, a.off[w]); }
+  for (int w = 1; w < nw; ++w) { mn = std::min(mn, a.off[w]); mx = std::max(mx, a.off[w]); }
   const int nblk_max = (Rmax + 127) / 128;
   const int slab = (int)align_up((size_t)(nblk_max * 128 + mx - mn) * RB + 1024, 1024);
   const int band = (int)align_up((size_t)Rmax * 2 * N, 1024);
+  const int xbytes = KX ? nblk_max * 4 * 4 * N * 4 : 0;   // edge-row exchange
   const int wbytes = (int)align_up(WB, 1024);
-  const int stages = std::min(WC_MAX_STAGES, (CP_SMEM - 1024 - wbytes - band) / slab);
+  const int stages = std::min(WC_MAX_STAGES, (CP_SMEM - 1024 - wbytes - band - xbytes) / slab);
   if (stages < 2) return SEED_E_UNSUPPORTED;
   if (a.nbands == 0) return SEED_OK;
-  const size_t smem = (size_t)wbytes + (size_t)stages * slab + band + 1024;
-  static PerDevice attr;
-  SEED_TRY(smem_optin(attr, conv_pool_kernel<N, RB, NW>, CP_SMEM));
+  const size_t smem = (size_t)wbytes + (size_t)stages * slab + band + xbytes + 1024;
   const int grid = (int)std::min<int64_t>(a.nbands, sm_count());
-  return launch_k(conv_pool_kernel<N, RB, NW>, dim3(grid), dim3(CP_THREADS), smem, st, a, stages, slab,
-                  band);
+  static PerDevice attr;
+  if constexpr (KX) {
+    SEED_TRY(smem_optin(attr, conv_pool_kx_kernel<N, RB>, CP_SMEM));
+    return launch_k(conv_pool_kx_kernel<N, RB>, dim3(grid), dim3(CP_THREADS), smem, st, a, stages, slab,
+                    band);
+  } else {
+    SEED_TRY(smem_optin(attr, conv_pool_kernel<N, RB, NW, EW>, CP_SMEM));
+    return launch_k(conv_pool_kernel<N, RB, NW, EW>, dim3(grid), dim3(64 + 32 * EW), smem, st, a, stages,
+                    slab, band);
+  }
+}
+
+// Which 9-window section convs take the column-tap-stacked kernel (A/B
+// measurement; profiles/r02/conv_pool_kx.md): SEED_CP_KX=0 none (default), 1 the
+// 16 -> 16-channel section-0 conv of the GRF net, 2 every 9-window shape.  Measured
+// at c4 s0: 775 us vs 593 us for the 9-window kernel — the tensor side is 3x
+// cheaper but the combine (three TMEM loads and two shuffles per output value)
+// doubles the epilogue's instructions, and the epilogue, not the MMAs, bounds
+// the kernel.  SEED_CP_EW selects 16 / 20 epilogue warps for the 9-window s0
+// kernel (measured slower: 617 / 625 us).
+static int cp_kx() {
+  static const int v = [] {
+    const char* e = getenv("SEED_CP_KX");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 }  // namespace
@@ -308,9 +544,21 @@ seed_status conv3w_conv_pool(const Conv3wFwd& f, const PadGeo& go, int pt, int p
     if (f.ch == 32 && f.cin_p == 16) return launch_conv_pool<32, 32, 3>(a, st);
     return SEED_E_UNSUPPORTED;
   }
-  if (f.ch == 16 && f.cin_p == 16) return launch_conv_pool<16, 32, 9>(a, st);
-  if (f.ch == 32 && f.cin_p == 16) return launch_conv_pool<32, 32, 9>(a, st);
-  if (f.ch == 32 && f.cin_p == 32) return launch_conv_pool<32, 64, 9>(a, st);
+  const int kx = cp_kx();
+  static const int ew = [] {
+    const char* e = getenv("SEED_CP_EW");
+    return e ? atoi(e) : 12;
+  }();
+  if (f.ch == 16 && f.cin_p == 16) {
+    if (kx >= 1) return launch_conv_pool<16, 32, 9, true>(a, st);
+    if (ew == 16) return launch_conv_pool<16, 32, 9, false, 16>(a, st);
+    if (ew == 20) return launch_conv_pool<16, 32, 9, false, 20>(a, st);
+    return launch_conv_pool<16, 32, 9>(a, st);
+  }
+  if (f.ch == 32 && f.cin_p == 16)
+    return kx >= 2 ? launch_conv_pool<32, 32, 9, true>(a, st) : launch_conv_pool<32, 32, 9>(a, st);
+  if (f.ch == 32 && f.cin_p == 32)
+    return kx >= 2 ? launch_conv_pool<32, 64, 9, true>(a, st) : launch_conv_pool<32, 64, 9>(a, st);
   return SEED_E_UNSUPPORTED;
 }
 
