@@ -14,7 +14,7 @@
 //   frame bands: G whole frames when a padded frame fits (small sections).
 // Warp 0 TMA-loads the band's input slab (win_engine.cuh load_slab), warp 1
 // issues the window MMAs into one of two TMEM accumulators (so the next band's
-// MMAs overlap this band's epilogue), warps 2-9 drain the accumulator (x scale +
+// MMAs overlap this band's epilogue), warps 2-13 drain the accumulator (x scale +
 // bias, bf16: the conv epilogue of W3FwdEpi<W3_PLAIN>) into a shared-memory band
 // buffer, then pool from it (pool_max9: the same first-maximum / -inf rules as
 // conv3w_pool_fwd_kernel) and write h0, hr0 = relu(h0), the argmax bytes and the
@@ -47,6 +47,7 @@ struct CpArgs {
   int k, nbpf;              // row bands: pool rows per band, bands per frame
   int64_t nbands;
   FastDiv fP, fWp, fRow, fFrame;   // gi.P, gi.Wp, pool items per output row / per frame
+  int bb_rs, bb_h1;         // band buffer: bytes per image row, offset of the odd-column half
   float in_scale;
   const float* bias;
   uint8_t* h0;
@@ -60,6 +61,7 @@ struct Band {
   int nf, oy0, oy1;   // frames, pool rows [oy0, oy1) of each frame
   int R;              // conv rows of the band (from row0)
   int base;           // row0 - f0 * gi.P
+  int ybase;          // first padded image row of the band (row bands), 0 (frame bands)
 };
 
 __device__ __forceinline__ Band band_of(const CpArgs& a, int64_t bi) {
@@ -69,6 +71,7 @@ __device__ __forceinline__ Band band_of(const CpArgs& a, int64_t bi) {
     b.nf = (int)min((int64_t)a.G, a.F - b.f0);
     b.oy0 = 0; b.oy1 = a.go.H;
     b.base = 0;
+    b.ybase = 0;
     b.R = b.nf * a.gi.P;
   } else {
     b.f0 = bi / a.nbpf;
@@ -79,10 +82,23 @@ __device__ __forceinline__ Band band_of(const CpArgs& a, int64_t bi) {
     // padded rows Y of the taps (pt, pb <= 1: within [0, H + 1])
     const int Ya = 2 * b.oy0 - a.pt + 1, Yb = 2 * (b.oy1 - 1) - a.pt + 3;
     b.base = Ya * a.gi.Wp;
+    b.ybase = Ya;
     b.R = (Yb - Ya + 1) * a.gi.Wp;
   }
   b.row0 = b.f0 * a.gi.P + b.base;
   return b;
+}
+
+// Band buffer layout: per padded image row of the band, the even columns then the
+// odd ones (pixel X at (X & 1) * bb_h1 + (X >> 1) * 2N), rows bb_rs bytes apart.
+// The pool's taps of consecutive output columns are consecutive pixels of one half
+// (stride 2 in X), so a warp's 16-byte tap loads cover a contiguous range (no bank
+// conflicts; with whole rows of 32 / 64 bytes the stride-2 taps hit 4 of the 8
+// 16-byte bank groups); bb_h1 = 16 mod 32 puts the drain's even / odd-column stores
+// of one chunk on disjoint bank groups.
+template <int N>
+__device__ __forceinline__ uint32_t bb_off(const CpArgs& a, const Band& b, uint32_t fl, int Y, int X) {
+  return (uint32_t)(((int)fl * (a.gi.H + 2) + Y - b.ybase) * a.bb_rs + (X & 1) * a.bb_h1 + (X >> 1) * (2 * N));
 }
 
 // The max-pool of one band from the shared-memory band buffer (epilogue thread et
@@ -109,13 +125,16 @@ __device__ __forceinline__ void pool_band(const CpArgs& a, const Band& b, const 
       continue;
     }
     // tap (ky, kx) of output (Y-1, X-1): conv pixel (2(Y-1) - pt + ky, 2(X-1) - pl + kx),
-    // band row fl*P + (y+1)*Wp + (x+1) - base
-    const int r0 = (int)fl * a.gi.P + (2 * Y - 1 - a.pt) * a.gi.Wp + 2 * X - 1 - a.pl - b.base;
+    // padded (2Y - 1 - pt + ky, 2X - 1 - pl + kx)
+    const int Xc = 2 * X - 1 - a.pl;
+    const uint8_t* t0 = bandbuf + bb_off<N>(a, b, fl, 2 * Y - 1 - a.pt, Xc) + 16 * j;
+    const uint8_t* t1 = bandbuf + bb_off<N>(a, b, fl, 2 * Y - 1 - a.pt, Xc + 1) + 16 * j;
     uint4 in[9];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) {
-      const int r = r0 + (t / 3) * a.gi.Wp + t % 3;
-      in[t] = *reinterpret_cast<const uint4*>(bandbuf + (size_t)r * RBO + (swz_chunk(r, RBO, j) << 4));
+    for (int ky = 0; ky < 3; ++ky) {
+      in[3 * ky] = *reinterpret_cast<const uint4*>(t0 + ky * a.bb_rs);
+      in[3 * ky + 1] = *reinterpret_cast<const uint4*>(t1 + ky * a.bb_rs);
+      in[3 * ky + 2] = *reinterpret_cast<const uint4*>(t0 + ky * a.bb_rs + 2 * N);
     }
     uint4 best, rl;
     uint2 am;
@@ -227,11 +246,11 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           float v[N];
 #pragma unroll
           for (int c = 0; c < N; ++c) v[c] = __uint_as_float(vr[c]) * a.in_scale + bias[c];
-          uint8_t* row = bandbuf + (size_t)r * RBO;
+          uint8_t* row = bandbuf + bb_off<N>(a, b, fl, (int)Y, (int)X);
 #pragma unroll
           for (int j = 0; j < NC; ++j) {
             const uint4 u = pack8(v + 8 * j);
-            *reinterpret_cast<uint4*>(row + (swz_chunk(r, RBO, j) << 4)) = border ? ninf : u;
+            *reinterpret_cast<uint4*>(row + 16 * j) = border ? ninf : u;
             if (a.conv_dbg) {
               const int64_t g = b.row0 + r;
               *reinterpret_cast<uint4*>(a.conv_dbg + g * RBO + (swz_chunk(g, RBO, j) << 4)) = u;
@@ -359,20 +378,22 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
     float bias[NO];
 #pragma unroll
     for (int c = 0; c < NO; ++c) bias[c] = __ldg(a.bias + c);
-    auto is_border = [&](const Band& b, int r) {
+    // band-buffer offset of band row r; border flag
+    auto locate = [&](const Band& b, int r, bool& border) {
       uint32_t fl, rem, Y, X;
       a.fP.divmod((uint32_t)(r + b.base), fl, rem);
       a.fWp.divmod(rem, Y, X);
-      return Y == 0 || (int)Y == a.gi.H + 1 || X == 0 || (int)X == a.gi.W + 1;
+      border = Y == 0 || (int)Y == a.gi.H + 1 || X == 0 || (int)X == a.gi.W + 1;
+      return bb_off<NO>(a, b, fl, (int)Y, (int)X);
     };
     // conv row r of the band, chunk j -> band buffer (bf16, -inf at frame borders), debug
     // copy; bias b8 = the chunk's 8 biases
-    auto put = [&](const Band& b, int r, int j, bool border, const float* v, const float* b8) {
+    auto put = [&](const Band& b, int r, uint32_t off, int j, bool border, const float* v, const float* b8) {
       float o[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) o[k] = fmaf(v[k], a.in_scale, b8[k]);
       const uint4 u = pack8(o);
-      *reinterpret_cast<uint4*>(bandbuf + (size_t)r * RBO + (swz_chunk(r, RBO, j) << 4)) = border ? ninf : u;
+      *reinterpret_cast<uint4*>(bandbuf + off + 16 * j) = border ? ninf : u;
       if (a.conv_dbg) {
         const int64_t g = b.row0 + r;
         *reinterpret_cast<uint4*>(a.conv_dbg + g * RBO + (swz_chunk(g, RBO, j) << 4)) = u;
@@ -386,7 +407,8 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
         const uint32_t idx = cb + mt, slot = idx % NSLOT;
         const int grp = mt * 4 + q;
         const int r = grp * 32 + lane;
-        const bool border = r < b.R ? is_border(b, r) : true;
+        bool border = true;
+        const uint32_t off = r < b.R ? locate(b, r, border) : 0u;
         mbar_wait(&tfull[slot], (idx / NSLOT) & 1);
         tc_fence_after();
         const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + slot * NN;
@@ -420,7 +442,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
           }
         } else if (r < b.R) {
 #pragma unroll
-          for (int j = 0; j < NC; ++j) put(b, r, j, border, v + 8 * j, bias + 8 * j);
+          for (int j = 0; j < NC; ++j) put(b, r, off, j, border, v + 8 * j, bias + 8 * j);
         }
       }
       cb += nblk;
@@ -441,7 +463,9 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
           v[k] = nb ? pv[k] + nb[k] : pv[k];
           b8[k] = __ldg(a.bias + j * 8 + k);
         }
-        put(b, r, j, is_border(b, r), v, b8);
+        bool border;
+        const uint32_t off = locate(b, r, border);
+        put(b, r, off, j, border, v, b8);
       }
       asm volatile("bar.sync 1, %0;" ::"n"(CP_EPI) : "memory");   // band buffer complete
       pool_band<NO>(a, b, bandbuf, et);
@@ -490,7 +514,10 @@ seed_status launch_conv_pool(CpArgs a, cudaStream_t st) {
   for (int w = 1; w < nw; ++w) { mn = std::min(mn, a.off[w]); mx = std::max(mx, a.off[w]); }
   const int nblk_max = (Rmax + 127) / 128;
   const int slab = (int)align_up((size_t)(nblk_max * 128 + mx - mn) * RB + 1024, 1024);
-  const int band = (int)align_up((size_t)Rmax * 2 * N, 1024);
+  const int hw = (gi.Wp + 1) / 2;
+  a.bb_h1 = hw * 2 * N + 16;
+  a.bb_rs = 2 * hw * 2 * N + 32;
+  const int band = (int)align_up((size_t)(Rmax / gi.Wp) * a.bb_rs, 1024);
   const int xbytes = KX ? nblk_max * 4 * 4 * N * 4 : 0;   // edge-row exchange
   const int wbytes = (int)align_up(WB, 1024);
   const int stages = std::min(WC_MAX_STAGES, (CP_SMEM - 1024 - wbytes - band - xbytes) / slab);
