@@ -623,88 +623,111 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
 }
 
 // Backward: thread = (frame, 2x2 block of input pixels (y + pt, x + pl) in
-// {2a, 2a+1} x {2b, 2b+1}, chunk j).  The block's pixels receive gradient only from
+// {2a, 2a+1} x {2b, 2b+1}).  The block's pixels receive gradient only from
 // the 2x2 windows (a-1 | a) x (b-1 | b): an even offset is tap 2 of window a-1 and
 // tap 0 of window a, an odd offset tap 1 of window a.  The four windows' (argmax,
 // dout) are loaded once for the four pixels; sums in ascending window order.
-// chunk i of the border rows of a padded row space (per frame: top / bottom rows,
-// and the left / right pixels of the interior rows) <- 0
-__device__ __forceinline__ void zero_border_chunk(int64_t i, int NC, int RB, const PadGeo& g, uint8_t* buf) {
-  const int j = (int)(i % NC);
-  const int64_t r = i / NC;
-  const int per = 2 * g.Wp + 2 * g.H;
-  const int64_t f = r / per;
-  const int k = (int)(r - f * per);
-  int Y, X;
-  if (k < 2 * g.Wp) { Y = k < g.Wp ? 0 : g.H + 1; X = k % g.Wp; }
-  else { Y = 1 + (k - 2 * g.Wp) / 2; X = ((k - 2 * g.Wp) & 1) ? g.W + 1 : 0; }
-  *chunk_at(buf, f * g.P + (int64_t)Y * g.Wp + X, RB, j) = make_uint4(0, 0, 0, 0);
+// 16-byte chunk j of padded row `row` (32-bit row index, 64-bit byte address)
+__device__ __forceinline__ uint4* chunk_at32(uint8_t* base, uint32_t row, int RB, int j) {
+  return reinterpret_cast<uint4*>(base + (size_t)row * RB + (swz_chunk(row, RB, j) << 4));
+}
+__device__ __forceinline__ const uint4* chunk_at32(const uint8_t* base, uint32_t row, int RB, int j) {
+  return reinterpret_cast<const uint4*>(base + (size_t)row * RB + (swz_chunk(row, RB, j) << 4));
 }
 
+// One thread per (2x2 block, 16-byte chunk j): a warp's loads / stores of one
+// pixel cover whole 32-byte sectors (one thread per block and all chunks was 1.3-2.6x
+// slower).  32-bit index arithmetic (with 64-bit indices the kernel was ALU-bound,
+// 85 % of the ALU pipe, c4 s0 309 us).  Threads past `total` zero one border chunk
+// each of din (per frame: top / bottom rows, then the left / right pixels of the
+// interior rows).
 template <int NC>
 __global__ void __launch_bounds__(256) conv3w_pool_bwd_kernel(
-    PadGeo gi, PadGeo go, int pt, int pl, int64_t total, int64_t nz, FastDiv frow, FastDiv fnby,
-    const uint8_t* __restrict__ dout, const uint8_t* __restrict__ arg, uint8_t* __restrict__ din) {
+    PadGeo gi, PadGeo go, int pt, int pl, int total, int nz, FastDiv fnbx, FastDiv fnby, FastDiv fper,
+    FastDiv fwp, const uint8_t* __restrict__ dout, const uint8_t* __restrict__ arg, uint8_t* __restrict__ din) {
   pdl_wait();
   constexpr int C = NC * 8, RB = NC * 16;
-  // flat thread index -> (frame f, block row a, block column b, chunk j): full 256-thread
-  // blocks instead of one 2-row strip per block (measured: 4.0 TB/s at c4 s0 with
-  // strip blocks of 98 active threads); threads past `total` zero the border rows
-  // of din (formerly a separate launch)
-  const int64_t tt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int tt = blockIdx.x * blockDim.x + threadIdx.x;
   if (tt >= total) {
-    if (tt < total + nz) zero_border_chunk(tt - total, NC, RB, gi, din);
+    if (tt >= total + nz) return;
+    const uint32_t zi = (uint32_t)(tt - total);
+    const int j = (int)(zi % NC);
+    uint32_t f, k, Y, X;
+    fper.divmod(zi / NC, f, k);
+    if (k < 2u * gi.Wp) {
+      uint32_t hi;
+      fwp.divmod(k, hi, X);
+      Y = hi ? gi.H + 1 : 0;
+    } else {
+      const uint32_t e = k - 2u * gi.Wp;
+      Y = 1 + (e >> 1);
+      X = (e & 1) ? gi.W + 1 : 0;
+    }
+    *chunk_at32(din, f * gi.P + Y * gi.Wp + X, RB, j) = make_uint4(0, 0, 0, 0);
     return;
   }
-  uint32_t fa, rem, f32, a32;
-  frow.divmod((uint32_t)tt, fa, rem);
-  fnby.divmod(fa, f32, a32);
-  const int b = (int)rem / NC, j = (int)rem % NC;
-  const int f = (int)f32, a = (int)a32;
-  const int64_t fo = (int64_t)f * go.P, fi = (int64_t)f * gi.P;
-  uint2 av[4];
-  uint4 dv[4];
+  uint32_t fa, rem, f, a;
+  fnbx.divmod((uint32_t)tt, fa, rem);   // fnbx: blocks per row x NC
+  fnby.divmod(fa, f, a);
+  const uint32_t b = rem / NC;
+  const int j = (int)(rem % NC);
+  const uint32_t fo = f * go.P, fi = f * gi.P;
+  uint32_t orow[4];
+  bool ok[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {   // windows (a-1, b-1), (a-1, b), (a, b-1), (a, b)
-    const int oy = a - 1 + (q >> 1), ox = b - 1 + (q & 1);
-    const bool ok = oy >= 0 && oy < go.H && ox >= 0 && ox < go.W;
-    const int64_t o = fo + (int64_t)(oy + 1) * go.Wp + (ox + 1);
-    av[q] = ok ? __ldg(reinterpret_cast<const uint2*>(arg + o * C + 8 * j)) : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
-    dv[q] = ok ? __ldg(chunk_at(dout, o, RB, j)) : make_uint4(0, 0, 0, 0);
+    const int oy = (int)a - 1 + (q >> 1), ox = (int)b - 1 + (q & 1);
+    ok[q] = oy >= 0 && oy < go.H && ox >= 0 && ox < go.W;
+    orow[q] = fo + (uint32_t)(oy + 1) * go.Wp + (uint32_t)(ox + 1);
   }
+  uint32_t irow[4];
+  bool in[4];
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    const int dy = p >> 1, dx = p & 1;
-    const int y = 2 * a + dy - pt, x = 2 * b + dx - pl;
-    if (y < 0 || y >= gi.H || x < 0 || x >= gi.W) continue;
-    float s[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) s[k] = 0.f;
+    const int y = 2 * (int)a + (p >> 1) - pt, x = 2 * (int)b + (p & 1) - pl;
+    in[p] = y >= 0 && y < gi.H && x >= 0 && x < gi.W;
+    irow[p] = fi + (uint32_t)(y + 1) * gi.Wp + (uint32_t)(x + 1);
+  }
+  {
+    uint2 av[4];
+    uint4 dv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int wy = q >> 1, wx = q & 1;   // window a-1+wy, b-1+wx
-      // tap of this pixel in that window: even offset -> 2 (wy = 0) / 0 (wy = 1); odd -> 1 (wy = 1 only)
-      const int ky = dy == 0 ? (wy == 0 ? 2 : 0) : (wy == 1 ? 1 : -1);
-      const int kx = dx == 0 ? (wx == 0 ? 2 : 0) : (wx == 1 ? 1 : -1);
-      if (ky < 0 || kx < 0) continue;
-      const uint32_t w4 = (uint32_t)(ky * 3 + kx) * 0x01010101u;
-      const uint32_t mx = __vcmpeq4(av[q].x, w4), my = __vcmpeq4(av[q].y, w4);
-      const uint32_t mk[4] = {__byte_perm(mx, 0, 0x1100), __byte_perm(mx, 0, 0x3322),
-                              __byte_perm(my, 0, 0x1100), __byte_perm(my, 0, 0x3322)};
-      const uint32_t dw[4] = {dv[q].x, dv[q].y, dv[q].z, dv[q].w};
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t d = dw[r] & mk[r];
-        s[2 * r] += bf16_lo(d);
-        s[2 * r + 1] += bf16_hi(d);
-      }
+      av[q] = ok[q] ? __ldg(reinterpret_cast<const uint2*>(arg + (size_t)orow[q] * C + 8 * j))
+                    : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+      dv[q] = ok[q] ? __ldg(chunk_at32(dout, orow[q], RB, j)) : make_uint4(0, 0, 0, 0);
     }
-    *chunk_at(din, fi + (int64_t)(y + 1) * gi.Wp + (x + 1), RB, j) = pack8(s);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int dy = p >> 1, dx = p & 1;
+      if (!in[p]) continue;
+      float s[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s[k] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int wy = q >> 1, wx = q & 1;   // window a-1+wy, b-1+wx
+        // tap of this pixel in that window: even offset -> 2 (wy = 0) / 0 (wy = 1); odd -> 1 (wy = 1 only)
+        const int ky = dy == 0 ? (wy == 0 ? 2 : 0) : (wy == 1 ? 1 : -1);
+        const int kx = dx == 0 ? (wx == 0 ? 2 : 0) : (wx == 1 ? 1 : -1);
+        if (ky < 0 || kx < 0) continue;
+        const uint32_t w4 = (uint32_t)(ky * 3 + kx) * 0x01010101u;
+        const uint32_t mx = __vcmpeq4(av[q].x, w4), my = __vcmpeq4(av[q].y, w4);
+        const uint32_t mk[4] = {__byte_perm(mx, 0, 0x1100), __byte_perm(mx, 0, 0x3322),
+                                __byte_perm(my, 0, 0x1100), __byte_perm(my, 0, 0x3322)};
+        const uint32_t dw[4] = {dv[q].x, dv[q].y, dv[q].z, dv[q].w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t d = dw[r] & mk[r];
+          s[2 * r] += bf16_lo(d);
+          s[2 * r + 1] += bf16_hi(d);
+        }
+      }
+      *chunk_at32(din, irow[p], RB, j) = pack8(s);
+    }
   }
 }
 
-// zero the border rows of a padded row space (per frame: top / bottom rows, and
-// the left / right pixels of the interior rows)
 
 seed_status conv3w_pool_fwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C, int pt, int pl,
                             const uint8_t* conv, uint8_t* h0, uint8_t* hr0, uint8_t* arg,
@@ -728,19 +751,22 @@ seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
   const int NC = C / 8;
   const int nby = (gi.H + pt + 1) >> 1, nbx = (gi.W + pl + 1) >> 1;
   const int64_t total = F * nby * nbx * NC;
-  const int64_t nz = F * (2 * gi.Wp + 2 * gi.H) * NC;
-  if (total + nz >= (1ll << 31)) return SEED_E_SHAPE;
-  const FastDiv frow((uint32_t)(nbx * NC)), fnby((uint32_t)nby);
+  const int per = 2 * gi.Wp + 2 * gi.H;
+  const int64_t nz = F * per * NC;
+  // 32-bit thread and row indices
+  if (total + nz >= (1ll << 31) || F * gi.P >= (1ll << 32) || F * go.P >= (1ll << 32)) return SEED_E_SHAPE;
+  const FastDiv fnbx((uint32_t)(nbx * NC)), fnby((uint32_t)nby), fper((uint32_t)per), fwp((uint32_t)gi.Wp);
   const dim3 grid((unsigned)((total + nz + 255) / 256));
+  const int t32 = (int)total, z32 = (int)nz;
   if (NC == 2)
-    return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(256), 0, st, gi, go, pt, pl, total, nz, frow, fnby,
-                    dout, arg, din);
+    return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(256), 0, st, gi, go, pt, pl, t32, z32, fnbx, fnby,
+                    fper, fwp, dout, arg, din);
   if (NC == 4)
-    return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(256), 0, st, gi, go, pt, pl, total, nz, frow, fnby,
-                    dout, arg, din);
+    return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(256), 0, st, gi, go, pt, pl, t32, z32, fnbx, fnby,
+                    fper, fwp, dout, arg, din);
   if (NC == 8)
-    return launch_k(conv3w_pool_bwd_kernel<8>, grid, dim3(256), 0, st, gi, go, pt, pl, total, nz, frow, fnby,
-                    dout, arg, din);
+    return launch_k(conv3w_pool_bwd_kernel<8>, grid, dim3(256), 0, st, gi, go, pt, pl, t32, z32, fnbx, fnby,
+                    fper, fwp, dout, arg, din);
   return SEED_E_UNSUPPORTED;
 }
 
