@@ -95,6 +95,20 @@ static inline int sm_count() {
 // programmatic edge).  Because every kernel waits, completion is transitive.
 // SEED_PDL=0 in the environment launches without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// pdl_wait() + an explicit trigger once every CTA has passed its wait: the next
+// kernel is launched while this one runs (its pre-wait prologue overlaps), instead
+// of at this kernel's completion.  Safe for the next kernel's pre-wait reads of
+// data written two or more kernels earlier (this kernel's wait has seen them
+// complete); no kernel reads before its wait what the kernel just before it writes
+// (the pre-wait reads are parameter images, written by the previous step's Adam /
+// image refresh).  Used by the LSTM, heads / loss, GEMM, space-to-depth, clip /
+// Adam and inference kernels; measured c2 step 0.190 -> 0.184 ms, the deep steps
+// unchanged (in the window-conv kernels as well it cost c3 / c4 ~1 %:
+// profiles/r02/pdl_trigger.md).
+__device__ __forceinline__ void pdl_wait_trig() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 inline bool pdl_enabled() {
   static int on = -1;

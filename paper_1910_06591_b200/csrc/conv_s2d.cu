@@ -126,7 +126,7 @@ static Win3WgradArgs s2d_wgrad3_args(const uint8_t* src, int64_t rows, const uin
 // chunks 2r, 2r+1 of the row (a warp writes 8 whole rows, 1 KB contiguous)
 __global__ void s2d_obs_kernel(int64_t nrows, FastDiv P, FastDiv Wd, int H, int W,
                                const uint8_t* __restrict__ obs, uint8_t* __restrict__ S0) {
-  pdl_wait();
+  pdl_wait_trig();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t g = t >> 2;
   if (g >= nrows) return;

@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_wait();
+  pdl_wait_trig();
   GEMM_STAMP(1, threadIdx.x == 0)
   const uint32_t tmem = *tmem_slot;
 
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
 template <class Prob>
 __global__ void __launch_bounds__(256) splitk_finish(const Prob p, const float* __restrict__ part,
                                                      int splits) {
-  pdl_wait();
+  pdl_wait_trig();
   const size_t MN = (size_t)p.M * p.N;
   const size_t n4 = (MN + 3) / 4;
   const bool vec = (p.N & 3) == 0;

@@ -80,7 +80,7 @@ __global__ void infer_pre_kernel(int n, int A, int U, int Kxp, int num_actors,
                                  const int32_t* __restrict__ tla, float* __restrict__ hpre,
                                  float* __restrict__ cpre, int32_t* __restrict__ prev,
                                  __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ hb) {
-  pdl_wait();
+  pdl_wait_trig();
   const int E = Kxp - 256;
   const int per = U + E;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(ICH_THREADS) infer_cell_heads_kernel(
     uint64_t counter, float* __restrict__ th, float* __restrict__ tc, int32_t* __restrict__ tla,
     int32_t* __restrict__ action_out, float* __restrict__ blp_out, float* __restrict__ logits_out,
     int num_actors) {
-  pdl_wait();
+  pdl_wait_trig();
   constexpr int U = LSTM_U, NW = ICH_THREADS / 32;
   const int i = blockIdx.x, j = threadIdx.x, warp = j >> 5, lane = j & 31;
   const int A1 = A + 1;

@@ -965,7 +965,7 @@ namespace seed {
 __global__ void r2d2_rewards_kernel(int B, int T, float gamma, const float* __restrict__ reward,
                                     const uint8_t* __restrict__ done, float* __restrict__ r,
                                     float* __restrict__ disc) {
-  pdl_wait();
+  pdl_wait_trig();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B * T) return;
   const int b = i / T, t = i % T;
@@ -977,7 +977,7 @@ __global__ void r2d2_rewards_kernel(int B, int T, float gamma, const float* __re
 // dueling combine: Q[f][a] = V[f] + A[f][a] - mean_j A[f][j]  (warp per row)
 __global__ void dueling_q_kernel(int F, int A, const float* __restrict__ adv, const float* __restrict__ val,
                                  float* __restrict__ q) {
-  pdl_wait();
+  pdl_wait_trig();
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (f >= F) return;
   float s = 0.f;
@@ -991,7 +991,7 @@ __global__ void dueling_q_kernel(int F, int A, const float* __restrict__ adv, co
 // its backward: dV = sum_a dQ_a, dA_j = dQ_j - (1/A) sum_a dQ_a
 __global__ void dueling_bwd_kernel(int F, int A, const float* __restrict__ dq, float* __restrict__ dadv,
                                    float* __restrict__ dval) {
-  pdl_wait();
+  pdl_wait_trig();
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (f >= F) return;
   float s = 0.f;
@@ -1006,7 +1006,7 @@ __global__ void dueling_bwd_kernel(int F, int A, const float* __restrict__ dq, f
 __global__ void last_state_kernel(int B, int T1, int U, const float* __restrict__ H,
                                   const float* __restrict__ C, float* __restrict__ h0,
                                   float* __restrict__ c0) {
-  pdl_wait();
+  pdl_wait_trig();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B * U) return;
   const int b = i / U, u = i % U;
@@ -1017,7 +1017,7 @@ __global__ void last_state_kernel(int B, int T1, int U, const float* __restrict_
 
 // R2D2 loss partials in the clip + Adam kernel's [B][4] layout: {loss_b, 0, 0, nonfinite}
 __global__ void r2d2_loss_part_kernel(int B, const float* __restrict__ loss, float* __restrict__ part) {
-  pdl_wait();
+  pdl_wait_trig();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const float l = loss[b];

@@ -14,7 +14,7 @@ __global__ void __launch_bounds__(256) dense_fwd_f32(int R, int I, int O, const 
                                                      const float* __restrict__ b,
                                                      float* __restrict__ Y, int ldy,
                                                      float* __restrict__ Yv, int relu) {
-  pdl_wait();
+  pdl_wait_trig();
   extern __shared__ float shf[];
   float* Wt = shf;                  // [I][O]
   float* xs = shf + I * O;          // [8][I]
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) dense_dgrad_f32(int R, int I, int O, cons
                                                        const float* __restrict__ W,
                                                        const float* __restrict__ mask,
                                                        float* __restrict__ dX) {
-  pdl_wait();
+  pdl_wait_trig();
   extern __shared__ float shf[];
   float* Ws = shf;              // [O][I]
   float* ds = shf + O * I;      // [DG_ROWS][O]
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256) dense_wgrad_f32(int R, int I, int O, cons
                                                        int ldy, const float* __restrict__ dv,
                                                        const float* __restrict__ X,
                                                        float* __restrict__ gW, float* __restrict__ gb) {
-  pdl_wait();
+  pdl_wait_trig();
   const int o = blockIdx.x;
   const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int i = blockIdx.y * 32 + lane;
@@ -155,7 +155,7 @@ seed_status launch_dense_dgrad(int R, int I, int O, const float* dy, int ldy, co
 //     loss sums;
 //  3. all threads write the closed-form output gradients (H7).
 __global__ void __launch_bounds__(256) policy_loss_kernel(const LossArgs a) {
-  pdl_wait();
+  pdl_wait_trig();
   __shared__ float s_lse[256], s_tlp[256], s_H[256], s_pg[256];
   const int b = blockIdx.x;
   const int T = a.T, T1 = a.T + 1, A = a.A;
@@ -309,7 +309,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(HL_THREADS, MINB)
   }
   // everything above reads the batch and the heads weights (last written by the
   // previous step's Adam, >= 2 kernels back); H comes from the preceding kernel
-  pdl_wait();
+  pdl_wait_trig();
   cluster_sync_all();   // every CTA of the cluster runs before any DSMEM store
   // ---- phase 1: heads forward of this CTA's rows, one (row, output) dot product
   // per thread; results stored into all CL CTAs' sL (DSMEM all-gather)
@@ -512,7 +512,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(HL_THREADS, MINB)
 // g, g+8, ... in order, then the 8 group sums are added in order.
 __global__ void __launch_bounds__(256) heads_wgrad_finish(int NP, int A1, int I, const float* __restrict__ wpart,
                                                           float* __restrict__ g_w, float* __restrict__ g_b) {
-  pdl_wait();
+  pdl_wait_trig();
   const int n = A1 * (I + 1);
   const int q = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
   __shared__ float sh[8][33];
@@ -570,7 +570,7 @@ seed_status launch_policy_loss(const LossArgs& a, cudaStream_t st) {
 __global__ void core_extras_kernel(int F, int A, int Kxp, const int32_t* __restrict__ prev_action,
                                    const float* __restrict__ reward,
                                    const uint8_t* __restrict__ done, __nv_bfloat16* X) {
-  pdl_wait();
+  pdl_wait_trig();
   const int E = Kxp - 256;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)F * E) return;
@@ -597,7 +597,7 @@ __device__ __forceinline__ double block_sum_double(double v, double* sh8) {
 }
 
 __global__ void __launch_bounds__(256) grad_norm_kernel(const NormArgs a) {
-  pdl_wait();
+  pdl_wait_trig();
   // 4 float4 per thread, all loads issued first; squares and sums in double
   const int64_t P4 = a.P / 4;
   const float4* g4 = reinterpret_cast<const float4*>(a.g);
@@ -713,7 +713,7 @@ __device__ __forceinline__ AdamIn adam_load(const AdamArgs& a, int64_t gi) {
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a) {
-  pdl_wait();
+  pdl_wait_trig();
   __shared__ uint32_t bounds[8][2];   // source parameter range of each bf16 image
   if (threadIdx.x < a.nimg) {
     bounds[threadIdx.x][0] = (uint32_t)a.img[threadIdx.x].src;

@@ -141,7 +141,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   // which waited on their predecessors): start its load before the PDL wait so it
   // overlaps the preceding kernel's tail
   load_wh_slice(Ws, a.wh, r);   // in flight during the state loads below
-  pdl_wait();
+  pdl_wait_trig();
   for (int i = tid; i < BBT * T1; i += 256) {
     const int b = i / T1, t = i % T1;
     dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
@@ -352,7 +352,7 @@ __global__ void __cluster_dims__(LSTM_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     fence_mbar_init();
   }
   load_wh_slice(Ws, a.wh, r);   // before the PDL wait, as in the forward
-  pdl_wait();
+  pdl_wait_trig();
   for (int i = tid; i < BBT * T1; i += 256) {
     const int b = i / T1, t = i % T1;
     dn_s[i] = (b < BB) ? a.done[(size_t)(b0 + b) * T1 + t] : 0;
