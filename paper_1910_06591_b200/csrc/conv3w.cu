@@ -657,6 +657,14 @@ __global__ void __launch_bounds__(ROWK_THREADS) conv3w_pool_fwd_kernel(
 // the 2x2 windows (a-1 | a) x (b-1 | b): an even offset is tap 2 of window a-1 and
 // tap 0 of window a, an odd offset tap 1 of window a.  The four windows' (argmax,
 // dout) are loaded once for the four pixels; sums in ascending window order.
+// prmt.b32 with selector nibbles >= 8: the selected byte's top bit replicated over
+// the output byte (__byte_perm uses the low 3 bits of each nibble only)
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t x, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"(sel));
+  return r;
+}
+
 // 16-byte chunk j of padded row `row` (32-bit row index, 64-bit byte address)
 __device__ __forceinline__ uint4* chunk_at32(uint8_t* base, uint32_t row, int RB, int j) {
   return reinterpret_cast<uint4*>(base + (size_t)row * RB + (swz_chunk(row, RB, j) << 4));
@@ -741,14 +749,19 @@ __global__ void __launch_bounds__(256) conv3w_pool_bwd_kernel(
         const int ky = dy == 0 ? (wy == 0 ? 2 : 0) : (wy == 1 ? 1 : -1);
         const int kx = dx == 0 ? (wx == 0 ? 2 : 0) : (wx == 1 ? 1 : -1);
         if (ky < 0 || kx < 0) continue;
+        // argmax byte == tap: the argmax bytes are 0..8 or 0xFF (no window), so a byte
+        // of av ^ w4 is 0 (match), 1..15 or >= 0xF7; byte b of ((av ^ w4) | 0x80) - 1
+        // has its top bit clear exactly on a match (no borrow crosses bytes); the top
+        // bits are replicated into 16-bit lane masks (byte_perm sign mode)
         const uint32_t w4 = (uint32_t)(ky * 3 + kx) * 0x01010101u;
-        const uint32_t mx = __vcmpeq4(av[q].x, w4), my = __vcmpeq4(av[q].y, w4);
-        const uint32_t mk[4] = {__byte_perm(mx, 0, 0x1100), __byte_perm(mx, 0, 0x3322),
-                                __byte_perm(my, 0, 0x1100), __byte_perm(my, 0, 0x3322)};
+        const uint32_t nx = ((av[q].x ^ w4) | 0x80808080u) - 0x01010101u;
+        const uint32_t ny = ((av[q].y ^ w4) | 0x80808080u) - 0x01010101u;
+        const uint32_t nm[4] = {prmt_sign(nx, 0x9988), prmt_sign(nx, 0xBBAA), prmt_sign(ny, 0x9988),
+                                prmt_sign(ny, 0xBBAA)};
         const uint32_t dw[4] = {dv[q].x, dv[q].y, dv[q].z, dv[q].w};
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const uint32_t d = dw[r] & mk[r];
+          const uint32_t d = dw[r] & ~nm[r];
           s[2 * r] += bf16_lo(d);
           s[2 * r + 1] += bf16_hi(d);
         }
