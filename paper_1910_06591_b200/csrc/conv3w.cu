@@ -367,13 +367,34 @@ seed_status conv3w_dgrad(const Conv3wDgrad& a, cudaStream_t st) {
 // win_engine.cuh win3_wgrad_kernel: D[(kx, c)][(j, co)], tap ky = 2 - j.
 //   9-window input: dW[co][ky][kx][c] = sum_h X[h + kx][c] dY[h + 1 - Wp + j*Wp][co]
 //   x-im2col input: dW[co][ky][(kx, c)] = sum_h X[h][(kx, c)] dY[h - Wp + j*Wp][co] (atom 0)
+struct W3Fin3 {
+  int xim, Cp, CI, CO;
+  int ci_full, co_off, c_off;   // the [co_off..][3][3][c_off..] block of a [..][3][3][ci_full] tensor
+  float scale;
+  float* g_w;
+  float* g_b;
+  __device__ void weight3(int i, int n, float t) const {
+    const int atom = i / Cp, ch = i % Cp;
+    const int ky = 2 - n / CO, co = n % CO;
+    int kx, c;
+    if (xim) {
+      // channel 3*CI of the x-im2col input is constant 1 (conv3_obs_kernel): its
+      // row of the accumulator against tap ky = 1 (dY unshifted) is the bias gradient
+      if (atom == 0 && ch == 3 * CI && ky == 1) g_b[co] = t;
+      if (atom != 0 || ch >= 3 * CI) return;
+      kx = ch / CI; c = ch % CI;
+    } else {
+      if (atom >= 3 || ch >= CI) return;
+      kx = atom; c = ch;
+    }
+    g_w[(((size_t)(co_off + co) * 3 + ky) * 3 + kx) * ci_full + c_off + c] = t * scale;
+  }
+  __device__ void bias(int n, float t) const { g_b[n] = t; }
+};
 
 size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool) {
   return win3_wgrad_part_bytes(rows, ch, 3, ch == 64 ? 128 : 64);   // 64-ch inputs: 256 partial rows
 }
-
-static seed_status wgrad_launch(const Conv3wWgrad& a, const Win3WgradArgs& w, const W3Fin3& f, bool bias,
-                                Win3FinishInfo* info, cudaStream_t st);
 
 seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
   Win3WgradArgs w{};
@@ -387,75 +408,24 @@ seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
   f.ci_full = a.ci_full > 0 ? a.ci_full : a.cin; f.co_off = a.co_off; f.c_off = a.c_off;
   const bool bias = !a.xim && a.g_b;
   if (a.xim && !a.g_b) return SEED_E_ARG;   // x-im2col: the bias comes with the weights
-  if (a.defer && a.defer->n >= W3_FINISH_MAX) return SEED_E_ARG;
-  Win3FinishInfo fi{};
-  Win3FinishInfo* info = a.defer ? &fi : nullptr;
-  const seed_status r = wgrad_launch(a, w, f, bias, info, st);
-  if (r != SEED_OK || !a.defer) return r;
-  a.defer->e[a.defer->n++] = W3FinishEntry{a.part, fi.G, fi.tot, fi.NW, fi.PC, fi.prows, f};
-  return SEED_OK;
-}
-
-static seed_status wgrad_launch(const Conv3wWgrad& a, const Win3WgradArgs& w, const W3Fin3& f, bool bias,
-                                Win3FinishInfo* info, cudaStream_t st) {
   if (a.xf == XF_U8) {
     if (a.ch == 16 && a.cin_p == 16 && !a.xim && a.obs_u8)
-      return launch_win3_wgrad<16, 32, W3Fin3, 3, XF_U8>(w, f, true, st, info);
+      return launch_win3_wgrad<16, 32, W3Fin3, 3, XF_U8>(w, f, true, st);
     return SEED_E_UNSUPPORTED;
   }
   if (a.xf == XF_RELU) {
-    if (a.ch == 16 && a.cin_p == 16 && !a.xim) return launch_win3_wgrad<16, 32, W3Fin3, 3, XF_RELU>(w, f, true, st, info);
-    if (a.ch == 32 && a.cin_p == 32 && !a.xim) return launch_win3_wgrad<32, 64, W3Fin3, 3, XF_RELU>(w, f, true, st, info);
+    if (a.ch == 16 && a.cin_p == 16 && !a.xim) return launch_win3_wgrad<16, 32, W3Fin3, 3, XF_RELU>(w, f, true, st);
+    if (a.ch == 32 && a.cin_p == 32 && !a.xim) return launch_win3_wgrad<32, 64, W3Fin3, 3, XF_RELU>(w, f, true, st);
     return SEED_E_UNSUPPORTED;
   }
-  if (a.ch == 16 && a.cin_p == 16) return launch_win3_wgrad<16, 32>(w, f, bias, st, info);
-  if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, bias, st, info);
-  if (a.ch == 64 && a.cin_p == 16) return launch_win3_wgrad<64, 32>(w, f, bias, st, info);   // DMLab 4x s0
-  if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, bias, st, info);
-  if (a.ch == 32 && a.cin_p == 32) return launch_win3_wgrad<32, 64>(w, f, bias, st, info);
-  if (a.ch == 64 && a.cin_p == 32) return launch_win3_wgrad<64, 64>(w, f, bias, st, info);
-  if (a.ch == 64 && a.cin_p == 64) return launch_win3_wgrad<64, 128>(w, f, bias, st, info);
+  if (a.ch == 16 && a.cin_p == 16) return launch_win3_wgrad<16, 32>(w, f, bias, st);
+  if (a.ch == 32 && a.cin_p == 16) return launch_win3_wgrad<32, 32>(w, f, bias, st);
+  if (a.ch == 64 && a.cin_p == 16) return launch_win3_wgrad<64, 32>(w, f, bias, st);   // DMLab 4x s0
+  if (a.ch == 16 && a.cin_p == 32) return launch_win3_wgrad<16, 64>(w, f, bias, st);
+  if (a.ch == 32 && a.cin_p == 32) return launch_win3_wgrad<32, 64>(w, f, bias, st);
+  if (a.ch == 64 && a.cin_p == 32) return launch_win3_wgrad<64, 64>(w, f, bias, st);
+  if (a.ch == 64 && a.cin_p == 64) return launch_win3_wgrad<64, 128>(w, f, bias, st);
   return SEED_E_UNSUPPORTED;
-}
-
-// All deferred finishes in one launch: block b belongs to the entry k with
-// first[k] <= b < first[k+1]; per entry the same fixed-order sum as
-// win3_wgrad_finish (8 interleaved z groups, then the groups in order).
-__global__ void __launch_bounds__(256) w3_finish_all_kernel(const W3FinishList L) {
-  pdl_wait();
-  int k = 0;
-  while (k + 1 < L.n && (int)blockIdx.x >= L.first[k + 1]) ++k;
-  const W3FinishEntry& e = L.e[k];
-  const int o = ((int)blockIdx.x - L.first[k]) * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
-  __shared__ float sh[8][33];
-  float s = 0.f;
-  if (o < e.tot) {
-    const size_t idx = o < e.prows * e.NW ? (size_t)(o / e.NW) * e.PC + (o % e.NW)
-                                          : (size_t)e.NW + (o - e.prows * e.NW);
-    const size_t zs = (size_t)e.prows * e.PC;
-#pragma unroll 8
-    for (int z = g; z < e.G; z += 8) s += __ldcg(e.part + (size_t)z * zs + idx);
-  }
-  sh[g][threadIdx.x & 31] = s;
-  __syncthreads();
-  if (g == 0 && o < e.tot) {
-    float t = 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) t += sh[q][threadIdx.x & 31];
-    if (o >= e.prows * e.NW) e.fin.bias(o - e.prows * e.NW, t);
-    else e.fin.weight3(o / e.NW, o % e.NW, t);
-  }
-}
-
-seed_status conv3w_wgrad_finish_all(W3FinishList& l, cudaStream_t st) {
-  if (l.n == 0) return SEED_OK;
-  int blocks = 0;
-  for (int k = 0; k < l.n; ++k) {
-    l.first[k] = blocks;
-    blocks += ceil_div(l.e[k].tot, 32);
-  }
-  l.first[l.n] = blocks;
-  return launch_k(w3_finish_all_kernel, dim3(blocks), dim3(256), 0, st, l);
 }
 
 // ------------------------------------------------------------------ row-parallel kernels

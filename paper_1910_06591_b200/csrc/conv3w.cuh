@@ -116,48 +116,6 @@ seed_status conv3w_dgrad(const Conv3wDgrad& a, cudaStream_t st);
 // Weight + bias gradient: dW[co][ky][kx][c] = scale * sum_g X[g + off][c] dY[g][co],
 // db[co] = sum_g dY[g][co] (fixed-order split sum; part = scratch); xf as Conv3wFwd
 // (XF_RELU: X = relu(rows), XF_U8: X from obs_u8)
-// weight-gradient finish: (row i, column n) of the summed partials -> dW / db
-struct W3Fin3 {
-  int xim, Cp, CI, CO;
-  int ci_full, co_off, c_off;   // the [co_off..][3][3][c_off..] block of a [..][3][3][ci_full] tensor
-  float scale;
-  float* g_w;
-  float* g_b;
-  __device__ void weight3(int i, int n, float t) const {
-    const int atom = i / Cp, ch = i % Cp;
-    const int ky = 2 - n / CO, co = n % CO;
-    int kx, c;
-    if (xim) {
-      // channel 3*CI of the x-im2col input is constant 1 (conv3_obs_kernel): its
-      // row of the accumulator against tap ky = 1 (dY unshifted) is the bias gradient
-      if (atom == 0 && ch == 3 * CI && ky == 1) g_b[co] = t;
-      if (atom != 0 || ch >= 3 * CI) return;
-      kx = ch / CI; c = ch % CI;
-    } else {
-      if (atom >= 3 || ch >= CI) return;
-      kx = atom; c = ch;
-    }
-    g_w[(((size_t)(co_off + co) * 3 + ky) * 3 + kx) * ci_full + c_off + c] = t * scale;
-  }
-  __device__ void bias(int n, float t) const { g_b[n] = t; }
-};
-
-// Deferred finishes (deep_backward): the weight-gradient kernels of a backward
-// write their partials into separate regions and one launch sums them all
-// (fixed z order, as win3_wgrad_finish) instead of one finish launch per conv.
-constexpr int W3_FINISH_MAX = 24;
-struct W3FinishEntry {
-  const float* part;
-  int G, tot, NW, PC, prows;
-  W3Fin3 fin;
-};
-struct W3FinishList {
-  int n = 0;
-  int first[W3_FINISH_MAX + 1];   // first block of each entry (set at launch)
-  W3FinishEntry e[W3_FINISH_MAX];
-};
-seed_status conv3w_wgrad_finish_all(W3FinishList& l, cudaStream_t st);
-
 struct Conv3wWgrad {
   int cin_p, cin, ch;     // X row channels, real input channels, dY channels
   bool xim;
@@ -173,7 +131,6 @@ struct Conv3wWgrad {
                           // a [..][3][3][ci_full] tensor: plane pairs of the 4x torso)
   float* g_b;             // fp32 [ch] (nullptr: no bias gradient)
   int ci_full, co_off, c_off;
-  W3FinishList* defer;    // non-null: no finish launch, the finish is appended here
 };
 seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st);
 size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool xim);

@@ -576,32 +576,12 @@ static seed_status deep_forward(const StepCtx& c, const seed_batch* bt, const bf
   return SEED_OK;
 }
 
-static bool wgrad_defer() {
-  static const bool on = [] {
-    const char* e = getenv("SEED_WGRAD_DEFER");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const bf16* lowp,
                                  const float* params, float* grads, cudaStream_t st) {
   const NetPlan& p = *c.p;
   const LearnerWs& w = c.w;
   const int64_t F = w.F;
-  // the weight gradients' partials go to one region each (w.wpart) and are summed
-  // by one launch after the sections (conv3w_wgrad_finish_all) instead of a finish
-  // launch per conv; SEED_WGRAD_DEFER=0 finishes each at once (A/B)
-  W3FinishList fl;
-  const bool defer = wgrad_defer() && w.wpart;
-  uint8_t* wp = defer ? c.at<uint8_t>(w.wpart) : nullptr;
-  auto part_for = [&](int64_t rows, int ch, bool xim) {
-    if (!defer) return c.at<float>(w.splitk);
-    float* r = reinterpret_cast<float*>(wp);
-    wp += align_up(conv3w_wgrad_part_bytes(rows, ch, xim), 256);
-    return r;
-  };
-  const int wk = defer ? 1 : 2;   // launches per weight gradient
+  float* part = c.at<float>(w.splitk);
   for (int s = p.nsec - 1; s >= 0; --s) {
     const DeepSec& d = p.sec[s];
     const LearnerWs::Sec& b = w.sec[s];
@@ -616,11 +596,10 @@ static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const b
       // t1 = conv1(u1): dt1 = dh
       Conv3wWgrad wg{};
       wg.cin_p = d.ch; wg.cin = d.ch; wg.ch = d.ch; wg.g = go; wg.rows = Mr; wg.scale = 1.f;
-      wg.X = c.at<uint8_t>(b.u1[r]); wg.dY = c.at<uint8_t>(cur); wg.part = part_for(Mr, d.ch, false);
+      wg.X = c.at<uint8_t>(b.u1[r]); wg.dY = c.at<uint8_t>(cur); wg.part = part;
       wg.g_w = grads + p.t[d.t_rw[r][1]].off; wg.g_b = grads + p.t[d.t_rb[r][1]].off;
-      wg.defer = defer ? &fl : nullptr;
       SEED_TRY(conv3w_wgrad(wg, st));
-      c.mark("deep_res_wgrad1", wk);
+      c.mark("deep_res_wgrad1", 2);
       Conv3wDgrad dg{};
       dg.mode = D3W_MASK; dg.cin = d.ch; dg.ch = d.ch; dg.g = go; dg.rows = Mr;
       dg.dY = c.at<uint8_t>(cur); dg.wimg = lowp + d.im_rdg[r][1]; dg.mask = c.at<uint8_t>(b.u1[r]);
@@ -628,10 +607,10 @@ static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const b
       SEED_TRY(conv3w_dgrad(dg, st));
       c.mark("deep_res_dgrad1");
       // t0 = conv0(relu(h[r])): dh[r] = dh + dconv0 * (h[r] > 0)
-      wg.X = c.at<uint8_t>(b.hr[r]); wg.dY = c.at<uint8_t>(b.dt0); wg.part = part_for(Mr, d.ch, false);
+      wg.X = c.at<uint8_t>(b.hr[r]); wg.dY = c.at<uint8_t>(b.dt0);
       wg.g_w = grads + p.t[d.t_rw[r][0]].off; wg.g_b = grads + p.t[d.t_rb[r][0]].off;
       SEED_TRY(conv3w_wgrad(wg, st));
-      c.mark("deep_res_wgrad0", wk);
+      c.mark("deep_res_wgrad0", 2);
       Conv3wDgrad d0 = dg;
       d0.mode = D3W_RES; d0.dY = c.at<uint8_t>(b.dt0); d0.wimg = lowp + d.im_rdg[r][0];
       d0.mask = c.at<uint8_t>(b.hr[r]); d0.dres = c.at<uint8_t>(cur); d0.dX = c.at<uint8_t>(oth);
@@ -651,11 +630,10 @@ static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const b
       wg.xf = XF_U8;
       wg.obs_u8 = (const uint8_t*)bt->obs;
     }
-    wg.dY = c.at<uint8_t>(b.dconv); wg.part = part_for(F * gi.P, d.ch, d.xim);
+    wg.dY = c.at<uint8_t>(b.dconv); wg.part = part;
     wg.g_w = grads + p.t[d.t_w].off; wg.g_b = grads + p.t[d.t_b].off;
-    wg.defer = defer ? &fl : nullptr;
     SEED_TRY(conv3w_wgrad(wg, st));
-    c.mark("deep_conv_wgrad", wk);
+    c.mark("deep_conv_wgrad", 2);
     if (s > 0) {
       Conv3wDgrad dg{};
       dg.mode = D3W_PLAIN; dg.cin = d.cin; dg.ch = d.ch; dg.g = gi; dg.rows = F * gi.P;
@@ -664,10 +642,6 @@ static seed_status deep_backward(const StepCtx& c, const seed_batch* bt, const b
       SEED_TRY(conv3w_dgrad(dg, st));
       c.mark("deep_conv_dgrad");
     }
-  }
-  if (defer) {
-    SEED_TRY(conv3w_wgrad_finish_all(fl, st));
-    c.mark("deep_wgrad_finish");
   }
   return SEED_OK;
 }

@@ -288,17 +288,6 @@ seed_status make_learner_ws(const NetPlan& p, int T, int B, LearnerWs* w) {
   }
   w->splitk_bytes = sk;
   w->splitk = bump(cur, sk + 16);
-  // deep backward (learner.cu deep_backward): the 3x3 weight gradients of the
-  // sections with <= 64 channels write their partials into separate regions,
-  // summed by one launch at the end
-  size_t wp = 0;
-  for (int sct = 0; sct < p.nsec; ++sct) {
-    const DeepSec& d = p.sec[sct];
-    if (d.ch > 64) continue;
-    wp += align_up(conv3w_wgrad_part_bytes(F * (d.H + 2) * (d.W + 2), d.ch, d.xim), 256);
-    wp += 4 * align_up(conv3w_wgrad_part_bytes(F * (d.H2 + 2) * (d.W2 + 2), d.ch, false), 256);
-  }
-  w->wpart = wp ? bump(cur, wp) : 0;
   w->splitk2 = bump(cur, sk + 16);   // partials of the second (aux-stream) backward branch
   w->total = cur;
   return SEED_OK;

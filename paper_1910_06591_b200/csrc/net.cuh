@@ -98,7 +98,6 @@ struct LearnerWs {
   size_t logits, values, vs, pg, dlogits, dvalues, loss_part, flag, norm_part, step_in, splitk,
       colsum_part, dH, hpart, splitk2;
   size_t splitk_bytes;
-  size_t wpart;   // deferred weight-gradient partials of the deep backward (one region per conv)
   // shallow
   size_t obs_bf16, act1, act2, X, xproj, H, Hprev, gates, Cst, dG, dfc, dY2, dY1;
   // shallow (conv_s2d.cuh): obs_bf16 = S0, act1 = S1, dY2 / dY1 pre-swizzled s2d rows

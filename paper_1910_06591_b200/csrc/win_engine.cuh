@@ -889,17 +889,10 @@ inline size_t win3_wgrad_part_bytes(int64_t M, int CO, int NB = 3, int rbx = 128
   return (size_t)wgrad_grid(M, &r) * wgrad_prows(rbx, NB) * (NB + 1) * CO * 4;
 }
 
-// the finish of a weight gradient launched without it (launch_win3_wgrad's info)
-struct Win3FinishInfo {
-  int G, tot, NW, PC, prows;
-};
-
 // bias = false: no all-ones MMA (the bias gradient is a column of the weight
-// accumulator, e.g. from a constant-1 input channel).  info non-null: the finish
-// is not launched, its geometry is returned (the caller sums the partials later).
+// accumulator, e.g. from a constant-1 input channel)
 template <int CO, int RBX, class Fin, int NB = 3, int XF = XF_NONE>
-seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias, cudaStream_t st,
-                              Win3FinishInfo* info = nullptr) {
+seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias, cudaStream_t st) {
   Win3WgradArgs a = a0;
   const int G = wgrad_grid(a.M, &a.rows_per_cta);
   const int arows = WG_KS + 256 / RBX - 1 + (wgrad_prows(RBX, NB) == 256 ? 2 : 0);   // + the second MMA's rows
@@ -918,10 +911,6 @@ seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias
                     dim3(G), dim3(threads), smem, st, a, stages, a_bytes, b_bytes, stg_bytes));
   constexpr int PROWS = wgrad_prows(RBX, NB);
   const int tot = PROWS * NB * CO + (bias ? CO : 0);
-  if (info) {
-    *info = Win3FinishInfo{G, tot, NB * CO, (NB + 1) * CO, PROWS};
-    return SEED_OK;
-  }
   return launch_k(win3_wgrad_finish<CO, Fin, NB, PROWS>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
                   (const float*)a.part, G, tot, fin);
 }
