@@ -625,10 +625,9 @@ def inference_leg(S, torch, world, rank, dist, iters=20):
             frames = np.random.default_rng(rank).integers(0, 256, size=(NA, 84 * 84 * 4),
                                                           dtype=np.uint8)
             ids = req["actor_ids"]
-            obs_list = [frames[i] for i in ids]
             hact = torch.empty(n, dtype=torch.int32).pin_memory()
-            sd = srv.stage_requests(obs_list, ids, req["reward"], req["done"], threads=8,
-                                    chunk=128, stream=s)
+            sd = srv.stage_requests_table(frames, ids, req["reward"], req["done"], threads=8,
+                                          chunk=128, stream=s)
             torch.cuda.synchronize()
             g2 = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g2, stream=s):
@@ -649,19 +648,22 @@ def inference_leg(S, torch, world, rank, dist, iters=20):
             h2d_us = tp0.elapsed_time(tp1) * 1e3 / iters
             cur = torch.cuda.current_stream()
             tot = 0.0
+            host = 0.0
             for _ in range(iters):
                 t0.record(cur)
-                srv.stage_requests(obs_list, ids, req["reward"], req["done"], stream=cur)
+                th = time.perf_counter()
+                srv.stage_requests_table(frames, ids, req["reward"], req["done"], stream=cur)
+                host += time.perf_counter() - th
                 g2.replay()
                 hact.copy_(a, non_blocking=True)
                 t1.record(cur)
                 torch.cuda.synchronize()
                 tot += t0.elapsed_time(t1)
             hus = tmax(tot * 1e3 / iters)
-            row.update(host_fed_us=round(hus, 2),
+            row.update(host_fed_us=round(hus, 2), host_stage_call_us=round(host * 1e6 / iters, 2),
                        host_fed_steps_per_s=round(world * n / hus * 1e6, 1),
                        h2d_bytes=int(hobs.numel()), h2d_probe_us=round(h2d_us, 2),
-                       host_fed_api="InferenceServer.stage_requests (seed_stage_requests: 8 "
+                       host_fed_api="InferenceServer.stage_requests_table (seed_stage_requests: 8 "
                                     "host threads pack per-actor frames into pinned staging, "
                                     "128-request chunks copied as packed) + graph replay + "
                                     "D2H of the actions",

@@ -655,12 +655,12 @@ class InferenceServer:
         return a, blp
 
     def stage_requests(self, obs_list, actor_ids, rewards, dones, threads=8, chunk=128,
-                       stream=None):
+                       stream=None, _ptrs=None):
         if getattr(self, "_stager", None) is None:
             h = C.c_void_p()
             L.check(L.load().seed_stager_create(threads, C.byref(h)), "seed_stager_create")
             self._stager = h
-        return self._stage(obs_list, actor_ids, rewards, dones, chunk, stream)
+        return self._stage(obs_list, actor_ids, rewards, dones, chunk, stream, _ptrs)
 
     def __del__(self):
         h = getattr(self, "_stager", None)
@@ -671,21 +671,43 @@ class InferenceServer:
                 pass
             self._stager = None
 
-    def _stage(self, obs_list, actor_ids, rewards, dones, chunk, stream):
+    def stage_requests_table(self, table, actor_ids, rewards, dones, threads=8, chunk=128,
+                             stream=None):
+        """stage_requests for frames held in one host table [num_actors][obs_bytes]
+        (e.g. each actor's latest frame): request i's frame is table[actor_ids[i]].
+        The n frame pointers are computed vectorised (no per-request Python work)."""
+        import numpy as np
+        ids = np.ascontiguousarray(actor_ids, np.int32)
+        if table.ndim != 2 or table.strides[1] != table.itemsize:
+            raise ValueError("table: [num_actors][frame] with contiguous rows")
+        if ids.size and (ids.min() < 0 or ids.max() >= table.shape[0]):
+            raise ValueError("actor id outside the table")
+        ob = int(table.shape[1]) * table.itemsize
+        base = table.__array_interface__["data"][0]
+        ptrs = (base + ids.astype(np.uint64) * np.uint64(table.strides[0])).astype(np.uintp)
+        return self.stage_requests(None, ids, rewards, dones, threads, chunk, stream,
+                                   _ptrs=(ptrs, ob))
+
+    def _stage(self, obs_list, actor_ids, rewards, dones, chunk, stream, _ptrs=None):
         """Host-fed requests (seed_stage_requests): obs_list = n host uint8 arrays
         (one per request, e.g. the actors' latest frames), actor_ids / rewards / dones
         host numpy arrays -> device (actor_ids, obs, reward, done) views of this
         server's staging buffers, filled asynchronously on `stream`."""
         import numpy as np
-        n = len(obs_list)
-        ob = int(obs_list[0].nbytes)
+        if _ptrs is not None:
+            ptr_arr, ob = _ptrs
+            n = len(ptr_arr)
+        else:
+            n = len(obs_list)
+            ob = int(obs_list[0].nbytes)
+            ptr_arr = np.array([o.__array_interface__["data"][0] for o in obs_list], dtype=np.uintp)
         if getattr(self, "_stage_n", 0) < n or getattr(self, "_stage_ob", 0) != ob:
             self._pin_obs = torch.empty(n * ob, dtype=torch.uint8).pin_memory()
             self._pin_meta = torch.empty(9 * n + 16, dtype=torch.uint8).pin_memory()
             self._dev_obs = torch.empty(n * ob, dtype=torch.uint8, device=self.h.device)
             self._dev_meta = torch.empty(9 * n + 16, dtype=torch.uint8, device=self.h.device)
             self._stage_n, self._stage_ob = n, ob
-        ptrs = (C.c_void_p * n)(*[o.ctypes.data for o in obs_list])
+        ptrs = C.c_void_p(ptr_arr.ctypes.data)
         ids = np.ascontiguousarray(actor_ids, np.int32)
         rw = np.ascontiguousarray(rewards, np.float32)
         dn = np.ascontiguousarray(dones, np.uint8)

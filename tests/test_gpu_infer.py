@@ -303,6 +303,14 @@ def test_stage_requests_host_fed_equals_device_fed():
     torch.cuda.synchronize()
     assert torch.equal(a1, a2) and torch.equal(b1, b2)
     assert torch.equal(srv.h, srv2.h) and torch.equal(srv.c, srv2.c)
+    # the table form (frames indexed by actor id, pointers computed vectorised) stages
+    # the same bytes
+    ids_t, obs_t, rw_t, dn_t = srv.stage_requests_table(frames, ids, req["reward"], req["done"])
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(obs_t.cpu().numpy(), frames[ids])
+    np.testing.assert_array_equal(ids_t.cpu().numpy(), ids)
+    np.testing.assert_array_equal(rw_t.cpu().numpy(), req["reward"])
+    np.testing.assert_array_equal(dn_t.cpu().numpy(), req["done"])
 
 
 def test_wire_actors_to_inference_and_back():
