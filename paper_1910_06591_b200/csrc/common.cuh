@@ -102,9 +102,10 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // complete); no kernel reads before its wait what the kernel just before it writes
 // (the pre-wait reads are parameter images, written by the previous step's Adam /
 // image refresh).  Used by the LSTM, heads / loss, GEMM, space-to-depth, clip /
-// Adam and inference kernels; measured c2 step 0.190 -> 0.184 ms, the deep steps
-// unchanged (in the window-conv kernels as well it cost c3 / c4 ~1 %:
-// profiles/r02/pdl_trigger.md).
+// Adam and inference kernels and (WinConvArgs::trig) the space-to-depth window
+// convs; measured c2 step 0.190 -> 0.181 ms, the deep steps unchanged (in the 3x3
+// window-conv kernels as well it cost c3 / c4 ~1 %: profiles/r02/pdl_trigger.md).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait_trig() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -114,6 +114,7 @@ struct S2dFin2 {
 static Win3WgradArgs s2d_wgrad3_args(const uint8_t* src, int64_t rows, const uint8_t* dy, int wsp,
                                      float* part) {
   Win3WgradArgs a{};
+  a.trig = 1;
   a.X = src; a.dy = dy; a.M = rows; a.part = part;
   a.boff = -wsp; a.bstride = wsp;
   return a;
@@ -183,6 +184,7 @@ seed_status shallow_s2d_conv1(const ShallowS2d& sg, int64_t F, const uint8_t* S0
                               const float* b1, uint8_t* S1, cudaStream_t st) {
   const S2dGeo& g = sg.g1;
   WinConvArgs a{};
+  a.trig = 1;
   a.src = S0; a.src_rows = sg.rows1(F); a.M = sg.rows1(F);
   a.off[0] = 0; a.off[1] = 1; a.off[2] = g.Ws; a.off[3] = g.Ws + 1;
   a.wimg = reinterpret_cast<const uint8_t*>(w1img);
@@ -196,6 +198,7 @@ seed_status shallow_s2d_conv2(const ShallowS2d& sg, int64_t F, const uint8_t* S1
                               const float* b2, bf16* act2, uint8_t* dY2z, cudaStream_t st) {
   const S2dGeo& g = sg.g2;
   WinConvArgs a{};
+  a.trig = 1;
   a.src = S1; a.src_rows = sg.rows2(F); a.M = sg.rows2(F);
   a.off[0] = 0; a.off[1] = 1; a.off[2] = g.Ws; a.off[3] = g.Ws + 1;
   a.wimg = reinterpret_cast<const uint8_t*>(w2img);
@@ -228,6 +231,7 @@ seed_status shallow_s2d_conv2_dgrad(const ShallowS2d& sg, int64_t F, const uint8
                                     cudaStream_t st) {
   const S2dGeo& g = sg.g2;
   WinConvArgs a{};
+  a.trig = 1;
   a.src = dY2; a.src_rows = sg.rows2(F); a.M = sg.rows2(F);
   a.off[0] = 0; a.off[1] = -1; a.off[2] = -g.Ws; a.off[3] = -g.Ws - 1;
   a.wimg = reinterpret_cast<const uint8_t*>(w2dg_img);

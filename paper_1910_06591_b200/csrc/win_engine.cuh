@@ -79,6 +79,8 @@ struct WinConvArgs {
   int off[WIN_MAX];      // window row offsets
   const uint8_t* wimg;   // pre-swizzled weight image [NW][N][RB]
   U8Rows u8;             // XF_U8 source
+  int trig;              // 1: explicit PDL trigger after the wait (common.cuh pdl_wait_trig;
+                         // set for the space-to-depth convs, measured slower for the 3x3 ones)
 };
 
 __device__ __forceinline__ uint4 pack8(const float* o) {
@@ -301,6 +303,7 @@ __global__ void __launch_bounds__(WCF_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0)
     bulk_g2s(smem_u32(Ws), a.wimg, WB, &wbar);
   }
   pdl_wait();
+  if (a.trig) pdl_trigger();
   const uint32_t tmem = tbase;
   if (warp == 0) {
     int it = 0;
@@ -668,6 +671,7 @@ struct Win3WgradArgs {
   int64_t rows_per_cta;
   float* part;           // [grid][128][4*CO] (cols [0, 3CO) weights, [3CO, 4CO) bias in row 0)
   U8Rows u8;             // XF_U8 source of the X rows
+  int trig;              // as WinConvArgs::trig (also for the finish launch)
 };
 
 template <int CO, int RBX, bool BIAS, int NB = 3, int XF = XF_NONE>
@@ -717,6 +721,7 @@ __global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0),
   __syncthreads();
   tc_fence_after();
   pdl_wait();
+  if (a.trig) pdl_trigger();
   const uint32_t tmem = tbase;
   if (warp == 0) {
     for (int it = 0; it < nks; ++it) {
@@ -860,8 +865,9 @@ __global__ void __launch_bounds__(WC_THREADS + (XF != XF_NONE ? 32 * XF_CW : 0),
 // o >= 128*3CO: bias column -> Fin::bias
 template <int CO, class Fin, int NB = 3, int PROWS = 128>
 __global__ void __launch_bounds__(256) win3_wgrad_finish(const float* __restrict__ part, int G,
-                                                         int tot, const Fin f) {
+                                                         int tot, const Fin f, int trig) {
   pdl_wait();
+  if (trig) pdl_trigger();
   constexpr int NW = NB * CO, PC = (NB + 1) * CO;
   const int o = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
   __shared__ float sh[8][33];
@@ -912,7 +918,7 @@ seed_status launch_win3_wgrad(const Win3WgradArgs& a0, const Fin& fin, bool bias
   constexpr int PROWS = wgrad_prows(RBX, NB);
   const int tot = PROWS * NB * CO + (bias ? CO : 0);
   return launch_k(win3_wgrad_finish<CO, Fin, NB, PROWS>, dim3(ceil_div(tot, 32)), dim3(256), 0, st,
-                  (const float*)a.part, G, tot, fin);
+                  (const float*)a.part, G, tot, fin, a.trig);
 }
 
 }  // namespace seed
