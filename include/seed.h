@@ -29,7 +29,8 @@
  *            environment switches for A/B measurement, read once (SEED_PDL,
  *            SEED_DP_BUCKETS, SEED_DP_COMMS, SEED_FUSE_POOL=0 unfused section conv +
  *            max-pool, SEED_CP_KX / SEED_CP_EW its column-tap-stacked form / epilogue
- *            warps, SEED_KX, SEED_XF_U8, SEED_PEER_DEBUG) or per call
+ *            warps, SEED_KX, SEED_XF_U8, SEED_DEEP_TRIG early PDL triggers of the 3x3
+ *            kernels, SEED_PEER_DEBUG) or per call
  *            (SEED_STORE_CONV=1: the fused section conv + max-pool also stores the
  *            conv rows, a test hook).  Calls on
  *            different streams with disjoint buffers (and distinct seed_exec /

@@ -12,6 +12,19 @@ __device__ __forceinline__ const uint4* chunk_at(const uint8_t* base, int64_t m,
   return reinterpret_cast<const uint4*>(base + m * RB + (swz_chunk(m, RB, j) << 4));
 }
 
+// Explicit PDL triggers in the 3x3 kernels (common.cuh pdl_wait_trig): SEED_DEEP_TRIG
+// bit 0 = weight gradients + finishes, bit 1 = forward / data-gradient convs, bit 2 =
+// max-pool backward.  Default 2 (profiles/r02/pdl_trigger.md, c4 over two rounds:
+// none 5.649 / 5.652 ms, convs 5.637 / 5.636, weight gradients 5.668 / 5.699, pool
+// backward 5.658 / 5.657, all 5.668 / 5.672).
+static int deep_trig() {
+  static const int v = [] {
+    const char* e = getenv("SEED_DEEP_TRIG");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
 // ------------------------------------------------------------------ epilogues
 template <int MODE, int NN>
 struct W3FwdEpi {
@@ -269,6 +282,7 @@ static U8Rows u8_rows(const uint8_t* obs, const PadGeo& g) {
 template <int MODE, int N, int RB, int NW, int XF = XF_NONE>
 static seed_status fwd_t(const Conv3wFwd& a, cudaStream_t st) {
   WinConvArgs w{};
+  w.trig = (deep_trig() >> 1) & 1;
   w.src = a.in; w.src_rows = a.rows; w.M = a.rows;
   w.wimg = reinterpret_cast<const uint8_t*>(a.wimg);
   if (XF == XF_U8) w.u8 = u8_rows(a.obs_u8, a.g);
@@ -327,6 +341,7 @@ seed_status conv3w_forward(const Conv3wFwd& a, cudaStream_t st) {
 template <int MODE, int N, int RB>
 static seed_status dgrad_t(const Conv3wDgrad& a, cudaStream_t st) {
   WinConvArgs w{};
+  w.trig = (deep_trig() >> 1) & 1;
   w.src = a.dY; w.src_rows = a.rows; w.M = a.rows;
   w.wimg = reinterpret_cast<const uint8_t*>(a.wimg);
   // row windows ky at -(ky-1)*Wp; the image stacks the column taps as groups 2 - kx
@@ -398,6 +413,7 @@ size_t conv3w_wgrad_part_bytes(int64_t rows, int ch, bool) {
 
 seed_status conv3w_wgrad(const Conv3wWgrad& a, cudaStream_t st) {
   Win3WgradArgs w{};
+  w.trig = deep_trig() & 1;
   w.X = a.X; w.dy = a.dY; w.M = a.rows; w.part = a.part;
   if (a.xf == XF_U8) w.u8 = u8_rows(a.obs_u8, a.g);
   w.boff = a.xim ? -a.g.Wp : 1 - a.g.Wp;
@@ -652,8 +668,10 @@ __device__ __forceinline__ const uint4* chunk_at32(const uint8_t* base, uint32_t
 template <int NC>
 __global__ void __launch_bounds__(256) conv3w_pool_bwd_kernel(
     PadGeo gi, PadGeo go, int pt, int pl, int total, int nz, FastDiv fnbx, FastDiv fnby, FastDiv fper,
-    FastDiv fwp, const uint8_t* __restrict__ dout, const uint8_t* __restrict__ arg, uint8_t* __restrict__ din) {
+    FastDiv fwp, const uint8_t* __restrict__ dout, const uint8_t* __restrict__ arg, uint8_t* __restrict__ din,
+    int trig) {
   pdl_wait();
+  if (trig) pdl_trigger();
   constexpr int C = NC * 8, RB = NC * 16;
   const int tt = blockIdx.x * blockDim.x + threadIdx.x;
   if (tt >= total) {
@@ -773,13 +791,13 @@ seed_status conv3w_pool_bwd(int64_t F, const PadGeo& gi, const PadGeo& go, int C
   const int t32 = (int)total, z32 = (int)nz;
   if (NC == 2)
     return launch_k(conv3w_pool_bwd_kernel<2>, grid, dim3(256), 0, st, gi, go, pt, pl, t32, z32, fnbx, fnby,
-                    fper, fwp, dout, arg, din);
+                    fper, fwp, dout, arg, din, (deep_trig() >> 2) & 1);
   if (NC == 4)
     return launch_k(conv3w_pool_bwd_kernel<4>, grid, dim3(256), 0, st, gi, go, pt, pl, t32, z32, fnbx, fnby,
-                    fper, fwp, dout, arg, din);
+                    fper, fwp, dout, arg, din, (deep_trig() >> 2) & 1);
   if (NC == 8)
     return launch_k(conv3w_pool_bwd_kernel<8>, grid, dim3(256), 0, st, gi, go, pt, pl, t32, z32, fnbx, fnby,
-                    fper, fwp, dout, arg, din);
+                    fper, fwp, dout, arg, din, (deep_trig() >> 2) & 1);
   return SEED_E_UNSUPPORTED;
 }
 
