@@ -116,9 +116,11 @@ __device__ __forceinline__ void pool_band(const CpArgs& a, const Band& b, const 
     a.fRow.divmod(rem, Yr, c2);
     const int X = (int)(c2 / NC), j = (int)(c2 % NC);
     const int Y = Ylo + (int)Yr;
-    const int64_t g = (b.f0 + fl) * a.go.P + (int64_t)Y * a.go.Wp + X;
-    uint4* ph = reinterpret_cast<uint4*>(a.h0 + g * RBO + (swz_chunk(g, RBO, j) << 4));
-    uint4* pr = reinterpret_cast<uint4*>(a.hr0 + g * RBO + (swz_chunk(g, RBO, j) << 4));
+    // output row (32-bit: F * go.P < 2^32, checked by the launcher)
+    const uint32_t g = ((uint32_t)b.f0 + fl) * (uint32_t)a.go.P + (uint32_t)(Y * a.go.Wp + X);
+    const size_t off = (size_t)g * RBO + ((size_t)swz_chunk(g, RBO, j) << 4);
+    uint4* ph = reinterpret_cast<uint4*>(a.h0 + off);
+    uint4* pr = reinterpret_cast<uint4*>(a.hr0 + off);
     if (Y == 0 || Y == a.go.H + 1 || X == 0 || X == a.go.W + 1) {
       *ph = make_uint4(0, 0, 0, 0);
       *pr = make_uint4(0, 0, 0, 0);
@@ -141,7 +143,7 @@ __device__ __forceinline__ void pool_band(const CpArgs& a, const Band& b, const 
     pool_max9(in, best, rl, am);
     *ph = best;
     *pr = rl;
-    *reinterpret_cast<uint2*>(a.arg + g * N + 8 * j) = am;
+    *reinterpret_cast<uint2*>(a.arg + (size_t)g * N + 8 * j) = am;
   }
 }
 
@@ -504,6 +506,7 @@ seed_status launch_conv_pool(CpArgs a, cudaStream_t st) {
   if (a.pt < 0 || a.pt > 1 || a.pl < 0 || a.pl > 1 || 2 * (a.go.H - 1) - a.pt + 2 > gi.H ||
       2 * (a.go.W - 1) - a.pl + 2 > gi.W)
     return SEED_E_UNSUPPORTED;
+  if (a.F * a.go.P >= (1ll << 32)) return SEED_E_SHAPE;   // 32-bit output rows (pool_band)
   a.fP = FastDiv((uint32_t)gi.P); a.fWp = FastDiv((uint32_t)gi.Wp);
   a.fRow = FastDiv((uint32_t)(a.go.Wp * (N / 8)));
   a.fFrame = FastDiv((uint32_t)((a.go.H + 2) * a.go.Wp * (N / 8)));
